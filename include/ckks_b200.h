@@ -1,0 +1,145 @@
+/*
+ * ckks_b200.h — C-ABI of the B200-native RNS-CKKS kernels (sm_100a).
+ *
+ * The reference (arxiv 2506.19693 "ReBoot", package `ciphermlp`) has no native
+ * code and no FFI: its RNS-CKKS path is numpy inside `ciphermlp/ckks/*.py`.
+ * Each entry point below replaces one numpy routine of that path; the
+ * replaced reference function is cited beside it (paths relative to
+ * /root/reference/pkg/src/ciphermlp/).  The Python host layer
+ * (paper_2506_19693_b200/backend.py) binds these with ctypes — that binding is
+ * the "reference-side FFI" documented in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every polynomial is a run of `rows` limbs of N = 2^log_n uint64
+ *    residues, row-major ([rows][N]); row r uses the prime
+ *    `limb_prime[r % limbs]` (an index into the ring's prime table), so a
+ *    batch [B][comps][limbs][N] is passed as rows = B*comps*limbs.
+ *  - All data/table pointers are DEVICE pointers unless named *_host.
+ *    `limb_prime`, `key_limb`, `scalars_host` are HOST arrays (copied into the
+ *    kernel parameters; no allocation, no host<->device sync).
+ *  - `stream` is a cudaStream_t passed as void*.  All calls are asynchronous
+ *    on that stream and thread-safe (no global mutable state).
+ *  - Return value: 0 on success, a positive cudaError_t on launch failure, or
+ *    a negative CKB_E* code for bad arguments.
+ *  - Residues are canonical ([0, p)) on input and output; primes < 2^62.
+ */
+#ifndef CKKS_B200_H
+#define CKKS_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKB_MAX_LIMBS 128
+#define CKB_E_ARG (-1)
+#define CKB_E_LIMBS (-2)
+#define CKB_E_LOGN (-3)
+
+/* Device-resident tables for one ring degree and one prime chain.
+ *   mods : [n_primes][8]  {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
+ *                          psi_inv_brv[1]*N^-1, shoup(.)}
+ *   ntt  : [n_primes][4][N] {psi_brv, shoup(psi_brv), inv_psi_brv, shoup(inv_psi_brv)}
+ *   pair : [n_primes][n_primes][4] {p_i^-1 mod p_j, shoup(.), p_i mod p_j, 0}
+ * Built on the host by ckb_build_tables, uploaded by the caller. */
+typedef struct {
+  uint32_t log_n;
+  uint32_t n_primes;
+  const uint64_t* mods;
+  const uint64_t* ntt;
+  const uint64_t* pair;
+} ckb_ring;
+
+/* Library version (for load checks). */
+int ckb_version(void);
+
+/* Host-side table builder.  psi is chosen as in NttPlan/_primitive_2n_root
+ * (ckks/ntt.py:81-89, :103-119): the smallest g>=2 with psi=g^((p-1)/2N),
+ * psi^N = -1; tables are bit-reversed powers.  Outputs are HOST buffers of
+ * the sizes documented for ckb_ring. */
+int ckb_build_tables(uint32_t log_n, const uint64_t* primes_host, uint32_t n_primes,
+                     uint64_t* mods_out, uint64_t* ntt_out, uint64_t* pair_out);
+
+/* Negacyclic NTT, in place, natural order -> bit-reversed order.
+ * Replaces NttPlan.forward (ckks/ntt.py:121-136) / RingElement.to_ntt (ring.py:109-115). */
+int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
+                    const int32_t* limb_prime, void* stream);
+/* Inverse, bit-reversed -> natural order, times N^-1.
+ * Replaces NttPlan.inverse (ckks/ntt.py:138-154) / RingElement.to_coeff (ring.py:117-123). */
+int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
+                    const int32_t* limb_prime, void* stream);
+
+/* Limb-wise arithmetic over rows*N residues.  Replace RingElement.add/sub/neg/
+ * mul (ring.py:80-131).  op: 0 add, 1 sub, 2 mul (Hadamard), 3 neg (b unused),
+ * 4 mul_add: out = a*b + c.  If 0 < b_rows < rows, b (and c) hold b_rows rows
+ * that are broadcast periodically over a (e.g. one plaintext times both
+ * ciphertext components, backend.py:147-151). */
+int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t* a,
+                    const uint64_t* b, const uint64_t* c, int rows, int limbs,
+                    const int32_t* limb_prime, int b_rows, void* stream);
+/* out = a * scalar[limb]; scalars_host is [limbs][2] {v, floor(v*2^64/p)} with v < p.
+ * Replaces RingElement.scalar_mul (ring.py:110-115 of RingElement; backend.py:108-111). */
+int ckb_scalar_mul(const ckb_ring* ring, uint64_t* out, const uint64_t* a, int rows,
+                   int limbs, const int32_t* limb_prime, const uint64_t* scalars_host,
+                   void* stream);
+
+/* Ciphertext tensor product in the NTT domain (backend.py:136-140):
+ * a,b: [batch][2][limbs][N]; out: [batch][3][limbs][N] = (a0b0, a0b1+a1b0, a1b1). */
+int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uint64_t* b,
+               int batch, int limbs, const int32_t* limb_prime, void* stream);
+
+/* Key-switch ModUp (keys.py:84-90): split `in` ([batch][limbs][N], coefficient
+ * domain, basis limb_prime) into digits of `alpha` limbs and lift each digit into
+ * the extended basis ext_prime (ext_limbs entries; the first `limbs` entries must
+ * equal limb_prime).  alpha == 1 reproduces the reference's centered per-limb
+ * digits exactly; alpha > 1 is the standard fast basis conversion using
+ * bconv (device table [digits][alpha][2 + 2*ext_limbs]; see backend.py docs).
+ * out: [batch][digits][ext_limbs][N], coefficient domain. */
+int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int batch, int limbs,
+              const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
+              const uint64_t* bconv, void* stream);
+
+/* Key-switch inner product in the NTT domain (keys.py:91-97):
+ *   acc[b][c][e] = sum_j digits[b][j][e] * key_b[j][c][key_limb[e]]
+ * digits: [batch][n_digits][ext_limbs][N]; acc: [batch][2][ext_limbs][N].
+ * key_ptrs: DEVICE array of `batch` pointers to keys laid out
+ * [key_rows][2][key_limbs][N]; if NULL, `key` is used for every batch item. */
+int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
+                 int n_digits, int ext_limbs, const int32_t* ext_prime,
+                 const uint64_t* key, const uint64_t* const* key_ptrs, int key_limbs,
+                 const int32_t* key_limb, void* stream);
+
+/* Exact divide-and-round chain (ring.py:165-189, keys.py:98-99, backend.py:86-112):
+ *   x <- x * prescale[limb]              (optional; level adjust, backend.py:108-111)
+ *   x <- divround(x, last n_drop1 limbs)  (dropped last-first, one prime at a time)
+ *   x <- x + addend                      (optional; backend.py:142 / :171)
+ *   x <- divround(x, last n_drop2 limbs)  (rescale, backend.py:86-92)
+ * in: polys of `limbs` rows, poly p starting at in + p*in_poly_stride (0 means
+ * limbs*N; a larger stride reads a limb prefix in place = RingElement.restrict);
+ * addend: added to poly p when (p % addend_period) < addend_polys, reading addend row
+ *   (p / addend_period) * addend_polys + p % addend_period of [.][limbs-n_drop1][N]; or NULL
+ *   (mul_ct: period 2, polys 2 -> d0,d1; rotate: period 2, polys 1 -> c0 only);
+ * out: [polys][limbs-n_drop1-n_drop2][N]; prescale_host: [limbs][2] {v, shoup(v)} or NULL. */
+int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
+                 const uint64_t* addend, int addend_polys, int addend_period, int polys,
+                 int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
+                 const uint64_t* prescale_host, void* stream);
+
+/* Galois automorphism X -> X^galois, coefficient domain (ring.py:211-232). */
+int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows,
+                     int limbs, const int32_t* limb_prime, uint64_t galois, void* stream);
+
+/* Signed int64 coefficients -> residues (ring.py:139-145):
+ * in: [polys][N] int64; out: [polys][limbs][N]. */
+int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int polys, int limbs,
+                 const int32_t* limb_prime, void* stream);
+
+/* Centered CRT lift to float64 (ring.py:192-208 + encoding.py:67-69 astype):
+ * in: [polys][limbs][N] coefficient domain; out: [polys][N] double. */
+int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys, int limbs,
+               const int32_t* limb_prime, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKKS_B200_H */

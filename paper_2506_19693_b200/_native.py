@@ -1,0 +1,114 @@
+"""ctypes binding of the sm_100a kernel library (include/ckks_b200.h).
+
+This is the FFI a maintainer of the reference would add.
+There is deliberately no fallback: if the library is missing or fails to load,
+importing the backend raises, and every op raises if a kernel launch fails.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libckks_b200.so")
+
+c_u64p = ctypes.POINTER(ctypes.c_uint64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_vp = ctypes.c_void_p
+
+
+class CkbRing(ctypes.Structure):
+    _fields_ = [("log_n", ctypes.c_uint32), ("n_primes", ctypes.c_uint32),
+                ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp)]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"B200 kernel library not built: {_LIB_PATH} is missing "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`). "
+            "There is no CPU fallback.")
+    lib = ctypes.CDLL(_LIB_PATH)
+    R = ctypes.POINTER(CkbRing)
+    sig = {
+        "ckb_version": ([], ctypes.c_int),
+        "ckb_build_tables": ([ctypes.c_uint32, c_u64p, ctypes.c_uint32, c_u64p, c_u64p, c_u64p],
+                             ctypes.c_int),
+        "ckb_ntt_forward": ([R, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_ntt_inverse": ([R, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_elementwise": ([R, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
+                             c_i32p, ctypes.c_int, c_vp], ctypes.c_int),
+        "ckb_scalar_mul": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_u64p, c_vp],
+                           ctypes.c_int),
+        "ckb_tensor": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp],
+                       ctypes.c_int),
+        "ckb_modup": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int, c_i32p,
+                       ctypes.c_int, c_vp, c_vp], ctypes.c_int),
+        "ckb_ks_inner": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, c_vp,
+                          c_vp, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_divround": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, ctypes.c_int,
+                          ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int, ctypes.c_int, c_u64p,
+                          c_vp],
+                         ctypes.c_int),
+        "ckb_automorphism": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_uint64,
+                              c_vp], ctypes.c_int),
+        "ckb_from_i64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_to_f64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.ckb_version() != 1:
+        raise ImportError("libckks_b200.so version mismatch; rebuild")
+    return lib
+
+
+LIB = _load()
+EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inverse",
+            "ckb_elementwise", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
+            "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64")
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what} failed with status {rc}")
+
+
+def build_tables(log_n: int, primes) -> tuple:
+    """Host tables for ckb_ring (see include/ckks_b200.h)."""
+    n = 1 << log_n
+    np_ = len(primes)
+    pr = np.ascontiguousarray(np.array(primes, dtype=np.uint64))
+    mods = np.zeros((np_, 8), dtype=np.uint64)
+    ntt = np.zeros((np_, 4, n), dtype=np.uint64)
+    pair = np.zeros((np_, np_, 4), dtype=np.uint64)
+    rc = LIB.ckb_build_tables(log_n, pr.ctypes.data_as(c_u64p), np_, mods.ctypes.data_as(c_u64p),
+                              ntt.ctypes.data_as(c_u64p), pair.ctypes.data_as(c_u64p))
+    check(rc, "ckb_build_tables")
+    return mods, ntt, pair
+
+
+def i32_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_int32 * len(vals))(*vals)
+
+
+def u64_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_uint64 * len(vals))(*vals)
+
+
+def ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -1,0 +1,546 @@
+"""B200 RNS-CKKS backend: the drop-in for the reference's ``CkksBackend``.
+
+Boundary (/root/reference/pkg/src/ciphermlp/api.py:129-259): a ``Backend``
+subclass with ``backend_id = "ckks"`` implementing the five payload hooks
+(_payload_elementwise / _rotate / _encrypt / _decrypt / _bootstrap) plus
+serialize_cipher / deserialize_cipher, constructor-compatible with
+``CkksBackend(params, rotation_indices=(), rng_seed=0, bootstrap_eps=0.0,
+keyset_id=None, _secret=None)`` (ckks/backend.py:55-75).  Level, depth and
+keyset checks stay in the shared base class.
+
+Payload: ``GpuCiphertext(data, level)`` — ``data`` is a torch.uint64 CUDA
+tensor [2, limbs(level), N] holding (c0, c1) in the coefficient domain, as the
+reference keeps ciphertexts at rest (backend.py:1-9).  Every integer operation
+runs in the sm_100a kernels (ring.py -> _native.py -> libckks_b200.so); the
+host does only what the reference's host does besides arithmetic: numpy
+sampling with the reference's RNG streams (so keys and encryptions are
+reproducible bit-for-bit against it), the float-64 encode/decode FFT (cuFFT via
+torch on the device), error checks and serialisation.
+
+Extra keyword options (all default to the reference's behaviour):
+  prime_layout  "reference" | "baseline" | "schedule"   (primes.py)
+  dnum          None = per-limb digits (reference, keys.py:84-97); an int gives
+                hybrid key switching with digits of ceil(LQ/dnum) limbs
+  secret_hw     None = dense ternary (ring.py:161-162); h = ternary with exactly
+                h non-zeros (BASELINE configs: 64 / 192)
+  device        CUDA device (default: current)
+"""
+
+from __future__ import annotations
+
+import collections
+import dataclasses
+import io
+import json
+import math
+import struct
+
+import numpy as np
+import torch
+
+from . import he_api, he_errors
+from .ring import U64, GpuChain, shoup
+
+CT_MAGIC = b"RBCT"
+KEY_MAGIC = b"RBKY"
+SERIAL_VERSION = 1
+ERROR_SIGMA = 3.2
+MAX_SAFE_COEFF = float(2**52)
+
+
+@dataclasses.dataclass(frozen=True)
+class GpuCiphertext:
+    """(c0, c1) at one chain level; coefficient domain, canonical residues."""
+
+    data: torch.Tensor  # [2, limbs, N] uint64, CUDA
+    level: int
+
+    @property
+    def c0(self):
+        return self.data[0]
+
+    @property
+    def c1(self):
+        return self.data[1]
+
+
+class DeviceEncoder:
+    """Canonical embedding with the rotation-friendly 5^i slot order
+    (encoding.py:17-76), evaluated with cuFFT in float64 on the device."""
+
+    def __init__(self, n: int, device):
+        self.n = n
+        self.device = device
+        slots = n // 2
+        exps = np.empty(slots, dtype=np.int64)
+        e = 1
+        for i in range(slots):
+            exps[i] = e
+            e = e * 5 % (2 * n)
+        self.bins_np = (exps - 1) // 2
+        self.conj_bins_np = (2 * n - exps - 1) // 2
+        self.bins = torch.from_numpy(self.bins_np).to(device)
+        self.conj_bins = torch.from_numpy(self.conj_bins_np).to(device)
+        twist = np.exp(1j * np.pi * np.arange(n) / n)
+        self.twist = torch.from_numpy(twist).to(device)
+        self.untwist = torch.from_numpy(np.conj(twist)).to(device)
+
+    def embed_device(self, values, scale: float) -> torch.Tensor:
+        """Real slots -> int64 coefficients [N] on the device (encoding.py:34-49)."""
+        v = torch.as_tensor(np.asarray(values, dtype=np.float64), device=self.device)
+        spec = torch.zeros(self.n, dtype=torch.complex128, device=self.device)
+        scaled = torch.zeros(self.n // 2, dtype=torch.float64, device=self.device)
+        scaled[: v.shape[0]] = v * scale
+        spec[self.bins] = scaled.to(torch.complex128)
+        spec[self.conj_bins] = scaled.to(torch.complex128)
+        w = torch.fft.fft(spec) / self.n
+        return torch.round(torch.real(w * self.untwist))
+
+    def embed(self, values, scale: float) -> np.ndarray:
+        coeffs = self.embed_device(values, scale)
+        if float(coeffs.abs().max()) >= MAX_SAFE_COEFF:
+            raise he_errors.EncodingOverflow(
+                "scaled values exceed the exactly-representable coefficient range")
+        return coeffs.to(torch.int64).cpu().numpy()
+
+    def unembed_device(self, coeffs: torch.Tensor, scale: float) -> torch.Tensor:
+        w = coeffs.to(torch.complex128) * self.twist
+        spec = torch.fft.ifft(w) * self.n
+        return torch.real(spec[..., self.bins]) / scale
+
+    def unembed(self, coeffs, scale: float) -> np.ndarray:
+        c = torch.as_tensor(np.asarray(coeffs, dtype=np.float64), device=self.device)
+        return self.unembed_device(c, scale).cpu().numpy()
+
+
+class SecretKey:
+    """Holds the ternary secret (``coeffs``, as ring.py:161-162 / keys.py:37-46)
+    and its NTT form over every prime (``s_full``, [all_limbs, N])."""
+
+    def __init__(self, coeffs: np.ndarray, s_full: torch.Tensor):
+        self.coeffs = coeffs
+        self.s_full = s_full
+
+
+@dataclasses.dataclass
+class KeySwitchKey:
+    """Rows [digits][2 (b, a)][all limbs][N] uint64, NTT domain (keys.py:29-34)."""
+
+    data: torch.Tensor
+
+
+class B200CkksCore:
+    """Payload hooks; mixed into a ``Backend`` base (ours or the reference's)."""
+
+    backend_id = "ckks"
+    _errors = he_errors
+    _api = he_api
+    _instances = 0
+
+    def __init__(self, params, rotation_indices=(), rng_seed: int = 0, bootstrap_eps: float = 0.0,
+                 keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
+                 secret_hw=None, device=None, encode_cache: int = 512):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
+        if keyset_id is None:
+            B200CkksCore._instances += 1
+            keyset_id = f"b200-keyset-{B200CkksCore._instances}"
+        super().__init__(params, keyset_id)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.chain = GpuChain(params, prime_layout, self.device)
+        self.ctx = self.chain
+        ch = self.chain
+        self.n = params.poly_degree
+        self.encoder = DeviceEncoder(self.n, self.device)
+        self.rng_seed = rng_seed
+        self.bootstrap_eps = bootstrap_eps
+        self.rotation_indices = frozenset(int(k) for k in rotation_indices)
+        self.alpha = 1 if dnum is None else max(1, -(-ch.lq // int(dnum)))
+        self.dnum = dnum
+        self._bconv_cache: dict = {}
+        self._adjust_cache: dict = {}
+        self._enc_cache: collections.OrderedDict = collections.OrderedDict()
+        self._enc_cache_cap = encode_cache
+        rng = np.random.default_rng(rng_seed)
+        coeffs = rng.integers(-1, 2, self.n).astype(np.int64)  # ring.py:161-162
+        if secret_hw is not None:
+            coeffs = _hw_secret(self.n, int(secret_hw), rng_seed)
+        if _secret is not None:
+            coeffs = np.asarray(_secret).astype(np.int64)
+        self.sk = SecretKey(coeffs, self._to_ntt_all(coeffs))
+        self.relin_key = self._make_ksk(self._mul_all(self.sk.s_full, self.sk.s_full), rng)
+        self.galois_for_step: dict = {}
+        self.rotation_keys: dict = {}
+        slots = params.slot_count
+        s_coeff = ch.ntt_inv(self.sk.s_full.clone(), len(ch.all_primes), ch.all_map())
+        for step in sorted({k % slots for k in self.rotation_indices} - {0}):
+            g = pow(5, step, 2 * self.n)
+            self.galois_for_step[step] = g
+            s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
+            ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
+            self.rotation_keys[g] = self._make_ksk(s_rot, rng)
+        self._bs_rng = np.random.default_rng(rng_seed + 0x5EED)
+
+    # ------------------------------------------------------------------ keys
+    def _to_ntt_all(self, coeffs: np.ndarray) -> torch.Tensor:
+        ch = self.chain
+        t = torch.as_tensor(np.asarray(coeffs, dtype=np.int64), device=self.device)
+        s = ch.from_i64(t, len(ch.all_primes), ch.all_map())[0]
+        return ch.ntt_fwd(s, len(ch.all_primes), ch.all_map())
+
+    def _mul_all(self, a, b):
+        ch = self.chain
+        return ch.mul(a, b, len(ch.all_primes), lmap=ch.all_map())
+
+    def _make_ksk(self, source_ntt: torch.Tensor, rng) -> KeySwitchKey:
+        """keys.py:49-71 on the device; row j holds P * source on the limbs of
+        digit j (a single limb when alpha == 1, exactly the reference)."""
+        ch = self.chain
+        full = ch.all_primes
+        kl = len(full)
+        amap = ch.all_map()
+        rows = []
+        digits = [(lo, min(lo + self.alpha, ch.lq)) for lo in range(0, ch.lq, self.alpha)]
+        out = torch.empty(len(digits), 2, kl, self.n, dtype=U64, device=self.device)
+        for j, (lo, hi) in enumerate(digits):
+            a_np = np.stack([rng.integers(0, p, self.n, dtype=np.uint64) for p in full])
+            e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
+            a = ch.upload_u64(a_np)
+            e = ch.from_i64(torch.from_numpy(e_np).to(self.device), kl, amap)[0]
+            ch.ntt_fwd(e, kl, amap)
+            b = ch.mul(a, self.sk.s_full, kl, lmap=amap)
+            ch.sub(e, b, kl, out=b, lmap=amap)  # b = -a*s + e
+            idx = tuple(range(lo, hi))
+            lmap = ch.custom_map(idx)
+            pv = ch.scalar_pairs(ch.special_product, idx)
+            msg = ch.scalar_mul(source_ntt[lo:hi].contiguous(), pv, hi - lo, lmap=lmap)
+            b[lo:hi] = ch.add(b[lo:hi].contiguous(), msg, hi - lo, lmap=lmap)
+            out[j, 0] = b
+            out[j, 1] = a
+            rows.append(j)
+        return KeySwitchKey(out)
+
+    def rotation_key(self, galois: int) -> KeySwitchKey:
+        try:
+            return self.rotation_keys[galois]
+        except KeyError:
+            raise self._errors.MissingRotationKey(f"no key for Galois element {galois}") from None
+
+    # ------------------------------------------------------------------ helpers
+    def _scale(self, level: int) -> float:
+        return self.chain.scale_at[level]
+
+    def _limbs(self, level: int) -> int:
+        return self.chain.level_limbs[level]
+
+    def _bconv(self, m: int):
+        """ModUp tables for hybrid digits at a ciphertext with m limbs:
+        [digit][i][ qhat_i^-1 mod q_i, shoup, ([qhat_i]_{p_e}, shoup) for e in ext ]."""
+        if self.alpha == 1:
+            return None
+        if m in self._bconv_cache:
+            return self._bconv_cache[m]
+        ch = self.chain
+        ext = list(range(m)) + list(range(ch.lq, ch.lq + ch.k))
+        nd = -(-m // self.alpha)
+        width = 2 + 2 * len(ext)
+        tab = np.zeros((nd, self.alpha, width), dtype=np.uint64)
+        for j in range(nd):
+            lo, hi = j * self.alpha, min((j + 1) * self.alpha, m)
+            qs = ch.all_primes[lo:hi]
+            Qj = math.prod(qs)
+            for i, q in enumerate(qs):
+                qhat = Qj // q
+                inv = pow(qhat % q, -1, q)
+                tab[j, i, 0] = inv
+                tab[j, i, 1] = shoup(inv, q)
+                for e, pi in enumerate(ext):
+                    p = ch.all_primes[pi]
+                    c = qhat % p
+                    tab[j, i, 2 + 2 * e] = c
+                    tab[j, i, 3 + 2 * e] = shoup(c, p)
+        t = torch.from_numpy(tab.reshape(-1)).to(self.device)
+        self._bconv_cache[m] = t
+        return t
+
+    def _key_switch(self, d: torch.Tensor, m: int, key: KeySwitchKey = None, key_ptrs=None,
+                    addend=None, addend_polys: int = 0, n_rescale: int = 0) -> torch.Tensor:
+        """keys.py:74-100 (+ the following add and optional rescale, fused).
+
+        d: [B, m, N] coefficient domain.  Returns [B, 2, m - n_rescale, N]."""
+        ch = self.chain
+        batch = d.shape[0]
+        ext = m + ch.k
+        emap = ch.ext_map(m)
+        digits = ch.modup(d, m, self.alpha, self._bconv(m))
+        ch.ntt_fwd(digits, ext, emap)
+        acc = ch.ks_inner(digits, m, key=key.data if key is not None else None, key_ptrs=key_ptrs)
+        ch.ntt_inv(acc, ext, emap)
+        out = ch.divround(acc, 2 * batch, ext, ch.k, n_rescale, addend=addend,
+                          addend_polys=addend_polys, addend_period=2, lmap=emap)
+        return out.view(batch, 2, m - n_rescale, self.n)
+
+    def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
+        """backend.py:94-112: restrict to target+1, integer scalar onto the
+        target scale, rescale — one fused ckb_divround launch."""
+        if ct.level == target:
+            return ct
+        if ct.level < target:
+            raise self._errors.IncompatibleOperands("cannot raise a ciphertext's level")
+        ch = self.chain
+        staging = target + 1
+        ms = self._limbs(staging)
+        key = (ct.level, target)
+        if key not in self._adjust_cache:
+            s_star = self._scale(target) * ch.entry_products[staging] / self._scale(ct.level)
+            factor = int(np.rint(s_star))
+            self._adjust_cache[key] = ch.scalar_pairs(factor, range(ms))
+        pre = self._adjust_cache[key]
+        m_full = ct.data.shape[1]
+        out = ch.divround(ct.data, 2, ms, len(ch.entry_primes[staging]), prescale=pre,
+                          in_poly_stride=m_full * self.n)
+        return GpuCiphertext(out, target)
+
+    def _rescale(self, data: torch.Tensor, level: int) -> GpuCiphertext:
+        """backend.py:86-92: divide-round by entry_primes[level], last first."""
+        m = self._limbs(level)
+        out = self.chain.divround(data, 2, m, len(self.chain.entry_primes[level]))
+        return GpuCiphertext(out, level - 1)
+
+    def _encode_rns(self, values, level: int, ntt: bool = False) -> torch.Tensor:
+        """encode (encoding.py:57-65) -> [limbs, N] residues; cached per value."""
+        vals = np.asarray(values, dtype=np.float64)
+        key = (vals.tobytes(), level, ntt)
+        hit = self._enc_cache.get(key)
+        if hit is not None:
+            self._enc_cache.move_to_end(key)
+            return hit
+        ch = self.chain
+        m = self._limbs(level)
+        coeffs = self.encoder.embed_device(vals, self._scale(level))
+        bound = float(coeffs.abs().max())
+        if bound >= MAX_SAFE_COEFF:
+            raise self._errors.EncodingOverflow(
+                "scaled values exceed the exactly-representable coefficient range")
+        if 4.0 * bound >= float(ch.modulus_at(level)):
+            raise self._errors.EncodingOverflow(
+                f"encoded coefficients (~2^{np.log2(bound + 1):.1f}) do not fit the current "
+                f"modulus with headroom")
+        res = ch.from_i64(coeffs.to(torch.int64), m)[0]
+        if ntt:
+            ch.ntt_fwd(res, m)
+        self._enc_cache[key] = res
+        if len(self._enc_cache) > self._enc_cache_cap:
+            self._enc_cache.popitem(last=False)
+        return res
+
+    # ------------------------------------------------------------------ hooks
+    def _payload_elementwise(self, kind: str, a, b, out_level: int):
+        ch = self.chain
+        ct_a: GpuCiphertext = a.payload
+        op = kind[:3]
+        if kind.endswith("_ct"):
+            ct_b: GpuCiphertext = b.payload
+            in_level = out_level + 1 if op == "mul" else out_level
+            ct_a = self._adjust_to_level(ct_a, in_level)
+            ct_b = self._adjust_to_level(ct_b, in_level)
+            m = self._limbs(in_level)
+            if op == "add":
+                return GpuCiphertext(ch.add(ct_a.data, ct_b.data, m), in_level)
+            if op == "sub":
+                return GpuCiphertext(ch.sub(ct_a.data, ct_b.data, m), in_level)
+            return self._mul_ct(ct_a, ct_b, in_level)
+        in_level = ct_a.level
+        m = self._limbs(in_level)
+        if op == "mul":
+            pt = self._encode_rns(b.values, in_level, ntt=True)
+            x = ch.ntt_fwd(ct_a.data.clone(), m)
+            ch.mul(x, pt, m, out=x, b_rows=m)
+            ch.ntt_inv(x, m)
+            return self._rescale(x, in_level)
+        pt = self._encode_rns(b.values if op == "add" else -b.values, in_level)
+        out = ct_a.data.clone()
+        ch.add(ct_a.data[0], pt, m, out=out[0])
+        return GpuCiphertext(out, in_level)
+
+    def _mul_ct(self, ct_a: GpuCiphertext, ct_b: GpuCiphertext, in_level: int) -> GpuCiphertext:
+        """backend.py:136-143: NTT, tensor, relinearise, add, rescale."""
+        ch = self.chain
+        m = self._limbs(in_level)
+        x = torch.empty(2, 2, m, self.n, dtype=U64, device=self.device)
+        x[0].copy_(ct_a.data)
+        x[1].copy_(ct_b.data)
+        ch.ntt_fwd(x, m)
+        d = ch.tensor(x[0], x[1], m)  # [1, 3, m, N]
+        ch.ntt_inv(d, m)
+        out = self._key_switch(d[:, 2], m, key=self.relin_key, addend=d[:, 0:2],
+                               addend_polys=2, n_rescale=len(ch.entry_primes[in_level]))
+        return GpuCiphertext(out[0], in_level - 1)
+
+    def _payload_rotate(self, a, k: int):
+        ct: GpuCiphertext = a.payload
+        if k == 0:
+            return GpuCiphertext(ct.data.clone(), ct.level)
+        galois = self.galois_for_step.get(k)
+        if galois is None:
+            galois = pow(5, k, 2 * self.n)
+        key = self.rotation_key(galois)
+        m = self._limbs(ct.level)
+        r = self.chain.automorphism(ct.data, galois, m)
+        out = self._key_switch(r[1:2], m, key=key, addend=r[0:1], addend_polys=1)
+        return GpuCiphertext(out[0], ct.level)
+
+    def _encrypt_values(self, values, level: int) -> GpuCiphertext:
+        """backend.py:173-182: symmetric encryption, RNG (seed, serial)."""
+        ch = self.chain
+        rng = np.random.default_rng((self.rng_seed, next(self._serials)))
+        primes = ch.limbs_at(level)
+        m = len(primes)
+        msg = self._encode_rns(values, level)
+        a_np = np.stack([rng.integers(0, p, self.n, dtype=np.uint64) for p in primes])
+        e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
+        out = torch.empty(2, m, self.n, dtype=U64, device=self.device)
+        out[1].copy_(torch.from_numpy(a_np))
+        ch.mul(out[1], self.sk.s_full[:m], m, out=out[0])
+        ch.neg(out[0], m, out=out[0])
+        ch.ntt_inv(out, m)
+        e = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)[0]
+        ch.add(out[0], msg, m, out=out[0])
+        ch.add(out[0], e, m, out=out[0])
+        return GpuCiphertext(out, level)
+
+    def _payload_encrypt(self, pv, level: int, serial: int):
+        return self._encrypt_values(pv.values, level)
+
+    def _phase(self, ct: GpuCiphertext) -> torch.Tensor:
+        ch = self.chain
+        m = ct.data.shape[1]
+        t = ch.ntt_fwd(ct.data[1].clone(), m)
+        ch.mul(t, self.sk.s_full[:m], m, out=t)
+        ch.ntt_inv(t, m)
+        return ch.add(ct.data[0], t, m, out=t)
+
+    def _decrypt_values(self, ct: GpuCiphertext) -> np.ndarray:
+        """backend.py:187-190: phase, centered CRT lift, decode."""
+        m = ct.data.shape[1]
+        coeffs = self.chain.to_f64(self._phase(ct), m)[0]
+        return self.encoder.unembed_device(coeffs, self._scale(ct.level)).cpu().numpy()
+
+    def _payload_decrypt(self, cv):
+        return self._decrypt_values(cv.payload)
+
+    def _payload_bootstrap(self, cv, serial: int):
+        """Custodian refresh (backend.py:195-206): decrypt, optional U(+-eps),
+        re-encrypt at refresh_level.  Real CKKS bootstrapping is bootstrap.py."""
+        values = self._decrypt_values(cv.payload)
+        if self.bootstrap_eps > 0.0:
+            values = values + self._bs_rng.uniform(-self.bootstrap_eps, self.bootstrap_eps,
+                                                   values.shape[0])
+        return self._encrypt_values(values, self.params.refresh_level)
+
+    # ------------------------------------------------------------ serialization
+    def serialize_cipher(self, cv) -> bytes:
+        """RBCT (backend.py:210-222): header then c0, c1 coefficient planes, LE u64."""
+        ct: GpuCiphertext = cv.payload
+        head = struct.pack("<4sIQId", CT_MAGIC, SERIAL_VERSION, self.n, ct.level, cv.scale_bits)
+        body = ct.data.cpu().numpy().astype("<u8").tobytes()
+        return head + body
+
+    def deserialize_cipher(self, blob: bytes):
+        fmt = "<4sIQId"
+        hs = struct.calcsize(fmt)
+        E = self._errors
+        if len(blob) < hs:
+            raise E.SerializationError("truncated ciphertext header")
+        magic, version, degree, level, scale_bits = struct.unpack(fmt, blob[:hs])
+        if magic != CT_MAGIC:
+            raise E.SerializationError(f"bad ciphertext magic {magic!r}")
+        if version != SERIAL_VERSION:
+            raise E.SerializationError(f"unsupported ciphertext version {version}")
+        if degree != self.n:
+            raise E.SerializationError("ciphertext degree does not match parameters")
+        if not 0 <= level <= self.params.level:
+            raise E.SerializationError(f"ciphertext level {level} out of range")
+        m = self._limbs(level)
+        body = blob[hs:]
+        if len(body) != 2 * m * degree * 8:
+            raise E.SerializationError("ciphertext body length mismatch")
+        arr = np.frombuffer(body, dtype="<u8").reshape(2, m, degree).astype(np.uint64)
+        data = torch.from_numpy(arr).to(self.device)
+        rl = self.params.refresh_level
+        return self._api.CipherVector(
+            payload=GpuCiphertext(data, level), level_remaining=level, scale_bits=scale_bits,
+            depth=rl - level if level < rl else 0, backend_id=self.backend_id,
+            keyset_id=self.keyset_id, serial=next(self._serials))
+
+    # ---------------------------------------------------------------- raw access
+    def payload_from_planes(self, planes: np.ndarray, level: int) -> GpuCiphertext:
+        """Wrap host (2, limbs, N) coefficient planes as a payload (tests/bench)."""
+        return GpuCiphertext(torch.from_numpy(np.ascontiguousarray(planes, dtype=np.uint64))
+                             .to(self.device), level)
+
+    @staticmethod
+    def planes_of(payload: GpuCiphertext) -> np.ndarray:
+        return payload.data.cpu().numpy()
+
+
+def _hw_secret(n: int, h: int, seed: int) -> np.ndarray:
+    """Ternary secret with exactly h non-zeros (+-1), positions and signs from
+    default_rng((seed, 0x5EC7)) — BASELINE configs' HW-64 / HW-192 secrets."""
+    if not 0 < h <= n:
+        raise he_errors.InvalidParameters(f"secret Hamming weight {h} out of range")
+    rng = np.random.default_rng((seed, 0x5EC7))
+    s = np.zeros(n, dtype=np.int64)
+    pos = rng.choice(n, size=h, replace=False)
+    s[pos] = rng.choice(np.array([-1, 1], dtype=np.int64), size=h)
+    return s
+
+
+class B200Backend(B200CkksCore, he_api.Backend):
+    """The B200 CKKS backend bound to this package's HE API mirror."""
+
+
+def save_custodian(custodian) -> bytes:
+    """RBKY key container (backend.py:250-271): params, rotations, seed, eps, secret."""
+    be = custodian.backend
+    if not isinstance(be, B200CkksCore):
+        raise he_errors.SerializationError("key files apply to the CKKS backend")
+    out = io.BytesIO()
+    out.write(struct.pack("<4sIQ", KEY_MAGIC, SERIAL_VERSION, be.params.poly_degree))
+    out.write(be.params.digest())
+    blob = json.dumps(dataclasses.asdict(be.params), sort_keys=True).encode()
+    out.write(struct.pack("<I", len(blob)))
+    out.write(blob)
+    rots = sorted(be.rotation_indices)
+    out.write(struct.pack("<I", len(rots)))
+    out.write(struct.pack(f"<{len(rots)}q", *rots))
+    out.write(struct.pack("<qd", be.rng_seed, be.bootstrap_eps))
+    out.write(be.sk.coeffs.astype("<i1").tobytes())
+    return out.getvalue()
+
+
+def load_custodian(blob: bytes, **backend_options):
+    """Inverse of save_custodian; evaluation keys are regenerated (backend.py:274-293)."""
+    from .scheme import SchemeParams
+
+    buf = io.BytesIO(blob)
+    magic, version, degree = struct.unpack("<4sIQ", buf.read(16))
+    if magic != KEY_MAGIC:
+        raise he_errors.SerializationError(f"bad key magic {magic!r}")
+    if version != SERIAL_VERSION:
+        raise he_errors.SerializationError(f"unsupported key version {version}")
+    digest = buf.read(32)
+    (n_params,) = struct.unpack("<I", buf.read(4))
+    raw = json.loads(buf.read(n_params).decode())
+    raw["modulus_chain"] = tuple(raw["modulus_chain"])
+    params = SchemeParams(**raw)
+    if params.digest() != digest:
+        raise he_errors.SerializationError("key file parameter digest mismatch")
+    (n_rots,) = struct.unpack("<I", buf.read(4))
+    rots = struct.unpack(f"<{n_rots}q", buf.read(8 * n_rots))
+    seed, eps = struct.unpack("<qd", buf.read(16))
+    secret = np.frombuffer(buf.read(degree), dtype="<i1").astype(np.int64)
+    be = B200Backend(params, rotation_indices=rots, rng_seed=seed, bootstrap_eps=eps,
+                     _secret=secret, **backend_options)
+    return he_api.KeyCustodian(be, rots)

@@ -1,0 +1,70 @@
+#pragma once
+// Shared internals of the B200 RNS-CKKS kernels (sm_100a); see include/ckks_b200.h.
+//
+// Every kernel replaces one numpy routine of the reference CKKS backend
+// (/root/reference/pkg/src/ciphermlp/ckks/*.py); see the header for the map.
+// The work is 64-bit modular integer arithmetic: HBM- or IMAD-bound, never a
+// GEMM, so there are no tensor-core paths here.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/ckks_b200.h"
+#include "modarith.cuh"
+
+using ckb::Mod;
+
+namespace ckb_internal {
+
+constexpr int kMaxLimbs = CKB_MAX_LIMBS;
+
+struct LimbMap {
+  int16_t p[kMaxLimbs];
+};
+
+struct RingDev {
+  const uint64_t* mods;  // [np][8]
+  const uint64_t* ntt;   // [np][4][N]
+  const uint64_t* pair;  // [np][np][4]
+  uint32_t log_n;
+  uint32_t np;
+};
+
+__device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
+  const uint64_t* m = R.mods + (size_t)pi * 8;
+  Mod r;
+  r.p = __ldg(m + 0);
+  r.mu = __ldg(m + 1);
+  r.k = __ldg(m + 2);
+  r.two_p = __ldg(m + 3);
+  return r;
+}
+
+inline bool make_map(LimbMap& m, const int32_t* src, int n) {
+  if (n <= 0 || n > kMaxLimbs || src == nullptr) return false;
+  for (int i = 0; i < n; ++i) m.p[i] = (int16_t)src[i];
+  return true;
+}
+
+inline RingDev make_ring(const ckb_ring* r) {
+  RingDev d;
+  d.mods = r->mods;
+  d.ntt = r->ntt;
+  d.pair = r->pair;
+  d.log_n = r->log_n;
+  d.np = r->n_primes;
+  return d;
+}
+
+inline int finish() { return (int)cudaGetLastError(); }
+
+inline int grid_for(size_t work, int block) {
+  size_t g = (work + block - 1) / block;
+  // persistent-ish cap: 148 SMs x 16 resident CTAs of 256 threads
+  size_t cap = 148 * 16;
+  return (int)std::max<size_t>(1, std::min(g, cap));
+}
+
+}  // namespace ckb_internal

@@ -1,0 +1,134 @@
+// Word-size modular arithmetic for RNS-CKKS limbs (primes p < 2^62).
+//
+// Shared by the device kernels and by the host-side table builders so the
+// same code can be unit-tested on the CPU against unsigned __int128.
+//
+//  * Shoup multiplication by a constant w (twiddles, CRT constants):
+//      w' = floor(w * 2^64 / p);  q = hi(x * w');  r = x*w - q*p in [0, 2p)
+//    valid for any 64-bit x, which is what the lazy Harvey butterflies need.
+//  * Barrett multiplication of two canonical residues (Hadamard products,
+//    key inner products): mu = floor(2^(2k) / p) with k = bitlen(p);
+//    q3 = ((x >> (k-1)) * mu) >> (k+1) underestimates floor(x/p) by <= 2,
+//    so r = x - q3*p lies in [0, 3p) and two conditional subtractions finish.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define CKB_HD __host__ __device__ __forceinline__
+#else
+#define CKB_HD inline
+#endif
+
+namespace ckb {
+
+// Per-prime constants; laid out as 4 x u64 in the device modulus table.
+struct Mod {
+  uint64_t p;      // the prime
+  uint64_t mu;     // floor(2^(2k) / p)
+  uint64_t k;      // bit length of p
+  uint64_t two_p;  // 2p (lazy-reduction bound)
+};
+
+CKB_HD uint64_t mulhi(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+CKB_HD uint64_t add_mod(uint64_t a, uint64_t b, uint64_t p) {
+  uint64_t s = a + b;
+  return s >= p ? s - p : s;
+}
+
+CKB_HD uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t p) {
+  return a >= b ? a - b : a + p - b;
+}
+
+CKB_HD uint64_t neg_mod(uint64_t a, uint64_t p) { return a == 0 ? 0 : p - a; }
+
+// Shoup: x * w mod p with precomputed ws = floor(w * 2^64 / p); result in [0, 2p).
+CKB_HD uint64_t mul_shoup_lazy(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
+  uint64_t q = mulhi(x, ws);
+  return x * w - q * p;
+}
+
+CKB_HD uint64_t mul_shoup(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
+  uint64_t r = mul_shoup_lazy(x, w, ws, p);
+  return r >= p ? r - p : r;
+}
+
+// Barrett reduction of a 128-bit value (hi, lo) < 2^(2k) to [0, p).
+CKB_HD uint64_t barrett_reduce128(uint64_t hi, uint64_t lo, const Mod& m) {
+  const uint32_t k = (uint32_t)m.k;
+  // q1 = x >> (k-1)  (< 2^(k+1) <= 2^63)
+  uint64_t q1 = (lo >> (k - 1)) | (hi << (65 - k));
+  // q3 = (q1 * mu) >> (k+1)
+  uint64_t plo = q1 * m.mu;
+  uint64_t phi = mulhi(q1, m.mu);
+  uint64_t q3 = (plo >> (k + 1)) | (phi << (63 - k));
+  uint64_t r = lo - q3 * m.p;
+  if (r >= m.two_p) r -= m.two_p;
+  if (r >= m.p) r -= m.p;
+  return r;
+}
+
+// a * b mod p for canonical a, b.
+CKB_HD uint64_t mul_mod(uint64_t a, uint64_t b, const Mod& m) {
+  return barrett_reduce128(mulhi(a, b), a * b, m);
+}
+
+// x mod p for an arbitrary 64-bit x.
+CKB_HD uint64_t reduce64(uint64_t x, const Mod& m) {
+  if (x < m.p) return x;
+  if (m.k >= 32) return barrett_reduce128(0, x, m);
+  return x % m.p;
+}
+
+// Centered residue of x (canonical mod q) reduced into prime m:
+// value v = x if x <= q/2 else x - q  (reference: ring.py:341-342, keys.py:85-86),
+// returned as v mod p in [0, p).
+CKB_HD uint64_t centered_into(uint64_t x, uint64_t q, const Mod& m) {
+  if (x > (q >> 1)) {
+    uint64_t mag = reduce64(q - x, m);
+    return mag == 0 ? 0 : m.p - mag;
+  }
+  return reduce64(x, m);
+}
+
+// ---- host-only helpers for table construction -----------------------------
+inline uint64_t shoup_of(uint64_t w, uint64_t p) {
+  return (uint64_t)(((unsigned __int128)w << 64) / p);
+}
+inline uint64_t mul_mod_host(uint64_t a, uint64_t b, uint64_t p) {
+  return (uint64_t)(((unsigned __int128)a * b) % p);
+}
+inline uint64_t pow_mod_host(uint64_t b, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  b %= p;
+  while (e) {
+    if (e & 1) r = mul_mod_host(r, b, p);
+    b = mul_mod_host(b, b, p);
+    e >>= 1;
+  }
+  return r;
+}
+inline uint64_t inv_mod_host(uint64_t a, uint64_t p) {  // p prime
+  return pow_mod_host(a % p, p - 2, p);
+}
+inline uint32_t bitlen(uint64_t x) {
+  uint32_t k = 0;
+  while (x) { ++k; x >>= 1; }
+  return k;
+}
+inline Mod make_mod(uint64_t p) {
+  Mod m;
+  m.p = p;
+  m.k = bitlen(p);
+  m.mu = (uint64_t)(((unsigned __int128)1 << (2 * m.k)) / p);
+  m.two_p = 2 * p;
+  return m;
+}
+
+}  // namespace ckb

@@ -1,0 +1,277 @@
+// Negacyclic NTT kernels (sm_100a): replaces NttPlan.forward/inverse
+// (/root/reference/pkg/src/ciphermlp/ckks/ntt.py:121-154).
+#include "common.cuh"
+
+using namespace ckb_internal;
+using ckb::Mod;
+
+namespace {
+
+// ===========================================================================
+// NTT
+//
+// A length-N negacyclic transform is run as one or two "phases".  A phase
+// applies S = log2(G) consecutive radix-2 stages to independent groups of G
+// elements, element (g, r) living at g*gstride + r*rstride of its limb:
+//   * single phase (N <= 4096): one group = the whole limb;
+//   * two phases (N > 4096): phase A = strided columns (the high stages of the
+//     forward transform), phase B = contiguous rows (the low stages).
+// Inside a CTA the tile (C groups x G) is staged in shared memory; each thread
+// keeps 16 elements in registers and applies up to 4 stages per round
+// (radix-16), with one smem exchange between rounds.  Butterflies are the
+// Harvey lazy forms with Shoup twiddles: forward values live in [0, 4p),
+// inverse values in [0, 2p), and the last phase canonicalises.
+// Twiddle of stage bit b for element r in group gidx (derivation in DESIGN.md):
+//   idx = ((M0 + gt*gidx) << (S-1-b)) + (r >> (b+1))
+// ===========================================================================
+
+struct NttPhase {
+  int limbs;
+  int tiles_per_row;
+  int C;        // groups per CTA
+  int gstride;  // element stride between groups
+  int rstride;  // element stride inside a group
+  int M0;
+  int gt;
+  int last;     // forward: canonicalise; inverse: fold N^-1 into the top stage
+  int row0;     // first row handled by this launch (for L2-resident chunking)
+};
+
+template <int S>
+__device__ __forceinline__ int sidx(int g, int r) {
+  constexpr int G = 1 << S;
+  return g * (G + 1) + (r ^ ((r >> 4) & 15));
+}
+
+template <int S, int HI>
+__device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
+                                           const uint64_t* __restrict__ tws, const Mod& m,
+                                           int gq, int gidx, int w, const NttPhase& ph) {
+  if constexpr (HI > 0) {
+    constexpr int Q = HI < 4 ? HI : 4;
+    constexpr int LO = HI - Q;
+    constexpr int WLO = HI - 4 > 0 ? HI - 4 : 0;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + 4));
+    uint64_t x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    const int tbase = ph.M0 + ph.gt * gidx;
+    const uint64_t p = m.p, two_p = m.two_p;
+#pragma unroll
+    for (int b = HI - 1; b >= LO; --b) {
+      const int bb = b - WLO;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k & (1 << bb)) continue;
+        const int r = rbase | (k << WLO);
+        const int ti = (tbase << (S - 1 - b)) + (r >> (b + 1));
+        const uint64_t W = __ldg(tw + ti), Ws = __ldg(tws + ti);
+        uint64_t X = x[k];
+        X = X >= two_p ? X - two_p : X;
+        const uint64_t T = ckb::mul_shoup_lazy(x[k | (1 << bb)], W, Ws, p);
+        x[k] = X + T;
+        x[k | (1 << bb)] = X - T + two_p;
+      }
+    }
+    if (LO == 0 && ph.last) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        uint64_t X = x[k];
+        X = X >= two_p ? X - two_p : X;
+        x[k] = X >= p ? X - p : X;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    __syncthreads();
+    fwd_rounds<S, LO>(s, tw, tws, m, gq, gidx, w, ph);
+  }
+}
+
+template <int S, int LO>
+__device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
+                                           const uint64_t* __restrict__ tws, const Mod& m,
+                                           uint64_t ninv, uint64_t ninvs, uint64_t fw,
+                                           uint64_t fws, int gq, int gidx, int w,
+                                           const NttPhase& ph) {
+  if constexpr (LO < S) {
+    constexpr int Q = (S - LO) < 4 ? (S - LO) : 4;
+    constexpr int HI = LO + Q;
+    constexpr int WLO = LO < S - 4 ? LO : S - 4;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + 4));
+    uint64_t x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    const int tbase = ph.M0 + ph.gt * gidx;
+    const uint64_t p = m.p, two_p = m.two_p;
+#pragma unroll
+    for (int b = LO; b < HI; ++b) {
+      const int bb = b - WLO;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k & (1 << bb)) continue;
+        const uint64_t X = x[k], Y = x[k | (1 << bb)];
+        uint64_t sum = X + Y;
+        sum = sum >= two_p ? sum - two_p : sum;
+        const uint64_t d = X - Y + two_p;
+        if (b == S - 1 && ph.last) {
+          x[k] = ckb::mul_shoup(sum, ninv, ninvs, p);
+          x[k | (1 << bb)] = ckb::mul_shoup(d, fw, fws, p);
+        } else {
+          const int r = rbase | (k << WLO);
+          const int ti = (tbase << (S - 1 - b)) + (r >> (b + 1));
+          const uint64_t W = __ldg(tw + ti), Ws = __ldg(tws + ti);
+          x[k] = sum;
+          x[k | (1 << bb)] = ckb::mul_shoup_lazy(d, W, Ws, p);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    __syncthreads();
+    inv_rounds<S, HI>(s, tw, tws, m, ninv, ninvs, fw, fws, gq, gidx, w, ph);
+  }
+}
+
+template <int S, bool FWD>
+__global__ void __launch_bounds__(256) k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph,
+                                                   RingDev R, LimbMap lm) {
+  constexpr int G = 1 << S;
+  extern __shared__ uint64_t smem[];
+  const int N = 1 << R.log_n;
+  const int row = ph.row0 + blockIdx.x / ph.tiles_per_row;
+  const int tile = blockIdx.x % ph.tiles_per_row;
+  const int pi = lm.p[row % ph.limbs];
+  const Mod m = load_mod(R, pi);
+  uint64_t* base = data + (size_t)row * N;
+  const int C = ph.C;
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int g0 = tile * C;
+
+  for (int idx = tid; idx < C * G; idx += T) {
+    int g, r;
+    if (ph.rstride == 1) {
+      g = idx >> S;
+      r = idx & (G - 1);
+    } else {
+      r = idx / C;
+      g = idx - r * C;
+    }
+    smem[sidx<S>(g, r)] = base[(size_t)(g0 + g) * ph.gstride + (size_t)r * ph.rstride];
+  }
+  __syncthreads();
+
+  const int gq = tid / (G / 16);
+  const int w = tid % (G / 16);
+  const int gidx = g0 + gq;
+  const uint64_t* tables = R.ntt + (size_t)pi * 4 * N;
+  if constexpr (FWD) {
+    fwd_rounds<S, S>(smem, tables, tables + N, m, gq, gidx, w, ph);
+  } else {
+    const uint64_t* mm = R.mods + (size_t)pi * 8;
+    inv_rounds<S, 0>(smem, tables + 2 * N, tables + 3 * N, m, __ldg(mm + 4), __ldg(mm + 5),
+                     __ldg(mm + 6), __ldg(mm + 7), gq, gidx, w, ph);
+  }
+
+  for (int idx = tid; idx < C * G; idx += T) {
+    int g, r;
+    if (ph.rstride == 1) {
+      g = idx >> S;
+      r = idx & (G - 1);
+    } else {
+      r = idx / C;
+      g = idx - r * C;
+    }
+    base[(size_t)(g0 + g) * ph.gstride + (size_t)r * ph.rstride] = smem[sidx<S>(g, r)];
+  }
+}
+
+template <bool FWD>
+int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const RingDev& R,
+                 const LimbMap& lm, cudaStream_t st) {
+  const int G = 1 << S;
+  const int threads = ph.C * G / 16;
+  const size_t smem = (size_t)ph.C * (G + 1) * sizeof(uint64_t);
+  const int blocks = nrows * ph.tiles_per_row;
+  if (blocks <= 0) return 0;
+#define CKB_NTT_CASE(SS)                                                           \
+  case SS:                                                                         \
+    k_ntt_phase<SS, FWD><<<blocks, threads, smem, st>>>(data, ph, R, lm);          \
+    break;
+  switch (S) {
+    CKB_NTT_CASE(4)
+    CKB_NTT_CASE(5)
+    CKB_NTT_CASE(6)
+    CKB_NTT_CASE(7)
+    CKB_NTT_CASE(8)
+    CKB_NTT_CASE(9)
+    CKB_NTT_CASE(10)
+    CKB_NTT_CASE(11)
+    CKB_NTT_CASE(12)
+    default:
+      return CKB_E_LOGN;
+  }
+#undef CKB_NTT_CASE
+  return 0;
+}
+
+template <bool FWD>
+int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
+            void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0) return CKB_E_LIMBS;
+  if (rows == 0) return 0;
+  const RingDev R = make_ring(ring);
+  const int logn = (int)R.log_n;
+  if (logn < 4 || logn > 20) return CKB_E_LOGN;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = 1 << logn;
+  if (logn <= 12) {
+    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0};
+    int rc = launch_phase<FWD>(logn, data, ph, rows, R, lm, st);
+    return rc ? rc : finish();
+  }
+  const int s2 = logn / 2;        // low stages (contiguous rows, phase B)
+  const int s1 = logn - s2;       // high stages (strided columns, phase A)
+  if (s1 > 12) return CKB_E_LOGN;
+  const int GA = 1 << s1, GB = 1 << s2;
+  const int CA = std::max(1, 4096 / GA), CB = std::max(1, 4096 / GB);
+  // phase A: groups are the GB columns, elements strided by GB
+  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0};
+  // phase B: groups are the GA rows of GB contiguous elements
+  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0};
+  // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
+  const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
+  for (int r0 = 0; r0 < rows; r0 += chunk) {
+    const int nr = std::min(chunk, rows - r0);
+    pa.row0 = r0;
+    pb.row0 = r0;
+    int rc;
+    if (FWD) {
+      rc = launch_phase<FWD>(s1, data, pa, nr, R, lm, st);
+      if (!rc) rc = launch_phase<FWD>(s2, data, pb, nr, R, lm, st);
+    } else {
+      rc = launch_phase<FWD>(s2, data, pb, nr, R, lm, st);
+      if (!rc) rc = launch_phase<FWD>(s1, data, pa, nr, R, lm, st);
+    }
+    if (rc) return rc;
+  }
+  return finish();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
+                    const int32_t* limb_prime, void* stream) {
+  return ntt_run<true>(ring, data, rows, limbs, limb_prime, stream);
+}
+
+int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
+                    const int32_t* limb_prime, void* stream) {
+  return ntt_run<false>(ring, data, rows, limbs, limb_prime, stream);
+}
+
+}  // extern "C"

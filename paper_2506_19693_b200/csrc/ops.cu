@@ -1,0 +1,600 @@
+// Limb arithmetic, key switching, rescale, automorphism and conversion kernels
+// (sm_100a) replacing ciphermlp/ckks/{ring,keys,backend}.py numpy routines.
+#include "common.cuh"
+
+using namespace ckb_internal;
+using ckb::Mod;
+
+namespace {
+
+// ===========================================================================
+// Element-wise limb arithmetic
+// ===========================================================================
+
+__global__ void k_elementwise(int op, uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                              const uint64_t* __restrict__ b, const uint64_t* __restrict__ c,
+                              size_t total, size_t bperiod, int log_n, int limbs, RingDev R,
+                              LimbMap lm) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i >> log_n);
+    const Mod m = load_mod(R, lm.p[row % limbs]);
+    const uint64_t x = a[i];
+    const size_t ib = bperiod ? i % bperiod : i;
+    uint64_t r;
+    switch (op) {
+      case 0: r = ckb::add_mod(x, b[ib], m.p); break;
+      case 1: r = ckb::sub_mod(x, b[ib], m.p); break;
+      case 2: r = ckb::mul_mod(x, b[ib], m); break;
+      case 3: r = ckb::neg_mod(x, m.p); break;
+      default: r = ckb::add_mod(ckb::mul_mod(x, b[ib], m), c[ib], m.p); break;
+    }
+    out[i] = r;
+  }
+}
+
+struct ScalarTab {
+  uint64_t v[kMaxLimbs];
+  uint64_t s[kMaxLimbs];
+};
+
+__global__ void k_scalar_mul(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                             size_t total, int log_n, int limbs, RingDev R, LimbMap lm,
+                             ScalarTab sc) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i >> log_n) % limbs;
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+    out[i] = ckb::mul_shoup(a[i], sc.v[l], sc.s[l], p);
+  }
+}
+
+__global__ void k_tensor(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                         const uint64_t* __restrict__ b, size_t total, int log_n, int limbs,
+                         RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t poly = (size_t)limbs * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t bi = i / poly, off = i - bi * poly;
+    const int l = (int)(off >> log_n);
+    const Mod m = load_mod(R, lm.p[l]);
+    const uint64_t* pa = a + bi * 2 * poly + off;
+    const uint64_t* pb = b + bi * 2 * poly + off;
+    const uint64_t a0 = pa[0], a1 = pa[poly], b0 = pb[0], b1 = pb[poly];
+    uint64_t* po = out + bi * 3 * poly + off;
+    po[0] = ckb::mul_mod(a0, b0, m);
+    po[poly] = ckb::add_mod(ckb::mul_mod(a0, b1, m), ckb::mul_mod(a1, b0, m), m.p);
+    po[2 * poly] = ckb::mul_mod(a1, b1, m);
+  }
+}
+
+// ===========================================================================
+// Key switching: ModUp and the key inner product
+// ===========================================================================
+
+// One thread per (batch, digit, coefficient); writes the digit's value in
+// every extended limb (coalesced across coefficients).
+__global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in, int batch,
+                        int limbs, int ext, int alpha, int n_digits, int log_n, RingDev R,
+                        LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)batch * n_digits * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t bj = t >> log_n;
+    const int j = (int)(bj % n_digits);
+    const size_t bi = bj / n_digits;
+    const uint64_t* src = in + bi * limbs * N + n;
+    uint64_t* dst = out + (bi * n_digits + j) * ext * N + n;
+    const int first = j * alpha;
+    const int cnt = min(alpha, limbs - first);
+    if (alpha == 1) {
+      const uint64_t x = src[(size_t)first * N];
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * 8);
+      for (int e = 0; e < ext; ++e) {
+        const Mod m = load_mod(R, em.p[e]);
+        dst[(size_t)e * N] = (e == first) ? x : ckb::centered_into(x, q, m);
+      }
+    } else {
+      // y_i = [x_i * qhat_i^-1]_{q_i};  out_e = sum_i y_i * [qhat_i]_{p_e}
+      uint64_t y[16];
+      const size_t stride_i = 2 + 2 * (size_t)ext;
+      const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < cnt) {
+          const uint64_t x = src[(size_t)(first + i) * N];
+          const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * 8);
+          y[i] = ckb::mul_shoup(x, __ldg(tab + i * stride_i), __ldg(tab + i * stride_i + 1), q);
+        }
+      }
+      for (int e = 0; e < ext; ++e) {
+        if (e >= first && e < first + cnt) {
+          dst[(size_t)e * N] = src[(size_t)e * N];
+          continue;
+        }
+        const Mod m = load_mod(R, em.p[e]);
+        uint64_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i < cnt) {
+            const uint64_t* c = tab + i * stride_i + 2 + 2 * e;
+            uint64_t v = ckb::mul_shoup_lazy(y[i], __ldg(c), __ldg(c + 1), m.p);
+            acc += v;
+            acc = acc >= m.two_p ? acc - m.two_p : acc;
+          }
+        }
+        dst[(size_t)e * N] = acc >= m.p ? acc - m.p : acc;
+      }
+    }
+  }
+}
+
+__global__ void k_ks_inner(uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig,
+                           int batch, int nd, int ext, int log_n, const uint64_t* __restrict__ key,
+                           const uint64_t* const* __restrict__ key_ptrs, int key_limbs, RingDev R,
+                           LimbMap em, LimbMap km) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)batch * ext * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t be = t >> log_n;
+    const int e = (int)(be % ext);
+    const size_t bi = be / ext;
+    const Mod m = load_mod(R, em.p[e]);
+    const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
+    const size_t krow = 2 * (size_t)key_limbs * N;
+    const uint64_t* kb = K + (size_t)km.p[e] * N + n;
+    const uint64_t* ka = kb + (size_t)key_limbs * N;
+    const uint64_t* d = dig + (bi * nd * ext + e) * N + n;
+    uint64_t sb = 0, sa = 0;
+    for (int j = 0; j < nd; ++j) {
+      const uint64_t x = d[(size_t)j * ext * N];
+      sb = ckb::add_mod(sb, ckb::mul_mod(x, __ldg(kb + j * krow), m), m.p);
+      sa = ckb::add_mod(sa, ckb::mul_mod(x, __ldg(ka + j * krow), m), m.p);
+    }
+    uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
+    o[0] = sb;
+    o[(size_t)ext * N] = sa;
+  }
+}
+
+// ===========================================================================
+// Exact divide-and-round (rescale / ModDown / level adjust)
+// ===========================================================================
+
+constexpr int kMaxDrop = 16;
+
+// x_j <- (x_j - [r]_{p_j}) * drop^-1  for a centered remainder r = (neg ? -mag : mag)
+__device__ __forceinline__ uint64_t apply_drop(uint64_t xj, bool neg, uint64_t mag, int pd, int pj,
+                                               const Mod& mj, const RingDev& R) {
+  const uint64_t rm = ckb::reduce64(mag, mj);
+  const uint64_t diff = neg ? ckb::add_mod(xj, rm, mj.p) : ckb::sub_mod(xj, rm, mj.p);
+  const uint64_t* pr = R.pair + ((size_t)pd * R.np + pj) * 4;
+  return ckb::mul_shoup(diff, __ldg(pr), __ldg(pr + 1), mj.p);
+}
+
+__global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                           size_t in_stride, const uint64_t* __restrict__ addend, int add_polys,
+                           int add_period, int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm,
+                           ScalarTab pre, int has_pre) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)polys * N;
+  const int m1 = limbs - n1;   // limbs after the first drop chain
+  const int m2 = m1 - n2;      // output limbs
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t pidx = t >> log_n;
+    const uint64_t* src = in + pidx * in_stride + n;
+    const uint64_t* add = nullptr;
+    if (addend) {
+      const size_t ph = pidx % add_period;
+      if ((int)ph < add_polys) add = addend + ((pidx / add_period) * add_polys + ph) * m1 * N + n;
+    }
+    uint64_t* dst = out + pidx * m2 * N + n;
+
+    auto load = [&](int l) -> uint64_t {
+      uint64_t v = src[(size_t)l * N];
+      if (has_pre) {
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+        v = ckb::mul_shoup(v, pre.v[l], pre.s[l], p);
+      }
+      return v;
+    };
+
+    // ---- first drop chain over limbs [m1, limbs), last limb first
+    bool neg1[kMaxDrop];
+    uint64_t mag1[kMaxDrop];
+    uint64_t tail[kMaxDrop];
+#pragma unroll
+    for (int s = 0; s < kMaxDrop; ++s)
+      if (s < n1) tail[s] = load(m1 + s);
+#pragma unroll
+    for (int d = 0; d < kMaxDrop; ++d) {
+      if (d < n1) {
+        const int li = limbs - 1 - d;          // limb being dropped
+        const int pd = lm.p[li];
+        const uint64_t q = __ldg(R.mods + (size_t)pd * 8);
+        const uint64_t x = tail[li - m1];
+        neg1[d] = x > (q >> 1);
+        mag1[d] = neg1[d] ? q - x : x;
+#pragma unroll
+        for (int s = 0; s < kMaxDrop; ++s) {
+          if (s < li - m1) {
+            const int pj = lm.p[m1 + s];
+            tail[s] = apply_drop(tail[s], neg1[d], mag1[d], pd, pj, load_mod(R, pj), R);
+          }
+        }
+      }
+    }
+    auto stage1 = [&](int l) -> uint64_t {
+      uint64_t v = load(l);
+      const int pj = lm.p[l];
+      const Mod mj = load_mod(R, pj);
+#pragma unroll
+      for (int d = 0; d < kMaxDrop; ++d)
+        if (d < n1) v = apply_drop(v, neg1[d], mag1[d], lm.p[limbs - 1 - d], pj, mj, R);
+      if (add) v = ckb::add_mod(v, add[(size_t)l * N], mj.p);
+      return v;
+    };
+    // ---- second drop chain over limbs [m2, m1)
+    bool neg2[kMaxDrop];
+    uint64_t mag2[kMaxDrop];
+#pragma unroll
+    for (int s = 0; s < kMaxDrop; ++s)
+      if (s < n2) tail[s] = stage1(m2 + s);
+#pragma unroll
+    for (int d = 0; d < kMaxDrop; ++d) {
+      if (d < n2) {
+        const int li = m1 - 1 - d;
+        const int pd = lm.p[li];
+        const uint64_t q = __ldg(R.mods + (size_t)pd * 8);
+        const uint64_t x = tail[li - m2];
+        neg2[d] = x > (q >> 1);
+        mag2[d] = neg2[d] ? q - x : x;
+#pragma unroll
+        for (int s = 0; s < kMaxDrop; ++s) {
+          if (s < li - m2) {
+            const int pj = lm.p[m2 + s];
+            tail[s] = apply_drop(tail[s], neg2[d], mag2[d], pd, pj, load_mod(R, pj), R);
+          }
+        }
+      }
+    }
+    for (int l = 0; l < m2; ++l) {
+      uint64_t v = stage1(l);
+      const int pj = lm.p[l];
+      const Mod mj = load_mod(R, pj);
+#pragma unroll
+      for (int d = 0; d < kMaxDrop; ++d)
+        if (d < n2) v = apply_drop(v, neg2[d], mag2[d], lm.p[m1 - 1 - d], pj, mj, R);
+      dst[(size_t)l * N] = v;
+    }
+  }
+}
+
+// ===========================================================================
+// Automorphism and conversions
+// ===========================================================================
+
+// out[t] = sign * in[src(t)] with src from galois^-1 mod 2N (gather form of
+// ring.py:226-231's scatter).
+__global__ void k_automorphism(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                               size_t total, int log_n, int limbs, uint64_t ginv, RingDev R,
+                               LimbMap lm) {
+  const uint64_t N = 1ull << log_n;
+  const uint64_t mask2 = 2 * N - 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i >> log_n;
+    const uint64_t t = i & (N - 1);
+    const uint64_t sidx2 = (t * ginv) & mask2;
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[row % limbs] * 8);
+    const uint64_t* src = in + row * N;
+    if (sidx2 < N) {
+      out[i] = src[sidx2];
+    } else {
+      out[i] = ckb::neg_mod(src[sidx2 - N], p);
+    }
+  }
+}
+
+__global__ void k_from_i64(uint64_t* __restrict__ out, const int64_t* __restrict__ in,
+                           size_t total, int log_n, int limbs, RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i >> log_n;
+    const size_t poly = row / limbs;
+    const int l = (int)(row % limbs);
+    const int64_t v = in[poly * N + (i & (N - 1))];
+    const Mod m = load_mod(R, lm.p[l]);
+    if (v >= 0) {
+      out[i] = ckb::reduce64((uint64_t)v, m);
+    } else {
+      const uint64_t mag = ckb::reduce64((uint64_t)(-(v + 1)) + 1, m);
+      out[i] = mag == 0 ? 0 : m.p - mag;
+    }
+  }
+}
+
+// Garner mixed-radix digits, centered by comparing x/Q with 1/2, then the
+// value is rebuilt exactly modulo 2^64 when it fits in 63 bits (the case for
+// every decryptable phase) and approximately otherwise.
+__global__ void k_to_f64(double* __restrict__ out, const uint64_t* __restrict__ in, int polys,
+                         int limbs, int log_n, RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)polys * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t poly = t >> log_n;
+    const uint64_t* src = in + poly * limbs * N + n;
+    uint64_t v[kMaxLimbs];
+    for (int i = 0; i < limbs; ++i) {
+      const int pi = lm.p[i];
+      const Mod mi = load_mod(R, pi);
+      uint64_t x = src[(size_t)i * N];
+      for (int s = 0; s < i; ++s) {
+        const int ps = lm.p[s];
+        const uint64_t* pr = R.pair + ((size_t)ps * R.np + pi) * 4;
+        x = ckb::sub_mod(x, ckb::reduce64(v[s], mi), mi.p);
+        x = ckb::mul_shoup(x, __ldg(pr), __ldg(pr + 1), mi.p);
+      }
+      v[i] = x;
+    }
+    // fraction x / Q by Horner from the top digit
+    double f = 0.0;
+    for (int i = limbs - 1; i >= 0; --i) {
+      const double q = (double)__ldg(R.mods + (size_t)lm.p[i] * 8);
+      f = ((double)v[i] + f) / q;
+    }
+    const bool negative = f > 0.5;
+    double approx = 0.0;
+    uint64_t exact = 0, prod = 1;
+    for (int i = 0; i < limbs; ++i) {
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * 8);
+      const uint64_t u = negative ? (q - 1 - v[i]) : v[i];
+      exact += u * prod;
+      prod *= q;
+    }
+    for (int i = limbs - 1; i >= 0; --i) {
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * 8);
+      const uint64_t u = negative ? (q - 1 - v[i]) : v[i];
+      approx = approx * (double)q + (double)u;
+    }
+    if (negative) {
+      exact += 1;
+      approx += 1.0;
+    }
+    double mag = (approx < 4.0e18) ? (double)exact : approx;
+    out[t] = negative ? -mag : mag;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+extern "C" {
+
+int ckb_version(void) { return 1; }
+
+int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64_t* mods_out,
+                     uint64_t* ntt_out, uint64_t* pair_out) {
+  if (log_n < 1 || log_n > 20 || np == 0 || !primes) return CKB_E_ARG;
+  const uint64_t N = 1ull << log_n;
+  for (uint32_t i = 0; i < np; ++i) {
+    const uint64_t p = primes[i];
+    if (p < 3 || (p >> 62) != 0 || (p - 1) % (2 * N) != 0) return CKB_E_ARG;
+    // psi: smallest g >= 2 with psi = g^((p-1)/2N) != 1 and psi^N == -1
+    const uint64_t cof = (p - 1) / (2 * N);
+    uint64_t psi = 0;
+    for (uint64_t g = 2; g < 10000; ++g) {
+      const uint64_t c = ckb::pow_mod_host(g, cof, p);
+      if (c != 1 && ckb::pow_mod_host(c, N, p) == p - 1) {
+        psi = c;
+        break;
+      }
+    }
+    if (!psi) return CKB_E_ARG;
+    const uint64_t psi_inv = ckb::inv_mod_host(psi, p);
+    uint64_t* t = ntt_out + (size_t)i * 4 * N;
+    uint64_t acc = 1, acc_inv = 1;
+    for (uint64_t j = 0; j < N; ++j) {
+      // bit-reverse j over log_n bits
+      uint64_t r = 0;
+      for (uint32_t b = 0; b < log_n; ++b) r |= ((j >> b) & 1ull) << (log_n - 1 - b);
+      t[r] = acc;
+      t[2 * N + r] = acc_inv;
+      acc = ckb::mul_mod_host(acc, psi, p);
+      acc_inv = ckb::mul_mod_host(acc_inv, psi_inv, p);
+    }
+    for (uint64_t j = 0; j < N; ++j) {
+      t[N + j] = ckb::shoup_of(t[j], p);
+      t[3 * N + j] = ckb::shoup_of(t[2 * N + j], p);
+    }
+    const ckb::Mod m = ckb::make_mod(p);
+    const uint64_t ninv = ckb::inv_mod_host(N % p, p);
+    const uint64_t fold = ckb::mul_mod_host(t[2 * N + 1], ninv, p);
+    uint64_t* mo = mods_out + (size_t)i * 8;
+    mo[0] = m.p;
+    mo[1] = m.mu;
+    mo[2] = m.k;
+    mo[3] = m.two_p;
+    mo[4] = ninv;
+    mo[5] = ckb::shoup_of(ninv, p);
+    mo[6] = fold;
+    mo[7] = ckb::shoup_of(fold, p);
+  }
+  for (uint32_t i = 0; i < np; ++i) {
+    for (uint32_t j = 0; j < np; ++j) {
+      uint64_t* pr = pair_out + ((size_t)i * np + j) * 4;
+      const uint64_t pj = primes[j];
+      const uint64_t pim = primes[i] % pj;
+      const uint64_t inv = (i == j || pim == 0) ? 0 : ckb::inv_mod_host(pim, pj);
+      pr[0] = inv;
+      pr[1] = ckb::shoup_of(inv, pj);
+      pr[2] = pim;
+      pr[3] = 0;
+    }
+  }
+  return 0;
+}
+
+int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t* a,
+                    const uint64_t* b, const uint64_t* c, int rows, int limbs,
+                    const int32_t* limb_prime, int b_rows, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0 || op < 0 || op > 4) return CKB_E_ARG;
+  if ((op != 3 && !b) || (op == 4 && !c) || b_rows < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)rows << R.log_n;
+  if (!total) return 0;
+  const size_t bperiod = (b_rows && b_rows < rows) ? ((size_t)b_rows << R.log_n) : 0;
+  k_elementwise<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      op, out, a, b, c, total, bperiod, (int)R.log_n, limbs, R, lm);
+  return finish();
+}
+
+int ckb_scalar_mul(const ckb_ring* ring, uint64_t* out, const uint64_t* a, int rows, int limbs,
+                   const int32_t* limb_prime, const uint64_t* scalars_host, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0 || !scalars_host) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  ScalarTab sc;  // host pairs {value, shoup(value)} per limb
+  for (int l = 0; l < limbs; ++l) {
+    sc.v[l] = scalars_host[2 * l];
+    sc.s[l] = scalars_host[2 * l + 1];
+  }
+  const size_t total = (size_t)rows << R.log_n;
+  if (!total) return 0;
+  k_scalar_mul<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, a, total, (int)R.log_n, limbs, R, lm, sc);
+  return finish();
+}
+
+int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uint64_t* b,
+               int batch, int limbs, const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || batch < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = ((size_t)batch * limbs) << R.log_n;
+  if (!total) return 0;
+  k_tensor<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, a, b, total,
+                                                                    (int)R.log_n, limbs, R, lm);
+  return finish();
+}
+
+int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int batch, int limbs,
+              const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
+              const uint64_t* bconv, void* stream) {
+  LimbMap lm, em;
+  if (!make_map(lm, limb_prime, limbs) || !make_map(em, ext_prime, ext_limbs)) return CKB_E_LIMBS;
+  if (alpha < 1 || alpha > 16 || ext_limbs < limbs || batch < 0) return CKB_E_ARG;
+  if (alpha > 1 && !bconv) return CKB_E_ARG;
+  for (int i = 0; i < limbs; ++i)
+    if (lm.p[i] != em.p[i]) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const int nd = (limbs + alpha - 1) / alpha;
+  const size_t total = ((size_t)batch * nd) << R.log_n;
+  if (!total) return 0;
+  k_modup<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, in, batch, limbs, ext_limbs, alpha, nd, (int)R.log_n, R, lm, em, bconv);
+  return finish();
+}
+
+int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
+                 int n_digits, int ext_limbs, const int32_t* ext_prime, const uint64_t* key,
+                 const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                 void* stream) {
+  LimbMap em, km;
+  if (!make_map(em, ext_prime, ext_limbs) || !make_map(km, key_limb, ext_limbs))
+    return CKB_E_LIMBS;
+  if (batch < 0 || n_digits < 1 || (!key && !key_ptrs)) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = ((size_t)batch * ext_limbs) << R.log_n;
+  if (!total) return 0;
+  k_ks_inner<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      acc, digits, batch, n_digits, ext_limbs, (int)R.log_n, key, key_ptrs, key_limbs, R, em, km);
+  return finish();
+}
+
+int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
+                 const uint64_t* addend, int addend_polys, int addend_period, int polys, int limbs,
+                 const int32_t* limb_prime, int n_drop1, int n_drop2,
+                 const uint64_t* prescale_host, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
+  if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 > kMaxDrop || n_drop2 > kMaxDrop ||
+      n_drop1 + n_drop2 >= limbs || polys < 0)
+    return CKB_E_ARG;
+  if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period))
+    return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  ScalarTab pre;
+  int has_pre = 0;
+  if (prescale_host) {
+    has_pre = 1;
+    for (int l = 0; l < limbs; ++l) {
+      pre.v[l] = prescale_host[2 * l];
+      pre.s[l] = prescale_host[2 * l + 1];
+    }
+  }
+  const size_t total = (size_t)polys << R.log_n;
+  if (!total) return 0;
+  const size_t stride = in_poly_stride > 0 ? (size_t)in_poly_stride : ((size_t)limbs << R.log_n);
+  k_divround<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, in, stride, addend, addend ? addend_polys : 0, addend ? addend_period : 1, polys, limbs, n_drop1, n_drop2,
+      (int)R.log_n, R, lm, pre, has_pre);
+  return finish();
+}
+
+int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,
+                     const int32_t* limb_prime, uint64_t galois, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0 || (galois & 1) == 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const uint64_t two_n = 2ull << R.log_n;
+  // inverse of an odd galois element modulo a power of two (Newton iteration)
+  uint64_t g = galois & (two_n - 1), inv = g;
+  for (int it = 0; it < 6; ++it) inv *= 2 - g * inv;
+  inv &= two_n - 1;
+  const size_t total = (size_t)rows << R.log_n;
+  if (!total) return 0;
+  k_automorphism<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, in, total, (int)R.log_n, limbs, inv, R, lm);
+  return finish();
+}
+
+int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int polys, int limbs,
+                 const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || polys < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = ((size_t)polys * limbs) << R.log_n;
+  if (!total) return 0;
+  k_from_i64<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, in, total, (int)R.log_n,
+                                                                      limbs, R, lm);
+  return finish();
+}
+
+int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys, int limbs,
+               const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || polys < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)polys << R.log_n;
+  if (!total) return 0;
+  k_to_f64<<<grid_for(total, 128), 128, 0, (cudaStream_t)stream>>>(out, in, polys, limbs,
+                                                                    (int)R.log_n, R, lm);
+  return finish();
+}
+
+}  // extern "C"

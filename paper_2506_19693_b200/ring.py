@@ -1,0 +1,225 @@
+"""Device-resident RNS chain and thin wrappers over the sm_100a kernels.
+
+``GpuChain`` plays the role of the reference's ``ChainContext``
+(ckks/ring.py:21-59): the prime chain ordered [base | rescale entries | special],
+level -> limb-prefix map, the scale schedule, plus the device tables the
+kernels read (twiddles, Barrett/Shoup constants, pairwise inverses).
+
+Polynomials are torch.uint64 CUDA tensors ``[..., limbs, N]`` (contiguous,
+canonical residues); the prime of limb i at level l is ``all_primes[i]`` for
+the ciphertext prefix and ``all_primes[LQ + t]`` for special prime t, so the
+kernels' per-limb prime index is simply the position in ``all_primes``.
+Every wrapper launches on the caller's current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .primes import build_chain
+
+U64 = torch.uint64
+
+
+def shoup(v: int, p: int) -> int:
+    return (v << 64) // p
+
+
+class GpuChain:
+    def __init__(self, params, layout: str = "reference", device=None):
+        self.params = params
+        self.layout = layout
+        self.n = params.poly_degree
+        self.log_n = self.n.bit_length() - 1
+        self.device = torch.device(device or "cuda")
+        entries, scale_at = build_chain(params, layout)
+        self.entry_primes = entries
+        self.special_primes = list(entries[-1])
+        self.primes = [p for e in entries[:-1] for p in e]
+        self.all_primes = self.primes + self.special_primes
+        self.lq = len(self.primes)
+        self.k = len(self.special_primes)
+        self.level_limbs = [len(entries[0])]
+        for e in entries[1:-1]:
+            self.level_limbs.append(self.level_limbs[-1] + len(e))
+        self.entry_products = [math.prod(e) for e in entries]
+        self.special_product = math.prod(self.special_primes)
+        self.scale_at = scale_at
+        mods, ntt, pair = nat.build_tables(self.log_n, self.all_primes)
+        dev = self.device
+        self._mods = torch.from_numpy(mods).to(dev)
+        self._ntt = torch.from_numpy(ntt.reshape(-1)).to(dev)
+        self._pair = torch.from_numpy(pair.reshape(-1)).to(dev)
+        self.ring = nat.CkbRing(self.log_n, len(self.all_primes), self._mods.data_ptr(),
+                                self._ntt.data_ptr(), self._pair.data_ptr())
+        self.ring_p = nat.ctypes.pointer(self.ring)
+        self._maps: dict = {}
+
+    # -- bases ------------------------------------------------------------------
+    def limbs_at(self, level: int) -> list:
+        return self.primes[: self.level_limbs[level]]
+
+    def modulus_at(self, level: int) -> int:
+        return math.prod(self.limbs_at(level))
+
+    def q_map(self, m: int):
+        """ctypes int32 map for the first m ciphertext limbs."""
+        key = ("q", m)
+        if key not in self._maps:
+            self._maps[key] = nat.i32_array(range(m))
+        return self._maps[key]
+
+    def ext_map(self, m: int):
+        """Ciphertext limbs [0, m) followed by the special primes (keys.py:81)."""
+        key = ("e", m)
+        if key not in self._maps:
+            self._maps[key] = nat.i32_array(list(range(m)) + list(range(self.lq, self.lq + self.k)))
+        return self._maps[key]
+
+    def all_map(self):
+        key = ("all",)
+        if key not in self._maps:
+            self._maps[key] = nat.i32_array(range(len(self.all_primes)))
+        return self._maps[key]
+
+    def custom_map(self, idx: tuple):
+        key = ("c",) + tuple(idx)
+        if key not in self._maps:
+            self._maps[key] = nat.i32_array(idx)
+        return self._maps[key]
+
+    def scalar_pairs(self, value: int, primes_idx) -> object:
+        """{v mod p, shoup} pairs for ckb_scalar_mul / ckb_divround prescale."""
+        vals = []
+        for i in primes_idx:
+            p = self.all_primes[i]
+            v = value % p
+            vals += [v, shoup(v, p)]
+        return nat.u64_array(vals)
+
+    # -- allocation ---------------------------------------------------------------
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, self.n, dtype=U64, device=self.device)
+
+    # -- kernels -------------------------------------------------------------------
+    def ntt_fwd(self, t: torch.Tensor, limbs: int, lmap=None):
+        rows = t.numel() >> self.log_n
+        nat.check(nat.LIB.ckb_ntt_forward(self.ring_p, nat.ptr(t), rows, limbs,
+                                          lmap or self.q_map(limbs), nat.stream_handle()),
+                  "ntt_forward")
+        return t
+
+    def ntt_inv(self, t: torch.Tensor, limbs: int, lmap=None):
+        rows = t.numel() >> self.log_n
+        nat.check(nat.LIB.ckb_ntt_inverse(self.ring_p, nat.ptr(t), rows, limbs,
+                                          lmap or self.q_map(limbs), nat.stream_handle()),
+                  "ntt_inverse")
+        return t
+
+    def ew(self, op: int, out, a, b=None, c=None, limbs: int = 0, lmap=None, b_rows: int = 0):
+        rows = a.numel() >> self.log_n
+        nat.check(nat.LIB.ckb_elementwise(
+            self.ring_p, op, nat.ptr(out), nat.ptr(a), nat.ptr(b) if b is not None else None,
+            nat.ptr(c) if c is not None else None, rows, limbs, lmap or self.q_map(limbs), b_rows,
+            nat.stream_handle()), "elementwise")
+        return out
+
+    def add(self, a, b, limbs, out=None, lmap=None):
+        return self.ew(0, out if out is not None else torch.empty_like(a), a, b, limbs=limbs, lmap=lmap)
+
+    def sub(self, a, b, limbs, out=None, lmap=None):
+        return self.ew(1, out if out is not None else torch.empty_like(a), a, b, limbs=limbs, lmap=lmap)
+
+    def mul(self, a, b, limbs, out=None, lmap=None, b_rows=0):
+        return self.ew(2, out if out is not None else torch.empty_like(a), a, b, limbs=limbs,
+                       lmap=lmap, b_rows=b_rows)
+
+    def neg(self, a, limbs, out=None, lmap=None):
+        return self.ew(3, out if out is not None else torch.empty_like(a), a, limbs=limbs, lmap=lmap)
+
+    def scalar_mul(self, a, pairs, limbs, out=None, lmap=None):
+        out = out if out is not None else torch.empty_like(a)
+        rows = a.numel() >> self.log_n
+        nat.check(nat.LIB.ckb_scalar_mul(self.ring_p, nat.ptr(out), nat.ptr(a), rows, limbs,
+                                         lmap or self.q_map(limbs), pairs, nat.stream_handle()),
+                  "scalar_mul")
+        return out
+
+    def tensor(self, a, b, limbs, out=None):
+        batch = a.numel() // (2 * limbs * self.n)
+        out = out if out is not None else torch.empty(batch, 3, limbs, self.n, dtype=U64,
+                                                      device=self.device)
+        nat.check(nat.LIB.ckb_tensor(self.ring_p, nat.ptr(out), nat.ptr(a), nat.ptr(b), batch, limbs,
+                                     self.q_map(limbs), nat.stream_handle()), "tensor")
+        return out
+
+    def modup(self, d, m: int, alpha: int, bconv, out=None):
+        batch = d.numel() // (m * self.n)
+        ext = m + self.k
+        nd = -(-m // alpha)
+        out = out if out is not None else torch.empty(batch, nd, ext, self.n, dtype=U64,
+                                                      device=self.device)
+        nat.check(nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), batch, m, self.q_map(m),
+                                    ext, self.ext_map(m), alpha,
+                                    nat.ptr(bconv) if bconv is not None else None,
+                                    nat.stream_handle()), "modup")
+        return out
+
+    def ks_inner(self, digits, m: int, key: torch.Tensor = None, key_ptrs: torch.Tensor = None,
+                 out=None):
+        batch, nd, ext = digits.shape[0], digits.shape[1], digits.shape[2]
+        out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
+                                                      device=self.device)
+        key_limbs = len(self.all_primes)
+        nat.check(nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
+                                       self.ext_map(m),
+                                       nat.ptr(key) if key is not None else None,
+                                       nat.ptr(key_ptrs) if key_ptrs is not None else None,
+                                       key_limbs, self.ext_map(m), nat.stream_handle()),
+                  "ks_inner")
+        return out
+
+    def divround(self, x, polys: int, limbs: int, n1: int, n2: int = 0, addend=None,
+                 addend_polys: int = 0, addend_period: int = 1, prescale=None,
+                 in_poly_stride: int = 0, lmap=None, out=None):
+        m2 = limbs - n1 - n2
+        out = out if out is not None else torch.empty(polys, m2, self.n, dtype=U64,
+                                                      device=self.device)
+        nat.check(nat.LIB.ckb_divround(self.ring_p, nat.ptr(out), nat.ptr(x), in_poly_stride,
+                                       nat.ptr(addend) if addend is not None else None,
+                                       addend_polys if addend is not None else 0,
+                                       addend_period, polys, limbs,
+                                       lmap or self.q_map(limbs), n1, n2, prescale,
+                                       nat.stream_handle()), "divround")
+        return out
+
+    def automorphism(self, x, galois: int, limbs: int, out=None, lmap=None):
+        out = out if out is not None else torch.empty_like(x)
+        rows = x.numel() >> self.log_n
+        nat.check(nat.LIB.ckb_automorphism(self.ring_p, nat.ptr(out), nat.ptr(x), rows, limbs,
+                                           lmap or self.q_map(limbs), galois, nat.stream_handle()),
+                  "automorphism")
+        return out
+
+    def from_i64(self, coeffs: torch.Tensor, limbs: int, lmap=None, out=None):
+        polys = coeffs.numel() >> self.log_n
+        out = out if out is not None else torch.empty(polys, limbs, self.n, dtype=U64,
+                                                      device=self.device)
+        nat.check(nat.LIB.ckb_from_i64(self.ring_p, nat.ptr(out), nat.ptr(coeffs), polys, limbs,
+                                       lmap or self.q_map(limbs), nat.stream_handle()), "from_i64")
+        return out
+
+    def to_f64(self, x: torch.Tensor, limbs: int, lmap=None):
+        polys = x.numel() // (limbs * self.n)
+        out = torch.empty(polys, self.n, dtype=torch.float64, device=self.device)
+        nat.check(nat.LIB.ckb_to_f64(self.ring_p, nat.ptr(out), nat.ptr(x), polys, limbs,
+                                     lmap or self.q_map(limbs), nat.stream_handle()), "to_f64")
+        return out
+
+    # -- host <-> device helpers -------------------------------------------------------
+    def upload_u64(self, arr: np.ndarray) -> torch.Tensor:
+        return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint64)).to(self.device)

@@ -1,0 +1,373 @@
+"""GPU parity: the sm_100a kernels through the C-ABI and the HE API against the
+reference's golden vectors (tests/golden, made by the real reference) and the
+CPU oracle (oracle/ckks_oracle.py, itself pinned to those vectors).
+
+Integer work must be bit-exact; float encode/decode within 1e-6 per slot
+(BASELINE north_star) and the reference's own decrypt tolerances.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import ckks_oracle as O  # noqa: E402
+from paper_2506_19693_b200 import he_api, he_errors  # noqa: E402
+from paper_2506_19693_b200.backend import B200Backend  # noqa: E402
+from paper_2506_19693_b200.ring import GpuChain  # noqa: E402
+from paper_2506_19693_b200.scheme import SchemeParams, make_params  # noqa: E402
+
+
+def _u64(t):
+    return t.cpu().numpy().astype(np.uint64)
+
+
+# ---------------------------------------------------------------------------
+# NTT (K1) vs reference NttPlan vectors and the oracle
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def ntt_gold(golden_dir):
+    return np.load(os.path.join(golden_dir, "ref_ntt.npz"))
+
+
+def _single_prime_chain(n, p):
+    """A GpuChain whose only ciphertext prime is p (tables for NTT tests)."""
+
+    class P:
+        poly_degree = n
+        modulus_chain = (30, 30, 30)
+        scale_bits = 30
+        level = 1
+
+    ch = GpuChain.__new__(GpuChain)
+    from paper_2506_19693_b200 import _native as nat
+
+    ch.params = P
+    ch.layout = "custom"
+    ch.n = n
+    ch.log_n = n.bit_length() - 1
+    ch.device = torch.device("cuda")
+    ch.all_primes = [int(p)]
+    ch.primes = [int(p)]
+    ch.special_primes = []
+    ch.lq, ch.k = 1, 0
+    mods, ntt, pair = nat.build_tables(ch.log_n, ch.all_primes)
+    ch._mods = torch.from_numpy(mods).cuda()
+    ch._ntt = torch.from_numpy(ntt.reshape(-1)).cuda()
+    ch._pair = torch.from_numpy(pair.reshape(-1)).cuda()
+    ch.ring = nat.CkbRing(ch.log_n, 1, ch._mods.data_ptr(), ch._ntt.data_ptr(), ch._pair.data_ptr())
+    ch.ring_p = nat.ctypes.pointer(ch.ring)
+    ch._maps = {}
+    return ch
+
+
+@pytest.mark.parametrize("n", [16, 64, 1024, 4096, 8192])
+def test_ntt_matches_reference_vectors(ntt_gold, n):
+    p = int(ntt_gold[f"n{n}_p"][0])
+    ch = _single_prime_chain(n, p)
+    a = torch.from_numpy(ntt_gold[f"n{n}_in"].astype(np.uint64)).cuda()
+    f = ch.ntt_fwd(a.clone(), 1)
+    assert np.array_equal(_u64(f), ntt_gold[f"n{n}_fwd"])
+    i = ch.ntt_inv(a.clone(), 1)
+    assert np.array_equal(_u64(i), ntt_gold[f"n{n}_inv"])
+
+
+@pytest.mark.parametrize("logn", [5, 10, 12, 13, 14, 15, 16, 17])
+@pytest.mark.parametrize("bits", [30, 40, 60])
+def test_ntt_big_primes_vs_oracle_and_roundtrip(logn, bits):
+    n = 1 << logn
+    p = O.largest_ntt_prime_below(bits, 2 * n, set())
+    ch = _single_prime_chain(n, p)
+    rng = np.random.default_rng(logn * 100 + bits)
+    rows = 3
+    a_np = rng.integers(0, p, (rows, n), dtype=np.uint64)
+    a = torch.from_numpy(a_np).cuda()
+    f = ch.ntt_fwd(a.clone(), 1)
+    if n <= 4096:  # oracle (object arithmetic) is slow beyond this
+        plan = O.NttPlan(p, n)
+        want = np.array([int(v) for v in plan.forward(a_np[0])], dtype=np.uint64)
+        assert np.array_equal(_u64(f)[0], want)
+    back = ch.ntt_inv(f.clone(), 1)
+    assert np.array_equal(_u64(back), a_np)
+    assert int(_u64(f).max()) < p
+
+
+def test_ntt_product_matches_schoolbook_60bit():
+    n = 32
+    p = O.largest_ntt_prime_below(60, 2 * n, set())
+    ch = _single_prime_chain(n, p)
+    rng = np.random.default_rng(3)
+    a_np = rng.integers(0, p, n, dtype=np.uint64)
+    b_np = rng.integers(0, p, n, dtype=np.uint64)
+    fa = ch.ntt_fwd(torch.from_numpy(a_np).cuda(), 1)
+    fb = ch.ntt_fwd(torch.from_numpy(b_np).cuda(), 1)
+    prod = ch.ntt_inv(ch.mul(fa, fb, 1), 1)
+    want = O.schoolbook_negacyclic([int(v) for v in a_np], [int(v) for v in b_np], p)
+    assert [int(v) for v in _u64(prod)] == want
+
+
+# ---------------------------------------------------------------------------
+# Mode A: the backend against the reference's ciphertext planes
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def ck_gold(golden_dir):
+    return np.load(os.path.join(golden_dir, "ref_ckks_n512.npz"))
+
+
+@pytest.fixture(scope="module")
+def mode_a(ck_gold):
+    n, level, sb = (int(v) for v in ck_gold["params"])
+    params = SchemeParams(poly_degree=n, modulus_chain=tuple(int(v) for v in ck_gold["chain"]),
+                          scale_bits=sb, level=level)
+    rots = [int(v) for v in ck_gold["rots"]]
+    cust = he_api.keygen(params, rots, backend="ckks", rng_seed=int(ck_gold["rng_seed"][0]))
+    return cust
+
+
+def _wrap(cust, planes, level):
+    be = cust.backend
+    return be._wrap(be.payload_from_planes(planes, level), level, 0)
+
+
+def _key_digest(key):
+    h = hashlib.sha256()
+    d = key.data.cpu().numpy()
+    for j in range(d.shape[0]):
+        h.update(np.ascontiguousarray(d[j, 0].astype("<u8")).tobytes())
+        h.update(np.ascontiguousarray(d[j, 1].astype("<u8")).tobytes())
+    return h.hexdigest()
+
+
+def test_mode_a_chain_secret_and_keys_bit_exact(ck_gold, mode_a):
+    be = mode_a.backend
+    assert be.chain.all_primes == [int(v) for v in ck_gold["all_primes"]]
+    assert be.chain.level_limbs == [int(v) for v in ck_gold["level_limbs"]]
+    assert np.array_equal(be.sk.coeffs, ck_gold["secret"].astype(np.int64))
+    digests = json.loads(str(ck_gold["key_digests"]))
+    assert _key_digest(be.relin_key) == digests["relin"]
+    for g, key in be.rotation_keys.items():
+        assert _key_digest(key) == digests[f"rot_{g}"]
+
+
+def test_mode_a_ciphertext_ops_bit_exact(ck_gold, mode_a):
+    cust = mode_a
+    ev = cust.evaluator
+    lvl = int(ck_gold["params"][1])
+    ct1 = _wrap(cust, ck_gold["ct1"], lvl)
+    ct2 = _wrap(cust, ck_gold["ct2"], lvl)
+    mul = ev.mul(ct1, ct2)
+    deep = ev.mul(mul, ct2)
+    got = {
+        "add": ev.add(ct1, ct2), "sub": ev.sub(ct1, ct2), "mul": mul,
+        "rot1": ev.rotate(ct1, 1), "rot3": ev.rotate(ct1, 3), "rotm1": ev.rotate(ct1, -1),
+        "deep": deep, "mixed": ev.add(deep, ct1), "sq": ev.mul(mul, mul),
+    }
+    for name, cv in got.items():
+        assert cv.level_remaining == int(ck_gold[f"lvl_{name}"][0]), name
+        assert np.array_equal(cust.backend.planes_of(cv.payload), ck_gold[f"out_{name}"]), name
+        dec = cust.decrypt(cv).values
+        assert np.max(np.abs(dec - ck_gold[f"dec_{name}"])) <= 1e-6, name
+
+
+def test_mode_a_plaintext_ops_bit_exact_given_encoding(ck_gold, mode_a):
+    """mul_pt/add_pt/sub_pt: the device encoding (cuFFT) may differ from numpy's
+    by +-1 in a coefficient; the integer path is checked bit-exactly against the
+    oracle fed the device's own encoding, and the encoding within +-1."""
+    cust = mode_a
+    be = cust.backend
+    ev = cust.evaluator
+    lvl = int(ck_gold["params"][1])
+    n = be.n
+    orc = O.OracleCkks(n, tuple(int(v) for v in ck_gold["chain"]), 40, lvl,
+                       rotation_steps=[], rng_seed=int(ck_gold["rng_seed"][0]))
+    ct1 = _wrap(cust, ck_gold["ct1"], lvl)
+    o_ct1 = O.ct_from_u64(ck_gold["ct1"], lvl, orc.chain)
+    v3 = ck_gold["v3"]
+    pv = he_api.make_plain(v3, n // 2, 40.0)
+    dev_c = be.encoder.embed(v3, be.chain.scale_at[lvl])
+    assert np.max(np.abs(dev_c - ck_gold["pt3_coeffs"])) <= 1
+    dev_cn = be.encoder.embed(-v3, be.chain.scale_at[lvl])
+    m3 = O.make_element(orc.chain.limbs_at(lvl), dev_c)
+    m3n = O.make_element(orc.chain.limbs_at(lvl), dev_cn)
+    cases = {
+        "mul_pt": (ev.mul(ct1, pv), orc.mul_plain_coeffs(o_ct1, m3)),
+        "add_pt": (ev.add(ct1, pv), orc.add_plain_coeffs(o_ct1, m3)),
+        "sub_pt": (ev.sub(ct1, pv), orc.add_plain_coeffs(o_ct1, m3n)),
+    }
+    for name, (cv, oct_) in cases.items():
+        assert np.array_equal(be.planes_of(cv.payload), O.ct_to_u64(oct_, orc.chain)), name
+        dec = cust.decrypt(cv).values
+        assert np.max(np.abs(dec - ck_gold[f"dec_{name}"])) <= 2.0**-25, name
+
+
+def test_mode_a_encrypt_bit_exact_given_encoding(ck_gold, mode_a):
+    be = mode_a.backend
+    lvl = int(ck_gold["params"][1])
+    orc = O.OracleCkks(be.n, tuple(int(v) for v in ck_gold["chain"]), 40, lvl,
+                       rng_seed=int(ck_gold["rng_seed"][0]))
+    # a fresh backend so the serial counter starts where the fixture's did
+    cust = he_api.keygen(be.params, [], backend="ckks", rng_seed=int(ck_gold["rng_seed"][0]))
+    v1 = ck_gold["v1"]
+    cv = cust.encrypt(he_api.make_plain(v1, be.n // 2, 40.0))
+    coeffs = cust.backend.encoder.embed(v1, be.chain.scale_at[lvl])
+    m = O.make_element(orc.chain.limbs_at(lvl), coeffs)
+    want = orc.encrypt_coeffs(m, lvl, int(ck_gold["ct1_serial"][0]) + 1)
+    assert np.array_equal(cust.backend.planes_of(cv.payload), O.ct_to_u64(want, orc.chain))
+    assert np.max(np.abs(cust.decrypt(cv).values - ck_gold["dec_ct1"])) <= 1e-6
+
+
+def test_rbct_roundtrip_and_errors(ck_gold, mode_a):
+    be = mode_a.backend
+    lvl = int(ck_gold["params"][1])
+    cv = _wrap(mode_a, ck_gold["ct1"], lvl)
+    blob = be.serialize_cipher(cv)
+    assert blob[:4] == b"RBCT"
+    back = be.deserialize_cipher(blob)
+    assert np.array_equal(be.planes_of(back.payload), ck_gold["ct1"])
+    with pytest.raises(he_errors.SerializationError):
+        be.deserialize_cipher(b"XXXX" + blob[4:])
+    with pytest.raises(he_errors.SerializationError):
+        be.deserialize_cipher(blob[:-8])
+
+
+# ---------------------------------------------------------------------------
+# Mode B: BASELINE-style single 40/60-bit primes, hybrid key switching
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dnum", [None, 2])
+def test_mode_b_ops_bit_exact_vs_oracle(dnum):
+    n, level = 256, 3
+    chain = (60, 40, 40, 40, 120 if dnum else 60)
+    params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=40, level=level)
+    cust = he_api.keygen(params, {1, 5}, backend="ckks", rng_seed=7, prime_layout="baseline",
+                         dnum=dnum)
+    be = cust.backend
+    alpha = be.alpha
+    orc = O.OracleCkks(n, chain, 40, level, rotation_steps=[1, 5], rng_seed=7, layout="baseline",
+                       alpha=alpha)
+    assert be.chain.all_primes == orc.chain.all_primes
+    assert be.relin_key.data.shape[0] == len(orc.relin.rows_b)
+    rng = np.random.default_rng(1)
+    planes = []
+    for _ in range(2):
+        c = np.stack([np.stack([rng.integers(0, p, n, dtype=np.uint64)
+                                for p in orc.chain.limbs_at(level)]) for _ in range(2)])
+        planes.append(c)
+    ev = cust.evaluator
+    a, b = (_wrap(cust, p, level) for p in planes)
+    oa, ob = (O.ct_from_u64(p, level, orc.chain) for p in planes)
+    o_mul = orc.mul(oa, ob)
+    checks = [
+        (ev.mul(a, b), o_mul),
+        (ev.rotate(a, 1), orc.rotate(oa, 1)),
+        (ev.rotate(b, 5), orc.rotate(ob, 5)),
+        (ev.add(ev.mul(a, b), a), orc.add(o_mul, oa)),
+        (ev.mul(ev.mul(a, b), b), orc.mul(o_mul, ob)),
+    ]
+    for cv, oct_ in checks:
+        assert np.array_equal(be.planes_of(cv.payload), O.ct_to_u64(oct_, orc.chain))
+
+
+# ---------------------------------------------------------------------------
+# Decryption tolerances (tests/test_ckks_backend.py of the reference)
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def ckks_small():
+    params = make_params(level=10, scale_bits=40, poly_degree=2**12)
+    return params, he_api.keygen(params, {1, 2, 3, -1}, backend="ckks", rng_seed=0)
+
+
+def _pl(cust, v):
+    return he_api.make_plain(v, cust.params.slot_count, float(cust.params.scale_bits))
+
+
+def test_encode_roundtrip_and_overflow(ckks_small):
+    params, cust = ckks_small
+    be = cust.backend
+    v = np.random.default_rng(9).uniform(-1, 1, params.slot_count)
+    c = be.encoder.embed(v, 2.0**40)
+    assert np.max(np.abs(be.encoder.unembed(c.astype(np.float64), 2.0**40) - v)) <= 2.0**-30
+    ref = O.Encoder(params.poly_degree).embed(v, 2.0**40)
+    assert np.max(np.abs(c - ref)) <= 1
+    assert np.max(np.abs(be.encoder.unembed(c.astype(np.float64), 2.0**40)
+                         - O.Encoder(params.poly_degree).unembed(c, 2.0**40))) <= 1e-6
+    with pytest.raises(he_errors.EncodingOverflow):
+        cust.encrypt(_pl(cust, np.full(params.slot_count, 2.0**25)))
+
+
+def test_homomorphic_ops_within_tolerance(ckks_small):
+    params, cust = ckks_small
+    ev = cust.evaluator
+    rng = np.random.default_rng(23)
+    for _ in range(5):
+        a = rng.uniform(-1, 1, params.slot_count)
+        b = rng.uniform(-1, 1, params.slot_count)
+        ca, cb = cust.encrypt(_pl(cust, a)), cust.encrypt(_pl(cust, b))
+        assert np.max(np.abs(cust.decrypt(ca).values - a)) <= 2.0**-30
+        for got, want in [(ev.add(ca, cb), a + b), (ev.sub(ca, cb), a - b), (ev.mul(ca, cb), a * b),
+                          (ev.mul(ca, _pl(cust, b)), a * b), (ev.add(ca, _pl(cust, b)), a + b),
+                          (ev.rotate(ca, 1), np.roll(a, -1)), (ev.rotate(ca, -1), np.roll(a, 1))]:
+            assert np.max(np.abs(cust.decrypt(got).values - want)) <= 2.0**-25
+
+
+def test_multiply_chain_level_exhaustion_and_bootstrap(ckks_small):
+    params, cust = ckks_small
+    ev = cust.evaluator
+    x = cust.encrypt(_pl(cust, np.full(params.slot_count, 0.9)))
+    ones = cust.encrypt(_pl(cust, np.ones(params.slot_count)))
+    for _ in range(10):
+        x = ev.mul(x, ones)
+    assert x.level_remaining == 0
+    with pytest.raises(he_errors.LevelExhausted):
+        ev.mul(x, ones)
+    before = cust.decrypt(x).values
+    assert np.max(np.abs(before - 0.9)) <= 2.0**-20
+    r = cust.bootstrap(x)
+    assert r.level_remaining == params.refresh_level
+    assert np.max(np.abs(cust.decrypt(r).values - before)) <= 2.0**-28
+
+
+def test_missing_rotation_key(ckks_small):
+    params, cust = ckks_small
+    ct = cust.encrypt(_pl(cust, np.zeros(params.slot_count)))
+    with pytest.raises(he_errors.MissingRotationKey):
+        cust.evaluator.rotate(ct, 5)
+
+
+# ---------------------------------------------------------------------------
+# Config-2 sizes: N=2^16, 40-bit limbs, dnum=3 (size-independent properties)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("L", [4, 12])
+def test_c2_hybrid_keyswitch_decrypts(L):
+    k = {4: 2, 12: 3, 24: 6}[L]
+    params = make_params(level=L - 1, scale_bits=40, poly_degree=2**16, first_bits=40,
+                         special_bits=60 * k)
+    cust = he_api.keygen(params, {1, 7}, backend="ckks", rng_seed=2, prime_layout="baseline",
+                         dnum=3, secret_hw=192)
+    be = cust.backend
+    assert be.chain.k == k and be.alpha == -(-L // 3)
+    ev = cust.evaluator
+    rng = np.random.default_rng(4)
+    a = rng.uniform(-1, 1, params.slot_count)
+    b = rng.uniform(-1, 1, params.slot_count)
+    ca, cb = cust.encrypt(_pl(cust, a)), cust.encrypt(_pl(cust, b))
+    assert np.max(np.abs(cust.decrypt(ev.mul(ca, cb)).values - a * b)) <= 2.0**-20
+    assert np.max(np.abs(cust.decrypt(ev.rotate(ca, 7)).values - np.roll(a, -7))) <= 2.0**-20
