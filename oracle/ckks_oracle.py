@@ -537,15 +537,17 @@ def make_keyswitch_key(chain: Chain, s_full: Elem, source_ntt: Elem, rng, alpha:
     return KSKey(rows_b, rows_a)
 
 
-def modup_digit(d: Elem, lo: int, hi: int, ext) -> Elem:
+def modup_digit(d: Elem, lo: int, hi: int, ext, centered: bool = True) -> Elem:
     """Digit [lo, hi) of d (coefficient domain) lifted into the ext basis.
 
-    alpha == 1: the reference's centered digit (keys.py:85-89).
-    alpha > 1: fast basis conversion y_i = [x_i * qhat_i^-1]_{q_i},
-               out_p = sum_i y_i * [qhat_i]_p  (x's own limbs copied).
+    centered (alpha == 1): the reference's centered digit (keys.py:85-89).
+    otherwise (alpha > 1, including a short last digit): fast basis conversion
+               y_i = [x_i * qhat_i^-1]_{q_i}, out_p = sum_i y_i * [qhat_i]_p
+               (the digit's own limbs are copied).
     """
     n = len(d.planes[0])
-    if hi - lo == 1:
+    if centered:
+        assert hi - lo == 1
         q = d.primes[lo]
         digit = [int(v) for v in d.planes[lo].tolist()]
         digit = [v - q if v > q // 2 else v for v in digit]
@@ -584,7 +586,7 @@ def key_switch(chain: Chain, d: Elem, key: KSKey, alpha: int = 1):
     ext = tuple(current + chain.special_primes)
     acc_b = acc_a = None
     for j, (lo, hi) in enumerate(digit_ranges(len(current), alpha)):
-        dig = e_ntt(modup_digit(d, lo, hi, ext), chain)
+        dig = e_ntt(modup_digit(d, lo, hi, ext, centered=(alpha == 1)), chain)
         kb = e_restrict(key.rows_b[j], ext)
         ka = e_restrict(key.rows_a[j], ext)
         tb, ta = e_mul(dig, kb, chain), e_mul(dig, ka, chain)

@@ -347,9 +347,9 @@ __global__ void k_to_f64(double* __restrict__ out, const uint64_t* __restrict__ 
       }
       v[i] = x;
     }
-    // fraction x / Q by Horner from the top digit
+    // fraction x / Q = sum_i v_i / (q_i * ... * q_{limbs-1}), Horner from digit 0
     double f = 0.0;
-    for (int i = limbs - 1; i >= 0; --i) {
+    for (int i = 0; i < limbs; ++i) {
       const double q = (double)__ldg(R.mods + (size_t)lm.p[i] * 8);
       f = ((double)v[i] + f) / q;
     }
