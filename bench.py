@@ -1,0 +1,430 @@
+"""Benchmark: BASELINE.json config 2 (HE primitive sweep) on the B200 backend.
+
+Workload (one "step"): a batch of 64 ciphertexts at N=2^16, L=24 40-bit limbs,
+hybrid key switching dnum=3 with k=6 60-bit special primes:
+  * NTT + iNTT of every limb of the batch,
+  * ct x ct multiply + relinearise + rescale of 64 pairs (HMult),
+  * rotation of 64 ciphertexts by 64 seeded steps in [1, 2^15), 64 keys (HRot).
+Inputs are uniformly random limbs (seeded), resident in HBM (1.5 GiB per
+operand batch, larger than the 126 MB L2, so no flush is needed).
+
+metric  = BASELINE's "encrypted train ms/step; bootstrap ms; keyswitch GB/s vs
+          HBM peak"; value = key-switching throughput: algorithmic bytes of the
+          HMult + HRot batches (BASELINE.md §3 formulas, each distinct key once
+          per batch) / their device time, in GB/s.
+Extra keys: per-stage times, NTT GB/s, the roofline of the dominant kernel,
+the config-1 encrypted training step (ms/step, replayed reference
+train_iteration; decrypted weights vs the reference), e2e through host
+buffers, the CPU oracle baseline, clocks.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_LOG = 16
+BATCH = 64
+L_LIMBS = 24
+DNUM = 3
+W = 8
+
+
+def c2_params(L):
+    from paper_2506_19693_b200.scheme import make_params
+
+    k = -(-40 * (-(-L // DNUM)) // 60)
+    return make_params(level=L - 1, scale_bits=40, poly_degree=1 << N_LOG, first_bits=40,
+                       special_bits=60 * k), k
+
+
+def alg_bytes(L, k, batch, n_rot_keys):
+    """BASELINE.md §3 (W=8): HMult (4l + 2b(l+k) + 2(l-1)) N W, HRot (4l + 2b(l+k)) N W,
+    keys counted once per distinct key per batch."""
+    n = 1 << N_LOG
+    beta = DNUM
+    key = 2 * beta * (L + k) * n * W
+    hmult = batch * (4 * L + 2 * (L - 1)) * n * W + key
+    hrot = batch * 4 * L * n * W + n_rot_keys * key
+    ntt = 2 * (2 * batch * 2 * L * n * W)  # fwd + inv over both components
+    return hmult, hrot, ntt
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle port of the reference algorithm, reference prime layout)
+# ---------------------------------------------------------------------------
+
+
+def _cpu_case(L):
+    from oracle import parallel_ref as PR
+
+    return PR.make_random_case(1 << N_LOG, L, seed=5)
+
+
+def _cpu_hmult(case, procs):
+    """One HMult (mul + relinearise + rescale) of one ciphertext with the
+    reference's algorithm and prime layout (per-limb digits, sub-2^31 primes;
+    oracle/ckks_oracle.py), key switch split over `procs` host processes
+    (oracle/parallel_ref.py).  Returns seconds."""
+    from oracle import parallel_ref as PR
+
+    chain, (a, b), kb, ka = case
+    _, secs = PR.hmult_parallel(chain, a, b, kb, ka, procs)
+    return secs
+
+
+def _cpu_sample_text(L, procs):
+    return (f"one HMult of one ciphertext (N=2^16, {L} x 40-bit entries in the reference's "
+            f"sub-2^31 prime layout = {2 * L}+2 limbs, per-limb digits), numpy oracle port of "
+            f"ckks/backend.py:136-143, key switch split over {procs} processes; bytes = "
+            f"BASELINE HMult formula at the B200 arm's parameters")
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port, numpy) on all
+    host cores; one step = one HMult of one ciphertext."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import parallel_ref as PR
+
+    L = args.limbs
+    _, k = c2_params(L)
+    hm, _, _ = alg_bytes(L, k, 1, 0)
+    procs = args.ref_procs or PR.default_procs()
+    case = _cpu_case(L)
+    times = []
+    for step in range(args.warmup + args.steps):
+        dt = _cpu_hmult(case, procs)
+        if step >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = hm / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": f"c2 HMult at N=2^16, L={L}: reference algorithm and prime layout "
+                               f"on the host CPU", "batch_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": _cpu_sample_text(L, procs)},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "encrypted train ms/step; bootstrap ms; keyswitch GB/s vs HBM peak"
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+
+def run_c1_train(device_index):
+    """Config 1: the reference train_iteration's HE call sequence replayed on the
+    B200 backend (BASELINE primes 1x60 + 8x40 + 1x60, HW-64 secret)."""
+    import torch
+
+    from paper_2506_19693_b200 import he_api
+    from paper_2506_19693_b200.replay import Program
+    from paper_2506_19693_b200.scheme import make_params
+
+    path = os.path.join(ROOT, "tests", "golden", "c1_trace.npz")
+    z = np.load(path)
+    prog = Program.load(path)
+    n, level, sb = (int(v) for v in z["params"])
+    params = make_params(level=level, scale_bits=sb, poly_degree=n)
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=3,
+                         prime_layout="baseline", secret_hw=64)
+    torch.cuda.synchronize()
+    keygen_s = time.perf_counter() - t0
+    env = prog.run(cust, 0, prog.n_setup)
+    times = []
+    for rep in range(3):
+        e = dict(env)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e = prog.run(cust, prog.n_setup, None, e)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    w = np.stack([cust.decrypt(e[o]).values for o in prog.outputs])
+    err_sim = float(np.max(np.abs(w - z["sim_weights"])))
+    err_ref = float(np.max(np.abs(w - z["ckks_weights"]))) if "ckks_weights" in z else None
+    ref_s = float(z["ckks_seconds"][1]) if "ckks_seconds" in z else None
+    return {"ms_per_step": 1e3 * min(times), "ops": len(prog.ops) - prog.n_setup,
+            "keygen_s": keygen_s, "weights_max_abs_err_vs_sim": err_sim,
+            "weights_max_abs_err_vs_reference_ckks": err_ref,
+            "reference_cpu_s_per_step_build_container": ref_s}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--limbs", type=int, default=L_LIMBS)
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c1", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-procs", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_19693_b200 import he_api, ring
+    from paper_2506_19693_b200.ring import KernelTimer
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    L, bsz = args.limbs, args.batch
+    params, k = c2_params(L)
+    rng = np.random.default_rng(1234 + rank)
+    steps_rot = [int(s) for s in rng.integers(1, 1 << 15, bsz)]
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, set(steps_rot), backend="ckks", rng_seed=99 + rank,
+                         prime_layout="baseline", dnum=DNUM, secret_hw=192)
+    be = cust.backend
+    torch.cuda.synchronize()
+    keygen_s = time.perf_counter() - t0
+    lvl = params.level
+    m = be.chain.level_limbs[lvl]
+    n = 1 << N_LOG
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + rank)
+
+    def rand_batch():
+        t = torch.empty(bsz, 2, m, n, dtype=torch.int64, device="cuda")
+        for i, p in enumerate(be.chain.limbs_at(lvl)):
+            t[:, :, i].random_(0, p, generator=gen)
+        return t.view(torch.uint64)
+
+    A, B = rand_batch(), rand_batch()
+    X = torch.empty_like(A)
+
+    def step():
+        X.copy_(A)
+        be.batch_ntt(X, lvl)
+        be.batch_ntt(X, lvl, inverse=True)
+        out_m = be.batch_hmult(A, B, lvl)
+        out_r = be.batch_hrot(A, steps_rot, lvl)
+        return out_m, out_r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    timer = KernelTimer()
+    ring.TIMER = timer
+    stage = {"ntt": [], "hmult": [], "hrot": []}
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    start, end = ev(), ev()
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0.record()
+        X.copy_(A)
+        be.batch_ntt(X, lvl)
+        be.batch_ntt(X, lvl, inverse=True)
+        e1.record()
+        be.batch_hmult(A, B, lvl)
+        e2.record()
+        be.batch_hrot(A, steps_rot, lvl)
+        e3.record()
+        stage["ntt"].append((e0, e1))
+        stage["hmult"].append((e1, e2))
+        stage["hrot"].append((e2, e3))
+    end.record()
+    torch.cuda.synchronize()
+    ring.TIMER = None
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    t = torch.tensor([total_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    st_ms = {kk: float(np.mean([a.elapsed_time(b) for a, b in v])) for kk, v in stage.items()}
+    hm_b, hr_b, ntt_b = alg_bytes(L, k, bsz, bsz)
+    ks_ms = st_ms["hmult"] + st_ms["hrot"]
+    value_per_rank = (hm_b + hr_b) / (ks_ms / 1e3) / 1e9
+    value = value_per_rank * world  # weak scaling: every rank its own batch
+    ksum = timer.summary()
+    launches = sum(d["launches"] for d in ksum.values())
+    dom_name = max(ksum, key=lambda nm: ksum[nm]["ms"])
+    dom = ksum[dom_name]
+    peak, peak_kind = load_peaks()
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+    kernels = {nm: {"ms_per_step": d["ms"] / args.steps, "launches_per_step": d["launches"] /
+                    args.steps, "GBps_alg": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                    "share": d["ms"] / sum(x["ms"] for x in ksum.values())}
+               for nm, d in ksum.items()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"c2 primitive sweep: N=2^16, L={L} x 40-bit, dnum={DNUM}, "
+                               f"k={k} x 60-bit special, batch {bsz} ct: NTT+iNTT, HMult, "
+                               f"HRot ({bsz} distinct keys)",
+                   "batch_per_gpu": bsz, "l2": "inputs 1.5 GiB per operand > 126 MB L2 (no flush)",
+                   "parallelism": f"replicas x{world} (independent ciphertext batches)"},
+        "stages_ms": st_ms,
+        "hmult_GBps": hm_b / (st_ms["hmult"] / 1e3) / 1e9,
+        "hrot_GBps": hr_b / (st_ms["hrot"] / 1e3) / 1e9,
+        "ntt_GBps": ntt_b / (st_ms["ntt"] / 1e3) / 1e9,
+        "hmult_us_per_ct": 1e3 * st_ms["hmult"] / bsz,
+        "hrot_us_per_ct": 1e3 * st_ms["hrot"] / bsz,
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None},
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "keygen_s": keygen_s,
+    }
+    if clk:
+        line["clocks"] = clk
+
+    if not args.no_e2e:
+        # e2e: host (pinned) inputs -> device -> HMult + HRot -> host, per step
+        hA = A.cpu().pin_memory()
+        hB = B.cpu().pin_memory()
+        m_out = be.chain.level_limbs[lvl - 1]
+        hOm = torch.empty(bsz, 2, m_out, n, dtype=torch.uint64).pin_memory()
+        hOr = torch.empty(bsz, 2, m, n, dtype=torch.uint64).pin_memory()
+        dA, dB = torch.empty_like(A), torch.empty_like(B)
+
+        def e2e_step():
+            dA.copy_(hA, non_blocking=True)
+            dB.copy_(hB, non_blocking=True)
+            om = be.batch_hmult(dA, dB, lvl)
+            orr = be.batch_hrot(dA, steps_rot, lvl)
+            hOm.copy_(om, non_blocking=True)
+            hOr.copy_(orr, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        s0, s1 = ev(), ev()
+        s0.record()
+        for _ in range(max(1, args.steps // 2)):
+            e2e_step()
+        s1.record()
+        torch.cuda.synchronize()
+        e2e_ms = s0.elapsed_time(s1) / max(1, args.steps // 2)
+        line["e2e"] = {"value": world * (hm_b + hr_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
+                       "ms_per_step": e2e_ms,
+                       "h2d_bytes_per_step": hA.numel() * 8 + hB.numel() * 8,
+                       "d2h_bytes_per_step": hOm.numel() * 8 + hOr.numel() * 8}
+        del hA, hB, hOm, hOr, dA, dB
+    del A, B, X
+    torch.cuda.empty_cache()
+
+    if rank == 0 and world == 1 and not args.no_c1:
+        try:
+            line["c1_train"] = run_c1_train(local)
+        except Exception as exc:  # report, never hide
+            line["c1_train"] = {"error": repr(exc)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import parallel_ref as PR
+
+        procs = args.ref_procs or PR.default_procs()
+        secs = _cpu_hmult(_cpu_case(L), procs)
+        hm1, _, _ = alg_bytes(L, k, 1, 0)
+        line["cpu_baseline"] = {"value": hm1 / secs / 1e9, "unit": "GB/s", "cores": procs,
+                                "kind": "port", "seconds": secs,
+                                "sample": _cpu_sample_text(L, procs)}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

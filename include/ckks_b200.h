@@ -88,14 +88,16 @@ int ckb_scalar_mul(const ckb_ring* ring, uint64_t* out, const uint64_t* a, int r
 int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uint64_t* b,
                int batch, int limbs, const int32_t* limb_prime, void* stream);
 
-/* Key-switch ModUp (keys.py:84-90): split `in` ([batch][limbs][N], coefficient
- * domain, basis limb_prime) into digits of `alpha` limbs and lift each digit into
+/* Key-switch ModUp (keys.py:84-90): split `in` (batch item b at
+ * in + b*in_batch_stride, 0 meaning limbs*N; [limbs][N] coefficient domain,
+ * basis limb_prime) into digits of `alpha` limbs and lift each digit into
  * the extended basis ext_prime (ext_limbs entries; the first `limbs` entries must
  * equal limb_prime).  alpha == 1 reproduces the reference's centered per-limb
  * digits exactly; alpha > 1 is the standard fast basis conversion using
  * bconv (device table [digits][alpha][2 + 2*ext_limbs]; see backend.py docs).
  * out: [batch][digits][ext_limbs][N], coefficient domain. */
-int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int batch, int limbs,
+int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
+              int batch, int limbs,
               const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
               const uint64_t* bconv, void* stream);
 
@@ -117,17 +119,21 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
  * in: polys of `limbs` rows, poly p starting at in + p*in_poly_stride (0 means
  * limbs*N; a larger stride reads a limb prefix in place = RingElement.restrict);
  * addend: added to poly p when (p % addend_period) < addend_polys, reading addend row
- *   (p / addend_period) * addend_polys + p % addend_period of [.][limbs-n_drop1][N]; or NULL
- *   (mul_ct: period 2, polys 2 -> d0,d1; rotate: period 2, polys 1 -> c0 only);
+ *   (p / addend_period) * addend_stride + p % addend_period of [.][limbs-n_drop1][N]; or NULL
+ *   (mul_ct on [B][3] tensor products: period 2, polys 2, stride 3 -> d0,d1;
+ *    rotate on [B][2] automorphed inputs: period 2, polys 1, stride 2 -> c0 only);
  * out: [polys][limbs-n_drop1-n_drop2][N]; prescale_host: [limbs][2] {v, shoup(v)} or NULL. */
 int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
-                 const uint64_t* addend, int addend_polys, int addend_period, int polys,
-                 int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
+                 const uint64_t* addend, int addend_polys, int addend_period, int addend_stride,
+                 int polys, int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
                  const uint64_t* prescale_host, void* stream);
 
-/* Galois automorphism X -> X^galois, coefficient domain (ring.py:211-232). */
+/* Galois automorphism X -> X^galois, coefficient domain (ring.py:211-232).
+ * If galois_inv_items (DEVICE, one galois^-1 mod 2N per item of rows_per_item
+ * rows) is non-NULL, each item gets its own automorphism (batched rotations). */
 int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows,
-                     int limbs, const int32_t* limb_prime, uint64_t galois, void* stream);
+                     int limbs, const int32_t* limb_prime, uint64_t galois,
+                     const uint64_t* galois_inv_items, int rows_per_item, void* stream);
 
 /* Signed int64 coefficients -> residues (ring.py:139-145):
  * in: [polys][N] int64; out: [polys][limbs][N]. */

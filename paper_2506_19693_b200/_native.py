@@ -49,16 +49,16 @@ def _load():
                            ctypes.c_int),
         "ckb_tensor": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp],
                        ctypes.c_int),
-        "ckb_modup": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int, c_i32p,
-                       ctypes.c_int, c_vp, c_vp], ctypes.c_int),
+        "ckb_modup": ([R, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, c_i32p,
+                       ctypes.c_int, c_i32p, ctypes.c_int, c_vp, c_vp], ctypes.c_int),
         "ckb_ks_inner": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, c_vp,
                           c_vp, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_divround": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, ctypes.c_int,
-                          ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int, ctypes.c_int, c_u64p,
-                          c_vp],
+                          ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int,
+                          ctypes.c_int, c_u64p, c_vp],
                          ctypes.c_int),
         "ckb_automorphism": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_uint64,
-                              c_vp], ctypes.c_int),
+                              c_vp, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_from_i64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_to_f64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
     }

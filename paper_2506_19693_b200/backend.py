@@ -264,21 +264,23 @@ class B200CkksCore:
         self._bconv_cache[m] = t
         return t
 
-    def _key_switch(self, d: torch.Tensor, m: int, key: KeySwitchKey = None, key_ptrs=None,
-                    addend=None, addend_polys: int = 0, n_rescale: int = 0) -> torch.Tensor:
+    def _key_switch(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
+                    key: KeySwitchKey = None, key_ptrs=None, addend=None, addend_polys: int = 0,
+                    addend_stride: int = None, n_rescale: int = 0) -> torch.Tensor:
         """keys.py:74-100 (+ the following add and optional rescale, fused).
 
-        d: [B, m, N] coefficient domain.  Returns [B, 2, m - n_rescale, N]."""
+        d: batch items of [m, N] (coefficient domain) starting at d, item b at
+        b*d_stride elements (0 = contiguous).  Returns [batch, 2, m - n_rescale, N]."""
         ch = self.chain
-        batch = d.shape[0]
         ext = m + ch.k
         emap = ch.ext_map(m)
-        digits = ch.modup(d, m, self.alpha, self._bconv(m))
+        digits = ch.modup(d, m, self.alpha, self._bconv(m), batch=batch, in_batch_stride=d_stride)
         ch.ntt_fwd(digits, ext, emap)
         acc = ch.ks_inner(digits, m, key=key.data if key is not None else None, key_ptrs=key_ptrs)
         ch.ntt_inv(acc, ext, emap)
         out = ch.divround(acc, 2 * batch, ext, ch.k, n_rescale, addend=addend,
-                          addend_polys=addend_polys, addend_period=2, lmap=emap)
+                          addend_polys=addend_polys, addend_period=2, addend_stride=addend_stride,
+                          lmap=emap)
         return out.view(batch, 2, m - n_rescale, self.n)
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
@@ -374,8 +376,8 @@ class B200CkksCore:
         ch.ntt_fwd(x, m)
         d = ch.tensor(x[0], x[1], m)  # [1, 3, m, N]
         ch.ntt_inv(d, m)
-        out = self._key_switch(d[:, 2], m, key=self.relin_key, addend=d[:, 0:2],
-                               addend_polys=2, n_rescale=len(ch.entry_primes[in_level]))
+        out = self._key_switch(d[:, 2], m, key=self.relin_key, addend=d, addend_polys=2,
+                               addend_stride=3, n_rescale=len(ch.entry_primes[in_level]))
         return GpuCiphertext(out[0], in_level - 1)
 
     def _payload_rotate(self, a, k: int):
@@ -388,7 +390,7 @@ class B200CkksCore:
         key = self.rotation_key(galois)
         m = self._limbs(ct.level)
         r = self.chain.automorphism(ct.data, galois, m)
-        out = self._key_switch(r[1:2], m, key=key, addend=r[0:1], addend_polys=1)
+        out = self._key_switch(r[1], m, key=key, addend=r, addend_polys=1, addend_stride=2)
         return GpuCiphertext(out[0], ct.level)
 
     def _encrypt_values(self, values, level: int) -> GpuCiphertext:
@@ -473,6 +475,57 @@ class B200CkksCore:
             payload=GpuCiphertext(data, level), level_remaining=level, scale_bits=scale_bits,
             depth=rl - level if level < rl else 0, backend_id=self.backend_id,
             keyset_id=self.keyset_id, serial=next(self._serials))
+
+    # ------------------------------------------------------------ batched engine
+    # One launch per stage across a whole batch of ciphertexts (the
+    # config-2 workload: 64 independent ciphertexts).  Same
+    # arithmetic as the per-ciphertext hooks, which are these with B = 1.
+
+    def batch_hmult(self, a: torch.Tensor, b: torch.Tensor, level: int) -> torch.Tensor:
+        """ct x ct multiply + relinearise + rescale of B pairs at one level.
+        a, b: [B, 2, limbs(level), N] -> [B, 2, limbs(level-1), N]."""
+        ch = self.chain
+        m = self._limbs(level)
+        bsz = a.shape[0]
+        xy = torch.empty(2, bsz, 2, m, self.n, dtype=U64, device=self.device)
+        xy[0].copy_(a)
+        xy[1].copy_(b)
+        ch.ntt_fwd(xy, m)
+        d = ch.tensor(xy[0], xy[1], m)
+        ch.ntt_inv(d, m)
+        return self._key_switch(d[:, 2], m, batch=bsz, d_stride=3 * m * self.n,
+                                key=self.relin_key, addend=d, addend_polys=2, addend_stride=3,
+                                n_rescale=len(ch.entry_primes[level]))
+
+    def _rotation_tables(self, steps):
+        key = tuple(int(s) for s in steps)
+        cache = self.__dict__.setdefault("_rot_tab_cache", {})
+        if key not in cache:
+            slots = self.params.slot_count
+            two_n = 2 * self.n
+            gal = [self.galois_for_step.get(s % slots, pow(5, s % slots, two_n)) for s in key]
+            keys = [self.rotation_key(g) for g in gal]
+            ginv = torch.tensor([pow(g, -1, two_n) for g in gal], dtype=torch.int64,
+                                device=self.device).view(U64)
+            ptrs = torch.tensor([k.data.data_ptr() for k in keys], dtype=torch.int64,
+                                device=self.device)
+            cache[key] = (ginv, ptrs, keys)
+        return cache[key]
+
+    def batch_hrot(self, a: torch.Tensor, steps, level: int) -> torch.Tensor:
+        """Rotate item i of a [B, 2, limbs, N] batch left by steps[i] (own key each)."""
+        ch = self.chain
+        m = self._limbs(level)
+        bsz = a.shape[0]
+        ginv, ptrs, _ = self._rotation_tables(steps)
+        r = ch.automorphism(a, 0, m, ginv_items=ginv, rows_per_item=2 * m)
+        return self._key_switch(r[:, 1], m, batch=bsz, d_stride=2 * m * self.n, key_ptrs=ptrs,
+                                addend=r, addend_polys=1, addend_stride=2)
+
+    def batch_ntt(self, a: torch.Tensor, level: int, inverse: bool = False) -> torch.Tensor:
+        """In-place NTT / iNTT of every limb of a [..., limbs(level), N] batch."""
+        m = self._limbs(level)
+        return self.chain.ntt_inv(a, m) if inverse else self.chain.ntt_fwd(a, m)
 
     # ---------------------------------------------------------------- raw access
     def payload_from_planes(self, planes: np.ndarray, level: int) -> GpuCiphertext:

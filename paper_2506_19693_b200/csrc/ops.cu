@@ -75,8 +75,8 @@ __global__ void k_tensor(uint64_t* __restrict__ out, const uint64_t* __restrict_
 
 // One thread per (batch, digit, coefficient); writes the digit's value in
 // every extended limb (coalesced across coefficients).
-__global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in, int batch,
-                        int limbs, int ext, int alpha, int n_digits, int log_n, RingDev R,
+__global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                        size_t in_bstride, int batch, int limbs, int ext, int alpha, int n_digits, int log_n, RingDev R,
                         LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
   const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)batch * n_digits * N;
@@ -86,7 +86,7 @@ __global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__
     const size_t bj = t >> log_n;
     const int j = (int)(bj % n_digits);
     const size_t bi = bj / n_digits;
-    const uint64_t* src = in + bi * limbs * N + n;
+    const uint64_t* src = in + bi * in_bstride + n;
     uint64_t* dst = out + (bi * n_digits + j) * ext * N + n;
     const int first = j * alpha;
     const int cnt = min(alpha, limbs - first);
@@ -179,7 +179,7 @@ __device__ __forceinline__ uint64_t apply_drop(uint64_t xj, bool neg, uint64_t m
 
 __global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
                            size_t in_stride, const uint64_t* __restrict__ addend, int add_polys,
-                           int add_period, int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm,
+                           int add_period, int add_stride, int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm,
                            ScalarTab pre, int has_pre) {
   const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)polys * N;
@@ -193,7 +193,7 @@ __global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restric
     const uint64_t* add = nullptr;
     if (addend) {
       const size_t ph = pidx % add_period;
-      if ((int)ph < add_polys) add = addend + ((pidx / add_period) * add_polys + ph) * m1 * N + n;
+      if ((int)ph < add_polys) add = addend + ((pidx / add_period) * add_stride + ph) * m1 * N + n;
     }
     uint64_t* dst = out + pidx * m2 * N + n;
 
@@ -284,14 +284,16 @@ __global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restric
 // out[t] = sign * in[src(t)] with src from galois^-1 mod 2N (gather form of
 // ring.py:226-231's scatter).
 __global__ void k_automorphism(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
-                               size_t total, int log_n, int limbs, uint64_t ginv, RingDev R,
-                               LimbMap lm) {
+                               size_t total, int log_n, int limbs, uint64_t ginv0,
+                               const uint64_t* __restrict__ ginv_items, int rows_per_item,
+                               RingDev R, LimbMap lm) {
   const uint64_t N = 1ull << log_n;
   const uint64_t mask2 = 2 * N - 1;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t row = i >> log_n;
     const uint64_t t = i & (N - 1);
+    const uint64_t ginv = ginv_items ? __ldg(ginv_items + row / rows_per_item) : ginv0;
     const uint64_t sidx2 = (t * ginv) & mask2;
     const uint64_t p = __ldg(R.mods + (size_t)lm.p[row % limbs] * 8);
     const uint64_t* src = in + row * N;
@@ -492,7 +494,8 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
   return finish();
 }
 
-int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int batch, int limbs,
+int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
+              int batch, int limbs,
               const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
               const uint64_t* bconv, void* stream) {
   LimbMap lm, em;
@@ -505,8 +508,9 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int batch
   const int nd = (limbs + alpha - 1) / alpha;
   const size_t total = ((size_t)batch * nd) << R.log_n;
   if (!total) return 0;
+  const size_t bstride = in_batch_stride > 0 ? (size_t)in_batch_stride : ((size_t)limbs << R.log_n);
   k_modup<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      out, in, batch, limbs, ext_limbs, alpha, nd, (int)R.log_n, R, lm, em, bconv);
+      out, in, bstride, batch, limbs, ext_limbs, alpha, nd, (int)R.log_n, R, lm, em, bconv);
   return finish();
 }
 
@@ -527,7 +531,8 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
 }
 
 int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
-                 const uint64_t* addend, int addend_polys, int addend_period, int polys, int limbs,
+                 const uint64_t* addend, int addend_polys, int addend_period, int addend_stride,
+                 int polys, int limbs,
                  const int32_t* limb_prime, int n_drop1, int n_drop2,
                  const uint64_t* prescale_host, void* stream) {
   LimbMap lm;
@@ -535,7 +540,8 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 > kMaxDrop || n_drop2 > kMaxDrop ||
       n_drop1 + n_drop2 >= limbs || polys < 0)
     return CKB_E_ARG;
-  if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period))
+  if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period ||
+                 addend_stride < addend_polys))
     return CKB_E_ARG;
   const RingDev R = make_ring(ring);
   ScalarTab pre;
@@ -551,15 +557,18 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   if (!total) return 0;
   const size_t stride = in_poly_stride > 0 ? (size_t)in_poly_stride : ((size_t)limbs << R.log_n);
   k_divround<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      out, in, stride, addend, addend ? addend_polys : 0, addend ? addend_period : 1, polys, limbs, n_drop1, n_drop2,
+      out, in, stride, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
+      addend ? addend_stride : 0, polys, limbs, n_drop1, n_drop2,
       (int)R.log_n, R, lm, pre, has_pre);
   return finish();
 }
 
 int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,
-                     const int32_t* limb_prime, uint64_t galois, void* stream) {
+                     const int32_t* limb_prime, uint64_t galois, const uint64_t* galois_inv_items,
+                     int rows_per_item, void* stream) {
   LimbMap lm;
-  if (!make_map(lm, limb_prime, limbs) || rows < 0 || (galois & 1) == 0) return CKB_E_ARG;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0) return CKB_E_ARG;
+  if (galois_inv_items ? rows_per_item < 1 : (galois & 1) == 0) return CKB_E_ARG;
   const RingDev R = make_ring(ring);
   const uint64_t two_n = 2ull << R.log_n;
   // inverse of an odd galois element modulo a power of two (Newton iteration)
@@ -569,7 +578,7 @@ int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, in
   const size_t total = (size_t)rows << R.log_n;
   if (!total) return 0;
   k_automorphism<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      out, in, total, (int)R.log_n, limbs, inv, R, lm);
+      out, in, total, (int)R.log_n, limbs, inv, galois_inv_items, rows_per_item, R, lm);
   return finish();
 }
 

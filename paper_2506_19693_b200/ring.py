@@ -23,10 +23,47 @@ from . import _native as nat
 from .primes import build_chain
 
 U64 = torch.uint64
+W = 8  # bytes per residue
 
 
 def shoup(v: int, p: int) -> int:
     return (v << 64) // p
+
+
+class KernelTimer:
+    """Optional per-kernel CUDA-event timing (bench.py): every wrapper call
+    records start/end events on the launching (current) stream plus its
+    algorithmic bytes and kernel-launch count."""
+
+    def __init__(self):
+        self.records = []
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for name, s, e, nbytes, launches in self.records:
+            d = out.setdefault(name, {"ms": 0.0, "calls": 0, "bytes": 0, "launches": 0})
+            d["ms"] += s.elapsed_time(e)
+            d["calls"] += 1
+            d["bytes"] += nbytes
+            d["launches"] += launches
+        return out
+
+
+TIMER = None  # set to a KernelTimer to instrument
+
+
+def _run(name, nbytes, launches, fn):
+    t = TIMER
+    if t is None:
+        return fn()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    r = fn()
+    e.record()
+    t.records.append((name, s, e, nbytes, launches))
+    return r
 
 
 class GpuChain:
@@ -106,26 +143,35 @@ class GpuChain:
         return torch.empty(*shape, self.n, dtype=U64, device=self.device)
 
     # -- kernels -------------------------------------------------------------------
+    def _ntt_launches(self, rows: int) -> int:
+        if self.log_n <= 12:
+            return 1
+        chunk = max(1, (48 << 20) // (self.n * W))
+        return 2 * (-(-rows // chunk))
+
     def ntt_fwd(self, t: torch.Tensor, limbs: int, lmap=None):
         rows = t.numel() >> self.log_n
-        nat.check(nat.LIB.ckb_ntt_forward(self.ring_p, nat.ptr(t), rows, limbs,
-                                          lmap or self.q_map(limbs), nat.stream_handle()),
-                  "ntt_forward")
+        _run("ntt", 2 * rows * self.n * W, self._ntt_launches(rows), lambda: nat.check(
+            nat.LIB.ckb_ntt_forward(self.ring_p, nat.ptr(t), rows, limbs,
+                                    lmap or self.q_map(limbs), nat.stream_handle()),
+            "ntt_forward"))
         return t
 
     def ntt_inv(self, t: torch.Tensor, limbs: int, lmap=None):
         rows = t.numel() >> self.log_n
-        nat.check(nat.LIB.ckb_ntt_inverse(self.ring_p, nat.ptr(t), rows, limbs,
-                                          lmap or self.q_map(limbs), nat.stream_handle()),
-                  "ntt_inverse")
+        _run("intt", 2 * rows * self.n * W, self._ntt_launches(rows), lambda: nat.check(
+            nat.LIB.ckb_ntt_inverse(self.ring_p, nat.ptr(t), rows, limbs,
+                                    lmap or self.q_map(limbs), nat.stream_handle()),
+            "ntt_inverse"))
         return t
 
     def ew(self, op: int, out, a, b=None, c=None, limbs: int = 0, lmap=None, b_rows: int = 0):
         rows = a.numel() >> self.log_n
-        nat.check(nat.LIB.ckb_elementwise(
+        nb = 2 * rows + (0 if b is None else (b_rows or rows)) + (0 if c is None else rows)
+        _run("elementwise", nb * self.n * W, 1, lambda: nat.check(nat.LIB.ckb_elementwise(
             self.ring_p, op, nat.ptr(out), nat.ptr(a), nat.ptr(b) if b is not None else None,
             nat.ptr(c) if c is not None else None, rows, limbs, lmap or self.q_map(limbs), b_rows,
-            nat.stream_handle()), "elementwise")
+            nat.stream_handle()), "elementwise"))
         return out
 
     def add(self, a, b, limbs, out=None, lmap=None):
@@ -144,29 +190,35 @@ class GpuChain:
     def scalar_mul(self, a, pairs, limbs, out=None, lmap=None):
         out = out if out is not None else torch.empty_like(a)
         rows = a.numel() >> self.log_n
-        nat.check(nat.LIB.ckb_scalar_mul(self.ring_p, nat.ptr(out), nat.ptr(a), rows, limbs,
-                                         lmap or self.q_map(limbs), pairs, nat.stream_handle()),
-                  "scalar_mul")
+        _run("scalar_mul", 2 * rows * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_scalar_mul(self.ring_p, nat.ptr(out), nat.ptr(a), rows, limbs,
+                                   lmap or self.q_map(limbs), pairs, nat.stream_handle()),
+            "scalar_mul"))
         return out
 
     def tensor(self, a, b, limbs, out=None):
         batch = a.numel() // (2 * limbs * self.n)
         out = out if out is not None else torch.empty(batch, 3, limbs, self.n, dtype=U64,
                                                       device=self.device)
-        nat.check(nat.LIB.ckb_tensor(self.ring_p, nat.ptr(out), nat.ptr(a), nat.ptr(b), batch, limbs,
-                                     self.q_map(limbs), nat.stream_handle()), "tensor")
+        _run("tensor", 7 * batch * limbs * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_tensor(self.ring_p, nat.ptr(out), nat.ptr(a), nat.ptr(b), batch, limbs,
+                               self.q_map(limbs), nat.stream_handle()), "tensor"))
         return out
 
-    def modup(self, d, m: int, alpha: int, bconv, out=None):
-        batch = d.numel() // (m * self.n)
+    def modup(self, d, m: int, alpha: int, bconv, batch: int = None, in_batch_stride: int = 0,
+              out=None):
+        """d: batch items of [m][N] (item b at d + b*in_batch_stride elements)."""
+        if batch is None:
+            batch = d.numel() // (m * self.n)
         ext = m + self.k
         nd = -(-m // alpha)
         out = out if out is not None else torch.empty(batch, nd, ext, self.n, dtype=U64,
                                                       device=self.device)
-        nat.check(nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), batch, m, self.q_map(m),
-                                    ext, self.ext_map(m), alpha,
-                                    nat.ptr(bconv) if bconv is not None else None,
-                                    nat.stream_handle()), "modup")
+        _run("modup", (batch * m + batch * nd * ext) * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), in_batch_stride, batch,
+                              m, self.q_map(m), ext, self.ext_map(m), alpha,
+                              nat.ptr(bconv) if bconv is not None else None,
+                              nat.stream_handle()), "modup"))
         return out
 
     def ks_inner(self, digits, m: int, key: torch.Tensor = None, key_ptrs: torch.Tensor = None,
@@ -175,49 +227,62 @@ class GpuChain:
         out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
                                                       device=self.device)
         key_limbs = len(self.all_primes)
-        nat.check(nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
-                                       self.ext_map(m),
-                                       nat.ptr(key) if key is not None else None,
-                                       nat.ptr(key_ptrs) if key_ptrs is not None else None,
-                                       key_limbs, self.ext_map(m), nat.stream_handle()),
-                  "ks_inner")
+        n_keys = batch if key_ptrs is not None else 1
+        nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext
+        _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
+                                 self.ext_map(m), nat.ptr(key) if key is not None else None,
+                                 nat.ptr(key_ptrs) if key_ptrs is not None else None,
+                                 key_limbs, self.ext_map(m), nat.stream_handle()), "ks_inner"))
         return out
 
     def divround(self, x, polys: int, limbs: int, n1: int, n2: int = 0, addend=None,
-                 addend_polys: int = 0, addend_period: int = 1, prescale=None,
-                 in_poly_stride: int = 0, lmap=None, out=None):
+                 addend_polys: int = 0, addend_period: int = 1, addend_stride: int = None,
+                 prescale=None, in_poly_stride: int = 0, lmap=None, out=None):
         m2 = limbs - n1 - n2
         out = out if out is not None else torch.empty(polys, m2, self.n, dtype=U64,
                                                       device=self.device)
-        nat.check(nat.LIB.ckb_divround(self.ring_p, nat.ptr(out), nat.ptr(x), in_poly_stride,
-                                       nat.ptr(addend) if addend is not None else None,
-                                       addend_polys if addend is not None else 0,
-                                       addend_period, polys, limbs,
-                                       lmap or self.q_map(limbs), n1, n2, prescale,
-                                       nat.stream_handle()), "divround")
+        if addend_stride is None:
+            addend_stride = addend_polys
+        n_add = 0 if addend is None else (polys // addend_period) * addend_polys * (limbs - n1)
+        nb = polys * limbs + n_add + polys * m2
+        _run("divround", nb * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_divround(self.ring_p, nat.ptr(out), nat.ptr(x), in_poly_stride,
+                                 nat.ptr(addend) if addend is not None else None,
+                                 addend_polys if addend is not None else 0,
+                                 addend_period, addend_stride, polys, limbs,
+                                 lmap or self.q_map(limbs), n1, n2, prescale,
+                                 nat.stream_handle()), "divround"))
         return out
 
-    def automorphism(self, x, galois: int, limbs: int, out=None, lmap=None):
+    def automorphism(self, x, galois: int, limbs: int, out=None, lmap=None, ginv_items=None,
+                     rows_per_item: int = 0):
+        """X -> X^galois per row; with ginv_items (device u64 [items]) each item of
+        rows_per_item rows uses its own galois^-1 mod 2N."""
         out = out if out is not None else torch.empty_like(x)
         rows = x.numel() >> self.log_n
-        nat.check(nat.LIB.ckb_automorphism(self.ring_p, nat.ptr(out), nat.ptr(x), rows, limbs,
-                                           lmap or self.q_map(limbs), galois, nat.stream_handle()),
-                  "automorphism")
+        _run("automorphism", 2 * rows * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_automorphism(self.ring_p, nat.ptr(out), nat.ptr(x), rows, limbs,
+                                     lmap or self.q_map(limbs), galois,
+                                     nat.ptr(ginv_items) if ginv_items is not None else None,
+                                     rows_per_item, nat.stream_handle()), "automorphism"))
         return out
 
     def from_i64(self, coeffs: torch.Tensor, limbs: int, lmap=None, out=None):
         polys = coeffs.numel() >> self.log_n
         out = out if out is not None else torch.empty(polys, limbs, self.n, dtype=U64,
                                                       device=self.device)
-        nat.check(nat.LIB.ckb_from_i64(self.ring_p, nat.ptr(out), nat.ptr(coeffs), polys, limbs,
-                                       lmap or self.q_map(limbs), nat.stream_handle()), "from_i64")
+        _run("from_i64", (polys + polys * limbs) * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_from_i64(self.ring_p, nat.ptr(out), nat.ptr(coeffs), polys, limbs,
+                                 lmap or self.q_map(limbs), nat.stream_handle()), "from_i64"))
         return out
 
     def to_f64(self, x: torch.Tensor, limbs: int, lmap=None):
         polys = x.numel() // (limbs * self.n)
         out = torch.empty(polys, self.n, dtype=torch.float64, device=self.device)
-        nat.check(nat.LIB.ckb_to_f64(self.ring_p, nat.ptr(out), nat.ptr(x), polys, limbs,
-                                     lmap or self.q_map(limbs), nat.stream_handle()), "to_f64")
+        _run("to_f64", (polys * limbs + polys) * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_to_f64(self.ring_p, nat.ptr(out), nat.ptr(x), polys, limbs,
+                               lmap or self.q_map(limbs), nat.stream_handle()), "to_f64"))
         return out
 
     # -- host <-> device helpers -------------------------------------------------------
