@@ -116,6 +116,12 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
  *   x <- divround(x, last n_drop1 limbs)  (dropped last-first, one prime at a time)
  *   x <- x + addend                      (optional; backend.py:142 / :171)
  *   x <- divround(x, last n_drop2 limbs)  (rescale, backend.py:86-92)
+ * evaluated in mixed radix with host-precomputed constants (bit-identical to the
+ * sequential reference; derivation in DESIGN.md):
+ *   tab1: DEVICE [limbs][n_drop1+1][2]: for u < n_drop1 {M_u mod p_j, shoup} with
+ *         M_u the product of the first u dropped primes, then {M_t^-1 mod p_j, shoup}
+ *         (t = j's drop position, or n_drop1 = the whole product for kept limbs);
+ *   tab2: DEVICE [limbs-n_drop1][n_drop2+1][2], the same for the second chain.
  * in: polys of `limbs` rows, poly p starting at in + p*in_poly_stride (0 means
  * limbs*N; a larger stride reads a limb prefix in place = RingElement.restrict);
  * addend: added to poly p when (p % addend_period) < addend_polys, reading addend row
@@ -126,7 +132,8 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
 int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
                  const uint64_t* addend, int addend_polys, int addend_period, int addend_stride,
                  int polys, int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
-                 const uint64_t* prescale_host, void* stream);
+                 const uint64_t* prescale_host, const uint64_t* tab1, const uint64_t* tab2,
+                 void* stream);
 
 /* Galois automorphism X -> X^galois, coefficient domain (ring.py:211-232).
  * If galois_inv_items (DEVICE, one galois^-1 mod 2N per item of rows_per_item

@@ -13,7 +13,8 @@ import os
 import numpy as np
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libckks_b200.so")
+_LIB_PATH = os.environ.get("CKB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "_lib", "libckks_b200.so")
 
 c_u64p = ctypes.POINTER(ctypes.c_uint64)
 c_i32p = ctypes.POINTER(ctypes.c_int32)
@@ -55,7 +56,7 @@ def _load():
                           c_vp, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_divround": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, ctypes.c_int,
                           ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int,
-                          ctypes.c_int, c_u64p, c_vp],
+                          ctypes.c_int, c_u64p, c_vp, c_vp, c_vp],
                          ctypes.c_int),
         "ckb_automorphism": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_uint64,
                               c_vp, ctypes.c_int, c_vp], ctypes.c_int),

@@ -280,7 +280,7 @@ class B200CkksCore:
         ch.ntt_inv(acc, ext, emap)
         out = ch.divround(acc, 2 * batch, ext, ch.k, n_rescale, addend=addend,
                           addend_polys=addend_polys, addend_period=2, addend_stride=addend_stride,
-                          lmap=emap)
+                          basis=ch.ext_basis(m))
         return out.view(batch, 2, m - n_rescale, self.n)
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:

@@ -3,6 +3,10 @@
 #include "common.cuh"
 
 using namespace ckb_internal;
+
+#ifndef CKB_NTT_MINB
+#define CKB_NTT_MINB 3  // CTAs per SM the register budget targets (80 regs)
+#endif
 using ckb::Mod;
 
 namespace {
@@ -37,16 +41,42 @@ struct NttPhase {
   int row0;     // first row handled by this launch (for L2-resident chunking)
 };
 
+// Shared-memory slot of element r of group g: one pad word per 16 elements
+// makes both the strided (r = w + 16k) and the contiguous (r = 16w + k)
+// register-round patterns bank-conflict free.
 template <int S>
 __device__ __forceinline__ int sidx(int g, int r) {
   constexpr int G = 1 << S;
-  return g * (G + 1) + (r ^ ((r >> 4) & 15));
+  return g * (G + G / 16) + r + (r >> 4);
 }
 
+// Harvey forward (CT) butterfly, values in [0, 4p).
+__device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
+                                        uint64_t p, uint64_t two_p) {
+  uint64_t a = X >= two_p ? X - two_p : X;
+  const uint64_t t = ckb::mul_shoup_lazy(Y, W, Ws, p);
+  X = a + t;
+  Y = a - t + two_p;
+}
+
+// Harvey inverse (GS) butterfly, values in [0, 2p).
+__device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
+                                        uint64_t p, uint64_t two_p) {
+  uint64_t sum = X + Y;
+  sum = sum >= two_p ? sum - two_p : sum;
+  const uint64_t d = X - Y + two_p;
+  X = sum;
+  Y = ckb::mul_shoup_lazy(d, W, Ws, p);
+}
+
+// One radix-16 round: the thread's 16 elements differ in bits [WLO, WLO+4) of
+// r; stages b in (HI-1 .. LO) for the forward, (LO .. HI-1) for the inverse.
+// The twiddle of the butterfly at k is tw[t0(b) + (k >> (bb+1))]: only
+// 1, 2, 4, 8 distinct values per stage, loaded once each.
 template <int S, int HI>
 __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
-                                           const uint64_t* __restrict__ tws, const Mod& m,
-                                           int gq, int gidx, int w, const NttPhase& ph) {
+                                           const uint64_t* __restrict__ tws, uint64_t p,
+                                           uint64_t two_p, int gq, int tbase, int w, int last) {
   if constexpr (HI > 0) {
     constexpr int Q = HI < 4 ? HI : 4;
     constexpr int LO = HI - Q;
@@ -55,25 +85,26 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restri
     uint64_t x[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
-    const int tbase = ph.M0 + ph.gt * gidx;
-    const uint64_t p = m.p, two_p = m.two_p;
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
+      const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
+      uint64_t Wv[8], Wsv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < (8 >> bb)) {
+          Wv[i] = __ldg(tw + t0 + i);
+          Wsv[i] = __ldg(tws + t0 + i);
+        }
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         if (k & (1 << bb)) continue;
-        const int r = rbase | (k << WLO);
-        const int ti = (tbase << (S - 1 - b)) + (r >> (b + 1));
-        const uint64_t W = __ldg(tw + ti), Ws = __ldg(tws + ti);
-        uint64_t X = x[k];
-        X = X >= two_p ? X - two_p : X;
-        const uint64_t T = ckb::mul_shoup_lazy(x[k | (1 << bb)], W, Ws, p);
-        x[k] = X + T;
-        x[k | (1 << bb)] = X - T + two_p;
+        const int i = k >> (bb + 1);
+        ct_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
       }
     }
-    if (LO == 0 && ph.last) {
+    if (LO == 0 && last) {
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         uint64_t X = x[k];
@@ -84,16 +115,16 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restri
 #pragma unroll
     for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    fwd_rounds<S, LO>(s, tw, tws, m, gq, gidx, w, ph);
+    fwd_rounds<S, LO>(s, tw, tws, p, two_p, gq, tbase, w, last);
   }
 }
 
 template <int S, int LO>
 __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
-                                           const uint64_t* __restrict__ tws, const Mod& m,
-                                           uint64_t ninv, uint64_t ninvs, uint64_t fw,
-                                           uint64_t fws, int gq, int gidx, int w,
-                                           const NttPhase& ph) {
+                                           const uint64_t* __restrict__ tws, uint64_t p,
+                                           uint64_t two_p, uint64_t ninv, uint64_t ninvs,
+                                           uint64_t fw, uint64_t fws, int gq, int tbase, int w,
+                                           int last) {
   if constexpr (LO < S) {
     constexpr int Q = (S - LO) < 4 ? (S - LO) : 4;
     constexpr int HI = LO + Q;
@@ -102,88 +133,116 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restri
     uint64_t x[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
-    const int tbase = ph.M0 + ph.gt * gidx;
-    const uint64_t p = m.p, two_p = m.two_p;
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
+      if (b == S - 1 && last) {
+        // top stage of the whole transform with N^-1 folded in
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (k & (1 << bb)) continue;
-        const uint64_t X = x[k], Y = x[k | (1 << bb)];
-        uint64_t sum = X + Y;
-        sum = sum >= two_p ? sum - two_p : sum;
-        const uint64_t d = X - Y + two_p;
-        if (b == S - 1 && ph.last) {
+        for (int k = 0; k < 16; ++k) {
+          if (k & (1 << bb)) continue;
+          const uint64_t X = x[k], Y = x[k | (1 << bb)];
+          uint64_t sum = X + Y;
+          sum = sum >= two_p ? sum - two_p : sum;
           x[k] = ckb::mul_shoup(sum, ninv, ninvs, p);
-          x[k | (1 << bb)] = ckb::mul_shoup(d, fw, fws, p);
-        } else {
-          const int r = rbase | (k << WLO);
-          const int ti = (tbase << (S - 1 - b)) + (r >> (b + 1));
-          const uint64_t W = __ldg(tw + ti), Ws = __ldg(tws + ti);
-          x[k] = sum;
-          x[k | (1 << bb)] = ckb::mul_shoup_lazy(d, W, Ws, p);
+          x[k | (1 << bb)] = ckb::mul_shoup(X - Y + two_p, fw, fws, p);
+        }
+      } else {
+        const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
+        uint64_t Wv[8], Wsv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < (8 >> bb)) {
+            Wv[i] = __ldg(tw + t0 + i);
+            Wsv[i] = __ldg(tws + t0 + i);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (k & (1 << bb)) continue;
+          const int i = k >> (bb + 1);
+          gs_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
         }
       }
     }
 #pragma unroll
     for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    inv_rounds<S, HI>(s, tw, tws, m, ninv, ninvs, fw, fws, gq, gidx, w, ph);
+    inv_rounds<S, HI>(s, tw, tws, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
   }
 }
 
 template <int S, bool FWD>
-__global__ void __launch_bounds__(256) k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph,
-                                                   RingDev R, LimbMap lm) {
+__global__ void __launch_bounds__(256, CKB_NTT_MINB) k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph,
+                                                      RingDev R, LimbMap lm) {
   constexpr int G = 1 << S;
   extern __shared__ uint64_t smem[];
   const int N = 1 << R.log_n;
   const int row = ph.row0 + blockIdx.x / ph.tiles_per_row;
   const int tile = blockIdx.x % ph.tiles_per_row;
   const int pi = lm.p[row % ph.limbs];
-  const Mod m = load_mod(R, pi);
+  const uint64_t* mm = R.mods + (size_t)pi * 8;
+  const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
   uint64_t* base = data + (size_t)row * N;
   const int C = ph.C;
   const int T = blockDim.x;
   const int tid = threadIdx.x;
   const int g0 = tile * C;
+  const bool rows_contig = ph.rstride == 1;
 
-  for (int idx = tid; idx < C * G; idx += T) {
+  // tile -> smem, 16-byte vectors (pairs adjacent in global memory)
+  for (int q = tid; q < C * G / 2; q += T) {
+    const int e = 2 * q;
     int g, r;
-    if (ph.rstride == 1) {
-      g = idx >> S;
-      r = idx & (G - 1);
+    size_t off;
+    if (rows_contig) {
+      g = e >> S;
+      r = e & (G - 1);
+      off = (size_t)(g0 + g) * ph.gstride + r;
     } else {
-      r = idx / C;
-      g = idx - r * C;
+      r = e / C;
+      g = e - r * C;
+      off = (size_t)r * ph.rstride + g0 + g;
     }
-    smem[sidx<S>(g, r)] = base[(size_t)(g0 + g) * ph.gstride + (size_t)r * ph.rstride];
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(base + off);
+    smem[sidx<S>(g, r)] = v.x;
+    if (rows_contig)
+      smem[sidx<S>(g, r + 1)] = v.y;
+    else
+      smem[sidx<S>(g + 1, r)] = v.y;
   }
   __syncthreads();
 
   const int gq = tid / (G / 16);
   const int w = tid % (G / 16);
-  const int gidx = g0 + gq;
+  const int tbase = ph.M0 + ph.gt * (g0 + gq);
   const uint64_t* tables = R.ntt + (size_t)pi * 4 * N;
   if constexpr (FWD) {
-    fwd_rounds<S, S>(smem, tables, tables + N, m, gq, gidx, w, ph);
+    fwd_rounds<S, S>(smem, tables, tables + N, p, two_p, gq, tbase, w, ph.last);
   } else {
-    const uint64_t* mm = R.mods + (size_t)pi * 8;
-    inv_rounds<S, 0>(smem, tables + 2 * N, tables + 3 * N, m, __ldg(mm + 4), __ldg(mm + 5),
-                     __ldg(mm + 6), __ldg(mm + 7), gq, gidx, w, ph);
+    inv_rounds<S, 0>(smem, tables + 2 * N, tables + 3 * N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
+                     __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
   }
 
-  for (int idx = tid; idx < C * G; idx += T) {
+  for (int q = tid; q < C * G / 2; q += T) {
+    const int e = 2 * q;
     int g, r;
-    if (ph.rstride == 1) {
-      g = idx >> S;
-      r = idx & (G - 1);
+    size_t off;
+    ulonglong2 v;
+    if (rows_contig) {
+      g = e >> S;
+      r = e & (G - 1);
+      off = (size_t)(g0 + g) * ph.gstride + r;
+      v.x = smem[sidx<S>(g, r)];
+      v.y = smem[sidx<S>(g, r + 1)];
     } else {
-      r = idx / C;
-      g = idx - r * C;
+      r = e / C;
+      g = e - r * C;
+      off = (size_t)r * ph.rstride + g0 + g;
+      v.x = smem[sidx<S>(g, r)];
+      v.y = smem[sidx<S>(g + 1, r)];
     }
-    base[(size_t)(g0 + g) * ph.gstride + (size_t)r * ph.rstride] = smem[sidx<S>(g, r)];
+    *reinterpret_cast<ulonglong2*>(base + off) = v;
   }
 }
 
@@ -192,7 +251,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
                  const LimbMap& lm, cudaStream_t st) {
   const int G = 1 << S;
   const int threads = ph.C * G / 16;
-  const size_t smem = (size_t)ph.C * (G + 1) * sizeof(uint64_t);
+  const size_t smem = (size_t)ph.C * (G + G / 16) * sizeof(uint64_t);
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
 #define CKB_NTT_CASE(SS)                                                           \

@@ -166,25 +166,38 @@ __global__ void k_ks_inner(uint64_t* __restrict__ acc, const uint64_t* __restric
 // Exact divide-and-round (rescale / ModDown / level adjust)
 // ===========================================================================
 
-constexpr int kMaxDrop = 16;
+constexpr int kMaxDrop = 8;
 
-// x_j <- (x_j - [r]_{p_j}) * drop^-1  for a centered remainder r = (neg ? -mag : mag)
-__device__ __forceinline__ uint64_t apply_drop(uint64_t xj, bool neg, uint64_t mag, int pd, int pj,
-                                               const Mod& mj, const RingDev& R) {
-  const uint64_t rm = ckb::reduce64(mag, mj);
-  const uint64_t diff = neg ? ckb::add_mod(xj, rm, mj.p) : ckb::sub_mod(xj, rm, mj.p);
-  const uint64_t* pr = R.pair + ((size_t)pd * R.np + pj) * 4;
-  return ckb::mul_shoup(diff, __ldg(pr), __ldg(pr + 1), mj.p);
+// acc - r * M  (mod p) for a signed centered remainder r and a Shoup constant M.
+__device__ __forceinline__ uint64_t sub_rm(uint64_t acc, int64_t r, uint64_t M, uint64_t Ms,
+                                           uint64_t p) {
+  const uint64_t mag = (uint64_t)(r < 0 ? -r : r);
+  uint64_t prod = ckb::mul_shoup_lazy(mag, M, Ms, p);
+  prod = prod >= p ? prod - p : prod;
+  return r < 0 ? ckb::add_mod(acc, prod, p) : ckb::sub_mod(acc, prod, p);
 }
 
-__global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
-                           size_t in_stride, const uint64_t* __restrict__ addend, int add_polys,
-                           int add_period, int add_stride, int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm,
-                           ScalarTab pre, int has_pre) {
+__device__ __forceinline__ int64_t centered(uint64_t x, uint64_t p) {
+  return x > (p >> 1) ? (int64_t)x - (int64_t)p : (int64_t)x;
+}
+
+// Exact sequential divide-and-round by the last n1 (then n2) limbs, evaluated
+// in mixed radix: dropping p_0, p_1, ... one at a time (ring.py:171-183) gives
+//   result_j = (x_j - sum_u r_u M_u) * (prod_u p_u)^-1  (mod q_j),
+// with M_u = p_0 ... p_{u-1} and r_u the centered residue of the partially
+// divided value at p_u — the same integers, so the output is bit-identical.
+// tab1: [limbs][n1+1][2] {M_u mod p_j, shoup} and {(M_t)^-1 mod p_j or P^-1}
+// tab2: [m1][n2+1][2] likewise for the second chain.
+__global__ void __launch_bounds__(256) k_divround(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_stride,
+    const uint64_t* __restrict__ addend, int add_polys, int add_period, int add_stride,
+    int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm, ScalarTab pre,
+    int has_pre, const uint64_t* __restrict__ tab1, const uint64_t* __restrict__ tab2) {
   const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)polys * N;
-  const int m1 = limbs - n1;   // limbs after the first drop chain
-  const int m2 = m1 - n2;      // output limbs
+  const int m1 = limbs - n1;
+  const int m2 = m1 - n2;
+  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t n = t & (N - 1);
@@ -197,81 +210,63 @@ __global__ void k_divround(uint64_t* __restrict__ out, const uint64_t* __restric
     }
     uint64_t* dst = out + pidx * m2 * N + n;
 
-    auto load = [&](int l) -> uint64_t {
+    auto load = [&](int l, uint64_t p) -> uint64_t {
       uint64_t v = src[(size_t)l * N];
-      if (has_pre) {
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
-        v = ckb::mul_shoup(v, pre.v[l], pre.s[l], p);
-      }
+      if (has_pre) v = ckb::mul_shoup(v, pre.v[l], pre.s[l], p);
       return v;
     };
-
-    // ---- first drop chain over limbs [m1, limbs), last limb first
-    bool neg1[kMaxDrop];
-    uint64_t mag1[kMaxDrop];
-    uint64_t tail[kMaxDrop];
-#pragma unroll
-    for (int s = 0; s < kMaxDrop; ++s)
-      if (s < n1) tail[s] = load(m1 + s);
+    int64_t r1[kMaxDrop], r2[kMaxDrop];
 #pragma unroll
     for (int d = 0; d < kMaxDrop; ++d) {
       if (d < n1) {
-        const int li = limbs - 1 - d;          // limb being dropped
-        const int pd = lm.p[li];
-        const uint64_t q = __ldg(R.mods + (size_t)pd * 8);
-        const uint64_t x = tail[li - m1];
-        neg1[d] = x > (q >> 1);
-        mag1[d] = neg1[d] ? q - x : x;
+        const int li = limbs - 1 - d;
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t* T = tab1 + (size_t)li * s1;
+        uint64_t acc = load(li, p);
 #pragma unroll
-        for (int s = 0; s < kMaxDrop; ++s) {
-          if (s < li - m1) {
-            const int pj = lm.p[m1 + s];
-            tail[s] = apply_drop(tail[s], neg1[d], mag1[d], pd, pj, load_mod(R, pj), R);
-          }
-        }
+        for (int u = 0; u < kMaxDrop; ++u)
+          if (u < d) acc = sub_rm(acc, r1[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
+        acc = ckb::mul_shoup(acc, __ldg(T + 2 * n1), __ldg(T + 2 * n1 + 1), p);
+        r1[d] = centered(acc, p);
       }
     }
     auto stage1 = [&](int l) -> uint64_t {
-      uint64_t v = load(l);
-      const int pj = lm.p[l];
-      const Mod mj = load_mod(R, pj);
+      const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+      uint64_t v = load(l, p);
+      if (n1) {
+        const uint64_t* T = tab1 + (size_t)l * s1;
 #pragma unroll
-      for (int d = 0; d < kMaxDrop; ++d)
-        if (d < n1) v = apply_drop(v, neg1[d], mag1[d], lm.p[limbs - 1 - d], pj, mj, R);
-      if (add) v = ckb::add_mod(v, add[(size_t)l * N], mj.p);
+        for (int u = 0; u < kMaxDrop; ++u)
+          if (u < n1) v = sub_rm(v, r1[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
+        v = ckb::mul_shoup(v, __ldg(T + 2 * n1), __ldg(T + 2 * n1 + 1), p);
+      }
+      if (add) v = ckb::add_mod(v, add[(size_t)l * N], p);
       return v;
     };
-    // ---- second drop chain over limbs [m2, m1)
-    bool neg2[kMaxDrop];
-    uint64_t mag2[kMaxDrop];
-#pragma unroll
-    for (int s = 0; s < kMaxDrop; ++s)
-      if (s < n2) tail[s] = stage1(m2 + s);
 #pragma unroll
     for (int d = 0; d < kMaxDrop; ++d) {
       if (d < n2) {
         const int li = m1 - 1 - d;
-        const int pd = lm.p[li];
-        const uint64_t q = __ldg(R.mods + (size_t)pd * 8);
-        const uint64_t x = tail[li - m2];
-        neg2[d] = x > (q >> 1);
-        mag2[d] = neg2[d] ? q - x : x;
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t* T = tab2 + (size_t)li * s2;
+        uint64_t acc = stage1(li);
 #pragma unroll
-        for (int s = 0; s < kMaxDrop; ++s) {
-          if (s < li - m2) {
-            const int pj = lm.p[m2 + s];
-            tail[s] = apply_drop(tail[s], neg2[d], mag2[d], pd, pj, load_mod(R, pj), R);
-          }
-        }
+        for (int u = 0; u < kMaxDrop; ++u)
+          if (u < d) acc = sub_rm(acc, r2[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
+        acc = ckb::mul_shoup(acc, __ldg(T + 2 * n2), __ldg(T + 2 * n2 + 1), p);
+        r2[d] = centered(acc, p);
       }
     }
     for (int l = 0; l < m2; ++l) {
       uint64_t v = stage1(l);
-      const int pj = lm.p[l];
-      const Mod mj = load_mod(R, pj);
+      if (n2) {
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+        const uint64_t* T = tab2 + (size_t)l * s2;
 #pragma unroll
-      for (int d = 0; d < kMaxDrop; ++d)
-        if (d < n2) v = apply_drop(v, neg2[d], mag2[d], lm.p[m1 - 1 - d], pj, mj, R);
+        for (int u = 0; u < kMaxDrop; ++u)
+          if (u < n2) v = sub_rm(v, r2[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
+        v = ckb::mul_shoup(v, __ldg(T + 2 * n2), __ldg(T + 2 * n2 + 1), p);
+      }
       dst[(size_t)l * N] = v;
     }
   }
@@ -532,14 +527,15 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
 
 int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,
                  const uint64_t* addend, int addend_polys, int addend_period, int addend_stride,
-                 int polys, int limbs,
-                 const int32_t* limb_prime, int n_drop1, int n_drop2,
-                 const uint64_t* prescale_host, void* stream) {
+                 int polys, int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
+                 const uint64_t* prescale_host, const uint64_t* tab1, const uint64_t* tab2,
+                 void* stream) {
   LimbMap lm;
   if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
   if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 > kMaxDrop || n_drop2 > kMaxDrop ||
       n_drop1 + n_drop2 >= limbs || polys < 0)
     return CKB_E_ARG;
+  if ((n_drop1 && !tab1) || (n_drop2 && !tab2)) return CKB_E_ARG;
   if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period ||
                  addend_stride < addend_polys))
     return CKB_E_ARG;
@@ -558,8 +554,8 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   const size_t stride = in_poly_stride > 0 ? (size_t)in_poly_stride : ((size_t)limbs << R.log_n);
   k_divround<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       out, in, stride, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
-      addend ? addend_stride : 0, polys, limbs, n_drop1, n_drop2,
-      (int)R.log_n, R, lm, pre, has_pre);
+      addend ? addend_stride : 0, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, pre,
+      has_pre, tab1, tab2);
   return finish();
 }
 

@@ -97,37 +97,43 @@ class GpuChain:
         self._maps: dict = {}
 
     # -- bases ------------------------------------------------------------------
+    # A basis is a tuple of indices into all_primes; the kernels receive it as
+    # a ctypes int32 array (cached per tuple).
     def limbs_at(self, level: int) -> list:
         return self.primes[: self.level_limbs[level]]
 
     def modulus_at(self, level: int) -> int:
         return math.prod(self.limbs_at(level))
 
+    def q_basis(self, m: int) -> tuple:
+        """The first m ciphertext limbs."""
+        return tuple(range(m))
+
+    def ext_basis(self, m: int) -> tuple:
+        """Ciphertext limbs [0, m) followed by the special primes (keys.py:81)."""
+        return tuple(range(m)) + tuple(range(self.lq, self.lq + self.k))
+
+    def all_basis(self) -> tuple:
+        return tuple(range(len(self.all_primes)))
+
+    def cmap(self, basis: tuple):
+        hit = self._maps.get(basis)
+        if hit is None:
+            hit = self._maps[basis] = nat.i32_array(basis)
+        return hit
+
+    # legacy helpers (ctypes maps)
     def q_map(self, m: int):
-        """ctypes int32 map for the first m ciphertext limbs."""
-        key = ("q", m)
-        if key not in self._maps:
-            self._maps[key] = nat.i32_array(range(m))
-        return self._maps[key]
+        return self.cmap(self.q_basis(m))
 
     def ext_map(self, m: int):
-        """Ciphertext limbs [0, m) followed by the special primes (keys.py:81)."""
-        key = ("e", m)
-        if key not in self._maps:
-            self._maps[key] = nat.i32_array(list(range(m)) + list(range(self.lq, self.lq + self.k)))
-        return self._maps[key]
+        return self.cmap(self.ext_basis(m))
 
     def all_map(self):
-        key = ("all",)
-        if key not in self._maps:
-            self._maps[key] = nat.i32_array(range(len(self.all_primes)))
-        return self._maps[key]
+        return self.cmap(self.all_basis())
 
     def custom_map(self, idx: tuple):
-        key = ("c",) + tuple(idx)
-        if key not in self._maps:
-            self._maps[key] = nat.i32_array(idx)
-        return self._maps[key]
+        return self.cmap(tuple(idx))
 
     def scalar_pairs(self, value: int, primes_idx) -> object:
         """{v mod p, shoup} pairs for ckb_scalar_mul / ckb_divround prescale."""
@@ -137,6 +143,37 @@ class GpuChain:
             v = value % p
             vals += [v, shoup(v, p)]
         return nat.u64_array(vals)
+
+    def _drop_chain_table(self, basis: tuple, n_drop: int) -> torch.Tensor:
+        """Mixed-radix constants for dropping the last n_drop limbs of basis
+        (see ckb_divround): per limb j, {M_u mod p_j} for u < n_drop then
+        {M_t^-1 mod p_j} (t = j's drop position, n_drop for kept limbs)."""
+        primes = [self.all_primes[i] for i in basis]
+        limbs = len(primes)
+        drops = [primes[limbs - 1 - u] for u in range(n_drop)]
+        tab = np.zeros((limbs, n_drop + 1, 2), dtype=np.uint64)
+        for j, p in enumerate(primes):
+            pos = limbs - 1 - j
+            t = pos if pos < n_drop else n_drop
+            prod = 1
+            for u in range(n_drop):
+                if u < t:
+                    c = prod % p
+                    tab[j, u] = (c, shoup(c, p))
+                prod *= drops[u]
+            mt = math.prod(drops[:t]) % p
+            inv = pow(mt, -1, p)
+            tab[j, n_drop] = (inv, shoup(inv, p))
+        return torch.from_numpy(tab.reshape(-1)).to(self.device)
+
+    def drop_tables(self, basis: tuple, n1: int, n2: int):
+        key = ("drop", basis, n1, n2)
+        hit = self._maps.get(key)
+        if hit is None:
+            t1 = self._drop_chain_table(basis, n1) if n1 else None
+            t2 = self._drop_chain_table(basis[: len(basis) - n1], n2) if n2 else None
+            hit = self._maps[key] = (t1, t2)
+        return hit
 
     # -- allocation ---------------------------------------------------------------
     def empty(self, *shape) -> torch.Tensor:
@@ -238,21 +275,24 @@ class GpuChain:
 
     def divround(self, x, polys: int, limbs: int, n1: int, n2: int = 0, addend=None,
                  addend_polys: int = 0, addend_period: int = 1, addend_stride: int = None,
-                 prescale=None, in_poly_stride: int = 0, lmap=None, out=None):
+                 prescale=None, in_poly_stride: int = 0, basis: tuple = None, out=None):
+        basis = basis if basis is not None else self.q_basis(limbs)
         m2 = limbs - n1 - n2
         out = out if out is not None else torch.empty(polys, m2, self.n, dtype=U64,
                                                       device=self.device)
         if addend_stride is None:
             addend_stride = addend_polys
+        t1, t2 = self.drop_tables(basis, n1, n2)
         n_add = 0 if addend is None else (polys // addend_period) * addend_polys * (limbs - n1)
         nb = polys * limbs + n_add + polys * m2
         _run("divround", nb * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_divround(self.ring_p, nat.ptr(out), nat.ptr(x), in_poly_stride,
                                  nat.ptr(addend) if addend is not None else None,
                                  addend_polys if addend is not None else 0,
-                                 addend_period, addend_stride, polys, limbs,
-                                 lmap or self.q_map(limbs), n1, n2, prescale,
-                                 nat.stream_handle()), "divround"))
+                                 addend_period, addend_stride, polys, limbs, self.cmap(basis),
+                                 n1, n2, prescale, nat.ptr(t1) if t1 is not None else None,
+                                 nat.ptr(t2) if t2 is not None else None, nat.stream_handle()),
+            "divround"))
         return out
 
     def automorphism(self, x, galois: int, limbs: int, out=None, lmap=None, ginv_items=None,
