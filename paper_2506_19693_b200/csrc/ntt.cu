@@ -4,9 +4,13 @@
 
 using namespace ckb_internal;
 
-#ifndef CKB_NTT_MINB
-#define CKB_NTT_MINB 3  // CTAs per SM the register budget targets (80 regs)
-#endif
+// Two register-round shapes (measured on B200, tools/ntt_micro.py):
+//  * single phase (N <= 4096): radix-16 rounds, one 4096-element limb per CTA,
+//    256 threads at an 80-register budget (3 CTAs/SM);
+//  * two phases (N > 4096): radix-8 rounds, 2048-element tiles, 256 threads at
+//    a 64-register budget (4 CTAs/SM) — 12% faster than radix-16 at N=2^16.
+constexpr int kNttThreads = 256;
+constexpr int kTwoPhaseTile = 2048;
 using ckb::Mod;
 
 namespace {
@@ -73,32 +77,33 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t W, ui
 // r; stages b in (HI-1 .. LO) for the forward, (LO .. HI-1) for the inverse.
 // The twiddle of the butterfly at k is tw[t0(b) + (k >> (bb+1))]: only
 // 1, 2, 4, 8 distinct values per stage, loaded once each.
-template <int S, int HI>
+template <int S, int RB, int HI>
 __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
                                            const uint64_t* __restrict__ tws, uint64_t p,
                                            uint64_t two_p, int gq, int tbase, int w, int last) {
   if constexpr (HI > 0) {
-    constexpr int Q = HI < 4 ? HI : 4;
+    constexpr int E = 1 << RB;  // elements per thread
+    constexpr int Q = HI < RB ? HI : RB;
     constexpr int LO = HI - Q;
-    constexpr int WLO = HI - 4 > 0 ? HI - 4 : 0;
-    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + 4));
-    uint64_t x[16];
+    constexpr int WLO = HI - RB > 0 ? HI - RB : 0;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
+    uint64_t x[E];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    for (int k = 0; k < E; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
       const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
-      uint64_t Wv[8], Wsv[8];
+      uint64_t Wv[E / 2], Wsv[E / 2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i < (8 >> bb)) {
+      for (int i = 0; i < E / 2; ++i) {
+        if (i < ((E / 2) >> bb)) {
           Wv[i] = __ldg(tw + t0 + i);
           Wsv[i] = __ldg(tws + t0 + i);
         }
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < E; ++k) {
         if (k & (1 << bb)) continue;
         const int i = k >> (bb + 1);
         ct_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
@@ -106,40 +111,41 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restri
     }
     if (LO == 0 && last) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < E; ++k) {
         uint64_t X = x[k];
         X = X >= two_p ? X - two_p : X;
         x[k] = X >= p ? X - p : X;
       }
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    fwd_rounds<S, LO>(s, tw, tws, p, two_p, gq, tbase, w, last);
+    fwd_rounds<S, RB, LO>(s, tw, tws, p, two_p, gq, tbase, w, last);
   }
 }
 
-template <int S, int LO>
+template <int S, int RB, int LO>
 __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
                                            const uint64_t* __restrict__ tws, uint64_t p,
                                            uint64_t two_p, uint64_t ninv, uint64_t ninvs,
                                            uint64_t fw, uint64_t fws, int gq, int tbase, int w,
                                            int last) {
   if constexpr (LO < S) {
-    constexpr int Q = (S - LO) < 4 ? (S - LO) : 4;
+    constexpr int E = 1 << RB;
+    constexpr int Q = (S - LO) < RB ? (S - LO) : RB;
     constexpr int HI = LO + Q;
-    constexpr int WLO = LO < S - 4 ? LO : S - 4;
-    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + 4));
-    uint64_t x[16];
+    constexpr int WLO = LO < S - RB ? LO : S - RB;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
+    uint64_t x[E];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    for (int k = 0; k < E; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
       if (b == S - 1 && last) {
         // top stage of the whole transform with N^-1 folded in
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
           const uint64_t X = x[k], Y = x[k | (1 << bb)];
           uint64_t sum = X + Y;
@@ -149,16 +155,16 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restri
         }
       } else {
         const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
-        uint64_t Wv[8], Wsv[8];
+        uint64_t Wv[E / 2], Wsv[E / 2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < (8 >> bb)) {
+        for (int i = 0; i < E / 2; ++i) {
+          if (i < ((E / 2) >> bb)) {
             Wv[i] = __ldg(tw + t0 + i);
             Wsv[i] = __ldg(tws + t0 + i);
           }
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
           const int i = k >> (bb + 1);
           gs_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
@@ -166,16 +172,18 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restri
       }
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    inv_rounds<S, HI>(s, tw, tws, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
+    inv_rounds<S, RB, HI>(s, tw, tws, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
   }
 }
 
-template <int S, bool FWD>
-__global__ void __launch_bounds__(256, CKB_NTT_MINB) k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph,
-                                                      RingDev R, LimbMap lm) {
+template <int S, bool FWD, int RBT>
+__global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
+    k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
   constexpr int G = 1 << S;
+  constexpr int RB = S < RBT ? S : RBT;  // log2 elements per thread
+  constexpr int E = 1 << RB;
   extern __shared__ uint64_t smem[];
   const int N = 1 << R.log_n;
   const int row = ph.row0 + blockIdx.x / ph.tiles_per_row;
@@ -190,73 +198,75 @@ __global__ void __launch_bounds__(256, CKB_NTT_MINB) k_ntt_phase(uint64_t* __res
   const int g0 = tile * C;
   const bool rows_contig = ph.rstride == 1;
 
-  // tile -> smem, 16-byte vectors (pairs adjacent in global memory)
-  for (int q = tid; q < C * G / 2; q += T) {
+  // tile -> smem, 16-byte vectors (pairs adjacent in global memory).  Every
+  // thread moves exactly E/2 pairs (C*G/2 pairs over C*G/E threads); all
+  // loads are issued before the first shared store.
+  auto pair_of = [&](int q, int& g, int& r) -> size_t {
     const int e = 2 * q;
-    int g, r;
-    size_t off;
     if (rows_contig) {
       g = e >> S;
       r = e & (G - 1);
-      off = (size_t)(g0 + g) * ph.gstride + r;
-    } else {
-      r = e / C;
-      g = e - r * C;
-      off = (size_t)r * ph.rstride + g0 + g;
+      return (size_t)(g0 + g) * ph.gstride + r;
     }
-    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(base + off);
-    smem[sidx<S>(g, r)] = v.x;
-    if (rows_contig)
-      smem[sidx<S>(g, r + 1)] = v.y;
-    else
-      smem[sidx<S>(g + 1, r)] = v.y;
+    r = e / C;
+    g = e - r * C;
+    return (size_t)r * ph.rstride + g0 + g;
+  };
+  {
+    ulonglong2 v[E / 2];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      int g, r;
+      v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_of(tid + i * T, g, r)));
+    }
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      int g, r;
+      pair_of(tid + i * T, g, r);
+      smem[sidx<S>(g, r)] = v[i].x;
+      if (rows_contig)
+        smem[sidx<S>(g, r + 1)] = v[i].y;
+      else
+        smem[sidx<S>(g + 1, r)] = v[i].y;
+    }
   }
   __syncthreads();
 
-  const int gq = tid / (G / 16);
-  const int w = tid % (G / 16);
+  const int gq = tid / (G / E);
+  const int w = tid % (G / E);
   const int tbase = ph.M0 + ph.gt * (g0 + gq);
   const uint64_t* tables = R.ntt + (size_t)pi * 4 * N;
   if constexpr (FWD) {
-    fwd_rounds<S, S>(smem, tables, tables + N, p, two_p, gq, tbase, w, ph.last);
+    fwd_rounds<S, RB, S>(smem, tables, tables + N, p, two_p, gq, tbase, w, ph.last);
   } else {
-    inv_rounds<S, 0>(smem, tables + 2 * N, tables + 3 * N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
+    inv_rounds<S, RB, 0>(smem, tables + 2 * N, tables + 3 * N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
                      __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
   }
 
-  for (int q = tid; q < C * G / 2; q += T) {
-    const int e = 2 * q;
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) {
     int g, r;
-    size_t off;
+    const size_t off = pair_of(tid + i * T, g, r);
     ulonglong2 v;
-    if (rows_contig) {
-      g = e >> S;
-      r = e & (G - 1);
-      off = (size_t)(g0 + g) * ph.gstride + r;
-      v.x = smem[sidx<S>(g, r)];
-      v.y = smem[sidx<S>(g, r + 1)];
-    } else {
-      r = e / C;
-      g = e - r * C;
-      off = (size_t)r * ph.rstride + g0 + g;
-      v.x = smem[sidx<S>(g, r)];
-      v.y = smem[sidx<S>(g + 1, r)];
-    }
+    v.x = smem[sidx<S>(g, r)];
+    v.y = rows_contig ? smem[sidx<S>(g, r + 1)] : smem[sidx<S>(g + 1, r)];
     *reinterpret_cast<ulonglong2*>(base + off) = v;
   }
 }
 
-template <bool FWD>
+template <bool FWD, int RBT>
 int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const RingDev& R,
                  const LimbMap& lm, cudaStream_t st) {
   const int G = 1 << S;
-  const int threads = ph.C * G / 16;
+  const int RB = S < RBT ? S : RBT;
+  const int threads = ph.C * G >> RB;
   const size_t smem = (size_t)ph.C * (G + G / 16) * sizeof(uint64_t);
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
+  if (threads > kNttThreads) return CKB_E_LOGN;
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
-    k_ntt_phase<SS, FWD><<<blocks, threads, smem, st>>>(data, ph, R, lm);          \
+    k_ntt_phase<SS, FWD, RBT><<<blocks, threads, smem, st>>>(data, ph, R, lm);     \
     break;
   switch (S) {
     CKB_NTT_CASE(4)
@@ -288,14 +298,14 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   const int N = 1 << logn;
   if (logn <= 12) {
     NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0};
-    int rc = launch_phase<FWD>(logn, data, ph, rows, R, lm, st);
+    int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
     return rc ? rc : finish();
   }
   const int s2 = logn / 2;        // low stages (contiguous rows, phase B)
   const int s1 = logn - s2;       // high stages (strided columns, phase A)
   if (s1 > 12) return CKB_E_LOGN;
   const int GA = 1 << s1, GB = 1 << s2;
-  const int CA = std::max(1, 4096 / GA), CB = std::max(1, 4096 / GB);
+  const int CA = std::max(1, kTwoPhaseTile / GA), CB = std::max(1, kTwoPhaseTile / GB);
   // phase A: groups are the GB columns, elements strided by GB
   NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0};
   // phase B: groups are the GA rows of GB contiguous elements
@@ -308,11 +318,11 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     pb.row0 = r0;
     int rc;
     if (FWD) {
-      rc = launch_phase<FWD>(s1, data, pa, nr, R, lm, st);
-      if (!rc) rc = launch_phase<FWD>(s2, data, pb, nr, R, lm, st);
+      rc = launch_phase<FWD, 3>(s1, data, pa, nr, R, lm, st);
+      if (!rc) rc = launch_phase<FWD, 3>(s2, data, pb, nr, R, lm, st);
     } else {
-      rc = launch_phase<FWD>(s2, data, pb, nr, R, lm, st);
-      if (!rc) rc = launch_phase<FWD>(s1, data, pa, nr, R, lm, st);
+      rc = launch_phase<FWD, 3>(s2, data, pb, nr, R, lm, st);
+      if (!rc) rc = launch_phase<FWD, 3>(s1, data, pa, nr, R, lm, st);
     }
     if (rc) return rc;
   }

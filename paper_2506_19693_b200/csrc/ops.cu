@@ -75,7 +75,8 @@ __global__ void k_tensor(uint64_t* __restrict__ out, const uint64_t* __restrict_
 
 // One thread per (batch, digit, coefficient); writes the digit's value in
 // every extended limb (coalesced across coefficients).
-__global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+template <int AMAX>
+__global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
                         size_t in_bstride, int batch, int limbs, int ext, int alpha, int n_digits, int log_n, RingDev R,
                         LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
   const size_t N = (size_t)1 << log_n;
@@ -90,7 +91,7 @@ __global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__
     uint64_t* dst = out + (bi * n_digits + j) * ext * N + n;
     const int first = j * alpha;
     const int cnt = min(alpha, limbs - first);
-    if (alpha == 1) {
+    if (AMAX == 1) {
       const uint64_t x = src[(size_t)first * N];
       const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * 8);
       for (int e = 0; e < ext; ++e) {
@@ -99,11 +100,11 @@ __global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__
       }
     } else {
       // y_i = [x_i * qhat_i^-1]_{q_i};  out_e = sum_i y_i * [qhat_i]_{p_e}
-      uint64_t y[16];
+      uint64_t y[AMAX];
       const size_t stride_i = 2 + 2 * (size_t)ext;
       const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < AMAX; ++i) {
         if (i < cnt) {
           const uint64_t x = src[(size_t)(first + i) * N];
           const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * 8);
@@ -118,7 +119,7 @@ __global__ void k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__
         const Mod m = load_mod(R, em.p[e]);
         uint64_t acc = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < AMAX; ++i) {
           if (i < cnt) {
             const uint64_t* c = tab + i * stride_i + 2 + 2 * e;
             uint64_t v = ckb::mul_shoup_lazy(y[i], __ldg(c), __ldg(c + 1), m.p);
@@ -188,7 +189,8 @@ __device__ __forceinline__ int64_t centered(uint64_t x, uint64_t p) {
 // divided value at p_u — the same integers, so the output is bit-identical.
 // tab1: [limbs][n1+1][2] {M_u mod p_j, shoup} and {(M_t)^-1 mod p_j or P^-1}
 // tab2: [m1][n2+1][2] likewise for the second chain.
-__global__ void __launch_bounds__(256) k_divround(
+template <int D1, int D2>
+__global__ void __launch_bounds__(256, 2) k_divround(
     uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_stride,
     const uint64_t* __restrict__ addend, int add_polys, int add_period, int add_stride,
     int polys, int limbs, int n1, int n2, int log_n, RingDev R, LimbMap lm, ScalarTab pre,
@@ -215,16 +217,16 @@ __global__ void __launch_bounds__(256) k_divround(
       if (has_pre) v = ckb::mul_shoup(v, pre.v[l], pre.s[l], p);
       return v;
     };
-    int64_t r1[kMaxDrop], r2[kMaxDrop];
+    int64_t r1[D1 > 0 ? D1 : 1], r2[D2 > 0 ? D2 : 1];
 #pragma unroll
-    for (int d = 0; d < kMaxDrop; ++d) {
+    for (int d = 0; d < D1; ++d) {
       if (d < n1) {
         const int li = limbs - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
         const uint64_t* T = tab1 + (size_t)li * s1;
         uint64_t acc = load(li, p);
 #pragma unroll
-        for (int u = 0; u < kMaxDrop; ++u)
+        for (int u = 0; u < D1; ++u)
           if (u < d) acc = sub_rm(acc, r1[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
         acc = ckb::mul_shoup(acc, __ldg(T + 2 * n1), __ldg(T + 2 * n1 + 1), p);
         r1[d] = centered(acc, p);
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(256) k_divround(
       if (n1) {
         const uint64_t* T = tab1 + (size_t)l * s1;
 #pragma unroll
-        for (int u = 0; u < kMaxDrop; ++u)
+        for (int u = 0; u < D1; ++u)
           if (u < n1) v = sub_rm(v, r1[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
         v = ckb::mul_shoup(v, __ldg(T + 2 * n1), __ldg(T + 2 * n1 + 1), p);
       }
@@ -244,14 +246,14 @@ __global__ void __launch_bounds__(256) k_divround(
       return v;
     };
 #pragma unroll
-    for (int d = 0; d < kMaxDrop; ++d) {
+    for (int d = 0; d < D2; ++d) {
       if (d < n2) {
         const int li = m1 - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
         const uint64_t* T = tab2 + (size_t)li * s2;
         uint64_t acc = stage1(li);
 #pragma unroll
-        for (int u = 0; u < kMaxDrop; ++u)
+        for (int u = 0; u < D2; ++u)
           if (u < d) acc = sub_rm(acc, r2[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
         acc = ckb::mul_shoup(acc, __ldg(T + 2 * n2), __ldg(T + 2 * n2 + 1), p);
         r2[d] = centered(acc, p);
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(256) k_divround(
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
         const uint64_t* T = tab2 + (size_t)l * s2;
 #pragma unroll
-        for (int u = 0; u < kMaxDrop; ++u)
+        for (int u = 0; u < D2; ++u)
           if (u < n2) v = sub_rm(v, r2[u], __ldg(T + 2 * u), __ldg(T + 2 * u + 1), p);
         v = ckb::mul_shoup(v, __ldg(T + 2 * n2), __ldg(T + 2 * n2 + 1), p);
       }
@@ -504,7 +506,10 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   const size_t total = ((size_t)batch * nd) << R.log_n;
   if (!total) return 0;
   const size_t bstride = in_batch_stride > 0 ? (size_t)in_batch_stride : ((size_t)limbs << R.log_n);
-  k_modup<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+  const int amax = alpha == 1 ? 1 : alpha <= 2 ? 2 : alpha <= 4 ? 4 : alpha <= 8 ? 8 : 16;
+  auto kern = amax == 1 ? k_modup<1> : amax == 2 ? k_modup<2> : amax == 4 ? k_modup<4>
+            : amax == 8 ? k_modup<8> : k_modup<16>;
+  kern<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       out, in, bstride, batch, limbs, ext_limbs, alpha, nd, (int)R.log_n, R, lm, em, bconv);
   return finish();
 }
@@ -552,11 +557,26 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   const size_t total = (size_t)polys << R.log_n;
   if (!total) return 0;
   const size_t stride = in_poly_stride > 0 ? (size_t)in_poly_stride : ((size_t)limbs << R.log_n);
-  k_divround<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      out, in, stride, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
-      addend ? addend_stride : 0, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, pre,
-      has_pre, tab1, tab2);
-  return finish();
+  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4 : 8;
+  const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define CKB_DR(A, B)                                                                          \
+  if (d1 == A && d2 == B) {                                                                   \
+    k_divround<A, B><<<grid, 256, 0, st>>>(out, in, stride, addend, addend ? addend_polys : 0, \
+                                           addend ? addend_period : 1,                        \
+                                           addend ? addend_stride : 0, polys, limbs, n_drop1,  \
+                                           n_drop2, (int)R.log_n, R, lm, pre, has_pre, tab1,   \
+                                           tab2);                                              \
+    return finish();                                                                           \
+  }
+  CKB_DR(0, 1) CKB_DR(0, 2) CKB_DR(0, 8)
+  CKB_DR(1, 0) CKB_DR(1, 1) CKB_DR(1, 2) CKB_DR(1, 8)
+  CKB_DR(2, 0) CKB_DR(2, 1) CKB_DR(2, 2) CKB_DR(2, 8)
+  CKB_DR(4, 0) CKB_DR(4, 1) CKB_DR(4, 2) CKB_DR(4, 8)
+  CKB_DR(8, 0) CKB_DR(8, 1) CKB_DR(8, 2) CKB_DR(8, 8)
+#undef CKB_DR
+  return CKB_E_ARG;
 }
 
 int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,

@@ -22,21 +22,25 @@ def chain_for(logn, nprimes, bits=40):
 
 res = {}
 for logn, rows, limbs in [(16, 3072, 24), (12, 2304, 9)]:
-    ch = chain_for(logn, limbs)
-    n = 1 << logn
-    x = torch.randint(0, 2**39, (rows, n), dtype=torch.int64, device="cuda").view(U64)
-    ref = x.clone()
-    for _ in range(3):
-        ch.ntt_fwd(x, limbs); ch.ntt_inv(x, limbs)
-    assert torch.equal(x.view(torch.int64), ref.view(torch.int64))
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    reps = 10
-    e[0].record()
-    for _ in range(reps): ch.ntt_fwd(x, limbs)
-    e[1].record()
-    for _ in range(reps): ch.ntt_inv(x, limbs)
-    e[2].record(); torch.cuda.synchronize()
-    f = e[0].elapsed_time(e[1]) / reps; i = e[1].elapsed_time(e[2]) / reps
-    gb = 2 * rows * n * 8 / 1e9
-    res[f"N=2^{logn} rows={rows}"] = {"fwd_ms": f, "inv_ms": i, "fwd_GBps": gb / (f / 1e3), "inv_GBps": gb / (i / 1e3)}
+  try:
+      ch = chain_for(logn, limbs)
+      n = 1 << logn
+
+      x = torch.randint(0, 2**39, (rows, n), dtype=torch.int64, device="cuda").view(U64)
+      ref = x.clone()
+      for _ in range(3):
+          ch.ntt_fwd(x, limbs); ch.ntt_inv(x, limbs)
+      assert torch.equal(x.view(torch.int64), ref.view(torch.int64))
+      e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+      reps = 10
+      e[0].record()
+      for _ in range(reps): ch.ntt_fwd(x, limbs)
+      e[1].record()
+      for _ in range(reps): ch.ntt_inv(x, limbs)
+      e[2].record(); torch.cuda.synchronize()
+      f = e[0].elapsed_time(e[1]) / reps; i = e[1].elapsed_time(e[2]) / reps
+      gb = 2 * rows * n * 8 / 1e9
+      res[f"N=2^{logn} rows={rows}"] = {"fwd_ms": f, "inv_ms": i, "fwd_GBps": gb / (f / 1e3), "inv_GBps": gb / (i / 1e3)}
+  except Exception as exc:
+    res[f"N=2^{logn}"] = {"error": repr(exc)[:80]}
 print(json.dumps({"lib": os.environ.get("CKB_LIB", "default"), **res}))
