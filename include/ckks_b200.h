@@ -135,6 +135,32 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
                  const uint64_t* prescale_host, const uint64_t* tab1, const uint64_t* tab2,
                  void* stream);
 
+/* NTT-domain divide-and-round, step 1 (ring.py:165-189 / keys.py:98-99 /
+ * backend.py:86-92 for ciphertexts kept in the NTT domain): from the
+ * coefficient-domain dropped limbs T build the correction polynomial
+ *   E_j = (sum_u r1_u M1_u) * P1^-1 + sum_u r2_u M2_u  (mod q_j), j < limbs-n_drop1-n_drop2
+ * T per poly: rows [0, n1+n2) = x limbs [limbs-n1-n2, limbs), then (if has_addend)
+ * n2 rows = addend limbs [limbs-n1-n2, limbs-n1); all coefficient domain.
+ * tab1/tab2 as for ckb_divround; tabE: DEVICE [m2][n1+n2][2] {M1_u*P1^-1 mod q_j, shoup}
+ * then {M2_u mod q_j, shoup}.  E: [polys][m2][N], coefficient domain (NTT it next). */
+int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
+                          int polys, int limbs, const int32_t* limb_prime, int n_drop1,
+                          int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
+                          const uint64_t* tabE, void* stream);
+/* NTT-domain divide-and-round, step 2: out_j = (x_j * P1^-1 + add_j - E_j) * P2^-1 with x,
+ * addend and E (after its forward NTT) in the NTT domain; addend addressing as ckb_divround. */
+int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t* x,
+                             int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                             int addend_period, int addend_stride, const uint64_t* E, int polys,
+                             int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
+                             const uint64_t* tab1, const uint64_t* tab2, void* stream);
+/* Galois automorphism on NTT-domain limbs (a permutation of the bit-reversed
+ * evaluation slots; ring.py:222-232 transported to the evaluation domain).
+ * galois_items (DEVICE, one galois per item of rows_per_item rows) or NULL. */
+int ckb_automorphism_ntt(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows,
+                         uint64_t galois, const uint64_t* galois_items, int rows_per_item,
+                         void* stream);
+
 /* Galois automorphism X -> X^galois, coefficient domain (ring.py:211-232).
  * If galois_inv_items (DEVICE, one galois^-1 mod 2N per item of rows_per_item
  * rows) is non-NULL, each item gets its own automorphism (batched rotations). */

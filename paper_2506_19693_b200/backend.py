@@ -9,8 +9,12 @@ keyset_id=None, _secret=None)`` (ckks/backend.py:55-75).  Level, depth and
 keyset checks stay in the shared base class.
 
 Payload: ``GpuCiphertext(data, level)`` — ``data`` is a torch.uint64 CUDA
-tensor [2, limbs(level), N] holding (c0, c1) in the coefficient domain, as the
-reference keeps ciphertexts at rest (backend.py:1-9).  Every integer operation
+tensor [2, limbs(level), N] holding (c0, c1) in the NTT (evaluation) domain.
+The reference keeps ciphertexts in the coefficient domain (backend.py:1-9);
+here they rest in the evaluation domain so multiplies need no forward
+transforms, and the divide-and-round steps (ModDown, rescale) are applied as
+NTT-domain corrections — the same integers, so ``planes_of`` (one inverse
+NTT) is bit-identical to the reference's planes.  Every integer operation
 runs in the sm_100a kernels (ring.py -> _native.py -> libckks_b200.so); the
 host does only what the reference's host does besides arithmetic: numpy
 sampling with the reference's RNG streams (so keys and encryptions are
@@ -50,7 +54,8 @@ MAX_SAFE_COEFF = float(2**52)
 
 @dataclasses.dataclass(frozen=True)
 class GpuCiphertext:
-    """(c0, c1) at one chain level; coefficient domain, canonical residues."""
+    """(c0, c1) at one chain level; NTT domain (bit-reversed evaluation slots of
+    NttPlan.forward), canonical residues."""
 
     data: torch.Tensor  # [2, limbs, N] uint64, CUDA
     level: int
@@ -264,28 +269,22 @@ class B200CkksCore:
         self._bconv_cache[m] = t
         return t
 
-    def _key_switch(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
-                    key: KeySwitchKey = None, key_ptrs=None, addend=None, addend_polys: int = 0,
-                    addend_stride: int = None, n_rescale: int = 0) -> torch.Tensor:
-        """keys.py:74-100 (+ the following add and optional rescale, fused).
-
-        d: batch items of [m, N] (coefficient domain) starting at d, item b at
-        b*d_stride elements (0 = contiguous).  Returns [batch, 2, m - n_rescale, N]."""
+    def _key_switch_acc(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
+                        key: KeySwitchKey = None, key_ptrs=None) -> torch.Tensor:
+        """keys.py:74-97: digits of d (coefficient domain, batch items of [m, N]
+        at b*d_stride), lifted to Q_l u P, NTT, inner product with the key rows.
+        Returns the NTT-domain accumulator [batch, 2, m + k, N]; the division by
+        P (keys.py:98-99) is left to the caller so it can fuse adds/rescales."""
         ch = self.chain
         ext = m + ch.k
-        emap = ch.ext_map(m)
         digits = ch.modup(d, m, self.alpha, self._bconv(m), batch=batch, in_batch_stride=d_stride)
-        ch.ntt_fwd(digits, ext, emap)
-        acc = ch.ks_inner(digits, m, key=key.data if key is not None else None, key_ptrs=key_ptrs)
-        ch.ntt_inv(acc, ext, emap)
-        out = ch.divround(acc, 2 * batch, ext, ch.k, n_rescale, addend=addend,
-                          addend_polys=addend_polys, addend_period=2, addend_stride=addend_stride,
-                          basis=ch.ext_basis(m))
-        return out.view(batch, 2, m - n_rescale, self.n)
+        ch.ntt_fwd(digits, ext, ch.ext_map(m))
+        return ch.ks_inner(digits, m, key=key.data if key is not None else None,
+                           key_ptrs=key_ptrs)
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
-        """backend.py:94-112: restrict to target+1, integer scalar onto the
-        target scale, rescale — one fused ckb_divround launch."""
+        """backend.py:94-112: restrict to target+1 limbs, multiply by the integer
+        that lands the target scale, rescale (NTT domain)."""
         if ct.level == target:
             return ct
         if ct.level < target:
@@ -298,17 +297,22 @@ class B200CkksCore:
             s_star = self._scale(target) * ch.entry_products[staging] / self._scale(ct.level)
             factor = int(np.rint(s_star))
             self._adjust_cache[key] = ch.scalar_pairs(factor, range(ms))
-        pre = self._adjust_cache[key]
-        m_full = ct.data.shape[1]
-        out = ch.divround(ct.data, 2, ms, len(ch.entry_primes[staging]), prescale=pre,
-                          in_poly_stride=m_full * self.n)
+        x = ct.data[:, :ms].contiguous()
+        ch.scalar_mul(x, self._adjust_cache[key], ms, out=x)
+        out = ch.divround_ntt(x, 2, ms, len(ch.entry_primes[staging]))
         return GpuCiphertext(out, target)
 
     def _rescale(self, data: torch.Tensor, level: int) -> GpuCiphertext:
-        """backend.py:86-92: divide-round by entry_primes[level], last first."""
+        """backend.py:86-92: divide-round by entry_primes[level] (NTT domain)."""
         m = self._limbs(level)
-        out = self.chain.divround(data, 2, m, len(self.chain.entry_primes[level]))
+        out = self.chain.divround_ntt(data, 2, m, len(self.chain.entry_primes[level]))
         return GpuCiphertext(out, level - 1)
+
+    def _to_ntt(self, coeff: torch.Tensor) -> torch.Tensor:
+        return self.chain.ntt_fwd(coeff, coeff.shape[-2])
+
+    def _to_coeff(self, data: torch.Tensor) -> torch.Tensor:
+        return self.chain.ntt_inv(data.clone(), data.shape[-2])
 
     def _encode_rns(self, values, level: int, ntt: bool = False) -> torch.Tensor:
         """encode (encoding.py:57-65) -> [limbs, N] residues; cached per value."""
@@ -357,28 +361,32 @@ class B200CkksCore:
         m = self._limbs(in_level)
         if op == "mul":
             pt = self._encode_rns(b.values, in_level, ntt=True)
-            x = ch.ntt_fwd(ct_a.data.clone(), m)
-            ch.mul(x, pt, m, out=x, b_rows=m)
-            ch.ntt_inv(x, m)
+            x = ch.mul(ct_a.data, pt, m, b_rows=m)
             return self._rescale(x, in_level)
-        pt = self._encode_rns(b.values if op == "add" else -b.values, in_level)
+        pt = self._encode_rns(b.values if op == "add" else -b.values, in_level, ntt=True)
         out = ct_a.data.clone()
         ch.add(ct_a.data[0], pt, m, out=out[0])
         return GpuCiphertext(out, in_level)
 
     def _mul_ct(self, ct_a: GpuCiphertext, ct_b: GpuCiphertext, in_level: int) -> GpuCiphertext:
-        """backend.py:136-143: NTT, tensor, relinearise, add, rescale."""
-        ch = self.chain
-        m = self._limbs(in_level)
-        x = torch.empty(2, 2, m, self.n, dtype=U64, device=self.device)
-        x[0].copy_(ct_a.data)
-        x[1].copy_(ct_b.data)
-        ch.ntt_fwd(x, m)
-        d = ch.tensor(x[0], x[1], m)  # [1, 3, m, N]
-        ch.ntt_inv(d, m)
-        out = self._key_switch(d[:, 2], m, key=self.relin_key, addend=d, addend_polys=2,
-                               addend_stride=3, n_rescale=len(ch.entry_primes[in_level]))
+        """backend.py:136-143: tensor, relinearise, add, rescale — NTT domain."""
+        out = self._hmult(ct_a.data.unsqueeze(0), ct_b.data.unsqueeze(0), in_level)
         return GpuCiphertext(out[0], in_level - 1)
+
+    def _hmult(self, a: torch.Tensor, b: torch.Tensor, level: int) -> torch.Tensor:
+        """[B, 2, m, N] x [B, 2, m, N] (NTT) -> [B, 2, m - e, N] (NTT)."""
+        ch = self.chain
+        m = self._limbs(level)
+        bsz = a.shape[0]
+        e = len(ch.entry_primes[level])
+        d = ch.tensor(a, b, m)  # [B, 3, m, N]
+        d2 = ch.ntt_inv(d[:, 2].contiguous(), m)
+        acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key)
+        tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
+        out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, e, addend=d, addend_polys=2,
+                              addend_period=2, addend_stride=3, addend_tail=tail,
+                              basis=ch.ext_basis(m))
+        return out.view(bsz, 2, m - e, self.n)
 
     def _payload_rotate(self, a, k: int):
         ct: GpuCiphertext = a.payload
@@ -388,13 +396,26 @@ class B200CkksCore:
         if galois is None:
             galois = pow(5, k, 2 * self.n)
         key = self.rotation_key(galois)
-        m = self._limbs(ct.level)
-        r = self.chain.automorphism(ct.data, galois, m)
-        out = self._key_switch(r[1], m, key=key, addend=r, addend_polys=1, addend_stride=2)
+        out = self._hrot(ct.data.unsqueeze(0), ct.level, galois=galois, key=key)
         return GpuCiphertext(out[0], ct.level)
 
+    def _hrot(self, a: torch.Tensor, level: int, galois: int = 0, key: KeySwitchKey = None,
+              g_items=None, key_ptrs=None) -> torch.Tensor:
+        """backend.py:155-171 on [B, 2, m, N] NTT-domain ciphertexts: automorphism
+        (a slot permutation in the NTT domain), key switch of c1', add c0'."""
+        ch = self.chain
+        m = self._limbs(level)
+        bsz = a.shape[0]
+        r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
+        c1 = ch.ntt_inv(r[:, 1].contiguous(), m)
+        acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs)
+        out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, 0, addend=r, addend_polys=1,
+                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m))
+        return out.view(bsz, 2, m, self.n)
+
     def _encrypt_values(self, values, level: int) -> GpuCiphertext:
-        """backend.py:173-182: symmetric encryption, RNG (seed, serial)."""
+        """backend.py:173-182: symmetric encryption, RNG (seed, serial); the
+        result c0 = -a*s + NTT(m + e), c1 = a is the NTT form of the reference's."""
         ch = self.chain
         rng = np.random.default_rng((self.rng_seed, next(self._serials)))
         primes = ch.limbs_at(level)
@@ -404,24 +425,23 @@ class B200CkksCore:
         e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
         out = torch.empty(2, m, self.n, dtype=U64, device=self.device)
         out[1].copy_(torch.from_numpy(a_np))
+        me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)[0]
+        ch.add(me, msg, m, out=me)
+        ch.ntt_fwd(me, m)
         ch.mul(out[1], self.sk.s_full[:m], m, out=out[0])
-        ch.neg(out[0], m, out=out[0])
-        ch.ntt_inv(out, m)
-        e = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)[0]
-        ch.add(out[0], msg, m, out=out[0])
-        ch.add(out[0], e, m, out=out[0])
+        ch.sub(me, out[0], m, out=out[0])
         return GpuCiphertext(out, level)
 
     def _payload_encrypt(self, pv, level: int, serial: int):
         return self._encrypt_values(pv.values, level)
 
     def _phase(self, ct: GpuCiphertext) -> torch.Tensor:
+        """c0 + c1*s, coefficient domain."""
         ch = self.chain
         m = ct.data.shape[1]
-        t = ch.ntt_fwd(ct.data[1].clone(), m)
-        ch.mul(t, self.sk.s_full[:m], m, out=t)
-        ch.ntt_inv(t, m)
-        return ch.add(ct.data[0], t, m, out=t)
+        t = ch.mul(ct.data[1], self.sk.s_full[:m], m)
+        ch.add(ct.data[0], t, m, out=t)
+        return ch.ntt_inv(t, m)
 
     def _decrypt_values(self, ct: GpuCiphertext) -> np.ndarray:
         """backend.py:187-190: phase, centered CRT lift, decode."""
@@ -434,7 +454,7 @@ class B200CkksCore:
 
     def _payload_bootstrap(self, cv, serial: int):
         """Custodian refresh (backend.py:195-206): decrypt, optional U(+-eps),
-        re-encrypt at refresh_level.  Real CKKS bootstrapping is bootstrap.py."""
+        re-encrypt at refresh_level."""
         values = self._decrypt_values(cv.payload)
         if self.bootstrap_eps > 0.0:
             values = values + self._bs_rng.uniform(-self.bootstrap_eps, self.bootstrap_eps,
@@ -446,7 +466,7 @@ class B200CkksCore:
         """RBCT (backend.py:210-222): header then c0, c1 coefficient planes, LE u64."""
         ct: GpuCiphertext = cv.payload
         head = struct.pack("<4sIQId", CT_MAGIC, SERIAL_VERSION, self.n, ct.level, cv.scale_bits)
-        body = ct.data.cpu().numpy().astype("<u8").tobytes()
+        body = self._to_coeff(ct.data).cpu().numpy().astype("<u8").tobytes()
         return head + body
 
     def deserialize_cipher(self, blob: bytes):
@@ -469,7 +489,7 @@ class B200CkksCore:
         if len(body) != 2 * m * degree * 8:
             raise E.SerializationError("ciphertext body length mismatch")
         arr = np.frombuffer(body, dtype="<u8").reshape(2, m, degree).astype(np.uint64)
-        data = torch.from_numpy(arr).to(self.device)
+        data = self._to_ntt(torch.from_numpy(arr).to(self.device))
         rl = self.params.refresh_level
         return self._api.CipherVector(
             payload=GpuCiphertext(data, level), level_remaining=level, scale_bits=scale_bits,
@@ -483,19 +503,8 @@ class B200CkksCore:
 
     def batch_hmult(self, a: torch.Tensor, b: torch.Tensor, level: int) -> torch.Tensor:
         """ct x ct multiply + relinearise + rescale of B pairs at one level.
-        a, b: [B, 2, limbs(level), N] -> [B, 2, limbs(level-1), N]."""
-        ch = self.chain
-        m = self._limbs(level)
-        bsz = a.shape[0]
-        xy = torch.empty(2, bsz, 2, m, self.n, dtype=U64, device=self.device)
-        xy[0].copy_(a)
-        xy[1].copy_(b)
-        ch.ntt_fwd(xy, m)
-        d = ch.tensor(xy[0], xy[1], m)
-        ch.ntt_inv(d, m)
-        return self._key_switch(d[:, 2], m, batch=bsz, d_stride=3 * m * self.n,
-                                key=self.relin_key, addend=d, addend_polys=2, addend_stride=3,
-                                n_rescale=len(ch.entry_primes[level]))
+        a, b: [B, 2, limbs(level), N] NTT domain -> [B, 2, limbs(level-1), N]."""
+        return self._hmult(a, b, level)
 
     def _rotation_tables(self, steps):
         key = tuple(int(s) for s in steps)
@@ -505,22 +514,16 @@ class B200CkksCore:
             two_n = 2 * self.n
             gal = [self.galois_for_step.get(s % slots, pow(5, s % slots, two_n)) for s in key]
             keys = [self.rotation_key(g) for g in gal]
-            ginv = torch.tensor([pow(g, -1, two_n) for g in gal], dtype=torch.int64,
-                                device=self.device).view(U64)
+            g_items = torch.tensor(gal, dtype=torch.int64, device=self.device).view(U64)
             ptrs = torch.tensor([k.data.data_ptr() for k in keys], dtype=torch.int64,
                                 device=self.device)
-            cache[key] = (ginv, ptrs, keys)
+            cache[key] = (g_items, ptrs, keys)
         return cache[key]
 
     def batch_hrot(self, a: torch.Tensor, steps, level: int) -> torch.Tensor:
-        """Rotate item i of a [B, 2, limbs, N] batch left by steps[i] (own key each)."""
-        ch = self.chain
-        m = self._limbs(level)
-        bsz = a.shape[0]
-        ginv, ptrs, _ = self._rotation_tables(steps)
-        r = ch.automorphism(a, 0, m, ginv_items=ginv, rows_per_item=2 * m)
-        return self._key_switch(r[:, 1], m, batch=bsz, d_stride=2 * m * self.n, key_ptrs=ptrs,
-                                addend=r, addend_polys=1, addend_stride=2)
+        """Rotate item i of a [B, 2, limbs, N] NTT-domain batch left by steps[i]."""
+        g_items, ptrs, _ = self._rotation_tables(steps)
+        return self._hrot(a, level, g_items=g_items, key_ptrs=ptrs)
 
     def batch_ntt(self, a: torch.Tensor, level: int, inverse: bool = False) -> torch.Tensor:
         """In-place NTT / iNTT of every limb of a [..., limbs(level), N] batch."""
@@ -529,13 +532,13 @@ class B200CkksCore:
 
     # ---------------------------------------------------------------- raw access
     def payload_from_planes(self, planes: np.ndarray, level: int) -> GpuCiphertext:
-        """Wrap host (2, limbs, N) coefficient planes as a payload (tests/bench)."""
-        return GpuCiphertext(torch.from_numpy(np.ascontiguousarray(planes, dtype=np.uint64))
-                             .to(self.device), level)
+        """Wrap host (2, limbs, N) coefficient-domain planes (RBCT order) as a payload."""
+        t = torch.from_numpy(np.ascontiguousarray(planes, dtype=np.uint64)).to(self.device)
+        return GpuCiphertext(self._to_ntt(t), level)
 
-    @staticmethod
-    def planes_of(payload: GpuCiphertext) -> np.ndarray:
-        return payload.data.cpu().numpy()
+    def planes_of(self, payload: GpuCiphertext) -> np.ndarray:
+        """Coefficient-domain (2, limbs, N) planes of a payload (RBCT order)."""
+        return self._to_coeff(payload.data).cpu().numpy()
 
 
 def _hw_secret(n: int, h: int, seed: int) -> np.ndarray:

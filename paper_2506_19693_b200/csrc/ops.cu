@@ -274,6 +274,153 @@ __global__ void __launch_bounds__(256, 2) k_divround(
   }
 }
 
+// ---------------------------------------------------------------------------
+// NTT-domain divide-and-round.  With x (and the addend) in the NTT domain, the
+// exact result (x_j * P1^-1 + add_j - E_j) * P2^-1 needs only the
+// coefficient-domain values of the dropped limbs: the correction polynomial
+//   E_j = (sum_u r1_u M1_u) * P1^-1 + sum_u r2_u M2_u   (mod q_j)
+// is built here from those limbs (T, coefficient domain) and is then
+// transformed with one forward NTT per output limb.
+// T per poly: rows [0, n1+n2) = x limbs [m2, limbs) (coefficient domain),
+//             rows [n1+n2, n1+2*n2) = addend limbs [m2, m1) (coefficient domain).
+// tabE: [m2][n1+n2][2] {M1_u * P1^-1 mod q_j, shoup} then {M2_u mod q_j, shoup}.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t add_rm(uint64_t acc, int64_t r, uint64_t M, uint64_t Ms,
+                                           uint64_t p) {
+  return sub_rm(acc, -r, M, Ms, p);
+}
+
+template <int D1, int D2>
+__global__ void __launch_bounds__(256, 2) k_divround_corr(
+    uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
+    int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
+    const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)polys * N;
+  const int m1 = limbs - n1;
+  const int m2 = m1 - n2;
+  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2);
+  const int trows = n1 + n2 + (has_add ? n2 : 0);
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t pidx = t >> log_n;
+    const uint64_t* src = T + pidx * trows * N + n;
+    int64_t r1[D1 > 0 ? D1 : 1], r2[D2 > 0 ? D2 : 1];
+#pragma unroll
+    for (int d = 0; d < D1; ++d) {
+      if (d < n1) {
+        const int li = limbs - 1 - d;
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t* Tb = tab1 + (size_t)li * s1;
+        uint64_t acc = src[(size_t)(li - m2) * N];
+#pragma unroll
+        for (int u = 0; u < D1; ++u)
+          if (u < d) acc = sub_rm(acc, r1[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), p);
+        acc = ckb::mul_shoup(acc, __ldg(Tb + 2 * n1), __ldg(Tb + 2 * n1 + 1), p);
+        r1[d] = centered(acc, p);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < D2; ++d) {
+      if (d < n2) {
+        const int li = m1 - 1 - d;
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        uint64_t v = src[(size_t)(li - m2) * N];
+        if (n1) {
+          const uint64_t* Ta = tab1 + (size_t)li * s1;
+#pragma unroll
+          for (int u = 0; u < D1; ++u)
+            if (u < n1) v = sub_rm(v, r1[u], __ldg(Ta + 2 * u), __ldg(Ta + 2 * u + 1), p);
+          v = ckb::mul_shoup(v, __ldg(Ta + 2 * n1), __ldg(Ta + 2 * n1 + 1), p);
+        }
+        if (has_add) v = ckb::add_mod(v, src[(size_t)(n1 + n2 + li - m2) * N], p);
+        const uint64_t* Tb = tab2 + (size_t)li * s2;
+#pragma unroll
+        for (int u = 0; u < D2; ++u)
+          if (u < d) v = sub_rm(v, r2[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), p);
+        v = ckb::mul_shoup(v, __ldg(Tb + 2 * n2), __ldg(Tb + 2 * n2 + 1), p);
+        r2[d] = centered(v, p);
+      }
+    }
+    uint64_t* dst = E + pidx * m2 * N + n;
+    for (int j = 0; j < m2; ++j) {
+      const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * 8);
+      const uint64_t* Te = tabE + (size_t)j * sE;
+      uint64_t e = 0;
+#pragma unroll
+      for (int u = 0; u < D1; ++u)
+        if (u < n1) e = add_rm(e, r1[u], __ldg(Te + 2 * u), __ldg(Te + 2 * u + 1), p);
+#pragma unroll
+      for (int u = 0; u < D2; ++u)
+        if (u < n2)
+          e = add_rm(e, r2[u], __ldg(Te + 2 * (n1 + u)), __ldg(Te + 2 * (n1 + u) + 1), p);
+      dst[(size_t)j * N] = e;
+    }
+  }
+}
+
+// out_j = (x_j * P1^-1 + add_j - E_j) * P2^-1, all in the NTT domain.
+__global__ void k_divround_combine(uint64_t* __restrict__ out, const uint64_t* __restrict__ x,
+                                   size_t x_stride, const uint64_t* __restrict__ addend,
+                                   int add_polys, int add_period, int add_stride,
+                                   const uint64_t* __restrict__ E, int polys, int limbs, int n1,
+                                   int n2, int log_n, RingDev R, LimbMap lm,
+                                   const uint64_t* __restrict__ tab1,
+                                   const uint64_t* __restrict__ tab2) {
+  const size_t N = (size_t)1 << log_n;
+  const int m1 = limbs - n1;
+  const int m2 = m1 - n2;
+  const size_t total = (size_t)polys * m2 * N;
+  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1);
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t pj = t >> log_n;
+    const int j = (int)(pj % m2);
+    const size_t pidx = pj / m2;
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * 8);
+    uint64_t v = x[pidx * x_stride + (size_t)j * N + n];
+    if (n1) {
+      const uint64_t* Ta = tab1 + (size_t)j * s1 + 2 * n1;
+      v = ckb::mul_shoup(v, __ldg(Ta), __ldg(Ta + 1), p);
+    }
+    if (addend) {
+      const size_t ph = pidx % add_period;
+      if ((int)ph < add_polys)
+        v = ckb::add_mod(
+            v, addend[((pidx / add_period) * add_stride + ph) * m1 * N + (size_t)j * N + n], p);
+    }
+    v = ckb::sub_mod(v, E[t], p);
+    if (n2) {
+      const uint64_t* Tb = tab2 + (size_t)j * s2 + 2 * n2;
+      v = ckb::mul_shoup(v, __ldg(Tb), __ldg(Tb + 1), p);
+    }
+    out[t] = v;
+  }
+}
+
+// NTT-domain automorphism: slot i of the bit-reversed NTT holds the value at
+// psi^(2 brv(i) + 1), and (X -> X^g) maps it to psi^((2 brv(i) + 1) g), so
+// out[i] = in[brv(((2 brv(i) + 1) g mod 2N - 1) / 2)] — a pure permutation.
+__global__ void k_automorphism_ntt(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                                   size_t total, int log_n, uint64_t g0,
+                                   const uint64_t* __restrict__ g_items, int rows_per_item) {
+  const uint64_t N = 1ull << log_n;
+  const uint64_t mask2 = 2 * N - 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i >> log_n;
+    const uint32_t t = (uint32_t)(i & (N - 1));
+    const uint64_t g = g_items ? __ldg(g_items + row / rows_per_item) : g0;
+    const uint32_t bt = __brev(t) >> (32 - log_n);
+    const uint64_t e = ((2ull * bt + 1) * g) & mask2;
+    const uint32_t src = __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
+    out[i] = in[row * N + src];
+  }
+}
+
 // ===========================================================================
 // Automorphism and conversions
 // ===========================================================================
@@ -619,6 +766,77 @@ int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys,
   if (!total) return 0;
   k_to_f64<<<grid_for(total, 128), 128, 0, (cudaStream_t)stream>>>(out, in, polys, limbs,
                                                                     (int)R.log_n, R, lm);
+  return finish();
+}
+
+int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
+                          int polys, int limbs, const int32_t* limb_prime, int n_drop1,
+                          int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
+                          const uint64_t* tabE, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
+  if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 > kMaxDrop || n_drop2 > kMaxDrop ||
+      n_drop1 + n_drop2 >= limbs || n_drop1 + n_drop2 == 0 || polys < 0 || !tabE)
+    return CKB_E_ARG;
+  if ((n_drop1 && !tab1) || (n_drop2 && !tab2)) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)polys << R.log_n;
+  if (!total) return 0;
+  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4 : 8;
+  const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define CKB_DC(A, B)                                                                        \
+  if (d1 == A && d2 == B) {                                                                 \
+    k_divround_corr<A, B><<<grid, 256, 0, st>>>(E, T, has_addend, polys, limbs, n_drop1,    \
+                                                n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
+                                                tabE);                                      \
+    return finish();                                                                        \
+  }
+  CKB_DC(0, 1) CKB_DC(0, 2) CKB_DC(0, 8)
+  CKB_DC(1, 0) CKB_DC(1, 1) CKB_DC(1, 2) CKB_DC(1, 8)
+  CKB_DC(2, 0) CKB_DC(2, 1) CKB_DC(2, 2) CKB_DC(2, 8)
+  CKB_DC(4, 0) CKB_DC(4, 1) CKB_DC(4, 2) CKB_DC(4, 8)
+  CKB_DC(8, 0) CKB_DC(8, 1) CKB_DC(8, 2) CKB_DC(8, 8)
+#undef CKB_DC
+  return CKB_E_ARG;
+}
+
+int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t* x,
+                             int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                             int addend_period, int addend_stride, const uint64_t* E, int polys,
+                             int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
+                             const uint64_t* tab1, const uint64_t* tab2, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
+  if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 + n_drop2 >= limbs || polys < 0 || !E)
+    return CKB_E_ARG;
+  if ((n_drop1 && !tab1) || (n_drop2 && !tab2)) return CKB_E_ARG;
+  if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period ||
+                 addend_stride < addend_polys))
+    return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const int m2 = limbs - n_drop1 - n_drop2;
+  const size_t total = ((size_t)polys * m2) << R.log_n;
+  if (!total) return 0;
+  const size_t xs = x_poly_stride > 0 ? (size_t)x_poly_stride : ((size_t)limbs << R.log_n);
+  k_divround_combine<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, x, xs, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
+      addend ? addend_stride : 0, E, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1,
+      tab2);
+  return finish();
+}
+
+int ckb_automorphism_ntt(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows,
+                         uint64_t galois, const uint64_t* galois_items, int rows_per_item,
+                         void* stream) {
+  if (rows < 0) return CKB_E_ARG;
+  if (galois_items ? rows_per_item < 1 : (galois & 1) == 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)rows << R.log_n;
+  if (!total) return 0;
+  k_automorphism_ntt<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, in, total, (int)R.log_n, galois, galois_items, rows_per_item);
   return finish();
 }
 

@@ -295,6 +295,94 @@ class GpuChain:
             "divround"))
         return out
 
+    def _corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
+        """tabE for ckb_divround_ntt_corr: per output limb j, {M1_u * P1^-1 mod q_j}
+        for u < n1 then {M2_u mod q_j} for u < n2."""
+        primes = [self.all_primes[i] for i in basis]
+        limbs = len(primes)
+        m1 = limbs - n1
+        m2 = m1 - n2
+        d1 = [primes[limbs - 1 - u] for u in range(n1)]
+        d2 = [primes[m1 - 1 - u] for u in range(n2)]
+        P1 = math.prod(d1)
+        tab = np.zeros((m2, max(1, n1 + n2), 2), dtype=np.uint64)
+        for j in range(m2):
+            p = primes[j]
+            p1inv = pow(P1 % p, -1, p)
+            for u in range(n1):
+                c = math.prod(d1[:u]) % p * p1inv % p
+                tab[j, u] = (c, shoup(c, p))
+            for u in range(n2):
+                c = math.prod(d2[:u]) % p
+                tab[j, n1 + u] = (c, shoup(c, p))
+        return torch.from_numpy(tab.reshape(-1)).to(self.device)
+
+    def corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
+        key = ("corr", basis, n1, n2)
+        hit = self._maps.get(key)
+        if hit is None:
+            hit = self._maps[key] = self._corr_table(basis, n1, n2)
+        return hit
+
+    def divround_ntt(self, x, polys: int, limbs: int, n1: int, n2: int = 0, *,
+                     x_poly_stride: int = 0, addend=None, addend_polys: int = 0,
+                     addend_period: int = 1, addend_stride: int = None, addend_tail=None,
+                     basis: tuple = None, out=None):
+        """Exact divide-and-round of NTT-domain polys (see ckb_divround_ntt_corr):
+        iNTT of the dropped limbs, correction polynomial, its NTT, combine.
+        addend_tail: [polys, n2, N] NTT-domain copy of the addend's limbs
+        [limbs-n1-n2, limbs-n1) (zeros for polys without an addend) when n2 > 0."""
+        basis = basis if basis is not None else self.q_basis(limbs)
+        n = self.n
+        m1 = limbs - n1
+        m2 = m1 - n2
+        xs = x_poly_stride if x_poly_stride else limbs * n
+        if addend_stride is None:
+            addend_stride = addend_polys
+        has_add = addend is not None and n2 > 0
+        trows = n1 + n2 + (n2 if has_add else 0)
+        T = torch.empty(polys, trows, n, dtype=U64, device=self.device)
+        xv = x.as_strided((polys, n1 + n2, n), (xs, n, 1), x.storage_offset() + m2 * n)
+        T[:, : n1 + n2].copy_(xv)
+        if has_add:
+            T[:, n1 + n2:].copy_(addend_tail)
+        tbasis = tuple(basis[m2:]) + (tuple(basis[m2:m1]) if has_add else ())
+        self.ntt_inv(T, trows, self.cmap(tbasis))
+        t1, t2 = self.drop_tables(basis, n1, n2)
+        tE = self.corr_table(basis, n1, n2)
+        E = torch.empty(polys, m2, n, dtype=U64, device=self.device)
+        nb = polys * trows + polys * m2
+        _run("divround_corr", nb * n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_divround_ntt_corr(self.ring_p, nat.ptr(E), nat.ptr(T), int(has_add), polys,
+                                          limbs, self.cmap(basis), n1, n2,
+                                          nat.ptr(t1) if t1 is not None else None,
+                                          nat.ptr(t2) if t2 is not None else None, nat.ptr(tE),
+                                          nat.stream_handle()), "divround_ntt_corr"))
+        self.ntt_fwd(E, m2, self.cmap(tuple(basis[:m2])))
+        out = out if out is not None else torch.empty(polys, m2, n, dtype=U64, device=self.device)
+        n_add = 0 if addend is None else (polys // addend_period) * addend_polys * m2
+        nb = polys * m2 * 3 + n_add
+        _run("divround_combine", nb * n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_divround_ntt_combine(self.ring_p, nat.ptr(out), nat.ptr(x), xs,
+                                             nat.ptr(addend) if addend is not None else None,
+                                             addend_polys if addend is not None else 0,
+                                             addend_period, addend_stride, nat.ptr(E), polys,
+                                             limbs, self.cmap(basis), n1, n2,
+                                             nat.ptr(t1) if t1 is not None else None,
+                                             nat.ptr(t2) if t2 is not None else None,
+                                             nat.stream_handle()), "divround_ntt_combine"))
+        return out
+
+    def automorphism_ntt(self, x, galois: int, out=None, g_items=None, rows_per_item: int = 0):
+        out = out if out is not None else torch.empty_like(x)
+        rows = x.numel() >> self.log_n
+        _run("automorphism", 2 * rows * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_automorphism_ntt(self.ring_p, nat.ptr(out), nat.ptr(x), rows, galois,
+                                         nat.ptr(g_items) if g_items is not None else None,
+                                         rows_per_item, nat.stream_handle()),
+            "automorphism_ntt"))
+        return out
+
     def automorphism(self, x, galois: int, limbs: int, out=None, lmap=None, ginv_items=None,
                      rows_per_item: int = 0):
         """X -> X^galois per row; with ginv_items (device u64 [items]) each item of
