@@ -297,8 +297,9 @@ class B200CkksCore:
             s_star = self._scale(target) * ch.entry_products[staging] / self._scale(ct.level)
             factor = int(np.rint(s_star))
             self._adjust_cache[key] = ch.scalar_pairs(factor, range(ms))
-        x = ct.data[:, :ms].contiguous()
-        ch.scalar_mul(x, self._adjust_cache[key], ms, out=x)
+        # out-of-place: payloads are immutable (api.py:51-65), never scale in place
+        src = ct.data if ms == ct.data.shape[1] else ct.data[:, :ms].contiguous()
+        x = ch.scalar_mul(src, self._adjust_cache[key], ms)
         out = ch.divround_ntt(x, 2, ms, len(ch.entry_primes[staging]))
         return GpuCiphertext(out, target)
 

@@ -280,6 +280,9 @@ def test_mode_b_ops_bit_exact_vs_oracle(dnum):
     ]
     for cv, oct_ in checks:
         assert np.array_equal(be.planes_of(cv.payload), O.ct_to_u64(oct_, orc.chain))
+    # inputs are never modified by an op (CipherVector immutability, api.py:51-65)
+    assert np.array_equal(be.planes_of(a.payload), planes[0])
+    assert np.array_equal(be.planes_of(b.payload), planes[1])
 
 
 # ---------------------------------------------------------------------------
