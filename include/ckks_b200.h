@@ -37,8 +37,8 @@ extern "C" {
 #define CKB_E_LOGN (-3)
 
 /* Device-resident tables for one ring degree and one prime chain.
- *   mods : [n_primes][8]  {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
- *                          psi_inv_brv[1]*N^-1, shoup(.)}
+ *   mods : [n_primes][16] {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
+ *                          psi_inv_brv[1]*N^-1, shoup(.), 2^64 mod p, shoup(.), 0...}
  *   ntt  : [n_primes][4][N] {psi_brv, shoup(psi_brv), inv_psi_brv, shoup(inv_psi_brv)}
  *   pair : [n_primes][n_primes][4] {p_i^-1 mod p_j, shoup(.), p_i mod p_j, 0}
  * Built on the host by ckb_build_tables, uploaded by the caller. */
@@ -95,21 +95,27 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
  * equal limb_prime).  alpha == 1 reproduces the reference's centered per-limb
  * digits exactly; alpha > 1 is the standard fast basis conversion using
  * bconv (device table [digits][alpha][2 + 2*ext_limbs]; see backend.py docs).
- * out: [batch][digits][ext_limbs][N], coefficient domain. */
+ * out: [batch][digits][ext_limbs][N], coefficient domain.  With skip_own (requires
+ * limbs % alpha == 0) a digit's own limbs are not written and each digit has
+ * ext_limbs - alpha rows (the ext basis without its own limbs): their NTT is the
+ * NTT-domain input itself, which ckb_ks_inner reads directly. */
 int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
-              int batch, int limbs,
-              const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
-              const uint64_t* bconv, void* stream);
+              int batch, int limbs, const int32_t* limb_prime, int ext_limbs,
+              const int32_t* ext_prime, int alpha, const uint64_t* bconv, int skip_own,
+              void* stream);
 
 /* Key-switch inner product in the NTT domain (keys.py:91-97):
  *   acc[b][c][e] = sum_j digits[b][j][e] * key_b[j][c][key_limb[e]]
- * digits: [batch][n_digits][ext_limbs][N]; acc: [batch][2][ext_limbs][N].
- * key_ptrs: DEVICE array of `batch` pointers to keys laid out
- * [key_rows][2][key_limbs][N]; if NULL, `key` is used for every batch item. */
+ * digits: [batch][n_digits][rows][N] with rows = ext_limbs, or (own != NULL)
+ * ext_limbs - alpha rows as written by ckb_modup(skip_own), the own limbs then
+ * read from `own` ([limbs][N] per item at b*own_batch_stride, NTT domain).
+ * acc: [batch][2][ext_limbs][N].  key_ptrs: DEVICE array of `batch` pointers to
+ * keys laid out [key_rows][2][key_limbs][N]; if NULL, `key` is used for every item. */
 int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
-                 int n_digits, int ext_limbs, const int32_t* ext_prime,
-                 const uint64_t* key, const uint64_t* const* key_ptrs, int key_limbs,
-                 const int32_t* key_limb, void* stream);
+                 int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
+                 const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                 const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                 void* stream);
 
 /* Exact divide-and-round chain (ring.py:165-189, keys.py:98-99, backend.py:86-112):
  *   x <- x * prescale[limb]              (optional; level adjust, backend.py:108-111)
@@ -141,8 +147,9 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
  *   E_j = (sum_u r1_u M1_u) * P1^-1 + sum_u r2_u M2_u  (mod q_j), j < limbs-n_drop1-n_drop2
  * T per poly: rows [0, n1+n2) = x limbs [limbs-n1-n2, limbs), then (if has_addend)
  * n2 rows = addend limbs [limbs-n1-n2, limbs-n1); all coefficient domain.
- * tab1/tab2 as for ckb_divround; tabE: DEVICE [m2][n1+n2][2] {M1_u*P1^-1 mod q_j, shoup}
- * then {M2_u mod q_j, shoup}.  E: [polys][m2][N], coefficient domain (NTT it next). */
+ * tab1/tab2 as for ckb_divround; tabE: DEVICE [m2][n1+n2+1][2] {M1_u*P1^-1 mod q_j, shoup},
+ * then {M2_u mod q_j, shoup}, then {C_j, 0} with C_j a multiple of q_j in [2^61, 2^62).
+ * E: [polys][m2][N], coefficient domain (NTT it next). */
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
                           int n_drop2, const uint64_t* tab1, const uint64_t* tab2,

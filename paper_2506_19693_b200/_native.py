@@ -51,9 +51,11 @@ def _load():
         "ckb_tensor": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp],
                        ctypes.c_int),
         "ckb_modup": ([R, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, c_i32p,
-                       ctypes.c_int, c_i32p, ctypes.c_int, c_vp, c_vp], ctypes.c_int),
-        "ckb_ks_inner": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, c_vp,
-                          c_vp, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+                       ctypes.c_int, c_i32p, ctypes.c_int, c_vp, ctypes.c_int, c_vp],
+                      ctypes.c_int),
+        "ckb_ks_inner": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p,
+                          ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int64, c_vp, c_vp,
+                          ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_divround": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, ctypes.c_int,
                           ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int,
                           ctypes.c_int, c_u64p, c_vp, c_vp, c_vp],
@@ -98,7 +100,7 @@ def build_tables(log_n: int, primes) -> tuple:
     n = 1 << log_n
     np_ = len(primes)
     pr = np.ascontiguousarray(np.array(primes, dtype=np.uint64))
-    mods = np.zeros((np_, 8), dtype=np.uint64)
+    mods = np.zeros((np_, 16), dtype=np.uint64)
     ntt = np.zeros((np_, 4, n), dtype=np.uint64)
     pair = np.zeros((np_, np_, 4), dtype=np.uint64)
     rc = LIB.ckb_build_tables(log_n, pr.ctypes.data_as(c_u64p), np_, mods.ctypes.data_as(c_u64p),

@@ -270,17 +270,24 @@ class B200CkksCore:
         return t
 
     def _key_switch_acc(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
-                        key: KeySwitchKey = None, key_ptrs=None) -> torch.Tensor:
+                        key: KeySwitchKey = None, key_ptrs=None, own: torch.Tensor = None,
+                        own_stride: int = 0) -> torch.Tensor:
         """keys.py:74-97: digits of d (coefficient domain, batch items of [m, N]
         at b*d_stride), lifted to Q_l u P, NTT, inner product with the key rows.
-        Returns the NTT-domain accumulator [batch, 2, m + k, N]; the division by
-        P (keys.py:98-99) is left to the caller so it can fuse adds/rescales."""
+        ``own`` is the NTT form of d (items at b*own_stride): a digit's own
+        limbs are then not re-transformed but read from it.  Returns the
+        NTT-domain accumulator [batch, 2, m + k, N]; the division by P
+        (keys.py:98-99) is left to the caller so it can fuse adds/rescales."""
         ch = self.chain
-        ext = m + ch.k
-        digits = ch.modup(d, m, self.alpha, self._bconv(m), batch=batch, in_batch_stride=d_stride)
-        ch.ntt_fwd(digits, ext, ch.ext_map(m))
-        return ch.ks_inner(digits, m, key=key.data if key is not None else None,
-                           key_ptrs=key_ptrs)
+        a = self.alpha
+        nd = -(-m // a)
+        skip = own is not None and m % a == 0 and nd * (m + ch.k - a) <= 128
+        digits = ch.modup(d, m, a, self._bconv(m), batch=batch, in_batch_stride=d_stride,
+                          skip_own=skip)
+        basis = ch.digit_basis(m, a, skip)
+        ch.ntt_fwd(digits, len(basis), ch.cmap(basis))
+        return ch.ks_inner(digits, m, a, key=key.data if key is not None else None,
+                           key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride)
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
         """backend.py:94-112: restrict to target+1 limbs, multiply by the integer
@@ -382,7 +389,8 @@ class B200CkksCore:
         e = len(ch.entry_primes[level])
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
         d2 = ch.ntt_inv(d[:, 2].contiguous(), m)
-        acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key)
+        acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key, own=d[:, 2],
+                                   own_stride=3 * m * self.n)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
         out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, e, addend=d, addend_polys=2,
                               addend_period=2, addend_stride=3, addend_tail=tail,
@@ -409,7 +417,8 @@ class B200CkksCore:
         bsz = a.shape[0]
         r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
         c1 = ch.ntt_inv(r[:, 1].contiguous(), m)
-        acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs)
+        acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
+                                   own_stride=2 * m * self.n)
         out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, 0, addend=r, addend_polys=1,
                               addend_period=2, addend_stride=2, basis=ch.ext_basis(m))
         return out.view(bsz, 2, m, self.n)

@@ -19,13 +19,14 @@ using ckb::Mod;
 namespace ckb_internal {
 
 constexpr int kMaxLimbs = CKB_MAX_LIMBS;
+constexpr int kModStride = 16;  // u64 per prime in ckb_ring.mods
 
 struct LimbMap {
   int16_t p[kMaxLimbs];
 };
 
 struct RingDev {
-  const uint64_t* mods;  // [np][8]
+  const uint64_t* mods;  // [np][16]
   const uint64_t* ntt;   // [np][4][N]
   const uint64_t* pair;  // [np][np][4]
   uint32_t log_n;
@@ -33,7 +34,7 @@ struct RingDev {
 };
 
 __device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
-  const uint64_t* m = R.mods + (size_t)pi * 8;
+  const uint64_t* m = R.mods + (size_t)pi * kModStride;
   Mod r;
   r.p = __ldg(m + 0);
   r.mu = __ldg(m + 1);

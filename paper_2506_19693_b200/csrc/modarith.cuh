@@ -79,12 +79,39 @@ CKB_HD uint64_t mul_mod(uint64_t a, uint64_t b, const Mod& m) {
   return barrett_reduce128(mulhi(a, b), a * b, m);
 }
 
+// x mod p for x < 16p (p < 2^60): four conditional subtractions.
+CKB_HD uint64_t reduce_16p(uint64_t x, uint64_t p) {
+  x = x >= 8 * p ? x - 8 * p : x;
+  x = x >= 4 * p ? x - 4 * p : x;
+  x = x >= 2 * p ? x - 2 * p : x;
+  return x >= p ? x - p : x;
+}
+
+// (hi, lo) += a * b, 128-bit multiply-accumulate.
+CKB_HD void mac128(uint64_t& hi, uint64_t& lo, uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\tmadc.hi.u64 %1, %2, %3, %1;"
+      : "+l"(lo), "+l"(hi)
+      : "l"(a), "l"(b));
+#else
+  unsigned __int128 acc = ((unsigned __int128)hi << 64) | lo;
+  acc += (unsigned __int128)a * b;
+  hi = (uint64_t)(acc >> 64);
+  lo = (uint64_t)acc;
+#endif
+}
+
 // x mod p for an arbitrary 64-bit x.
 CKB_HD uint64_t reduce64(uint64_t x, const Mod& m) {
   if (x < m.p) return x;
   if (m.k >= 32) return barrett_reduce128(0, x, m);
   return x % m.p;
 }
+
+// (hi * 2^64 + lo) mod p for any 128-bit value, given r64 = 2^64 mod p and
+// its Shoup companion.
+CKB_HD uint64_t reduce128_any(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r64s,
+                              const Mod& m);
 
 // Centered residue of x (canonical mod q) reduced into prime m:
 // value v = x if x <= q/2 else x - q  (reference: ring.py:341-342, keys.py:85-86),
@@ -95,6 +122,12 @@ CKB_HD uint64_t centered_into(uint64_t x, uint64_t q, const Mod& m) {
     return mag == 0 ? 0 : m.p - mag;
   }
   return reduce64(x, m);
+}
+
+CKB_HD uint64_t reduce128_any(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r64s,
+                              const Mod& m) {
+  const uint64_t h = mul_shoup(hi, r64, r64s, m.p);
+  return add_mod(h, reduce64(lo, m), m.p);
 }
 
 // ---- host-only helpers for table construction -----------------------------

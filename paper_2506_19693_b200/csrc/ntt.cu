@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int row = ph.row0 + blockIdx.x / ph.tiles_per_row;
   const int tile = blockIdx.x % ph.tiles_per_row;
   const int pi = lm.p[row % ph.limbs];
-  const uint64_t* mm = R.mods + (size_t)pi * 8;
+  const uint64_t* mm = R.mods + (size_t)pi * kModStride;
   const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
   uint64_t* base = data + (size_t)row * N;
   const int C = ph.C;

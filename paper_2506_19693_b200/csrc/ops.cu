@@ -44,7 +44,7 @@ __global__ void k_scalar_mul(uint64_t* __restrict__ out, const uint64_t* __restr
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int l = (int)(i >> log_n) % limbs;
-    const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * kModStride);
     out[i] = ckb::mul_shoup(a[i], sc.v[l], sc.s[l], p);
   }
 }
@@ -75,68 +75,92 @@ __global__ void k_tensor(uint64_t* __restrict__ out, const uint64_t* __restrict_
 
 // One thread per (batch, digit, coefficient); writes the digit's value in
 // every extended limb (coalesced across coefficients).
+// Digit j of item b covers limbs [j*alpha, j*alpha + cnt).  With skip_own the
+// digit's own limbs are not written (their NTT is already the input's NTT, read
+// directly by k_ks_inner) and each digit has ext - alpha output rows, ordered
+// as the ext basis without the own limbs.
+__device__ __forceinline__ int digit_row(int e, int first, int cnt, int skip_own) {
+  return skip_own ? (e < first ? e : e - cnt) : e;
+}
+
+// One CTA = one digit (blockIdx.y) over a range of (item, coefficient); the
+// digit's conversion constants are staged in shared memory.
 template <int AMAX>
-__global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
-                        size_t in_bstride, int batch, int limbs, int ext, int alpha, int n_digits, int log_n, RingDev R,
-                        LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
+__global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
+                                                const uint64_t* __restrict__ in, size_t in_bstride,
+                                                int batch, int limbs, int ext, int alpha,
+                                                int n_digits, int out_rows, int skip_own,
+                                                int log_n, RingDev R, LimbMap lm, LimbMap em,
+                                                const uint64_t* __restrict__ bconv) {
+  extern __shared__ uint64_t ctab[];
   const size_t N = (size_t)1 << log_n;
-  const size_t total = (size_t)batch * n_digits * N;
+  const int j = blockIdx.y;
+  const int first = j * alpha;
+  const int cnt = min(alpha, limbs - first);
+  const size_t stride_i = 2 + 2 * (size_t)ext;
+  if (AMAX > 1) {
+    const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
+    for (int q = threadIdx.x; q < cnt * (int)stride_i; q += blockDim.x) ctab[q] = __ldg(tab + q);
+    __syncthreads();
+  }
+  const size_t total = (size_t)batch * N;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t n = t & (N - 1);
-    const size_t bj = t >> log_n;
-    const int j = (int)(bj % n_digits);
-    const size_t bi = bj / n_digits;
+    const size_t bi = t >> log_n;
     const uint64_t* src = in + bi * in_bstride + n;
-    uint64_t* dst = out + (bi * n_digits + j) * ext * N + n;
-    const int first = j * alpha;
-    const int cnt = min(alpha, limbs - first);
+    uint64_t* dst = out + (bi * n_digits + j) * (size_t)out_rows * N + n;
     if (AMAX == 1) {
       const uint64_t x = src[(size_t)first * N];
-      const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * 8);
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * kModStride);
       for (int e = 0; e < ext; ++e) {
+        if (e == first) {
+          if (!skip_own) dst[(size_t)e * N] = x;
+          continue;
+        }
         const Mod m = load_mod(R, em.p[e]);
-        dst[(size_t)e * N] = (e == first) ? x : ckb::centered_into(x, q, m);
+        dst[(size_t)digit_row(e, first, 1, skip_own) * N] = ckb::centered_into(x, q, m);
       }
     } else {
       // y_i = [x_i * qhat_i^-1]_{q_i};  out_e = sum_i y_i * [qhat_i]_{p_e}
       uint64_t y[AMAX];
-      const size_t stride_i = 2 + 2 * (size_t)ext;
-      const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
 #pragma unroll
       for (int i = 0; i < AMAX; ++i) {
         if (i < cnt) {
           const uint64_t x = src[(size_t)(first + i) * N];
-          const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * 8);
-          y[i] = ckb::mul_shoup(x, __ldg(tab + i * stride_i), __ldg(tab + i * stride_i + 1), q);
+          const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * kModStride);
+          y[i] = ckb::mul_shoup(x, ctab[i * stride_i], ctab[i * stride_i + 1], q);
         }
       }
       for (int e = 0; e < ext; ++e) {
         if (e >= first && e < first + cnt) {
-          dst[(size_t)e * N] = src[(size_t)e * N];
+          if (!skip_own) dst[(size_t)e * N] = src[(size_t)e * N];
           continue;
         }
-        const Mod m = load_mod(R, em.p[e]);
+        const uint64_t p = __ldg(R.mods + (size_t)em.p[e] * kModStride);
         uint64_t acc = 0;
 #pragma unroll
         for (int i = 0; i < AMAX; ++i) {
           if (i < cnt) {
-            const uint64_t* c = tab + i * stride_i + 2 + 2 * e;
-            uint64_t v = ckb::mul_shoup_lazy(y[i], __ldg(c), __ldg(c + 1), m.p);
-            acc += v;
-            acc = acc >= m.two_p ? acc - m.two_p : acc;
+            const uint64_t* c = ctab + i * stride_i + 2 + 2 * e;
+            acc += ckb::mul_shoup_lazy(y[i], c[0], c[1], p);  // < 2p each
+            if ((i & 7) == 7) acc = ckb::reduce_16p(acc, p);
           }
         }
-        dst[(size_t)e * N] = acc >= m.p ? acc - m.p : acc;
+        dst[(size_t)digit_row(e, first, cnt, skip_own) * N] = ckb::reduce_16p(acc, p);
       }
     }
   }
 }
 
-__global__ void k_ks_inner(uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig,
-                           int batch, int nd, int ext, int log_n, const uint64_t* __restrict__ key,
-                           const uint64_t* const* __restrict__ key_ptrs, int key_limbs, RingDev R,
-                           LimbMap em, LimbMap km) {
+// acc[b][c][e] = sum_j digit_j[e] * key_b[j][c][key_limb(e)] with 128-bit lazy
+// accumulation and one reduction per output.  With own != NULL the digits'
+// own limbs come from `own` (the NTT-domain input the digits were cut from).
+__global__ void __launch_bounds__(256) k_ks_inner(
+    uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
+    int out_rows, int alpha, int limbs, const uint64_t* __restrict__ own, size_t own_bstride,
+    int log_n, const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs,
+    int key_limbs, RingDev R, LimbMap em, LimbMap km) {
   const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)batch * ext * N;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
@@ -145,21 +169,35 @@ __global__ void k_ks_inner(uint64_t* __restrict__ acc, const uint64_t* __restric
     const size_t be = t >> log_n;
     const int e = (int)(be % ext);
     const size_t bi = be / ext;
-    const Mod m = load_mod(R, em.p[e]);
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    Mod m;
+    m.p = __ldg(mm);
+    m.mu = __ldg(mm + 1);
+    m.k = __ldg(mm + 2);
+    m.two_p = __ldg(mm + 3);
     const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
     const size_t krow = 2 * (size_t)key_limbs * N;
     const uint64_t* kb = K + (size_t)km.p[e] * N + n;
     const uint64_t* ka = kb + (size_t)key_limbs * N;
-    const uint64_t* d = dig + (bi * nd * ext + e) * N + n;
-    uint64_t sb = 0, sa = 0;
+    const int own_digit = (own && e < limbs) ? e / alpha : -1;
+    uint64_t hb = 0, lb = 0, ha = 0, la = 0;
     for (int j = 0; j < nd; ++j) {
-      const uint64_t x = d[(size_t)j * ext * N];
-      sb = ckb::add_mod(sb, ckb::mul_mod(x, __ldg(kb + j * krow), m), m.p);
-      sa = ckb::add_mod(sa, ckb::mul_mod(x, __ldg(ka + j * krow), m), m.p);
+      uint64_t x;
+      if (j == own_digit) {
+        x = own[bi * own_bstride + (size_t)e * N + n];
+      } else {
+        const int first = j * alpha;
+        const int cnt = min(alpha, limbs - first);
+        const int row = own ? (e < first ? e : e - cnt) : e;
+        x = dig[((bi * nd + j) * (size_t)out_rows + row) * N + n];
+      }
+      ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
+      ckb::mac128(ha, la, x, __ldg(ka + j * krow));
     }
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
     uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
-    o[0] = sb;
-    o[(size_t)ext * N] = sa;
+    o[0] = ckb::reduce128_any(hb, lb, r64, r64s, m);
+    o[(size_t)ext * N] = ckb::reduce128_any(ha, la, r64, r64s, m);
   }
 }
 
@@ -222,7 +260,7 @@ __global__ void __launch_bounds__(256, 2) k_divround(
     for (int d = 0; d < D1; ++d) {
       if (d < n1) {
         const int li = limbs - 1 - d;
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         const uint64_t* T = tab1 + (size_t)li * s1;
         uint64_t acc = load(li, p);
 #pragma unroll
@@ -233,7 +271,7 @@ __global__ void __launch_bounds__(256, 2) k_divround(
       }
     }
     auto stage1 = [&](int l) -> uint64_t {
-      const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+      const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * kModStride);
       uint64_t v = load(l, p);
       if (n1) {
         const uint64_t* T = tab1 + (size_t)l * s1;
@@ -249,7 +287,7 @@ __global__ void __launch_bounds__(256, 2) k_divround(
     for (int d = 0; d < D2; ++d) {
       if (d < n2) {
         const int li = m1 - 1 - d;
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         const uint64_t* T = tab2 + (size_t)li * s2;
         uint64_t acc = stage1(li);
 #pragma unroll
@@ -262,7 +300,7 @@ __global__ void __launch_bounds__(256, 2) k_divround(
     for (int l = 0; l < m2; ++l) {
       uint64_t v = stage1(l);
       if (n2) {
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * 8);
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[l] * kModStride);
         const uint64_t* T = tab2 + (size_t)l * s2;
 #pragma unroll
         for (int u = 0; u < D2; ++u)
@@ -300,7 +338,7 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
   const size_t total = (size_t)polys * N;
   const int m1 = limbs - n1;
   const int m2 = m1 - n2;
-  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2);
+  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2 + 1);
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
@@ -312,7 +350,7 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
     for (int d = 0; d < D1; ++d) {
       if (d < n1) {
         const int li = limbs - 1 - d;
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         const uint64_t* Tb = tab1 + (size_t)li * s1;
         uint64_t acc = src[(size_t)(li - m2) * N];
 #pragma unroll
@@ -326,7 +364,7 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
     for (int d = 0; d < D2; ++d) {
       if (d < n2) {
         const int li = m1 - 1 - d;
-        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * 8);
+        const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         uint64_t v = src[(size_t)(li - m2) * N];
         if (n1) {
           const uint64_t* Ta = tab1 + (size_t)li * s1;
@@ -344,19 +382,29 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
         r2[d] = centered(v, p);
       }
     }
+    // E_j = sum_u r_u c_uj: each signed r is shifted by C_j (a multiple of q_j
+    // near 2^61) so every term is one lazy Shoup product (< 2 q_j) of a
+    // non-negative word; one reduction per 8 terms.
     uint64_t* dst = E + pidx * m2 * N + n;
     for (int j = 0; j < m2; ++j) {
-      const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * 8);
+      const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * kModStride);
       const uint64_t* Te = tabE + (size_t)j * sE;
+      const int64_t off = (int64_t)__ldg(Te + 2 * (n1 + n2));
       uint64_t e = 0;
 #pragma unroll
       for (int u = 0; u < D1; ++u)
-        if (u < n1) e = add_rm(e, r1[u], __ldg(Te + 2 * u), __ldg(Te + 2 * u + 1), p);
+        if (u < n1) {
+          e += ckb::mul_shoup_lazy((uint64_t)(r1[u] + off), __ldg(Te + 2 * u), __ldg(Te + 2 * u + 1), p);
+          if ((u & 7) == 7) e = ckb::reduce_16p(e, p);
+        }
 #pragma unroll
       for (int u = 0; u < D2; ++u)
-        if (u < n2)
-          e = add_rm(e, r2[u], __ldg(Te + 2 * (n1 + u)), __ldg(Te + 2 * (n1 + u) + 1), p);
-      dst[(size_t)j * N] = e;
+        if (u < n2) {
+          e += ckb::mul_shoup_lazy((uint64_t)(r2[u] + off), __ldg(Te + 2 * (n1 + u)),
+                                   __ldg(Te + 2 * (n1 + u) + 1), p);
+          if (((n1 + u) & 7) == 7) e = ckb::reduce_16p(e, p);
+        }
+      dst[(size_t)j * N] = ckb::reduce_16p(e, p);
     }
   }
 }
@@ -380,7 +428,7 @@ __global__ void k_divround_combine(uint64_t* __restrict__ out, const uint64_t* _
     const size_t pj = t >> log_n;
     const int j = (int)(pj % m2);
     const size_t pidx = pj / m2;
-    const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * 8);
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * kModStride);
     uint64_t v = x[pidx * x_stride + (size_t)j * N + n];
     if (n1) {
       const uint64_t* Ta = tab1 + (size_t)j * s1 + 2 * n1;
@@ -439,7 +487,7 @@ __global__ void k_automorphism(uint64_t* __restrict__ out, const uint64_t* __res
     const uint64_t t = i & (N - 1);
     const uint64_t ginv = ginv_items ? __ldg(ginv_items + row / rows_per_item) : ginv0;
     const uint64_t sidx2 = (t * ginv) & mask2;
-    const uint64_t p = __ldg(R.mods + (size_t)lm.p[row % limbs] * 8);
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[row % limbs] * kModStride);
     const uint64_t* src = in + row * N;
     if (sidx2 < N) {
       out[i] = src[sidx2];
@@ -496,20 +544,20 @@ __global__ void k_to_f64(double* __restrict__ out, const uint64_t* __restrict__ 
     // fraction x / Q = sum_i v_i / (q_i * ... * q_{limbs-1}), Horner from digit 0
     double f = 0.0;
     for (int i = 0; i < limbs; ++i) {
-      const double q = (double)__ldg(R.mods + (size_t)lm.p[i] * 8);
+      const double q = (double)__ldg(R.mods + (size_t)lm.p[i] * kModStride);
       f = ((double)v[i] + f) / q;
     }
     const bool negative = f > 0.5;
     double approx = 0.0;
     uint64_t exact = 0, prod = 1;
     for (int i = 0; i < limbs; ++i) {
-      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * 8);
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * kModStride);
       const uint64_t u = negative ? (q - 1 - v[i]) : v[i];
       exact += u * prod;
       prod *= q;
     }
     for (int i = limbs - 1; i >= 0; --i) {
-      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * 8);
+      const uint64_t q = __ldg(R.mods + (size_t)lm.p[i] * kModStride);
       const uint64_t u = negative ? (q - 1 - v[i]) : v[i];
       approx = approx * (double)q + (double)u;
     }
@@ -569,7 +617,7 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
     const ckb::Mod m = ckb::make_mod(p);
     const uint64_t ninv = ckb::inv_mod_host(N % p, p);
     const uint64_t fold = ckb::mul_mod_host(t[2 * N + 1], ninv, p);
-    uint64_t* mo = mods_out + (size_t)i * 8;
+    uint64_t* mo = mods_out + (size_t)i * kModStride;
     mo[0] = m.p;
     mo[1] = m.mu;
     mo[2] = m.k;
@@ -578,6 +626,10 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
     mo[5] = ckb::shoup_of(ninv, p);
     mo[6] = fold;
     mo[7] = ckb::shoup_of(fold, p);
+    const uint64_t r64 = (uint64_t)(((unsigned __int128)1 << 64) % p);
+    mo[8] = r64;
+    mo[9] = ckb::shoup_of(r64, p);
+    for (int z = 10; z < kModStride; ++z) mo[z] = 0;
   }
   for (uint32_t i = 0; i < np; ++i) {
     for (uint32_t j = 0; j < np; ++j) {
@@ -639,41 +691,51 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
 }
 
 int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
-              int batch, int limbs,
-              const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime, int alpha,
-              const uint64_t* bconv, void* stream) {
+              int batch, int limbs, const int32_t* limb_prime, int ext_limbs, const int32_t* ext_prime,
+              int alpha, const uint64_t* bconv, int skip_own, void* stream) {
   LimbMap lm, em;
   if (!make_map(lm, limb_prime, limbs) || !make_map(em, ext_prime, ext_limbs)) return CKB_E_LIMBS;
   if (alpha < 1 || alpha > 16 || ext_limbs < limbs || batch < 0) return CKB_E_ARG;
   if (alpha > 1 && !bconv) return CKB_E_ARG;
+  if (skip_own && limbs % alpha != 0) return CKB_E_ARG;
   for (int i = 0; i < limbs; ++i)
     if (lm.p[i] != em.p[i]) return CKB_E_ARG;
   const RingDev R = make_ring(ring);
   const int nd = (limbs + alpha - 1) / alpha;
-  const size_t total = ((size_t)batch * nd) << R.log_n;
-  if (!total) return 0;
+  const size_t total = (size_t)batch << R.log_n;
+  if (!total || !nd) return 0;
   const size_t bstride = in_batch_stride > 0 ? (size_t)in_batch_stride : ((size_t)limbs << R.log_n);
+  const int out_rows = skip_own ? ext_limbs - alpha : ext_limbs;
   const int amax = alpha == 1 ? 1 : alpha <= 2 ? 2 : alpha <= 4 ? 4 : alpha <= 8 ? 8 : 16;
   auto kern = amax == 1 ? k_modup<1> : amax == 2 ? k_modup<2> : amax == 4 ? k_modup<4>
             : amax == 8 ? k_modup<8> : k_modup<16>;
-  kern<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      out, in, bstride, batch, limbs, ext_limbs, alpha, nd, (int)R.log_n, R, lm, em, bconv);
+  const size_t smem = amax == 1 ? 0 : (size_t)alpha * (2 + 2 * (size_t)ext_limbs) * 8;
+  dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((total + 255) / 256, 4096 / nd + 1)),
+            (unsigned)nd);
+  kern<<<grid, 256, smem, (cudaStream_t)stream>>>(out, in, bstride, batch, limbs, ext_limbs,
+                                                   alpha, nd, out_rows, skip_own, (int)R.log_n,
+                                                   R, lm, em, bconv);
   return finish();
 }
 
 int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
-                 int n_digits, int ext_limbs, const int32_t* ext_prime, const uint64_t* key,
+                 int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
+                 const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
                  const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
                  void* stream) {
   LimbMap em, km;
   if (!make_map(em, ext_prime, ext_limbs) || !make_map(km, key_limb, ext_limbs))
     return CKB_E_LIMBS;
-  if (batch < 0 || n_digits < 1 || (!key && !key_ptrs)) return CKB_E_ARG;
+  if (batch < 0 || n_digits < 1 || (!key && !key_ptrs) || alpha < 1) return CKB_E_ARG;
+  if (own && limbs % alpha != 0) return CKB_E_ARG;
   const RingDev R = make_ring(ring);
   const size_t total = ((size_t)batch * ext_limbs) << R.log_n;
   if (!total) return 0;
+  const int out_rows = own ? ext_limbs - alpha : ext_limbs;
+  const size_t ob = own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << R.log_n);
   k_ks_inner<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      acc, digits, batch, n_digits, ext_limbs, (int)R.log_n, key, key_ptrs, key_limbs, R, em, km);
+      acc, digits, batch, n_digits, ext_limbs, out_rows, alpha, limbs, own, ob, (int)R.log_n, key,
+      key_ptrs, key_limbs, R, em, km);
   return finish();
 }
 

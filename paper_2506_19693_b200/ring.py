@@ -243,24 +243,40 @@ class GpuChain:
         return out
 
     def modup(self, d, m: int, alpha: int, bconv, batch: int = None, in_batch_stride: int = 0,
-              out=None):
-        """d: batch items of [m][N] (item b at d + b*in_batch_stride elements)."""
+              skip_own: bool = False, out=None):
+        """d: batch items of [m][N] (item b at d + b*in_batch_stride elements).
+        Returns digits [batch, nd, rows, N], rows = ext (or ext - alpha with skip_own)."""
         if batch is None:
             batch = d.numel() // (m * self.n)
         ext = m + self.k
         nd = -(-m // alpha)
-        out = out if out is not None else torch.empty(batch, nd, ext, self.n, dtype=U64,
+        rows = ext - alpha if skip_own else ext
+        out = out if out is not None else torch.empty(batch, nd, rows, self.n, dtype=U64,
                                                       device=self.device)
-        _run("modup", (batch * m + batch * nd * ext) * self.n * W, 1, lambda: nat.check(
+        _run("modup", (batch * m + batch * nd * rows) * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), in_batch_stride, batch,
                               m, self.q_map(m), ext, self.ext_map(m), alpha,
-                              nat.ptr(bconv) if bconv is not None else None,
+                              nat.ptr(bconv) if bconv is not None else None, int(skip_own),
                               nat.stream_handle()), "modup"))
         return out
 
-    def ks_inner(self, digits, m: int, key: torch.Tensor = None, key_ptrs: torch.Tensor = None,
+    def digit_basis(self, m: int, alpha: int, skip_own: bool) -> tuple:
+        """Per-row prime indices of a digits tensor [nd][rows] (for its NTT)."""
+        ext = self.ext_basis(m)
+        if not skip_own:
+            return ext
+        nd = -(-m // alpha)
+        out = ()
+        for j in range(nd):
+            own = set(range(j * alpha, min((j + 1) * alpha, m)))
+            out += tuple(pi for e, pi in enumerate(ext) if e not in own)
+        return out
+
+    def ks_inner(self, digits, m: int, alpha: int = 1, key: torch.Tensor = None,
+                 key_ptrs: torch.Tensor = None, own: torch.Tensor = None, own_bstride: int = 0,
                  out=None):
-        batch, nd, ext = digits.shape[0], digits.shape[1], digits.shape[2]
+        batch, nd = digits.shape[0], digits.shape[1]
+        ext = m + self.k
         out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
                                                       device=self.device)
         key_limbs = len(self.all_primes)
@@ -268,7 +284,9 @@ class GpuChain:
         nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext
         _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
-                                 self.ext_map(m), nat.ptr(key) if key is not None else None,
+                                 self.ext_map(m), alpha, m,
+                                 nat.ptr(own) if own is not None else None, own_bstride,
+                                 nat.ptr(key) if key is not None else None,
                                  nat.ptr(key_ptrs) if key_ptrs is not None else None,
                                  key_limbs, self.ext_map(m), nat.stream_handle()), "ks_inner"))
         return out
@@ -297,7 +315,8 @@ class GpuChain:
 
     def _corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
         """tabE for ckb_divround_ntt_corr: per output limb j, {M1_u * P1^-1 mod q_j}
-        for u < n1 then {M2_u mod q_j} for u < n2."""
+        for u < n1, {M2_u mod q_j} for u < n2, then {C_j, 0} with C_j the smallest
+        multiple of q_j >= 2^61 (shifts the signed remainders non-negative)."""
         primes = [self.all_primes[i] for i in basis]
         limbs = len(primes)
         m1 = limbs - n1
@@ -305,9 +324,10 @@ class GpuChain:
         d1 = [primes[limbs - 1 - u] for u in range(n1)]
         d2 = [primes[m1 - 1 - u] for u in range(n2)]
         P1 = math.prod(d1)
-        tab = np.zeros((m2, max(1, n1 + n2), 2), dtype=np.uint64)
+        tab = np.zeros((m2, n1 + n2 + 1, 2), dtype=np.uint64)
         for j in range(m2):
             p = primes[j]
+            tab[j, n1 + n2] = (p * -(-(1 << 61) // p), 0)  # C_j: multiple of q_j near 2^61
             p1inv = pow(P1 % p, -1, p)
             for u in range(n1):
                 c = math.prod(d1[:u]) % p * p1inv % p

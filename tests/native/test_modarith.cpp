@@ -51,6 +51,21 @@ int main() {
           __int128 c = (xr > q / 2) ? (__int128)xr - (__int128)q : (__int128)xr;
           __int128 cm = c % (__int128)p; if (cm < 0) cm += p;
           if (centered_into(xr, q, m) != (uint64_t)cm) ++fails;
+          if (bits <= 60) {
+            uint64_t y = rng() % (16 * p);
+            if (reduce_16p(y, p) != y % p) ++fails;
+          }
+          {
+            uint64_t hi = 0, lo = 0;
+            unsigned __int128 want128 = 0;
+            for (int k = 0; k < 5; ++k) {
+              uint64_t u = rng() % p, v = rng() % p;
+              mac128(hi, lo, u, v);
+              want128 += (unsigned __int128)u * v;
+            }
+            uint64_t r64 = (uint64_t)(((unsigned __int128)1 << 64) % p);
+            if (reduce128_any(hi, lo, r64, shoup_of(r64, p), m) != (uint64_t)(want128 % p)) ++fails;
+          }
         }
       }
       p -= step;
