@@ -388,7 +388,7 @@ class B200CkksCore:
         bsz = a.shape[0]
         e = len(ch.entry_primes[level])
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
-        d2 = ch.ntt_inv(d[:, 2].contiguous(), m)
+        d2 = ch.ntt_inv(d[:, 2].clone(memory_format=torch.contiguous_format), m)
         acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key, own=d[:, 2],
                                    own_stride=3 * m * self.n)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
@@ -416,7 +416,7 @@ class B200CkksCore:
         m = self._limbs(level)
         bsz = a.shape[0]
         r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
-        c1 = ch.ntt_inv(r[:, 1].contiguous(), m)
+        c1 = ch.ntt_inv(r[:, 1].clone(memory_format=torch.contiguous_format), m)
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
                                    own_stride=2 * m * self.n)
         out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, 0, addend=r, addend_polys=1,

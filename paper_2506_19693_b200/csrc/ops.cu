@@ -155,45 +155,55 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
 
 // acc[b][c][e] = sum_j digit_j[e] * key_b[j][c][key_limb(e)] with 128-bit lazy
 // accumulation and one reduction per output.  With own != NULL the digits'
-// own limbs come from `own` (the NTT-domain input the digits were cut from).
+// own limbs come from `own` (the NTT-domain input the digits were cut from);
+// od.p[e] is the digit that owns ext limb e (-1 for none), and digit j holds
+// limb e at row e - (e >= (j+1)*alpha ? alpha : 0).  ND > 0: fully unrolled.
+template <int ND>
 __global__ void __launch_bounds__(256) k_ks_inner(
     uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
-    int out_rows, int alpha, int limbs, const uint64_t* __restrict__ own, size_t own_bstride,
-    int log_n, const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs,
-    int key_limbs, RingDev R, LimbMap em, LimbMap km) {
+    int out_rows, int alpha, const uint64_t* __restrict__ own, size_t own_bstride, int log_n,
+    const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
+    RingDev R, LimbMap em, LimbMap km, LimbMap od) {
   const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)batch * ext * N;
+  const int ndig = ND > 0 ? ND : nd;
+  const size_t krow = 2 * (size_t)key_limbs * N;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t n = t & (N - 1);
     const size_t be = t >> log_n;
     const int e = (int)(be % ext);
     const size_t bi = be / ext;
+    const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
+    const uint64_t* kb = K + (size_t)km.p[e] * N + n;
+    const uint64_t* ka = kb + (size_t)key_limbs * N;
+    const int owner = own ? od.p[e] : -1;
+    const uint64_t* dbase = dig + bi * (size_t)ndig * out_rows * N + n;
+    uint64_t hb = 0, lb = 0, ha = 0, la = 0;
+#pragma unroll
+    for (int j = 0; j < (ND > 0 ? ND : 1); ++j) {
+      if (ND == 0) break;
+      const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
+      const uint64_t x = (j == owner) ? own[bi * own_bstride + (size_t)e * N + n]
+                                      : dbase[((size_t)j * out_rows + row) * N];
+      ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
+      ckb::mac128(ha, la, x, __ldg(ka + j * krow));
+    }
+    if (ND == 0) {
+      for (int j = 0; j < ndig; ++j) {
+        const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
+        const uint64_t x = (j == owner) ? own[bi * own_bstride + (size_t)e * N + n]
+                                        : dbase[((size_t)j * out_rows + row) * N];
+        ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
+        ckb::mac128(ha, la, x, __ldg(ka + j * krow));
+      }
+    }
     const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
     Mod m;
     m.p = __ldg(mm);
     m.mu = __ldg(mm + 1);
     m.k = __ldg(mm + 2);
     m.two_p = __ldg(mm + 3);
-    const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
-    const size_t krow = 2 * (size_t)key_limbs * N;
-    const uint64_t* kb = K + (size_t)km.p[e] * N + n;
-    const uint64_t* ka = kb + (size_t)key_limbs * N;
-    const int own_digit = (own && e < limbs) ? e / alpha : -1;
-    uint64_t hb = 0, lb = 0, ha = 0, la = 0;
-    for (int j = 0; j < nd; ++j) {
-      uint64_t x;
-      if (j == own_digit) {
-        x = own[bi * own_bstride + (size_t)e * N + n];
-      } else {
-        const int first = j * alpha;
-        const int cnt = min(alpha, limbs - first);
-        const int row = own ? (e < first ? e : e - cnt) : e;
-        x = dig[((bi * nd + j) * (size_t)out_rows + row) * N + n];
-      }
-      ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
-      ckb::mac128(ha, la, x, __ldg(ka + j * krow));
-    }
     const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
     uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
     o[0] = ckb::reduce128_any(hb, lb, r64, r64s, m);
@@ -723,19 +733,33 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
                  const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
                  const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
                  void* stream) {
-  LimbMap em, km;
+  LimbMap em, km, od;
   if (!make_map(em, ext_prime, ext_limbs) || !make_map(km, key_limb, ext_limbs))
     return CKB_E_LIMBS;
   if (batch < 0 || n_digits < 1 || (!key && !key_ptrs) || alpha < 1) return CKB_E_ARG;
   if (own && limbs % alpha != 0) return CKB_E_ARG;
+  for (int e = 0; e < ext_limbs; ++e) od.p[e] = (int16_t)(e < limbs ? e / alpha : -1);
   const RingDev R = make_ring(ring);
   const size_t total = ((size_t)batch * ext_limbs) << R.log_n;
   if (!total) return 0;
   const int out_rows = own ? ext_limbs - alpha : ext_limbs;
   const size_t ob = own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << R.log_n);
-  k_ks_inner<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      acc, digits, batch, n_digits, ext_limbs, out_rows, alpha, limbs, own, ob, (int)R.log_n, key,
-      key_ptrs, key_limbs, R, em, km);
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define CKB_KS(ND)                                                                           \
+  k_ks_inner<ND><<<grid, 256, 0, st>>>(acc, digits, batch, n_digits, ext_limbs, out_rows,   \
+                                       alpha, own, ob, (int)R.log_n, key, key_ptrs,         \
+                                       key_limbs, R, em, km, od)
+  switch (n_digits) {
+    case 1: CKB_KS(1); break;
+    case 2: CKB_KS(2); break;
+    case 3: CKB_KS(3); break;
+    case 4: CKB_KS(4); break;
+    case 6: CKB_KS(6); break;
+    case 8: CKB_KS(8); break;
+    default: CKB_KS(0); break;
+  }
+#undef CKB_KS
   return finish();
 }
 
