@@ -43,6 +43,7 @@ struct NttPhase {
   int gt;
   int last;     // forward: canonicalise; inverse: fold N^-1 into the top stage
   int row0;     // first row handled by this launch (for L2-resident chunking)
+  int logC;     // log2(C)
 };
 
 // Shared-memory slot of element r of group g: one pad word per 16 elements
@@ -208,8 +209,8 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
       r = e & (G - 1);
       return (size_t)(g0 + g) * ph.gstride + r;
     }
-    r = e / C;
-    g = e - r * C;
+    r = e >> ph.logC;
+    g = e & (C - 1);
     return (size_t)r * ph.rstride + g0 + g;
   };
   {
@@ -297,7 +298,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   cudaStream_t st = (cudaStream_t)stream;
   const int N = 1 << logn;
   if (logn <= 12) {
-    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0};
+    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0};
     int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
     return rc ? rc : finish();
   }
@@ -307,9 +308,10 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   const int GA = 1 << s1, GB = 1 << s2;
   const int CA = std::max(1, kTwoPhaseTile / GA), CB = std::max(1, kTwoPhaseTile / GB);
   // phase A: groups are the GB columns, elements strided by GB
-  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0};
+  auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
+  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA)};
   // phase B: groups are the GA rows of GB contiguous elements
-  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0};
+  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB)};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
   const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
   for (int r0 = 0; r0 < rows; r0 += chunk) {
