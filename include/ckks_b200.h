@@ -175,6 +175,12 @@ int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, in
                      int limbs, const int32_t* limb_prime, uint64_t galois,
                      const uint64_t* galois_inv_items, int rows_per_item, void* stream);
 
+/* Canonicalise arbitrary 64-bit words per limb (x mod p): used after an
+ * integer all-reduce of residue tensors across ranks (sum of <= 16 residues
+ * below 2^60 cannot overflow), SURVEY §8(e). */
+int ckb_reduce(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,
+               const int32_t* limb_prime, void* stream);
+
 /* Signed int64 coefficients -> residues (ring.py:139-145):
  * in: [polys][N] int64; out: [polys][limbs][N]. */
 int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int polys, int limbs,

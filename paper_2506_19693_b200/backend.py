@@ -296,25 +296,35 @@ class B200CkksCore:
             return ct
         if ct.level < target:
             raise self._errors.IncompatibleOperands("cannot raise a ciphertext's level")
+        return GpuCiphertext(self._adjust_data(ct.data, ct.level, target), target)
+
+    def _adjust_data(self, data: torch.Tensor, origin: int, target: int) -> torch.Tensor:
+        """_adjust_to_level on [..., 2, limbs(origin), N] (any batch shape)."""
         ch = self.chain
         staging = target + 1
         ms = self._limbs(staging)
-        key = (ct.level, target)
+        key = (origin, target)
         if key not in self._adjust_cache:
-            s_star = self._scale(target) * ch.entry_products[staging] / self._scale(ct.level)
+            s_star = self._scale(target) * ch.entry_products[staging] / self._scale(origin)
             factor = int(np.rint(s_star))
             self._adjust_cache[key] = ch.scalar_pairs(factor, range(ms))
         # out-of-place: payloads are immutable (api.py:51-65), never scale in place
-        src = ct.data if ms == ct.data.shape[1] else ct.data[:, :ms].contiguous()
+        src = data if ms == data.shape[-2] else data[..., :ms, :].contiguous()
         x = ch.scalar_mul(src, self._adjust_cache[key], ms)
-        out = ch.divround_ntt(x, 2, ms, len(ch.entry_primes[staging]))
-        return GpuCiphertext(out, target)
+        polys = x.numel() // (ms * self.n)
+        out = ch.divround_ntt(x, polys, ms, len(ch.entry_primes[staging]))
+        return out.view(*data.shape[:-2], ms - len(ch.entry_primes[staging]), self.n)
 
     def _rescale(self, data: torch.Tensor, level: int) -> GpuCiphertext:
         """backend.py:86-92: divide-round by entry_primes[level] (NTT domain)."""
+        return GpuCiphertext(self._rescale_data(data, level), level - 1)
+
+    def _rescale_data(self, data: torch.Tensor, level: int) -> torch.Tensor:
         m = self._limbs(level)
-        out = self.chain.divround_ntt(data, 2, m, len(self.chain.entry_primes[level]))
-        return GpuCiphertext(out, level - 1)
+        e = len(self.chain.entry_primes[level])
+        polys = data.numel() // (m * self.n)
+        out = self.chain.divround_ntt(data, polys, m, e)
+        return out.view(*data.shape[:-2], m - e, self.n)
 
     def _to_ntt(self, coeff: torch.Tensor) -> torch.Tensor:
         return self.chain.ntt_fwd(coeff, coeff.shape[-2])
@@ -423,24 +433,36 @@ class B200CkksCore:
                               addend_period=2, addend_stride=2, basis=ch.ext_basis(m))
         return out.view(bsz, 2, m, self.n)
 
-    def _encrypt_values(self, values, level: int) -> GpuCiphertext:
+    def _encrypt_values(self, values, level: int, serial: int = None) -> GpuCiphertext:
         """backend.py:173-182: symmetric encryption, RNG (seed, serial); the
         result c0 = -a*s + NTT(m + e), c1 = a is the NTT form of the reference's."""
+        return GpuCiphertext(self._encrypt_batch([values], level, [serial])[0], level)
+
+    def _encrypt_batch(self, values_list, level: int, serials) -> torch.Tensor:
+        """Encrypt several vectors at one level -> [B, 2, m, N]; serial None draws
+        the next serial (the reference's default_rng((seed, serial)) stream)."""
         ch = self.chain
-        rng = np.random.default_rng((self.rng_seed, next(self._serials)))
         primes = ch.limbs_at(level)
         m = len(primes)
-        msg = self._encode_rns(values, level)
-        a_np = np.stack([rng.integers(0, p, self.n, dtype=np.uint64) for p in primes])
-        e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
-        out = torch.empty(2, m, self.n, dtype=U64, device=self.device)
-        out[1].copy_(torch.from_numpy(a_np))
-        me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)[0]
-        ch.add(me, msg, m, out=me)
+        bsz = len(values_list)
+        a_np = np.empty((bsz, m, self.n), dtype=np.uint64)
+        e_np = np.empty((bsz, self.n), dtype=np.int64)
+        msgs = []
+        for i, (values, serial) in enumerate(zip(values_list, serials)):
+            msgs.append(self._encode_rns(values, level))
+            sr = next(self._serials) if serial is None else serial
+            rng = np.random.default_rng((self.rng_seed, sr))
+            for j, p in enumerate(primes):
+                a_np[i, j] = rng.integers(0, p, self.n, dtype=np.uint64)
+            e_np[i] = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
+        out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)
+        out[:, 1].copy_(torch.from_numpy(a_np))
+        me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)  # [B, m, N]
+        ch.add(me, torch.stack(msgs), m, out=me)
         ch.ntt_fwd(me, m)
-        ch.mul(out[1], self.sk.s_full[:m], m, out=out[0])
-        ch.sub(me, out[0], m, out=out[0])
-        return GpuCiphertext(out, level)
+        a_s = ch.mul(out[:, 1].contiguous(), self.sk.s_full[:m], m, b_rows=m)
+        out[:, 0].copy_(ch.sub(me, a_s, m))
+        return out
 
     def _payload_encrypt(self, pv, level: int, serial: int):
         return self._encrypt_values(pv.values, level)

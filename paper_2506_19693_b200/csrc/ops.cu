@@ -479,6 +479,16 @@ __global__ void k_automorphism_ntt(uint64_t* __restrict__ out, const uint64_t* _
   }
 }
 
+// x mod p for arbitrary 64-bit words (after an integer all-reduce of residues).
+__global__ void k_reduce(uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t total,
+                         int log_n, int limbs, RingDev R, LimbMap lm) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)((i >> log_n) % limbs);
+    out[i] = ckb::reduce64(in[i], load_mod(R, lm.p[l]));
+  }
+}
+
 // ===========================================================================
 // Automorphism and conversions
 // ===========================================================================
@@ -923,6 +933,18 @@ int ckb_automorphism_ntt(const ckb_ring* ring, uint64_t* out, const uint64_t* in
   if (!total) return 0;
   k_automorphism_ntt<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       out, in, total, (int)R.log_n, galois, galois_items, rows_per_item);
+  return finish();
+}
+
+int ckb_reduce(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,
+               const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)rows << R.log_n;
+  if (!total) return 0;
+  k_reduce<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, in, total, (int)R.log_n,
+                                                                    limbs, R, lm);
   return finish();
 }
 

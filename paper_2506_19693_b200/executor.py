@@ -1,0 +1,220 @@
+"""Wavefront-batched execution of a recorded HE program.
+
+``nn.train_iteration`` (/root/reference/pkg/src/ciphermlp/nn.py:344-404) runs
+B independent per-sample pipelines (nn.py:363-382) and then the update.  Issued
+one HE call at a time, each call is a handful of small kernels on ~0.5 MB
+ciphertexts (config 1), so the step is launch- and host-bound and every
+rotation re-reads its key.  HE ops are pure functions of their operands, so
+the program (replay.Program: the exact call sequence the layer code makes) can
+be executed in dependency waves: all ops whose inputs are ready form a wave,
+and ops of a wave that share a signature — (kind, operand levels, rotation
+step, plaintext) — run as ONE batched launch sequence over stacked operands
+(one key read per rotation group, one plaintext per mul_pt group).
+
+Results are identical to sequential execution: every integer op is exact,
+encryption randomness is drawn from the serial each call would have had in
+program order (pre-assigned here), and refreshes run in program order.
+"""
+
+from __future__ import annotations
+
+import collections
+
+import numpy as np
+import torch
+
+from .backend import GpuCiphertext
+
+
+class WaveExecutor:
+    def __init__(self, program, custodian):
+        self.prog = program
+        self.cust = custodian
+        self.be = custodian.backend
+        self._plan()
+
+    # -- planning ------------------------------------------------------------
+    def _plan(self):
+        """Serials (as the HE API would assign them) and dependency waves."""
+        ops = self.prog.ops
+        be = self.be
+        ser = {}
+        counter = 0
+        depth = {}
+        waves = collections.defaultdict(list)
+        level = {}
+        self._last_bs_depth = 0
+        top = be.params.level
+        rl = be.params.refresh_level
+        self.n_setup = self.prog.n_setup
+        for i, op in enumerate(ops):
+            tag = op[0]
+            if tag == "enc":
+                ser[i] = counter + 1          # api.py:225 then backend.py:174
+                counter += 2
+                out, ins, lvl = op[1], [], top
+            elif tag == "ew":
+                kind, out, a, b = op[1], op[2], op[3], op[4]
+                ins = [a] + ([b] if kind.endswith("_ct") else [])
+                lvl = min(level[x] for x in ins)
+                if kind.startswith("mul"):
+                    lvl -= 1
+                counter += 1
+            elif tag == "rot":
+                out, ins = op[1], [op[2]]
+                lvl = level[op[2]]
+                counter += 1
+            elif tag == "bs":
+                out, ins = op[1], [op[2]]
+                ser[i] = counter + 1          # api.py:246 then backend.py:174 (re-encrypt)
+                counter += 2
+                lvl = rl
+            else:
+                raise ValueError(tag)
+            d = 1 + max((depth[x] for x in ins), default=0)
+            if tag == "bs":  # refreshes keep program order (bs_rng stream)
+                d = max(d, self._last_bs_depth + 1)
+                self._last_bs_depth = d
+            depth[out] = d
+            level[out] = lvl
+            waves[d].append(i)
+        self.serial_of = ser
+        self.level_of = level
+        self.waves = [waves[d] for d in sorted(waves)]
+        self.serials_used = counter
+
+    # -- execution -----------------------------------------------------------
+    def run(self, env=None, only_after_setup: bool = False) -> dict:
+        """Execute the program; returns id -> GpuCiphertext for live values.
+        With only_after_setup, ops before program.n_setup must already be in env."""
+        be = self.be
+        ops = self.prog.ops
+        env = {} if env is None else {k: getattr(v, "payload", v) for k, v in env.items()}
+        keep = set(self.prog.outputs)
+        last = self.prog._last_use
+        slots = be.params.slot_count
+        pts = self.prog.plaintexts
+
+        def pvals(i):
+            v = np.zeros(slots)
+            v[: pts.shape[1]] = pts[i]
+            return v
+
+        for wave in self.waves:
+            if only_after_setup:
+                wave = [i for i in wave if i >= self.n_setup]
+                if not wave:
+                    continue
+            groups = collections.defaultdict(list)
+            for i in wave:
+                op = ops[i]
+                tag = op[0]
+                if tag == "enc":
+                    groups[("enc",)].append(i)
+                elif tag == "ew":
+                    kind, _, a, b = op[1], op[2], op[3], op[4]
+                    la = env[a].level
+                    if kind.endswith("_ct"):
+                        groups[(kind, la, env[b].level)].append(i)
+                    else:
+                        groups[(kind, la, b)].append(i)
+                elif tag == "rot":
+                    groups[("rot", env[op[2]].level, op[3] % slots)].append(i)
+                else:
+                    groups[("bs", i)].append(i)
+            for key, idx in groups.items():
+                self._run_group(key, idx, env, pvals)
+            for i in wave:
+                for ref in _inputs(ops[i]):
+                    if last.get(ref) == i and ref not in keep:
+                        env.pop(ref, None)
+        # leave the backend's serial counter where sequential execution would
+        import itertools
+
+        be._serials = itertools.count(self.serials_used)
+        return env
+
+    def _stack(self, items):
+        if len(items) == 1:
+            return items[0].unsqueeze(0)
+        return torch.stack(items)
+
+    def _run_group(self, key, idx, env, pvals):
+        be = self.be
+        ch = be.chain
+        ops = self.prog.ops
+        tag = key[0]
+        if tag == "enc":
+            top = be.params.level
+            data = be._encrypt_batch([pvals(ops[i][2]) for i in idx], top,
+                                     [self.serial_of[i] for i in idx])
+            for j, i in enumerate(idx):
+                env[ops[i][1]] = GpuCiphertext(data[j], top)
+            return
+        if tag == "bs":
+            i = idx[0]
+            src = env[ops[i][2]]
+            values = be._decrypt_values(src)
+            if be.bootstrap_eps > 0.0:
+                values = values + be._bs_rng.uniform(-be.bootstrap_eps, be.bootstrap_eps,
+                                                     values.shape[0])
+            rl = be.params.refresh_level
+            env[ops[i][1]] = GpuCiphertext(
+                be._encrypt_batch([values], rl, [self.serial_of[i]])[0], rl)
+            return
+        if tag == "rot":
+            _, lvl, step = key
+            x = self._stack([env[ops[i][2]].data for i in idx])
+            if step == 0:
+                out = x.clone()
+            else:
+                g = be.galois_for_step.get(step, pow(5, step, 2 * be.n))
+                out = be._hrot(x, lvl, galois=g, key=be.rotation_key(g))
+            for j, i in enumerate(idx):
+                env[ops[i][1]] = GpuCiphertext(out[j], lvl)
+            return
+        kind = tag
+        op3 = kind[:3]
+        if kind.endswith("_ct"):
+            _, la, lb = key
+            lvl = min(la, lb)
+            in_level = lvl
+            a = self._stack([env[ops[i][3]].data for i in idx])
+            b = self._stack([env[ops[i][4]].data for i in idx])
+            if la != in_level:
+                a = be._adjust_data(a, la, in_level)
+            if lb != in_level:
+                b = be._adjust_data(b, lb, in_level)
+            m = be._limbs(in_level)
+            if op3 == "add":
+                out, out_level = ch.add(a, b, m), in_level
+            elif op3 == "sub":
+                out, out_level = ch.sub(a, b, m), in_level
+            else:
+                out, out_level = be._hmult(a.contiguous(), b.contiguous(), in_level), in_level - 1
+        else:
+            _, la, pid = key
+            m = be._limbs(la)
+            vals = pvals(pid)
+            a = self._stack([env[ops[i][3]].data for i in idx])
+            if op3 == "mul":
+                pt = be._encode_rns(vals, la, ntt=True)
+                out = be._rescale_data(ch.mul(a, pt, m, b_rows=m), la)
+                out_level = la - 1
+            else:
+                pt = be._encode_rns(vals if op3 == "add" else -vals, la, ntt=True)
+                pt2 = torch.zeros(2, m, be.n, dtype=pt.dtype, device=pt.device)
+                pt2[0].copy_(pt)  # (c0 + pt, c1 + 0), broadcast over the batch
+                out = ch.ew(0, torch.empty_like(a), a, pt2, limbs=m, b_rows=2 * m)
+                out_level = la
+        for j, i in enumerate(idx):
+            env[ops[i][2]] = GpuCiphertext(out[j], out_level)
+
+
+def _inputs(op):
+    tag = op[0]
+    if tag == "ew":
+        return [op[3]] + ([op[4]] if op[1].endswith("_ct") else [])
+    if tag in ("rot", "bs"):
+        return [op[2]]
+    return []

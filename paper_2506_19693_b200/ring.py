@@ -416,6 +416,15 @@ class GpuChain:
                                      rows_per_item, nat.stream_handle()), "automorphism"))
         return out
 
+    def reduce(self, x: torch.Tensor, limbs: int, out=None, lmap=None):
+        """x mod p per limb for arbitrary 64-bit words (after an all-reduce)."""
+        out = out if out is not None else torch.empty_like(x)
+        rows = x.numel() >> self.log_n
+        _run("reduce", 2 * rows * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_reduce(self.ring_p, nat.ptr(out), nat.ptr(x), rows, limbs,
+                               lmap or self.q_map(limbs), nat.stream_handle()), "reduce"))
+        return out
+
     def from_i64(self, coeffs: torch.Tensor, limbs: int, lmap=None, out=None):
         polys = coeffs.numel() >> self.log_n
         out = out if out is not None else torch.empty(polys, limbs, self.n, dtype=U64,

@@ -374,3 +374,49 @@ def test_c2_hybrid_keyswitch_decrypts(L):
     ca, cb = cust.encrypt(_pl(cust, a)), cust.encrypt(_pl(cust, b))
     assert np.max(np.abs(cust.decrypt(ev.mul(ca, cb)).values - a * b)) <= 2.0**-20
     assert np.max(np.abs(cust.decrypt(ev.rotate(ca, 7)).values - np.roll(a, -7))) <= 2.0**-20
+
+
+# ---------------------------------------------------------------------------
+# Config-1 step: the reference train_iteration's HE calls, replayed
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def c1_program(golden_dir):
+    from paper_2506_19693_b200.replay import Program
+
+    path = os.path.join(golden_dir, "c1_trace.npz")
+    return Program.load(path), np.load(path)
+
+
+def _c1_custodian(z):
+    n, level, sb = (int(v) for v in z["params"])
+    params = make_params(level=level, scale_bits=sb, poly_degree=n)
+    return he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=3,
+                         prime_layout="baseline", secret_hw=64)
+
+
+def test_c1_step_weights_match_reference(c1_program):
+    """Decrypted weights/velocities after one encrypted step agree with the
+    reference CKKS run and the exact float model within 1e-3 (north_star)."""
+    prog, z = c1_program
+    cust = _c1_custodian(z)
+    env = prog.run(cust)
+    w = np.stack([cust.decrypt(env[o]).values for o in prog.outputs])
+    assert np.max(np.abs(w - z["sim_weights"])) <= 1e-3
+    if "ckks_weights" in z:
+        assert np.max(np.abs(w - z["ckks_weights"])) <= 1e-3
+
+
+def test_wave_executor_bit_identical_to_sequential(c1_program):
+    from paper_2506_19693_b200.executor import WaveExecutor
+
+    prog, z = c1_program
+    seq = _c1_custodian(z)
+    env_seq = prog.run(seq)
+    bat = _c1_custodian(z)
+    env_bat = WaveExecutor(prog, bat).run()
+    for o in prog.outputs:
+        a = seq.backend.planes_of(env_seq[o].payload)
+        b = bat.backend.planes_of(env_bat[o])
+        assert np.array_equal(a, b)
