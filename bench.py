@@ -212,14 +212,20 @@ def run_c1_train(device_index):
     torch.cuda.synchronize()
     keygen_s = time.perf_counter() - t0
     env = prog.run(cust, 0, prog.n_setup)
+    import itertools
+
     times = []
+    first = None
+    s0 = next(cust.backend._serials)  # serial counter after setup (peek, then restore)
     for rep in range(3):
+        cust.backend._serials = itertools.count(s0)  # every repetition = the same step
         e = dict(env)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e = prog.run(cust, prog.n_setup, None, e)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
+        first = first or e
     from paper_2506_19693_b200.executor import WaveExecutor
 
     ex = WaveExecutor(prog, cust)
@@ -231,7 +237,7 @@ def run_c1_train(device_index):
         torch.cuda.synchronize()
         wtimes.append(time.perf_counter() - t0)
     wb = np.stack([cust.backend._decrypt_values(ew[o]) for o in prog.outputs])
-    w = np.stack([cust.decrypt(e[o]).values for o in prog.outputs])
+    w = np.stack([cust.decrypt(first[o]).values for o in prog.outputs])
     err_sim = float(np.max(np.abs(w - z["sim_weights"])))
     err_ref = float(np.max(np.abs(w - z["ckks_weights"]))) if "ckks_weights" in z else None
     ref_s = float(z["ckks_seconds"][1]) if "ckks_seconds" in z else None
