@@ -101,6 +101,15 @@ class DeviceEncoder:
         w = torch.fft.fft(spec) / self.n
         return torch.round(torch.real(w * self.untwist))
 
+    def embed_complex_device(self, z, scale: float) -> torch.Tensor:
+        """Complex slots -> int64 coefficients (conjugate spectrum on the mirrored bins)."""
+        zt = torch.as_tensor(np.asarray(z, dtype=np.complex128), device=self.device) * scale
+        spec = torch.zeros(self.n, dtype=torch.complex128, device=self.device)
+        spec[self.bins[: zt.shape[0]]] = zt
+        spec[self.conj_bins[: zt.shape[0]]] = torch.conj(zt)
+        w = torch.fft.fft(spec) / self.n
+        return torch.round(torch.real(w * self.untwist))
+
     def embed(self, values, scale: float) -> np.ndarray:
         coeffs = self.embed_device(values, scale)
         if float(coeffs.abs().max()) >= MAX_SAFE_COEFF:
@@ -144,7 +153,8 @@ class B200CkksCore:
 
     def __init__(self, params, rotation_indices=(), rng_seed: int = 0, bootstrap_eps: float = 0.0,
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
-                 secret_hw=None, device=None, encode_cache: int = 512):
+                 secret_hw=None, device=None, encode_cache: int = 512,
+                 conjugation_key: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -182,6 +192,11 @@ class B200CkksCore:
         for step in sorted({k % slots for k in self.rotation_indices} - {0}):
             g = pow(5, step, 2 * self.n)
             self.galois_for_step[step] = g
+            s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
+            ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
+            self.rotation_keys[g] = self._make_ksk(s_rot, rng)
+        if conjugation_key:  # X -> X^(2N-1): complex conjugation of the slots
+            g = 2 * self.n - 1
             s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
             ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
             self.rotation_keys[g] = self._make_ksk(s_rot, rng)
@@ -527,6 +542,79 @@ class B200CkksCore:
             payload=GpuCiphertext(data, level), level_remaining=level, scale_bits=scale_bits,
             depth=rl - level if level < rl else 0, backend_id=self.backend_id,
             keyset_id=self.keyset_id, serial=next(self._serials))
+
+    # ------------------------------------------------------ bootstrapping helpers
+    def encode_complex_ntt(self, z, level: int, scale: float = None) -> torch.Tensor:
+        """Complex slot vector -> NTT-domain plaintext [limbs(level), N] at
+        scale_at[level] (or `scale`)."""
+        ch = self.chain
+        m = self._limbs(level)
+        coeffs = self.encoder.embed_complex_device(z, self._scale(level) if scale is None
+                                                   else scale)
+        if float(coeffs.abs().max()) >= MAX_SAFE_COEFF:
+            raise self._errors.EncodingOverflow("complex plaintext exceeds 2^52")
+        res = ch.from_i64(coeffs.to(torch.int64), m)[0]
+        return ch.ntt_fwd(res, m)
+
+    def monomial_ntt(self, power: int, level: int) -> torch.Tensor:
+        """NTT form of X^power over the limbs of `level` (cached)."""
+        key = ("mono", power, level)
+        hit = self._adjust_cache.get(key)
+        if hit is None:
+            ch = self.chain
+            m = self._limbs(level)
+            c = torch.zeros(self.n, dtype=torch.int64, device=self.device)
+            c[power % self.n] = -1 if (power // self.n) % 2 else 1
+            hit = ch.ntt_fwd(ch.from_i64(c, m)[0], m)
+            self._adjust_cache[key] = hit
+        return hit
+
+    def hoisted_rotations(self, data: torch.Tensor, level: int, galois_list) -> list:
+        """Rotate one ciphertext ([2, m, N], NTT domain) by several Galois
+        elements sharing a single ModUp: the digits are lifted and transformed
+        once and permuted per rotation in the NTT domain (an automorphism
+        commutes with the basis extension up to multiples of Q_j, which the key
+        switch absorbs as noise)."""
+        ch = self.chain
+        m = self._limbs(level)
+        ext = m + ch.k
+        c1 = ch.ntt_inv(data[1].clone(), m)
+        digits = ch.modup(c1, m, self.alpha, self._bconv(m), batch=1)
+        ch.ntt_fwd(digits, ext, ch.ext_map(m))
+        out = []
+        for g in galois_list:
+            key = self.rotation_key(g)
+            dg = ch.automorphism_ntt(digits, g)
+            acc = ch.ks_inner(dg, m, self.alpha, key=key.data)
+            c0 = ch.automorphism_ntt(data[0], g)
+            r = ch.divround_ntt(acc, 2, ext, ch.k, 0, addend=c0, addend_polys=1,
+                                addend_period=2, addend_stride=1, basis=ch.ext_basis(m))
+            out.append(r.view(2, m, self.n))
+        return out
+
+    def rotate_data(self, data: torch.Tensor, level: int, galois: int) -> torch.Tensor:
+        return self._hrot(data.unsqueeze(0), level, galois=galois,
+                          key=self.rotation_key(galois))[0]
+
+    def mod_raise(self, ct: GpuCiphertext) -> GpuCiphertext:
+        """Bootstrapping step 1: reinterpret a level-0 ciphertext (one limb q0)
+        modulo the full chain Q_L by centred lifting of its coefficients."""
+        ch = self.chain
+        m0 = self._limbs(ct.level)
+        if ct.level != 0 or m0 != 1:
+            raise self._errors.IncompatibleOperands("mod_raise needs a one-limb level-0 ciphertext")
+        top = self.params.level
+        m = self._limbs(top)
+        coeff = ch.ntt_inv(ct.data.clone(), 1)
+        out = torch.empty(2, 1, m, self.n, dtype=U64, device=self.device)
+        from . import _native as nat
+
+        basis = tuple(range(m))
+        nat.check(nat.LIB.ckb_modup(ch.ring_p, nat.ptr(out), nat.ptr(coeff), 0, 2, 1,
+                                    ch.q_map(1), m, ch.cmap(basis), 1, None, 0,
+                                    nat.stream_handle()), "mod_raise")
+        data = out.view(2, m, self.n)
+        return GpuCiphertext(ch.ntt_fwd(data, m), top)
 
     # ------------------------------------------------------------ batched engine
     # One launch per stage across a whole batch of ciphertexts (the
