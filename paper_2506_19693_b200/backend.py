@@ -347,22 +347,24 @@ class B200CkksCore:
     def _to_coeff(self, data: torch.Tensor) -> torch.Tensor:
         return self.chain.ntt_inv(data.clone(), data.shape[-2])
 
-    def _encode_rns(self, values, level: int, ntt: bool = False) -> torch.Tensor:
-        """encode (encoding.py:57-65) -> [limbs, N] residues; cached per value."""
+    def _encode_rns(self, values, level: int, ntt: bool = False, scale: float = None,
+                    limit: float = MAX_SAFE_COEFF) -> torch.Tensor:
+        """encode (encoding.py:57-65) -> [limbs, N] residues at scale_at[level]
+        (or an explicit scale); cached per value."""
         vals = np.asarray(values, dtype=np.float64)
-        key = (vals.tobytes(), level, ntt)
+        key = (vals.tobytes(), level, ntt, scale)
         hit = self._enc_cache.get(key)
         if hit is not None:
             self._enc_cache.move_to_end(key)
             return hit
         ch = self.chain
         m = self._limbs(level)
-        coeffs = self.encoder.embed_device(vals, self._scale(level))
+        coeffs = self.encoder.embed_device(vals, self._scale(level) if scale is None else scale)
         bound = float(coeffs.abs().max())
-        if bound >= MAX_SAFE_COEFF:
+        if bound >= limit:
             raise self._errors.EncodingOverflow(
                 "scaled values exceed the exactly-representable coefficient range")
-        if 4.0 * bound >= float(ch.modulus_at(level)):
+        if 4 * int(bound) >= ch.modulus_at(level):
             raise self._errors.EncodingOverflow(
                 f"encoded coefficients (~2^{np.log2(bound + 1):.1f}) do not fit the current "
                 f"modulus with headroom")
@@ -496,6 +498,15 @@ class B200CkksCore:
         coeffs = self.chain.to_f64(self._phase(ct), m)[0]
         return self.encoder.unembed_device(coeffs, self._scale(ct.level)).cpu().numpy()
 
+    def decrypt_complex(self, ct: GpuCiphertext, scale: float = None) -> np.ndarray:
+        """Complex slot values (the reference decodes real parts only)."""
+        m = ct.data.shape[1]
+        coeffs = self.chain.to_f64(self._phase(ct), m)[0]
+        w = coeffs.to(torch.complex128) * self.encoder.twist
+        spec = torch.fft.ifft(w) * self.n
+        sc = self._scale(ct.level) if scale is None else scale
+        return (spec[self.encoder.bins] / sc).cpu().numpy()
+
     def _payload_decrypt(self, cv):
         return self._decrypt_values(cv.payload)
 
@@ -544,15 +555,17 @@ class B200CkksCore:
             keyset_id=self.keyset_id, serial=next(self._serials))
 
     # ------------------------------------------------------ bootstrapping helpers
-    def encode_complex_ntt(self, z, level: int, scale: float = None) -> torch.Tensor:
+    def encode_complex_ntt(self, z, level: int, scale: float = None) -> torch.Tensor:  # noqa: D401
         """Complex slot vector -> NTT-domain plaintext [limbs(level), N] at
         scale_at[level] (or `scale`)."""
         ch = self.chain
         m = self._limbs(level)
         coeffs = self.encoder.embed_complex_device(z, self._scale(level) if scale is None
                                                    else scale)
-        if float(coeffs.abs().max()) >= MAX_SAFE_COEFF:
-            raise self._errors.EncodingOverflow("complex plaintext exceeds 2^52")
+        # bootstrapping plaintexts are encoded at ~q_level (up to 2^61): float64
+        # rounding then costs 2^-52 relative, far below the ciphertext noise
+        if float(coeffs.abs().max()) >= float(2**62):
+            raise self._errors.EncodingOverflow("complex plaintext exceeds 2^62")
         res = ch.from_i64(coeffs.to(torch.int64), m)[0]
         return ch.ntt_fwd(res, m)
 

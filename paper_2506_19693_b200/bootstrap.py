@@ -41,6 +41,12 @@ def bootstrap_rotations(params, levels: int = 3) -> set:
 
 
 class Bootstrapper:
+    """Values inside are (data [2, m, N] NTT domain, level, scale) triples: the
+    bootstrapping levels (prime_layout="bootstrap": ~60-bit primes above the
+    refresh level) run at scale ~q0 ≈ 2^60 with every plaintext encoded at the
+    prime it is about to be divided by, so the noise floor is ~2^-45 of the
+    O(1) slot values while the user scale stays 2^scale_bits below."""
+
     def __init__(self, backend, K: int = 28, r: int = 2, degree: int = 119, levels: int = 3):
         be = self.be = backend
         ch = be.chain
@@ -48,87 +54,105 @@ class Bootstrapper:
         n = be.n
         slots = n // 2
         self.slots = slots
-        L = be.params.level
-        q0 = ch.entry_products[0]
-        self.q0 = q0
+        self.q0 = ch.entry_products[0]
         cts = BC.grouped_transform(slots, 2 * n, levels, inverse=True)
         stc = BC.grouped_transform(slots, 2 * n, levels, inverse=False)
-        # CtS overall scalar: value_L = V (c + q0 I)'/scale_L  ->  (c + q0 I)'/(2 q0 (K+1))
-        kappa = ch.scale_at[L] / (2.0 * q0 * (K + 1)) / slots
-        k_lvl = abs(kappa) ** (1.0 / levels)
-        cts = [{k: v * k_lvl for k, v in m.items()} for m in cts]
-        self.cts_plans = [BC.bsgs_plan(m, slots) for m in cts]
-        # StC overall scalar sigma = q0 / (2π scale_0), spread over the levels
-        sigma = q0 / (2.0 * math.pi * ch.scale_at[0])
-        s_lvl = sigma ** (1.0 / levels)
-        self.stc_plans = [BC.bsgs_plan({k: v * s_lvl for k, v in m.items()}, slots) for m in stc]
+        # raised ct read at scale q0 has slots V u', u = (c + q0 I)/q0; CoeffToSlot
+        # maps them to P u' / (2 (K+1)) (the 1/2 pairs with ct + conj(ct))
+        k_lvl = (1.0 / (2.0 * (K + 1) * slots)) ** (1.0 / levels)
+        self.cts_plans = [BC.bsgs_plan({k: v * k_lvl for k, v in m.items()}, slots)
+                          for m in cts]
+        # EvalMod leaves sin(2π u) ≈ 2π c/q0; SlotToCoeff multiplies by V P, and the
+        # factor sigma = q0 / (2π scale_0) is taken by the tracked scale (scale/sigma)
+        self.sigma = self.q0 / (2.0 * math.pi * ch.scale_at[0])
+        self.stc_plans = [BC.bsgs_plan(m, slots) for m in stc]
         self.cheb = BC.cheb_coeffs(BC.evalmod_function(K, r), degree)
         self._pt_cache: dict = {}
-        self._const_cache: dict = {}
-        two_n = 2 * n
-        self.conj = two_n - 1
-
-    # -- plaintext caches ------------------------------------------------------
-    def _pt(self, tag, level, z):
-        key = (tag, level)
-        hit = self._pt_cache.get(key)
-        if hit is None:
-            hit = self._pt_cache[key] = self.be.encode_complex_ntt(z, level)
-        return hit
+        self.conj = 2 * n - 1
 
     def _galois(self, step: int) -> int:
         return pow(5, step % self.slots, 2 * self.be.n)
 
-    # -- homomorphic building blocks on (data, level) pairs ----------------------
+    def _q(self, level: int) -> float:
+        return float(self.be.chain.entry_products[level])
+
+    # -- tracked-scale arithmetic --------------------------------------------------
+    def _drop_to(self, x, level: int, scale: float):
+        """Bring x down to `level` landing exactly on `scale` (restrict, integer
+        factor, rescale: the reference's adjust trick with tracked scales)."""
+        data, lvl, sc = x
+        if lvl == level:
+            return x
+        be, ch = self.be, self.be.chain
+        staging = level + 1
+        ms = be._limbs(staging)
+        factor = int(round(scale * self._q(staging) / sc))
+        src = data if ms == data.shape[-2] else data[..., :ms, :].contiguous()
+        y = ch.scalar_mul(src, ch.scalar_pairs(factor, range(ms)), ms)
+        out = be._rescale_data(y, staging)
+        return out, level, sc * factor / self._q(staging)
+
     def _align(self, a, b):
-        (da, la), (db, lb) = a, b
-        if la > lb:
-            da, la = self.be._adjust_data(da, la, lb), lb
-        elif lb > la:
-            db, lb = self.be._adjust_data(db, lb, la), la
-        return da, db, la
+        if a[1] > b[1]:
+            a = self._drop_to(a, b[1], b[2])
+        elif b[1] > a[1]:
+            b = self._drop_to(b, a[1], a[2])
+        return a, b
 
-    def _add(self, a, b):
-        da, db, lvl = self._align(a, b)
-        return self.be.chain.add(da, db, self.be._limbs(lvl)), lvl
-
-    def _sub(self, a, b):
-        da, db, lvl = self._align(a, b)
-        return self.be.chain.sub(da, db, self.be._limbs(lvl)), lvl
+    def _add(self, a, b, sub=False):
+        a, b = self._align(a, b)
+        if abs(a[2] - b[2]) > 2.0**-40 * abs(a[2]):
+            raise RuntimeError(f"adding ciphertexts with scales {a[2]} != {b[2]} at level {a[1]}")
+        m = self.be._limbs(a[1])
+        f = self.be.chain.sub if sub else self.be.chain.add
+        return f(a[0], b[0], m), a[1], a[2]
 
     def _mul(self, a, b):
-        da, db, lvl = self._align(a, b)
-        out = self.be._hmult(da.unsqueeze(0).contiguous(), db.unsqueeze(0).contiguous(), lvl)
-        return out[0], lvl - 1
+        a, b = self._align(a, b)
+        out = self.be._hmult(a[0].unsqueeze(0).contiguous(), b[0].unsqueeze(0).contiguous(), a[1])
+        return out[0], a[1] - 1, a[2] * b[2] / self._q(a[1])
 
-    def _mul_const(self, a, c: float):
-        da, lvl = a
-        key = (float(c), lvl)
-        pt = self._const_cache.get(key)
-        if pt is None:
-            pt = self._const_cache[key] = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True)
+    def _mul_const(self, a, c: float, out_scale: float = None):
+        """c * a, one level; lands exactly on out_scale (default: a's scale)."""
+        data, lvl, sc = a
+        q = self._q(lvl)
+        pt_scale = q if out_scale is None else out_scale * q / sc
+        pt = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True, scale=pt_scale,
+                                 limit=2.0**62)
         m = self.be._limbs(lvl)
-        return self.be._rescale_data(self.be.chain.mul(da, pt, m, b_rows=m), lvl), lvl - 1
+        out = self.be._rescale_data(self.be.chain.mul(data, pt, m, b_rows=m), lvl)
+        return out, lvl - 1, sc * pt_scale / q
+
+    def _restrict(self, a, level: int):
+        """Drop limbs down to `level` (exact; the scale is unchanged)."""
+        data, lvl, sc = a
+        if lvl == level:
+            return a
+        assert lvl > level
+        return data[:, : self.be._limbs(level)].contiguous(), level, sc
 
     def _add_const(self, a, c: float):
-        da, lvl = a
+        data, lvl, sc = a
         m = self.be._limbs(lvl)
-        pt = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True)
-        out = da.clone()
-        self.be.chain.add(da[0], pt, m, out=out[0])
-        return out, lvl
+        pt = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True, scale=sc, limit=2.0**62)
+        out = data.clone()
+        self.be.chain.add(data[0], pt, m, out=out[0])
+        return out, lvl, sc
 
     def _double(self, a):
-        da, lvl = a
-        return self.be.chain.add(da, da, self.be._limbs(lvl)), lvl
+        return self.be.chain.add(a[0], a[0], self.be._limbs(a[1])), a[1], a[2]
 
     # -- linear transforms ------------------------------------------------------------
-    def _linear(self, x, plan, tag):
-        """sum_g rot(sum_b pt_gb * rot(x, b s), g n1 s) with hoisted baby steps."""
+    def _linear(self, x, plan, tag, out_scale: float = None):
+        """sum_g rot(sum_b pt_gb * rot(x, b s), g n1 s), hoisted baby steps.  The
+        diagonals are encoded at q_level (scale preserved) or so that the result
+        lands on out_scale."""
         be, ch = self.be, self.be.chain
-        data, lvl = x
+        data, lvl, sc = x
         s, n1, rows = plan
         m = be._limbs(lvl)
+        q = self._q(lvl)
+        pt_scale = q if out_scale is None else out_scale * q / sc
         babies = sorted({b for row in rows.values() for b in row if b})
         rots = dict(zip(babies, be.hoisted_rotations(data, lvl, [self._galois(b * s)
                                                                  for b in babies])))
@@ -137,14 +161,17 @@ class Bootstrapper:
         for g, row in sorted(rows.items()):
             inner = None
             for b, diag in row.items():
-                pt = self._pt((tag, g, b), lvl, diag)
+                key = (tag, g, b, lvl, pt_scale)
+                pt = self._pt_cache.get(key)
+                if pt is None:
+                    pt = self._pt_cache[key] = be.encode_complex_ntt(diag, lvl, scale=pt_scale)
                 term = ch.mul(rots[b], pt, m, b_rows=m)
                 inner = term if inner is None else ch.add(inner, term, m, out=inner)
             inner = be._rescale_data(inner, lvl)
             if g:
                 inner = be.rotate_data(inner, lvl - 1, self._galois(g * n1 * s))
             acc = inner if acc is None else ch.add(acc, inner, be._limbs(lvl - 1), out=acc)
-        return acc, lvl - 1
+        return acc, lvl - 1, sc * pt_scale / q
 
     # -- EvalMod ------------------------------------------------------------------
     def _chebyshev_basis(self, x):
@@ -158,7 +185,7 @@ class Bootstrapper:
                 T[k] = self._add_const(self._double(self._mul(h, h)), -1.0)
             else:
                 a, b = get(k // 2), get(k // 2 + 1)
-                T[k] = self._sub(self._double(self._mul(a, b)), get(1))
+                T[k] = self._add(self._double(self._mul(a, b)), get(1), sub=True)
             return T[k]
 
         for k in range(2, 17):
@@ -167,21 +194,25 @@ class Bootstrapper:
         get(64)
         return T
 
-    def _eval_cheb(self, c, T):
+    def _eval_cheb(self, c, T, level: int, scale: float):
+        """sum_k c_k T_k as a ciphertext exactly at (level, scale): every term
+        is steered onto the target by the scale of its coefficient plaintext
+        (leaves) or of its quotient (giant-step products), so same-level
+        additions never mix scales."""
         c = np.asarray(c, dtype=np.float64)
         deg = len(c) - 1
-        while deg > 0 and abs(c[deg]) < 1e-300:
+        while deg > 0 and c[deg] == 0.0:
             deg -= 1
         c = c[: deg + 1]
         if deg < 16:
             acc = None
             for k in range(1, deg + 1):
-                if abs(c[k]) < 1e-18:
+                if c[k] == 0.0:
                     continue
-                term = self._mul_const(T[k], c[k])
+                term = self._mul_const(self._restrict(T[k], level + 1), c[k], out_scale=scale)
                 acc = term if acc is None else self._add(acc, term)
             if acc is None:
-                acc = self._mul_const(T[1], 0.0)
+                acc = self._mul_const(self._restrict(T[1], level + 1), 0.0, out_scale=scale)
             return self._add_const(acc, c[0])
         n = 1 << (deg.bit_length() - 1)
         q = np.zeros(deg - n + 1)
@@ -190,11 +221,20 @@ class Bootstrapper:
         rem = c[:n].copy()
         for j in range(1, deg - n + 1):
             rem[n - j] -= c[n + j]
-        return self._add(self._mul(self._eval_cheb(q, T), T[n]), self._eval_cheb(rem, T))
+        tn = self._restrict(T[n], level + 1)
+        qv = self._eval_cheb(q, T, level + 1, scale * self._q(level + 1) / tn[2])
+        prod = self._mul(qv, tn)
+        return self._add(prod, self._eval_cheb(rem, T, level, scale))
+
+    def _cheb_level(self, T, deg: int) -> int:
+        """Lowest-depth target level: leaves need T_1..T_15 one level above."""
+        leaf = min(T[k][1] for k in range(1, 16)) - 1
+        splits = max(0, deg.bit_length() - 4)  # giant steps 16, 32, 64, ...
+        return leaf - splits
 
     def _evalmod(self, x):
         T = self._chebyshev_basis(x)
-        y = self._eval_cheb(self.cheb, T)
+        y = self._eval_cheb(self.cheb, T, self._cheb_level(T, len(self.cheb) - 1), x[2])
         for _ in range(self.r):
             y = self._add_const(self._double(self._mul(y, y)), -1.0)
         return y
@@ -203,28 +243,30 @@ class Bootstrapper:
     def bootstrap(self, ct: GpuCiphertext) -> GpuCiphertext:
         be, ch = self.be, self.be.chain
         raised = be.mod_raise(ct)
-        x = (raised.data, raised.level)
+        x = (raised.data, raised.level, float(self.q0))  # read at scale q0: slots = V u'
         for t, plan in enumerate(self.cts_plans):
             x = self._linear(x, plan, ("cts", t))
-        data, lvl = x
+        data, lvl, sc = x
         m = be._limbs(lvl)
         conj = be.rotate_data(data, lvl, self.conj)
-        re = (ch.add(data, conj, m), lvl)
-        diff = ch.sub(data, conj, m)
-        mono = be.monomial_ntt(3 * be.n // 2, lvl)  # -X^{N/2} = X^{3N/2}
-        im = (ch.mul(diff, mono, m, b_rows=m), lvl)
+        re = (ch.add(data, conj, m), lvl, sc)
+        mono = be.monomial_ntt(3 * be.n // 2, lvl)  # -X^{N/2}: multiplies slots by -i
+        im = (ch.mul(ch.sub(data, conj, m), mono, m, b_rows=m), lvl, sc)
         y_re = self._evalmod(re)
         y_im = self._evalmod(im)
-        d_im, l_im = y_im
+        d_im, l_im, s_im = y_im
         y_im = (ch.mul(d_im, be.monomial_ntt(be.n // 2, l_im), be._limbs(l_im),
-                       b_rows=be._limbs(l_im)), l_im)
+                       b_rows=be._limbs(l_im)), l_im, s_im)
         z = self._add(y_re, y_im)
-        for t, plan in enumerate(self.stc_plans):
-            z = self._linear(z, plan, ("stc", t))
-        data, lvl = z
+        z = (z[0], z[1], z[2] / self.sigma)
         rl = be.params.refresh_level
+        for t, plan in enumerate(self.stc_plans):
+            last = t == len(self.stc_plans) - 1
+            target = ch.scale_at[z[1] - 1] if last else None
+            z = self._linear(z, plan, ("stc", t), out_scale=target)
+        data, lvl, sc = z
         if lvl > rl:
-            data, lvl = be._adjust_data(data, lvl, rl), rl
+            data, lvl, sc = self._drop_to(z, rl, ch.scale_at[rl])
         if lvl < rl:
             raise RuntimeError(f"bootstrapping consumed too many levels ({lvl} < {rl})")
         return GpuCiphertext(data, lvl)

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256) k_ks_inner(
 // Exact divide-and-round (rescale / ModDown / level adjust)
 // ===========================================================================
 
-constexpr int kMaxDrop = 8;
+constexpr int kMaxDrop = 16;
 
 // acc - r * M  (mod p) for a signed centered remainder r and a Shoup constant M.
 __device__ __forceinline__ uint64_t sub_rm(uint64_t acc, int64_t r, uint64_t M, uint64_t Ms,
@@ -800,7 +800,8 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   const size_t total = (size_t)polys << R.log_n;
   if (!total) return 0;
   const size_t stride = in_poly_stride > 0 ? (size_t)in_poly_stride : ((size_t)limbs << R.log_n);
-  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4 : 8;
+  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4
+               : n_drop1 <= 8 ? 8 : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
   const int grid = grid_for(total, 256);
   cudaStream_t st = (cudaStream_t)stream;
@@ -818,6 +819,7 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
   CKB_DR(2, 0) CKB_DR(2, 1) CKB_DR(2, 2) CKB_DR(2, 8)
   CKB_DR(4, 0) CKB_DR(4, 1) CKB_DR(4, 2) CKB_DR(4, 8)
   CKB_DR(8, 0) CKB_DR(8, 1) CKB_DR(8, 2) CKB_DR(8, 8)
+  CKB_DR(16, 0) CKB_DR(16, 1) CKB_DR(16, 2)
 #undef CKB_DR
   return CKB_E_ARG;
 }
@@ -878,7 +880,8 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   const RingDev R = make_ring(ring);
   const size_t total = (size_t)polys << R.log_n;
   if (!total) return 0;
-  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4 : 8;
+  const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4
+               : n_drop1 <= 8 ? 8 : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
   const int grid = grid_for(total, 256);
   cudaStream_t st = (cudaStream_t)stream;
@@ -894,6 +897,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   CKB_DC(2, 0) CKB_DC(2, 1) CKB_DC(2, 2) CKB_DC(2, 8)
   CKB_DC(4, 0) CKB_DC(4, 1) CKB_DC(4, 2) CKB_DC(4, 8)
   CKB_DC(8, 0) CKB_DC(8, 1) CKB_DC(8, 2) CKB_DC(8, 8)
+  CKB_DC(16, 0) CKB_DC(16, 1) CKB_DC(16, 2)
 #undef CKB_DC
   return CKB_E_ARG;
 }

@@ -10,6 +10,12 @@ Three layouts:
 ``baseline``   — BASELINE.json's rule: one prime per chain entry of <= 60 bits,
                  the largest prime = 1 mod 2N below 2^bits (wider entries become
                  ceil(bits/60) such primes).  Used for configs 1-2.
+``bootstrap``  — for parameter sets with bootstrap_depth > 0: the user levels
+                 1..refresh_level follow ``schedule`` at 2^scale_bits, the
+                 bootstrapping levels above use the largest primes below
+                 2^bits of their chain entries (~60 bits), where the
+                 bootstrapper tracks scales itself (bootstrap.py); scale_at
+                 is nominal above refresh_level.
 ``schedule``   — one prime per entry, rescale primes nearest to
                  scale_at[l]^2 / 2^scale_bits top-down (the reference's
                  schedule-stabilising rule with single word-size primes); keeps
@@ -129,6 +135,20 @@ def build_chain(params, layout: str = "reference"):
             entry = split_entry(scale_at[lv] ** 2 / nominal, two_n, used)
             rescale[lv - 1] = entry
             scale_at[lv - 1] = scale_at[lv] ** 2 / math.prod(entry)
+    elif layout == "bootstrap":
+        base = _wide(chain[0], two_n, used)
+        special = _wide(chain[-1], two_n, used)
+        rl = params.refresh_level
+        for lv in range(level, rl, -1):
+            p = largest_below(chain[lv], two_n, used)
+            used.add(p)
+            rescale[lv - 1] = [p]
+            scale_at[lv - 1] = nominal
+        for lv in range(rl, 0, -1):
+            p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS)
+            used.add(p)
+            rescale[lv - 1] = [p]
+            scale_at[lv - 1] = scale_at[lv] ** 2 / p
     elif layout in ("baseline", "schedule"):
         base = _wide(chain[0], two_n, used)
         special = _wide(chain[-1], two_n, used)

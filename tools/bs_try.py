@@ -9,11 +9,11 @@ from paper_2506_19693_b200.bootstrap import Bootstrapper, bootstrap_rotations
 logn = int(sys.argv[1]) if len(sys.argv) > 1 else 13
 n = 1 << logn
 L = 24
-params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * L + (420,), scale_bits=45,
+params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,), scale_bits=45,
                       level=L, bootstrap_depth=16)
 t0 = time.time()
 rots = bootstrap_rotations(params)
-cust = he_api.keygen(params, rots, backend="ckks", rng_seed=1, prime_layout="schedule",
+cust = he_api.keygen(params, rots, backend="ckks", rng_seed=1, prime_layout="bootstrap",
                      dnum=3, secret_hw=192, conjugation_key=True)
 be = cust.backend
 torch.cuda.synchronize()
