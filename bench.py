@@ -249,6 +249,43 @@ def run_c1_train(device_index):
             "reference_cpu_s_per_step_build_container": ref_s}
 
 
+def run_c3_bootstrap():
+    """Config 3: full-slot bootstrapping of one ciphertext at N=2^16 (2^15 slots,
+    U[-1,1]), input at level 0, HW-192 secret, CtS/StC 3 BSGS levels each,
+    EvalMod = degree-119 Chebyshev + 2 double-angle steps (bootstrap.py)."""
+    import torch
+
+    from paper_2506_19693_b200 import he_api
+    from paper_2506_19693_b200.scheme import SchemeParams
+
+    n, L = 1 << 16, 24
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                          scale_bits=45, level=L, bootstrap_depth=16)
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, set(), backend="ckks", rng_seed=11, prime_layout="bootstrap",
+                         dnum=3, secret_hw=192, real_bootstrap=True)
+    be = cust.backend
+    torch.cuda.synchronize()
+    keygen_s = time.perf_counter() - t0
+    rng = np.random.default_rng(3)
+    v = rng.uniform(-1, 1, n // 2)
+    ct = be._encrypt_values(v, 0)
+    times = []
+    out = None
+    for rep in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = be.bootstrap_ct(ct)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    err = float(np.max(np.abs(be._decrypt_values(out) - v)))
+    return {"ms": 1e3 * float(np.median(times[1:])), "first_call_ms": 1e3 * times[0],
+            "max_abs_err": err, "precision_bits": -math.log2(err), "level_out": out.level,
+            "keys": len(be.rotation_keys) + 1, "keygen_s": keygen_s,
+            "params": "N=2^16, 2^15 slots, Q = 60 + 8x45 (user) + 16x60 (bootstrap) bits, "
+                      "P = 11x60, dnum=3, HW 192, K=28, Chebyshev 119 + 2 double angles"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -260,6 +297,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -428,6 +466,11 @@ def main():
             line["c1_train"] = run_c1_train(local)
         except Exception as exc:  # report, never hide
             line["c1_train"] = {"error": repr(exc)}
+    if rank == 0 and world == 1 and not args.no_c3:
+        try:
+            line["c3_bootstrap"] = run_c3_bootstrap()
+        except Exception as exc:
+            line["c3_bootstrap"] = {"error": repr(exc)}
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import parallel_ref as PR
 

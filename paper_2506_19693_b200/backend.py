@@ -154,7 +154,7 @@ class B200CkksCore:
     def __init__(self, params, rotation_indices=(), rng_seed: int = 0, bootstrap_eps: float = 0.0,
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
-                 conjugation_key: bool = False):
+                 conjugation_key: bool = False, real_bootstrap: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -171,12 +171,27 @@ class B200CkksCore:
         self.rng_seed = rng_seed
         self.bootstrap_eps = bootstrap_eps
         self.rotation_indices = frozenset(int(k) for k in rotation_indices)
+        self.real_bootstrap = bool(real_bootstrap)
+        key_steps = set(self.rotation_indices)
+        if self.real_bootstrap:
+            if prime_layout != "bootstrap" or not params.bootstrap_depth:
+                raise self._errors.InvalidParameters(
+                    "real_bootstrap needs prime_layout='bootstrap' and bootstrap_depth > 0")
+            from .bootstrap import bootstrap_rotations
+
+            key_steps |= bootstrap_rotations(params)
+            conjugation_key = True
+        self._bootstrapper = None
         self.alpha = 1 if dnum is None else max(1, -(-ch.lq // int(dnum)))
         self.dnum = dnum
         self._bconv_cache: dict = {}
         self._adjust_cache: dict = {}
         self._enc_cache: collections.OrderedDict = collections.OrderedDict()
         self._enc_cache_cap = encode_cache
+        # the reference's 2^52 exactness guard (encoding.py:46-48); the bootstrap
+        # layout encodes top-level values at ~2^60 where float64 rounding
+        # (2^-52 relative) is far below the noise
+        self._encode_limit = float(2**62) if prime_layout == "bootstrap" else MAX_SAFE_COEFF
         rng = np.random.default_rng(rng_seed)
         coeffs = rng.integers(-1, 2, self.n).astype(np.int64)  # ring.py:161-162
         if secret_hw is not None:
@@ -189,7 +204,7 @@ class B200CkksCore:
         self.rotation_keys: dict = {}
         slots = params.slot_count
         s_coeff = ch.ntt_inv(self.sk.s_full.clone(), len(ch.all_primes), ch.all_map())
-        for step in sorted({k % slots for k in self.rotation_indices} - {0}):
+        for step in sorted({k % slots for k in key_steps} - {0}):
             g = pow(5, step, 2 * self.n)
             self.galois_for_step[step] = g
             s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
@@ -348,7 +363,7 @@ class B200CkksCore:
         return self.chain.ntt_inv(data.clone(), data.shape[-2])
 
     def _encode_rns(self, values, level: int, ntt: bool = False, scale: float = None,
-                    limit: float = MAX_SAFE_COEFF) -> torch.Tensor:
+                    limit: float = None) -> torch.Tensor:
         """encode (encoding.py:57-65) -> [limbs, N] residues at scale_at[level]
         (or an explicit scale); cached per value."""
         vals = np.asarray(values, dtype=np.float64)
@@ -361,7 +376,7 @@ class B200CkksCore:
         m = self._limbs(level)
         coeffs = self.encoder.embed_device(vals, self._scale(level) if scale is None else scale)
         bound = float(coeffs.abs().max())
-        if bound >= limit:
+        if bound >= (self._encode_limit if limit is None else limit):
             raise self._errors.EncodingOverflow(
                 "scaled values exceed the exactly-representable coefficient range")
         if 4 * int(bound) >= ch.modulus_at(level):
@@ -512,7 +527,12 @@ class B200CkksCore:
 
     def _payload_bootstrap(self, cv, serial: int):
         """Custodian refresh (backend.py:195-206): decrypt, optional U(+-eps),
-        re-encrypt at refresh_level."""
+        re-encrypt at refresh_level.  With real_bootstrap=True the ciphertext is
+        instead dropped to level 0 and bootstrapped homomorphically
+        (bootstrap.py); the serial is still consumed as the refresh would."""
+        if self.real_bootstrap:
+            next(self._serials)
+            return self.bootstrap_ct(cv.payload)
         values = self._decrypt_values(cv.payload)
         if self.bootstrap_eps > 0.0:
             values = values + self._bs_rng.uniform(-self.bootstrap_eps, self.bootstrap_eps,
@@ -604,6 +624,16 @@ class B200CkksCore:
                                 addend_period=2, addend_stride=1, basis=ch.ext_basis(m))
             out.append(r.view(2, m, self.n))
         return out
+
+    def bootstrap_ct(self, ct: GpuCiphertext) -> GpuCiphertext:
+        """Homomorphic bootstrapping of a payload (any level) to refresh_level."""
+        if self._bootstrapper is None:
+            from .bootstrap import Bootstrapper
+
+            self._bootstrapper = Bootstrapper(self)
+        if ct.level > 0:
+            ct = GpuCiphertext(self._adjust_data(ct.data, ct.level, 0), 0)
+        return self._bootstrapper.bootstrap(ct)
 
     def rotate_data(self, data: torch.Tensor, level: int, galois: int) -> torch.Tensor:
         return self._hrot(data.unsqueeze(0), level, galois=galois,

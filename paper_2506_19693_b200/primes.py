@@ -13,9 +13,11 @@ Three layouts:
 ``bootstrap``  — for parameter sets with bootstrap_depth > 0: the user levels
                  1..refresh_level follow ``schedule`` at 2^scale_bits, the
                  bootstrapping levels above use the largest primes below
-                 2^bits of their chain entries (~60 bits), where the
-                 bootstrapper tracks scales itself (bootstrap.py); scale_at
-                 is nominal above refresh_level.
+                 2^bits of their chain entries (~60 bits).  The level schedule
+                 stays exact: above refresh_level scale_at[l] =
+                 sqrt(scale_at[l-1] q_l), rising towards q (fresh encryptions at
+                 the top are encoded at ~2^60); the bootstrapper itself tracks
+                 scales explicitly (bootstrap.py).
 ``schedule``   — one prime per entry, rescale primes nearest to
                  scale_at[l]^2 / 2^scale_bits top-down (the reference's
                  schedule-stabilising rule with single word-size primes); keeps
@@ -139,16 +141,20 @@ def build_chain(params, layout: str = "reference"):
         base = _wide(chain[0], two_n, used)
         special = _wide(chain[-1], two_n, used)
         rl = params.refresh_level
+        top_primes = {}
         for lv in range(level, rl, -1):
             p = largest_below(chain[lv], two_n, used)
             used.add(p)
-            rescale[lv - 1] = [p]
-            scale_at[lv - 1] = nominal
+            top_primes[lv] = p
+        scale_at[rl] = nominal
         for lv in range(rl, 0, -1):
             p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS)
             used.add(p)
             rescale[lv - 1] = [p]
             scale_at[lv - 1] = scale_at[lv] ** 2 / p
+        for lv in range(rl + 1, level + 1):  # consistent upward: s_l = sqrt(s_{l-1} q_l)
+            rescale[lv - 1] = [top_primes[lv]]
+            scale_at[lv] = math.sqrt(scale_at[lv - 1] * top_primes[lv])
     elif layout in ("baseline", "schedule"):
         base = _wide(chain[0], two_n, used)
         special = _wide(chain[-1], two_n, used)

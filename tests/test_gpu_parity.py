@@ -420,3 +420,30 @@ def test_wave_executor_bit_identical_to_sequential(c1_program):
         a = seq.backend.planes_of(env_seq[o].payload)
         b = bat.backend.planes_of(env_bat[o])
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# Config 3: homomorphic bootstrapping (no reference counterpart: parity
+# unpinned; the check is decrypt(bootstrap(ct)) against the input values)
+# ---------------------------------------------------------------------------
+
+
+def test_real_bootstrap_precision_n8192():
+    n, L = 1 << 13, 24
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                          scale_bits=45, level=L, bootstrap_depth=16)
+    cust = he_api.keygen(params, {1}, backend="ckks", rng_seed=1, prime_layout="bootstrap",
+                         dnum=3, secret_hw=192, real_bootstrap=True)
+    be = cust.backend
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-1, 1, n // 2)
+    ct = cust.encrypt(he_api.make_plain(v, n // 2, 45.0))
+    # consume levels, then refresh through the HE API
+    ct = cust.evaluator.mul(ct, he_api.make_plain(np.ones(n // 2), n // 2, 45.0))
+    r = cust.bootstrap(ct)
+    assert r.level_remaining == params.refresh_level
+    err = np.max(np.abs(cust.decrypt(r).values - v))
+    assert err <= 2.0**-15, err
+    # the refreshed ciphertext keeps computing
+    sq = cust.evaluator.mul(r, r)
+    assert np.max(np.abs(cust.decrypt(sq).values - v * v)) <= 2.0**-14
