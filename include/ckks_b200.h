@@ -39,7 +39,7 @@ extern "C" {
 /* Device-resident tables for one ring degree and one prime chain.
  *   mods : [n_primes][16] {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
  *                          psi_inv_brv[1]*N^-1, shoup(.), 2^64 mod p, shoup(.), 0...}
- *   ntt  : [n_primes][4][N] {psi_brv, shoup(psi_brv), inv_psi_brv, shoup(inv_psi_brv)}
+ *   ntt  : [n_primes][2][N][2] {psi_brv[j], shoup(.)} pairs, then {inv_psi_brv[j], shoup(.)}
  *   pair : [n_primes][n_primes][4] {p_i^-1 mod p_j, shoup(.), p_i mod p_j, 0}
  * Built on the host by ckb_build_tables, uploaded by the caller. */
 typedef struct {
@@ -180,6 +180,13 @@ int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, in
  * below 2^60 cannot overflow), SURVEY §8(e). */
 int ckb_reduce(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows, int limbs,
                const int32_t* limb_prime, void* stream);
+
+/* Device sampling (ring.py:148-158 distributions; counter-based Philox4x32-10):
+ * a: [items][limbs][N] uniform residues mod each limb's prime (or NULL),
+ * e: [items][N] rint(N(0, sigma^2)) int64 (or NULL); seeds: DEVICE [items] u64,
+ * one independent stream per item, so batched and one-at-a-time sampling agree. */
+int ckb_sample(const ckb_ring* ring, uint64_t* a, int64_t* e, const uint64_t* seeds, int items,
+               int limbs, const int32_t* limb_prime, double sigma, void* stream);
 
 /* Signed int64 coefficients -> residues (ring.py:139-145):
  * in: [polys][N] int64; out: [polys][limbs][N]. */

@@ -154,7 +154,8 @@ class B200CkksCore:
     def __init__(self, params, rotation_indices=(), rng_seed: int = 0, bootstrap_eps: float = 0.0,
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
-                 conjugation_key: bool = False, real_bootstrap: bool = False):
+                 conjugation_key: bool = False, real_bootstrap: bool = False,
+                 sampler: str = None):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -170,6 +171,14 @@ class B200CkksCore:
         self.encoder = DeviceEncoder(self.n, self.device)
         self.rng_seed = rng_seed
         self.bootstrap_eps = bootstrap_eps
+        # "numpy": the reference's default_rng streams (bit-exact keys/encryptions,
+        # ring.py:148-162, backend.py:174); "philox": counter-based device
+        # sampling (ckb_sample), one stream per (seed, serial) — the default
+        # off the reference prime layout, where no bit-exact stream exists.
+        self.sampler = sampler or ("numpy" if prime_layout == "reference" else "philox")
+        if self.sampler not in ("numpy", "philox"):
+            raise self._errors.InvalidParameters(f"unknown sampler {self.sampler!r}")
+        self._ksk_count = 0
         self.rotation_indices = frozenset(int(k) for k in rotation_indices)
         self.real_bootstrap = bool(real_bootstrap)
         key_steps = set(self.rotation_indices)
@@ -239,10 +248,20 @@ class B200CkksCore:
         digits = [(lo, min(lo + self.alpha, ch.lq)) for lo in range(0, ch.lq, self.alpha)]
         out = torch.empty(len(digits), 2, kl, self.n, dtype=U64, device=self.device)
         for j, (lo, hi) in enumerate(digits):
-            a_np = np.stack([rng.integers(0, p, self.n, dtype=np.uint64) for p in full])
-            e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
-            a = ch.upload_u64(a_np)
-            e = ch.from_i64(torch.from_numpy(e_np).to(self.device), kl, amap)[0]
+            if self.sampler == "philox":
+                seed = torch.tensor([_mix64(self.rng_seed, 0x4B45590000 + self._ksk_count, j)],
+                                    dtype=torch.int64, device=self.device).view(U64)
+                a_d, e_d = ch.sample(seed, kl, lmap=amap)
+                a_np = None
+            else:
+                a_np = np.stack([rng.integers(0, p, self.n, dtype=np.uint64) for p in full])
+                e_np = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
+            if a_np is None:
+                a = a_d[0]
+                e = ch.from_i64(e_d, kl, amap)[0]
+            else:
+                a = ch.upload_u64(a_np)
+                e = ch.from_i64(torch.from_numpy(e_np).to(self.device), kl, amap)[0]
             ch.ntt_fwd(e, kl, amap)
             b = ch.mul(a, self.sk.s_full, kl, lmap=amap)
             ch.sub(e, b, kl, out=b, lmap=amap)  # b = -a*s + e
@@ -254,6 +273,7 @@ class B200CkksCore:
             out[j, 0] = b
             out[j, 1] = a
             rows.append(j)
+        self._ksk_count += 1
         return KeySwitchKey(out)
 
     def rotation_key(self, galois: int) -> KeySwitchKey:
@@ -477,9 +497,19 @@ class B200CkksCore:
         primes = ch.limbs_at(level)
         m = len(primes)
         bsz = len(values_list)
+        msgs = []
+        if self.sampler == "philox":
+            srs = [next(self._serials) if sr is None else sr for sr in serials]
+            seeds = torch.tensor([_mix64(self.rng_seed, 0x454E43, sr) for sr in srs],
+                                 dtype=torch.int64, device=self.device).view(U64)
+            a_d, e_d = ch.sample(seeds, m)
+            msgs = [self._encode_rns(values, level) for values in values_list]
+            out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)
+            out[:, 1].copy_(a_d)
+            me = ch.from_i64(e_d, m)
+            return self._finish_encrypt(out, me, msgs, m)
         a_np = np.empty((bsz, m, self.n), dtype=np.uint64)
         e_np = np.empty((bsz, self.n), dtype=np.int64)
-        msgs = []
         for i, (values, serial) in enumerate(zip(values_list, serials)):
             msgs.append(self._encode_rns(values, level))
             sr = next(self._serials) if serial is None else serial
@@ -490,6 +520,11 @@ class B200CkksCore:
         out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)
         out[:, 1].copy_(torch.from_numpy(a_np))
         me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)  # [B, m, N]
+        return self._finish_encrypt(out, me, msgs, m)
+
+    def _finish_encrypt(self, out, me, msgs, m):
+        """c1 = a (NTT domain), c0 = NTT(m + e) - a*s."""
+        ch = self.chain
         ch.add(me, torch.stack(msgs), m, out=me)
         ch.ntt_fwd(me, m)
         a_s = ch.mul(out[:, 1].contiguous(), self.sk.s_full[:m], m, b_rows=m)
@@ -702,6 +737,16 @@ class B200CkksCore:
     def planes_of(self, payload: GpuCiphertext) -> np.ndarray:
         """Coefficient-domain (2, limbs, N) planes of a payload (RBCT order)."""
         return self._to_coeff(payload.data).cpu().numpy()
+
+
+def _mix64(*parts) -> int:
+    """splitmix64-style hash of integers -> a 64-bit Philox key (signed for torch)."""
+    x = 0x9E3779B97F4A7C15
+    for v in parts:
+        x = (x ^ (int(v) & 0xFFFFFFFFFFFFFFFF)) * 0xBF58476D1CE4E5B9 & 0xFFFFFFFFFFFFFFFF
+        x = (x ^ (x >> 31)) * 0x94D049BB133111EB & 0xFFFFFFFFFFFFFFFF
+        x ^= x >> 29
+    return x - (1 << 64) if x >= 1 << 63 else x
 
 
 def _hw_secret(n: int, h: int, seed: int) -> np.ndarray:

@@ -44,6 +44,7 @@ struct NttPhase {
   int last;     // forward: canonicalise; inverse: fold N^-1 into the top stage
   int row0;     // first row handled by this launch (for L2-resident chunking)
   int logC;     // log2(C)
+  int items;    // > 0: rows enumerated limb-major (rows = items * limbs)
 };
 
 // Shared-memory slot of element r of group g: one pad word per 16 elements
@@ -79,8 +80,8 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t W, ui
 // The twiddle of the butterfly at k is tw[t0(b) + (k >> (bb+1))]: only
 // 1, 2, 4, 8 distinct values per stage, loaded once each.
 template <int S, int RB, int HI>
-__device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
-                                           const uint64_t* __restrict__ tws, uint64_t p,
+__device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __restrict__ tw,
+                                           uint64_t p,
                                            uint64_t two_p, int gq, int tbase, int w, int last) {
   if constexpr (HI > 0) {
     constexpr int E = 1 << RB;  // elements per thread
@@ -99,8 +100,9 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restri
 #pragma unroll
       for (int i = 0; i < E / 2; ++i) {
         if (i < ((E / 2) >> bb)) {
-          Wv[i] = __ldg(tw + t0 + i);
-          Wsv[i] = __ldg(tws + t0 + i);
+          const ulonglong2 wp = __ldg(tw + t0 + i);  // {w, shoup(w)}
+          Wv[i] = wp.x;
+          Wsv[i] = wp.y;
         }
       }
 #pragma unroll
@@ -121,13 +123,13 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const uint64_t* __restri
 #pragma unroll
     for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    fwd_rounds<S, RB, LO>(s, tw, tws, p, two_p, gq, tbase, w, last);
+    fwd_rounds<S, RB, LO>(s, tw, p, two_p, gq, tbase, w, last);
   }
 }
 
 template <int S, int RB, int LO>
-__device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restrict__ tw,
-                                           const uint64_t* __restrict__ tws, uint64_t p,
+__device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __restrict__ tw,
+                                           uint64_t p,
                                            uint64_t two_p, uint64_t ninv, uint64_t ninvs,
                                            uint64_t fw, uint64_t fws, int gq, int tbase, int w,
                                            int last) {
@@ -160,8 +162,9 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restri
 #pragma unroll
         for (int i = 0; i < E / 2; ++i) {
           if (i < ((E / 2) >> bb)) {
-            Wv[i] = __ldg(tw + t0 + i);
-            Wsv[i] = __ldg(tws + t0 + i);
+            const ulonglong2 wp = __ldg(tw + t0 + i);
+            Wv[i] = wp.x;
+            Wsv[i] = wp.y;
           }
         }
 #pragma unroll
@@ -175,7 +178,7 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const uint64_t* __restri
 #pragma unroll
     for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
     __syncthreads();
-    inv_rounds<S, RB, HI>(s, tw, tws, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
+    inv_rounds<S, RB, HI>(s, tw, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
   }
 }
 
@@ -187,7 +190,9 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   constexpr int E = 1 << RB;
   extern __shared__ uint64_t smem[];
   const int N = 1 << R.log_n;
-  const int row = ph.row0 + blockIdx.x / ph.tiles_per_row;
+  const int rl = ph.row0 + blockIdx.x / ph.tiles_per_row;
+  // limb-major enumeration keeps one prime's twiddle table hot in L2 per chunk
+  const int row = ph.items ? (rl % ph.items) * ph.limbs + rl / ph.items : rl;
   const int tile = blockIdx.x % ph.tiles_per_row;
   const int pi = lm.p[row % ph.limbs];
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
@@ -236,11 +241,12 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int gq = tid / (G / E);
   const int w = tid % (G / E);
   const int tbase = ph.M0 + ph.gt * (g0 + gq);
-  const uint64_t* tables = R.ntt + (size_t)pi * 4 * N;
+  // per prime: N forward then N inverse {w, shoup(w)} pairs
+  const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
   if constexpr (FWD) {
-    fwd_rounds<S, RB, S>(smem, tables, tables + N, p, two_p, gq, tbase, w, ph.last);
+    fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
   } else {
-    inv_rounds<S, RB, 0>(smem, tables + 2 * N, tables + 3 * N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
+    inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
                      __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
   }
 
@@ -298,7 +304,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   cudaStream_t st = (cudaStream_t)stream;
   const int N = 1 << logn;
   if (logn <= 12) {
-    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0};
+    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0};
     int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
     return rc ? rc : finish();
   }
@@ -309,9 +315,10 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   const int CA = std::max(1, kTwoPhaseTile / GA), CB = std::max(1, kTwoPhaseTile / GB);
   // phase A: groups are the GB columns, elements strided by GB
   auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
-  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA)};
+  const int items = (rows % limbs == 0 && rows / limbs > 1) ? rows / limbs : 0;
+  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA), items};
   // phase B: groups are the GA rows of GB contiguous elements
-  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB)};
+  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
   const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
   for (int r0 = 0; r0 < rows; r0 += chunk) {

@@ -489,6 +489,61 @@ __global__ void k_reduce(uint64_t* __restrict__ out, const uint64_t* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Counter-based sampling: Philox4x32-10 keyed by a per-item 64-bit
+// seed, counter = (coefficient, limb, stream, 0).  Uniform residues take 128
+// random bits reduced mod p (bias < 2^-60); the error is rint(sigma * z) with z
+// from Box-Muller (ring.py:148-158 distributions).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__global__ void k_sample(uint64_t* __restrict__ a, int64_t* __restrict__ e,
+                         const uint64_t* __restrict__ seeds, int items, int limbs, int log_n,
+                         double sigma, RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t total = (size_t)items * (limbs + 1) * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t n = (uint32_t)(t & (N - 1));
+    const size_t rj = t >> log_n;
+    const int j = (int)(rj % (limbs + 1));
+    const size_t it = rj / (limbs + 1);
+    const uint64_t sd = __ldg(seeds + it);
+    const uint2 key = make_uint2((uint32_t)sd, (uint32_t)(sd >> 32));
+    if (j < limbs) {
+      if (!a) continue;
+      const uint4 r = philox(make_uint4(n, (uint32_t)j, 0u, 0u), key);
+      const uint64_t hi = ((uint64_t)r.x << 32) | r.y, lo = ((uint64_t)r.z << 32) | r.w;
+      const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
+      Mod m;
+      m.p = __ldg(mm);
+      m.mu = __ldg(mm + 1);
+      m.k = __ldg(mm + 2);
+      m.two_p = __ldg(mm + 3);
+      a[(it * limbs + j) * N + n] = ckb::reduce128_any(hi & 0x3FFFFFFFFFFFFFFFull, lo, __ldg(mm + 8),
+                                                       __ldg(mm + 9), m);
+    } else {
+      if (!e) continue;
+      const uint4 r = philox(make_uint4(n, 0xFFFFFFFFu, 1u, 0u), key);
+      const double u1 = ((double)((((uint64_t)r.x << 32) | r.y) >> 11) + 1.0) * 0x1.0p-53;
+      const double u2 = (double)((((uint64_t)r.z << 32) | r.w) >> 11) * 0x1.0p-53;
+      const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+      e[it * N + n] = (int64_t)rint(sigma * z);
+    }
+  }
+}
+
 // ===========================================================================
 // Automorphism and conversions
 // ===========================================================================
@@ -619,24 +674,23 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
     }
     if (!psi) return CKB_E_ARG;
     const uint64_t psi_inv = ckb::inv_mod_host(psi, p);
+    // [N] forward then [N] inverse {w, shoup(w)} pairs, bit-reversed powers
     uint64_t* t = ntt_out + (size_t)i * 4 * N;
     uint64_t acc = 1, acc_inv = 1;
     for (uint64_t j = 0; j < N; ++j) {
       // bit-reverse j over log_n bits
       uint64_t r = 0;
       for (uint32_t b = 0; b < log_n; ++b) r |= ((j >> b) & 1ull) << (log_n - 1 - b);
-      t[r] = acc;
-      t[2 * N + r] = acc_inv;
+      t[2 * r] = acc;
+      t[2 * r + 1] = ckb::shoup_of(acc, p);
+      t[2 * N + 2 * r] = acc_inv;
+      t[2 * N + 2 * r + 1] = ckb::shoup_of(acc_inv, p);
       acc = ckb::mul_mod_host(acc, psi, p);
       acc_inv = ckb::mul_mod_host(acc_inv, psi_inv, p);
     }
-    for (uint64_t j = 0; j < N; ++j) {
-      t[N + j] = ckb::shoup_of(t[j], p);
-      t[3 * N + j] = ckb::shoup_of(t[2 * N + j], p);
-    }
     const ckb::Mod m = ckb::make_mod(p);
     const uint64_t ninv = ckb::inv_mod_host(N % p, p);
-    const uint64_t fold = ckb::mul_mod_host(t[2 * N + 1], ninv, p);
+    const uint64_t fold = ckb::mul_mod_host(t[2 * N + 2], ninv, p);  // inv_psi_brv[1] * N^-1
     uint64_t* mo = mods_out + (size_t)i * kModStride;
     mo[0] = m.p;
     mo[1] = m.mu;
@@ -949,6 +1003,18 @@ int ckb_reduce(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int rows
   if (!total) return 0;
   k_reduce<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, in, total, (int)R.log_n,
                                                                     limbs, R, lm);
+  return finish();
+}
+
+int ckb_sample(const ckb_ring* ring, uint64_t* a, int64_t* e, const uint64_t* seeds, int items,
+               int limbs, const int32_t* limb_prime, double sigma, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || items < 0 || !seeds) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = ((size_t)items * (limbs + 1)) << R.log_n;
+  if (!total) return 0;
+  k_sample<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(a, e, seeds, items, limbs,
+                                                                    (int)R.log_n, sigma, R, lm);
   return finish();
 }
 

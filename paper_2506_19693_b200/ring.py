@@ -425,6 +425,19 @@ class GpuChain:
                                lmap or self.q_map(limbs), nat.stream_handle()), "reduce"))
         return out
 
+    def sample(self, seeds: torch.Tensor, limbs: int, uniform: bool = True, gaussian: bool = True,
+               sigma: float = 3.2, lmap=None):
+        """Device samples per item: uniform residues [items, limbs, N] and
+        rounded Gaussian int64 [items, N] (ckb_sample)."""
+        items = seeds.numel()
+        a = torch.empty(items, limbs, self.n, dtype=U64, device=self.device) if uniform else None
+        e = torch.empty(items, self.n, dtype=torch.int64, device=self.device) if gaussian else None
+        _run("sample", items * (limbs + 1) * self.n * W, 1, lambda: nat.check(
+            nat.LIB.ckb_sample(self.ring_p, nat.ptr(a) if a is not None else None,
+                               nat.ptr(e) if e is not None else None, nat.ptr(seeds), items, limbs,
+                               lmap or self.q_map(limbs), sigma, nat.stream_handle()), "sample"))
+        return a, e
+
     def from_i64(self, coeffs: torch.Tensor, limbs: int, lmap=None, out=None):
         polys = coeffs.numel() >> self.log_n
         out = out if out is not None else torch.empty(polys, limbs, self.n, dtype=U64,

@@ -254,7 +254,7 @@ def test_mode_b_ops_bit_exact_vs_oracle(dnum):
     chain = (60, 40, 40, 40, 120 if dnum else 60)
     params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=40, level=level)
     cust = he_api.keygen(params, {1, 5}, backend="ckks", rng_seed=7, prime_layout="baseline",
-                         dnum=dnum)
+                         dnum=dnum, sampler="numpy")  # the oracle's key stream
     be = cust.backend
     alpha = be.alpha
     orc = O.OracleCkks(n, chain, 40, level, rotation_steps=[1, 5], rng_seed=7, layout="baseline",
@@ -447,3 +447,23 @@ def test_real_bootstrap_precision_n8192():
     # the refreshed ciphertext keeps computing
     sq = cust.evaluator.mul(r, r)
     assert np.max(np.abs(cust.decrypt(sq).values - v * v)) <= 2.0**-14
+
+
+def test_philox_sampler_distribution_and_batch_determinism():
+    """ckb_sample: uniform residues in [0, p), rounded N(0, 3.2^2) errors, one
+    stream per seed (batched == one at a time)."""
+    params = make_params(level=3, scale_bits=40, poly_degree=4096)
+    be = he_api.keygen(params, [], backend="ckks", prime_layout="baseline").backend
+    ch = be.chain
+    seeds = torch.tensor([11, 22, 33], dtype=torch.int64, device="cuda").view(torch.uint64)
+    a, e = ch.sample(seeds, 4)
+    a1, e1 = ch.sample(seeds[1:2].clone(), 4)
+    assert torch.equal(a[1:2].view(torch.int64), a1.view(torch.int64))
+    assert torch.equal(e[1:2], e1)
+    an = a.cpu().numpy().astype(np.float64)
+    for j, p in enumerate(ch.primes[:4]):
+        col = an[:, j]
+        assert col.max() < p and abs(col.mean() / p - 0.5) < 0.01
+    en = e.cpu().numpy()
+    assert abs(en.std() - 3.2) < 0.1 and abs(en.mean()) < 0.1
+    assert not torch.equal(a[0].view(torch.int64), a[1].view(torch.int64))
