@@ -268,6 +268,102 @@ def make_c1_trace(with_ckks: bool):
     print("c1 trace ops:", kinds, "plaintexts:", len(pts))
 
 
+def make_c4_trace():
+    """Config 4 with the survey's substitution: 196-feature
+    14x14 inputs (pixels U[0,1]), 196->128->10, 10 uniform random classes,
+    batch 128, N=2^16, L = tau(1) + 16 = 24 with bootstrap_depth 16, Xavier
+    init; one train_iteration recorded on the sim backend (the refresh calls
+    become real bootstrapping on the B200)."""
+    from ciphermlp.api import CipherVector, keygen
+    from ciphermlp.depth import tau_total
+    from ciphermlp.nn import (Hyperparams, build_model, classifier_format, layer_format,
+                              prepare_sample, train_iteration)
+    from ciphermlp.packing import Architecture, compute_dims, encrypt_packed, pack, required_rotations
+    from ciphermlp.params import make_params
+    import ciphermlp.simbackend as sb
+
+    arch = Architecture(196, (128,), 10)
+    n = 2**16
+    params = make_params(level=tau_total(1) + 16, scale_bits=45, poly_degree=n,
+                         bootstrap_depth=16)
+    shape = compute_dims(arch, n // 2)
+    rng = np.random.default_rng(20250704)
+    bsz = 128
+    x = rng.uniform(0, 1, size=(bsz, 196))
+    y = rng.integers(0, 10, bsz)
+    onehot = np.eye(10)[y]
+    w1 = rng.uniform(-1, 1, size=(196, 128)) * np.sqrt(6.0 / (196 + 128))
+    c1 = rng.uniform(-1, 1, size=(128, 10)) * np.sqrt(6.0 / (128 + 10))
+
+    ops, pts, ids = [], {}, {}
+
+    def pt_id(pv):
+        key = pv.values.tobytes()
+        if key not in pts:
+            pts[key] = len(pts)
+        return pts[key]
+
+    class Recording(sb.SimBackend):
+        def encrypt(self, pv):
+            cv = super().encrypt(pv)
+            ids[cv.serial] = len(ids)
+            ops.append(["enc", ids[cv.serial], pt_id(pv)])
+            return cv
+
+        def elementwise(self, kind, a, b):
+            cv = super().elementwise(kind, a, b)
+            arg = ids[b.serial] if isinstance(b, CipherVector) else pt_id(b)
+            ids[cv.serial] = len(ids)
+            ops.append(["ew", kind, ids[cv.serial], ids[a.serial], arg])
+            return cv
+
+        def rotate(self, a, k, allowed):
+            cv = super().rotate(a, k, allowed)
+            ids[cv.serial] = len(ids)
+            ops.append(["rot", ids[cv.serial], ids[a.serial], int(k)])
+            return cv
+
+        def bootstrap(self, cv):
+            out = super().bootstrap(cv)
+            ids[out.serial] = len(ids)
+            ops.append(["bs", ids[out.serial], ids[cv.serial]])
+            return out
+
+    orig = sb.SimBackend
+    sb.SimBackend = Recording
+    try:
+        cust = keygen(params, required_rotations(shape), backend="sim")
+        hyper = Hyperparams(learning_rate=0.05, momentum=0.9, iterations=1, batch_size=bsz)
+        model = build_model(arch, params, hyper, cust)
+        blk = model.blocks[0]
+        blk.layer_weights = encrypt_packed(cust, pack(w1, layer_format(blk.kind), shape))
+        blk.classifier_weights = encrypt_packed(cust, pack(c1, classifier_format(blk.kind), shape))
+        n_setup = len(ops)
+        batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(bsz)]
+        train_iteration(model, batch, cust, 1)
+    finally:
+        sb.SimBackend = orig
+    b = model.blocks[0]
+    outs = [ids[pm.payload.serial] for pm in (b.layer_weights, b.classifier_weights,
+                                              b.layer_velocity, b.classifier_velocity)]
+    sim_w = np.stack([cust.decrypt(pm.payload).values
+                      for pm in (b.layer_weights, b.classifier_weights,
+                                 b.layer_velocity, b.classifier_velocity)])
+    pt_arr = np.zeros((len(pts), shape.slots))
+    for k, i in pts.items():
+        pt_arr[i] = np.frombuffer(k, dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "c4_trace.npz"), ops=np.array(json.dumps(ops)),
+                        n_setup=np.array([n_setup]), plaintexts=pt_arr, outputs=np.array(outs),
+                        rotations=np.array(sorted(required_rotations(shape))),
+                        params=np.array([n, params.level, 45, 16]), sim_weights=sim_w,
+                        grid=np.array([shape.r, shape.c]))
+    kinds = {}
+    for op in ops:
+        key = op[1] if op[0] == "ew" else op[0]
+        kinds[key] = kinds.get(key, 0) + 1
+    print("c4 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-ckks", action="store_true")
@@ -279,6 +375,8 @@ def main():
         make_ckks()
     if a.only in ("", "c1"):
         make_c1_trace(a.c1_ckks)
+    if a.only == "c4":
+        make_c4_trace()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,42 @@
+"""Config 4 (SURVEY App. B substitution: 196->128->10, batch 128, N=2^16) with
+real bootstrapping: the reference train_iteration's HE calls, wave-batched."""
+import os, sys, time, json
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_19693_b200 import he_api
+from paper_2506_19693_b200.replay import Program
+from paper_2506_19693_b200.executor import WaveExecutor
+from paper_2506_19693_b200.scheme import SchemeParams
+
+
+def run(reps=2, verbose=True):
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c4_trace.npz")
+    z = np.load(path); prog = Program.load(path)
+    n, L, sb, bd = (int(v) for v in z["params"])
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                          scale_bits=45, level=L, bootstrap_depth=bd)
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=4,
+                         prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True)
+    torch.cuda.synchronize(); keygen_s = time.perf_counter() - t0
+    env = prog.run(cust, 0, prog.n_setup)
+    ex = WaveExecutor(prog, cust)
+    times = []
+    out = None
+    for rep in range(reps):
+        torch.cuda.reset_peak_memory_stats()
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        out = ex.run(dict(env), only_after_setup=True)
+        torch.cuda.synchronize(); times.append(time.perf_counter() - t0)
+        if verbose:
+            print(f"step {rep}: {times[-1]*1e3:.1f} ms, peak mem {torch.cuda.max_memory_allocated()/2**30:.1f} GiB", flush=True)
+    w = np.stack([cust.backend._decrypt_values(out[o]) for o in prog.outputs])
+    err = float(np.max(np.abs(w - z["sim_weights"])))
+    return {"ms_per_step": 1e3 * min(times), "first_step_ms": 1e3 * times[0], "ops": len(prog.ops) - prog.n_setup,
+            "waves": len(ex.waves), "bootstraps_per_step": 4, "keygen_s": keygen_s,
+            "weights_max_abs_err_vs_sim": err, "peak_mem_gib": torch.cuda.max_memory_allocated() / 2**30,
+            "workload": "196->128->10, batch 128, N=2^16, L=24 (8 user + 16 bootstrap levels), real bootstrapping"}
+
+
+if __name__ == "__main__":
+    print(json.dumps(run(reps=int(sys.argv[1]) if len(sys.argv) > 1 else 2)))
