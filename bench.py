@@ -298,6 +298,7 @@ def main():
     ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -471,6 +472,15 @@ def main():
             line["c3_bootstrap"] = run_c3_bootstrap()
         except Exception as exc:
             line["c3_bootstrap"] = {"error": repr(exc)}
+    if rank == 0 and world == 1 and not args.no_c4:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import c4_run
+
+            line["c4_train"] = c4_run.run(reps=2, verbose=False)
+        except Exception as exc:
+            line["c4_train"] = {"error": repr(exc)}
+        torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import parallel_ref as PR
 

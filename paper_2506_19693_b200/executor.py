@@ -154,6 +154,9 @@ class WaveExecutor:
         if tag == "bs":
             i = idx[0]
             src = env[ops[i][2]]
+            if be.real_bootstrap:  # homomorphic bootstrapping (bootstrap.py)
+                env[ops[i][1]] = be.bootstrap_ct(src)
+                return
             values = be._decrypt_values(src)
             if be.bootstrap_eps > 0.0:
                 values = values + be._bs_rng.uniform(-be.bootstrap_eps, be.bootstrap_eps,

@@ -31,10 +31,14 @@ def run(reps=2, verbose=True):
         if verbose:
             print(f"step {rep}: {times[-1]*1e3:.1f} ms, peak mem {torch.cuda.max_memory_allocated()/2**30:.1f} GiB", flush=True)
     w = np.stack([cust.backend._decrypt_values(out[o]) for o in prog.outputs])
-    err = float(np.max(np.abs(w - z["sim_weights"])))
+    err = np.max(np.abs(w - z["sim_weights"]), axis=1)  # layer w, classifier w, velocities
+    mag = np.max(np.abs(z["sim_weights"]), axis=1)
     return {"ms_per_step": 1e3 * min(times), "first_step_ms": 1e3 * times[0], "ops": len(prog.ops) - prog.n_setup,
             "waves": len(ex.waves), "bootstraps_per_step": 4, "keygen_s": keygen_s,
-            "weights_max_abs_err_vs_sim": err, "peak_mem_gib": torch.cuda.max_memory_allocated() / 2**30,
+            "weights_max_abs_err_vs_sim": float(err[:2].max()),
+            "velocities_max_abs_err_vs_sim": float(err[2:].max()),
+            "velocities_max_abs": float(mag[2:].max()),
+            "peak_mem_gib": torch.cuda.max_memory_allocated() / 2**30,
             "workload": "196->128->10, batch 128, N=2^16, L=24 (8 user + 16 bootstrap levels), real bootstrapping"}
 
 
