@@ -137,17 +137,19 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
           if (!skip_own) dst[(size_t)e * N] = src[(size_t)e * N];
           continue;
         }
-        const uint64_t p = __ldg(R.mods + (size_t)em.p[e] * kModStride);
-        uint64_t acc = 0;
+        // 128-bit lazy sum of full products (< alpha * 2^122), one reduction
+        const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+        uint64_t hi = 0, lo = 0;
 #pragma unroll
-        for (int i = 0; i < AMAX; ++i) {
-          if (i < cnt) {
-            const uint64_t* c = ctab + i * stride_i + 2 + 2 * e;
-            acc += ckb::mul_shoup_lazy(y[i], c[0], c[1], p);  // < 2p each
-            if ((i & 7) == 7) acc = ckb::reduce_16p(acc, p);
-          }
-        }
-        dst[(size_t)digit_row(e, first, cnt, skip_own) * N] = ckb::reduce_16p(acc, p);
+        for (int i = 0; i < AMAX; ++i)
+          if (i < cnt) ckb::mac128(hi, lo, y[i], ctab[i * stride_i + 2 + 2 * e]);
+        Mod m;
+        m.p = __ldg(mm);
+        m.mu = __ldg(mm + 1);
+        m.k = __ldg(mm + 2);
+        m.two_p = __ldg(mm + 3);
+        dst[(size_t)digit_row(e, first, cnt, skip_own) * N] =
+            ckb::reduce128_any(hi, lo, __ldg(mm + 8), __ldg(mm + 9), m);
       }
     }
   }
@@ -397,24 +399,22 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
     // non-negative word; one reduction per 8 terms.
     uint64_t* dst = E + pidx * m2 * N + n;
     for (int j = 0; j < m2; ++j) {
-      const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * kModStride);
+      const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
       const uint64_t* Te = tabE + (size_t)j * sE;
       const int64_t off = (int64_t)__ldg(Te + 2 * (n1 + n2));
-      uint64_t e = 0;
+      uint64_t hi = 0, lo = 0;  // 128-bit lazy sum of (r + C_j) * c, < 2^62 * q_j each
 #pragma unroll
       for (int u = 0; u < D1; ++u)
-        if (u < n1) {
-          e += ckb::mul_shoup_lazy((uint64_t)(r1[u] + off), __ldg(Te + 2 * u), __ldg(Te + 2 * u + 1), p);
-          if ((u & 7) == 7) e = ckb::reduce_16p(e, p);
-        }
+        if (u < n1) ckb::mac128(hi, lo, (uint64_t)(r1[u] + off), __ldg(Te + 2 * u));
 #pragma unroll
       for (int u = 0; u < D2; ++u)
-        if (u < n2) {
-          e += ckb::mul_shoup_lazy((uint64_t)(r2[u] + off), __ldg(Te + 2 * (n1 + u)),
-                                   __ldg(Te + 2 * (n1 + u) + 1), p);
-          if (((n1 + u) & 7) == 7) e = ckb::reduce_16p(e, p);
-        }
-      dst[(size_t)j * N] = ckb::reduce_16p(e, p);
+        if (u < n2) ckb::mac128(hi, lo, (uint64_t)(r2[u] + off), __ldg(Te + 2 * (n1 + u)));
+      Mod m;
+      m.p = __ldg(mm);
+      m.mu = __ldg(mm + 1);
+      m.k = __ldg(mm + 2);
+      m.two_p = __ldg(mm + 3);
+      dst[(size_t)j * N] = ckb::reduce128_any(hi, lo, __ldg(mm + 8), __ldg(mm + 9), m);
     }
   }
 }
