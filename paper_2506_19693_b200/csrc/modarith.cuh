@@ -130,6 +130,17 @@ CKB_HD uint64_t reduce128_any(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r
   return add_mod(h, reduce64(lo, m), m.p);
 }
 
+// Same for primes of at least 32 bits, branch-free: hi*2^64 via Shoup, lo via
+// Barrett (lo < 2^64 <= 2^(2k)).
+CKB_HD uint64_t reduce128_big(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r64s,
+                              const Mod& m) {
+  const uint64_t h = mul_shoup_lazy(hi, r64, r64s, m.p);     // [0, 2p)
+  const uint64_t l = barrett_reduce128(0, lo, m);            // [0, p)
+  uint64_t s = h + l;                                        // [0, 3p)
+  s = s >= m.two_p ? s - m.two_p : s;
+  return s >= m.p ? s - m.p : s;
+}
+
 // ---- host-only helpers for table construction -----------------------------
 inline uint64_t shoup_of(uint64_t w, uint64_t p) {
   return (uint64_t)(((unsigned __int128)w << 64) / p);

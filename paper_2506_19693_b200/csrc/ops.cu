@@ -83,8 +83,15 @@ __device__ __forceinline__ int digit_row(int e, int first, int cnt, int skip_own
   return skip_own ? (e < first ? e : e - cnt) : e;
 }
 
-// One CTA = one digit (blockIdx.y) over a range of (item, coefficient); the
-// digit's conversion constants are staged in shared memory.
+// One CTA = one digit (blockIdx.y) over a range of (item, coefficient pair);
+// the digit's conversion constants and every ext limb's modulus constants are
+// staged in shared memory.  alpha > 1: y_i = [x_i qhat_i^-1]_{q_i}, then per
+// ext limb a 128-bit lazy sum of y_i [qhat_i]_{p_e} and one reduction.  Two
+// coefficients per thread (16-byte loads and stores).
+struct ModSm {
+  uint64_t p, mu, k, two_p, r64, r64s;
+};
+
 template <int AMAX>
 __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
                                                 const uint64_t* __restrict__ in, size_t in_bstride,
@@ -92,64 +99,85 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
                                                 int n_digits, int out_rows, int skip_own,
                                                 int log_n, RingDev R, LimbMap lm, LimbMap em,
                                                 const uint64_t* __restrict__ bconv) {
-  extern __shared__ uint64_t ctab[];
+  extern __shared__ uint64_t sm[];
+  ModSm* mods = reinterpret_cast<ModSm*>(sm);
+  uint64_t* ctab = sm + 6 * ext;
   const size_t N = (size_t)1 << log_n;
   const int j = blockIdx.y;
   const int first = j * alpha;
   const int cnt = min(alpha, limbs - first);
   const size_t stride_i = 2 + 2 * (size_t)ext;
+  for (int e = threadIdx.x; e < ext; e += blockDim.x) {
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    mods[e] = ModSm{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3), __ldg(mm + 8),
+                    __ldg(mm + 9)};
+  }
   if (AMAX > 1) {
     const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
     for (int q = threadIdx.x; q < cnt * (int)stride_i; q += blockDim.x) ctab[q] = __ldg(tab + q);
-    __syncthreads();
   }
-  const size_t total = (size_t)batch * N;
+  __syncthreads();
+  const size_t half = N >> 1;
+  const size_t total = (size_t)batch * half;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = t & (N - 1);
-    const size_t bi = t >> log_n;
+    const size_t n = (t & (half - 1)) * 2;
+    const size_t bi = t / half;
     const uint64_t* src = in + bi * in_bstride + n;
     uint64_t* dst = out + (bi * n_digits + j) * (size_t)out_rows * N + n;
     if (AMAX == 1) {
-      const uint64_t x = src[(size_t)first * N];
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)first * N);
       const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * kModStride);
       for (int e = 0; e < ext; ++e) {
         if (e == first) {
-          if (!skip_own) dst[(size_t)e * N] = x;
+          if (!skip_own) *reinterpret_cast<ulonglong2*>(dst + (size_t)e * N) = x;
           continue;
         }
-        const Mod m = load_mod(R, em.p[e]);
-        dst[(size_t)digit_row(e, first, 1, skip_own) * N] = ckb::centered_into(x, q, m);
+        const ModSm ms = mods[e];
+        const Mod m{ms.p, ms.mu, ms.k, ms.two_p};
+        ulonglong2 o;
+        o.x = ckb::centered_into(x.x, q, m);
+        o.y = ckb::centered_into(x.y, q, m);
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)digit_row(e, first, 1, skip_own) * N) = o;
       }
     } else {
-      // y_i = [x_i * qhat_i^-1]_{q_i};  out_e = sum_i y_i * [qhat_i]_{p_e}
-      uint64_t y[AMAX];
+      uint64_t y0[AMAX], y1[AMAX];
 #pragma unroll
       for (int i = 0; i < AMAX; ++i) {
         if (i < cnt) {
-          const uint64_t x = src[(size_t)(first + i) * N];
+          const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(first + i) * N);
           const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * kModStride);
-          y[i] = ckb::mul_shoup(x, ctab[i * stride_i], ctab[i * stride_i + 1], q);
+          y0[i] = ckb::mul_shoup(x.x, ctab[i * stride_i], ctab[i * stride_i + 1], q);
+          y1[i] = ckb::mul_shoup(x.y, ctab[i * stride_i], ctab[i * stride_i + 1], q);
+        } else {
+          y0[i] = y1[i] = 0;  // short last digit: zero terms
         }
       }
       for (int e = 0; e < ext; ++e) {
         if (e >= first && e < first + cnt) {
-          if (!skip_own) dst[(size_t)e * N] = src[(size_t)e * N];
+          if (!skip_own)
+            *reinterpret_cast<ulonglong2*>(dst + (size_t)e * N) =
+                *reinterpret_cast<const ulonglong2*>(src + (size_t)e * N);
           continue;
         }
-        // 128-bit lazy sum of full products (< alpha * 2^122), one reduction
-        const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
-        uint64_t hi = 0, lo = 0;
+        uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
-        for (int i = 0; i < AMAX; ++i)
-          if (i < cnt) ckb::mac128(hi, lo, y[i], ctab[i * stride_i + 2 + 2 * e]);
-        Mod m;
-        m.p = __ldg(mm);
-        m.mu = __ldg(mm + 1);
-        m.k = __ldg(mm + 2);
-        m.two_p = __ldg(mm + 3);
-        dst[(size_t)digit_row(e, first, cnt, skip_own) * N] =
-            ckb::reduce128_any(hi, lo, __ldg(mm + 8), __ldg(mm + 9), m);
+        for (int i = 0; i < AMAX; ++i) {
+          const uint64_t c = (i < cnt) ? ctab[i * stride_i + 2 + 2 * e] : 0;
+          ckb::mac128(h0, l0, y0[i], c);
+          ckb::mac128(h1, l1, y1[i], c);
+        }
+        const ModSm ms = mods[e];
+        const Mod m{ms.p, ms.mu, ms.k, ms.two_p};
+        ulonglong2 o;
+        if (ms.k >= 32) {  // warp-uniform
+          o.x = ckb::reduce128_big(h0, l0, ms.r64, ms.r64s, m);
+          o.y = ckb::reduce128_big(h1, l1, ms.r64, ms.r64s, m);
+        } else {
+          o.x = ckb::reduce128_any(h0, l0, ms.r64, ms.r64s, m);
+          o.y = ckb::reduce128_any(h1, l1, ms.r64, ms.r64s, m);
+        }
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)digit_row(e, first, cnt, skip_own) * N) = o;
       }
     }
   }
@@ -167,8 +195,67 @@ __global__ void __launch_bounds__(256) k_ks_inner(
     const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
     RingDev R, LimbMap em, LimbMap km, LimbMap od) {
   const size_t N = (size_t)1 << log_n;
+  const int lh = log_n - 1;
+  const size_t total = (size_t)batch * ext << lh;
+  const size_t krow = 2 * (size_t)key_limbs * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = (t & ((N >> 1) - 1)) * 2;
+    const size_t be = t >> lh;
+    const int e = (int)(be % ext);
+    const size_t bi = be / ext;
+    const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
+    const uint64_t* kb = K + (size_t)km.p[e] * N + n;
+    const uint64_t* ka = kb + (size_t)key_limbs * N;
+    const int owner = own ? od.p[e] : -1;
+    const uint64_t* dbase = dig + bi * (size_t)ND * out_rows * N + n;
+    ulonglong2 x[ND], b[ND], a[ND];
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {  // issue every load first
+      const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
+      const uint64_t* xp = (j == owner) ? own + bi * own_bstride + (size_t)e * N + n
+                                        : dbase + ((size_t)j * out_rows + row) * N;
+      x[j] = *reinterpret_cast<const ulonglong2*>(xp);
+      b[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + j * krow));
+      a[j] = __ldg(reinterpret_cast<const ulonglong2*>(ka + j * krow));
+    }
+    uint64_t hb0 = 0, lb0 = 0, ha0 = 0, la0 = 0, hb1 = 0, lb1 = 0, ha1 = 0, la1 = 0;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      ckb::mac128(hb0, lb0, x[j].x, b[j].x);
+      ckb::mac128(ha0, la0, x[j].x, a[j].x);
+      ckb::mac128(hb1, lb1, x[j].y, b[j].y);
+      ckb::mac128(ha1, la1, x[j].y, a[j].y);
+    }
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    ulonglong2 ob, oa;
+    if (m.k >= 32) {
+      ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
+                           ckb::reduce128_big(hb1, lb1, r64, r64s, m));
+      oa = make_ulonglong2(ckb::reduce128_big(ha0, la0, r64, r64s, m),
+                           ckb::reduce128_big(ha1, la1, r64, r64s, m));
+    } else {
+      ob = make_ulonglong2(ckb::reduce128_any(hb0, lb0, r64, r64s, m),
+                           ckb::reduce128_any(hb1, lb1, r64, r64s, m));
+      oa = make_ulonglong2(ckb::reduce128_any(ha0, la0, r64, r64s, m),
+                           ckb::reduce128_any(ha1, la1, r64, r64s, m));
+    }
+    uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
+    *reinterpret_cast<ulonglong2*>(o) = ob;
+    *reinterpret_cast<ulonglong2*>(o + (size_t)ext * N) = oa;
+  }
+}
+
+// Runtime digit count (alpha = 1 chains with many digits).
+__global__ void __launch_bounds__(256) k_ks_inner_any(
+    uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
+    int out_rows, int alpha, const uint64_t* __restrict__ own, size_t own_bstride, int log_n,
+    const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
+    RingDev R, LimbMap em, LimbMap km, LimbMap od) {
+  const size_t N = (size_t)1 << log_n;
   const size_t total = (size_t)batch * ext * N;
-  const int ndig = ND > 0 ? ND : nd;
   const size_t krow = 2 * (size_t)key_limbs * N;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
@@ -180,32 +267,17 @@ __global__ void __launch_bounds__(256) k_ks_inner(
     const uint64_t* kb = K + (size_t)km.p[e] * N + n;
     const uint64_t* ka = kb + (size_t)key_limbs * N;
     const int owner = own ? od.p[e] : -1;
-    const uint64_t* dbase = dig + bi * (size_t)ndig * out_rows * N + n;
+    const uint64_t* dbase = dig + bi * (size_t)nd * out_rows * N + n;
     uint64_t hb = 0, lb = 0, ha = 0, la = 0;
-#pragma unroll
-    for (int j = 0; j < (ND > 0 ? ND : 1); ++j) {
-      if (ND == 0) break;
+    for (int j = 0; j < nd; ++j) {
       const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
       const uint64_t x = (j == owner) ? own[bi * own_bstride + (size_t)e * N + n]
                                       : dbase[((size_t)j * out_rows + row) * N];
       ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
       ckb::mac128(ha, la, x, __ldg(ka + j * krow));
     }
-    if (ND == 0) {
-      for (int j = 0; j < ndig; ++j) {
-        const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
-        const uint64_t x = (j == owner) ? own[bi * own_bstride + (size_t)e * N + n]
-                                        : dbase[((size_t)j * out_rows + row) * N];
-        ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
-        ckb::mac128(ha, la, x, __ldg(ka + j * krow));
-      }
-    }
     const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
-    Mod m;
-    m.p = __ldg(mm);
-    m.mu = __ldg(mm + 1);
-    m.k = __ldg(mm + 2);
-    m.two_p = __ldg(mm + 3);
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
     const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
     uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
     o[0] = ckb::reduce128_any(hb, lb, r64, r64s, m);
@@ -341,35 +413,52 @@ __device__ __forceinline__ uint64_t add_rm(uint64_t acc, int64_t r, uint64_t M, 
   return sub_rm(acc, -r, M, Ms, p);
 }
 
+// Two coefficients per thread; the E loop's per-limb constants (modulus,
+// r64, and the tabE row) are staged in shared memory once per CTA.
 template <int D1, int D2>
 __global__ void __launch_bounds__(256, 2) k_divround_corr(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
     int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
     const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE) {
+  extern __shared__ uint64_t sm[];
   const size_t N = (size_t)1 << log_n;
-  const size_t total = (size_t)polys * N;
   const int m1 = limbs - n1;
   const int m2 = m1 - n2;
   const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2 + 1);
+  const int row_w = 6 + sE;  // {p, mu, k, 2p, r64, r64s} then the tabE row
+  for (int q = threadIdx.x; q < m2 * row_w; q += blockDim.x) {
+    const int j = q / row_w, c = q % row_w;
+    const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
+    sm[q] = c < 4 ? __ldg(mm + c) : c < 6 ? __ldg(mm + 4 + c) : __ldg(tabE + (size_t)j * sE + c - 6);
+  }
+  __syncthreads();
+  const size_t half = N >> 1;
+  const size_t total = (size_t)polys * half;
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = t & (N - 1);
-    const size_t pidx = t >> log_n;
+    const size_t n = (t & (half - 1)) * 2;
+    const size_t pidx = t / half;
     const uint64_t* src = T + pidx * trows * N + n;
-    int64_t r1[D1 > 0 ? D1 : 1], r2[D2 > 0 ? D2 : 1];
+    int64_t r1[D1 > 0 ? D1 : 1][2], r2[D2 > 0 ? D2 : 1][2];
 #pragma unroll
     for (int d = 0; d < D1; ++d) {
       if (d < n1) {
         const int li = limbs - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         const uint64_t* Tb = tab1 + (size_t)li * s1;
-        uint64_t acc = src[(size_t)(li - m2) * N];
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(li - m2) * N);
+        uint64_t a0 = x.x, a1 = x.y;
 #pragma unroll
         for (int u = 0; u < D1; ++u)
-          if (u < d) acc = sub_rm(acc, r1[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), p);
-        acc = ckb::mul_shoup(acc, __ldg(Tb + 2 * n1), __ldg(Tb + 2 * n1 + 1), p);
-        r1[d] = centered(acc, p);
+          if (u < d) {
+            const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
+            a0 = sub_rm(a0, r1[u][0], M, Ms, p);
+            a1 = sub_rm(a1, r1[u][1], M, Ms, p);
+          }
+        const uint64_t W = __ldg(Tb + 2 * n1), Ws = __ldg(Tb + 2 * n1 + 1);
+        r1[d][0] = centered(ckb::mul_shoup(a0, W, Ws, p), p);
+        r1[d][1] = centered(ckb::mul_shoup(a1, W, Ws, p), p);
       }
     }
 #pragma unroll
@@ -377,44 +466,73 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
       if (d < n2) {
         const int li = m1 - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
-        uint64_t v = src[(size_t)(li - m2) * N];
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(li - m2) * N);
+        uint64_t v0 = x.x, v1 = x.y;
         if (n1) {
           const uint64_t* Ta = tab1 + (size_t)li * s1;
 #pragma unroll
           for (int u = 0; u < D1; ++u)
-            if (u < n1) v = sub_rm(v, r1[u], __ldg(Ta + 2 * u), __ldg(Ta + 2 * u + 1), p);
-          v = ckb::mul_shoup(v, __ldg(Ta + 2 * n1), __ldg(Ta + 2 * n1 + 1), p);
+            if (u < n1) {
+              const uint64_t M = __ldg(Ta + 2 * u), Ms = __ldg(Ta + 2 * u + 1);
+              v0 = sub_rm(v0, r1[u][0], M, Ms, p);
+              v1 = sub_rm(v1, r1[u][1], M, Ms, p);
+            }
+          const uint64_t W = __ldg(Ta + 2 * n1), Ws = __ldg(Ta + 2 * n1 + 1);
+          v0 = ckb::mul_shoup(v0, W, Ws, p);
+          v1 = ckb::mul_shoup(v1, W, Ws, p);
         }
-        if (has_add) v = ckb::add_mod(v, src[(size_t)(n1 + n2 + li - m2) * N], p);
+        if (has_add) {
+          const ulonglong2 a =
+              *reinterpret_cast<const ulonglong2*>(src + (size_t)(n1 + n2 + li - m2) * N);
+          v0 = ckb::add_mod(v0, a.x, p);
+          v1 = ckb::add_mod(v1, a.y, p);
+        }
         const uint64_t* Tb = tab2 + (size_t)li * s2;
 #pragma unroll
         for (int u = 0; u < D2; ++u)
-          if (u < d) v = sub_rm(v, r2[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), p);
-        v = ckb::mul_shoup(v, __ldg(Tb + 2 * n2), __ldg(Tb + 2 * n2 + 1), p);
-        r2[d] = centered(v, p);
+          if (u < d) {
+            const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
+            v0 = sub_rm(v0, r2[u][0], M, Ms, p);
+            v1 = sub_rm(v1, r2[u][1], M, Ms, p);
+          }
+        const uint64_t W = __ldg(Tb + 2 * n2), Ws = __ldg(Tb + 2 * n2 + 1);
+        r2[d][0] = centered(ckb::mul_shoup(v0, W, Ws, p), p);
+        r2[d][1] = centered(ckb::mul_shoup(v1, W, Ws, p), p);
       }
     }
     // E_j = sum_u r_u c_uj: each signed r is shifted by C_j (a multiple of q_j
-    // near 2^61) so every term is one lazy Shoup product (< 2 q_j) of a
-    // non-negative word; one reduction per 8 terms.
+    // near 2^61) so every term is a non-negative word; 128-bit lazy sum and
+    // one reduction per output.
     uint64_t* dst = E + pidx * m2 * N + n;
     for (int j = 0; j < m2; ++j) {
-      const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
-      const uint64_t* Te = tabE + (size_t)j * sE;
-      const int64_t off = (int64_t)__ldg(Te + 2 * (n1 + n2));
-      uint64_t hi = 0, lo = 0;  // 128-bit lazy sum of (r + C_j) * c, < 2^62 * q_j each
+      const uint64_t* S = sm + (size_t)j * row_w;
+      const uint64_t* Te = S + 6;
+      const int64_t off = (int64_t)Te[2 * (n1 + n2)];
+      uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
       for (int u = 0; u < D1; ++u)
-        if (u < n1) ckb::mac128(hi, lo, (uint64_t)(r1[u] + off), __ldg(Te + 2 * u));
+        if (u < n1) {
+          const uint64_t c = Te[2 * u];
+          ckb::mac128(h0, l0, (uint64_t)(r1[u][0] + off), c);
+          ckb::mac128(h1, l1, (uint64_t)(r1[u][1] + off), c);
+        }
 #pragma unroll
       for (int u = 0; u < D2; ++u)
-        if (u < n2) ckb::mac128(hi, lo, (uint64_t)(r2[u] + off), __ldg(Te + 2 * (n1 + u)));
-      Mod m;
-      m.p = __ldg(mm);
-      m.mu = __ldg(mm + 1);
-      m.k = __ldg(mm + 2);
-      m.two_p = __ldg(mm + 3);
-      dst[(size_t)j * N] = ckb::reduce128_any(hi, lo, __ldg(mm + 8), __ldg(mm + 9), m);
+        if (u < n2) {
+          const uint64_t c = Te[2 * (n1 + u)];
+          ckb::mac128(h0, l0, (uint64_t)(r2[u][0] + off), c);
+          ckb::mac128(h1, l1, (uint64_t)(r2[u][1] + off), c);
+        }
+      const Mod m{S[0], S[1], S[2], S[3]};
+      ulonglong2 o;
+      if (m.k >= 32) {  // warp-uniform
+        o.x = ckb::reduce128_big(h0, l0, S[4], S[5], m);
+        o.y = ckb::reduce128_big(h1, l1, S[4], S[5], m);
+      } else {
+        o.x = ckb::reduce128_any(h0, l0, S[4], S[5], m);
+        o.y = ckb::reduce128_any(h1, l1, S[4], S[5], m);
+      }
+      *reinterpret_cast<ulonglong2*>(dst + (size_t)j * N) = o;
     }
   }
 }
@@ -783,8 +901,10 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   const int amax = alpha == 1 ? 1 : alpha <= 2 ? 2 : alpha <= 4 ? 4 : alpha <= 8 ? 8 : 16;
   auto kern = amax == 1 ? k_modup<1> : amax == 2 ? k_modup<2> : amax == 4 ? k_modup<4>
             : amax == 8 ? k_modup<8> : k_modup<16>;
-  const size_t smem = amax == 1 ? 0 : (size_t)alpha * (2 + 2 * (size_t)ext_limbs) * 8;
-  dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((total + 255) / 256, 4096 / nd + 1)),
+  const size_t smem = (6 * (size_t)ext_limbs +
+                       (amax == 1 ? 0 : (size_t)alpha * (2 + 2 * (size_t)ext_limbs))) * 8;
+  const size_t work = (size_t)batch << (R.log_n - 1);
+  dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
             (unsigned)nd);
   kern<<<grid, 256, smem, (cudaStream_t)stream>>>(out, in, bstride, batch, limbs, ext_limbs,
                                                    alpha, nd, out_rows, skip_own, (int)R.log_n,
@@ -808,7 +928,7 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
   if (!total) return 0;
   const int out_rows = own ? ext_limbs - alpha : ext_limbs;
   const size_t ob = own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << R.log_n);
-  const int grid = grid_for(total, 256);
+  const int grid = grid_for(total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
 #define CKB_KS(ND)                                                                           \
   k_ks_inner<ND><<<grid, 256, 0, st>>>(acc, digits, batch, n_digits, ext_limbs, out_rows,   \
@@ -820,8 +940,13 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
     case 3: CKB_KS(3); break;
     case 4: CKB_KS(4); break;
     case 6: CKB_KS(6); break;
+    case 5: CKB_KS(5); break;
     case 8: CKB_KS(8); break;
-    default: CKB_KS(0); break;
+    default:
+      k_ks_inner_any<<<grid_for(total, 256), 256, 0, st>>>(
+          acc, digits, batch, n_digits, ext_limbs, out_rows, alpha, own, ob, (int)R.log_n, key,
+          key_ptrs, key_limbs, R, em, km, od);
+      break;
   }
 #undef CKB_KS
   return finish();
@@ -937,11 +1062,17 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4
                : n_drop1 <= 8 ? 8 : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
-  const int grid = grid_for(total, 256);
+  const int grid = grid_for(total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
+  const int m2 = limbs - n_drop1 - n_drop2;
+  const size_t smem = (size_t)m2 * (6 + 2 * (n_drop1 + n_drop2 + 1)) * 8;
+  if (smem > 200 * 1024) return CKB_E_ARG;
 #define CKB_DC(A, B)                                                                        \
   if (d1 == A && d2 == B) {                                                                 \
-    k_divround_corr<A, B><<<grid, 256, 0, st>>>(E, T, has_addend, polys, limbs, n_drop1,    \
+    if (smem > 48 * 1024)                                                                   \
+      cudaFuncSetAttribute(k_divround_corr<A, B>,                                           \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    k_divround_corr<A, B><<<grid, 256, smem, st>>>(E, T, has_addend, polys, limbs, n_drop1,    \
                                                 n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
                                                 tabE);                                      \
     return finish();                                                                        \
