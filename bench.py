@@ -286,6 +286,45 @@ def run_c3_bootstrap():
                       "P = 11x60, dnum=3, HW 192, K=28, Chebyshev 119 + 2 double angles"}
 
 
+def load_traffic() -> dict:
+    """Per-launch DRAM traffic of the profiled kernels (ncu dram__bytes_read.sum +
+    dram__bytes_write.sum), committed under profiles/ from the capture named in
+    each entry's "source"."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+TRAFFIC = load_traffic()
+
+
+def alu_probe_gbfly(p: int, reps: int = 3) -> float:
+    """Peak lazy-CT-butterfly rate (G butterflies/s) of the IMAD/ALU pipes,
+    register-resident (ckb_alu_probe): the NTT's binding roofline."""
+    import torch
+
+    from paper_2506_19693_b200 import _native as nat
+
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 16, 1000
+    w = (p * 2) // 3
+    nat.check(nat.LIB.ckb_alu_probe(p, w, 10, blocks, nat.ptr(sink), nat.stream_handle()), "probe")
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        nat.check(nat.LIB.ckb_alu_probe(p, w, iters, blocks, nat.ptr(sink), nat.stream_handle()),
+                  "probe")
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, blocks * 256 * 12 * iters / (a.elapsed_time(b) / 1e3) / 1e9)
+    return best
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -420,13 +459,23 @@ def main():
         "hrot_us_per_ct": 1e3 * st_ms["hrot"] / bsz,
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None},
+                     "traffic": (TRAFFIC.get(dom_name) or {}).get("dram_bytes_per_launch"),
+                     "traffic_detail": TRAFFIC.get(dom_name)},
         "kernels": kernels,
         "gpu_launches": launches,
         "keygen_s": keygen_s,
     }
     if clk:
         line["clocks"] = clk
+    if dom_name in ("ntt", "intt"):
+        # the binding roofline of the NTT is the ALU issue rate, not HBM:
+        # butterflies/s achieved vs the register-resident probe's peak
+        peak_bf = alu_probe_gbfly(int(be.chain.limbs_at(lvl)[-1]))
+        got_bf = dom["bytes"] * N_LOG / 32 / (dom["ms"] / 1e3) / 1e9  # bytes = 16 N per limb
+        line["roofline"]["alu"] = {"unit": "Gbutterfly/s", "achieved": got_bf, "peak": peak_bf,
+                                   "frac": got_bf / peak_bf,
+                                   "peak_source": "ckb_alu_probe (register-resident lazy CT "
+                                                  "butterflies, same arithmetic as the NTT)"}
 
     if not args.no_e2e:
         # e2e: host (pinned) inputs -> device -> HMult + HRot -> host, per step

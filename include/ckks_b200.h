@@ -198,6 +198,12 @@ int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int pol
 int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys, int limbs,
                const int32_t* limb_prime, void* stream);
 
+/* ALU roofline probe (no reference counterpart; SURVEY §8(d) "measure the IMAD
+ * pipe's peak with a microbenchmark"): blocks x 256 threads each run `iters`
+ * radix-8 rounds (12 lazy CT butterflies, the NTT's own) on register-resident
+ * residues mod p.  Butterflies launched = blocks * 256 * 12 * iters. */
+int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,8 @@ def _load():
         "ckb_reduce": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_sample": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_double,
                         c_vp], ctypes.c_int),
+        "ckb_alu_probe": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c_vp,
+                           c_vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -91,7 +93,7 @@ EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inver
             "ckb_elementwise", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
             "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_automorphism_ntt",
-            "ckb_reduce", "ckb_sample")
+            "ckb_reduce", "ckb_sample", "ckb_alu_probe")
 
 
 def check(rc: int, what: str) -> None:

@@ -338,6 +338,35 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   return finish();
 }
 
+// ALU ceiling probe (the IMAD pipe is the NTT's binding
+// roofline, so its peak is measured, not assumed).  Each thread keeps 8
+// residues in registers and runs radix-8 rounds of the same lazy CT butterfly
+// the NTT uses, twiddles in registers: no memory traffic at all.
+__global__ void __launch_bounds__(256) k_alu_probe(uint64_t p, uint64_t w0, int iters,
+                                                   uint64_t* __restrict__ sink) {
+  const uint64_t two_p = 2 * p;
+  uint64_t x[8], W[3], Ws[3];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = (threadIdx.x * 8 + k + blockIdx.x) % p;
+  W[0] = w0;
+  W[1] = (w0 * 3 + threadIdx.x) % p;
+  W[2] = (w0 * 7 + blockIdx.x) % p;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Ws[i] = (uint64_t)(((unsigned __int128)W[i] << 64) / p);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int b = 2; b >= 0; --b) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (!(k & (1 << b))) ct_bfly(x[k], x[k | (1 << b)], W[b], Ws[b], p, two_p);
+    }
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc ^= x[k];
+  if (acc == 0x5A5A5A5A5A5A5A5Aull) sink[0] = acc;  // keeps the loop live
+}
+
 }  // namespace
 
 extern "C" {
@@ -352,4 +381,10 @@ int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
   return ntt_run<false>(ring, data, rows, limbs, limb_prime, stream);
 }
 
+
+int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream) {
+  if (p < 3 || (p >> 62) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
+  k_alu_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w, iters, sink);
+  return finish();
+}
 }  // extern "C"
