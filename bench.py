@@ -249,6 +249,54 @@ def run_c1_train(device_index):
             "reference_cpu_s_per_step_build_container": ref_s}
 
 
+def run_c1_dp(local: int, world: int) -> dict:
+    """Config-1 step sharded by sample across `world` ranks (dp.py):
+    each rank runs its share of the 32 per-sample pipelines, one exact residue
+    all-reduce (NCCL int64 SUM + ckb_reduce) joins the δW partial sums, and the
+    update + refresh run replicated.  Device-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_19693_b200 import dist as hdist
+    from paper_2506_19693_b200 import he_api
+    from paper_2506_19693_b200.dp import DataParallelExecutor
+    from paper_2506_19693_b200.replay import Program
+    from paper_2506_19693_b200.scheme import make_params
+
+    path = os.path.join(ROOT, "tests", "golden", "c1_trace.npz")
+    z = np.load(path)
+    prog = Program.load(path)
+    n, level, sb = (int(v) for v in z["params"])
+    params = make_params(level=level, scale_bits=sb, poly_degree=n)
+    cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=3,
+                         prime_layout="baseline", secret_hw=64)
+    env = prog.run(cust, 0, prog.n_setup)
+    ex = DataParallelExecutor(prog, cust, encs_per_sample=3)
+    times = []
+    out = None
+    for rep in range(4):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = ex.run(dict(env), only_after_setup=True)
+        b.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rep:  # first repetition = warm-up
+            times.append(hdist.max_over_ranks(a.elapsed_time(b)))
+    # every rank must hold the same refreshed weights
+    planes = np.concatenate([cust.backend.planes_of(out[o]).ravel() for o in prog.outputs])
+    digest = int(np.bitwise_xor.reduce(planes.view(np.int64)))
+    lo = hdist.reduce_scalar(digest, dist.ReduceOp.MIN, torch.int64)
+    hi = hdist.reduce_scalar(digest, dist.ReduceOp.MAX, torch.int64)
+    return {"ms_per_step": min(times), "ranks": world, "samples": ex.plan.n_samples,
+            "samples_per_rank": len(hdist.shard(ex.plan.n_samples, dist.get_rank(), world)),
+            "allreduce_bytes_per_rank": ex.exchanged_bytes // len(range(4)),
+            "weights_identical_across_ranks": bool(lo == hi),
+            "timing": "CUDA events around the sharded step, max over ranks"}
+
+
 def run_c3_bootstrap():
     """Config 3: full-slot bootstrapping of one ciphertext at N=2^16 (2^15 slots,
     U[-1,1]), input at level 0, HW-192 secret, CtS/StC 3 BSGS levels each,
@@ -352,9 +400,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CKB_SAME_DEVICE / CKB_DIST_BACKEND: functional check of the N>1 code path
+    # on a one-GPU box (all ranks on cuda:0, exchange over gloo); never a bench number
+    if os.environ.get("CKB_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CKB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     L, bsz = args.limbs, args.batch
     params, k = c2_params(L)
@@ -422,10 +478,9 @@ def main():
     ring.TIMER = None
     clk = clocks.stop()
     total_ms = start.elapsed_time(end)
-    t = torch.tensor([total_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+    from paper_2506_19693_b200 import dist as hdist
+
+    ms_step = hdist.max_over_ranks(total_ms) / args.steps
     st_ms = {kk: float(np.mean([a.elapsed_time(b) for a, b in v])) for kk, v in stage.items()}
     hm_b, hr_b, ntt_b = alg_bytes(L, k, bsz, bsz)
     ks_ms = st_ms["hmult"] + st_ms["hrot"]
@@ -502,7 +557,7 @@ def main():
             e2e_step()
         s1.record()
         torch.cuda.synchronize()
-        e2e_ms = s0.elapsed_time(s1) / max(1, args.steps // 2)
+        e2e_ms = hdist.max_over_ranks(s0.elapsed_time(s1)) / max(1, args.steps // 2)
         line["e2e"] = {"value": world * (hm_b + hr_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                        "ms_per_step": e2e_ms,
                        "h2d_bytes_per_step": hA.numel() * 8 + hB.numel() * 8,
@@ -516,6 +571,13 @@ def main():
             line["c1_train"] = run_c1_train(local)
         except Exception as exc:  # report, never hide
             line["c1_train"] = {"error": repr(exc)}
+    if world > 1 and not args.no_c1:
+        try:
+            res = run_c1_dp(local, world)
+        except Exception as exc:
+            res = {"error": repr(exc)}
+        if rank == 0:
+            line["c1_train_dp"] = res
     if rank == 0 and world == 1 and not args.no_c3:
         try:
             line["c3_bootstrap"] = run_c3_bootstrap()

@@ -37,16 +37,26 @@ def allreduce_residues(x: torch.Tensor, reduce_mod, group=None) -> torch.Tensor:
     if ws > MAX_EXACT_RANKS:
         raise ValueError(f"exact residue all-reduce supports <= {MAX_EXACT_RANKS} ranks")
     if ws > 1:
-        y = x.view(torch.int64).clone()
+        y = x.view(torch.int64)
+        staged = y.is_cuda and dist.get_backend(group) == "gloo"
+        y = y.cpu() if staged else y.clone()  # NCCL reduces in place on the device
         dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
-        x = y.view(torch.uint64)
+        x = (y.to(x.device) if staged else y).view(torch.uint64)
     return reduce_mod(x)
 
 
-def max_over_ranks(value: float, device=None) -> float:
+def reduce_scalar(value, op=None, dtype=torch.float64):
+    """All-reduce one number (default MAX); gloo groups reduce it on the host,
+    NCCL groups on the current device."""
     _, ws = world()
     if ws == 1:
-        return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+        return value
+    dev = "cpu" if dist.get_backend() == "gloo" else torch.device("cuda",
+                                                                 torch.cuda.current_device())
+    t = torch.tensor([value], dtype=dtype, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op is None else op)
+    return t.item()
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    return float(reduce_scalar(float(value)))
