@@ -48,12 +48,15 @@ struct NttPhase {
 };
 
 // Shared-memory slot of element r of group g: one pad word per 16 elements
-// makes both the strided (r = w + 16k) and the contiguous (r = 16w + k)
-// register-round patterns bank-conflict free.
+// keeps the register rounds (r = w + 16k, r = 16w + k, ...) conflict-free, and
+// the G/128 extra words of group stride spread the column phase's tile I/O
+// (lanes = 4 rows x 4 column pairs) over distinct banks.  Chosen by
+// enumerating every shared access pattern of the two-phase kernels (an XOR
+// swizzle that is fully conflict-free costs more ALU issue than it saves).
 template <int S>
 __device__ __forceinline__ int sidx(int g, int r) {
   constexpr int G = 1 << S;
-  return g * (G + G / 16) + r + (r >> 4);
+  return g * (G + G / 16 + G / 128) + r + (r >> 4);
 }
 
 // Harvey forward (CT) butterfly, values in [0, 4p).
@@ -267,7 +270,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   const int G = 1 << S;
   const int RB = S < RBT ? S : RBT;
   const int threads = ph.C * G >> RB;
-  const size_t smem = (size_t)ph.C * (G + G / 16) * sizeof(uint64_t);
+  const size_t smem = (size_t)ph.C * (G + G / 16 + G / 128) * sizeof(uint64_t);
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
   if (threads > kNttThreads) return CKB_E_LOGN;
