@@ -21,7 +21,9 @@
  *    on that stream and thread-safe (no global mutable state).
  *  - Return value: 0 on success, a positive cudaError_t on launch failure, or
  *    a negative CKB_E* code for bad arguments.
- *  - Residues are canonical ([0, p)) on input and output; primes < 2^62.
+ *  - Residues are canonical ([0, p)) on input and output; primes < 2^60
+ *    (ckb_build_tables rejects larger ones: lazy butterflies and the carry-free
+ *    split dot products rely on it).
  */
 #ifndef CKKS_B200_H
 #define CKKS_B200_H
@@ -148,7 +150,7 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
  * T per poly: rows [0, n1+n2) = x limbs [limbs-n1-n2, limbs), then (if has_addend)
  * n2 rows = addend limbs [limbs-n1-n2, limbs-n1); all coefficient domain.
  * tab1/tab2 as for ckb_divround; tabE: DEVICE [m2][n1+n2+1][2] {M1_u*P1^-1 mod q_j, shoup},
- * then {M2_u mod q_j, shoup}, then {C_j, 0} with C_j a multiple of q_j in [2^61, 2^62).
+ * then {M2_u mod q_j, shoup}, then {C_j, 0} with C_j a multiple of q_j in [2^59, 2^61) (every r_u + C_j >= 0 and < 2^61).
  * E: [polys][m2][N], coefficient domain (NTT it next). */
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,

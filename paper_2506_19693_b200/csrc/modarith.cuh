@@ -130,6 +130,62 @@ CKB_HD uint64_t reduce128_any(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r
   return add_mod(h, reduce64(lo, m), m.p);
 }
 
+// Carry-free dot products.  An operand x < 2^61 is split as x = hi*2^30 + lo
+// (lo < 2^30, hi < 2^31); the four partial sums of 32x32-bit products then
+// grow by < 2^61 per term, so up to 8 terms accumulate in plain 64-bit words
+// with one IMAD.WIDE.U32 each (the 128-bit mad.lo.cc/madc.hi pair costs ~16
+// instructions per term).  fold() turns the partials into the exact 128-bit
+// sum.  Packed form of a split constant: (hi << 32) | lo.
+struct Split30 {
+  uint32_t lo, hi;
+};
+
+CKB_HD Split30 split30(uint64_t x) {
+  return Split30{(uint32_t)(x & 0x3FFFFFFFull), (uint32_t)(x >> 30)};
+}
+
+CKB_HD uint64_t pack30(uint64_t x) { return ((x >> 30) << 32) | (x & 0x3FFFFFFFull); }
+
+CKB_HD Split30 unpack30(uint64_t w) { return Split30{(uint32_t)w, (uint32_t)(w >> 32)}; }
+
+struct Acc4 {
+  uint64_t s00 = 0, s01 = 0, s10 = 0, s11 = 0;
+  CKB_HD void mac(Split30 a, Split30 b) {
+#if defined(__CUDA_ARCH__)
+    // one IMAD.WIDE.U32 each (plain C++ lets the compiler widen a factor)
+    asm("mad.wide.u32 %0, %4, %6, %0;\n\t"
+        "mad.wide.u32 %1, %4, %7, %1;\n\t"
+        "mad.wide.u32 %2, %5, %6, %2;\n\t"
+        "mad.wide.u32 %3, %5, %7, %3;"
+        : "+l"(s00), "+l"(s01), "+l"(s10), "+l"(s11)
+        : "r"(a.lo), "r"(a.hi), "r"(b.lo), "r"(b.hi));
+#else
+    s00 += (uint64_t)a.lo * b.lo;
+    s01 += (uint64_t)a.lo * b.hi;
+    s10 += (uint64_t)a.hi * b.lo;
+    s11 += (uint64_t)a.hi * b.hi;
+#endif
+  }
+  // (hi:lo) += s00 + (s01 + s10) * 2^30 + s11 * 2^60
+  CKB_HD void fold_into(uint64_t& hi, uint64_t& lo) const {
+    const uint64_t mid = s01 + s10;
+    const uint64_t mid_c = mid < s01 ? 1ull : 0ull;  // carry of the 65-bit mid
+    // mid * 2^30 = (mid_c:mid) << 30
+    const uint64_t m_lo = mid << 30;
+    const uint64_t m_hi = (mid >> 34) | (mid_c << 30);
+    const uint64_t t_lo = s11 << 60;
+    const uint64_t t_hi = s11 >> 4;
+    uint64_t l = lo + s00;
+    uint64_t h = hi + (l < s00 ? 1ull : 0ull);
+    l += m_lo;
+    h += m_hi + (l < m_lo ? 1ull : 0ull);
+    l += t_lo;
+    h += t_hi + (l < t_lo ? 1ull : 0ull);
+    lo = l;
+    hi = h;
+  }
+};
+
 // Same for primes of at least 32 bits, branch-free: hi*2^64 via Shoup, lo via
 // Barrett (lo < 2^64 <= 2^(2k)).
 CKB_HD uint64_t reduce128_big(uint64_t hi, uint64_t lo, uint64_t r64, uint64_t r64s,

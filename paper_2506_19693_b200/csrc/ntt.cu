@@ -59,6 +59,14 @@ __device__ __forceinline__ int sidx(int g, int r) {
   return g * (G + G / 16 + G / 128) + r + (r >> 4);
 }
 
+// Slot offset of element k of a thread's register set: rbase has zero bits in
+// [WLO, WLO+RB), so r = rbase + (k << WLO) adds without carries and
+// sidx(g, r) = sidx(g, rbase) + koff(k), a compile-time constant per k.
+template <int WLO>
+__device__ __forceinline__ constexpr int koff(int k) {
+  return (k << WLO) + ((k << WLO) >> 4);
+}
+
 // Harvey forward (CT) butterfly, values in [0, 4p).
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
                                         uint64_t p, uint64_t two_p) {
@@ -93,8 +101,9 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __rest
     constexpr int WLO = HI - RB > 0 ? HI - RB : 0;
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     uint64_t x[E];
+    uint64_t* sb = s + sidx<S>(gq, rbase);
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    for (int k = 0; k < E; ++k) x[k] = sb[koff<WLO>(k)];
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
@@ -124,7 +133,7 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __rest
       }
     }
 #pragma unroll
-    for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = x[k];
     __syncthreads();
     fwd_rounds<S, RB, LO>(s, tw, p, two_p, gq, tbase, w, last);
   }
@@ -143,8 +152,9 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
     constexpr int WLO = LO < S - RB ? LO : S - RB;
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     uint64_t x[E];
+    uint64_t* sb = s + sidx<S>(gq, rbase);
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = s[sidx<S>(gq, rbase | (k << WLO))];
+    for (int k = 0; k < E; ++k) x[k] = sb[koff<WLO>(k)];
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
@@ -179,7 +189,7 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
       }
     }
 #pragma unroll
-    for (int k = 0; k < E; ++k) s[sidx<S>(gq, rbase | (k << WLO))] = x[k];
+    for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = x[k];
     __syncthreads();
     inv_rounds<S, RB, HI>(s, tw, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
   }

@@ -112,9 +112,13 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
     mods[e] = ModSm{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3), __ldg(mm + 8),
                     __ldg(mm + 9)};
   }
-  if (AMAX > 1) {
+  if (AMAX > 1) {  // [qhat_i]_{p_e} staged in split form (pack30) for the carry-free sum
     const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
-    for (int q = threadIdx.x; q < cnt * (int)stride_i; q += blockDim.x) ctab[q] = __ldg(tab + q);
+    for (int q = threadIdx.x; q < cnt * (int)stride_i; q += blockDim.x) {
+      const int c = q % (int)stride_i;
+      const uint64_t v = __ldg(tab + q);
+      ctab[q] = (c >= 2 && !(c & 1)) ? ckb::pack30(v) : v;
+    }
   }
   __syncthreads();
   const size_t half = N >> 1;
@@ -141,16 +145,16 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
         *reinterpret_cast<ulonglong2*>(dst + (size_t)digit_row(e, first, 1, skip_own) * N) = o;
       }
     } else {
-      uint64_t y0[AMAX], y1[AMAX];
+      ckb::Split30 y0[AMAX], y1[AMAX];
 #pragma unroll
       for (int i = 0; i < AMAX; ++i) {
         if (i < cnt) {
           const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(first + i) * N);
           const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * kModStride);
-          y0[i] = ckb::mul_shoup(x.x, ctab[i * stride_i], ctab[i * stride_i + 1], q);
-          y1[i] = ckb::mul_shoup(x.y, ctab[i * stride_i], ctab[i * stride_i + 1], q);
+          y0[i] = ckb::split30(ckb::mul_shoup(x.x, ctab[i * stride_i], ctab[i * stride_i + 1], q));
+          y1[i] = ckb::split30(ckb::mul_shoup(x.y, ctab[i * stride_i], ctab[i * stride_i + 1], q));
         } else {
-          y0[i] = y1[i] = 0;  // short last digit: zero terms
+          y0[i] = y1[i] = ckb::Split30{0, 0};  // short last digit: zero terms
         }
       }
       for (int e = 0; e < ext; ++e) {
@@ -162,10 +166,16 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
         }
         uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
-        for (int i = 0; i < AMAX; ++i) {
-          const uint64_t c = (i < cnt) ? ctab[i * stride_i + 2 + 2 * e] : 0;
-          ckb::mac128(h0, l0, y0[i], c);
-          ckb::mac128(h1, l1, y1[i], c);
+        for (int i0 = 0; i0 < AMAX; i0 += 8) {  // <= 8 terms per 64-bit partial
+          ckb::Acc4 a0, a1;
+#pragma unroll
+          for (int i = i0; i < (i0 + 8 < AMAX ? i0 + 8 : AMAX); ++i) {
+            const ckb::Split30 c = ckb::unpack30((i < cnt) ? ctab[i * stride_i + 2 + 2 * e] : 0);
+            a0.mac(y0[i], c);
+            a1.mac(y1[i], c);
+          }
+          a0.fold_into(h0, l0);
+          a1.fold_into(h1, l1);
         }
         const ModSm ms = mods[e];
         const Mod m{ms.p, ms.mu, ms.k, ms.two_p};
@@ -429,7 +439,13 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
   for (int q = threadIdx.x; q < m2 * row_w; q += blockDim.x) {
     const int j = q / row_w, c = q % row_w;
     const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
-    sm[q] = c < 4 ? __ldg(mm + c) : c < 6 ? __ldg(mm + 4 + c) : __ldg(tabE + (size_t)j * sE + c - 6);
+    uint64_t v;
+    if (c < 6) {
+      v = c < 4 ? __ldg(mm + c) : __ldg(mm + 4 + c);
+    } else {  // tabE row
+      v = __ldg(tabE + (size_t)j * sE + c - 6);
+    }
+    sm[q] = v;
   }
   __syncthreads();
   const size_t half = N >> 1;
@@ -779,7 +795,7 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
   const uint64_t N = 1ull << log_n;
   for (uint32_t i = 0; i < np; ++i) {
     const uint64_t p = primes[i];
-    if (p < 3 || (p >> 62) != 0 || (p - 1) % (2 * N) != 0) return CKB_E_ARG;
+    if (p < 3 || (p >> 60) != 0 || (p - 1) % (2 * N) != 0) return CKB_E_ARG;  // < 2^60
     // psi: smallest g >= 2 with psi = g^((p-1)/2N) != 1 and psi^N == -1
     const uint64_t cof = (p - 1) / (2 * N);
     uint64_t psi = 0;

@@ -33,7 +33,8 @@ import numpy as np
 from .he_errors import InvalidParameters
 
 REF_MAX_LIMB_BITS = 30
-MAX_PRIME_BITS = 61  # lazy [0, 4p) butterflies need p < 2^62
+MAX_PRIME_BITS = 60  # every prime < 2^60: lazy [0, 4p) butterflies need p < 2^62, and the
+                     # carry-free split dot products (modarith.cuh Acc4) need one operand < 2^60
 _WITNESSES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
 
 
@@ -148,7 +149,7 @@ def build_chain(params, layout: str = "reference"):
             top_primes[lv] = p
         scale_at[rl] = nominal
         for lv in range(rl, 0, -1):
-            p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS)
+            p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS - 1)
             used.add(p)
             rescale[lv - 1] = [p]
             scale_at[lv - 1] = scale_at[lv] ** 2 / p
@@ -162,7 +163,7 @@ def build_chain(params, layout: str = "reference"):
             if layout == "baseline":
                 p = largest_below(chain[lv], two_n, used)
             else:
-                p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS)
+                p = nearest_prime(round(scale_at[lv] ** 2 / nominal), two_n, used, MAX_PRIME_BITS - 1)
             used.add(p)
             rescale[lv - 1] = [p]
             scale_at[lv - 1] = scale_at[lv] ** 2 / p

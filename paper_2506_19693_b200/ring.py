@@ -316,7 +316,7 @@ class GpuChain:
     def _corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
         """tabE for ckb_divround_ntt_corr: per output limb j, {M1_u * P1^-1 mod q_j}
         for u < n1, {M2_u mod q_j} for u < n2, then {C_j, 0} with C_j the smallest
-        multiple of q_j >= 2^61 (shifts the signed remainders non-negative)."""
+        multiple of q_j >= 2^59 (shifts the signed remainders, |r| < 2^59, to [0, 2^61))."""
         primes = [self.all_primes[i] for i in basis]
         limbs = len(primes)
         m1 = limbs - n1
@@ -327,7 +327,7 @@ class GpuChain:
         tab = np.zeros((m2, n1 + n2 + 1, 2), dtype=np.uint64)
         for j in range(m2):
             p = primes[j]
-            tab[j, n1 + n2] = (p * -(-(1 << 61) // p), 0)  # C_j: multiple of q_j near 2^61
+            tab[j, n1 + n2] = (p * -(-(1 << 59) // p), 0)  # C_j: multiple of q_j in [2^59, 2^61)
             p1inv = pow(P1 % p, -1, p)
             for u in range(n1):
                 c = math.prod(d1[:u]) % p * p1inv % p
