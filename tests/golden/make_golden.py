@@ -119,6 +119,12 @@ def make_ckks():
         out[f"lvl_{name}"] = np.array([cv.level_remaining], dtype=np.int64)
         out[f"dec_{name}"] = cust.decrypt(cv).values
     out["dec_ct1"] = cust.decrypt(ct1).values
+    # the reference's own serialisations (RBCT ciphertext, RBKY key container)
+    from ciphermlp.ckks.backend import save_custodian
+
+    out["rbct_ct1"] = np.frombuffer(be.serialize_cipher(ct1), dtype=np.uint8)
+    out["rbct_mul"] = np.frombuffer(be.serialize_cipher(ops["mul"]), dtype=np.uint8)
+    out["rbky"] = np.frombuffer(save_custodian(cust), dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, "ref_ckks_n512.npz"), **out)
 
 

@@ -243,6 +243,39 @@ def test_rbct_roundtrip_and_errors(ck_gold, mode_a):
         be.deserialize_cipher(blob[:-8])
 
 
+def test_rbct_bytes_identical_to_reference(ck_gold, mode_a):
+    """serialize_cipher (ckks/backend.py:210-218) byte for byte, and the
+    reference's blobs deserialize to its planes (fresh and post-multiply)."""
+    be = mode_a.backend
+    for name, lvl_key in (("ct1", None), ("mul", "lvl_mul")):
+        planes = ck_gold["ct1"] if name == "ct1" else ck_gold["out_mul"]
+        lvl = int(ck_gold["params"][1]) if lvl_key is None else int(ck_gold[lvl_key][0])
+        ref_blob = ck_gold[f"rbct_{name}"].tobytes()
+        assert be.serialize_cipher(_wrap(mode_a, planes, lvl)) == ref_blob
+        back = be.deserialize_cipher(ref_blob)
+        assert back.level_remaining == lvl
+        assert np.array_equal(be.planes_of(back.payload), planes)
+
+
+def test_rbky_reference_key_file_round_trip(ck_gold):
+    """The reference's RBKY key container (ckks/backend.py:250-293) loads into
+    the B200 backend: same secret, bit-identical regenerated keys, and
+    save_custodian writes the same bytes back."""
+    from paper_2506_19693_b200.backend import load_custodian, save_custodian
+
+    blob = ck_gold["rbky"].tobytes()
+    cust = load_custodian(blob)
+    be = cust.backend
+    assert np.array_equal(be.sk.coeffs, ck_gold["secret"].astype(np.int64))
+    digests = json.loads(str(ck_gold["key_digests"]))
+    assert _key_digest(be.relin_key) == digests["relin"]
+    for g, key in be.rotation_keys.items():
+        assert _key_digest(key) == digests[f"rot_{g}"]
+    assert save_custodian(cust) == blob
+    with pytest.raises(he_errors.SerializationError):
+        load_custodian(b"XXXX" + blob[4:])
+
+
 # ---------------------------------------------------------------------------
 # Mode B: BASELINE-style single 40/60-bit primes, hybrid key switching
 # ---------------------------------------------------------------------------
