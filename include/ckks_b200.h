@@ -206,6 +206,11 @@ int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys,
  * residues mod p.  Butterflies launched = blocks * 256 * 12 * iters. */
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream);
 
+/* The same probe with the butterfly computed on the FP64 pipe (residues as exact
+ * integers in doubles, p < 2^47): the ceiling of the FP64 NTT path. */
+int ckb_alu_probe_f64(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ def _load():
                         c_vp], ctypes.c_int),
         "ckb_alu_probe": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c_vp,
                            c_vp], ctypes.c_int),
+        "ckb_alu_probe_f64": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                               c_vp, c_vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -93,7 +95,8 @@ EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inver
             "ckb_elementwise", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
             "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_automorphism_ntt",
-            "ckb_reduce", "ckb_sample", "ckb_alu_probe")
+            "ckb_reduce", "ckb_sample", "ckb_alu_probe",
+            "ckb_alu_probe_f64")
 
 
 def check(rc: int, what: str) -> None:

@@ -45,6 +45,8 @@ struct NttPhase {
   int row0;     // first row handled by this launch (for L2-resident chunking)
   int logC;     // log2(C)
   int items;    // > 0: rows enumerated limb-major (rows = items * limbs)
+  int first;    // first phase of the transform: input is canonical uint64
+                // (the FP64 path keeps doubles between the two phases)
 };
 
 // Shared-memory slot of element r of group g: one pad word per 16 elements
@@ -195,6 +197,166 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 NTT path (primes < 2^46).  The integer butterfly is bound by the
+// 32-bit multiplier pipe (ten multiplies per Shoup product) while the FP64
+// pipe idles; B200 runs DFMA at full rate (ckb_alu_probe_f64: 2.27 T
+// butterflies/s vs 0.80 T for the integer form).  Residues are held as exact
+// integers in doubles and a product t = Y*W - q*p is formed exactly:
+//   q = rint(Y * (W/p)),  h = Y*W (rounded),  l = fma(Y, W, -h) (exact),
+//   t = fma(-q, p, h) + l  (exact integer, |t| <= 1.5p).
+// Bounds (p < 2^46): forward values grow by <= 1.5p per stage (|v| < 27p over
+// 17 stages, < 2^51, so Y*(W/p) stays below the 2^51 rint range); inverse
+// sums double per stage and are reduced to [-p/2, p/2] after every register
+// round (<= 3 stages: |v| <= 12p).  All arithmetic is exact integer
+// arithmetic, so results equal the integer path's bit for bit.
+// ---------------------------------------------------------------------------
+constexpr double kRint = 6755399441055744.0;  // 1.5 * 2^52
+
+__device__ __forceinline__ double u64_to_f64(uint64_t v) {  // exact for v < 2^52
+  return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+
+__device__ __forceinline__ uint64_t f64_to_u64(double d) {  // exact for 0 <= d < 2^52
+  return (uint64_t)__double_as_longlong(d + 4503599627370496.0) - 0x4330000000000000ull;
+}
+
+__device__ __forceinline__ double mulmod_f64(double Y, double W, double Wp, double p) {
+  const double q = (Y * Wp + kRint) - kRint;
+  const double h = Y * W;
+  const double l = fma(Y, W, -h);
+  return fma(-q, p, h) + l;
+}
+
+// v mod p into [-p/2, p/2] (exact)
+__device__ __forceinline__ double center_f64(double v, double p, double pinv) {
+  const double q = (v * pinv + kRint) - kRint;
+  return fma(-q, p, v);
+}
+
+// v mod p into [0, p)
+__device__ __forceinline__ double canon_f64(double v, double p, double pinv) {
+  const double r = center_f64(v, p, pinv);
+  return r < 0.0 ? r + p : r;
+}
+
+__device__ __forceinline__ void ct_bfly_f64(double& X, double& Y, double W, double Wp, double p) {
+  const double t = mulmod_f64(Y, W, Wp, p);
+  const double a = X;
+  X = a + t;
+  Y = a - t;
+}
+
+__device__ __forceinline__ void gs_bfly_f64(double& X, double& Y, double W, double Wp, double p) {
+  const double a = X, b = Y;
+  X = a + b;
+  Y = mulmod_f64(a - b, W, Wp, p);
+}
+
+template <int S, int RB, int HI>
+__device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __restrict__ tw,
+                                               double p, double pinv, int gq, int tbase, int w,
+                                               int last) {
+  if constexpr (HI > 0) {
+    constexpr int E = 1 << RB;
+    constexpr int Q = HI < RB ? HI : RB;
+    constexpr int LO = HI - Q;
+    constexpr int WLO = HI - RB > 0 ? HI - RB : 0;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
+    double x[E];
+    uint64_t* sb = s + sidx<S>(gq, rbase);
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
+#pragma unroll
+    for (int b = HI - 1; b >= LO; --b) {
+      const int bb = b - WLO;
+      const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
+      double Wv[E / 2], Wpv[E / 2];
+#pragma unroll
+      for (int i = 0; i < E / 2; ++i) {
+        if (i < ((E / 2) >> bb)) {
+          Wv[i] = u64_to_f64(__ldg(&tw[t0 + i].x));
+          Wpv[i] = Wv[i] * pinv;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << bb)) continue;
+        const int i = k >> (bb + 1);
+        ct_bfly_f64(x[k], x[k | (1 << bb)], Wv[i], Wpv[i], p);
+      }
+    }
+    if (LO == 0 && last) {
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        sb[koff<WLO>(k)] = f64_to_u64(canon_f64(x[k], p, pinv));
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(x[k]);
+    }
+    __syncthreads();
+    fwd_rounds_f64<S, RB, LO>(s, tw, p, pinv, gq, tbase, w, last);
+  }
+}
+
+template <int S, int RB, int LO>
+__device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const ulonglong2* __restrict__ tw,
+                                               double p, double pinv, double ninv, double ninvp,
+                                               double fw, double fwp, int gq, int tbase, int w,
+                                               int last) {
+  if constexpr (LO < S) {
+    constexpr int E = 1 << RB;
+    constexpr int Q = (S - LO) < RB ? (S - LO) : RB;
+    constexpr int HI = LO + Q;
+    constexpr int WLO = LO < S - RB ? LO : S - RB;
+    const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
+    double x[E];
+    uint64_t* sb = s + sidx<S>(gq, rbase);
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
+#pragma unroll
+    for (int b = LO; b < HI; ++b) {
+      const int bb = b - WLO;
+      if (b == S - 1 && last) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (k & (1 << bb)) continue;
+          const double X = x[k], Y = x[k | (1 << bb)];
+          x[k] = mulmod_f64(X + Y, ninv, ninvp, p);
+          x[k | (1 << bb)] = mulmod_f64(X - Y, fw, fwp, p);
+        }
+      } else {
+        const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
+        double Wv[E / 2], Wpv[E / 2];
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) {
+          if (i < ((E / 2) >> bb)) {
+            Wv[i] = u64_to_f64(__ldg(&tw[t0 + i].x));
+            Wpv[i] = Wv[i] * pinv;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (k & (1 << bb)) continue;
+          const int i = k >> (bb + 1);
+          gs_bfly_f64(x[k], x[k | (1 << bb)], Wv[i], Wpv[i], p);
+        }
+      }
+    }
+    if (HI == S && last) {
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        sb[koff<WLO>(k)] = f64_to_u64(canon_f64(x[k], p, pinv));
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv));
+    }
+    __syncthreads();
+    inv_rounds_f64<S, RB, HI>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last);
+  }
+}
+
 template <int S, bool FWD, int RBT>
 __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
@@ -210,6 +372,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int pi = lm.p[row % ph.limbs];
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
   const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
+  const bool f64 = (p >> 46) == 0;  // CTA-uniform: FP64 path for primes < 2^46
   uint64_t* base = data + (size_t)row * N;
   const int C = ph.C;
   const int T = blockDim.x;
@@ -238,6 +401,13 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
       int g, r;
       v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_of(tid + i * T, g, r)));
     }
+    if (f64 && ph.first) {  // canonical residues -> exact doubles
+#pragma unroll
+      for (int i = 0; i < E / 2; ++i) {
+        v[i].x = (uint64_t)__double_as_longlong(u64_to_f64(v[i].x));
+        v[i].y = (uint64_t)__double_as_longlong(u64_to_f64(v[i].y));
+      }
+    }
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       int g, r;
@@ -256,7 +426,16 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int tbase = ph.M0 + ph.gt * (g0 + gq);
   // per prime: N forward then N inverse {w, shoup(w)} pairs
   const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
-  if constexpr (FWD) {
+  if (f64) {
+    const double pd = (double)p, pinv = 1.0 / pd;
+    if constexpr (FWD) {
+      fwd_rounds_f64<S, RB, S>(smem, tables, pd, pinv, gq, tbase, w, ph.last);
+    } else {
+      const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
+      inv_rounds_f64<S, RB, 0>(smem, tables + N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv, gq,
+                               tbase, w, ph.last);
+    }
+  } else if constexpr (FWD) {
     fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
   } else {
     inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
@@ -317,7 +496,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   cudaStream_t st = (cudaStream_t)stream;
   const int N = 1 << logn;
   if (logn <= 12) {
-    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0};
+    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0, 1};
     int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
     return rc ? rc : finish();
   }
@@ -329,9 +508,9 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   // phase A: groups are the GB columns, elements strided by GB
   auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
   const int items = (rows % limbs == 0 && rows / limbs > 1) ? rows / limbs : 0;
-  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA), items};
+  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA), items, FWD ? 1 : 0};
   // phase B: groups are the GA rows of GB contiguous elements
-  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items};
+  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items, FWD ? 0 : 1};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
   const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
   for (int r0 = 0; r0 < rows; r0 += chunk) {
@@ -380,6 +559,31 @@ __global__ void __launch_bounds__(256) k_alu_probe(uint64_t p, uint64_t w0, int 
   if (acc == 0x5A5A5A5A5A5A5A5Aull) sink[0] = acc;  // keeps the loop live
 }
 
+// FP64 variant of the probe: the same radix-8 rounds on the FP64 pipe.
+__global__ void __launch_bounds__(256) k_alu_probe_f64(double p, double w0, int iters,
+                                                       uint64_t* __restrict__ sink) {
+  double x[8], W[3], Wp[3];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = (double)((threadIdx.x * 8 + k + blockIdx.x) % 1000003);
+  W[0] = w0;
+  W[1] = fmod(w0 * 3.0 + threadIdx.x, p);
+  W[2] = fmod(w0 * 7.0 + blockIdx.x, p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Wp[i] = W[i] / p;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int b = 2; b >= 0; --b) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (!(k & (1 << b))) ct_bfly_f64(x[k], x[k | (1 << b)], W[b], Wp[b], p);
+    }
+  }
+  double acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc += x[k];
+  if (acc == 1234.5) sink[0] = 1;
+}
+
 }  // namespace
 
 extern "C" {
@@ -398,6 +602,13 @@ int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream) {
   if (p < 3 || (p >> 62) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
   k_alu_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w, iters, sink);
+  return finish();
+}
+
+int ckb_alu_probe_f64(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink,
+                      void* stream) {
+  if (p < 3 || (p >> 47) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
+  k_alu_probe_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>((double)p, (double)w, iters, sink);
   return finish();
 }
 }  // extern "C"
