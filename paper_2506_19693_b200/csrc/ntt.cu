@@ -69,6 +69,17 @@ __device__ __forceinline__ constexpr int koff(int k) {
   return (k << WLO) + ((k << WLO) >> 4);
 }
 
+// Barrier between register rounds: when a group's G/E threads fit in one warp
+// (G/E <= 32), a warp only exchanges data with itself through shared memory.
+template <int S, int RB>
+__device__ __forceinline__ void round_sync() {
+  if constexpr ((1 << (S - RB)) <= 32) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
 // Harvey forward (CT) butterfly, values in [0, 4p).
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
                                         uint64_t p, uint64_t two_p) {
@@ -136,7 +147,7 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __rest
     }
 #pragma unroll
     for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = x[k];
-    __syncthreads();
+    round_sync<S, RB>();
     fwd_rounds<S, RB, LO>(s, tw, p, two_p, gq, tbase, w, last);
   }
 }
@@ -192,7 +203,7 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
     }
 #pragma unroll
     for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = x[k];
-    __syncthreads();
+    round_sync<S, RB>();
     inv_rounds<S, RB, HI>(s, tw, p, two_p, ninv, ninvs, fw, fws, gq, tbase, w, last);
   }
 }
@@ -294,7 +305,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __
 #pragma unroll
       for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(x[k]);
     }
-    __syncthreads();
+    round_sync<S, RB>();
     fwd_rounds_f64<S, RB, LO>(s, tw, p, pinv, gq, tbase, w, last);
   }
 }
@@ -352,7 +363,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const ulonglong2* __
       for (int k = 0; k < E; ++k)
         sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv));
     }
-    __syncthreads();
+    round_sync<S, RB>();
     inv_rounds_f64<S, RB, HI>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last);
   }
 }
@@ -383,11 +394,21 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   // tile -> smem, 16-byte vectors (pairs adjacent in global memory).  Every
   // thread moves exactly E/2 pairs (C*G/2 pairs over C*G/E threads); all
   // loads are issued before the first shared store.
-  auto pair_of = [&](int q, int& g, int& r) -> size_t {
-    const int e = 2 * q;
+  // Contiguous rows with a group per (part of a) warp: thread t moves pairs
+  // lt + (G/E) i of its own group (still 16-byte coalesced), so the whole
+  // phase only exchanges data inside a warp (__syncwarp, no CTA barrier).
+  constexpr bool kWarpGroups = (G / E) <= 32;
+  const bool warp_local = kWarpGroups && rows_contig;
+  auto pair_of = [&](int i, int& g, int& r) -> size_t {  // i-th pair of this thread
+    const int e = 2 * (tid + i * T);
     if (rows_contig) {
-      g = e >> S;
-      r = e & (G - 1);
+      if (kWarpGroups) {  // group tid/(G/E), pair (tid % (G/E)) + (G/E) i
+        g = tid / (G / E);
+        r = 2 * (tid % (G / E) + (G / E) * i);
+      } else {
+        g = e >> S;
+        r = e & (G - 1);
+      }
       return (size_t)(g0 + g) * ph.gstride + r;
     }
     r = e >> ph.logC;
@@ -399,7 +420,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       int g, r;
-      v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_of(tid + i * T, g, r)));
+      v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_of(i, g, r)));
     }
     if (f64 && ph.first) {  // canonical residues -> exact doubles
 #pragma unroll
@@ -411,7 +432,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       int g, r;
-      pair_of(tid + i * T, g, r);
+      pair_of(i, g, r);
       smem[sidx<S>(g, r)] = v[i].x;
       if (rows_contig)
         smem[sidx<S>(g, r + 1)] = v[i].y;
@@ -419,7 +440,10 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
         smem[sidx<S>(g + 1, r)] = v[i].y;
     }
   }
-  __syncthreads();
+  if (warp_local)
+    __syncwarp();
+  else
+    __syncthreads();
 
   const int gq = tid / (G / E);
   const int w = tid % (G / E);
@@ -441,11 +465,15 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
                      __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
   }
+  if (warp_local)
+    __syncwarp();
+  else
+    __syncthreads();  // the tile store reads across groups
 
 #pragma unroll
   for (int i = 0; i < E / 2; ++i) {
     int g, r;
-    const size_t off = pair_of(tid + i * T, g, r);
+    const size_t off = pair_of(i, g, r);
     ulonglong2 v;
     v.x = smem[sidx<S>(g, r)];
     v.y = rows_contig ? smem[sidx<S>(g, r + 1)] : smem[sidx<S>(g + 1, r)];
