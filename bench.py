@@ -349,7 +349,7 @@ def load_traffic() -> dict:
 TRAFFIC = load_traffic()
 
 
-def alu_probe_gbfly(p: int, reps: int = 3) -> float:
+def alu_probe_gbfly(p: int, reps: int = 3, f64: bool = False) -> float:
     """Peak lazy-CT-butterfly rate (G butterflies/s) of the IMAD/ALU pipes,
     register-resident (ckb_alu_probe): the NTT's binding roofline."""
     import torch
@@ -360,13 +360,13 @@ def alu_probe_gbfly(p: int, reps: int = 3) -> float:
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = sms * 16, 1000
     w = (p * 2) // 3
-    nat.check(nat.LIB.ckb_alu_probe(p, w, 10, blocks, nat.ptr(sink), nat.stream_handle()), "probe")
+    fn = nat.LIB.ckb_alu_probe_f64 if f64 else nat.LIB.ckb_alu_probe
+    nat.check(fn(p, w, 10, blocks, nat.ptr(sink), nat.stream_handle()), "probe")
     best = 0.0
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        nat.check(nat.LIB.ckb_alu_probe(p, w, iters, blocks, nat.ptr(sink), nat.stream_handle()),
-                  "probe")
+        nat.check(fn(p, w, iters, blocks, nat.ptr(sink), nat.stream_handle()), "probe")
         b.record()
         torch.cuda.synchronize()
         best = max(best, blocks * 256 * 12 * iters / (a.elapsed_time(b) / 1e3) / 1e9)
@@ -523,14 +523,26 @@ def main():
     if clk:
         line["clocks"] = clk
     if dom_name in ("ntt", "intt"):
-        # the binding roofline of the NTT is the ALU issue rate, not HBM:
-        # butterflies/s achieved vs the register-resident probe's peak
-        peak_bf = alu_probe_gbfly(int(be.chain.limbs_at(lvl)[-1]))
-        got_bf = dom["bytes"] * N_LOG / 32 / (dom["ms"] / 1e3) / 1e9  # bytes = 16 N per limb
-        line["roofline"]["alu"] = {"unit": "Gbutterfly/s", "achieved": got_bf, "peak": peak_bf,
-                                   "frac": got_bf / peak_bf,
-                                   "peak_source": "ckb_alu_probe (register-resident lazy CT "
-                                                  "butterflies, same arithmetic as the NTT)"}
+        # the NTT's binding roofline is the arithmetic pipes, not HBM: rows with
+        # primes < 2^46 run the FP64 butterfly, the others the integer one, each
+        # against its own register-resident probe; the mixed ceiling is the
+        # time the probes would need for this kernel's butterflies
+        p_int = int(be.chain.limbs_at(lvl)[0])  # the 60-bit base prime
+        p_f64 = int(be.chain.limbs_at(lvl)[-1])  # a 40-bit rescale prime
+        peak_int = alu_probe_gbfly(p_int)
+        peak_f64 = alu_probe_gbfly(p_f64, f64=True)
+        bf = dom["bytes"] * N_LOG / 32 / 1e9          # G butterflies (bytes = 16 N per limb)
+        bf_f64 = dom["f64_bytes"] * N_LOG / 32 / 1e9
+        floor_s = (bf - bf_f64) / peak_int + bf_f64 / peak_f64
+        got_s = dom["ms"] / 1e3
+        line["roofline"]["alu"] = {"unit": "Gbutterfly/s", "achieved": bf / got_s,
+                                   "peak": bf / floor_s, "frac": floor_s / got_s,
+                                   "f64_share": bf_f64 / bf, "peak_int": peak_int,
+                                   "peak_f64": peak_f64,
+                                   "peak_source": "ckb_alu_probe / ckb_alu_probe_f64 "
+                                                  "(register-resident butterflies, the "
+                                                  "NTT's own integer and FP64 arithmetic), "
+                                                  "weighted by this kernel's row mix"}
 
     if not args.no_e2e:
         # e2e: host (pinned) inputs -> device -> HMult + HRot -> host, per step

@@ -41,19 +41,23 @@ class KernelTimer:
     def summary(self) -> dict:
         torch.cuda.synchronize()
         out = {}
-        for name, s, e, nbytes, launches in self.records:
-            d = out.setdefault(name, {"ms": 0.0, "calls": 0, "bytes": 0, "launches": 0})
+        for name, s, e, nbytes, launches, f64_bytes in self.records:
+            d = out.setdefault(name, {"ms": 0.0, "calls": 0, "bytes": 0, "launches": 0,
+                                      "f64_bytes": 0})
             d["ms"] += s.elapsed_time(e)
             d["calls"] += 1
             d["bytes"] += nbytes
             d["launches"] += launches
+            d["f64_bytes"] += f64_bytes
         return out
 
 
 TIMER = None  # set to a KernelTimer to instrument
 
 
-def _run(name, nbytes, launches, fn):
+def _run(name, nbytes, launches, fn, f64_share=None):
+    """f64_share: callable giving the fraction of the work on the FP64 NTT path
+    (rows whose prime is < 2^46), evaluated only when instrumenting."""
     t = TIMER
     if t is None:
         return fn()
@@ -62,7 +66,8 @@ def _run(name, nbytes, launches, fn):
     s.record()
     r = fn()
     e.record()
-    t.records.append((name, s, e, nbytes, launches))
+    t.records.append((name, s, e, nbytes, launches,
+                      nbytes * f64_share() if f64_share is not None else 0))
     return r
 
 
@@ -186,20 +191,28 @@ class GpuChain:
         chunk = max(1, (48 << 20) // (self.n * W))
         return 2 * (-(-rows // chunk))
 
+    F64_PRIME_LIMIT = 1 << 46  # csrc/ntt.cu: primes below run the FP64 butterfly
+
+    def _f64_share(self, lmap, limbs: int):
+        return lambda: sum(self.all_primes[lmap[i]] < self.F64_PRIME_LIMIT
+                           for i in range(limbs)) / limbs
+
     def ntt_fwd(self, t: torch.Tensor, limbs: int, lmap=None):
         rows = t.numel() >> self.log_n
+        lm = lmap or self.q_map(limbs)
         _run("ntt", 2 * rows * self.n * W, self._ntt_launches(rows), lambda: nat.check(
-            nat.LIB.ckb_ntt_forward(self.ring_p, nat.ptr(t), rows, limbs,
-                                    lmap or self.q_map(limbs), nat.stream_handle()),
-            "ntt_forward"))
+            nat.LIB.ckb_ntt_forward(self.ring_p, nat.ptr(t), rows, limbs, lm,
+                                    nat.stream_handle()),
+            "ntt_forward"), self._f64_share(lm, limbs))
         return t
 
     def ntt_inv(self, t: torch.Tensor, limbs: int, lmap=None):
         rows = t.numel() >> self.log_n
+        lm = lmap or self.q_map(limbs)
         _run("intt", 2 * rows * self.n * W, self._ntt_launches(rows), lambda: nat.check(
-            nat.LIB.ckb_ntt_inverse(self.ring_p, nat.ptr(t), rows, limbs,
-                                    lmap or self.q_map(limbs), nat.stream_handle()),
-            "ntt_inverse"))
+            nat.LIB.ckb_ntt_inverse(self.ring_p, nat.ptr(t), rows, limbs, lm,
+                                    nat.stream_handle()),
+            "ntt_inverse"), self._f64_share(lm, limbs))
         return t
 
     def ew(self, op: int, out, a, b=None, c=None, limbs: int = 0, lmap=None, b_rows: int = 0):
