@@ -286,8 +286,9 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __
 #pragma unroll
       for (int i = 0; i < E / 2; ++i) {
         if (i < ((E / 2) >> bb)) {
-          Wv[i] = u64_to_f64(__ldg(&tw[t0 + i].x));
-          Wpv[i] = Wv[i] * pinv;
+          const ulonglong2 wp = __ldg(tw + t0 + i);  // {double(w), double(w)/p}
+          Wv[i] = __longlong_as_double((long long)wp.x);
+          Wpv[i] = __longlong_as_double((long long)wp.y);
         }
       }
 #pragma unroll
@@ -342,8 +343,9 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const ulonglong2* __
 #pragma unroll
         for (int i = 0; i < E / 2; ++i) {
           if (i < ((E / 2) >> bb)) {
-            Wv[i] = u64_to_f64(__ldg(&tw[t0 + i].x));
-            Wpv[i] = Wv[i] * pinv;
+            const ulonglong2 wp = __ldg(tw + t0 + i);
+            Wv[i] = __longlong_as_double((long long)wp.x);
+            Wpv[i] = __longlong_as_double((long long)wp.y);
           }
         }
 #pragma unroll

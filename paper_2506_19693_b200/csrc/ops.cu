@@ -1,6 +1,7 @@
 // Limb arithmetic, key switching, rescale, automorphism and conversion kernels
 // (sm_100a) replacing ciphermlp/ckks/{ring,keys,backend}.py numpy routines.
 #include "common.cuh"
+#include <cstring>
 
 using namespace ckb_internal;
 using ckb::Mod;
@@ -785,6 +786,12 @@ __global__ void k_to_f64(double* __restrict__ out, const uint64_t* __restrict__ 
 // C-ABI
 // ===========================================================================
 
+static uint64_t f64_bits(double d) {
+  uint64_t u;
+  memcpy(&u, &d, sizeof u);
+  return u;
+}
+
 extern "C" {
 
 int ckb_version(void) { return 1; }
@@ -815,16 +822,25 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
       // bit-reverse j over log_n bits
       uint64_t r = 0;
       for (uint32_t b = 0; b < log_n; ++b) r |= ((j >> b) & 1ull) << (log_n - 1 - b);
-      t[2 * r] = acc;
-      t[2 * r + 1] = ckb::shoup_of(acc, p);
-      t[2 * N + 2 * r] = acc_inv;
-      t[2 * N + 2 * r + 1] = ckb::shoup_of(acc_inv, p);
+      if ((p >> 46) == 0) {  // FP64 NTT path: {double(w), double(w)/p} (csrc/ntt.cu)
+        const double pd = (double)p;
+        t[2 * r] = f64_bits((double)acc);
+        t[2 * r + 1] = f64_bits((double)acc / pd);
+        t[2 * N + 2 * r] = f64_bits((double)acc_inv);
+        t[2 * N + 2 * r + 1] = f64_bits((double)acc_inv / pd);
+      } else {
+        t[2 * r] = acc;
+        t[2 * r + 1] = ckb::shoup_of(acc, p);
+        t[2 * N + 2 * r] = acc_inv;
+        t[2 * N + 2 * r + 1] = ckb::shoup_of(acc_inv, p);
+      }
       acc = ckb::mul_mod_host(acc, psi, p);
       acc_inv = ckb::mul_mod_host(acc_inv, psi_inv, p);
     }
     const ckb::Mod m = ckb::make_mod(p);
     const uint64_t ninv = ckb::inv_mod_host(N % p, p);
-    const uint64_t fold = ckb::mul_mod_host(t[2 * N + 2], ninv, p);  // inv_psi_brv[1] * N^-1
+    // inv_psi_brv[1] = psi^-(N/2) (bit-reversed index 1), times N^-1
+    const uint64_t fold = ckb::mul_mod_host(ckb::pow_mod_host(psi_inv, N / 2, p), ninv, p);
     uint64_t* mo = mods_out + (size_t)i * kModStride;
     mo[0] = m.p;
     mo[1] = m.mu;
