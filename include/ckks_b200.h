@@ -42,8 +42,8 @@ extern "C" {
  *   mods : [n_primes][16] {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
  *                          psi_inv_brv[1]*N^-1, shoup(.), 2^64 mod p, shoup(.), 0...}
  *   ntt  : [n_primes][2][N][2] {psi_brv[j], shoup(.)} pairs, then {inv_psi_brv[j], shoup(.)};
- *          for primes < 2^46 (the FP64 butterfly path) each pair is instead the
- *          IEEE-754 bits of {double(w), double(w) / p}
+ *          for primes < 2^46 (the FP64 butterfly path) each direction's 2N words
+ *          are instead [N] doubles w then [N] doubles w / p (IEEE-754 bits)
  *   pair : [n_primes][n_primes][4] {p_i^-1 mod p_j, shoup(.), p_i mod p_j, 0}
  * Built on the host by ckb_build_tables, uploaded by the caller. */
 typedef struct {

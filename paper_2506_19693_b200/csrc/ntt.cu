@@ -265,7 +265,7 @@ __device__ __forceinline__ void gs_bfly_f64(double& X, double& Y, double W, doub
 }
 
 template <int S, int RB, int HI>
-__device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __restrict__ tw,
+__device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, int gq, int tbase, int w,
                                                int last) {
   if constexpr (HI > 0) {
@@ -286,9 +286,8 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __
 #pragma unroll
       for (int i = 0; i < E / 2; ++i) {
         if (i < ((E / 2) >> bb)) {
-          const ulonglong2 wp = __ldg(tw + t0 + i);  // {double(w), double(w)/p}
-          Wv[i] = __longlong_as_double((long long)wp.x);
-          Wpv[i] = __longlong_as_double((long long)wp.y);
+          Wv[i] = __ldg(tw + t0 + i);  // contiguous double(w): 8 B per twiddle
+          Wpv[i] = Wv[i] * pinv;
         }
       }
 #pragma unroll
@@ -312,7 +311,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const ulonglong2* __
 }
 
 template <int S, int RB, int LO>
-__device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const ulonglong2* __restrict__ tw,
+__device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, double ninv, double ninvp,
                                                double fw, double fwp, int gq, int tbase, int w,
                                                int last) {
@@ -343,9 +342,8 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const ulonglong2* __
 #pragma unroll
         for (int i = 0; i < E / 2; ++i) {
           if (i < ((E / 2) >> bb)) {
-            const ulonglong2 wp = __ldg(tw + t0 + i);
-            Wv[i] = __longlong_as_double((long long)wp.x);
-            Wpv[i] = __longlong_as_double((long long)wp.y);
+            Wv[i] = __ldg(tw + t0 + i);  // contiguous double(w): 8 B per twiddle
+            Wpv[i] = Wv[i] * pinv;
           }
         }
 #pragma unroll
@@ -454,12 +452,14 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
   if (f64) {
     const double pd = (double)p, pinv = 1.0 / pd;
+    // FP64-path table: [N] double(w) forward, [N] w/p, then the inverse pair
+    const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
     if constexpr (FWD) {
-      fwd_rounds_f64<S, RB, S>(smem, tables, pd, pinv, gq, tbase, w, ph.last);
+      fwd_rounds_f64<S, RB, S>(smem, dtab, pd, pinv, gq, tbase, w, ph.last);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
-      inv_rounds_f64<S, RB, 0>(smem, tables + N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv, gq,
-                               tbase, w, ph.last);
+      inv_rounds_f64<S, RB, 0>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv,
+                               gq, tbase, w, ph.last);
     }
   } else if constexpr (FWD) {
     fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);

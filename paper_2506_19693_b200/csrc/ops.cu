@@ -822,12 +822,12 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
       // bit-reverse j over log_n bits
       uint64_t r = 0;
       for (uint32_t b = 0; b < log_n; ++b) r |= ((j >> b) & 1ull) << (log_n - 1 - b);
-      if ((p >> 46) == 0) {  // FP64 NTT path: {double(w), double(w)/p} (csrc/ntt.cu)
+      if ((p >> 46) == 0) {  // FP64 NTT path (csrc/ntt.cu): [N] double(w), then [N] w/p
         const double pd = (double)p;
-        t[2 * r] = f64_bits((double)acc);
-        t[2 * r + 1] = f64_bits((double)acc / pd);
-        t[2 * N + 2 * r] = f64_bits((double)acc_inv);
-        t[2 * N + 2 * r + 1] = f64_bits((double)acc_inv / pd);
+        t[r] = f64_bits((double)acc);
+        t[N + r] = f64_bits((double)acc / pd);
+        t[2 * N + r] = f64_bits((double)acc_inv);
+        t[3 * N + r] = f64_bits((double)acc_inv / pd);
       } else {
         t[2 * r] = acc;
         t[2 * r + 1] = ckb::shoup_of(acc, p);

@@ -37,11 +37,11 @@ def test_build_tables_match_oracle_plan(logn, bits):
     mods, ntt, pair = _native.build_tables(logn, [p])
     plan = O.NttPlan(p, n)
     t = ntt.reshape(1, 2, n, 2)
-    if p < 2**46:  # FP64 NTT path: {double(w), double(w)/p}
-        d = t.view(np.float64)
-        assert [int(v) for v in d[0, 0, :, 0]] == [int(v) for v in plan.psi_brv]
-        assert [int(v) for v in d[0, 1, :, 0]] == [int(v) for v in plan.inv_psi_brv]
-        assert list(d[0, 0, :8, 1]) == [float(w) / p for w in plan.psi_brv[:8]]
+    if p < 2**46:  # FP64 NTT path: [N] double(w), [N] w/p per direction
+        d = ntt.view(np.float64).reshape(1, 2, 2, n)
+        assert [int(v) for v in d[0, 0, 0]] == [int(v) for v in plan.psi_brv]
+        assert [int(v) for v in d[0, 1, 0]] == [int(v) for v in plan.inv_psi_brv]
+        assert list(d[0, 0, 1, :8]) == [float(w) / p for w in plan.psi_brv[:8]]
     else:
         assert [int(v) for v in t[0, 0, :, 0]] == [int(v) for v in plan.psi_brv]
         assert [int(v) for v in t[0, 1, :, 0]] == [int(v) for v in plan.inv_psi_brv]
