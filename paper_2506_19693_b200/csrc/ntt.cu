@@ -264,6 +264,36 @@ __device__ __forceinline__ void gs_bfly_f64(double& X, double& Y, double W, doub
   Y = mulmod_f64(a - b, W, Wp, p);
 }
 
+// A thread's twiddles for one stage are NT consecutive entries starting at a
+// multiple of NT (t0 = (tbase << (S-1-b)) + (rbase >> (b+1)) with rbase's
+// low bits zero), so they load as 16-byte vectors.
+template <int NT>
+__device__ __forceinline__ void load_tw_f64(const double* __restrict__ tw, int t0, double* Wv,
+                                            double* Wpv, double pinv) {
+  if constexpr (NT >= 2) {
+#pragma unroll
+    for (int i = 0; i < NT; i += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(tw + t0 + i));
+      Wv[i] = v.x;
+      Wv[i + 1] = v.y;
+    }
+  } else {
+    Wv[0] = __ldg(tw + t0);
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) Wpv[i] = Wv[i] * pinv;
+}
+
+__device__ __forceinline__ void load_tw_f64_n(int nt, const double* __restrict__ tw, int t0,
+                                              double* Wv, double* Wpv, double pinv) {
+  switch (nt) {  // constant after unrolling
+    case 8: load_tw_f64<8>(tw, t0, Wv, Wpv, pinv); break;
+    case 4: load_tw_f64<4>(tw, t0, Wv, Wpv, pinv); break;
+    case 2: load_tw_f64<2>(tw, t0, Wv, Wpv, pinv); break;
+    default: load_tw_f64<1>(tw, t0, Wv, Wpv, pinv); break;
+  }
+}
+
 template <int S, int RB, int HI>
 __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, int gq, int tbase, int w,
@@ -283,13 +313,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
       const int bb = b - WLO;
       const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
       double Wv[E / 2], Wpv[E / 2];
-#pragma unroll
-      for (int i = 0; i < E / 2; ++i) {
-        if (i < ((E / 2) >> bb)) {
-          Wv[i] = __ldg(tw + t0 + i);  // contiguous double(w): 8 B per twiddle
-          Wpv[i] = Wv[i] * pinv;
-        }
-      }
+      load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if (k & (1 << bb)) continue;
@@ -339,13 +363,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
       } else {
         const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
         double Wv[E / 2], Wpv[E / 2];
-#pragma unroll
-        for (int i = 0; i < E / 2; ++i) {
-          if (i < ((E / 2) >> bb)) {
-            Wv[i] = __ldg(tw + t0 + i);  // contiguous double(w): 8 B per twiddle
-            Wpv[i] = Wv[i] * pinv;
-          }
-        }
+        load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
