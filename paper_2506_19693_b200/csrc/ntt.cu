@@ -294,10 +294,29 @@ __device__ __forceinline__ void load_tw_f64_n(int nt, const double* __restrict__
   }
 }
 
+// gsrc (first round only): the group's elements straight from global memory
+// (contiguous rows: lanes read consecutive words), u64in: canonical residues.
+template <int E, int WLO>
+__device__ __forceinline__ void load_round_f64(double* x, const uint64_t* sb,
+                                               const uint64_t* __restrict__ gsrc, int rbase,
+                                               bool u64in) {
+  if (gsrc) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const uint64_t v = __ldcs(gsrc + rbase + (k << WLO));
+      x[k] = u64in ? u64_to_f64(v) : __longlong_as_double((long long)v);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
+  }
+}
+
 template <int S, int RB, int HI>
 __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, int gq, int tbase, int w,
-                                               int last) {
+                                               int last, const uint64_t* gsrc = nullptr,
+                                               bool u64in = false) {
   if constexpr (HI > 0) {
     constexpr int E = 1 << RB;
     constexpr int Q = HI < RB ? HI : RB;
@@ -306,8 +325,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-#pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
+    load_round_f64<E, WLO>(x, sb, HI == S ? gsrc : nullptr, rbase, u64in);
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
@@ -338,7 +356,8 @@ template <int S, int RB, int LO>
 __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, double ninv, double ninvp,
                                                double fw, double fwp, int gq, int tbase, int w,
-                                               int last) {
+                                               int last, const uint64_t* gsrc = nullptr,
+                                               bool u64in = false) {
   if constexpr (LO < S) {
     constexpr int E = 1 << RB;
     constexpr int Q = (S - LO) < RB ? (S - LO) : RB;
@@ -347,8 +366,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-#pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
+    load_round_f64<E, WLO>(x, sb, LO == 0 ? gsrc : nullptr, rbase, u64in);
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
@@ -433,7 +451,13 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     g = e & (C - 1);
     return (size_t)r * ph.rstride + g0 + g;
   };
-  {
+  // FP64 path on contiguous rows of a second phase (input = the first phase's
+  // L2-resident doubles): the first register round reads global memory
+  // directly, no tile staging through shared memory.  Measured (A/B,
+  // tools/ab_ntt.sh): forward -3%; a first phase streaming from DRAM is 9%
+  // faster with the 16-byte tile loads, so it keeps them.
+  const bool direct = f64 && warp_local && !ph.first;
+  if (!direct) {
     ulonglong2 v[E / 2];
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
@@ -472,12 +496,13 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     const double pd = (double)p, pinv = 1.0 / pd;
     // FP64-path table: [N] double(w) forward, [N] w/p, then the inverse pair
     const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
+    const uint64_t* gsrc = direct ? base + (size_t)(g0 + gq) * ph.gstride : nullptr;
     if constexpr (FWD) {
-      fwd_rounds_f64<S, RB, S>(smem, dtab, pd, pinv, gq, tbase, w, ph.last);
+      fwd_rounds_f64<S, RB, S>(smem, dtab, pd, pinv, gq, tbase, w, ph.last, gsrc, ph.first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
       inv_rounds_f64<S, RB, 0>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv,
-                               gq, tbase, w, ph.last);
+                               gq, tbase, w, ph.last, gsrc, ph.first);
     }
   } else if constexpr (FWD) {
     fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
