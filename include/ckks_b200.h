@@ -52,6 +52,10 @@ typedef struct {
   const uint64_t* mods;
   const uint64_t* ntt;
   const uint64_t* pair;
+  /* bit i set: prime i is < 2^46 and its NTT rows may run the dedicated FP64
+   * radix-16 kernel (host-side copy of the class the kernels derive from p;
+   * all zero = one kernel choosing the path per row, same results). */
+  uint64_t f64_mask[2];
 } ckb_ring;
 
 /* Library version (for load checks). */

@@ -23,7 +23,19 @@ c_vp = ctypes.c_void_p
 
 class CkbRing(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n_primes", ctypes.c_uint32),
-                ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp)]
+                ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp),
+                ("f64_mask", ctypes.c_uint64 * 2)]
+
+
+F64_PRIME_LIMIT = 1 << 46  # csrc/ntt.cu: primes below run the FP64 butterflies
+
+
+def f64_mask(primes) -> tuple:
+    m = 0
+    for i, p in enumerate(primes):
+        if int(p) < F64_PRIME_LIMIT and i < 128:
+            m |= 1 << i
+    return (m & (2**64 - 1), m >> 64)
 
 
 class NativeError(RuntimeError):

@@ -31,6 +31,7 @@ struct RingDev {
   const uint64_t* pair;  // [np][np][4]
   uint32_t log_n;
   uint32_t np;
+  uint64_t f64_mask[2];  // host-side prime classes (ckb_ring.f64_mask)
 };
 
 __device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
@@ -56,6 +57,8 @@ inline RingDev make_ring(const ckb_ring* r) {
   d.pair = r->pair;
   d.log_n = r->log_n;
   d.np = r->n_primes;
+  d.f64_mask[0] = r->f64_mask[0];
+  d.f64_mask[1] = r->f64_mask[1];
   return d;
 }
 

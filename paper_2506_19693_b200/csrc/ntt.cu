@@ -404,7 +404,9 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
   }
 }
 
-template <int S, bool FWD, int RBT>
+// MODE 0: each CTA picks the FP64 or integer butterflies from its prime;
+// MODE 1: FP64 rows only (others exit); MODE 2: integer rows only.
+template <int S, bool FWD, int RBT, int MODE = 0>
 __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
   constexpr int G = 1 << S;
@@ -419,7 +421,8 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int pi = lm.p[row % ph.limbs];
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
   const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
-  const bool f64 = (p >> 46) == 0;  // CTA-uniform: FP64 path for primes < 2^46
+  const bool f64 = MODE == 1 || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
+  if ((MODE == 1 && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
   uint64_t* base = data + (size_t)row * N;
   const int C = ph.C;
   const int T = blockDim.x;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int tbase = ph.M0 + ph.gt * (g0 + gq);
   // per prime: N forward then N inverse {w, shoup(w)} pairs
   const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
-  if (f64) {
+  if (MODE != 2 && f64) {
     const double pd = (double)p, pinv = 1.0 / pd;
     // FP64-path table: [N] double(w) forward, [N] w/p, then the inverse pair
     const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
@@ -504,11 +507,13 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
       inv_rounds_f64<S, RB, 0>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv,
                                gq, tbase, w, ph.last, gsrc, ph.first);
     }
-  } else if constexpr (FWD) {
-    fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
-  } else {
-    inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
-                     __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
+  } else if constexpr (MODE != 1) {
+    if constexpr (FWD) {
+      fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
+    } else {
+      inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
+                           __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
+    }
   }
   if (warp_local)
     __syncwarp();
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   }
 }
 
-template <bool FWD, int RBT>
+template <bool FWD, int RBT, int MODE = 0>
 int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const RingDev& R,
                  const LimbMap& lm, cudaStream_t st) {
   const int G = 1 << S;
@@ -538,7 +543,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   if (threads > kNttThreads) return CKB_E_LOGN;
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
-    k_ntt_phase<SS, FWD, RBT><<<blocks, threads, smem, st>>>(data, ph, R, lm);     \
+    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, ph, R, lm); \
     break;
   switch (S) {
     CKB_NTT_CASE(4)
@@ -578,6 +583,13 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   if (s1 > 12) return CKB_E_LOGN;
   const int GA = 1 << s1, GB = 1 << s2;
   const int CA = std::max(1, kTwoPhaseTile / GA), CB = std::max(1, kTwoPhaseTile / GB);
+  // prime classes of this launch (host copy in the ring): FP64 rows go to the
+  // radix-16 FP64 kernel, integer rows to the radix-8 integer kernel
+  bool any_f64 = false, any_int = false;
+  for (int i = 0; i < limbs; ++i) {
+    const int pi = lm.p[i];
+    ((R.f64_mask[pi >> 6] >> (pi & 63)) & 1 ? any_f64 : any_int) = true;
+  }
   // phase A: groups are the GB columns, elements strided by GB
   auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
   const int items = (rows % limbs == 0 && rows / limbs > 1) ? rows / limbs : 0;
@@ -590,13 +602,19 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     const int nr = std::min(chunk, rows - r0);
     pa.row0 = r0;
     pb.row0 = r0;
-    int rc;
+    int rc = 0;
+    auto run = [&](int S, const NttPhase& ph) {
+      if (!any_f64) return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
+      int r = launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
+      if (!r && any_int) r = launch_phase<FWD, 3, 2>(S, data, ph, nr, R, lm, st);
+      return r;
+    };
     if (FWD) {
-      rc = launch_phase<FWD, 3>(s1, data, pa, nr, R, lm, st);
-      if (!rc) rc = launch_phase<FWD, 3>(s2, data, pb, nr, R, lm, st);
+      rc = run(s1, pa);
+      if (!rc) rc = run(s2, pb);
     } else {
-      rc = launch_phase<FWD, 3>(s2, data, pb, nr, R, lm, st);
-      if (!rc) rc = launch_phase<FWD, 3>(s1, data, pa, nr, R, lm, st);
+      rc = run(s2, pb);
+      if (!rc) rc = run(s1, pa);
     }
     if (rc) return rc;
   }

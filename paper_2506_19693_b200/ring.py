@@ -97,7 +97,8 @@ class GpuChain:
         self._ntt = torch.from_numpy(ntt.reshape(-1)).to(dev)
         self._pair = torch.from_numpy(pair.reshape(-1)).to(dev)
         self.ring = nat.CkbRing(self.log_n, len(self.all_primes), self._mods.data_ptr(),
-                                self._ntt.data_ptr(), self._pair.data_ptr())
+                                self._ntt.data_ptr(), self._pair.data_ptr(),
+                                (nat.ctypes.c_uint64 * 2)(*nat.f64_mask(self.all_primes)))
         self.ring_p = nat.ctypes.pointer(self.ring)
         self._maps: dict = {}
 
@@ -191,7 +192,7 @@ class GpuChain:
         chunk = max(1, (48 << 20) // (self.n * W))
         return 2 * (-(-rows // chunk))
 
-    F64_PRIME_LIMIT = 1 << 46  # csrc/ntt.cu: primes below run the FP64 butterfly
+    F64_PRIME_LIMIT = nat.F64_PRIME_LIMIT
 
     def _f64_share(self, lmap, limbs: int):
         return lambda: sum(self.all_primes[lmap[i]] < self.F64_PRIME_LIMIT

@@ -16,7 +16,7 @@ def chain_for(logn, nprimes, bits=40):
     ch.all_primes = primes; ch.primes = primes; ch.special_primes = []; ch.lq, ch.k = len(primes), 0
     mods, ntt, pair = nat.build_tables(logn, primes)
     ch._mods = torch.from_numpy(mods).cuda(); ch._ntt = torch.from_numpy(ntt.reshape(-1)).cuda(); ch._pair = torch.from_numpy(pair.reshape(-1)).cuda()
-    ch.ring = nat.CkbRing(logn, len(primes), ch._mods.data_ptr(), ch._ntt.data_ptr(), ch._pair.data_ptr())
+    ch.ring = nat.CkbRing(logn, len(primes), ch._mods.data_ptr(), ch._ntt.data_ptr(), ch._pair.data_ptr(), (nat.ctypes.c_uint64 * 2)(*nat.f64_mask(primes)))
     ch.ring_p = nat.ctypes.pointer(ch.ring); ch._maps = {}
     return ch
 
