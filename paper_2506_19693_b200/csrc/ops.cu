@@ -555,42 +555,64 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
 }
 
 // out_j = (x_j * P1^-1 + add_j - E_j) * P2^-1, all in the NTT domain.
-__global__ void k_divround_combine(uint64_t* __restrict__ out, const uint64_t* __restrict__ x,
-                                   size_t x_stride, const uint64_t* __restrict__ addend,
-                                   int add_polys, int add_period, int add_stride,
-                                   const uint64_t* __restrict__ E, int polys, int limbs, int n1,
-                                   int n2, int log_n, RingDev R, LimbMap lm,
-                                   const uint64_t* __restrict__ tab1,
-                                   const uint64_t* __restrict__ tab2) {
+__global__ void __launch_bounds__(256) k_divround_combine(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ x, size_t x_stride,
+    const uint64_t* __restrict__ addend, int add_polys, int add_period, int add_stride,
+    const uint64_t* __restrict__ E, int polys, int limbs, int n1, int n2, int log_n, RingDev R,
+    LimbMap lm, const uint64_t* __restrict__ tab1, const uint64_t* __restrict__ tab2) {
+  // grid: x over coefficient pairs of one row, y over rows (poly, limb): the
+  // row's constants are loaded once, every access is a 16-byte vector
   const size_t N = (size_t)1 << log_n;
   const int m1 = limbs - n1;
   const int m2 = m1 - n2;
-  const size_t total = (size_t)polys * m2 * N;
+  const size_t rows = (size_t)polys * m2;
   const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1);
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
-       t += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = t & (N - 1);
-    const size_t pj = t >> log_n;
+  const size_t half = N >> 1;
+  for (size_t pj = blockIdx.y; pj < rows; pj += gridDim.y) {
     const int j = (int)(pj % m2);
     const size_t pidx = pj / m2;
     const uint64_t p = __ldg(R.mods + (size_t)lm.p[j] * kModStride);
-    uint64_t v = x[pidx * x_stride + (size_t)j * N + n];
+    uint64_t a1 = 0, a1s = 0, b2 = 0, b2s = 0;
     if (n1) {
-      const uint64_t* Ta = tab1 + (size_t)j * s1 + 2 * n1;
-      v = ckb::mul_shoup(v, __ldg(Ta), __ldg(Ta + 1), p);
+      a1 = __ldg(tab1 + (size_t)j * s1 + 2 * n1);
+      a1s = __ldg(tab1 + (size_t)j * s1 + 2 * n1 + 1);
     }
+    if (n2) {
+      b2 = __ldg(tab2 + (size_t)j * s2 + 2 * n2);
+      b2s = __ldg(tab2 + (size_t)j * s2 + 2 * n2 + 1);
+    }
+    const uint64_t* xr = x + pidx * x_stride + (size_t)j * N;
+    const uint64_t* ar = nullptr;
     if (addend) {
       const size_t ph = pidx % add_period;
       if ((int)ph < add_polys)
-        v = ckb::add_mod(
-            v, addend[((pidx / add_period) * add_stride + ph) * m1 * N + (size_t)j * N + n], p);
+        ar = addend + ((pidx / add_period) * add_stride + ph) * m1 * N + (size_t)j * N;
     }
-    v = ckb::sub_mod(v, E[t], p);
-    if (n2) {
-      const uint64_t* Tb = tab2 + (size_t)j * s2 + 2 * n2;
-      v = ckb::mul_shoup(v, __ldg(Tb), __ldg(Tb + 1), p);
+    const uint64_t* er = E + pj * N;
+    uint64_t* orow = out + pj * N;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < half;
+         q += (size_t)gridDim.x * blockDim.x) {
+      const size_t n = 2 * q;
+      ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + n);
+      const ulonglong2 e = *reinterpret_cast<const ulonglong2*>(er + n);
+      ulonglong2 a = make_ulonglong2(0, 0);
+      if (ar) a = *reinterpret_cast<const ulonglong2*>(ar + n);
+      if (n1) {
+        v.x = ckb::mul_shoup(v.x, a1, a1s, p);
+        v.y = ckb::mul_shoup(v.y, a1, a1s, p);
+      }
+      if (ar) {
+        v.x = ckb::add_mod(v.x, a.x, p);
+        v.y = ckb::add_mod(v.y, a.y, p);
+      }
+      v.x = ckb::sub_mod(v.x, e.x, p);
+      v.y = ckb::sub_mod(v.y, e.y, p);
+      if (n2) {
+        v.x = ckb::mul_shoup(v.x, b2, b2s, p);
+        v.y = ckb::mul_shoup(v.y, b2, b2s, p);
+      }
+      *reinterpret_cast<ulonglong2*>(orow + n) = v;
     }
-    out[t] = v;
   }
 }
 
@@ -1137,7 +1159,11 @@ int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t
   const size_t total = ((size_t)polys * m2) << R.log_n;
   if (!total) return 0;
   const size_t xs = x_poly_stride > 0 ? (size_t)x_poly_stride : ((size_t)limbs << R.log_n);
-  k_divround_combine<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+  const size_t rows = (size_t)polys * (limbs - n_drop1 - n_drop2);
+  const size_t pairs = (size_t)1 << (R.log_n - 1);
+  dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((pairs + 255) / 256, 64)),
+            (unsigned)std::min<size_t>(rows, 65535));
+  k_divround_combine<<<grid, 256, 0, (cudaStream_t)stream>>>(
       out, x, xs, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
       addend ? addend_stride : 0, E, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1,
       tab2);
