@@ -294,16 +294,29 @@ __device__ __forceinline__ void load_tw_f64_n(int nt, const double* __restrict__
   }
 }
 
-// gsrc (first round only): the group's elements straight from global memory
-// (contiguous rows: lanes read consecutive words), u64in: canonical residues.
-template <int E, int WLO>
+// Global I/O of the FP64 register rounds.  CM = false: the first round may
+// read contiguous rows straight from global memory (gsrc), rounds exchange
+// through shared memory with warp-local syncs where a group fits in a warp,
+// and the last round stores to shared memory (tile store).  CM = true (column
+// mapping, second phases): the first round reads and the last round writes
+// global memory with element stride gs; one CTA barrier between rounds.
+template <int E, int WLO, bool CM>
 __device__ __forceinline__ void load_round_f64(double* x, const uint64_t* sb,
-                                               const uint64_t* __restrict__ gsrc, int rbase,
-                                               bool u64in) {
-  if (gsrc) {
+                                               const uint64_t* __restrict__ gsrc, int gs,
+                                               int rbase, bool u64in) {
+  if (CM && gsrc) {
+    const uint64_t* g = gsrc + (size_t)rbase * gs;
+    const size_t step = (size_t)gs << WLO;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const uint64_t v = __ldcs(gsrc + rbase + (k << WLO));
+      const uint64_t v = __ldcs(g + k * step);
+      x[k] = u64in ? u64_to_f64(v) : __longlong_as_double((long long)v);
+    }
+  } else if (!CM && gsrc) {
+    const uint64_t* g = gsrc + rbase;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const uint64_t v = __ldcs(g + (k << WLO));
       x[k] = u64in ? u64_to_f64(v) : __longlong_as_double((long long)v);
     }
   } else {
@@ -312,11 +325,20 @@ __device__ __forceinline__ void load_round_f64(double* x, const uint64_t* sb,
   }
 }
 
-template <int S, int RB, int HI>
+template <int S, int RB, bool CM>
+__device__ __forceinline__ void rsync() {
+  if constexpr (CM) {
+    __syncthreads();
+  } else {
+    round_sync<S, RB>();
+  }
+}
+
+template <int S, int RB, int HI, bool CM>
 __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, int gq, int tbase, int w,
-                                               int last, const uint64_t* gsrc = nullptr,
-                                               bool u64in = false) {
+                                               int last, const uint64_t* gsrc, uint64_t* gdst,
+                                               int gs, bool u64in) {
   if constexpr (HI > 0) {
     constexpr int E = 1 << RB;
     constexpr int Q = HI < RB ? HI : RB;
@@ -325,7 +347,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-    load_round_f64<E, WLO>(x, sb, HI == S ? gsrc : nullptr, rbase, u64in);
+    load_round_f64<E, WLO, CM>(x, sb, HI == S ? gsrc : nullptr, gs, rbase, u64in);
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
@@ -339,6 +361,18 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
         ct_bfly_f64(x[k], x[k | (1 << bb)], Wv[i], Wpv[i], p);
       }
     }
+    if constexpr (CM && LO == 0) {  // column mapping: straight to global memory
+      const size_t step = (size_t)gs << WLO;
+      uint64_t* g = gdst + (size_t)rbase * gs;
+      if (last) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) __stcs(g + k * step, f64_to_u64(canon_f64(x[k], p, pinv)));
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) __stcs(g + k * step, (uint64_t)__double_as_longlong(x[k]));
+      }
+      return;
+    }
     if (LO == 0 && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k)
@@ -347,17 +381,17 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
 #pragma unroll
       for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(x[k]);
     }
-    round_sync<S, RB>();
-    fwd_rounds_f64<S, RB, LO>(s, tw, p, pinv, gq, tbase, w, last);
+    rsync<S, RB, CM>();
+    fwd_rounds_f64<S, RB, LO, CM>(s, tw, p, pinv, gq, tbase, w, last, gsrc, gdst, gs, u64in);
   }
 }
 
-template <int S, int RB, int LO>
+template <int S, int RB, int LO, bool CM>
 __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, double ninv, double ninvp,
                                                double fw, double fwp, int gq, int tbase, int w,
-                                               int last, const uint64_t* gsrc = nullptr,
-                                               bool u64in = false) {
+                                               int last, const uint64_t* gsrc, uint64_t* gdst,
+                                               int gs, bool u64in) {
   if constexpr (LO < S) {
     constexpr int E = 1 << RB;
     constexpr int Q = (S - LO) < RB ? (S - LO) : RB;
@@ -366,7 +400,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-    load_round_f64<E, WLO>(x, sb, LO == 0 ? gsrc : nullptr, rbase, u64in);
+    load_round_f64<E, WLO, CM>(x, sb, LO == 0 ? gsrc : nullptr, gs, rbase, u64in);
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
@@ -390,6 +424,19 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
         }
       }
     }
+    if constexpr (CM && HI == S) {
+      const size_t step = (size_t)gs << WLO;
+      uint64_t* g = gdst + (size_t)rbase * gs;
+      if (last) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) __stcs(g + k * step, f64_to_u64(canon_f64(x[k], p, pinv)));
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          __stcs(g + k * step, (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv)));
+      }
+      return;
+    }
     if (HI == S && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k)
@@ -399,13 +446,12 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
       for (int k = 0; k < E; ++k)
         sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv));
     }
-    round_sync<S, RB>();
-    inv_rounds_f64<S, RB, HI>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last);
+    rsync<S, RB, CM>();
+    inv_rounds_f64<S, RB, HI, CM>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last, gsrc,
+                                  gdst, gs, u64in);
   }
 }
 
-// MODE 0: each CTA picks the FP64 or integer butterflies from its prime;
-// MODE 1: FP64 rows only (others exit); MODE 2: integer rows only.
 template <int S, bool FWD, int RBT, int MODE = 0>
 __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
@@ -421,8 +467,8 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   const int pi = lm.p[row % ph.limbs];
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
   const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
-  const bool f64 = MODE == 1 || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
-  if ((MODE == 1 && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
+  const bool f64 = MODE == 1 || MODE == 3 || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
+  if (((MODE == 1 || MODE == 3) && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
   uint64_t* base = data + (size_t)row * N;
   const int C = ph.C;
   const int T = blockDim.x;
@@ -460,7 +506,16 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   // tools/ab_ntt.sh): forward -3%; a first phase streaming from DRAM is 9%
   // faster with the 16-byte tile loads, so it keeps them.
   const bool direct = f64 && warp_local && !ph.first;
-  if (!direct) {
+  // FP64-only kernel, column phase: lanes span the tile's C columns
+  // (gq = tid % C, w = tid / C) so both the first round's loads and the last
+  // round's stores go straight to global memory (each warp instruction
+  // touches 32/C rows x C contiguous words); one shared exchange between the
+  // two radix-16 rounds, behind a CTA barrier.
+  // (second phases only, chosen by the host: a first phase streaming from
+  // DRAM keeps the 16-byte tile loads — A/B: forward column phase +5% with
+  // the column mapping, inverse column phase -4%)
+  constexpr bool colmap = MODE == 3;
+  if (!direct && !colmap) {
     ulonglong2 v[E / 2];
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
@@ -487,11 +542,11 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
   }
   if (warp_local)
     __syncwarp();
-  else
+  else if (!colmap)
     __syncthreads();
 
-  const int gq = tid / (G / E);
-  const int w = tid % (G / E);
+  const int gq = colmap ? (tid & (C - 1)) : tid / (G / E);
+  const int w = colmap ? (tid >> ph.logC) : tid % (G / E);
   const int tbase = ph.M0 + ph.gt * (g0 + gq);
   // per prime: N forward then N inverse {w, shoup(w)} pairs
   const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
@@ -499,14 +554,20 @@ __global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
     const double pd = (double)p, pinv = 1.0 / pd;
     // FP64-path table: [N] double(w) forward, [N] w/p, then the inverse pair
     const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
-    const uint64_t* gsrc = direct ? base + (size_t)(g0 + gq) * ph.gstride : nullptr;
+    const uint64_t* gsrc = colmap ? base + g0 + gq
+                                  : (direct ? base + (size_t)(g0 + gq) * ph.gstride : nullptr);
+    uint64_t* gdst = colmap ? base + g0 + gq : nullptr;
+    const int gs = colmap ? ph.rstride : 1;
     if constexpr (FWD) {
-      fwd_rounds_f64<S, RB, S>(smem, dtab, pd, pinv, gq, tbase, w, ph.last, gsrc, ph.first);
+      fwd_rounds_f64<S, RB, S, colmap>(smem, dtab, pd, pinv, gq, tbase, w, ph.last, gsrc, gdst,
+                                       gs, ph.first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
-      inv_rounds_f64<S, RB, 0>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv,
-                               gq, tbase, w, ph.last, gsrc, ph.first);
+      inv_rounds_f64<S, RB, 0, colmap>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw,
+                                       fw * pinv, gq, tbase, w, ph.last, gsrc, gdst, gs,
+                                       ph.first);
     }
+    if constexpr (colmap) return;  // stored straight to global memory
   } else if constexpr (MODE != 1) {
     if constexpr (FWD) {
       fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
@@ -605,7 +666,9 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
       if (!any_f64) return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
-      int r = launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
+      const bool cm = ph.rstride != 1 && !ph.first;  // second-pass column phase
+      int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st)
+                 : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
       if (!r && any_int) r = launch_phase<FWD, 3, 2>(S, data, ph, nr, R, lm, st);
       return r;
     };
