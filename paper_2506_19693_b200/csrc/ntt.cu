@@ -453,7 +453,8 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
 }
 
 template <int S, bool FWD, int RBT, int MODE = 0>
-__global__ void __launch_bounds__(kNttThreads, RBT == 3 ? 4 : 3)
+__global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
+                                  MODE == 1 || MODE == 3 ? (FWD ? 6 : 8) : (RBT == 3 ? 4 : 3))
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
   constexpr int G = 1 << S;
   constexpr int RB = S < RBT ? S : RBT;  // log2 elements per thread
