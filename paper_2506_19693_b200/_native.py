@@ -144,5 +144,13 @@ def ptr(t: torch.Tensor):
     return ctypes.c_void_p(t.data_ptr())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle():
+    """The caller's current CUDA stream (every launch goes on it).  The raw
+    accessor avoids constructing a torch.cuda.Stream object per launch, which
+    dominated the host cost of small-ring (N=2^12) programs."""
+    if _raw_stream is not None:
+        return ctypes.c_void_p(_raw_stream(torch._C._cuda_getDevice()))
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
