@@ -138,6 +138,14 @@ class DataParallelExecutor(WaveExecutor):
             v[: pts.shape[1]] = pts[i]
             return v
 
+        def runs(i):  # ops this rank executes (joins: only when both operands are here)
+            k = plan.kind[i]
+            if k == "join":
+                a, b = plan.join_args[i]
+                return plan.present(plan.deps[a], rank) and plan.present(plan.deps[b], rank)
+            return k == "rep" or (isinstance(k, tuple) and k[1] == rank)
+
+        self._pre_encode(pvals, self.n_setup if only_after_setup else 0, runs)
         for wave in self.waves:
             if only_after_setup:
                 wave = [i for i in wave if i >= self.n_setup]

@@ -100,6 +100,7 @@ class WaveExecutor:
             v[: pts.shape[1]] = pts[i]
             return v
 
+        self._pre_encode(pvals, self.n_setup if only_after_setup else 0)
         for wave in self.waves:
             if only_after_setup:
                 wave = [i for i in wave if i >= self.n_setup]
@@ -133,6 +134,26 @@ class WaveExecutor:
 
         be._serials = itertools.count(self.serials_used)
         return env
+
+    def _pre_encode(self, pvals, start: int, runs=None) -> None:
+        """Every plaintext the program will encode, batched per (level, NTT form)
+        before the first wave (backend.encode_many); the per-op encodes then hit
+        the cache.  Levels are the static ones of _plan."""
+        ops = self.prog.ops
+        top = self.be.params.level
+        items = []
+        for i in range(start, len(ops)):
+            op = ops[i]
+            if runs is not None and not runs(i):
+                continue
+            if op[0] == "enc":
+                items.append((pvals(op[2]), top, False))
+            elif op[0] == "ew" and not op[1].endswith("_ct"):
+                kind, a, pid = op[1], op[3], op[4]
+                v = pvals(pid)
+                items.append((-v if kind.startswith("sub") else v, self.level_of[a], True))
+        if items and hasattr(self.be, "encode_many"):
+            self.be.encode_many(items)
 
     def _stack(self, items):
         if len(items) == 1:
