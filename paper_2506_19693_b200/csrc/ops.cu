@@ -952,9 +952,15 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   if (!total || !nd) return 0;
   const size_t bstride = in_batch_stride > 0 ? (size_t)in_batch_stride : ((size_t)limbs << R.log_n);
   const int out_rows = skip_own ? ext_limbs - alpha : ext_limbs;
-  const int amax = alpha == 1 ? 1 : alpha <= 2 ? 2 : alpha <= 4 ? 4 : alpha <= 8 ? 8 : 16;
-  auto kern = amax == 1 ? k_modup<1> : amax == 2 ? k_modup<2> : amax == 4 ? k_modup<4>
-            : amax == 8 ? k_modup<8> : k_modup<16>;
+  // exact digit width (a rounded-up template would multiply by zero constants)
+  using KernT = decltype(&k_modup<1>);
+  static const KernT kerns[17] = {nullptr,       k_modup<1>,  k_modup<2>,  k_modup<3>,
+                                  k_modup<4>,    k_modup<5>,  k_modup<6>,  k_modup<7>,
+                                  k_modup<8>,    k_modup<9>,  k_modup<10>, k_modup<11>,
+                                  k_modup<12>,   k_modup<13>, k_modup<14>, k_modup<15>,
+                                  k_modup<16>};
+  const int amax = alpha;
+  auto kern = kerns[alpha];
   const size_t smem = (6 * (size_t)ext_limbs +
                        (amax == 1 ? 0 : (size_t)alpha * (2 + 2 * (size_t)ext_limbs))) * 8;
   const size_t work = (size_t)batch << (R.log_n - 1);
