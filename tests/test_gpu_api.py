@@ -116,3 +116,36 @@ def test_empty_batches_are_no_ops(small):
                                    0, 1, lm, 0, nat.stream_handle()) == 0
     torch.cuda.synchronize()
     assert int(buf.view(torch.int64)[0]) == 0
+
+
+def test_streaming_pipeline_matches_direct(small):
+    """streaming.Pipeline (chunked H2D / compute / D2H on three streams) gives
+    the same planes as one direct batched call."""
+    from paper_2506_19693_b200.streaming import Pipeline
+
+    params, cust = small
+    be = cust.backend
+    lvl = params.level
+    m = be.chain.level_limbs[lvl]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+
+    def rand_batch(b):
+        t = torch.empty(b, 2, m, be.n, dtype=torch.int64, device="cuda")
+        for i, p in enumerate(be.chain.limbs_at(lvl)):
+            t[:, :, i].random_(0, p, generator=gen)
+        return t.view(torch.uint64)
+
+    a, b = rand_batch(5), rand_batch(5)
+    steps = [1, 2, 3, 1, 2]
+    want_m = be.batch_hmult(a, b, lvl).cpu()
+    want_r = be.batch_hrot(a, steps, lvl).cpu()
+    ha, hb = a.cpu().pin_memory(), b.cpu().pin_memory()
+    om = torch.empty_like(want_m).pin_memory()
+    orr = torch.empty_like(want_r).pin_memory()
+    Pipeline().run(lambda d, lo, hi: [be.batch_hmult(d[0], d[1], lvl),
+                                      be.batch_hrot(d[0], steps[lo:hi], lvl)],
+                   [ha, hb], [om, orr], chunk=2)
+    torch.cuda.synchronize()
+    assert torch.equal(om.view(torch.int64), want_m.view(torch.int64))
+    assert torch.equal(orr.view(torch.int64), want_r.view(torch.int64))
