@@ -129,23 +129,25 @@ def _cpu_case(L):
     return PR.make_random_case(1 << N_LOG, L, seed=5)
 
 
-def _cpu_hmult(case, procs):
-    """One HMult (mul + relinearise + rescale) of one ciphertext with the
-    reference's algorithm and prime layout (per-limb digits, sub-2^31 primes;
-    oracle/ckks_oracle.py), key switch split over `procs` host processes
-    (oracle/parallel_ref.py).  Returns seconds."""
+def _cpu_step(case, procs):
+    """One HMult (mul + relinearise + rescale) and one HRot of one ciphertext
+    with the reference's algorithm and prime layout (per-limb digits, sub-2^31
+    primes; oracle/ckks_oracle.py), each key switch split over `procs` host
+    processes (oracle/parallel_ref.py) — the B200 arm's step mix.  Returns
+    seconds."""
     from oracle import parallel_ref as PR
 
     chain, (a, b), kb, ka = case
-    _, secs = PR.hmult_parallel(chain, a, b, kb, ka, procs)
-    return secs
+    _, s1 = PR.hmult_parallel(chain, a, b, kb, ka, procs)
+    _, s2 = PR.hrot_parallel(chain, a, pow(5, 12345, 2 * chain.n), kb, ka, procs)
+    return s1 + s2
 
 
 def _cpu_sample_text(L, procs):
-    return (f"one HMult of one ciphertext (N=2^16, {L} x 40-bit entries in the reference's "
-            f"sub-2^31 prime layout = {2 * L}+2 limbs, per-limb digits), numpy oracle port of "
-            f"ckks/backend.py:136-143, key switch split over {procs} processes; bytes = "
-            f"BASELINE HMult formula at the B200 arm's parameters")
+    return (f"one HMult + one HRot of one ciphertext (N=2^16, {L} x 40-bit entries in the "
+            f"reference's sub-2^31 prime layout = {2 * L}+2 limbs, per-limb digits), numpy "
+            f"oracle port of ckks/backend.py:136-171, key switch split over {procs} processes; "
+            f"bytes = BASELINE HMult + HRot formulas at the B200 arm's parameters (1 key each)")
 
 
 def run_reference(args):
@@ -159,23 +161,23 @@ def run_reference(args):
 
     L = args.limbs
     _, k = c2_params(L)
-    hm, _, _ = alg_bytes(L, k, 1, 0)
+    hm, hr, _ = alg_bytes(L, k, 1, 1)
     procs = args.ref_procs or PR.default_procs()
     case = _cpu_case(L)
     times = []
     for step in range(args.warmup + args.steps):
-        dt = _cpu_hmult(case, procs)
+        dt = _cpu_step(case, procs)
         if step >= args.warmup:
             times.append(dt)
     ms = 1e3 * float(np.mean(times))
-    value = hm / (ms / 1e3) / 1e9
+    value = (hm + hr) / (ms / 1e3) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic",
-        "config": {"workload": f"c2 HMult at N=2^16, L={L}: reference algorithm and prime layout "
-                               f"on the host CPU", "batch_per_step": 1},
+        "config": {"workload": f"c2 HMult + HRot at N=2^16, L={L}: reference algorithm and "
+                               f"prime layout on the host CPU", "batch_per_step": 1},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": procs, "kind": "port",
                          "sample": _cpu_sample_text(L, procs)},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -615,9 +617,9 @@ def main():
         from oracle import parallel_ref as PR
 
         procs = args.ref_procs or PR.default_procs()
-        secs = _cpu_hmult(_cpu_case(L), procs)
-        hm1, _, _ = alg_bytes(L, k, 1, 0)
-        line["cpu_baseline"] = {"value": hm1 / secs / 1e9, "unit": "GB/s", "cores": procs,
+        secs = _cpu_step(_cpu_case(L), procs)
+        hm1, hr1, _ = alg_bytes(L, k, 1, 1)
+        line["cpu_baseline"] = {"value": (hm1 + hr1) / secs / 1e9, "unit": "GB/s", "cores": procs,
                                 "kind": "port", "seconds": secs,
                                 "sample": _cpu_sample_text(L, procs)}
     if world > 1:

@@ -113,6 +113,51 @@ def hmult_parallel(chain, a: "O.Ct", b: "O.Ct", kb_row: "O.Elem", ka_row: "O.Ele
     return out, time.perf_counter() - t0
 
 
+def _key_switch_parallel(ch, d2, kb_row, ka_row, procs):
+    """keys.py:74-100 for the coefficient-domain polynomial d2: the per-limb
+    digit lift + NTT + key multiply-accumulate split over `procs` processes,
+    then iNTT and the sequential divide-round by the special primes."""
+    from multiprocessing import shared_memory
+
+    ext = list(d2.primes) + list(ch.special_primes)
+    full = ch.all_primes
+    kb = [[kb_row.planes[full.index(p)] for p in ext]] * len(d2.primes)
+    ka = [[ka_row.planes[full.index(p)] for p in ext]] * len(d2.primes)
+    shape = (2, len(ext), ch.n)
+    shm = shared_memory.SharedMemory(create=True, size=int(np.prod(shape)) * 8)
+    try:
+        _STATE.update(chain=ch, d2=d2, kb=kb, ka=ka, ext=ext, shape=shape, shm=shm)
+        parts = [list(range(len(ext)))[i::procs] for i in range(procs)]
+        parts = [p for p in parts if p]
+        if procs > 1:
+            with mp.get_context("fork").Pool(len(parts)) as pool:
+                pool.map(_worker, parts)
+        else:
+            _worker(parts[0])
+        acc = np.ndarray(shape, dtype=np.uint64, buffer=shm.buf).copy()
+    finally:
+        _STATE.clear()
+        shm.close()
+        shm.unlink()
+    acc_b = O.Elem(tuple(ext), [acc[0, e] for e in range(len(ext))], True)
+    acc_a = O.Elem(tuple(ext), [acc[1, e] for e in range(len(ext))], True)
+    drops = list(reversed(ch.special_primes))
+    return (O.divide_round_by_primes(O.e_coeff(acc_b, ch), drops),
+            O.divide_round_by_primes(O.e_coeff(acc_a, ch), drops))
+
+
+def hrot_parallel(chain, a: "O.Ct", galois: int, kb_row: "O.Elem", ka_row: "O.Elem",
+                  procs: int) -> tuple:
+    """One rotation, reference algorithm (backend.py:155-171): automorphism of
+    both components, key switch of c1', (c0' + r0, r1).  Returns (Ct, seconds)."""
+    t0 = time.perf_counter()
+    c0 = O.apply_automorphism(a.c0, galois)
+    c1 = O.apply_automorphism(a.c1, galois)
+    r0, r1 = _key_switch_parallel(chain, c1, kb_row, ka_row, procs)
+    out = O.Ct(O.e_add(c0, r0), r1, a.level)
+    return out, time.perf_counter() - t0
+
+
 def default_procs() -> int:
     try:
         return len(os.sched_getaffinity(0))
