@@ -152,7 +152,7 @@ def _cpu_sample_text(L, procs):
 
 def run_reference(args):
     """--impl reference: the reference algorithm (oracle port, numpy) on all
-    host cores; one step = one HMult of one ciphertext."""
+    host cores; one step = one HMult + one HRot of one ciphertext."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
