@@ -52,6 +52,24 @@ ERROR_SIGMA = 3.2
 MAX_SAFE_COEFF = float(2**52)
 
 
+# While a CUDA graph is being captured (graphs.GraphedStep), the pinned
+# staging tensors of in-graph uploads are kept alive here for the graph's life.
+H2D_KEEPALIVE = None
+
+
+def _h2d(arr: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device without a stream sync: staged through pinned memory
+    (torch's caching host allocator) and copied asynchronously.  A plain copy
+    from pageable memory would make the host wait for all queued GPU work."""
+    t = torch.from_numpy(np.array(arr, copy=True, order="C"))  # writable, owned
+    if torch.device(device).type != "cuda":
+        return t.to(device)
+    pinned = t.pin_memory()
+    if H2D_KEEPALIVE is not None:
+        H2D_KEEPALIVE.append(pinned)
+    return pinned.to(device, non_blocking=True)
+
+
 @dataclasses.dataclass(frozen=True)
 class GpuCiphertext:
     """(c0, c1) at one chain level; NTT domain (bit-reversed evaluation slots of
@@ -92,7 +110,7 @@ class DeviceEncoder:
 
     def embed_device(self, values, scale: float) -> torch.Tensor:
         """Real slots -> int64 coefficients [N] on the device (encoding.py:34-49)."""
-        v = torch.as_tensor(np.asarray(values, dtype=np.float64), device=self.device)
+        v = _h2d(np.asarray(values, dtype=np.float64), self.device)
         spec = torch.zeros(self.n, dtype=torch.complex128, device=self.device)
         scaled = torch.zeros(self.n // 2, dtype=torch.float64, device=self.device)
         scaled[: v.shape[0]] = v * scale
@@ -103,7 +121,7 @@ class DeviceEncoder:
 
     def embed_device_batch(self, values: np.ndarray, scale: float) -> torch.Tensor:
         """[B, <= N/2] real slot rows -> [B, N] coefficients (one batched FFT)."""
-        v = torch.as_tensor(np.asarray(values, dtype=np.float64), device=self.device)
+        v = _h2d(np.asarray(values, dtype=np.float64), self.device)
         b = v.shape[0]
         spec = torch.zeros(b, self.n, dtype=torch.complex128, device=self.device)
         scaled = torch.zeros(b, self.n // 2, dtype=torch.float64, device=self.device)
@@ -566,8 +584,8 @@ class B200CkksCore:
         msgs = []
         if self.sampler == "philox":
             srs = [next(self._serials) if sr is None else sr for sr in serials]
-            seeds = torch.tensor([_mix64(self.rng_seed, 0x454E43, sr) for sr in srs],
-                                 dtype=torch.int64, device=self.device).view(U64)
+            seeds = _h2d(np.array([_mix64(self.rng_seed, 0x454E43, sr) for sr in srs],
+                                  dtype=np.int64), self.device).view(U64)
             a_d, e_d = ch.sample(seeds, m)
             msgs = [self._encode_rns(values, level) for values in values_list]
             out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)

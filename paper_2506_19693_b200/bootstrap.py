@@ -117,11 +117,21 @@ class Bootstrapper:
         data, lvl, sc = a
         q = self._q(lvl)
         pt_scale = q if out_scale is None else out_scale * q / sc
-        pt = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True, scale=pt_scale,
-                                 limit=2.0**62)
+        pt = self._const_pt(c, lvl, pt_scale)
         m = self.be._limbs(lvl)
         out = self.be._rescale_data(self.be.chain.mul(data, pt, m, b_rows=m), lvl)
         return out, lvl - 1, sc * pt_scale / q
+
+    def _const_pt(self, c: float, lvl: int, scale: float):
+        """NTT-form plaintext of the constant slot vector c at `scale`: part of
+        the bootstrapping constants, kept in this object's cache (like the
+        BSGS diagonals) rather than the backend's per-step encode cache."""
+        key = ("const", float(c), lvl, float(scale))
+        pt = self._pt_cache.get(key)
+        if pt is None:
+            pt = self._pt_cache[key] = self.be._encode_rns(
+                np.full(self.slots, c), lvl, ntt=True, scale=scale, limit=2.0**62)
+        return pt
 
     def _restrict(self, a, level: int):
         """Drop limbs down to `level` (exact; the scale is unchanged)."""
@@ -134,7 +144,7 @@ class Bootstrapper:
     def _add_const(self, a, c: float):
         data, lvl, sc = a
         m = self.be._limbs(lvl)
-        pt = self.be._encode_rns(np.full(self.slots, c), lvl, ntt=True, scale=sc, limit=2.0**62)
+        pt = self._const_pt(c, lvl, sc)
         out = data.clone()
         self.be.chain.add(data[0], pt, m, out=out[0])
         return out, lvl, sc

@@ -84,9 +84,12 @@ class WaveExecutor:
         self.serials_used = counter
 
     # -- execution -----------------------------------------------------------
-    def run(self, env=None, only_after_setup: bool = False) -> dict:
+    def run(self, env=None, only_after_setup: bool = False, defer_refresh: bool = False) -> dict:
         """Execute the program; returns id -> GpuCiphertext for live values.
-        With only_after_setup, ops before program.n_setup must already be in env."""
+        With only_after_setup, ops before program.n_setup must already be in env.
+        defer_refresh: debug refreshes (a host round trip each) are not run but
+        listed in self.deferred, to be finished by finish_deferred(env); used by
+        graphs.GraphedStep to capture everything else in one CUDA graph."""
         be = self.be
         ops = self.prog.ops
         env = {} if env is None else {k: getattr(v, "payload", v) for k, v in env.items()}
@@ -101,11 +104,21 @@ class WaveExecutor:
             return v
 
         self._pre_encode(pvals, self.n_setup if only_after_setup else 0)
+        self.deferred = []
+        self._pvals = pvals
+        deferring = defer_refresh and not be.real_bootstrap
         for wave in self.waves:
             if only_after_setup:
                 wave = [i for i in wave if i >= self.n_setup]
                 if not wave:
                     continue
+            if deferring:
+                bs = [i for i in wave if ops[i][0] == "bs"]
+                self.deferred.extend(bs)
+                wave = [i for i in wave if ops[i][0] != "bs"]
+                for i in wave:  # nothing may consume a deferred refresh
+                    if any(ops[j][1] in _inputs(ops[i]) for j in self.deferred):
+                        raise ValueError("an op reads a deferred refresh output")
             groups = collections.defaultdict(list)
             for i in wave:
                 op = ops[i]
@@ -133,6 +146,18 @@ class WaveExecutor:
         import itertools
 
         be._serials = itertools.count(self.serials_used)
+        return env
+
+    def finish_deferred(self, env: dict) -> dict:
+        """Run the refreshes run(defer_refresh=True) skipped, in program order."""
+        ops = self.prog.ops
+        keep = set(self.prog.outputs)
+        last = self.prog._last_use
+        for i in sorted(self.deferred):
+            self._run_group(("bs", i), [i], env, self._pvals)
+            for ref in _inputs(ops[i]):
+                if last.get(ref) == i and ref not in keep:
+                    env.pop(ref, None)
         return env
 
     def _pre_encode(self, pvals, start: int, runs=None) -> None:

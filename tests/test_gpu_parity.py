@@ -455,6 +455,27 @@ def test_wave_executor_bit_identical_to_sequential(c1_program):
         assert np.array_equal(a, b)
 
 
+def test_graphed_step_bit_identical_to_eager(c1_program):
+    """graphs.GraphedStep: the config-1 step captured as one CUDA graph (the
+    refreshes eager afterwards) reproduces the eager executor bit for bit, on
+    every replay."""
+    from paper_2506_19693_b200.executor import WaveExecutor
+    from paper_2506_19693_b200.graphs import GraphedStep
+
+    prog, z = c1_program
+    cust = _c1_custodian(z)
+    env = prog.run(cust, 0, prog.n_setup)
+    ex = WaveExecutor(prog, cust)
+    want_env = ex.run(dict(env), only_after_setup=True)
+    want = [cust.backend.planes_of(want_env[o]) for o in prog.outputs]
+    gs = GraphedStep(ex, env)
+    for _ in range(2):
+        got_env = gs.step()
+        got = [cust.backend.planes_of(got_env[o]) for o in prog.outputs]
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+
 # ---------------------------------------------------------------------------
 # Config 3: homomorphic bootstrapping (no reference counterpart: parity
 # unpinned; the check is decrypt(bootstrap(ct)) against the input values)
