@@ -351,7 +351,23 @@ def run_c3_bootstrap():
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     err = float(np.max(np.abs(be._decrypt_values(out) - v)))
-    return {"ms": 1e3 * float(np.median(times[1:])), "first_call_ms": 1e3 * times[0],
+    # the same bootstrap as one CUDA graph replay (graphs.GraphedCall): the
+    # input ciphertext is copied into the graph's static input every call
+    from paper_2506_19693_b200.backend import GpuCiphertext
+    from paper_2506_19693_b200.graphs import GraphedCall
+
+    gc = GraphedCall(lambda d: be.bootstrap_ct(GpuCiphertext(d, 0)).data, ct.data)
+    gtimes = []
+    for rep in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gc.load(ct.data)
+        gout = gc()
+        torch.cuda.synchronize()
+        gtimes.append(time.perf_counter() - t0)
+    graph_equal = bool(torch.equal(gout.view(torch.int64), out.data.view(torch.int64)))
+    return {"ms": 1e3 * float(np.median(gtimes)), "ms_eager": 1e3 * float(np.median(times[1:])),
+            "graph_output_equal_eager": graph_equal, "first_call_ms": 1e3 * times[0],
             "max_abs_err": err, "precision_bits": -math.log2(err), "level_out": out.level,
             "keys": len(be.rotation_keys) + 1, "keygen_s": keygen_s,
             "params": "N=2^16, 2^15 slots, Q = 60 + 8x45 (user) + 16x60 (bootstrap) bits, "

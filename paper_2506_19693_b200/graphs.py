@@ -51,3 +51,32 @@ class GraphedStep:
         env = dict(self.out_env)
         self.ex.deferred = list(self.deferred)
         return self.ex.finish_deferred(env)
+
+
+class GraphedCall:
+    """fn(*static_inputs) captured once and replayed: for fixed-shape device
+    pipelines such as one bootstrapping (bootstrap.Bootstrapper via
+    backend.bootstrap_ct).  Inputs are copied into static tensors with load()."""
+
+    def __init__(self, fn, *inputs, warmup: int = 2):
+        self.static_in = [x.clone() for x in inputs]
+        for _ in range(warmup):
+            fn(*self.static_in)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        self.keepalive: list = []
+        B.H2D_KEEPALIVE = self.keepalive
+        try:
+            with torch.cuda.graph(self.graph):
+                self.out = fn(*self.static_in)
+        finally:
+            B.H2D_KEEPALIVE = None
+        torch.cuda.synchronize()
+
+    def load(self, *inputs) -> None:
+        for dst, src in zip(self.static_in, inputs):
+            dst.copy_(src)
+
+    def __call__(self):
+        self.graph.replay()
+        return self.out
