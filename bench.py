@@ -609,11 +609,12 @@ def main():
         torch.cuda.synchronize()
         s0, s1 = ev(), ev()
         s0.record()
-        for _ in range(max(1, args.steps // 2)):
+        e2e_reps = max(4, args.steps)
+        for _ in range(e2e_reps):
             e2e_step()
         s1.record()
         torch.cuda.synchronize()
-        e2e_ms = hdist.max_over_ranks(s0.elapsed_time(s1)) / max(1, args.steps // 2)
+        e2e_ms = hdist.max_over_ranks(s0.elapsed_time(s1)) / e2e_reps
         line["e2e"] = {"value": world * (hm_b + hr_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                        "ms_per_step": e2e_ms, "pipelined_chunks": -(-bsz // chunk),
                        "h2d_bytes_per_step": hA.numel() * 8 + hB.numel() * 8,
