@@ -23,7 +23,6 @@ from __future__ import annotations
 import math
 
 import numpy as np
-import torch
 
 from . import bootstrap_consts as BC
 from .backend import GpuCiphertext

@@ -37,8 +37,6 @@ from . import dist as hdist
 from .backend import GpuCiphertext
 from .executor import WaveExecutor, _inputs
 
-REPLICATED = -1
-
 
 def _out(op):
     return op[2] if op[0] == "ew" else op[1]

@@ -1,5 +1,5 @@
 """Where does the config-1 step go: GPU kernel time (CUDA events per wrapper) vs wall."""
-import os, sys, time, json
+import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_19693_b200 import he_api, ring

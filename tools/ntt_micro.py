@@ -1,6 +1,6 @@
 """NTT micro-benchmark: forward+inverse over `rows` limbs of N=2^logn (CUDA events)."""
 import os, sys, json
-import numpy as np, torch
+import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import ckks_oracle as O
 from paper_2506_19693_b200 import _native as nat
