@@ -149,12 +149,34 @@ class WaveExecutor:
         return env
 
     def finish_deferred(self, env: dict) -> dict:
-        """Run the refreshes run(defer_refresh=True) skipped, in program order."""
+        """Run the debug refreshes run(defer_refresh=True) skipped — together:
+        one batched decrypt per level (one device->host copy), the eps noise
+        drawn in program order, one batched re-encryption with each refresh's
+        own serial — so the results equal refreshing one at a time."""
+        be = self.be
         ops = self.prog.ops
         keep = set(self.prog.outputs)
         last = self.prog._last_use
-        for i in sorted(self.deferred):
-            self._run_group(("bs", i), [i], env, self._pvals)
+        order = sorted(self.deferred)
+        if not order:
+            return env
+        values = {}
+        by_level: dict = {}
+        for i in order:
+            by_level.setdefault(env[ops[i][2]].level, []).append(i)
+        for lvl, idx in by_level.items():
+            dec = be._decrypt_values_batch(torch.stack([env[ops[i][2]].data for i in idx]), lvl)
+            for j, i in enumerate(idx):
+                values[i] = dec[j]
+        for i in order:  # backend.py:195-206: + U(-eps, eps), in program order
+            if be.bootstrap_eps > 0.0:
+                values[i] = values[i] + be._bs_rng.uniform(-be.bootstrap_eps, be.bootstrap_eps,
+                                                           values[i].shape[0])
+        rl = be.params.refresh_level
+        data = be._encrypt_batch([values[i] for i in order], rl,
+                                 [self.serial_of[i] for i in order])
+        for j, i in enumerate(order):
+            env[ops[i][1]] = GpuCiphertext(data[j], rl)
             for ref in _inputs(ops[i]):
                 if last.get(ref) == i and ref not in keep:
                     env.pop(ref, None)
