@@ -581,6 +581,8 @@ class B200CkksCore:
         primes = ch.limbs_at(level)
         m = len(primes)
         bsz = len(values_list)
+        if bsz > 1:  # one batched encode for the whole batch (then cache hits)
+            self.encode_many([(v, level, False) for v in values_list])
         msgs = []
         if self.sampler == "philox":
             srs = [next(self._serials) if sr is None else sr for sr in serials]
