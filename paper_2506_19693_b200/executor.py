@@ -27,10 +27,14 @@ from .backend import GpuCiphertext
 
 
 class WaveExecutor:
-    def __init__(self, program, custodian):
+    def __init__(self, program, custodian, max_group: int = None):
+        """max_group: split a wave's same-signature group into sub-batches of at
+        most this many ops (bounds the temporaries of very wide steps; results
+        are unchanged — every op is computed independently)."""
         self.prog = program
         self.cust = custodian
         self.be = custodian.backend
+        self.max_group = max_group
         self._plan()
 
     # -- planning ------------------------------------------------------------
@@ -137,7 +141,9 @@ class WaveExecutor:
                 else:
                     groups[("bs", i)].append(i)
             for key, idx in groups.items():
-                self._run_group(key, idx, env, pvals)
+                step = self.max_group or len(idx)
+                for lo in range(0, len(idx), step):
+                    self._run_group(key, idx[lo:lo + step], env, pvals)
             for i in wave:
                 for ref in _inputs(ops[i]):
                     if last.get(ref) == i and ref not in keep:

@@ -370,6 +370,108 @@ def make_c4_trace():
     print("c4 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape)
 
 
+def make_c5_trace():
+    """Config 5 (deep tabular): 64 N(0,1) features, binary labels from a seeded
+    random two-layer teacher, 64->64->64->64->64->2 local-error-signal MLP,
+    batch 256, N=2^16, L = tau(4) + 16 = 32 with bootstrap_depth 16 (above the
+    128-bit bound: insecure-test), Xavier init; one
+    train_iteration recorded on the sim backend like config 4."""
+    from ciphermlp.api import CipherVector, keygen
+    from ciphermlp.depth import tau_total
+    from ciphermlp.nn import (Hyperparams, build_model, classifier_format, layer_format,
+                              prepare_sample, train_iteration)
+    from ciphermlp.packing import Architecture, compute_dims, encrypt_packed, pack, required_rotations
+    from ciphermlp.params import make_params
+    import ciphermlp.simbackend as sb
+
+    hidden = (64, 64, 64, 64)
+    arch = Architecture(64, hidden, 2)
+    n = 2**16
+    params = make_params(level=tau_total(len(hidden)) + 16, scale_bits=45, poly_degree=n,
+                         bootstrap_depth=16)  # security_claim defaults to insecure-test
+    shape = compute_dims(arch, n // 2)
+    rng = np.random.default_rng(20250705)
+    bsz = 256
+    x = rng.normal(0, 1, size=(bsz, 64))
+    t1 = rng.normal(0, 1, size=(64, 16))
+    t2 = rng.normal(0, 1, size=(16, 2))
+    y = np.argmax(np.tanh(x @ t1) @ t2, axis=1)
+    onehot = np.eye(2)[y]
+
+    ops, pts, ids = [], {}, {}
+
+    def pt_id(pv):
+        key = pv.values.tobytes()
+        if key not in pts:
+            pts[key] = len(pts)
+        return pts[key]
+
+    class Recording(sb.SimBackend):
+        def encrypt(self, pv):
+            cv = super().encrypt(pv)
+            ids[cv.serial] = len(ids)
+            ops.append(["enc", ids[cv.serial], pt_id(pv)])
+            return cv
+
+        def elementwise(self, kind, a, b):
+            cv = super().elementwise(kind, a, b)
+            arg = ids[b.serial] if isinstance(b, CipherVector) else pt_id(b)
+            ids[cv.serial] = len(ids)
+            ops.append(["ew", kind, ids[cv.serial], ids[a.serial], arg])
+            return cv
+
+        def rotate(self, a, k, allowed):
+            cv = super().rotate(a, k, allowed)
+            ids[cv.serial] = len(ids)
+            ops.append(["rot", ids[cv.serial], ids[a.serial], int(k)])
+            return cv
+
+        def bootstrap(self, cv):
+            out = super().bootstrap(cv)
+            ids[out.serial] = len(ids)
+            ops.append(["bs", ids[out.serial], ids[cv.serial]])
+            return out
+
+    orig = sb.SimBackend
+    sb.SimBackend = Recording
+    try:
+        cust = keygen(params, required_rotations(shape), backend="sim")
+        hyper = Hyperparams(learning_rate=0.05, momentum=0.9, iterations=1, batch_size=bsz)
+        model = build_model(arch, params, hyper, cust)
+        dims = (64,) + hidden
+        for k, blk in enumerate(model.blocks):
+            fan_in, fan_out = dims[k], hidden[k]
+            w = rng.uniform(-1, 1, size=(fan_in, fan_out)) * np.sqrt(6.0 / (fan_in + fan_out))
+            c = rng.uniform(-1, 1, size=(fan_out, 2)) * np.sqrt(6.0 / (fan_out + 2))
+            blk.layer_weights = encrypt_packed(cust, pack(w, layer_format(blk.kind), shape))
+            blk.classifier_weights = encrypt_packed(cust, pack(c, classifier_format(blk.kind),
+                                                               shape))
+        n_setup = len(ops)
+        batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(bsz)]
+        train_iteration(model, batch, cust, 1)
+    finally:
+        sb.SimBackend = orig
+    outs, sim_w = [], []
+    for b in model.blocks:
+        for pm in (b.layer_weights, b.classifier_weights, b.layer_velocity,
+                   b.classifier_velocity):
+            outs.append(ids[pm.payload.serial])
+            sim_w.append(cust.decrypt(pm.payload).values)
+    pt_arr = np.zeros((len(pts), shape.slots))
+    for k, i in pts.items():
+        pt_arr[i] = np.frombuffer(k, dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "c5_trace.npz"), ops=np.array(json.dumps(ops)),
+                        n_setup=np.array([n_setup]), plaintexts=pt_arr, outputs=np.array(outs),
+                        rotations=np.array(sorted(required_rotations(shape))),
+                        params=np.array([n, params.level, 45, 16]), sim_weights=np.stack(sim_w),
+                        grid=np.array([shape.r, shape.c]))
+    kinds = {}
+    for op in ops:
+        key = op[1] if op[0] == "ew" else op[0]
+        kinds[key] = kinds.get(key, 0) + 1
+    print("c5 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-ckks", action="store_true")
@@ -383,6 +485,8 @@ def main():
         make_c1_trace(a.c1_ckks)
     if a.only == "c4":
         make_c4_trace()
+    if a.only == "c5":
+        make_c5_trace()
 
 
 if __name__ == "__main__":

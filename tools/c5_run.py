@@ -1,0 +1,59 @@
+"""Config 5 (deep tabular): 64->64->64->64->64->2, batch 256,
+N=2^16, L = 16 user + 16 bootstrap levels (insecure-test), 16 real bootstraps
+per step: the reference train_iteration's HE calls (tests/golden/c5_trace.npz),
+wave-batched in sub-batches of `max_group` ciphertexts."""
+import os, sys, time, json
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_19693_b200 import he_api
+from paper_2506_19693_b200.replay import Program
+from paper_2506_19693_b200.executor import WaveExecutor
+from paper_2506_19693_b200.scheme import SchemeParams
+
+
+def run(reps=1, max_group=64, verbose=True):
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                        "golden", "c5_trace.npz")
+    z = np.load(path); prog = Program.load(path)
+    n, L, sb, bd = (int(v) for v in z["params"])
+    user = L - bd
+    # P = 13 x 60 bits: 120 bits above the widest digit (11 x 60-bit bootstrap primes)
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * user + (60,) * bd + (780,),
+                          scale_bits=45, level=L, bootstrap_depth=bd)
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=5,
+                         prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True)
+    torch.cuda.synchronize(); keygen_s = time.perf_counter() - t0
+    env = prog.run(cust, 0, prog.n_setup)
+    ex = WaveExecutor(prog, cust, max_group=max_group)
+    times = []
+    out = None
+    for rep in range(reps):
+        torch.cuda.reset_peak_memory_stats()
+        cust.backend._enc_cache.clear()  # every step re-encodes its plaintexts
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        out = ex.run(dict(env), only_after_setup=True)
+        torch.cuda.synchronize(); times.append(time.perf_counter() - t0)
+        if verbose:
+            print(f"step {rep}: {times[-1]*1e3:.1f} ms, peak mem "
+                  f"{torch.cuda.max_memory_allocated()/2**30:.1f} GiB", flush=True)
+    w = np.stack([cust.backend._decrypt_values(out[o]) for o in prog.outputs])
+    ref = z["sim_weights"]
+    err = np.max(np.abs(w - ref), axis=1)
+    mag = np.max(np.abs(ref), axis=1)
+    kind = np.arange(len(prog.outputs)) % 4  # per block: layer w, classifier w, velocities
+    return {"ms_per_step": 1e3 * min(times), "first_step_ms": 1e3 * times[0],
+            "ops": len(prog.ops) - prog.n_setup, "waves": len(ex.waves),
+            "bootstraps_per_step": int(sum(1 for o in prog.ops if o[0] == "bs")),
+            "keygen_s": keygen_s, "max_group": max_group,
+            "weights_max_abs_err_vs_sim": float(err[kind < 2].max()),
+            "velocities_max_abs_err_vs_sim": float(err[kind >= 2].max()),
+            "velocities_max_abs": float(mag[kind >= 2].max()),
+            "peak_mem_gib": torch.cuda.max_memory_allocated() / 2**30,
+            "workload": "64->64->64->64->64->2, batch 256, N=2^16, L=32 (16 user + 16 bootstrap "
+                        "levels, insecure-test), P = 13 x 60 bits, real bootstrapping"}
+
+
+if __name__ == "__main__":
+    print(json.dumps(run(reps=int(sys.argv[1]) if len(sys.argv) > 1 else 1,
+                         max_group=int(sys.argv[2]) if len(sys.argv) > 2 else 64)))
