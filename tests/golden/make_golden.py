@@ -370,7 +370,7 @@ def make_c4_trace():
     print("c4 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape)
 
 
-def make_c5_trace():
+def make_c5_trace(init_scale: float = 0.25, lr: float = 0.005, out: str = "c5_trace.npz"):
     """Config 5 (deep tabular): 64 N(0,1) features, binary labels from a seeded
     random two-layer teacher, 64->64->64->64->64->2 local-error-signal MLP,
     batch 256, N=2^16, L = tau(4) + 16 = 32 with bootstrap_depth 16 (above the
@@ -436,13 +436,14 @@ def make_c5_trace():
     sb.SimBackend = Recording
     try:
         cust = keygen(params, required_rotations(shape), backend="sim")
-        hyper = Hyperparams(learning_rate=0.05, momentum=0.9, iterations=1, batch_size=bsz)
+        hyper = Hyperparams(learning_rate=lr, momentum=0.9, iterations=1, batch_size=bsz)
         model = build_model(arch, params, hyper, cust)
         dims = (64,) + hidden
         for k, blk in enumerate(model.blocks):
             fan_in, fan_out = dims[k], hidden[k]
             w = rng.uniform(-1, 1, size=(fan_in, fan_out)) * np.sqrt(6.0 / (fan_in + fan_out))
             c = rng.uniform(-1, 1, size=(fan_out, 2)) * np.sqrt(6.0 / (fan_out + 2))
+            w, c = w * init_scale, c * init_scale  # keeps the depth-4 z^2+z stack bounded
             blk.layer_weights = encrypt_packed(cust, pack(w, layer_format(blk.kind), shape))
             blk.classifier_weights = encrypt_packed(cust, pack(c, classifier_format(blk.kind),
                                                                shape))
@@ -460,7 +461,7 @@ def make_c5_trace():
     pt_arr = np.zeros((len(pts), shape.slots))
     for k, i in pts.items():
         pt_arr[i] = np.frombuffer(k, dtype=np.float64)
-    np.savez_compressed(os.path.join(HERE, "c5_trace.npz"), ops=np.array(json.dumps(ops)),
+    np.savez_compressed(os.path.join(HERE, out), ops=np.array(json.dumps(ops)),
                         n_setup=np.array([n_setup]), plaintexts=pt_arr, outputs=np.array(outs),
                         rotations=np.array(sorted(required_rotations(shape))),
                         params=np.array([n, params.level, 45, 16]), sim_weights=np.stack(sim_w),
@@ -469,7 +470,9 @@ def make_c5_trace():
     for op in ops:
         key = op[1] if op[0] == "ew" else op[0]
         kinds[key] = kinds.get(key, 0) + 1
-    print("c5 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape)
+    print("c5 trace ops:", kinds, "plaintexts:", len(pts), "grid", shape,
+          "max |weights, velocities| per block:",
+          [round(float(np.abs(v).max()), 3) for v in sim_w])
 
 
 def main():
