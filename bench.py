@@ -426,6 +426,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -648,6 +649,16 @@ def main():
             line["c4_train"] = c4_run.run(reps=2, verbose=False)
         except Exception as exc:
             line["c4_train"] = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_c5:
+        try:
+            torch.cuda.empty_cache()
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import c5_run
+
+            line["c5_train"] = c5_run.run(reps=1, max_group=64, verbose=False)
+        except Exception as exc:
+            line["c5_train"] = {"error": repr(exc)}
         torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import parallel_ref as PR
