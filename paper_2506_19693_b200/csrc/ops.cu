@@ -1120,9 +1120,10 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   const size_t total = (size_t)polys << R.log_n;
   if (!total) return 0;
   // register arrays are sized by D1: exact widths for the special-prime
-  // counts of the configs (6: config 2, 11: bootstrap layout)
+  // counts of the configs (6: config 2, 11: configs 3/4, 13: config 5)
   const int d1 = n_drop1 == 0 ? 0 : n_drop1 <= 1 ? 1 : n_drop1 <= 2 ? 2 : n_drop1 <= 4 ? 4
-               : n_drop1 <= 6 ? 6 : n_drop1 <= 8 ? 8 : n_drop1 <= 11 ? 11 : 16;
+               : n_drop1 <= 6 ? 6 : n_drop1 <= 8 ? 8 : n_drop1 <= 11 ? 11 : n_drop1 <= 13 ? 13
+               : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
   const int grid = grid_for(total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1146,6 +1147,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   CKB_DC(6, 0) CKB_DC(6, 1) CKB_DC(6, 2)
   CKB_DC(8, 0) CKB_DC(8, 1) CKB_DC(8, 2) CKB_DC(8, 8)
   CKB_DC(11, 0) CKB_DC(11, 1) CKB_DC(11, 2)
+  CKB_DC(13, 0) CKB_DC(13, 1) CKB_DC(13, 2)
   CKB_DC(16, 0) CKB_DC(16, 1) CKB_DC(16, 2)
 #undef CKB_DC
   return CKB_E_ARG;

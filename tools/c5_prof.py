@@ -1,0 +1,26 @@
+"""Config-5 step: CUDA-event kernel time per wrapper vs wall time."""
+import os, sys, time, json
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_19693_b200 import he_api, ring
+from paper_2506_19693_b200.replay import Program
+from paper_2506_19693_b200.executor import WaveExecutor
+from paper_2506_19693_b200.scheme import SchemeParams
+z = np.load("tests/golden/c5_trace.npz"); prog = Program.load("tests/golden/c5_trace.npz")
+n, L, sb, bd = (int(v) for v in z["params"])
+params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * (L - bd) + (60,) * bd + (780,),
+                      scale_bits=45, level=L, bootstrap_depth=bd)
+cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=5,
+                     prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True)
+env = prog.run(cust, 0, prog.n_setup)
+ex = WaveExecutor(prog, cust, max_group=64)
+ex.run(dict(env), only_after_setup=True)
+ring.TIMER = ring.KernelTimer()
+cust.backend._enc_cache.clear()
+torch.cuda.synchronize(); t0 = time.perf_counter()
+ex.run(dict(env), only_after_setup=True)
+torch.cuda.synchronize(); wall = 1e3 * (time.perf_counter() - t0)
+summ = ring.TIMER.summary(); ring.TIMER = None
+print(json.dumps({"wall_ms": wall, "kernel_ms": sum(d["ms"] for d in summ.values()),
+                  "launches": sum(d["launches"] for d in summ.values()),
+                  "kernels": {k: round(d["ms"], 1) for k, d in sorted(summ.items(), key=lambda x: -x[1]["ms"])}}))
