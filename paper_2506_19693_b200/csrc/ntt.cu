@@ -1,8 +1,10 @@
 // Negacyclic NTT kernels (sm_100a): replaces NttPlan.forward/inverse
 // (/root/reference/pkg/src/ciphermlp/ckks/ntt.py:121-154).
 #include "common.cuh"
+#include "fp64.cuh"
 
 using namespace ckb_internal;
+using namespace ckb_f64;
 
 // Two register-round shapes (measured on B200, tools/ntt_micro.py):
 //  * single phase (N <= 4096): radix-16 rounds, one 4096-element limb per CTA,
@@ -222,35 +224,6 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
 // round (<= 3 stages: |v| <= 12p).  All arithmetic is exact integer
 // arithmetic, so results equal the integer path's bit for bit.
 // ---------------------------------------------------------------------------
-constexpr double kRint = 6755399441055744.0;  // 1.5 * 2^52
-
-__device__ __forceinline__ double u64_to_f64(uint64_t v) {  // exact for v < 2^52
-  return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - 4503599627370496.0;
-}
-
-__device__ __forceinline__ uint64_t f64_to_u64(double d) {  // exact for 0 <= d < 2^52
-  return (uint64_t)__double_as_longlong(d + 4503599627370496.0) - 0x4330000000000000ull;
-}
-
-__device__ __forceinline__ double mulmod_f64(double Y, double W, double Wp, double p) {
-  const double q = (Y * Wp + kRint) - kRint;
-  const double h = Y * W;
-  const double l = fma(Y, W, -h);
-  return fma(-q, p, h) + l;
-}
-
-// v mod p into [-p/2, p/2] (exact)
-__device__ __forceinline__ double center_f64(double v, double p, double pinv) {
-  const double q = (v * pinv + kRint) - kRint;
-  return fma(-q, p, v);
-}
-
-// v mod p into [0, p)
-__device__ __forceinline__ double canon_f64(double v, double p, double pinv) {
-  const double r = center_f64(v, p, pinv);
-  return r < 0.0 ? r + p : r;
-}
-
 __device__ __forceinline__ void ct_bfly_f64(double& X, double& Y, double W, double Wp, double p) {
   const double t = mulmod_f64(Y, W, Wp, p);
   const double a = X;

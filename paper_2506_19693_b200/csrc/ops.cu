@@ -1,6 +1,7 @@
 // Limb arithmetic, key switching, rescale, automorphism and conversion kernels
 // (sm_100a) replacing ciphermlp/ckks/{ring,keys,backend}.py numpy routines.
 #include "common.cuh"
+#include "fp64.cuh"
 #include <cstring>
 
 using namespace ckb_internal;
@@ -190,6 +191,112 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
         }
         *reinterpret_cast<ulonglong2*>(dst + (size_t)digit_row(e, first, cnt, skip_own) * N) = o;
       }
+    }
+  }
+}
+
+// ModUp on both arithmetic pipes.  For a digit whose input primes are all
+// < 2^46 (y_i exact in a double) the outputs on primes < 2^46 are summed on the
+// FP64 pipe, sum_i mulmod_f64(y_i, c_ie) (|sum| < 1.5 * AMAX * p < 2^51, exact),
+// and the other outputs (60-bit special primes) on the integer pipe as in
+// k_modup; warps at different outputs keep both pipes busy.  One coefficient
+// per thread (register budget).  Smem: ModSm per ext limb, the integer table in
+// pack30 form, then per (i, e) {double(c), double(c)/p_e} and per e 1/p_e.
+template <int AMAX>
+__global__ void __launch_bounds__(256) k_modup_mixed(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_bstride, int batch,
+    int limbs, int ext, int alpha, int n_digits, int out_rows, int skip_own, int log_n,
+    RingDev R, LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
+  extern __shared__ uint64_t sm[];
+  ModSm* mods = reinterpret_cast<ModSm*>(sm);
+  uint64_t* ctab = sm + 6 * ext;
+  const size_t stride_i = 2 + 2 * (size_t)ext;
+  double2* cd = reinterpret_cast<double2*>(ctab + (size_t)alpha * stride_i);
+  double* pinv = reinterpret_cast<double*>(cd + (size_t)alpha * ext);
+  __shared__ int f64in;
+  const size_t N = (size_t)1 << log_n;
+  const int j = blockIdx.y;
+  const int first = j * alpha;
+  const int cnt = min(alpha, limbs - first);
+  for (int e = threadIdx.x; e < ext; e += blockDim.x) {
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    const uint64_t pe = __ldg(mm);
+    mods[e] = ModSm{pe, __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3), __ldg(mm + 8),
+                    __ldg(mm + 9)};
+    pinv[e] = 1.0 / (double)pe;
+  }
+  const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
+  for (int q = threadIdx.x; q < cnt * (int)stride_i; q += blockDim.x) {
+    const int c = q % (int)stride_i;
+    const uint64_t v = __ldg(tab + q);
+    ctab[q] = (c >= 2 && !(c & 1)) ? ckb::pack30(v) : v;
+  }
+  for (int q = threadIdx.x; q < cnt * ext; q += blockDim.x) {
+    const int i = q / ext, e = q % ext;
+    const uint64_t c = __ldg(tab + (size_t)i * stride_i + 2 + 2 * e);
+    const double pe = (double)__ldg(R.mods + (size_t)em.p[e] * kModStride);
+    cd[q] = make_double2((double)c, (double)c / pe);
+  }
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    for (int i = 0; i < cnt; ++i)
+      ok &= (__ldg(R.mods + (size_t)lm.p[first + i] * kModStride) >> 46) == 0;
+    f64in = ok;
+  }
+  __syncthreads();
+  const bool fin = f64in;
+  const size_t total = (size_t)batch * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t bi = t >> log_n;
+    const uint64_t* src = in + bi * in_bstride + n;
+    uint64_t* dst = out + (bi * n_digits + j) * (size_t)out_rows * N + n;
+    uint64_t y[AMAX];
+    double yd[AMAX];
+#pragma unroll
+    for (int i = 0; i < AMAX; ++i) {
+      if (i < cnt) {
+        const uint64_t q = __ldg(R.mods + (size_t)lm.p[first + i] * kModStride);
+        y[i] = ckb::mul_shoup(src[(size_t)(first + i) * N], ctab[i * stride_i],
+                              ctab[i * stride_i + 1], q);
+      } else {
+        y[i] = 0;
+      }
+      yd[i] = ckb_f64::u64_to_f64(y[i]);  // only used when fin (then y < 2^46)
+    }
+    for (int e = 0; e < ext; ++e) {
+      if (e >= first && e < first + cnt) {
+        if (!skip_own) dst[(size_t)e * N] = src[(size_t)e * N];
+        continue;
+      }
+      const ModSm ms = mods[e];
+      uint64_t o;
+      if (fin && (ms.p >> 46) == 0) {  // warp-uniform: FP64 pipe
+        const double pd = (double)ms.p;
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < AMAX; ++i)
+          if (i < cnt) {
+            const double2 c = cd[i * ext + e];
+            acc += ckb_f64::mulmod_f64(yd[i], c.x, c.y, pd);
+          }
+        o = ckb_f64::f64_to_u64(ckb_f64::canon_f64(acc, pd, pinv[e]));
+      } else {  // integer pipe (Acc4 carry-free sums, one reduction)
+        uint64_t h = 0, l = 0;
+#pragma unroll
+        for (int i0 = 0; i0 < AMAX; i0 += 8) {
+          ckb::Acc4 a;
+#pragma unroll
+          for (int i = i0; i < (i0 + 8 < AMAX ? i0 + 8 : AMAX); ++i)
+            if (i < cnt) a.mac(ckb::split30(y[i]), ckb::unpack30(ctab[i * stride_i + 2 + 2 * e]));
+          a.fold_into(h, l);
+        }
+        const Mod m{ms.p, ms.mu, ms.k, ms.two_p};
+        o = ms.k >= 32 ? ckb::reduce128_big(h, l, ms.r64, ms.r64s, m)
+                       : ckb::reduce128_any(h, l, ms.r64, ms.r64s, m);
+      }
+      dst[(size_t)digit_row(e, first, cnt, skip_own) * N] = o;
     }
   }
 }
@@ -961,6 +1068,34 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
                                   k_modup<16>};
   const int amax = alpha;
   auto kern = kerns[alpha];
+  // both pipes when some digit is all FP64-class primes and some output is too
+  auto is_f64 = [&](int pi) { return (R.f64_mask[pi >> 6] >> (pi & 63)) & 1; };
+  bool digit_f64 = false, out_f64 = false;
+  for (int d = 0; d < nd && !digit_f64; ++d) {
+    bool ok = true;
+    for (int i = d * alpha; i < std::min(limbs, (d + 1) * alpha); ++i) ok &= is_f64(lm.p[i]);
+    digit_f64 = ok;
+  }
+  for (int e = 0; e < ext_limbs; ++e) out_f64 |= is_f64(em.p[e]);
+  if (alpha > 1 && alpha <= 16 && digit_f64 && out_f64) {
+    using KernM = decltype(&k_modup_mixed<2>);
+    static const KernM mkerns[17] = {
+        nullptr, nullptr, k_modup_mixed<2>, k_modup_mixed<3>, k_modup_mixed<4>,
+        k_modup_mixed<5>, k_modup_mixed<6>, k_modup_mixed<7>, k_modup_mixed<8>,
+        k_modup_mixed<9>, k_modup_mixed<10>, k_modup_mixed<11>, k_modup_mixed<12>,
+        k_modup_mixed<13>, k_modup_mixed<14>, k_modup_mixed<15>, k_modup_mixed<16>};
+    const size_t msmem = (6 * (size_t)ext_limbs + (size_t)alpha * (2 + 2 * (size_t)ext_limbs)) * 8 +
+                         (size_t)alpha * ext_limbs * 16 + (size_t)ext_limbs * 8;
+    if (msmem > 48 * 1024)
+      cudaFuncSetAttribute(mkerns[alpha], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+    const size_t work = (size_t)batch << R.log_n;
+    dim3 mgrid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
+               (unsigned)nd);
+    mkerns[alpha]<<<mgrid, 256, msmem, (cudaStream_t)stream>>>(
+        out, in, bstride, batch, limbs, ext_limbs, alpha, nd, out_rows, skip_own, (int)R.log_n,
+        R, lm, em, bconv);
+    return finish();
+  }
   const size_t smem = (6 * (size_t)ext_limbs +
                        (amax == 1 ? 0 : (size_t)alpha * (2 + 2 * (size_t)ext_limbs))) * 8;
   const size_t work = (size_t)batch << (R.log_n - 1);
