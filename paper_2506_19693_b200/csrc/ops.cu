@@ -531,10 +531,31 @@ __device__ __forceinline__ uint64_t add_rm(uint64_t acc, int64_t r, uint64_t M, 
   return sub_rm(acc, -r, M, Ms, p);
 }
 
-// Two coefficients per thread; the E loop's per-limb constants (modulus,
-// r64, and the tabE row) are staged in shared memory once per CTA.
-template <int D1, int D2>
-__global__ void __launch_bounds__(256, 2) k_divround_corr(
+// V coefficients per thread (2: 16-byte accesses; 1 for wide drops, whose
+// remainder arrays would otherwise cap occupancy); the E loop's per-limb
+// constants (modulus, r64, and the tabE row) are staged in shared memory.
+template <int V>
+__device__ __forceinline__ void ld_v(uint64_t* x, const uint64_t* p) {
+  if constexpr (V == 2) {
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+    x[0] = v.x;
+    x[1] = v.y;
+  } else {
+    x[0] = *p;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void st_v(uint64_t* p, const uint64_t* x) {
+  if constexpr (V == 2) {
+    *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(x[0], x[1]);
+  } else {
+    *p = x[0];
+  }
+}
+
+template <int D1, int D2, int V>
+__global__ void __launch_bounds__(256, V == 2 ? 2 : 3) k_divround_corr(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
     int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
     const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE) {
@@ -556,33 +577,33 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
     sm[q] = v;
   }
   __syncthreads();
-  const size_t half = N >> 1;
-  const size_t total = (size_t)polys * half;
+  const size_t per = N / V;
+  const size_t total = (size_t)polys * per;
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = (t & (half - 1)) * 2;
-    const size_t pidx = t / half;
+    const size_t n = (t % per) * V;
+    const size_t pidx = t / per;
     const uint64_t* src = T + pidx * trows * N + n;
-    int64_t r1[D1 > 0 ? D1 : 1][2], r2[D2 > 0 ? D2 : 1][2];
+    int64_t r1[D1 > 0 ? D1 : 1][V], r2[D2 > 0 ? D2 : 1][V];
 #pragma unroll
     for (int d = 0; d < D1; ++d) {
       if (d < n1) {
         const int li = limbs - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
         const uint64_t* Tb = tab1 + (size_t)li * s1;
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(li - m2) * N);
-        uint64_t a0 = x.x, a1 = x.y;
+        uint64_t a[V];
+        ld_v<V>(a, src + (size_t)(li - m2) * N);
 #pragma unroll
         for (int u = 0; u < D1; ++u)
           if (u < d) {
             const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
-            a0 = sub_rm(a0, r1[u][0], M, Ms, p);
-            a1 = sub_rm(a1, r1[u][1], M, Ms, p);
+#pragma unroll
+            for (int c = 0; c < V; ++c) a[c] = sub_rm(a[c], r1[u][c], M, Ms, p);
           }
         const uint64_t W = __ldg(Tb + 2 * n1), Ws = __ldg(Tb + 2 * n1 + 1);
-        r1[d][0] = centered(ckb::mul_shoup(a0, W, Ws, p), p);
-        r1[d][1] = centered(ckb::mul_shoup(a1, W, Ws, p), p);
+#pragma unroll
+        for (int c = 0; c < V; ++c) r1[d][c] = centered(ckb::mul_shoup(a[c], W, Ws, p), p);
       }
     }
 #pragma unroll
@@ -590,73 +611,75 @@ __global__ void __launch_bounds__(256, 2) k_divround_corr(
       if (d < n2) {
         const int li = m1 - 1 - d;
         const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)(li - m2) * N);
-        uint64_t v0 = x.x, v1 = x.y;
+        uint64_t v[V];
+        ld_v<V>(v, src + (size_t)(li - m2) * N);
         if (n1) {
           const uint64_t* Ta = tab1 + (size_t)li * s1;
 #pragma unroll
           for (int u = 0; u < D1; ++u)
             if (u < n1) {
               const uint64_t M = __ldg(Ta + 2 * u), Ms = __ldg(Ta + 2 * u + 1);
-              v0 = sub_rm(v0, r1[u][0], M, Ms, p);
-              v1 = sub_rm(v1, r1[u][1], M, Ms, p);
+#pragma unroll
+              for (int c = 0; c < V; ++c) v[c] = sub_rm(v[c], r1[u][c], M, Ms, p);
             }
           const uint64_t W = __ldg(Ta + 2 * n1), Ws = __ldg(Ta + 2 * n1 + 1);
-          v0 = ckb::mul_shoup(v0, W, Ws, p);
-          v1 = ckb::mul_shoup(v1, W, Ws, p);
+#pragma unroll
+          for (int c = 0; c < V; ++c) v[c] = ckb::mul_shoup(v[c], W, Ws, p);
         }
         if (has_add) {
-          const ulonglong2 a =
-              *reinterpret_cast<const ulonglong2*>(src + (size_t)(n1 + n2 + li - m2) * N);
-          v0 = ckb::add_mod(v0, a.x, p);
-          v1 = ckb::add_mod(v1, a.y, p);
+          uint64_t a[V];
+          ld_v<V>(a, src + (size_t)(n1 + n2 + li - m2) * N);
+#pragma unroll
+          for (int c = 0; c < V; ++c) v[c] = ckb::add_mod(v[c], a[c], p);
         }
         const uint64_t* Tb = tab2 + (size_t)li * s2;
 #pragma unroll
         for (int u = 0; u < D2; ++u)
           if (u < d) {
             const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
-            v0 = sub_rm(v0, r2[u][0], M, Ms, p);
-            v1 = sub_rm(v1, r2[u][1], M, Ms, p);
+#pragma unroll
+            for (int c = 0; c < V; ++c) v[c] = sub_rm(v[c], r2[u][c], M, Ms, p);
           }
         const uint64_t W = __ldg(Tb + 2 * n2), Ws = __ldg(Tb + 2 * n2 + 1);
-        r2[d][0] = centered(ckb::mul_shoup(v0, W, Ws, p), p);
-        r2[d][1] = centered(ckb::mul_shoup(v1, W, Ws, p), p);
+#pragma unroll
+        for (int c = 0; c < V; ++c) r2[d][c] = centered(ckb::mul_shoup(v[c], W, Ws, p), p);
       }
     }
-    // E_j = sum_u r_u c_uj: each signed r is shifted by C_j (a multiple of q_j
-    // near 2^61) so every term is a non-negative word; 128-bit lazy sum and
-    // one reduction per output.
+    // E_j = sum_u r_u c_uj: each signed r is shifted by C_j (a multiple of q_j)
+    // so every term is a non-negative word; 128-bit lazy sum and one
+    // reduction per output.
     uint64_t* dst = E + pidx * m2 * N + n;
     for (int j = 0; j < m2; ++j) {
       const uint64_t* S = sm + (size_t)j * row_w;
       const uint64_t* Te = S + 6;
       const int64_t off = (int64_t)Te[2 * (n1 + n2)];
-      uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+      uint64_t h[V], l[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) h[c] = l[c] = 0;
 #pragma unroll
       for (int u = 0; u < D1; ++u)
         if (u < n1) {
-          const uint64_t c = Te[2 * u];
-          ckb::mac128(h0, l0, (uint64_t)(r1[u][0] + off), c);
-          ckb::mac128(h1, l1, (uint64_t)(r1[u][1] + off), c);
+          const uint64_t cc = Te[2 * u];
+#pragma unroll
+          for (int c = 0; c < V; ++c) ckb::mac128(h[c], l[c], (uint64_t)(r1[u][c] + off), cc);
         }
 #pragma unroll
       for (int u = 0; u < D2; ++u)
         if (u < n2) {
-          const uint64_t c = Te[2 * (n1 + u)];
-          ckb::mac128(h0, l0, (uint64_t)(r2[u][0] + off), c);
-          ckb::mac128(h1, l1, (uint64_t)(r2[u][1] + off), c);
+          const uint64_t cc = Te[2 * (n1 + u)];
+#pragma unroll
+          for (int c = 0; c < V; ++c) ckb::mac128(h[c], l[c], (uint64_t)(r2[u][c] + off), cc);
         }
       const Mod m{S[0], S[1], S[2], S[3]};
-      ulonglong2 o;
+      uint64_t o[V];
       if (m.k >= 32) {  // warp-uniform
-        o.x = ckb::reduce128_big(h0, l0, S[4], S[5], m);
-        o.y = ckb::reduce128_big(h1, l1, S[4], S[5], m);
+#pragma unroll
+        for (int c = 0; c < V; ++c) o[c] = ckb::reduce128_big(h[c], l[c], S[4], S[5], m);
       } else {
-        o.x = ckb::reduce128_any(h0, l0, S[4], S[5], m);
-        o.y = ckb::reduce128_any(h1, l1, S[4], S[5], m);
+#pragma unroll
+        for (int c = 0; c < V; ++c) o[c] = ckb::reduce128_any(h[c], l[c], S[4], S[5], m);
       }
-      *reinterpret_cast<ulonglong2*>(dst + (size_t)j * N) = o;
+      st_v<V>(dst + (size_t)j * N, o);
     }
   }
 }
@@ -1260,20 +1283,28 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
                : n_drop1 <= 6 ? 6 : n_drop1 <= 8 ? 8 : n_drop1 <= 11 ? 11 : n_drop1 <= 13 ? 13
                : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
-  const int grid = grid_for(total / 2, 256);
+  const bool one = n_drop1 >= 11;  // wide drops: one coefficient per thread
+  const int grid = grid_for(one ? total : total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
   const int m2 = limbs - n_drop1 - n_drop2;
   const size_t smem = (size_t)m2 * (6 + 2 * (n_drop1 + n_drop2 + 1)) * 8;
   if (smem > 200 * 1024) return CKB_E_ARG;
+#define CKB_DC_V(A, B, V)                                                                   \
+  {                                                                                         \
+    if (smem > 48 * 1024)                                                                   \
+      cudaFuncSetAttribute(k_divround_corr<A, B, V>,                                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    k_divround_corr<A, B, V><<<grid, 256, smem, st>>>(E, T, has_addend, polys, limbs,       \
+                                                     n_drop1, n_drop2, (int)R.log_n, R, lm, \
+                                                     tab1, tab2, tabE);                     \
+    return finish();                                                                        \
+  }
 #define CKB_DC(A, B)                                                                        \
   if (d1 == A && d2 == B) {                                                                 \
-    if (smem > 48 * 1024)                                                                   \
-      cudaFuncSetAttribute(k_divround_corr<A, B>,                                           \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
-    k_divround_corr<A, B><<<grid, 256, smem, st>>>(E, T, has_addend, polys, limbs, n_drop1,    \
-                                                n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
-                                                tabE);                                      \
-    return finish();                                                                        \
+    if constexpr (A >= 11) {                                                                \
+      if (one) CKB_DC_V(A, B, 1)                                                            \
+    }                                                                                       \
+    CKB_DC_V(A, B, 2)                                                                       \
   }
   CKB_DC(0, 1) CKB_DC(0, 2) CKB_DC(0, 8)
   CKB_DC(1, 0) CKB_DC(1, 1) CKB_DC(1, 2) CKB_DC(1, 8)
@@ -1285,6 +1316,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   CKB_DC(13, 0) CKB_DC(13, 1) CKB_DC(13, 2)
   CKB_DC(16, 0) CKB_DC(16, 1) CKB_DC(16, 2)
 #undef CKB_DC
+#undef CKB_DC_V
   return CKB_E_ARG;
 }
 
