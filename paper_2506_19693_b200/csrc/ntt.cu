@@ -292,6 +292,9 @@ __device__ __forceinline__ void load_round_f64(double* x, const uint64_t* sb,
       const uint64_t v = __ldcs(g + (k << WLO));
       x[k] = u64in ? u64_to_f64(v) : __longlong_as_double((long long)v);
     }
+  } else if (u64in) {  // canonical residues staged raw in shared memory
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = u64_to_f64(sb[koff<WLO>(k)]);
   } else {
 #pragma unroll
     for (int k = 0; k < E; ++k) x[k] = __longlong_as_double((long long)sb[koff<WLO>(k)]);
@@ -320,7 +323,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-    load_round_f64<E, WLO, CM>(x, sb, HI == S ? gsrc : nullptr, gs, rbase, u64in);
+    load_round_f64<E, WLO, CM>(x, sb, HI == S ? gsrc : nullptr, gs, rbase, HI == S && u64in);
 #pragma unroll
     for (int b = HI - 1; b >= LO; --b) {
       const int bb = b - WLO;
@@ -373,7 +376,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
     const int rbase = (w & ((1 << WLO) - 1)) | ((w >> WLO) << (WLO + RB));
     double x[E];
     uint64_t* sb = s + sidx<S>(gq, rbase);
-    load_round_f64<E, WLO, CM>(x, sb, LO == 0 ? gsrc : nullptr, gs, rbase, u64in);
+    load_round_f64<E, WLO, CM>(x, sb, LO == 0 ? gsrc : nullptr, gs, rbase, LO == 0 && u64in);
 #pragma unroll
     for (int b = LO; b < HI; ++b) {
       const int bb = b - WLO;
@@ -534,12 +537,12 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
     const int gs = colmap ? ph.rstride : 1;
     if constexpr (FWD) {
       fwd_rounds_f64<S, RB, S, colmap>(smem, dtab, pd, pinv, gq, tbase, w, ph.last, gsrc, gdst,
-                                       gs, ph.first);
+                                       gs, gsrc != nullptr && ph.first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
       inv_rounds_f64<S, RB, 0, colmap>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw,
                                        fw * pinv, gq, tbase, w, ph.last, gsrc, gdst, gs,
-                                       ph.first);
+                                       gsrc != nullptr && ph.first);
     }
     if constexpr (colmap) return;  // stored straight to global memory
   } else if constexpr (MODE != 1) {
@@ -640,7 +643,8 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
       if (!any_f64) return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
-      const bool cm = ph.rstride != 1 && !ph.first;  // second-pass column phase
+      // second-pass column phase: column-mapped direct I/O (MODE 3)
+      const bool cm = ph.rstride != 1 && !ph.first;
       int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st)
                  : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
       if (!r && any_int) r = launch_phase<FWD, 3, 2>(S, data, ph, nr, R, lm, st);

@@ -274,14 +274,14 @@ __global__ void __launch_bounds__(256) k_modup_mixed(
       uint64_t o;
       if (fin && (ms.p >> 46) == 0) {  // warp-uniform: FP64 pipe
         const double pd = (double)ms.p;
-        double acc = 0.0;
+        double acc[2] = {0.0, 0.0};  // two independent add chains
 #pragma unroll
         for (int i = 0; i < AMAX; ++i)
           if (i < cnt) {
             const double2 c = cd[i * ext + e];
-            acc += ckb_f64::mulmod_f64(yd[i], c.x, c.y, pd);
+            acc[i & 1] += ckb_f64::mulmod_f64(yd[i], c.x, c.y, pd);
           }
-        o = ckb_f64::f64_to_u64(ckb_f64::canon_f64(acc, pd, pinv[e]));
+        o = ckb_f64::f64_to_u64(ckb_f64::canon_f64(acc[0] + acc[1], pd, pinv[e]));
       } else {  // integer pipe (Acc4 carry-free sums, one reduction)
         uint64_t h = 0, l = 0;
 #pragma unroll
