@@ -346,7 +346,7 @@ class B200CkksCore:
                     c = qhat % p
                     tab[j, i, 2 + 2 * e] = c
                     tab[j, i, 3 + 2 * e] = shoup(c, p)
-        t = torch.from_numpy(tab.reshape(-1)).to(self.device)
+        t = self.chain.publish(torch.from_numpy(tab.reshape(-1)).to(self.device))
         self._bconv_cache[m] = t
         return t
 
@@ -732,7 +732,7 @@ class B200CkksCore:
             m = self._limbs(level)
             c = torch.zeros(self.n, dtype=torch.int64, device=self.device)
             c[power % self.n] = -1 if (power // self.n) % 2 else 1
-            hit = ch.ntt_fwd(ch.from_i64(c, m)[0], m)
+            hit = ch.publish(ch.ntt_fwd(ch.from_i64(c, m)[0], m))
             self._adjust_cache[key] = hit
         return hit
 
@@ -814,6 +814,7 @@ class B200CkksCore:
             g_items = torch.tensor(gal, dtype=torch.int64, device=self.device).view(U64)
             ptrs = torch.tensor([k.data.data_ptr() for k in keys], dtype=torch.int64,
                                 device=self.device)
+            self.chain.publish(ptrs)
             cache[key] = (g_items, ptrs, keys)
         return cache[key]
 

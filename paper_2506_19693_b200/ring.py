@@ -150,6 +150,13 @@ class GpuChain:
             vals += [v, shoup(v, p)]
         return nat.u64_array(vals)
 
+    def publish(self, t: torch.Tensor) -> torch.Tensor:
+        """A lazily built, cached device table: wait once for it to be complete
+        so groups issued on other streams (executor fork/join) can read it."""
+        if t is not None and t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        return t
+
     def _drop_chain_table(self, basis: tuple, n_drop: int) -> torch.Tensor:
         """Mixed-radix constants for dropping the last n_drop limbs of basis
         (see ckb_divround): per limb j, {M_u mod p_j} for u < n_drop then
@@ -176,8 +183,9 @@ class GpuChain:
         key = ("drop", basis, n1, n2)
         hit = self._maps.get(key)
         if hit is None:
-            t1 = self._drop_chain_table(basis, n1) if n1 else None
-            t2 = self._drop_chain_table(basis[: len(basis) - n1], n2) if n2 else None
+            t1 = self.publish(self._drop_chain_table(basis, n1) if n1 else None)
+            t2 = self.publish(self._drop_chain_table(basis[: len(basis) - n1], n2)
+                              if n2 else None)
             hit = self._maps[key] = (t1, t2)
         return hit
 
@@ -355,7 +363,7 @@ class GpuChain:
         key = ("corr", basis, n1, n2)
         hit = self._maps.get(key)
         if hit is None:
-            hit = self._maps[key] = self._corr_table(basis, n1, n2)
+            hit = self._maps[key] = self.publish(self._corr_table(basis, n1, n2))
         return hit
 
     def divround_ntt(self, x, polys: int, limbs: int, n1: int, n2: int = 0, *,
