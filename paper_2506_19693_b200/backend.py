@@ -737,7 +737,7 @@ class B200CkksCore:
         return hit
 
     def hoisted_rotations(self, data: torch.Tensor, level: int, galois_list) -> list:
-        """Rotate one ciphertext ([2, m, N], NTT domain) by several Galois
+        """Rotate ciphertexts ([..., 2, m, N], NTT domain) by several Galois
         elements sharing a single ModUp: the digits are lifted and transformed
         once and permuted per rotation in the NTT domain (an automorphism
         commutes with the basis extension up to multiples of Q_j, which the key
@@ -745,19 +745,29 @@ class B200CkksCore:
         ch = self.chain
         m = self._limbs(level)
         ext = m + ch.k
-        c1 = ch.ntt_inv(data[1].clone(), m)
-        digits = ch.modup(c1, m, self.alpha, self._bconv(m), batch=1)
+        lead = data.shape[:-3]
+        d = data.reshape(-1, 2, m, self.n)
+        b = d.shape[0]
+        c1 = ch.ntt_inv(d[:, 1].clone(memory_format=torch.contiguous_format), m)
+        digits = ch.modup(c1, m, self.alpha, self._bconv(m), batch=b)
         ch.ntt_fwd(digits, ext, ch.ext_map(m))
+        c0s = d[:, 0].contiguous()
         out = []
         for g in galois_list:
             key = self.rotation_key(g)
             dg = ch.automorphism_ntt(digits, g)
             acc = ch.ks_inner(dg, m, self.alpha, key=key.data)
-            c0 = ch.automorphism_ntt(data[0], g)
-            r = ch.divround_ntt(acc, 2, ext, ch.k, 0, addend=c0, addend_polys=1,
+            c0 = ch.automorphism_ntt(c0s, g)
+            r = ch.divround_ntt(acc, 2 * b, ext, ch.k, 0, addend=c0, addend_polys=1,
                                 addend_period=2, addend_stride=1, basis=ch.ext_basis(m))
-            out.append(r.view(2, m, self.n))
+            out.append(r.view(*lead, 2, m, self.n))
         return out
+
+    def bootstrap_batch(self, data: torch.Tensor, level: int) -> torch.Tensor:
+        """Bootstrap a batch [B, 2, m, N] of ciphertexts at one level together:
+        every stage runs once over the batch (the refreshed weights of a
+        training step are independent).  Returns [B, 2, m(refresh), N]."""
+        return self.bootstrap_ct(GpuCiphertext(data, level)).data
 
     def bootstrap_ct(self, ct: GpuCiphertext) -> GpuCiphertext:
         """Homomorphic bootstrapping of a payload (any level) to refresh_level."""
@@ -770,8 +780,11 @@ class B200CkksCore:
         return self._bootstrapper.bootstrap(ct)
 
     def rotate_data(self, data: torch.Tensor, level: int, galois: int) -> torch.Tensor:
-        return self._hrot(data.unsqueeze(0), level, galois=galois,
-                          key=self.rotation_key(galois))[0]
+        """[..., 2, m, N] -> the same, every item rotated by one Galois element."""
+        m = self._limbs(level)
+        out = self._hrot(data.reshape(-1, 2, m, self.n), level, galois=galois,
+                         key=self.rotation_key(galois))
+        return out.view(*data.shape[:-3], 2, m, self.n)
 
     def mod_raise(self, ct: GpuCiphertext) -> GpuCiphertext:
         """Bootstrapping step 1: reinterpret a level-0 ciphertext (one limb q0)
@@ -782,15 +795,17 @@ class B200CkksCore:
             raise self._errors.IncompatibleOperands("mod_raise needs a one-limb level-0 ciphertext")
         top = self.params.level
         m = self._limbs(top)
+        lead = ct.data.shape[:-3]
         coeff = ch.ntt_inv(ct.data.clone(), 1)
-        out = torch.empty(2, 1, m, self.n, dtype=U64, device=self.device)
+        polys = coeff.numel() // self.n
+        out = torch.empty(polys, 1, m, self.n, dtype=U64, device=self.device)
         from . import _native as nat
 
         basis = tuple(range(m))
-        nat.check(nat.LIB.ckb_modup(ch.ring_p, nat.ptr(out), nat.ptr(coeff), 0, 2, 1,
+        nat.check(nat.LIB.ckb_modup(ch.ring_p, nat.ptr(out), nat.ptr(coeff), 0, polys, 1,
                                     ch.q_map(1), m, ch.cmap(basis), 1, None, 0,
                                     nat.stream_handle()), "mod_raise")
-        data = out.view(2, m, self.n)
+        data = out.view(*lead, 2, m, self.n)
         return GpuCiphertext(ch.ntt_fwd(data, m), top)
 
     # ------------------------------------------------------------ batched engine

@@ -23,6 +23,7 @@ from __future__ import annotations
 import math
 
 import numpy as np
+import torch
 
 from . import bootstrap_consts as BC
 from .backend import GpuCiphertext
@@ -40,7 +41,8 @@ def bootstrap_rotations(params, levels: int = 3) -> set:
 
 
 class Bootstrapper:
-    """Values inside are (data [2, m, N] NTT domain, level, scale) triples: the
+    """Values inside are (data [B, 2, m, N] NTT domain, level, scale) triples
+    (B ciphertexts bootstrapped together; one ciphertext is B = 1): the
     bootstrapping levels (prime_layout="bootstrap": ~60-bit primes above the
     refresh level) run at scale ~q0 ≈ 2^60 with every plaintext encoded at the
     prime it is about to be divided by, so the noise floor is ~2^-45 of the
@@ -108,8 +110,8 @@ class Bootstrapper:
 
     def _mul(self, a, b):
         a, b = self._align(a, b)
-        out = self.be._hmult(a[0].unsqueeze(0).contiguous(), b[0].unsqueeze(0).contiguous(), a[1])
-        return out[0], a[1] - 1, a[2] * b[2] / self._q(a[1])
+        out = self.be._hmult(a[0].contiguous(), b[0].contiguous(), a[1])
+        return out, a[1] - 1, a[2] * b[2] / self._q(a[1])
 
     def _mul_const(self, a, c: float, out_scale: float = None):
         """c * a, one level; lands exactly on out_scale (default: a's scale)."""
@@ -138,14 +140,20 @@ class Bootstrapper:
         if lvl == level:
             return a
         assert lvl > level
-        return data[:, : self.be._limbs(level)].contiguous(), level, sc
+        return data[..., : self.be._limbs(level), :].contiguous(), level, sc
 
     def _add_const(self, a, c: float):
+        """(c0 + pt, c1) for every item: the plaintext pair [pt, 0] broadcast."""
         data, lvl, sc = a
         m = self.be._limbs(lvl)
-        pt = self._const_pt(c, lvl, sc)
-        out = data.clone()
-        self.be.chain.add(data[0], pt, m, out=out[0])
+        key = ("const2", float(c), lvl, float(sc))
+        pt2 = self._pt_cache.get(key)
+        if pt2 is None:
+            pt = self._const_pt(c, lvl, sc)
+            pt2 = torch.zeros(2, m, self.be.n, dtype=pt.dtype, device=pt.device)
+            pt2[0].copy_(pt)
+            pt2 = self._pt_cache[key] = self.be.chain.publish(pt2)
+        out = self.be.chain.ew(0, torch.empty_like(data), data, pt2, limbs=m, b_rows=2 * m)
         return out, lvl, sc
 
     def _double(self, a):
@@ -250,7 +258,11 @@ class Bootstrapper:
 
     # -- the whole procedure ----------------------------------------------------------
     def bootstrap(self, ct: GpuCiphertext) -> GpuCiphertext:
+        """ct.data [2, m, N] or a batch [B, 2, m, N] (all at ct.level)."""
         be, ch = self.be, self.be.chain
+        single = ct.data.dim() == 3
+        if single:
+            ct = GpuCiphertext(ct.data.unsqueeze(0), ct.level)
         raised = be.mod_raise(ct)
         x = (raised.data, raised.level, float(self.q0))  # read at scale q0: slots = V u'
         for t, plan in enumerate(self.cts_plans):
@@ -278,4 +290,4 @@ class Bootstrapper:
             data, lvl, sc = self._drop_to(z, rl, ch.scale_at[rl])
         if lvl < rl:
             raise RuntimeError(f"bootstrapping consumed too many levels ({lvl} < {rl})")
-        return GpuCiphertext(data, lvl)
+        return GpuCiphertext(data[0] if single else data, lvl)

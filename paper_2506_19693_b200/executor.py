@@ -76,12 +76,27 @@ class WaveExecutor:
             else:
                 raise ValueError(tag)
             d = 1 + max((depth[x] for x in ins), default=0)
-            if tag == "bs":  # refreshes keep program order (bs_rng stream)
+            if tag == "bs" and not be.real_bootstrap:
+                # debug refreshes keep program order (their bs_rng draws); real
+                # bootstraps are deterministic and batch freely
                 d = max(d, self._last_bs_depth + 1)
                 self._last_bs_depth = d
             depth[out] = d
             level[out] = lvl
             waves[d].append(i)
+        # real bootstraps whose outputs nothing in the step reads (the refreshed
+        # weights): deferred to one final wave and run as a single batch (each
+        # input is first brought to level 0, where bootstrapping starts anyway)
+        if be.real_bootstrap:
+            bs = [i for i, op in enumerate(ops) if op[0] == "bs"]
+            consumed = {x for op in ops for x in _inputs(op)}
+            if len(bs) > 1 and not any(ops[i][1] in consumed for i in bs):
+                last_d = max(waves) + 1
+                for d in list(waves):
+                    waves[d] = [i for i in waves[d] if ops[i][0] != "bs"]
+                    if not waves[d]:
+                        del waves[d]
+                waves[last_d] = bs
         self.serial_of = ser
         self.level_of = level
         self.waves = [waves[d] for d in sorted(waves)]
@@ -138,6 +153,8 @@ class WaveExecutor:
                         groups[(kind, la, b)].append(i)
                 elif tag == "rot":
                     groups[("rot", env[op[2]].level, op[3] % slots)].append(i)
+                elif be.real_bootstrap:  # one batched bootstrapping
+                    groups[("bs", "batch")].append(i)
                 else:
                     groups[("bs", i)].append(i)
             for key, idx in groups.items():
@@ -226,11 +243,22 @@ class WaveExecutor:
                 env[ops[i][1]] = GpuCiphertext(data[j], top)
             return
         if tag == "bs":
+            if be.real_bootstrap:  # homomorphic bootstrapping (bootstrap.py), batched
+                ins = [env[ops[i][2]] for i in idx]
+                lvl = min(c.level for c in ins)
+                if lvl > 0 or any(c.level != lvl for c in ins):
+                    lvl = 0  # bootstrapping starts from level 0 anyway
+                    datas = [c.data if c.level == 0 else be._adjust_data(c.data, c.level, 0)
+                             for c in ins]
+                else:
+                    datas = [c.data for c in ins]
+                out = be.bootstrap_batch(self._stack(datas), lvl)
+                rl = be.params.refresh_level
+                for j, i in enumerate(idx):
+                    env[ops[i][1]] = GpuCiphertext(out[j], rl)
+                return
             i = idx[0]
             src = env[ops[i][2]]
-            if be.real_bootstrap:  # homomorphic bootstrapping (bootstrap.py)
-                env[ops[i][1]] = be.bootstrap_ct(src)
-                return
             values = be._decrypt_values(src)
             if be.bootstrap_eps > 0.0:
                 values = values + be._bs_rng.uniform(-be.bootstrap_eps, be.bootstrap_eps,

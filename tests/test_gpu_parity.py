@@ -503,6 +503,31 @@ def test_real_bootstrap_precision_n8192():
     assert np.max(np.abs(cust.decrypt(sq).values - v * v)) <= 2.0**-14
 
 
+def test_batched_bootstrap_equals_single():
+    """backend.bootstrap_batch (all stages once over a batch, used for the
+    refreshes of a training step) gives each ciphertext's single bootstrap
+    bit for bit."""
+    n, L = 1 << 13, 24
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                          scale_bits=45, level=L, bootstrap_depth=16)
+    cust = he_api.keygen(params, {1}, backend="ckks", rng_seed=2, prime_layout="bootstrap",
+                         dnum=3, secret_hw=192, real_bootstrap=True)
+    be = cust.backend
+    rng = np.random.default_rng(1)
+    vals = [rng.uniform(-1, 1, n // 2) for _ in range(3)]
+    cts = [be._encrypt_values(v, 3) for v in vals]
+    single = [be.bootstrap_ct(c).data for c in cts]
+    batch = be.bootstrap_batch(torch.stack([c.data for c in cts]), 3)
+    for j in range(3):
+        assert torch.equal(batch[j].view(torch.int64), single[j].view(torch.int64))
+    from paper_2506_19693_b200.backend import GpuCiphertext
+
+    rl = params.refresh_level
+    err = max(float(np.max(np.abs(be._decrypt_values(GpuCiphertext(batch[j], rl)) - vals[j])))
+              for j in range(3))
+    assert err <= 2.0**-15
+
+
 def test_philox_sampler_distribution_and_batch_determinism():
     """ckb_sample: uniform residues in [0, p), rounded N(0, 3.2^2) errors, one
     stream per seed (batched == one at a time)."""
