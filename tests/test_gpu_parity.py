@@ -281,10 +281,12 @@ def test_rbky_reference_key_file_round_trip(ck_gold):
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("dnum", [None, 2])
-def test_mode_b_ops_bit_exact_vs_oracle(dnum):
-    n, level = 256, 3
-    chain = (60, 40, 40, 40, 120 if dnum else 60)
+@pytest.mark.parametrize("dnum,level,special", [(None, 3, 60), (2, 3, 120), (3, 5, 300)])
+def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
+    """(3, 5, 300): 5 special primes, so ModDown drops 5 + 1 primes and the
+    correction runs on the tensor cores (k_divround_corr_tc)."""
+    n = 256
+    chain = (60,) + (40,) * level + (special,)
     params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=40, level=level)
     cust = he_api.keygen(params, {1, 5}, backend="ckks", rng_seed=7, prime_layout="baseline",
                          dnum=dnum, sampler="numpy")  # the oracle's key stream
