@@ -321,7 +321,7 @@ def run_c1_dp(local: int, world: int) -> dict:
             "timing": "CUDA events around the sharded step, max over ranks"}
 
 
-def run_c3_bootstrap():
+def run_c3_bootstrap(special: int = 660):
     """Config 3: full-slot bootstrapping of one ciphertext at N=2^16 (2^15 slots,
     U[-1,1]), input at level 0, HW-192 secret, CtS/StC 3 BSGS levels each,
     EvalMod = degree-119 Chebyshev + 2 double-angle steps (bootstrap.py)."""
@@ -331,7 +331,7 @@ def run_c3_bootstrap():
     from paper_2506_19693_b200.scheme import SchemeParams
 
     n, L = 1 << 16, 24
-    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (special,),
                           scale_bits=45, level=L, bootstrap_depth=16)
     t0 = time.perf_counter()
     cust = he_api.keygen(params, set(), backend="ckks", rng_seed=11, prime_layout="bootstrap",

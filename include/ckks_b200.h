@@ -169,6 +169,17 @@ int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t
                              int addend_period, int addend_stride, const uint64_t* E, int polys,
                              int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
                              const uint64_t* tab1, const uint64_t* tab2, void* stream);
+/* ckb_divround_ntt_combine, then out += post (mod q_j) with post poly p at
+ * post + p*post_poly_stride (0 means (limbs-n_drop1-n_drop2)*N), rows as out:
+ * the accumulate of the rotate-and-sum schedules (packing.py:193-208,
+ * linalg.py:60-82: s + rotate(s, k)) folded into the key switch's epilogue, so
+ * the sum never makes a separate pass.  post may be NULL. */
+int ckb_divround_ntt_combine_acc(const ckb_ring* ring, uint64_t* out, const uint64_t* x,
+                                 int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                                 int addend_period, int addend_stride, const uint64_t* E,
+                                 int polys, int limbs, const int32_t* limb_prime, int n_drop1,
+                                 int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
+                                 const uint64_t* post, int64_t post_poly_stride, void* stream);
 /* Galois automorphism on NTT-domain limbs (a permutation of the bit-reversed
  * evaluation slots; ring.py:222-232 transported to the evaluation domain).
  * galois_items (DEVICE, one galois per item of rows_per_item rows) or NULL. */

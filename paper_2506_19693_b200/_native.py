@@ -83,6 +83,10 @@ def _load():
                                       ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int,
                                       ctypes.c_int, c_i32p, ctypes.c_int, ctypes.c_int, c_vp,
                                       c_vp, c_vp], ctypes.c_int),
+        "ckb_divround_ntt_combine_acc": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int,
+                                          ctypes.c_int, c_i32p, ctypes.c_int, ctypes.c_int, c_vp,
+                                          c_vp, c_vp, ctypes.c_int64, c_vp], ctypes.c_int),
         "ckb_automorphism_ntt": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_uint64, c_vp,
                                   ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_reduce": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
@@ -106,7 +110,8 @@ LIB = _load()
 EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inverse",
             "ckb_elementwise", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
-            "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_automorphism_ntt",
+            "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
+            "ckb_automorphism_ntt",
             "ckb_reduce", "ckb_sample", "ckb_alu_probe",
             "ckb_alu_probe_f64")
 

@@ -555,9 +555,12 @@ class B200CkksCore:
         return GpuCiphertext(out[0], ct.level)
 
     def _hrot(self, a: torch.Tensor, level: int, galois: int = 0, key: KeySwitchKey = None,
-              g_items=None, key_ptrs=None) -> torch.Tensor:
+              g_items=None, key_ptrs=None, accumulate: bool = False) -> torch.Tensor:
         """backend.py:155-171 on [B, 2, m, N] NTT-domain ciphertexts: automorphism
-        (a slot permutation in the NTT domain), key switch of c1', add c0'."""
+        (a slot permutation in the NTT domain), key switch of c1', add c0'.
+        accumulate: return a + rotate(a) instead — the add_ct of the
+        rotate-and-sum schedules (packing.py:193-208) done in the ModDown
+        combine pass, bit-identical to add_ct(a, rotate(a))."""
         ch = self.chain
         m = self._limbs(level)
         bsz = a.shape[0]
@@ -565,8 +568,12 @@ class B200CkksCore:
         c1 = ch.ntt_inv(r[:, 1].clone(memory_format=torch.contiguous_format), m)
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
                                    own_stride=2 * m * self.n)
+        post = None
+        if accumulate:
+            post = a if a.is_contiguous() else a.contiguous()
         out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, 0, addend=r, addend_polys=1,
-                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m))
+                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m),
+                              post=post)
         return out.view(bsz, 2, m, self.n)
 
     def _encrypt_values(self, values, level: int, serial: int = None) -> GpuCiphertext:

@@ -689,7 +689,8 @@ __global__ void __launch_bounds__(256) k_divround_combine(
     uint64_t* __restrict__ out, const uint64_t* __restrict__ x, size_t x_stride,
     const uint64_t* __restrict__ addend, int add_polys, int add_period, int add_stride,
     const uint64_t* __restrict__ E, int polys, int limbs, int n1, int n2, int log_n, RingDev R,
-    LimbMap lm, const uint64_t* __restrict__ tab1, const uint64_t* __restrict__ tab2) {
+    LimbMap lm, const uint64_t* __restrict__ tab1, const uint64_t* __restrict__ tab2,
+    const uint64_t* __restrict__ post, size_t post_stride) {
   // grid: x over coefficient pairs of one row, y over rows (poly, limb): the
   // row's constants are loaded once, every access is a 16-byte vector
   const size_t N = (size_t)1 << log_n;
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(256) k_divround_combine(
         ar = addend + ((pidx / add_period) * add_stride + ph) * m1 * N + (size_t)j * N;
     }
     const uint64_t* er = E + pj * N;
+    const uint64_t* pr = post ? post + pidx * post_stride + (size_t)j * N : nullptr;
     uint64_t* orow = out + pj * N;
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < half;
          q += (size_t)gridDim.x * blockDim.x) {
@@ -740,6 +742,11 @@ __global__ void __launch_bounds__(256) k_divround_combine(
       if (n2) {
         v.x = ckb::mul_shoup(v.x, b2, b2s, p);
         v.y = ckb::mul_shoup(v.y, b2, b2s, p);
+      }
+      if (pr) {  // fused accumulate: s + rot(s) (packing.py:193-208)
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(pr + n);
+        v.x = ckb::add_mod(v.x, w.x, p);
+        v.y = ckb::add_mod(v.y, w.y, p);
       }
       *reinterpret_cast<ulonglong2*>(orow + n) = v;
     }
@@ -1325,6 +1332,17 @@ int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t
                              int addend_period, int addend_stride, const uint64_t* E, int polys,
                              int limbs, const int32_t* limb_prime, int n_drop1, int n_drop2,
                              const uint64_t* tab1, const uint64_t* tab2, void* stream) {
+  return ckb_divround_ntt_combine_acc(ring, out, x, x_poly_stride, addend, addend_polys,
+                                      addend_period, addend_stride, E, polys, limbs, limb_prime,
+                                      n_drop1, n_drop2, tab1, tab2, nullptr, 0, stream);
+}
+
+int ckb_divround_ntt_combine_acc(const ckb_ring* ring, uint64_t* out, const uint64_t* x,
+                                 int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                                 int addend_period, int addend_stride, const uint64_t* E,
+                                 int polys, int limbs, const int32_t* limb_prime, int n_drop1,
+                                 int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
+                                 const uint64_t* post, int64_t post_poly_stride, void* stream) {
   LimbMap lm;
   if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
   if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 + n_drop2 >= limbs || polys < 0 || !E)
@@ -1345,7 +1363,8 @@ int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t
   k_divround_combine<<<grid, 256, 0, (cudaStream_t)stream>>>(
       out, x, xs, addend, addend ? addend_polys : 0, addend ? addend_period : 1,
       addend ? addend_stride : 0, E, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1,
-      tab2);
+      tab2, post,
+      post_poly_stride > 0 ? (size_t)post_poly_stride : ((size_t)m2 << R.log_n));
   return finish();
 }
 

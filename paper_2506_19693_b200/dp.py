@@ -149,6 +149,8 @@ class DataParallelExecutor(WaveExecutor):
                 wave = [i for i in wave if i >= self.n_setup]
             todo = []
             for i in wave:
+                if i in self.fused_adds:
+                    continue  # produced by its rotation (WaveExecutor._plan_fusion)
                 k = plan.kind[i]
                 if k == "rep" or (isinstance(k, tuple) and k[1] == rank):
                     todo.append(i)
@@ -184,7 +186,7 @@ class DataParallelExecutor(WaveExecutor):
                     else:
                         groups[(kind, la, b)].append(i)
                 elif tag == "rot":
-                    groups[("rot", env[op[2]].level, op[3] % slots)].append(i)
+                    groups[("rot", env[op[2]].level, op[3] % slots, i in self.fuse)].append(i)
                 else:
                     groups[("bs", i)].append(i)
             for key, idx in groups.items():

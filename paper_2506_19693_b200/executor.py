@@ -101,6 +101,34 @@ class WaveExecutor:
         self.level_of = level
         self.waves = [waves[d] for d in sorted(waves)]
         self.serials_used = counter
+        self._plan_fusion()
+
+    def _plan_fusion(self):
+        """Rotate-and-accumulate pairs: rot i (o = rotate(s, k)) whose result's
+        only reader is add_ct j = s + o (either operand order) — every rotation
+        of the recorded training steps (the log-depth sums of packing.py:193-208
+        and linalg.py:60-82).  Op i then produces j's output directly
+        (backend._hrot(accumulate=True): the add rides in the ModDown combine)
+        and j is skipped; modular addition is exact, so values are unchanged."""
+        ops = self.prog.ops
+        readers = collections.defaultdict(list)
+        for j, op in enumerate(ops):
+            for x in _inputs(op):
+                readers[x].append(j)
+        keep = set(self.prog.outputs)
+        self.fuse = {}
+        for i, op in enumerate(ops):
+            if op[0] != "rot":
+                continue
+            o, src = op[1], op[2]
+            rd = readers.get(o, [])
+            if o in keep or len(rd) != 1:
+                continue
+            j = rd[0]
+            add = ops[j]
+            if add[0] == "ew" and add[1] == "add_ct" and {add[3], add[4]} == {o, src}:
+                self.fuse[i] = j
+        self.fused_adds = set(self.fuse.values())
 
     # -- execution -----------------------------------------------------------
     def run(self, env=None, only_after_setup: bool = False, defer_refresh: bool = False) -> dict:
@@ -142,6 +170,8 @@ class WaveExecutor:
             for i in wave:
                 op = ops[i]
                 tag = op[0]
+                if i in self.fused_adds:
+                    continue  # produced by its rotation (_plan_fusion)
                 if tag == "enc":
                     groups[("enc",)].append(i)
                 elif tag == "ew":
@@ -152,7 +182,7 @@ class WaveExecutor:
                     else:
                         groups[(kind, la, b)].append(i)
                 elif tag == "rot":
-                    groups[("rot", env[op[2]].level, op[3] % slots)].append(i)
+                    groups[("rot", env[op[2]].level, op[3] % slots, i in self.fuse)].append(i)
                 elif be.real_bootstrap:  # one batched bootstrapping
                     groups[("bs", "batch")].append(i)
                 else:
@@ -268,15 +298,16 @@ class WaveExecutor:
                 be._encrypt_batch([values], rl, [self.serial_of[i]])[0], rl)
             return
         if tag == "rot":
-            _, lvl, step = key
+            _, lvl, step, fused = key
             x = self._stack([env[ops[i][2]].data for i in idx])
             if step == 0:
-                out = x.clone()
+                out = ch.add(x, x, be._limbs(lvl)) if fused else x.clone()
             else:
                 g = be.galois_for_step.get(step, pow(5, step, 2 * be.n))
-                out = be._hrot(x, lvl, galois=g, key=be.rotation_key(g))
+                out = be._hrot(x, lvl, galois=g, key=be.rotation_key(g), accumulate=fused)
             for j, i in enumerate(idx):
-                env[ops[i][1]] = GpuCiphertext(out[j], lvl)
+                dst = ops[self.fuse[i]][2] if fused else ops[i][1]
+                env[dst] = GpuCiphertext(out[j], lvl)
             return
         kind = tag
         op3 = kind[:3]

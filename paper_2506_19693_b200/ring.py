@@ -369,9 +369,11 @@ class GpuChain:
     def divround_ntt(self, x, polys: int, limbs: int, n1: int, n2: int = 0, *,
                      x_poly_stride: int = 0, addend=None, addend_polys: int = 0,
                      addend_period: int = 1, addend_stride: int = None, addend_tail=None,
-                     basis: tuple = None, out=None):
+                     basis: tuple = None, out=None, post=None):
         """Exact divide-and-round of NTT-domain polys (see ckb_divround_ntt_corr):
         iNTT of the dropped limbs, correction polynomial, its NTT, combine.
+        post: [polys, m2, N] NTT-domain polys added to the result in the same
+        pass (ckb_divround_ntt_combine_acc; the s + rotate(s) accumulate).
         addend_tail: [polys, n2, N] NTT-domain copy of the addend's limbs
         [limbs-n1-n2, limbs-n1) (zeros for polys without an addend) when n2 > 0."""
         basis = basis if basis is not None else self.q_basis(limbs)
@@ -403,16 +405,19 @@ class GpuChain:
         self.ntt_fwd(E, m2, self.cmap(tuple(basis[:m2])))
         out = out if out is not None else torch.empty(polys, m2, n, dtype=U64, device=self.device)
         n_add = 0 if addend is None else (polys // addend_period) * addend_polys * m2
-        nb = polys * m2 * 3 + n_add
+        nb = polys * m2 * (3 if post is None else 4) + n_add
+        if post is not None and (post.dtype != U64 or not post.is_contiguous()
+                                 or post.numel() != polys * m2 * n):
+            raise ValueError("post must be contiguous uint64 [polys, m2, N]")
         _run("divround_combine", nb * n * W, 1, lambda: nat.check(
-            nat.LIB.ckb_divround_ntt_combine(self.ring_p, nat.ptr(out), nat.ptr(x), xs,
-                                             nat.ptr(addend) if addend is not None else None,
-                                             addend_polys if addend is not None else 0,
-                                             addend_period, addend_stride, nat.ptr(E), polys,
-                                             limbs, self.cmap(basis), n1, n2,
-                                             nat.ptr(t1) if t1 is not None else None,
-                                             nat.ptr(t2) if t2 is not None else None,
-                                             nat.stream_handle()), "divround_ntt_combine"))
+            nat.LIB.ckb_divround_ntt_combine_acc(
+                self.ring_p, nat.ptr(out), nat.ptr(x), xs,
+                nat.ptr(addend) if addend is not None else None,
+                addend_polys if addend is not None else 0, addend_period, addend_stride,
+                nat.ptr(E), polys, limbs, self.cmap(basis), n1, n2,
+                nat.ptr(t1) if t1 is not None else None, nat.ptr(t2) if t2 is not None else None,
+                nat.ptr(post) if post is not None else None, 0, nat.stream_handle()),
+            "divround_ntt_combine"))
         return out
 
     def automorphism_ntt(self, x, galois: int, out=None, g_items=None, rows_per_item: int = 0):

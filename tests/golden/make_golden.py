@@ -9,6 +9,8 @@ Outputs (committed):
   ref_ckks_n512.npz  CkksBackend ciphertext planes for encrypt/add/sub/mul_ct/
                      mul_pt/add_pt/rotate/cross-level add (ckks/backend.py), the
                      secret, the prime chain and SHA-256 digests of every key row
+  ref_rbot_n512.npz  a reference RBOT model container (serialize.py) of a
+                     2-block model with its RBKY key file and decrypted payloads
   c1_trace.npz       the HE-API call sequence of one unchanged
                      nn.train_iteration (config 1 shape: 16->8->2, batch 32,
                      N=2^12, L=8) recorded on the sim backend, plus the sim
@@ -475,6 +477,33 @@ def make_c5_trace(init_scale: float = 0.25, lr: float = 0.005, out: str = "c5_tr
           [round(float(np.abs(v).max()), 3) for v in sim_w])
 
 
+def make_rbot():
+    """RBOT model container (serialize.py:38-60) of a freshly built 4->4->4->2
+    model (one RE and one CE block) under the n512 keyset, with its RBKY key
+    file and the decrypted values of all 8 payloads."""
+    from ciphermlp.api import keygen
+    from ciphermlp.ckks.backend import save_custodian
+    from ciphermlp.nn import Hyperparams, build_model
+    from ciphermlp.packing import Architecture
+    from ciphermlp.params import make_params
+    from ciphermlp.serialize import save_model
+
+    n = 512
+    params = make_params(level=3, scale_bits=40, poly_degree=n)
+    cust = keygen(params, {1, 3, -1}, backend="ckks", rng_seed=11)
+    arch = Architecture(4, (4, 4), 2)
+    model = build_model(arch, params, Hyperparams(learning_rate=0.05, rng_seed=3), cust)
+    out = {"rbky": np.frombuffer(save_custodian(cust), dtype=np.uint8),
+           "rbot": np.frombuffer(save_model(model, cust), dtype=np.uint8)}
+    dec = []
+    for b in model.blocks:
+        for pm in (b.layer_weights, b.classifier_weights, b.layer_velocity,
+                   b.classifier_velocity):
+            dec.append(cust.decrypt(pm.payload).values)
+    out["dec"] = np.stack(dec)
+    np.savez_compressed(os.path.join(HERE, "ref_rbot_n512.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-ckks", action="store_true")
@@ -484,6 +513,8 @@ def main():
         make_ntt()
     if a.only in ("", "ckks"):
         make_ckks()
+    if a.only in ("", "rbot"):
+        make_rbot()
     if a.only in ("", "c1"):
         make_c1_trace(a.c1_ckks)
     if a.only == "c4":

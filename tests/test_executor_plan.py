@@ -1,0 +1,50 @@
+"""WaveExecutor planning on the recorded traces (host logic, CPU): dependency
+waves and the rotate-and-accumulate fusion (executor._plan_fusion)."""
+
+import os
+import types
+
+import pytest
+
+from paper_2506_19693_b200.executor import WaveExecutor, _inputs
+from paper_2506_19693_b200.replay import Program
+
+
+def _stub_custodian(prog, real_bootstrap=False):
+    params = types.SimpleNamespace(level=30, refresh_level=8, slot_count=1 << 15)
+    be = types.SimpleNamespace(params=params, real_bootstrap=real_bootstrap)
+    return types.SimpleNamespace(backend=be)
+
+
+@pytest.mark.parametrize("name,n_rot", [("c1_trace.npz", 704), ("c4_trace.npz", 3840),
+                                        ("c5_trace.npz", 32256)])
+def test_every_rotation_fuses_with_its_accumulate(golden_dir, name, n_rot):
+    prog = Program.load(os.path.join(golden_dir, name))
+    ex = WaveExecutor(prog, _stub_custodian(prog, real_bootstrap=name != "c1_trace.npz"))
+    ops = prog.ops
+    assert sum(op[0] == "rot" for op in ops[prog.n_setup:]) == n_rot
+    assert len(ex.fuse) == n_rot and len(ex.fused_adds) == n_rot
+    readers = {}
+    for k, op in enumerate(ops):
+        for x in _inputs(op):
+            readers.setdefault(x, []).append(k)
+    wave_of = {x: w for w, wave in enumerate(ex.waves) for x in wave}
+    outputs = set(prog.outputs)
+    for i, j in ex.fuse.items():
+        rot, add = ops[i], ops[j]
+        assert rot[0] == "rot" and add[0] == "ew" and add[1] == "add_ct"
+        assert {add[3], add[4]} == {rot[1], rot[2]}
+        # the rotation's output has no other reader and is not a program output
+        assert readers[rot[1]] == [j] and rot[1] not in outputs
+        # the add runs in a later wave than the rotation (it is skipped there)
+        assert wave_of[j] > wave_of[i]
+
+
+def test_fusion_skips_rotations_with_other_readers(golden_dir):
+    prog = Program.load(os.path.join(golden_dir, "c1_trace.npz"))
+    i = next(k for k, op in enumerate(prog.ops) if op[0] == "rot" and k >= prog.n_setup)
+    out = prog.ops[i][1]
+    # make the rotation's output a program output: it must then be materialised
+    prog.outputs = list(prog.outputs) + [out]
+    ex = WaveExecutor(prog, _stub_custodian(prog))
+    assert i not in ex.fuse

@@ -22,7 +22,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
 
 from oracle import ckks_oracle as O  # noqa: E402
 from paper_2506_19693_b200 import he_api, he_errors  # noqa: E402
-from paper_2506_19693_b200.backend import B200Backend  # noqa: E402
+from paper_2506_19693_b200.backend import B200Backend, GpuCiphertext  # noqa: E402
 from paper_2506_19693_b200.ring import GpuChain  # noqa: E402
 from paper_2506_19693_b200.scheme import SchemeParams, make_params  # noqa: E402
 
@@ -283,8 +283,8 @@ def test_rbky_reference_key_file_round_trip(ck_gold):
 
 @pytest.mark.parametrize("dnum,level,special", [(None, 3, 60), (2, 3, 120), (3, 5, 300)])
 def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
-    """(3, 5, 300): 5 special primes, so ModDown drops 5 + 1 primes and the
-    correction runs on the tensor cores (k_divround_corr_tc)."""
+    """(3, 5, 300): 5 special primes, so ModDown with the fused rescale drops
+    5 + 1 primes (k_divround_corr<6, 1>)."""
     n = 256
     chain = (60,) + (40,) * level + (special,)
     params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=40, level=level)
@@ -315,6 +315,14 @@ def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
     ]
     for cv, oct_ in checks:
         assert np.array_equal(be.planes_of(cv.payload), O.ct_to_u64(oct_, orc.chain))
+    # fused rotate-and-accumulate (ckb_divround_ntt_combine_acc), batched:
+    # a + rot(a, 5) and b + rot(b, 5) in one key switch
+    g = pow(5, 5, 2 * n)
+    x = torch.stack([a.payload.data, b.payload.data])
+    acc = be._hrot(x, level, galois=g, key=be.rotation_key(g), accumulate=True)
+    for j, (ct, oct_) in enumerate(((a, oa), (b, ob))):
+        want = O.ct_to_u64(orc.add(oct_, orc.rotate(oct_, 5)), orc.chain)
+        assert np.array_equal(be.planes_of(GpuCiphertext(acc[j], level)), want)
     # inputs are never modified by an op (CipherVector immutability, api.py:51-65)
     assert np.array_equal(be.planes_of(a.payload), planes[0])
     assert np.array_equal(be.planes_of(b.payload), planes[1])

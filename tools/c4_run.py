@@ -9,11 +9,11 @@ from paper_2506_19693_b200.executor import WaveExecutor
 from paper_2506_19693_b200.scheme import SchemeParams
 
 
-def run(reps=2, verbose=True, graph=True):
+def run(reps=2, verbose=True, graph=True, special=660):
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c4_trace.npz")
     z = np.load(path); prog = Program.load(path)
     n, L, sb, bd = (int(v) for v in z["params"])
-    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (special,),
                           scale_bits=45, level=L, bootstrap_depth=bd)
     t0 = time.perf_counter()
     cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=4,

@@ -11,14 +11,14 @@ from paper_2506_19693_b200.executor import WaveExecutor
 from paper_2506_19693_b200.scheme import SchemeParams
 
 
-def run(reps=1, max_group=64, verbose=True):
+def run(reps=1, max_group=64, verbose=True, special=780):
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
                         "golden", "c5_trace.npz")
     z = np.load(path); prog = Program.load(path)
     n, L, sb, bd = (int(v) for v in z["params"])
     user = L - bd
     # P = 13 x 60 bits: 120 bits above the widest digit (11 x 60-bit bootstrap primes)
-    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * user + (60,) * bd + (780,),
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * user + (60,) * bd + (special,),
                           scale_bits=45, level=L, bootstrap_depth=bd)
     t0 = time.perf_counter()
     cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=5,
