@@ -554,6 +554,40 @@ __device__ __forceinline__ void st_v(uint64_t* p, const uint64_t* x) {
   }
 }
 
+// acc_c - sum_{u<cnt} r_u[c] * M_u  (mod p) for V lanes at once, with one
+// reduction instead of cnt sequential modular steps: each term is made
+// non-negative as (C - r_u) M_u with C = p << (clz(p) - 4) in [2^59, 2^60) a
+// multiple of p (|r_u| < 2^59), so the 128-bit lazy sum stays below
+// 2^125 for up to 16 terms.  Bit-identical to the sub_rm chain.
+template <int D, int V>
+__device__ __forceinline__ void sub_rm_lazy(uint64_t* acc, const int64_t (*r)[V], int cnt,
+                                            const uint64_t* __restrict__ Tb, const uint64_t* mm) {
+  const uint64_t p = __ldg(mm);
+  const int64_t C = (int64_t)(p << (__clzll((long long)p) - 4));
+  uint64_t h[V], l[V];
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    h[c] = 0;
+    l[c] = acc[c];
+  }
+#pragma unroll
+  for (int u = 0; u < D; ++u)
+    if (u < cnt) {
+      const uint64_t M = __ldg(Tb + 2 * u);
+#pragma unroll
+      for (int c = 0; c < V; ++c) ckb::mac128(h[c], l[c], (uint64_t)(C - r[u][c]), M);
+    }
+  const Mod m{p, __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+  const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+  if (m.k >= 32) {  // warp-uniform
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = ckb::reduce128_big(h[c], l[c], r64, r64s, m);
+  } else {
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = ckb::reduce128_any(h[c], l[c], r64, r64s, m);
+  }
+}
+
 template <int D1, int D2, int V>
 __global__ void __launch_bounds__(256, V == 2 ? 2 : 3) k_divround_corr(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
@@ -594,13 +628,17 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : 3) k_divround_corr(
         const uint64_t* Tb = tab1 + (size_t)li * s1;
         uint64_t a[V];
         ld_v<V>(a, src + (size_t)(li - m2) * N);
+        if (d >= 2) {  // compile-time after unrolling
+          sub_rm_lazy<D1, V>(a, r1, d, Tb, R.mods + (size_t)lm.p[li] * kModStride);
+        } else {
 #pragma unroll
-        for (int u = 0; u < D1; ++u)
-          if (u < d) {
-            const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
+          for (int u = 0; u < D1; ++u)
+            if (u < d) {
+              const uint64_t M = __ldg(Tb + 2 * u), Ms = __ldg(Tb + 2 * u + 1);
 #pragma unroll
-            for (int c = 0; c < V; ++c) a[c] = sub_rm(a[c], r1[u][c], M, Ms, p);
-          }
+              for (int c = 0; c < V; ++c) a[c] = sub_rm(a[c], r1[u][c], M, Ms, p);
+            }
+        }
         const uint64_t W = __ldg(Tb + 2 * n1), Ws = __ldg(Tb + 2 * n1 + 1);
 #pragma unroll
         for (int c = 0; c < V; ++c) r1[d][c] = centered(ckb::mul_shoup(a[c], W, Ws, p), p);
@@ -615,13 +653,17 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : 3) k_divround_corr(
         ld_v<V>(v, src + (size_t)(li - m2) * N);
         if (n1) {
           const uint64_t* Ta = tab1 + (size_t)li * s1;
+          if (n1 >= 2) {
+            sub_rm_lazy<D1, V>(v, r1, n1, Ta, R.mods + (size_t)lm.p[li] * kModStride);
+          } else {
 #pragma unroll
-          for (int u = 0; u < D1; ++u)
-            if (u < n1) {
-              const uint64_t M = __ldg(Ta + 2 * u), Ms = __ldg(Ta + 2 * u + 1);
+            for (int u = 0; u < D1; ++u)
+              if (u < n1) {
+                const uint64_t M = __ldg(Ta + 2 * u), Ms = __ldg(Ta + 2 * u + 1);
 #pragma unroll
-              for (int c = 0; c < V; ++c) v[c] = sub_rm(v[c], r1[u][c], M, Ms, p);
-            }
+                for (int c = 0; c < V; ++c) v[c] = sub_rm(v[c], r1[u][c], M, Ms, p);
+              }
+          }
           const uint64_t W = __ldg(Ta + 2 * n1), Ws = __ldg(Ta + 2 * n1 + 1);
 #pragma unroll
           for (int c = 0; c < V; ++c) v[c] = ckb::mul_shoup(v[c], W, Ws, p);
