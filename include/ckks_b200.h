@@ -76,6 +76,17 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
  * Replaces NttPlan.inverse (ckks/ntt.py:138-154) / RingElement.to_coeff (ring.py:117-123). */
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream);
+/* Out-of-place forms: dst ([rows][N], contiguous) = NTT / iNTT of the rows of
+ * src, row r = (item r / limbs, limb r % limbs) read at
+ * src + item*src_item_stride + limb*N (0: limbs*N).  The transform's first pass
+ * reads src, so a strided operand (one component of a [B][3][limbs][N] tensor
+ * product) is transformed without a staging copy.  dst must not overlap src. */
+int ckb_ntt_forward_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,
+                         int64_t src_item_stride, int rows, int limbs, const int32_t* limb_prime,
+                         void* stream);
+int ckb_ntt_inverse_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,
+                         int64_t src_item_stride, int rows, int limbs, const int32_t* limb_prime,
+                         void* stream);
 
 /* Limb-wise arithmetic over rows*N residues.  Replace RingElement.add/sub/neg/
  * mul (ring.py:80-131).  op: 0 add, 1 sub, 2 mul (Hadamard), 3 neg (b unused),
@@ -85,6 +96,18 @@ int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
 int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t* a,
                     const uint64_t* b, const uint64_t* c, int rows, int limbs,
                     const int32_t* limb_prime, int b_rows, void* stream);
+
+/* Plaintext multiply-accumulate over the terms of a baby-step/giant-step row
+ * (the CoeffToSlot / SlotToCoeff diagonals of bootstrapping):
+ *   out[r][n] = sum_t X_t[r][n] * pts[t][r % limbs][n]  (mod p of limb r % limbs)
+ * with X_t = x0 when term_idx[t] == -1, else stack + term_idx[t]*stack_stride
+ * (elements), all X_t laid out like out: `rows` rows of N.  n_terms <= 64;
+ * one 128-bit lazy sum and one reduction per coefficient.  Replaces a chain of
+ * RingElement.mul / add (ring.py:80-131) with one pass over the operands. */
+int ckb_pt_mac(const ckb_ring* ring, uint64_t* out, const uint64_t* x0, const uint64_t* stack,
+               int64_t stack_stride, const int32_t* term_idx, const uint64_t* pts,
+               int64_t pt_stride, int n_terms, int rows, int limbs, const int32_t* limb_prime,
+               void* stream);
 /* out = a * scalar[limb]; scalars_host is [limbs][2] {v, floor(v*2^64/p)} with v < p.
  * Replaces RingElement.scalar_mul (ring.py:110-115 of RingElement; backend.py:108-111). */
 int ckb_scalar_mul(const ckb_ring* ring, uint64_t* out, const uint64_t* a, int rows,
@@ -103,10 +126,13 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
  * equal limb_prime).  alpha == 1 reproduces the reference's centered per-limb
  * digits exactly; alpha > 1 is the standard fast basis conversion using
  * bconv (device table [digits][alpha][2 + 2*ext_limbs]; see backend.py docs).
- * out: [batch][digits][ext_limbs][N], coefficient domain.  With skip_own (requires
- * limbs % alpha == 0) a digit's own limbs are not written and each digit has
- * ext_limbs - alpha rows (the ext basis without its own limbs): their NTT is the
- * NTT-domain input itself, which ckb_ks_inner reads directly. */
+ * out: [batch][digits][ext_limbs][N], coefficient domain.  With skip_own a
+ * digit's own limbs are not written and digit j keeps ext_limbs - width_j rows
+ * (the ext basis without its own limbs) at row offset j*(ext_limbs - alpha) of
+ * its item; a short last digit (limbs % alpha != 0) therefore has more rows and
+ * an item holds (digits-1)*(ext_limbs-alpha) + ext_limbs - width_last rows.  The
+ * skipped limbs' NTT is the NTT-domain input itself, which ckb_ks_inner reads
+ * directly. */
 int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
               int batch, int limbs, const int32_t* limb_prime, int ext_limbs,
               const int32_t* ext_prime, int alpha, const uint64_t* bconv, int skip_own,
@@ -115,7 +141,7 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
 /* Key-switch inner product in the NTT domain (keys.py:91-97):
  *   acc[b][c][e] = sum_j digits[b][j][e] * key_b[j][c][key_limb[e]]
  * digits: [batch][n_digits][rows][N] with rows = ext_limbs, or (own != NULL)
- * ext_limbs - alpha rows as written by ckb_modup(skip_own), the own limbs then
+ * the compact per-digit layout written by ckb_modup(skip_own), the own limbs then
  * read from `own` ([limbs][N] per item at b*own_batch_stride, NTT domain).
  * acc: [batch][2][ext_limbs][N].  key_ptrs: DEVICE array of `batch` pointers to
  * keys laid out [key_rows][2][key_limbs][N]; if NULL, `key` is used for every item. */

@@ -362,7 +362,9 @@ class B200CkksCore:
         ch = self.chain
         a = self.alpha
         nd = -(-m // a)
-        skip = own is not None and m % a == 0 and nd * (m + ch.k - a) <= 128
+        # own limbs read from the NTT-domain input (a short last digit included);
+        # the digits' NTT limb map holds <= 128 rows
+        skip = own is not None and nd * (m + ch.k) - m <= 128
         digits = ch.modup(d, m, a, self._bconv(m), batch=batch, in_batch_stride=d_stride,
                           skip_own=skip)
         basis = ch.digit_basis(m, a, skip)
@@ -534,7 +536,7 @@ class B200CkksCore:
         bsz = a.shape[0]
         e = len(ch.entry_primes[level])
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
-        d2 = ch.ntt_inv(d[:, 2].clone(memory_format=torch.contiguous_format), m)
+        d2 = ch.ntt_from(d[:, 2], bsz, m, 3 * m * self.n, inverse=True)
         acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key, own=d[:, 2],
                                    own_stride=3 * m * self.n)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
@@ -565,7 +567,7 @@ class B200CkksCore:
         m = self._limbs(level)
         bsz = a.shape[0]
         r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
-        c1 = ch.ntt_inv(r[:, 1].clone(memory_format=torch.contiguous_format), m)
+        c1 = ch.ntt_from(r[:, 1], bsz, m, 2 * m * self.n, inverse=True)
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
                                    own_stride=2 * m * self.n)
         post = None
@@ -743,32 +745,35 @@ class B200CkksCore:
             self._adjust_cache[key] = hit
         return hit
 
-    def hoisted_rotations(self, data: torch.Tensor, level: int, galois_list) -> list:
+    def hoisted_rotations(self, data: torch.Tensor, level: int, galois_list,
+                          stack: bool = False):
         """Rotate ciphertexts ([..., 2, m, N], NTT domain) by several Galois
         elements sharing a single ModUp: the digits are lifted and transformed
         once and permuted per rotation in the NTT domain (an automorphism
         commutes with the basis extension up to multiples of Q_j, which the key
-        switch absorbs as noise)."""
+        switch absorbs as noise).  stack=True returns one tensor
+        [len(galois_list), ..., 2, m, N] instead of a list."""
         ch = self.chain
         m = self._limbs(level)
         ext = m + ch.k
         lead = data.shape[:-3]
         d = data.reshape(-1, 2, m, self.n)
         b = d.shape[0]
-        c1 = ch.ntt_inv(d[:, 1].clone(memory_format=torch.contiguous_format), m)
+        c1 = ch.ntt_from(d[:, 1], b, m, 2 * m * self.n, inverse=True)
         digits = ch.modup(c1, m, self.alpha, self._bconv(m), batch=b)
         ch.ntt_fwd(digits, ext, ch.ext_map(m))
         c0s = d[:, 0].contiguous()
-        out = []
-        for g in galois_list:
+        res = torch.empty(len(galois_list), b, 2, m, self.n, dtype=U64, device=self.device)
+        for i, g in enumerate(galois_list):
             key = self.rotation_key(g)
             dg = ch.automorphism_ntt(digits, g)
             acc = ch.ks_inner(dg, m, self.alpha, key=key.data)
             c0 = ch.automorphism_ntt(c0s, g)
-            r = ch.divround_ntt(acc, 2 * b, ext, ch.k, 0, addend=c0, addend_polys=1,
-                                addend_period=2, addend_stride=1, basis=ch.ext_basis(m))
-            out.append(r.view(*lead, 2, m, self.n))
-        return out
+            ch.divround_ntt(acc, 2 * b, ext, ch.k, 0, addend=c0, addend_polys=1,
+                            addend_period=2, addend_stride=1, basis=ch.ext_basis(m),
+                            out=res[i].view(2 * b, m, self.n))
+        res = res.view(len(galois_list), *lead, 2, m, self.n)
+        return res if stack else list(res.unbind(0))
 
     def bootstrap_batch(self, data: torch.Tensor, level: int) -> torch.Tensor:
         """Bootstrap a batch [B, 2, m, N] of ciphertexts at one level together:

@@ -171,19 +171,27 @@ class Bootstrapper:
         q = self._q(lvl)
         pt_scale = q if out_scale is None else out_scale * q / sc
         babies = sorted({b for row in rows.values() for b in row if b})
-        rots = dict(zip(babies, be.hoisted_rotations(data, lvl, [self._galois(b * s)
-                                                                 for b in babies])))
-        rots[0] = data
+        stack = (be.hoisted_rotations(data, lvl, [self._galois(b * s) for b in babies],
+                                      stack=True) if babies else None)
+        slot = {b: i for i, b in enumerate(babies)}
+        slot[0] = -1  # the unrotated input
+        data = data.contiguous()
         acc = None
         for g, row in sorted(rows.items()):
-            inner = None
-            for b, diag in row.items():
-                key = (tag, g, b, lvl, pt_scale)
-                pt = self._pt_cache.get(key)
-                if pt is None:
-                    pt = self._pt_cache[key] = be.encode_complex_ntt(diag, lvl, scale=pt_scale)
-                term = ch.mul(rots[b], pt, m, b_rows=m)
-                inner = term if inner is None else ch.add(inner, term, m, out=inner)
+            # one multiply-accumulate pass over the row's terms (ckb_pt_mac)
+            key = (tag, g, lvl, pt_scale)
+            hit = self._pt_cache.get(key)
+            if hit is None:
+                pts = torch.stack([be.encode_complex_ntt(diag, lvl, scale=pt_scale)
+                                   for diag in row.values()])
+                hit = self._pt_cache[key] = (ch.publish(pts), [slot[b] for b in row])
+            pts, idx = hit
+            inner = torch.empty_like(data)
+            for lo in range(0, len(idx), 64):
+                part = ch.pt_mac(data, stack, idx[lo:lo + 64], pts[lo:lo + 64], m,
+                                 out=inner if lo == 0 else None)
+                if lo:
+                    ch.add(inner, part, m, out=inner)
             inner = be._rescale_data(inner, lvl)
             if g:
                 inner = be.rotate_data(inner, lvl - 1, self._galois(g * n1 * s))

@@ -49,6 +49,8 @@ struct NttPhase {
   int items;    // > 0: rows enumerated limb-major (rows = items * limbs)
   int first;    // first phase of the transform: input is canonical uint64
                 // (the FP64 path keeps doubles between the two phases)
+  const uint64_t* src;  // out-of-place first phase: row (item i, limb l) is read
+  size_t src_istride;   // from src + i*src_istride + l*N (NULL: in place)
 };
 
 // Shared-memory slot of element r of group g: one pad word per 16 elements
@@ -447,6 +449,10 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   const bool f64 = MODE == 1 || MODE == 3 || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
   if (((MODE == 1 || MODE == 3) && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
   uint64_t* base = data + (size_t)row * N;
+  // tile loads of an out-of-place first phase come from the source row
+  const uint64_t* ibase = ph.src ? ph.src + (size_t)(row / ph.limbs) * ph.src_istride +
+                                       (size_t)(row % ph.limbs) * N
+                                 : base;
   const int C = ph.C;
   const int T = blockDim.x;
   const int tid = threadIdx.x;
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       int g, r;
-      v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_of(i, g, r)));
+      v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(ibase + pair_of(i, g, r)));
     }
     if (f64 && ph.first) {  // canonical residues -> exact doubles
 #pragma unroll
@@ -602,7 +608,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
 
 template <bool FWD>
 int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
-            void* stream) {
+            void* stream, const uint64_t* src = nullptr, size_t src_istride = 0) {
   LimbMap lm;
   if (!make_map(lm, limb_prime, limbs) || rows < 0) return CKB_E_LIMBS;
   if (rows == 0) return 0;
@@ -612,7 +618,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   cudaStream_t st = (cudaStream_t)stream;
   const int N = 1 << logn;
   if (logn <= 12) {
-    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0, 1};
+    NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0, 1, src, src_istride};
     int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
     return rc ? rc : finish();
   }
@@ -631,9 +637,11 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   // phase A: groups are the GB columns, elements strided by GB
   auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
   const int items = (rows % limbs == 0 && rows / limbs > 1) ? rows / limbs : 0;
-  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA), items, FWD ? 1 : 0};
+  NttPhase pa{limbs, GB / CA, CA, 1, GB, 1, 0, FWD ? 0 : 1, 0, lg(CA), items, FWD ? 1 : 0,
+              FWD ? src : nullptr, src_istride};
   // phase B: groups are the GA rows of GB contiguous elements
-  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items, FWD ? 0 : 1};
+  NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items, FWD ? 0 : 1,
+              FWD ? nullptr : src, src_istride};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
   const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
   for (int r0 = 0; r0 < rows; r0 += chunk) {
@@ -728,6 +736,22 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream) {
   return ntt_run<false>(ring, data, rows, limbs, limb_prime, stream);
+}
+
+int ckb_ntt_forward_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,
+                         int64_t src_item_stride, int rows, int limbs, const int32_t* limb_prime,
+                         void* stream) {
+  if (!src || src_item_stride < 0) return CKB_E_ARG;
+  return ntt_run<true>(ring, dst, rows, limbs, limb_prime, stream, src,
+                       src_item_stride ? (size_t)src_item_stride : ((size_t)limbs << ring->log_n));
+}
+
+int ckb_ntt_inverse_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,
+                         int64_t src_item_stride, int rows, int limbs, const int32_t* limb_prime,
+                         void* stream) {
+  if (!src || src_item_stride < 0) return CKB_E_ARG;
+  return ntt_run<false>(ring, dst, rows, limbs, limb_prime, stream, src,
+                        src_item_stride ? (size_t)src_item_stride : ((size_t)limbs << ring->log_n));
 }
 
 

@@ -13,25 +13,80 @@ namespace {
 // Element-wise limb arithmetic
 // ===========================================================================
 
-__global__ void k_elementwise(int op, uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
-                              const uint64_t* __restrict__ b, const uint64_t* __restrict__ c,
-                              size_t total, size_t bperiod, int log_n, int limbs, RingDev R,
-                              LimbMap lm) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int row = (int)(i >> log_n);
+// Limb-wise arithmetic, two coefficients per thread (16-byte accesses); b
+// (and c) broadcast with a period of brows rows when brows > 0.  The row
+// index is a 32-bit quantity, so the limb and broadcast-row lookups are
+// 32-bit modulos once per coefficient pair.
+template <int OP>
+__device__ __forceinline__ uint64_t ew_op(uint64_t x, uint64_t y, uint64_t z, const Mod& m) {
+  if constexpr (OP == 0) return ckb::add_mod(x, y, m.p);
+  if constexpr (OP == 1) return ckb::sub_mod(x, y, m.p);
+  if constexpr (OP == 2) return ckb::mul_mod(x, y, m);
+  if constexpr (OP == 3) return ckb::neg_mod(x, m.p);
+  return ckb::add_mod(ckb::mul_mod(x, y, m), z, m.p);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) k_elementwise(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+    const uint64_t* __restrict__ c, size_t pairs, unsigned brows, int log_n, unsigned limbs,
+    RingDev R, LimbMap lm) {
+  const int lh = log_n - 1;
+  const size_t hmask = ((size_t)1 << lh) - 1;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < pairs;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const unsigned row = (unsigned)(t >> lh);
+    const size_t n = (t & hmask) * 2;
     const Mod m = load_mod(R, lm.p[row % limbs]);
-    const uint64_t x = a[i];
-    const size_t ib = bperiod ? i % bperiod : i;
-    uint64_t r;
-    switch (op) {
-      case 0: r = ckb::add_mod(x, b[ib], m.p); break;
-      case 1: r = ckb::sub_mod(x, b[ib], m.p); break;
-      case 2: r = ckb::mul_mod(x, b[ib], m); break;
-      case 3: r = ckb::neg_mod(x, m.p); break;
-      default: r = ckb::add_mod(ckb::mul_mod(x, b[ib], m), c[ib], m.p); break;
+    const size_t i = ((size_t)row << log_n) + n;
+    const size_t ib = brows ? ((size_t)(row % brows) << log_n) + n : i;
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + i);
+    ulonglong2 y = make_ulonglong2(0, 0), z = make_ulonglong2(0, 0);
+    if constexpr (OP != 3) y = *reinterpret_cast<const ulonglong2*>(b + ib);
+    if constexpr (OP == 4) z = *reinterpret_cast<const ulonglong2*>(c + ib);
+    *reinterpret_cast<ulonglong2*>(out + i) =
+        make_ulonglong2(ew_op<OP>(x.x, y.x, z.x, m), ew_op<OP>(x.y, y.y, z.y, m));
+  }
+}
+
+// out = sum_t x_t (.) pt_t over the coefficient-wise products, one reduction:
+// the ciphertext operand of term t is x0 (idx -1) or stack + idx[t]*xstride,
+// each [items][comps*limbs][N]; its plaintext is pts + t*ptstride, [limbs][N]
+// broadcast over items and components.  128-bit lazy sums (T <= 64 terms of
+// products < 2^124).  Replaces the mul_pt + add_ct chain of a BSGS row.
+struct TermIdx {
+  int16_t p[64];
+};
+
+__global__ void __launch_bounds__(256) k_pt_mac(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ x0,
+    const uint64_t* __restrict__ stack, size_t xstride, TermIdx ti,
+    const uint64_t* __restrict__ pts, size_t ptstride, int T, size_t pairs, int log_n,
+    unsigned limbs, RingDev R, LimbMap lm) {
+  const int lh = log_n - 1;
+  const size_t hmask = ((size_t)1 << lh) - 1;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < pairs;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const unsigned row = (unsigned)(t >> lh);
+    const size_t n = (t & hmask) * 2;
+    const unsigned l = row % limbs;
+    const size_t i = ((size_t)row << log_n) + n;
+    const size_t ip = ((size_t)l << log_n) + n;
+    uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll 4
+    for (int k = 0; k < T; ++k) {
+      const uint64_t* xs = ti.p[k] < 0 ? x0 : stack + (size_t)ti.p[k] * xstride;
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(xs + i);
+      const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(pts + k * ptstride + ip));
+      ckb::mac128(h0, l0, x.x, w.x);
+      ckb::mac128(h1, l1, x.y, w.y);
     }
-    out[i] = r;
+    const uint64_t* mm = R.mods + (size_t)lm.p[l] * kModStride;
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    *reinterpret_cast<ulonglong2*>(out + i) =
+        make_ulonglong2(ckb::reduce128_any(h0, l0, r64, r64s, m),
+                        ckb::reduce128_any(h1, l1, r64, r64s, m));
   }
 }
 
@@ -98,7 +153,7 @@ template <int AMAX>
 __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
                                                 const uint64_t* __restrict__ in, size_t in_bstride,
                                                 int batch, int limbs, int ext, int alpha,
-                                                int n_digits, int out_rows, int skip_own,
+                                                int item_rows, int out_rows, int skip_own,
                                                 int log_n, RingDev R, LimbMap lm, LimbMap em,
                                                 const uint64_t* __restrict__ bconv) {
   extern __shared__ uint64_t sm[];
@@ -130,7 +185,7 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
     const size_t n = (t & (half - 1)) * 2;
     const size_t bi = t / half;
     const uint64_t* src = in + bi * in_bstride + n;
-    uint64_t* dst = out + (bi * n_digits + j) * (size_t)out_rows * N + n;
+    uint64_t* dst = out + (bi * (size_t)item_rows + (size_t)j * out_rows) * N + n;
     if (AMAX == 1) {
       const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)first * N);
       const uint64_t q = __ldg(R.mods + (size_t)lm.p[first] * kModStride);
@@ -203,9 +258,9 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
 // per thread (register budget).  Smem: ModSm per ext limb, the integer table in
 // pack30 form, then per (i, e) {double(c), double(c)/p_e} and per e 1/p_e.
 template <int AMAX>
-__global__ void __launch_bounds__(256) k_modup_mixed(
+__global__ void __launch_bounds__(256, AMAX <= 6 ? 4 : (AMAX <= 8 ? 3 : 2)) k_modup_mixed(
     uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_bstride, int batch,
-    int limbs, int ext, int alpha, int n_digits, int out_rows, int skip_own, int log_n,
+    int limbs, int ext, int alpha, int item_rows, int out_rows, int skip_own, int log_n,
     RingDev R, LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
   extern __shared__ uint64_t sm[];
   ModSm* mods = reinterpret_cast<ModSm*>(sm);
@@ -251,7 +306,7 @@ __global__ void __launch_bounds__(256) k_modup_mixed(
     const size_t n = t & (N - 1);
     const size_t bi = t >> log_n;
     const uint64_t* src = in + bi * in_bstride + n;
-    uint64_t* dst = out + (bi * n_digits + j) * (size_t)out_rows * N + n;
+    uint64_t* dst = out + (bi * (size_t)item_rows + (size_t)j * out_rows) * N + n;
     uint64_t y[AMAX];
     double yd[AMAX];
 #pragma unroll
@@ -309,7 +364,8 @@ __global__ void __launch_bounds__(256) k_modup_mixed(
 template <int ND>
 __global__ void __launch_bounds__(256) k_ks_inner(
     uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
-    int out_rows, int alpha, const uint64_t* __restrict__ own, size_t own_bstride, int log_n,
+    int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
+    size_t own_bstride, int log_n,
     const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
     RingDev R, LimbMap em, LimbMap km, LimbMap od) {
   const size_t N = (size_t)1 << log_n;
@@ -326,11 +382,12 @@ __global__ void __launch_bounds__(256) k_ks_inner(
     const uint64_t* kb = K + (size_t)km.p[e] * N + n;
     const uint64_t* ka = kb + (size_t)key_limbs * N;
     const int owner = own ? od.p[e] : -1;
-    const uint64_t* dbase = dig + bi * (size_t)ND * out_rows * N + n;
+    const uint64_t* dbase = dig + bi * (size_t)item_rows * N + n;
     ulonglong2 x[ND], b[ND], a[ND];
 #pragma unroll
     for (int j = 0; j < ND; ++j) {  // issue every load first
-      const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
+      const int cj = min(alpha, limbs - j * alpha);  // digit j's width (last may be short)
+      const int row = own ? e - (e >= j * alpha + cj ? cj : 0) : e;
       const uint64_t* xp = (j == owner) ? own + bi * own_bstride + (size_t)e * N + n
                                         : dbase + ((size_t)j * out_rows + row) * N;
       x[j] = *reinterpret_cast<const ulonglong2*>(xp);
@@ -369,7 +426,8 @@ __global__ void __launch_bounds__(256) k_ks_inner(
 // Runtime digit count (alpha = 1 chains with many digits).
 __global__ void __launch_bounds__(256) k_ks_inner_any(
     uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
-    int out_rows, int alpha, const uint64_t* __restrict__ own, size_t own_bstride, int log_n,
+    int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
+    size_t own_bstride, int log_n,
     const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
     RingDev R, LimbMap em, LimbMap km, LimbMap od) {
   const size_t N = (size_t)1 << log_n;
@@ -385,10 +443,11 @@ __global__ void __launch_bounds__(256) k_ks_inner_any(
     const uint64_t* kb = K + (size_t)km.p[e] * N + n;
     const uint64_t* ka = kb + (size_t)key_limbs * N;
     const int owner = own ? od.p[e] : -1;
-    const uint64_t* dbase = dig + bi * (size_t)nd * out_rows * N + n;
+    const uint64_t* dbase = dig + bi * (size_t)item_rows * N + n;
     uint64_t hb = 0, lb = 0, ha = 0, la = 0;
     for (int j = 0; j < nd; ++j) {
-      const int row = own ? e - (e >= (j + 1) * alpha ? alpha : 0) : e;
+      const int cj = min(alpha, limbs - j * alpha);  // digit j's width (last may be short)
+      const int row = own ? e - (e >= j * alpha + cj ? cj : 0) : e;
       const uint64_t x = (j == owner) ? own[bi * own_bstride + (size_t)e * N + n]
                                       : dbase[((size_t)j * out_rows + row) * N];
       ckb::mac128(hb, lb, x, __ldg(kb + j * krow));
@@ -1080,9 +1139,42 @@ int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t*
   const RingDev R = make_ring(ring);
   const size_t total = (size_t)rows << R.log_n;
   if (!total) return 0;
-  const size_t bperiod = (b_rows && b_rows < rows) ? ((size_t)b_rows << R.log_n) : 0;
-  k_elementwise<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      op, out, a, b, c, total, bperiod, (int)R.log_n, limbs, R, lm);
+  const unsigned brows = (b_rows && b_rows < rows) ? (unsigned)b_rows : 0u;
+  const size_t pairs = total / 2;
+  const int grid = grid_for(pairs, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (op) {
+#define CKB_EW(OP)                                                                            \
+  case OP:                                                                                    \
+    k_elementwise<OP><<<grid, 256, 0, st>>>(out, a, b, c, pairs, brows, (int)R.log_n,       \
+                                           (unsigned)limbs, R, lm);                         \
+    break;
+    CKB_EW(0) CKB_EW(1) CKB_EW(2) CKB_EW(3) CKB_EW(4)
+#undef CKB_EW
+  }
+  return finish();
+}
+
+int ckb_pt_mac(const ckb_ring* ring, uint64_t* out, const uint64_t* x0, const uint64_t* stack,
+               int64_t stack_stride, const int32_t* term_idx, const uint64_t* pts,
+               int64_t pt_stride, int n_terms, int rows, int limbs, const int32_t* limb_prime,
+               void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || rows < 0 || n_terms < 1 || n_terms > 64 || !pts ||
+      !term_idx || pt_stride < 0 || stack_stride < 0)
+    return CKB_E_ARG;
+  TermIdx ti;
+  for (int k = 0; k < n_terms; ++k) {
+    if (term_idx[k] < -1 || term_idx[k] > 32767) return CKB_E_ARG;
+    if ((term_idx[k] < 0 && !x0) || (term_idx[k] >= 0 && !stack)) return CKB_E_ARG;
+    ti.p[k] = (int16_t)term_idx[k];
+  }
+  const RingDev R = make_ring(ring);
+  const size_t pairs = ((size_t)rows << R.log_n) / 2;
+  if (!pairs) return 0;
+  k_pt_mac<<<grid_for(pairs, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, x0, stack, (size_t)stack_stride, ti, pts, (size_t)pt_stride, n_terms, pairs,
+      (int)R.log_n, (unsigned)limbs, R, lm);
   return finish();
 }
 
@@ -1122,7 +1214,6 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   if (!make_map(lm, limb_prime, limbs) || !make_map(em, ext_prime, ext_limbs)) return CKB_E_LIMBS;
   if (alpha < 1 || alpha > 16 || ext_limbs < limbs || batch < 0) return CKB_E_ARG;
   if (alpha > 1 && !bconv) return CKB_E_ARG;
-  if (skip_own && limbs % alpha != 0) return CKB_E_ARG;
   for (int i = 0; i < limbs; ++i)
     if (lm.p[i] != em.p[i]) return CKB_E_ARG;
   const RingDev R = make_ring(ring);
@@ -1130,7 +1221,10 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   const size_t total = (size_t)batch << R.log_n;
   if (!total || !nd) return 0;
   const size_t bstride = in_batch_stride > 0 ? (size_t)in_batch_stride : ((size_t)limbs << R.log_n);
+  // per-digit row stride; a short last digit (skip_own) keeps ext - width rows
   const int out_rows = skip_own ? ext_limbs - alpha : ext_limbs;
+  const int item_rows = skip_own ? (nd - 1) * out_rows + ext_limbs - (limbs - (nd - 1) * alpha)
+                                 : nd * ext_limbs;
   // exact digit width (a rounded-up template would multiply by zero constants)
   using KernT = decltype(&k_modup<1>);
   static const KernT kerns[17] = {nullptr,       k_modup<1>,  k_modup<2>,  k_modup<3>,
@@ -1164,7 +1258,8 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
     dim3 mgrid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
                (unsigned)nd);
     mkerns[alpha]<<<mgrid, 256, msmem, (cudaStream_t)stream>>>(
-        out, in, bstride, batch, limbs, ext_limbs, alpha, nd, out_rows, skip_own, (int)R.log_n,
+        out, in, bstride, batch, limbs, ext_limbs, alpha, item_rows, out_rows, skip_own,
+        (int)R.log_n,
         R, lm, em, bconv);
     return finish();
   }
@@ -1174,7 +1269,8 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
             (unsigned)nd);
   kern<<<grid, 256, smem, (cudaStream_t)stream>>>(out, in, bstride, batch, limbs, ext_limbs,
-                                                   alpha, nd, out_rows, skip_own, (int)R.log_n,
+                                                   alpha, item_rows, out_rows, skip_own,
+                                                   (int)R.log_n,
                                                    R, lm, em, bconv);
   return finish();
 }
@@ -1188,18 +1284,21 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
   if (!make_map(em, ext_prime, ext_limbs) || !make_map(km, key_limb, ext_limbs))
     return CKB_E_LIMBS;
   if (batch < 0 || n_digits < 1 || (!key && !key_ptrs) || alpha < 1) return CKB_E_ARG;
-  if (own && limbs % alpha != 0) return CKB_E_ARG;
+  if (own && (limbs > n_digits * alpha || limbs <= (n_digits - 1) * alpha)) return CKB_E_ARG;
   for (int e = 0; e < ext_limbs; ++e) od.p[e] = (int16_t)(e < limbs ? e / alpha : -1);
   const RingDev R = make_ring(ring);
   const size_t total = ((size_t)batch * ext_limbs) << R.log_n;
   if (!total) return 0;
-  const int out_rows = own ? ext_limbs - alpha : ext_limbs;
+  const int out_rows = own ? ext_limbs - alpha : ext_limbs;  // as written by ckb_modup
+  const int item_rows = own ? (n_digits - 1) * out_rows + ext_limbs - (limbs - (n_digits - 1) * alpha)
+                            : n_digits * ext_limbs;
   const size_t ob = own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << R.log_n);
   const int grid = grid_for(total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
 #define CKB_KS(ND)                                                                           \
   k_ks_inner<ND><<<grid, 256, 0, st>>>(acc, digits, batch, n_digits, ext_limbs, out_rows,   \
-                                       alpha, own, ob, (int)R.log_n, key, key_ptrs,         \
+                                       item_rows, alpha, limbs, own, ob, (int)R.log_n, key, \
+                                       key_ptrs,                                            \
                                        key_limbs, R, em, km, od)
   switch (n_digits) {
     case 1: CKB_KS(1); break;
@@ -1211,7 +1310,8 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
     case 8: CKB_KS(8); break;
     default:
       k_ks_inner_any<<<grid_for(total, 256), 256, 0, st>>>(
-          acc, digits, batch, n_digits, ext_limbs, out_rows, alpha, own, ob, (int)R.log_n, key,
+          acc, digits, batch, n_digits, ext_limbs, out_rows, item_rows, alpha, limbs, own, ob,
+          (int)R.log_n, key,
           key_ptrs, key_limbs, R, em, km, od);
       break;
   }

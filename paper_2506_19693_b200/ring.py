@@ -224,6 +224,22 @@ class GpuChain:
             "ntt_inverse"), self._f64_share(lm, limbs))
         return t
 
+    def ntt_from(self, src: torch.Tensor, items: int, limbs: int, item_stride: int,
+                 inverse: bool = False, lmap=None, out=None):
+        """Out-of-place (i)NTT of `items` items of [limbs][N] read at
+        src + i*item_stride elements (a strided view, e.g. one component of a
+        [B, 3, limbs, N] tensor) into a fresh contiguous [items, limbs, N]."""
+        out = out if out is not None else torch.empty(items, limbs, self.n, dtype=U64,
+                                                      device=self.device)
+        rows = items * limbs
+        lm = lmap or self.q_map(limbs)
+        fn = nat.LIB.ckb_ntt_inverse_from if inverse else nat.LIB.ckb_ntt_forward_from
+        _run("intt" if inverse else "ntt", 2 * rows * self.n * W, self._ntt_launches(rows),
+             lambda: nat.check(fn(self.ring_p, nat.ptr(out), nat.ptr(src), item_stride, rows,
+                                  limbs, lm, nat.stream_handle()), "ntt_from"),
+             self._f64_share(lm, limbs))
+        return out
+
     def ew(self, op: int, out, a, b=None, c=None, limbs: int = 0, lmap=None, b_rows: int = 0):
         rows = a.numel() >> self.log_n
         nb = 2 * rows + (0 if b is None else (b_rows or rows)) + (0 if c is None else rows)
@@ -231,6 +247,23 @@ class GpuChain:
             self.ring_p, op, nat.ptr(out), nat.ptr(a), nat.ptr(b) if b is not None else None,
             nat.ptr(c) if c is not None else None, rows, limbs, lmap or self.q_map(limbs), b_rows,
             nat.stream_handle()), "elementwise"))
+        return out
+
+    def pt_mac(self, x0, stack, term_idx, pts, limbs: int, out=None, lmap=None):
+        """sum_t X_t (.) pts[t] (ckb_pt_mac): X_t = x0 for term_idx[t] == -1, else
+        stack[term_idx[t]]; every X_t shaped like x0 ([..., limbs, N]); pts
+        [T, limbs, N] broadcast over the leading rows."""
+        ref = x0 if x0 is not None else stack[0]
+        out = out if out is not None else torch.empty_like(ref)
+        rows = ref.numel() >> self.log_n
+        t = len(term_idx)
+        sst = stack[0].numel() if stack is not None else 0
+        nb = t * rows + t * limbs + rows
+        _run("pt_mac", nb * self.n * W, 1, lambda: nat.check(nat.LIB.ckb_pt_mac(
+            self.ring_p, nat.ptr(out), nat.ptr(x0) if x0 is not None else None,
+            nat.ptr(stack) if stack is not None else None, sst, nat.i32_array(term_idx),
+            nat.ptr(pts), limbs * self.n, t, rows, limbs, lmap or self.q_map(limbs),
+            nat.stream_handle()), "pt_mac"))
         return out
 
     def add(self, a, b, limbs, out=None, lmap=None):
@@ -267,15 +300,16 @@ class GpuChain:
     def modup(self, d, m: int, alpha: int, bconv, batch: int = None, in_batch_stride: int = 0,
               skip_own: bool = False, out=None):
         """d: batch items of [m][N] (item b at d + b*in_batch_stride elements).
-        Returns digits [batch, nd, rows, N], rows = ext (or ext - alpha with skip_own)."""
+        Returns digits [batch, rows, N]: nd * ext rows, or with skip_own the
+        compact layout without each digit's own limbs (len(digit_basis(...)) rows;
+        a short last digit keeps ext - width rows)."""
         if batch is None:
             batch = d.numel() // (m * self.n)
         ext = m + self.k
-        nd = -(-m // alpha)
-        rows = ext - alpha if skip_own else ext
-        out = out if out is not None else torch.empty(batch, nd, rows, self.n, dtype=U64,
+        rows = len(self.digit_basis(m, alpha, True)) if skip_own else -(-m // alpha) * ext
+        out = out if out is not None else torch.empty(batch, rows, self.n, dtype=U64,
                                                       device=self.device)
-        _run("modup", (batch * m + batch * nd * rows) * self.n * W, 1, lambda: nat.check(
+        _run("modup", (batch * m + batch * rows) * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), in_batch_stride, batch,
                               m, self.q_map(m), ext, self.ext_map(m), alpha,
                               nat.ptr(bconv) if bconv is not None else None, int(skip_own),
@@ -297,13 +331,16 @@ class GpuChain:
     def ks_inner(self, digits, m: int, alpha: int = 1, key: torch.Tensor = None,
                  key_ptrs: torch.Tensor = None, own: torch.Tensor = None, own_bstride: int = 0,
                  out=None):
-        batch, nd = digits.shape[0], digits.shape[1]
+        """digits: ckb_modup's output ([batch, rows, N]; skip_own layout when own
+        is given)."""
+        batch = digits.shape[0]
+        nd = -(-m // alpha)
         ext = m + self.k
         out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
                                                       device=self.device)
         key_limbs = len(self.all_primes)
         n_keys = batch if key_ptrs is not None else 1
-        nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext
+        nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext  # own rows counted as read
         _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
                                  self.ext_map(m), alpha, m,
@@ -385,13 +422,15 @@ class GpuChain:
             addend_stride = addend_polys
         has_add = addend is not None and n2 > 0
         trows = n1 + n2 + (n2 if has_add else 0)
-        T = torch.empty(polys, trows, n, dtype=U64, device=self.device)
-        xv = x.as_strided((polys, n1 + n2, n), (xs, n, 1), x.storage_offset() + m2 * n)
-        T[:, : n1 + n2].copy_(xv)
-        if has_add:
-            T[:, n1 + n2:].copy_(addend_tail)
         tbasis = tuple(basis[m2:]) + (tuple(basis[m2:m1]) if has_add else ())
-        self.ntt_inv(T, trows, self.cmap(tbasis))
+        xv = x.as_strided((polys, n1 + n2, n), (xs, n, 1), x.storage_offset() + m2 * n)
+        if has_add:
+            T = torch.empty(polys, trows, n, dtype=U64, device=self.device)
+            T[:, : n1 + n2].copy_(xv)
+            T[:, n1 + n2:].copy_(addend_tail)
+            self.ntt_inv(T, trows, self.cmap(tbasis))
+        else:  # the dropped limbs transformed straight out of x (no staging copy)
+            T = self.ntt_from(xv, polys, trows, xs, inverse=True, lmap=self.cmap(tbasis))
         t1, t2 = self.drop_tables(basis, n1, n2)
         tE = self.corr_table(basis, n1, n2)
         E = torch.empty(polys, m2, n, dtype=U64, device=self.device)

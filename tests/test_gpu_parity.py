@@ -103,6 +103,67 @@ def test_ntt_big_primes_vs_oracle_and_roundtrip(logn, bits):
     assert int(_u64(f).max()) < p
 
 
+@pytest.mark.parametrize("logn", [12, 16])
+def test_ntt_out_of_place_matches_in_place(logn):
+    """ckb_ntt_{forward,inverse}_from on a strided component view (items of
+    [3][m][N], FP64-path and integer-path primes mixed) equals the in-place
+    transform of a contiguous copy, and leaves the source untouched."""
+    n = 1 << logn
+    params = SchemeParams(poly_degree=n, modulus_chain=(60, 40, 40, 60), scale_bits=40, level=2)
+    ch = GpuChain(params, layout="baseline")
+    m, b = 3, 5
+    rng = np.random.default_rng(logn)
+    x_np = np.stack([np.stack([np.stack([rng.integers(0, p, n, dtype=np.uint64)
+                                         for p in ch.all_primes[:m]]) for _ in range(3)])
+                     for _ in range(b)])
+    x = torch.from_numpy(x_np).cuda()
+    for inverse in (False, True):
+        got = ch.ntt_from(x[:, 1], b, m, 3 * m * n, inverse=inverse)
+        want = x[:, 1].contiguous()
+        (ch.ntt_inv if inverse else ch.ntt_fwd)(want, m)
+        assert torch.equal(got, want)
+    assert np.array_equal(_u64(x), x_np)
+
+
+def test_pt_mac_equals_mul_add_chain():
+    """ckb_pt_mac (the BSGS row of bootstrapping) equals the mul_pt / add_ct
+    chain it replaces, bit for bit, with terms from x0 and from a stack, and
+    the broadcast elementwise kernels equal numpy on odd row counts."""
+    n = 1 << 12
+    params = SchemeParams(poly_degree=n, modulus_chain=(60, 40, 45, 60), scale_bits=40, level=2)
+    ch = GpuChain(params, layout="baseline")
+    m, b, nst = 3, 3, 5
+    rng = np.random.default_rng(11)
+    primes = ch.all_primes[:m]
+
+    def rand(*lead):
+        return torch.from_numpy(np.stack([rng.integers(0, p, (*lead, n), dtype=np.uint64)
+                                          for p in primes], axis=-2)).cuda()
+
+    x0 = rand(b, 2)
+    stack = rand(nst, b, 2)
+    idx = [-1, 3, 0, 4, 4, -1, 1]
+    pts = rand(len(idx))
+    got = ch.pt_mac(x0, stack, idx, pts, m)
+    want = None
+    for t, k in enumerate(idx):
+        term = ch.mul(x0 if k < 0 else stack[k], pts[t], m, b_rows=m)
+        want = term if want is None else ch.add(want, term, m)
+    assert torch.equal(got, want)
+    # elementwise against numpy (object ints): mul with a broadcast plaintext
+    a_np, p_np = _u64(x0[0]), _u64(pts[0])
+    prod = _u64(ch.mul(x0[0], pts[0], m, b_rows=m))
+    for c in range(2):
+        for j, p in enumerate(primes):
+            w = (a_np[c, j].astype(object) * p_np[j].astype(object)) % p
+            assert np.array_equal(prod[c, j], w.astype(np.uint64))
+    s_, b_np = _u64(ch.sub(x0[1], x0[0], m)), _u64(x0[1])
+    for c in range(2):
+        for j, p in enumerate(primes):
+            w = (b_np[c, j].astype(object) - a_np[c, j].astype(object)) % p
+            assert np.array_equal(s_[c, j], w.astype(np.uint64))
+
+
 def test_ntt_product_matches_schoolbook_60bit():
     n = 32
     p = O.largest_ntt_prime_below(60, 2 * n, set())
@@ -281,7 +342,8 @@ def test_rbky_reference_key_file_round_trip(ck_gold):
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("dnum,level,special", [(None, 3, 60), (2, 3, 120), (3, 5, 300)])
+@pytest.mark.parametrize("dnum,level,special", [(None, 3, 60), (2, 3, 120), (3, 5, 300),
+                                                  (1, 3, 240)])
 def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
     """(3, 5, 300): 5 special primes, so ModDown with the fused rescale drops
     5 + 1 primes (k_divround_corr<6, 1>)."""

@@ -1,0 +1,14 @@
+"""Print the headline numbers of a bench.py log (the last JSON line)."""
+import json
+import sys
+
+line = [ln for ln in open(sys.argv[1]) if ln.startswith("{")][-1]
+d = json.loads(line)
+print("c2 %.1f GB/s  hmult %.1f us/ct  hrot %.1f us/ct  stages %s" % (
+    d["value"], d["hmult_us_per_ct"], d["hrot_us_per_ct"],
+    {k: round(v, 2) for k, v in d["stages_ms"].items()}))
+print("kernels", {k: round(v["ms_per_step"], 2) for k, v in d["kernels"].items()})
+print("roofline frac %.3f alu %.3f | e2e %.1f | c1 %.2f ms | c3 %.1f ms | c4 %.0f ms | c5 %.0f ms | clocks %s" % (
+    d["roofline"]["frac"], d["roofline"]["alu"]["frac"], d["e2e"]["value"],
+    d["c1_train"]["ms_per_step"], d["c3_bootstrap"]["ms"], d["c4_train"]["ms_per_step"],
+    d["c5_train"]["ms_per_step"], d["clocks"]))

@@ -25,6 +25,10 @@ x = getattr(ct, "payload", ct)
 torch.cuda.synchronize(); t0 = time.perf_counter(); be.bootstrap_ct(x); torch.cuda.synchronize()
 print("one bootstrap ms", 1e3 * (time.perf_counter() - t0))
 ring.TIMER = ring.KernelTimer()
+be.bootstrap_ct(x)
+bs = ring.TIMER.summary(); ring.TIMER = None
+print("bootstrap kernels", json.dumps({k: [round(d["ms"], 2), round(d["f64_bytes"] / max(d["bytes"], 1), 2)] for k, d in sorted(bs.items(), key=lambda x: -x[1]["ms"])}))
+ring.TIMER = ring.KernelTimer()
 cust.backend._enc_cache.clear()
 torch.cuda.synchronize(); t0 = time.perf_counter()
 ex.run(dict(env), only_after_setup=True)
@@ -32,4 +36,4 @@ torch.cuda.synchronize(); wall = 1e3 * (time.perf_counter() - t0)
 summ = ring.TIMER.summary(); ring.TIMER = None
 tot = sum(d["ms"] for d in summ.values())
 print(json.dumps({"wall_ms": wall, "kernel_ms": tot, "launches": sum(d["launches"] for d in summ.values()),
-                  "kernels": {k: round(d["ms"], 1) for k, d in sorted(summ.items(), key=lambda x: -x[1]["ms"])}}))
+                  "kernels": {k: [round(d["ms"], 1), round(d["f64_bytes"] / max(d["bytes"], 1), 2)] for k, d in sorted(summ.items(), key=lambda x: -x[1]["ms"])}}))

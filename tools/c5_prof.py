@@ -23,4 +23,4 @@ torch.cuda.synchronize(); wall = 1e3 * (time.perf_counter() - t0)
 summ = ring.TIMER.summary(); ring.TIMER = None
 print(json.dumps({"wall_ms": wall, "kernel_ms": sum(d["ms"] for d in summ.values()),
                   "launches": sum(d["launches"] for d in summ.values()),
-                  "kernels": {k: round(d["ms"], 1) for k, d in sorted(summ.items(), key=lambda x: -x[1]["ms"])}}))
+                  "kernels": {k: [round(d["ms"], 1), round(d["f64_bytes"] / max(d["bytes"], 1), 2)] for k, d in sorted(summ.items(), key=lambda x: -x[1]["ms"])}}))
