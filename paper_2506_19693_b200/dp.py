@@ -126,7 +126,7 @@ class DataParallelExecutor(WaveExecutor):
         plan = self.plan
         rank = self.rank
         env = {} if env is None else {k: getattr(v, "payload", v) for k, v in env.items()}
-        keep = set(self.prog.outputs)
+        keep = self.prog.keep
         last = self.prog._last_use
         slots = be.params.slot_count
         pts = self.prog.plaintexts

@@ -88,7 +88,7 @@ class WaveExecutor:
         # weights): deferred to one final wave and run as a single batch (each
         # input is first brought to level 0, where bootstrapping starts anyway)
         if be.real_bootstrap:
-            bs = [i for i, op in enumerate(ops) if op[0] == "bs"]
+            bs = [i for i, op in enumerate(ops) if op[0] == "bs" and i >= self.n_setup]
             consumed = {x for op in ops for x in _inputs(op)}
             if len(bs) > 1 and not any(ops[i][1] in consumed for i in bs):
                 last_d = max(waves) + 1
@@ -115,7 +115,7 @@ class WaveExecutor:
         for j, op in enumerate(ops):
             for x in _inputs(op):
                 readers[x].append(j)
-        keep = set(self.prog.outputs)
+        keep = self.prog.keep
         self.fuse = {}
         for i, op in enumerate(ops):
             if op[0] != "rot":
@@ -140,7 +140,7 @@ class WaveExecutor:
         be = self.be
         ops = self.prog.ops
         env = {} if env is None else {k: getattr(v, "payload", v) for k, v in env.items()}
-        keep = set(self.prog.outputs)
+        keep = self.prog.keep
         last = self.prog._last_use
         slots = be.params.slot_count
         pts = self.prog.plaintexts
@@ -208,7 +208,7 @@ class WaveExecutor:
         own serial — so the results equal refreshing one at a time."""
         be = self.be
         ops = self.prog.ops
-        keep = set(self.prog.outputs)
+        keep = self.prog.keep
         last = self.prog._last_use
         order = sorted(self.deferred)
         if not order:

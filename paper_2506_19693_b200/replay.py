@@ -19,21 +19,48 @@ from .he_api import make_plain
 
 
 class Program:
-    def __init__(self, ops, plaintexts: np.ndarray, outputs, n_setup: int = 0):
+    def __init__(self, ops, plaintexts: np.ndarray, outputs, n_setup: int = 0, carry=()):
+        """carry: ids a later program (the next training step) reads; kept
+        alive like the outputs."""
         self.ops = ops
         self.plaintexts = plaintexts
         self.outputs = [int(o) for o in outputs]
         self.n_setup = int(n_setup)
+        self.carry = {int(c) for c in carry}
         last = {}
         for i, op in enumerate(ops):
             for ref in _inputs(op):
                 last[ref] = i
         self._last_use = last
 
+    @property
+    def keep(self) -> set:
+        """Ids kept alive past their last use: the outputs and the carry."""
+        return set(self.outputs) | self.carry
+
     @classmethod
     def load(cls, path: str) -> "Program":
+        """The recorded step (setup ops, then one train_iteration).  Traces with
+        a second iteration (ops_step2) keep the values it reads alive."""
         z = np.load(path)
-        return cls(json.loads(str(z["ops"])), z["plaintexts"], z["outputs"], int(z["n_setup"][0]))
+        ops = json.loads(str(z["ops"]))
+        carry = ()
+        if "ops_step2" in z:
+            ops2 = json.loads(str(z["ops_step2"]))
+            defined = {_output(op) for op in ops2}
+            carry = {x for op in ops2 for x in _inputs(op)} - defined
+        return cls(ops, z["plaintexts"], z["outputs"], int(z["n_setup"][0]), carry)
+
+    @classmethod
+    def load_step2(cls, path: str) -> "Program":
+        """The trace's second train_iteration (the steady state: weights and
+        velocities refreshed to the refresh level by step 1's bootstraps) as a
+        program whose "setup" is everything before it: run it with
+        only_after_setup on the environment step 1 leaves."""
+        z = np.load(path)
+        ops = json.loads(str(z["ops"]))
+        ops2 = json.loads(str(z["ops_step2"]))
+        return cls(ops + ops2, z["plaintexts"], z["outputs_step2"], len(ops))
 
     def run(self, custodian, start: int = 0, stop: int = None, env: dict = None) -> dict:
         ev = custodian.evaluator
@@ -41,7 +68,7 @@ class Program:
         bits = float(custodian.params.scale_bits)
         pts = {}
         env = {} if env is None else env
-        keep = set(self.outputs)
+        keep = self.keep
         stop = len(self.ops) if stop is None else stop
 
         def pt(i):
@@ -68,6 +95,10 @@ class Program:
                 if self._last_use.get(ref) == i and ref not in keep:
                     env.pop(ref, None)
         return env
+
+
+def _output(op):
+    return op[2] if op[0] == "ew" else op[1]
 
 
 def _inputs(op):

@@ -276,7 +276,7 @@ def make_c1_trace(with_ckks: bool):
     print("c1 trace ops:", kinds, "plaintexts:", len(pts))
 
 
-def make_c4_trace():
+def make_c4_trace(lr: float = 0.005):
     """Config 4 with the survey's substitution: 196-feature
     14x14 inputs (pixels U[0,1]), 196->128->10, 10 uniform random classes,
     batch 128, N=2^16, L = tau(1) + 16 = 24 with bootstrap_depth 16, Xavier
@@ -341,7 +341,9 @@ def make_c4_trace():
     sb.SimBackend = Recording
     try:
         cust = keygen(params, required_rotations(shape), backend="sim")
-        hyper = Hyperparams(learning_rate=0.05, momentum=0.9, iterations=1, batch_size=bsz)
+        # lr 0.005 (as config 5): with 0.05 the exact model's second step already
+        # diverges (classifier velocity ~5e6), far outside what CKKS can carry
+        hyper = Hyperparams(learning_rate=lr, momentum=0.9, iterations=1, batch_size=bsz)
         model = build_model(arch, params, hyper, cust)
         blk = model.blocks[0]
         blk.layer_weights = encrypt_packed(cust, pack(w1, layer_format(blk.kind), shape))
@@ -349,14 +351,24 @@ def make_c4_trace():
         n_setup = len(ops)
         batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(bsz)]
         train_iteration(model, batch, cust, 1)
+        b = model.blocks[0]
+        state = (b.layer_weights, b.classifier_weights, b.layer_velocity, b.classifier_velocity)
+        outs = [ids[pm.payload.serial] for pm in state]
+        sim_w = np.stack([cust.decrypt(pm.payload).values for pm in state])
+        # step 2 (steady state: the refreshed weights and velocities sit at the
+        # refresh level) on the next minibatch of the same generator
+        s2 = len(ops)
+        x2 = rng.uniform(0, 1, size=(bsz, 196))
+        onehot2 = np.eye(10)[rng.integers(0, 10, bsz)]
+        batch2 = [prepare_sample(x2[i], onehot2[i], shape, cust) for i in range(bsz)]
+        train_iteration(model, batch2, cust, 2)
+        state = (b.layer_weights, b.classifier_weights, b.layer_velocity, b.classifier_velocity)
+        outs2 = [ids[pm.payload.serial] for pm in state]
+        sim_w2 = np.stack([cust.decrypt(pm.payload).values for pm in state])
     finally:
         sb.SimBackend = orig
-    b = model.blocks[0]
-    outs = [ids[pm.payload.serial] for pm in (b.layer_weights, b.classifier_weights,
-                                              b.layer_velocity, b.classifier_velocity)]
-    sim_w = np.stack([cust.decrypt(pm.payload).values
-                      for pm in (b.layer_weights, b.classifier_weights,
-                                 b.layer_velocity, b.classifier_velocity)])
+    ops2 = ops[s2:]
+    ops = ops[:s2]
     pt_arr = np.zeros((len(pts), shape.slots))
     for k, i in pts.items():
         pt_arr[i] = np.frombuffer(k, dtype=np.float64)
@@ -364,7 +376,8 @@ def make_c4_trace():
                         n_setup=np.array([n_setup]), plaintexts=pt_arr, outputs=np.array(outs),
                         rotations=np.array(sorted(required_rotations(shape))),
                         params=np.array([n, params.level, 45, 16]), sim_weights=sim_w,
-                        grid=np.array([shape.r, shape.c]))
+                        grid=np.array([shape.r, shape.c]), ops_step2=np.array(json.dumps(ops2)),
+                        outputs_step2=np.array(outs2), sim_weights_step2=sim_w2)
     kinds = {}
     for op in ops:
         key = op[1] if op[0] == "ew" else op[0]
@@ -452,14 +465,28 @@ def make_c5_trace(init_scale: float = 0.25, lr: float = 0.005, out: str = "c5_tr
         n_setup = len(ops)
         batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(bsz)]
         train_iteration(model, batch, cust, 1)
+
+        def state():
+            o, w = [], []
+            for b in model.blocks:
+                for pm in (b.layer_weights, b.classifier_weights, b.layer_velocity,
+                           b.classifier_velocity):
+                    o.append(ids[pm.payload.serial])
+                    w.append(cust.decrypt(pm.payload).values)
+            return o, w
+
+        outs, sim_w = state()
+        # step 2 (steady state, refreshed weights) on the next minibatch
+        s2 = len(ops)
+        x2 = rng.normal(0, 1, size=(bsz, 64))
+        onehot2 = np.eye(2)[np.argmax(np.tanh(x2 @ t1) @ t2, axis=1)]
+        batch2 = [prepare_sample(x2[i], onehot2[i], shape, cust) for i in range(bsz)]
+        train_iteration(model, batch2, cust, 2)
+        outs2, sim_w2 = state()
     finally:
         sb.SimBackend = orig
-    outs, sim_w = [], []
-    for b in model.blocks:
-        for pm in (b.layer_weights, b.classifier_weights, b.layer_velocity,
-                   b.classifier_velocity):
-            outs.append(ids[pm.payload.serial])
-            sim_w.append(cust.decrypt(pm.payload).values)
+    ops2 = ops[s2:]
+    ops = ops[:s2]
     pt_arr = np.zeros((len(pts), shape.slots))
     for k, i in pts.items():
         pt_arr[i] = np.frombuffer(k, dtype=np.float64)
@@ -467,7 +494,8 @@ def make_c5_trace(init_scale: float = 0.25, lr: float = 0.005, out: str = "c5_tr
                         n_setup=np.array([n_setup]), plaintexts=pt_arr, outputs=np.array(outs),
                         rotations=np.array(sorted(required_rotations(shape))),
                         params=np.array([n, params.level, 45, 16]), sim_weights=np.stack(sim_w),
-                        grid=np.array([shape.r, shape.c]))
+                        grid=np.array([shape.r, shape.c]), ops_step2=np.array(json.dumps(ops2)),
+                        outputs_step2=np.array(outs2), sim_weights_step2=np.stack(sim_w2))
     kinds = {}
     for op in ops:
         key = op[1] if op[0] == "ew" else op[0]

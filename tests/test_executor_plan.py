@@ -48,3 +48,27 @@ def test_fusion_skips_rotations_with_other_readers(golden_dir):
     prog.outputs = list(prog.outputs) + [out]
     ex = WaveExecutor(prog, _stub_custodian(prog))
     assert i not in ex.fuse
+
+
+@pytest.mark.parametrize("name,n_bs", [("c4_trace.npz", 4), ("c5_trace.npz", 16)])
+def test_steady_step_program(golden_dir, name, n_bs):
+    """The recorded second train_iteration: step 1 keeps exactly the state it
+    reads (its refreshed weights and velocities), step 2 starts after step 1,
+    reads nothing else from it, and its real bootstraps are deferred into one
+    batched final wave."""
+    path = os.path.join(golden_dir, name)
+    p1 = Program.load(path)
+    p2 = Program.load_step2(path)
+    assert p1.carry == set(p1.outputs)
+    assert p2.n_setup == len(p1.ops) and p2.ops[: len(p1.ops)] == p1.ops
+    defined_before = {op[2] if op[0] == "ew" else op[1] for op in p1.ops}
+    reads = {x for op in p2.ops[p2.n_setup:] for x in _inputs(op)}
+    defined_after = {op[2] if op[0] == "ew" else op[1] for op in p2.ops[p2.n_setup:]}
+    assert (reads - defined_after) <= p1.keep and not (defined_after & defined_before)
+    ex = WaveExecutor(p2, _stub_custodian(p2, real_bootstrap=True))
+    bs = [i for i, op in enumerate(p2.ops) if op[0] == "bs" and i >= p2.n_setup]
+    assert len(bs) == n_bs and sorted(ex.waves[-1]) == bs
+    # step-2 levels start from the refresh level: every op after setup sits at
+    # or below it (the step consumes user levels only)
+    assert max(ex.level_of[op[2] if op[0] == "ew" else op[1]]
+               for op in p2.ops[p2.n_setup:] if op[0] != "enc") <= 8

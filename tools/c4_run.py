@@ -47,11 +47,51 @@ def run(reps=2, verbose=True, graph=True, special=660):
         graph_equal = bool(np.array_equal(wg, w))
     err = np.max(np.abs(w - z["sim_weights"]), axis=1)  # layer w, classifier w, velocities
     mag = np.max(np.abs(z["sim_weights"]), axis=1)
+    step1_ms = graph_ms if graph_ms is not None else 1e3 * min(times)
+    # steady state: the trace's second train_iteration, on the weights and
+    # velocities step 1 left (refreshed to the refresh level by its bootstraps)
+    if graph:
+        del gs, og
+    prog2 = Program.load_step2(path)
+    env2 = {k: out[k] for k in prog.keep}
+    del out
+    ex2 = WaveExecutor(prog2, cust)
+    t2 = []
+    for rep in range(reps):
+        cust.backend._enc_cache.clear()
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        out2 = ex2.run(dict(env2), only_after_setup=True)
+        torch.cuda.synchronize(); t2.append(time.perf_counter() - t0)
+    w2 = np.stack([cust.backend._decrypt_values(out2[o]) for o in prog2.outputs])
+    step2_ms = 1e3 * min(t2)
+    step2_eager_ms = step2_ms
+    if graph:
+        del out2
+        gs2 = GraphedStep(ex2, env2, warmup=1)
+        g2 = []
+        for rep in range(reps):
+            torch.cuda.synchronize(); t0 = time.perf_counter()
+            og2 = gs2.step()
+            torch.cuda.synchronize(); g2.append(time.perf_counter() - t0)
+        wg2 = np.stack([cust.backend._decrypt_values(og2[o]) for o in prog2.outputs])
+        graph_equal = graph_equal and bool(np.array_equal(wg2, w2))
+        step2_ms = 1e3 * min(g2)
+    err2 = np.max(np.abs(w2 - z["sim_weights_step2"]), axis=1)
     res_graph = {} if graph_ms is None else {
-        "ms_per_step_eager_waves": 1e3 * min(times), "graph_weights_equal_eager": graph_equal,
-        "timing": "ms_per_step: the whole step (4 real bootstraps included) as one CUDA graph "
-                  "replay, every plaintext re-encoded; wall clock, device sync on both sides"}
-    return {"ms_per_step": graph_ms if graph_ms is not None else 1e3 * min(times), **res_graph,
+        "ms_per_step_eager_waves": (1e3 * min(times) + 7 * step2_eager_ms) / 8,
+        "graph_weights_equal_eager": graph_equal,
+        "timing": "ms_per_step: mean over the 8 steps of BASELINE config 4 = (step 1 + 7 x "
+                  "steady step) / 8; each step (4 real bootstraps included) one CUDA graph "
+                  "replay, every plaintext re-encoded, samples freshly encrypted; wall clock, "
+                  "device sync on both sides"}
+    return {"ms_per_step": (step1_ms + 7 * step2_ms) / 8, **res_graph, "steps": 8,
+            "step1_ms": step1_ms, "steady_step_ms": step2_ms,
+            "steady_note": "step 1 runs on freshly encrypted top-level weights (levels 24..17, "
+                           "the 60-bit bootstrap primes still present); steps 2..8 on the "
+                           "refreshed weights at the refresh level (levels 8..1): the recorded "
+                           "second train_iteration (tests/golden/c4_trace.npz ops_step2)",
+            "step2_weights_max_abs_err_vs_sim": float(err2[:2].max()),
+            "step2_velocities_max_abs_err_vs_sim": float(err2[2:].max()),
             "first_step_ms": 1e3 * times[0], "ops": len(prog.ops) - prog.n_setup,
             "waves": len(ex.waves), "bootstraps_per_step": 4, "keygen_s": keygen_s,
             "weights_max_abs_err_vs_sim": float(err[:2].max()),

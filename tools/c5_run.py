@@ -42,7 +42,33 @@ def run(reps=1, max_group=64, verbose=True, special=780):
     err = np.max(np.abs(w - ref), axis=1)
     mag = np.max(np.abs(ref), axis=1)
     kind = np.arange(len(prog.outputs)) % 4  # per block: layer w, classifier w, velocities
-    return {"ms_per_step": 1e3 * min(times), "first_step_ms": 1e3 * times[0],
+    # steady state: the trace's second train_iteration on step 1's refreshed state
+    prog2 = Program.load_step2(path)
+    env2 = {k: out[k] for k in prog.keep}
+    del out
+    ex2 = WaveExecutor(prog2, cust, max_group=max_group)
+    t2 = []
+    for rep in range(reps):
+        cust.backend._enc_cache.clear()
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        out2 = ex2.run(dict(env2), only_after_setup=True)
+        torch.cuda.synchronize(); t2.append(time.perf_counter() - t0)
+        if verbose:
+            print(f"steady step {rep}: {t2[-1]*1e3:.1f} ms", flush=True)
+    w2 = np.stack([cust.backend._decrypt_values(out2[o]) for o in prog2.outputs])
+    err2 = np.max(np.abs(w2 - z["sim_weights_step2"]), axis=1)
+    step1_ms, step2_ms = 1e3 * min(times), 1e3 * min(t2)
+    return {"ms_per_step": (step1_ms + 4 * step2_ms) / 5, "steps": 5, "step1_ms": step1_ms,
+            "steady_step_ms": step2_ms,
+            "timing": "ms_per_step: mean over the 5 steps of BASELINE config 5 = (step 1 + 4 x "
+                      "steady step) / 5; eager wave executor, every plaintext re-encoded, samples "
+                      "freshly encrypted; wall clock, device sync on both sides",
+            "steady_note": "step 1 runs on freshly encrypted top-level weights; steps 2..5 on "
+                           "the refreshed weights at the refresh level: the recorded second "
+                           "train_iteration (tests/golden/c5_trace.npz ops_step2)",
+            "step2_weights_max_abs_err_vs_sim": float(err2[kind < 2].max()),
+            "step2_velocities_max_abs_err_vs_sim": float(err2[kind >= 2].max()),
+            "first_step_ms": 1e3 * times[0],
             "ops": len(prog.ops) - prog.n_setup, "waves": len(ex.waves),
             "bootstraps_per_step": int(sum(1 for o in prog.ops if o[0] == "bs")),
             "keygen_s": keygen_s, "max_group": max_group,
