@@ -183,11 +183,22 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
  * n2 rows = addend limbs [limbs-n1-n2, limbs-n1); all coefficient domain.
  * tab1/tab2 as for ckb_divround; tabE: DEVICE [m2][n1+n2+1][2] {M1_u*P1^-1 mod q_j, shoup},
  * then {M2_u mod q_j, shoup}, then {C_j, 0} with C_j a multiple of q_j in [2^59, 2^61) (every r_u + C_j >= 0 and < 2^61).
- * E: [polys][m2][N], coefficient domain (NTT it next). */
+ * E: [polys][m2][N], coefficient domain (NTT it next).
+ * tabH (optional, used when n_drop1 >= 6 and n_drop2 <= 2): DEVICE [m1][n1]
+ * {p_u^-1 mod q_j} for the kept limbs j < m1 = limbs - n_drop1, then [n1][2]
+ * {(P1/p_u)^-1 mod p_u, shoup} for the dropped limbs u (drop order, u = 0 the
+ * last limb).  The first chain's centred residue then comes from one fast
+ * basis conversion, c1 = sum_u y_u (P1/p_u) - rho P1 with rho = round(sum y_u/p_u)
+ * in FP64; coefficients whose rounding is within 2^-30 of ambiguous take the
+ * mixed-radix path, so E is bit-identical either way. */
+/* Test hook: the |frac(sum y_u/p_u) - 1/2| margin below which ckb_divround_ntt_corr
+ * settles rho exactly (default 0.5 - 2^-30; 0 sends every coefficient through
+ * the exact path).  Process-global; returns CKB_E_ARG outside [0, 0.5]. */
+int ckb_debug_hps_margin(double margin);
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
                           int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
-                          const uint64_t* tabE, void* stream);
+                          const uint64_t* tabE, const uint64_t* tabH, void* stream);
 /* NTT-domain divide-and-round, step 2: out_j = (x_j * P1^-1 + add_j - E_j) * P2^-1 with x,
  * addend and E (after its forward NTT) in the NTT domain; addend addressing as ckb_divround. */
 int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t* x,

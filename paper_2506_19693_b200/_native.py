@@ -82,8 +82,9 @@ def _load():
                               c_vp, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_from_i64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_to_f64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_debug_hps_margin": ([ctypes.c_double], ctypes.c_int),
         "ckb_divround_ntt_corr": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p,
-                                   ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, c_vp],
+                                   ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp],
                                   ctypes.c_int),
         "ckb_divround_ntt_combine": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int,
@@ -119,7 +120,7 @@ EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inver
             "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
             "ckb_elementwise", "ckb_pt_mac", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
-            "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
+            "ckb_debug_hps_margin", "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
             "ckb_automorphism_ntt",
             "ckb_reduce", "ckb_sample", "ckb_alu_probe",
             "ckb_alu_probe_f64")

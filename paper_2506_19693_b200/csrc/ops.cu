@@ -467,6 +467,12 @@ __global__ void __launch_bounds__(256) k_ks_inner_any(
 // ===========================================================================
 
 constexpr int kMaxDrop = 16;
+// first-drop width from which the correction takes the fast basis-conversion
+// form (k_divround_corr_hps) when the caller passes its table
+constexpr int kHpsMinDrop = 6;
+// |frac - 1/2| below which rho is settled by exact_rho (tests lower it to 0 to
+// run every coefficient through the exact path)
+static double g_hps_margin = 0.5 - 0x1p-30;
 
 // acc - r * M  (mod p) for a signed centered remainder r and a Shoup constant M.
 __device__ __forceinline__ uint64_t sub_rm(uint64_t acc, int64_t r, uint64_t M, uint64_t Ms,
@@ -781,6 +787,147 @@ __global__ void __launch_bounds__(256, V == 2 ? 2 : 3) k_divround_corr(
         for (int c = 0; c < V; ++c) o[c] = ckb::reduce128_any(h[c], l[c], S[4], S[5], m);
       }
       st_v<V>(dst + (size_t)j * N, o);
+    }
+  }
+}
+
+// Wide first drops (n1 >= 6 special primes): the centred residue of x mod P1
+// from one fast basis conversion instead of the O(n1^2) mixed-radix chain.
+//   y_u = [x_u (P1/p_u)^-1]_{p_u},  S = sum_u y_u (P1/p_u),  rho = round(S/P1)
+//   c1 = S - rho P1 (the centred residue: |c1| < P1/2 since P1 is odd)
+//   E1_j = c1 P1^-1 = sum_u y_u [p_u^-1]_{q_j} - rho  (mod q_j)
+// rho = rint(sum_u y_u / p_u) in FP64 (error < 2^-47 for n1 <= 16).  When the
+// fractional part lies within 2^-30 of 1/2 (probability ~2^-29 per
+// coefficient) rho is settled exactly by exact_rho below, so the integers are
+// always the sequential chain's and the output is bit-identical.
+// tabH: [m1][n1] {p_u^-1 mod q_j} for every kept limb, then [n1][2]
+// {(P1/p_u)^-1 mod p_u, shoup}.  Smem per output row: {p, mu, k, 2p, r64,
+// r64s}, the tabE row (C_j and the r2 constants), then the tabH row.
+
+// Rare path: S/P1 = floor(f) + 1/2 +- 2^-30, so rho is floor(f) when the
+// centred residue c1 is positive and floor(f) + 1 when it is negative.  The
+// sign of c1 is that of its top nonzero centred mixed-radix digit (the digits
+// of the sequential chain, ring.py:171-183); local arrays are fine here.
+__device__ __noinline__ uint64_t exact_rho(const uint64_t* __restrict__ src, size_t N, int limbs,
+                                           int m2, int n1, double f,
+                                           const uint64_t* __restrict__ tab1, RingDev R,
+                                           const LimbMap& lm) {
+  int64_t r[kMaxDrop];
+  const int s1 = 2 * (n1 + 1);
+  int64_t top = 0;
+  for (int d = 0; d < n1; ++d) {
+    const int li = limbs - 1 - d;
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[li] * kModStride);
+    const uint64_t* Tb = tab1 + (size_t)li * s1;
+    uint64_t a = src[(size_t)(li - m2) * N];
+    for (int u = 0; u < d; ++u) a = sub_rm(a, r[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), p);
+    r[d] = centered(ckb::mul_shoup(a, __ldg(Tb + 2 * n1), __ldg(Tb + 2 * n1 + 1), p), p);
+    if (r[d] != 0) top = r[d];
+  }
+  const uint64_t fl = (uint64_t)floor(f);
+  return top > 0 ? fl : fl + 1;
+}
+
+template <int D1, int D2>
+__global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
+    uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
+    int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
+    const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE,
+    const uint64_t* __restrict__ tabH, double margin) {
+  extern __shared__ uint64_t sm[];
+  const size_t N = (size_t)1 << log_n;
+  const int m1 = limbs - n1;
+  const int m2 = m1 - n2;
+  const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2 + 1);
+  const int row_w = 6 + sE + n1;
+  for (int q = threadIdx.x; q < m2 * row_w; q += blockDim.x) {
+    const int j = q / row_w, c = q % row_w;
+    const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
+    uint64_t v;
+    if (c < 6) {
+      v = c < 4 ? __ldg(mm + c) : __ldg(mm + 4 + c);
+    } else if (c < 6 + sE) {
+      v = __ldg(tabE + (size_t)j * sE + c - 6);
+    } else {
+      v = __ldg(tabH + (size_t)j * n1 + c - 6 - sE);
+    }
+    sm[q] = v;
+  }
+  // per drop: (P1/p_u)^-1 pair, p_u and 1/p_u, after the rows
+  uint64_t* dsm = sm + (size_t)m2 * row_w;
+  double* dinv = reinterpret_cast<double*>(dsm + 3 * kMaxDrop);
+  for (int u = threadIdx.x; u < n1; u += blockDim.x) {
+    const uint64_t p = __ldg(R.mods + (size_t)lm.p[limbs - 1 - u] * kModStride);
+    dsm[3 * u] = __ldg(tabH + (size_t)m1 * n1 + 2 * u);
+    dsm[3 * u + 1] = __ldg(tabH + (size_t)m1 * n1 + 2 * u + 1);
+    dsm[3 * u + 2] = p;
+    dinv[u] = 1.0 / (double)p;
+  }
+  __syncthreads();
+  const size_t total = (size_t)polys * N;
+  const int trows = n1 + n2 + (has_add ? n2 : 0);
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = t & (N - 1);
+    const size_t pidx = t >> log_n;
+    const uint64_t* src = T + pidx * trows * N + n;
+    uint64_t y[D1];
+    double f = 0.0;
+#pragma unroll
+    for (int u = 0; u < D1; ++u) {
+      if (u < n1) {
+        y[u] = ckb::mul_shoup(src[(size_t)(limbs - 1 - u - m2) * N], dsm[3 * u], dsm[3 * u + 1],
+                              dsm[3 * u + 2]);
+        f = fma((double)y[u], dinv[u], f);
+      } else {
+        y[u] = 0;
+      }
+    }
+    const double rho_d = rint(f);
+    const uint64_t rho = fabs(f - rho_d) < margin  // 0.5 - 2^-30 (ckb_debug_hps_margin)
+                             ? (uint64_t)rho_d
+                             : exact_rho(src, N, limbs, m2, n1, f, tab1, R, lm);
+    int64_t r2[D2 > 0 ? D2 : 1];
+#pragma unroll
+    for (int d = 0; d < D2; ++d) {
+      if (d < n2) {
+        const int li = m1 - 1 - d;
+        const uint64_t* mm = R.mods + (size_t)lm.p[li] * kModStride;
+        const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+        const uint64_t* Ta = tab1 + (size_t)li * s1;
+        // (x - c1) P1^-1 = x P1^-1 - E1 at this limb
+        uint64_t v = ckb::mul_shoup(src[(size_t)(li - m2) * N], __ldg(Ta + 2 * n1),
+                                    __ldg(Ta + 2 * n1 + 1), m.p);
+        const uint64_t* H = tabH + (size_t)li * n1;
+        uint64_t h = 0, l = (m.p << (__clzll((long long)m.p) - 4)) - rho;  // + multiple of p
+#pragma unroll
+        for (int u = 0; u < D1; ++u)
+          if (u < n1) ckb::mac128(h, l, y[u], __ldg(H + u));
+        v = ckb::sub_mod(v, ckb::reduce128_any(h, l, __ldg(mm + 8), __ldg(mm + 9), m), m.p);
+        if (has_add) v = ckb::add_mod(v, src[(size_t)(n1 + n2 + li - m2) * N], m.p);
+        const uint64_t* Tb = tab2 + (size_t)li * s2;
+#pragma unroll
+        for (int u = 0; u < D2; ++u)
+          if (u < d) v = sub_rm(v, r2[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), m.p);
+        r2[d] = centered(ckb::mul_shoup(v, __ldg(Tb + 2 * n2), __ldg(Tb + 2 * n2 + 1), m.p), m.p);
+      }
+    }
+    uint64_t* dst = E + pidx * m2 * N + n;
+    for (int j = 0; j < m2; ++j) {
+      const uint64_t* S = sm + (size_t)j * row_w;
+      const uint64_t* Te = S + 6;
+      const uint64_t* H = Te + sE;
+      const int64_t off = (int64_t)Te[2 * (n1 + n2)];  // C_j: multiple of q_j in [2^59, 2^61)
+      uint64_t h = 0, l = (uint64_t)off - rho;
+#pragma unroll
+      for (int u = 0; u < D1; ++u)
+        if (u < n1) ckb::mac128(h, l, y[u], H[u]);
+#pragma unroll
+      for (int u = 0; u < D2; ++u)
+        if (u < n2) ckb::mac128(h, l, (uint64_t)(r2[u] + off), Te[2 * (n1 + u)]);
+      const Mod m{S[0], S[1], S[2], S[3]};
+      dst[(size_t)j * N] = m.k >= 32 ? ckb::reduce128_big(h, l, S[4], S[5], m)
+                                     : ckb::reduce128_any(h, l, S[4], S[5], m);
     }
   }
 }
@@ -1413,10 +1560,16 @@ int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys,
   return finish();
 }
 
+int ckb_debug_hps_margin(double margin) {
+  if (!(margin >= 0.0 && margin <= 0.5)) return CKB_E_ARG;
+  g_hps_margin = margin;
+  return 0;
+}
+
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
                           int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
-                          const uint64_t* tabE, void* stream) {
+                          const uint64_t* tabE, const uint64_t* tabH, void* stream) {
   LimbMap lm;
   if (!make_map(lm, limb_prime, limbs)) return CKB_E_LIMBS;
   if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 > kMaxDrop || n_drop2 > kMaxDrop ||
@@ -1432,6 +1585,27 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
                : n_drop1 <= 6 ? 6 : n_drop1 <= 8 ? 8 : n_drop1 <= 11 ? 11 : n_drop1 <= 13 ? 13
                : 16;
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
+  cudaStream_t st0 = (cudaStream_t)stream;
+  if (tabH && n_drop1 >= kHpsMinDrop && n_drop2 <= 2) {  // fast basis-conversion form
+    const int m2h = limbs - n_drop1 - n_drop2;
+    const size_t smh = (size_t)m2h * (6 + 2 * (n_drop1 + n_drop2 + 1) + n_drop1) * 8 +
+                       4 * kMaxDrop * 8;
+    if (smh > 200 * 1024) return CKB_E_ARG;
+#define CKB_DH(A, B)                                                                        \
+  if (d1 == A && d2 == B) {                                                                 \
+    if (smh > 48 * 1024)                                                                    \
+      cudaFuncSetAttribute(k_divround_corr_hps<A, B>,                                       \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh);          \
+    k_divround_corr_hps<A, B><<<grid_for(total, 256), 256, smh, st0>>>(                     \
+        E, T, has_addend, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
+        tabE, tabH, g_hps_margin);                                                          \
+    return finish();                                                                        \
+  }
+    CKB_DH(6, 0) CKB_DH(6, 1) CKB_DH(6, 2) CKB_DH(8, 0) CKB_DH(8, 1) CKB_DH(8, 2)
+    CKB_DH(11, 0) CKB_DH(11, 1) CKB_DH(11, 2) CKB_DH(13, 0) CKB_DH(13, 1) CKB_DH(13, 2)
+    CKB_DH(16, 0) CKB_DH(16, 1) CKB_DH(16, 2)
+#undef CKB_DH
+  }
   const bool one = n_drop1 >= 11;  // wide drops: one coefficient per thread
   const int grid = grid_for(one ? total : total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;

@@ -201,6 +201,7 @@ class GpuChain:
         return 2 * (-(-rows // chunk))
 
     F64_PRIME_LIMIT = nat.F64_PRIME_LIMIT
+    use_hps = True  # wide ModDown drops via the fast basis-conversion correction
 
     def _f64_share(self, lmap, limbs: int):
         return lambda: sum(self.all_primes[lmap[i]] < self.F64_PRIME_LIMIT
@@ -396,6 +397,37 @@ class GpuChain:
                 tab[j, n1 + u] = (c, shoup(c, p))
         return torch.from_numpy(tab.reshape(-1)).to(self.device)
 
+    HPS_MIN_DROP = 6  # csrc/ops.cu kHpsMinDrop
+
+    def _hps_table(self, basis: tuple, n1: int) -> torch.Tensor:
+        """tabH for ckb_divround_ntt_corr: per kept limb j < m1, {p_u^-1 mod q_j}
+        for the dropped primes p_u (u = 0 the last limb), then per dropped prime
+        {(P1/p_u)^-1 mod p_u, shoup}."""
+        primes = [self.all_primes[i] for i in basis]
+        limbs = len(primes)
+        m1 = limbs - n1
+        d1 = [primes[limbs - 1 - u] for u in range(n1)]
+        P1 = math.prod(d1)
+        tab = np.zeros(m1 * n1 + 2 * n1, dtype=np.uint64)
+        for j in range(m1):
+            q = primes[j]
+            for u, p in enumerate(d1):
+                tab[j * n1 + u] = pow(p % q, -1, q)
+        for u, p in enumerate(d1):
+            w = pow((P1 // p) % p, -1, p)
+            tab[m1 * n1 + 2 * u] = w
+            tab[m1 * n1 + 2 * u + 1] = shoup(w, p)
+        return torch.from_numpy(tab).to(self.device)
+
+    def hps_table(self, basis: tuple, n1: int, n2: int):
+        if n1 < self.HPS_MIN_DROP or n2 > 2:
+            return None
+        key = ("hps", basis, n1)
+        hit = self._maps.get(key)
+        if hit is None:
+            hit = self._maps[key] = self.publish(self._hps_table(basis, n1))
+        return hit
+
     def corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
         key = ("corr", basis, n1, n2)
         hit = self._maps.get(key)
@@ -433,6 +465,7 @@ class GpuChain:
             T = self.ntt_from(xv, polys, trows, xs, inverse=True, lmap=self.cmap(tbasis))
         t1, t2 = self.drop_tables(basis, n1, n2)
         tE = self.corr_table(basis, n1, n2)
+        tH = self.hps_table(basis, n1, n2) if self.use_hps else None
         E = torch.empty(polys, m2, n, dtype=U64, device=self.device)
         nb = polys * trows + polys * m2
         _run("divround_corr", nb * n * W, 1, lambda: nat.check(
@@ -440,6 +473,7 @@ class GpuChain:
                                           limbs, self.cmap(basis), n1, n2,
                                           nat.ptr(t1) if t1 is not None else None,
                                           nat.ptr(t2) if t2 is not None else None, nat.ptr(tE),
+                                          nat.ptr(tH) if tH is not None else None,
                                           nat.stream_handle()), "divround_ntt_corr"))
         self.ntt_fwd(E, m2, self.cmap(tuple(basis[:m2])))
         out = out if out is not None else torch.empty(polys, m2, n, dtype=U64, device=self.device)

@@ -343,7 +343,7 @@ def test_rbky_reference_key_file_round_trip(ck_gold):
 
 
 @pytest.mark.parametrize("dnum,level,special", [(None, 3, 60), (2, 3, 120), (3, 5, 300),
-                                                  (1, 3, 240)])
+                                                  (1, 3, 240), (3, 5, 360), (2, 3, 660)])
 def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
     """(3, 5, 300): 5 special primes, so ModDown with the fused rescale drops
     5 + 1 primes (k_divround_corr<6, 1>)."""
@@ -388,6 +388,48 @@ def test_mode_b_ops_bit_exact_vs_oracle(dnum, level, special):
     # inputs are never modified by an op (CipherVector immutability, api.py:51-65)
     assert np.array_equal(be.planes_of(a.payload), planes[0])
     assert np.array_equal(be.planes_of(b.payload), planes[1])
+
+
+def test_moddown_fast_conversion_paths_agree():
+    """Wide ModDown drops (>= 6 special primes) take the fast basis-conversion
+    correction; its exact-rho path (every coefficient forced through it with
+    margin 0), its default path and the mixed-radix kernel (use_hps off) give
+    the same ciphertexts bit for bit, for HMult (drop + fused rescale) and
+    HRot (drop only)."""
+    from paper_2506_19693_b200 import _native as nat
+    from paper_2506_19693_b200.ring import GpuChain as GC
+
+    n, level = 1024, 4
+    chain = (60,) + (40,) * level + (660,)
+    params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=40, level=level)
+    cust = he_api.keygen(params, {3}, backend="ckks", rng_seed=9, prime_layout="baseline",
+                         dnum=2)
+    be = cust.backend
+    assert be.chain.k == 11
+    rng = np.random.default_rng(2)
+    planes = [np.stack([np.stack([rng.integers(0, p, n, dtype=np.uint64)
+                                  for p in be.chain.limbs_at(level)]) for _ in range(2)])
+              for _ in range(2)]
+    a, b = (_wrap(cust, p, level) for p in planes)
+    ev = cust.evaluator
+
+    def run():
+        return (be.planes_of(ev.mul(a, b).payload), be.planes_of(ev.rotate(a, 3).payload))
+
+    base = run()
+    try:
+        assert nat.LIB.ckb_debug_hps_margin(0.0) == 0
+        forced = run()
+        assert nat.LIB.ckb_debug_hps_margin(0.6) != 0
+    finally:
+        nat.LIB.ckb_debug_hps_margin(0.5 - 2.0**-30)
+    GC.use_hps = False
+    try:
+        chained = run()
+    finally:
+        GC.use_hps = True
+    for x, y, z in zip(base, forced, chained):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
 
 
 # ---------------------------------------------------------------------------

@@ -1,4 +1,4 @@
-"""Config-4 step: histogram of the wave executor's batched groups (kind, level,
+"""Config-4 step (argv[1] == "2": the steady second step): histogram of the wave executor's batched groups (kind, level,
 batch size) and the kernel-time breakdown with rows per kernel."""
 import collections, json, os, sys, time
 import numpy as np, torch
@@ -17,6 +17,12 @@ cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", r
                      prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True)
 env = prog.run(cust, 0, prog.n_setup)
 ex = WaveExecutor(prog, cust)
+if len(sys.argv) > 1 and sys.argv[1] == "2":
+    out = ex.run(dict(env), only_after_setup=True)
+    prog = Program.load_step2(path)
+    env = {k: out[k] for k in Program.load(path).keep}
+    del out
+    ex = WaveExecutor(prog, cust)
 hist = collections.Counter()
 orig = WaveExecutor._run_group
 def rec(self, key, idx, env_, pvals):
