@@ -97,6 +97,17 @@ int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t*
                     const uint64_t* b, const uint64_t* c, int rows, int limbs,
                     const int32_t* limb_prime, int b_rows, void* stream);
 
+/* Linear combination with per-limb integer scalars:
+ *   out[poly][j][n] = sum_k scalars[k][j] * X_k[poly][j][n]  (mod p of limb j)
+ * X_k = terms_host[k] (a HOST array of device pointers), polys of term_limbs[k]
+ * >= limbs limbs each (read restricted to the first `limbs`); scalars: DEVICE
+ * [n_terms][limbs] residues.  n_terms <= 16.  Multiplying by a constant slot
+ * vector is multiplying by an integer, so the Chebyshev leaves of
+ * bootstrapping's EvalMod become one pass (then one rescale). */
+int ckb_scalar_mac(const ckb_ring* ring, uint64_t* out, const uint64_t* const* terms_host,
+                   const int32_t* term_limbs, const uint64_t* scalars, int n_terms, int polys,
+                   int limbs, const int32_t* limb_prime, void* stream);
+
 /* Plaintext multiply-accumulate over the terms of a baby-step/giant-step row
  * (the CoeffToSlot / SlotToCoeff diagonals of bootstrapping):
  *   out[r][n] = sum_t X_t[r][n] * pts[t][r % limbs][n]  (mod p of limb r % limbs)

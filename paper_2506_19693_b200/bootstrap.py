@@ -230,15 +230,26 @@ class Bootstrapper:
             deg -= 1
         c = c[: deg + 1]
         if deg < 16:
-            acc = None
-            for k in range(1, deg + 1):
-                if c[k] == 0.0:
-                    continue
-                term = self._mul_const(self._restrict(T[k], level + 1), c[k], out_scale=scale)
-                acc = term if acc is None else self._add(acc, term)
-            if acc is None:
-                acc = self._mul_const(self._restrict(T[1], level + 1), 0.0, out_scale=scale)
-            return self._add_const(acc, c[0])
+            # leaf: sum_k c_k T_k at (level + 1, scale * q) in one pass — a
+            # constant slot vector encodes to the integer round(c * pt_scale),
+            # so every term is an integer multiple of T_k read at level + 1
+            # (ckb_scalar_mac) — then a single rescale onto (level, scale)
+            be, ch = self.be, self.be.chain
+            lvl = level + 1
+            m = be._limbs(lvl)
+            q = self._q(lvl)
+            ks = [k for k in range(1, deg + 1) if c[k] != 0.0] or [1]
+            key = ("leaf", c.tobytes(), level, float(scale),
+                   tuple((T[k][1], float(T[k][2])) for k in ks))
+            sc = self._pt_cache.get(key)
+            if sc is None:
+                for k in ks:
+                    assert T[k][1] >= lvl, "Chebyshev leaf below its operands' level"
+                ints = [int(np.rint(c[k] * (scale * q / T[k][2]))) for k in ks]
+                sc = self._pt_cache[key] = ch.scalar_table(ints, m)
+            acc = ch.scalar_mac([T[k][0].contiguous() for k in ks], sc, m)
+            acc = be._rescale_data(acc, lvl)
+            return self._add_const((acc, level, scale), c[0])
         n = 1 << (deg.bit_length() - 1)
         q = np.zeros(deg - n + 1)
         q[0] = c[n]
@@ -278,14 +289,16 @@ class Bootstrapper:
         data, lvl, sc = x
         m = be._limbs(lvl)
         conj = be.rotate_data(data, lvl, self.conj)
-        re = (ch.add(data, conj, m), lvl, sc)
+        re = ch.add(data, conj, m)
         mono = be.monomial_ntt(3 * be.n // 2, lvl)  # -X^{N/2}: multiplies slots by -i
-        im = (ch.mul(ch.sub(data, conj, m), mono, m, b_rows=m), lvl, sc)
-        y_re = self._evalmod(re)
-        y_im = self._evalmod(im)
-        d_im, l_im, s_im = y_im
-        y_im = (ch.mul(d_im, be.monomial_ntt(be.n // 2, l_im), be._limbs(l_im),
-                       b_rows=be._limbs(l_im)), l_im, s_im)
+        im = ch.mul(ch.sub(data, conj, m), mono, m, b_rows=m)
+        # the real and imaginary parts through one batched EvalMod (same level
+        # and scale; every op is per-ciphertext, so results are unchanged)
+        bsz = data.shape[0]
+        y, l_y, s_y = self._evalmod((torch.cat([re, im]), lvl, sc))
+        y_re = (y[:bsz], l_y, s_y)
+        y_im = (ch.mul(y[bsz:].contiguous(), be.monomial_ntt(be.n // 2, l_y), be._limbs(l_y),
+                       b_rows=be._limbs(l_y)), l_y, s_y)
         z = self._add(y_re, y_im)
         z = (z[0], z[1], z[2] / self.sigma)
         rl = be.params.refresh_level

@@ -1302,6 +1302,65 @@ int ckb_elementwise(const ckb_ring* ring, int op, uint64_t* out, const uint64_t*
   return finish();
 }
 
+// out[poly][j] = sum_k a[k][j] * X_k[poly][j]  (mod q_j), j < limbs: a linear
+// combination of ciphertexts with per-limb integer scalars (the leaves of the
+// Chebyshev evaluation in bootstrapping: constant plaintexts are scalars).
+// X_k: polys of pstride[k] >= limbs limbs (a ciphertext at a higher level is
+// read restricted to its first limbs).  128-bit lazy sum, one reduction.
+struct TermPtrs {
+  const uint64_t* p[16];
+  int pstride[16];
+};
+
+__global__ void __launch_bounds__(256) k_scalar_mac(uint64_t* __restrict__ out, TermPtrs tp,
+                                                    const uint64_t* __restrict__ sc, int K,
+                                                    size_t pairs, int log_n, int limbs,
+                                                    RingDev R, LimbMap lm) {
+  const int lh = log_n - 1;
+  const size_t hmask = ((size_t)1 << lh) - 1;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < pairs;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const unsigned row = (unsigned)(t >> lh);
+    const size_t n = (t & hmask) * 2;
+    const unsigned poly = row / (unsigned)limbs, j = row % (unsigned)limbs;
+    uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int k = 0; k < K; ++k) {
+      const uint64_t a = __ldg(sc + (size_t)k * limbs + j);
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(
+          tp.p[k] + (((size_t)poly * tp.pstride[k] + j) << log_n) + n);
+      ckb::mac128(h0, l0, x.x, a);
+      ckb::mac128(h1, l1, x.y, a);
+    }
+    const uint64_t* mm = R.mods + (size_t)lm.p[j] * kModStride;
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    *reinterpret_cast<ulonglong2*>(out + ((size_t)row << log_n) + n) =
+        make_ulonglong2(ckb::reduce128_any(h0, l0, r64, r64s, m),
+                        ckb::reduce128_any(h1, l1, r64, r64s, m));
+  }
+}
+
+int ckb_scalar_mac(const ckb_ring* ring, uint64_t* out, const uint64_t* const* terms_host,
+                   const int32_t* term_limbs, const uint64_t* scalars, int n_terms, int polys,
+                   int limbs, const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || polys < 0 || n_terms < 1 || n_terms > 16 || !scalars ||
+      !terms_host || !term_limbs)
+    return CKB_E_ARG;
+  TermPtrs tp;
+  for (int k = 0; k < n_terms; ++k) {
+    if (!terms_host[k] || term_limbs[k] < limbs) return CKB_E_ARG;
+    tp.p[k] = terms_host[k];
+    tp.pstride[k] = term_limbs[k];
+  }
+  const RingDev R = make_ring(ring);
+  const size_t pairs = (((size_t)polys * limbs) << R.log_n) / 2;
+  if (!pairs) return 0;
+  k_scalar_mac<<<grid_for(pairs, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, tp, scalars, n_terms, pairs, (int)R.log_n, limbs, R, lm);
+  return finish();
+}
+
 int ckb_pt_mac(const ckb_ring* ring, uint64_t* out, const uint64_t* x0, const uint64_t* stack,
                int64_t stack_stride, const int32_t* term_idx, const uint64_t* pts,
                int64_t pt_stride, int n_terms, int rows, int limbs, const int32_t* limb_prime,

@@ -267,6 +267,31 @@ class GpuChain:
             nat.stream_handle()), "pt_mac"))
         return out
 
+    def scalar_table(self, scalars, limbs: int) -> torch.Tensor:
+        """Device [K][limbs] residues of Python-int scalars (any sign) for
+        scalar_mac; build once and reuse (no upload inside graph captures)."""
+        tab = np.array([[int(a) % self.all_primes[j] for j in range(limbs)] for a in scalars],
+                       dtype=np.uint64)
+        return self.publish(torch.from_numpy(tab.reshape(-1)).to(self.device))
+
+    def scalar_mac(self, terms, sc: torch.Tensor, limbs: int, out=None):
+        """sum_k a_k * terms[k] (ckb_scalar_mac): terms are ciphertext tensors
+        [..., m_k, N] with m_k >= limbs (read restricted to the first `limbs`),
+        the same leading shape; sc = scalar_table([a_k], limbs)."""
+        lead = terms[0].shape[:-2]
+        polys = int(np.prod(lead)) if len(lead) else 1
+        if any(t.shape[:-2] != lead or not t.is_contiguous() for t in terms):
+            raise ValueError("scalar_mac terms must be contiguous with one leading shape")
+        out = out if out is not None else torch.empty(*lead, limbs, self.n, dtype=U64,
+                                                      device=self.device)
+        ptrs = (nat.c_vp * len(terms))(*[t.data_ptr() for t in terms])
+        tl = nat.i32_array([t.shape[-2] for t in terms])
+        nb = len(terms) * polys * limbs + polys * limbs
+        _run("scalar_mac", nb * self.n * W, 1, lambda: nat.check(nat.LIB.ckb_scalar_mac(
+            self.ring_p, nat.ptr(out), ptrs, tl, nat.ptr(sc), len(terms), polys, limbs,
+            self.q_map(limbs), nat.stream_handle()), "scalar_mac"))
+        return out
+
     def add(self, a, b, limbs, out=None, lmap=None):
         return self.ew(0, out if out is not None else torch.empty_like(a), a, b, limbs=limbs, lmap=lmap)
 

@@ -164,6 +164,28 @@ def test_pt_mac_equals_mul_add_chain():
             assert np.array_equal(s_[c, j], w.astype(np.uint64))
 
 
+def test_scalar_mac_equals_scalar_mul_chain():
+    """ckb_scalar_mac (Chebyshev leaves): sum_k a_k X_k with signed big-int
+    scalars and operands at higher levels read restricted, equals numpy."""
+    n = 1 << 10
+    params = SchemeParams(poly_degree=n, modulus_chain=(60, 40, 45, 60, 60), scale_bits=40,
+                          level=3)
+    ch = GpuChain(params, layout="baseline")
+    rng = np.random.default_rng(5)
+    m = 3
+    xs_np, xs = [], []
+    for mk in (3, 4, 4, 3):  # limbs per poly of each term (>= m)
+        a = np.stack([np.stack([rng.integers(0, p, n, dtype=np.uint64)
+                                for p in ch.all_primes[:mk]]) for _ in range(2 * 2)])
+        xs_np.append(a.reshape(2, 2, mk, n))
+        xs.append(torch.from_numpy(a.reshape(2, 2, mk, n)).cuda())
+    ints = [3, -(1 << 70) + 5, 0, (1 << 90) + 12345]
+    got = _u64(ch.scalar_mac(xs, ch.scalar_table(ints, m), m))
+    for j, p in enumerate(ch.all_primes[:m]):
+        want = sum((x[:, :, j].astype(object) * (a % p)) for x, a in zip(xs_np, ints)) % p
+        assert np.array_equal(got[:, :, j], want.astype(np.uint64))
+
+
 def test_ntt_product_matches_schoolbook_60bit():
     n = 32
     p = O.largest_ntt_prime_below(60, 2 * n, set())
