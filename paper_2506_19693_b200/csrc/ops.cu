@@ -257,10 +257,11 @@ __global__ void __launch_bounds__(256) k_modup(uint64_t* __restrict__ out,
 // k_modup; warps at different outputs keep both pipes busy.  One coefficient
 // per thread (register budget).  Smem: ModSm per ext limb, the integer table in
 // pack30 form, then per (i, e) {double(c), double(c)/p_e} and per e 1/p_e.
-template <int AMAX>
-__global__ void __launch_bounds__(256, AMAX <= 6 ? 4 : (AMAX <= 8 ? 3 : 2)) k_modup_mixed(
+template <int AMAX, bool COMPACT>
+__global__ void __launch_bounds__(256) k_modup_mixed(
     uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_bstride, int batch,
-    int limbs, int ext, int alpha, int item_rows, int out_rows, int skip_own, int log_n,
+    int limbs, int ext, int alpha, int n_digits, int out_rows, int skip_own, int log_n,
+    int item_rows,
     RingDev R, LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
   extern __shared__ uint64_t sm[];
   ModSm* mods = reinterpret_cast<ModSm*>(sm);
@@ -306,7 +307,10 @@ __global__ void __launch_bounds__(256, AMAX <= 6 ? 4 : (AMAX <= 8 ? 3 : 2)) k_mo
     const size_t n = t & (N - 1);
     const size_t bi = t >> log_n;
     const uint64_t* src = in + bi * in_bstride + n;
-    uint64_t* dst = out + (bi * (size_t)item_rows + (size_t)j * out_rows) * N + n;
+    // uniform digits (every digit item_rows / n_digits rows): the index form the
+    // kernel was tuned with; compact layout of a short last digit otherwise
+    uint64_t* dst = COMPACT ? out + (bi * (size_t)item_rows + (size_t)j * out_rows) * N + n
+                            : out + (bi * n_digits + j) * (size_t)out_rows * N + n;
     uint64_t y[AMAX];
     double yd[AMAX];
 #pragma unroll
@@ -1450,12 +1454,17 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   }
   for (int e = 0; e < ext_limbs; ++e) out_f64 |= is_f64(em.p[e]);
   if (alpha > 1 && alpha <= 16 && digit_f64 && out_f64) {
-    using KernM = decltype(&k_modup_mixed<2>);
-    static const KernM mkerns[17] = {
-        nullptr, nullptr, k_modup_mixed<2>, k_modup_mixed<3>, k_modup_mixed<4>,
-        k_modup_mixed<5>, k_modup_mixed<6>, k_modup_mixed<7>, k_modup_mixed<8>,
-        k_modup_mixed<9>, k_modup_mixed<10>, k_modup_mixed<11>, k_modup_mixed<12>,
-        k_modup_mixed<13>, k_modup_mixed<14>, k_modup_mixed<15>, k_modup_mixed<16>};
+    using KernM = decltype(&k_modup_mixed<2, false>);
+#define CKB_MM(C)                                                                            \
+  {nullptr, nullptr, k_modup_mixed<2, C>, k_modup_mixed<3, C>, k_modup_mixed<4, C>,          \
+   k_modup_mixed<5, C>, k_modup_mixed<6, C>, k_modup_mixed<7, C>, k_modup_mixed<8, C>,       \
+   k_modup_mixed<9, C>, k_modup_mixed<10, C>, k_modup_mixed<11, C>, k_modup_mixed<12, C>,    \
+   k_modup_mixed<13, C>, k_modup_mixed<14, C>, k_modup_mixed<15, C>, k_modup_mixed<16, C>}
+    static const KernM mk_u[17] = CKB_MM(false);
+    static const KernM mk_c[17] = CKB_MM(true);
+#undef CKB_MM
+    const bool compact = item_rows != nd * out_rows;
+    const KernM* mkerns = compact ? mk_c : mk_u;
     const size_t msmem = (6 * (size_t)ext_limbs + (size_t)alpha * (2 + 2 * (size_t)ext_limbs)) * 8 +
                          (size_t)alpha * ext_limbs * 16 + (size_t)ext_limbs * 8;
     if (msmem > 48 * 1024)
@@ -1464,9 +1473,8 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
     dim3 mgrid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
                (unsigned)nd);
     mkerns[alpha]<<<mgrid, 256, msmem, (cudaStream_t)stream>>>(
-        out, in, bstride, batch, limbs, ext_limbs, alpha, item_rows, out_rows, skip_own,
-        (int)R.log_n,
-        R, lm, em, bconv);
+        out, in, bstride, batch, limbs, ext_limbs, alpha, nd, out_rows, skip_own, (int)R.log_n,
+        item_rows, R, lm, em, bconv);
     return finish();
   }
   const size_t smem = (6 * (size_t)ext_limbs +
