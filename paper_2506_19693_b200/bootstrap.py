@@ -175,8 +175,9 @@ class Bootstrapper:
                                       stack=True) if babies else None)
         slot = {b: i for i, b in enumerate(babies)}
         slot[0] = -1  # the unrotated input
-        data = data.contiguous()
-        acc = None
+        data = data.contiguous().view(-1, 2, m, be.n)
+        bsz, k = data.shape[0], ch.k
+        acc = addend = None
         for g, row in sorted(rows.items()):
             # one multiply-accumulate pass over the row's terms (ckb_pt_mac)
             key = (tag, g, lvl, pt_scale)
@@ -192,11 +193,32 @@ class Bootstrapper:
                                  out=inner if lo == 0 else None)
                 if lo:
                     ch.add(inner, part, m, out=inner)
-            inner = be._rescale_data(inner, lvl)
-            if g:
-                inner = be.rotate_data(inner, lvl - 1, self._galois(g * n1 * s))
-            acc = inner if acc is None else ch.add(acc, inner, be._limbs(lvl - 1), out=acc)
-        return acc, lvl - 1, sc * pt_scale / q
+            if not g:
+                addend = inner if addend is None else ch.add(addend, inner, m, out=addend)
+                continue
+            # giant step: the rotation's key switch is accumulated in the
+            # extended basis Q u P (rotation commutes with the exact rescale),
+            # its c0' joins the addend; one ModDown + rescale ends the level
+            galois = self._galois(g * n1 * s)
+            r = ch.automorphism_ntt(inner, galois)
+            c1 = ch.ntt_from(r[:, 1], bsz, m, 2 * m * be.n, inverse=True)
+            ks = be._key_switch_acc(c1, m, batch=bsz, key=be.rotation_key(galois), own=r[:, 1],
+                                    own_stride=2 * m * be.n)
+            acc = ks if acc is None else ch.add(acc, ks, m + k, out=acc, lmap=ch.ext_map(m))
+            # only c0' joins the addend: clear c1' (the key switch has read it)
+            # and add the whole item (contiguous rows)
+            r[:, 1].zero_()
+            addend = r if addend is None else ch.add(addend, r, m, out=addend)
+        e = len(ch.entry_primes[lvl])
+        if acc is None:
+            out = be._rescale_data(addend, lvl)
+        else:
+            tail = addend[:, :, m - e:m].reshape(2 * bsz, e, be.n)
+            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=addend, addend_polys=2,
+                                  addend_period=2, addend_stride=2, addend_tail=tail,
+                                  basis=ch.ext_basis(m))
+            out = out.view(bsz, 2, m - e, be.n)
+        return out.view(*x[0].shape[:-2], m - e, be.n), lvl - 1, sc * pt_scale / q
 
     # -- EvalMod ------------------------------------------------------------------
     def _chebyshev_basis(self, x):
