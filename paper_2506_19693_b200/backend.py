@@ -430,11 +430,12 @@ class B200CkksCore:
         sc = self._scale(level) if scale is None else scale
         coeffs = self.encoder.embed_device(vals, sc)
         lim = self._encode_limit if limit is None else limit
-        # Every coefficient is an average of slot values times the scale, so
-        # |c_j| <= scale * max|v| (+ 1/2 from rounding): when that host-side
-        # bound already clears both checks, skip the exact device max (a host
-        # sync per encode); otherwise fall back to it — same error semantics.
-        host_bound = sc * float(np.max(np.abs(vals))) * (1 + 1e-9) + 1.0 if vals.size else 0.0
+        # Every coefficient is (1/N) x a sum over the N spectrum entries (each
+        # slot twice), so |c_j| <= scale * 2 sum|v| / N <= scale * max|v| (+ 1/2
+        # from rounding): when that host-side bound already clears both checks,
+        # skip the exact device max (a host sync per encode, not allowed inside
+        # a graph capture); otherwise fall back to it — same error semantics.
+        host_bound = _coeff_bound(vals, sc, self.n)
         if host_bound < lim and 4 * int(host_bound) < ch.modulus_at(level):
             res = ch.from_i64(coeffs.to(torch.int64), m)[0]
             if ntt:
@@ -478,7 +479,7 @@ class B200CkksCore:
             m = self._limbs(level)
             keys, rows = [], []
             for key, vals in grp.items():
-                hb = sc * float(np.max(np.abs(vals))) * (1 + 1e-9) + 1.0
+                hb = _coeff_bound(vals, sc, self.n)
                 if hb < self._encode_limit and 4 * int(hb) < ch.modulus_at(level):
                     keys.append(key)
                     rows.append(vals)
@@ -864,6 +865,15 @@ class B200CkksCore:
     def planes_of(self, payload: GpuCiphertext) -> np.ndarray:
         """Coefficient-domain (2, limbs, N) planes of a payload (RBCT order)."""
         return self._to_coeff(payload.data).cpu().numpy()
+
+
+def _coeff_bound(vals: np.ndarray, scale: float, n: int) -> float:
+    """Upper bound on |coefficient| of the encoding of real slots vals at scale
+    (encoding.py:34-49: coefficients are spectrum sums / N, each slot twice)."""
+    if not vals.size:
+        return 0.0
+    a = np.abs(vals)
+    return scale * min(float(np.max(a)), 2.0 * float(np.sum(a)) / n) * (1 + 1e-9) + 1.0
 
 
 def _mix64(*parts) -> int:

@@ -34,6 +34,9 @@ def timed(name, fn):
 
 B = BS.Bootstrapper
 B._linear = timed("linear", B._linear)
+if len(sys.argv) > 1 and sys.argv[1] == "evalmod":  # EvalMod internals instead
+    for nm in ("_mul", "_add", "_add_const", "_double", "_drop_to", "_chebyshev_basis"):
+        setattr(B, nm, timed(nm, getattr(B, nm)))
 B._evalmod = timed("evalmod", B._evalmod)
 be.mod_raise = timed("mod_raise", be.mod_raise)
 for bsz in (1, 4):
@@ -44,6 +47,11 @@ for bsz in (1, 4):
         be.bootstrap_batch(data, 0)
         torch.cuda.synchronize(); wall = 1e3 * (time.perf_counter() - t0)
     stages = [(nm, round(s.elapsed_time(e), 2)) for nm, s, e in rec]
+    if len(sys.argv) > 1:
+        agg = {}
+        for nm, t in stages:
+            a = agg.setdefault(nm, [0, 0.0]); a[0] += 1; a[1] = round(a[1] + t, 2)
+        stages = agg
     print(json.dumps({"batch": bsz, "wall_ms": round(wall, 2), "stages": stages}))
 ring.TIMER = ring.KernelTimer()
 be.bootstrap_batch(ct.data.unsqueeze(0).expand(4, -1, -1, -1).contiguous(), 0)
