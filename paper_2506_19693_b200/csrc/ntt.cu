@@ -1,5 +1,7 @@
 // Negacyclic NTT kernels (sm_100a): replaces NttPlan.forward/inverse
 // (/root/reference/pkg/src/ciphermlp/ckks/ntt.py:121-154).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fp64.cuh"
 
@@ -606,6 +608,20 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   return 0;
 }
 
+// Launches holding rows of both prime classes run as ONE launch of the
+// per-CTA-dispatch kernel (MODE 0: radix-8 for both paths): FP64-row CTAs and
+// integer-row CTAs then share the SMs, the FP64/L1-latency-bound and the
+// multiplier-bound work overlapping (measured: c2 479 -> 485 GB/s, config-4
+// steady step forward NTT -5%, against the class-split MODE 1 + MODE 2 pair
+// whose FP64 kernel alone is faster).  CKB_NTT_MIXED=0 restores the split.
+inline bool mixed_one_kernel() {
+  static const bool on = [] {
+    const char* v = getenv("CKB_NTT_MIXED");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <bool FWD>
 int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
             void* stream, const uint64_t* src = nullptr, size_t src_istride = 0) {
@@ -650,7 +666,8 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     pb.row0 = r0;
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
-      if (!any_f64) return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
+      if (!any_f64 || (any_int && mixed_one_kernel()))
+        return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
       // second-pass column phase: column-mapped direct I/O (MODE 3)
       const bool cm = ph.rstride != 1 && !ph.first;
       int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st)

@@ -12,7 +12,7 @@ print("roofline frac %.3f alu %.3f | e2e %.1f | c1 %.2f ms | c3 %.1f ms | c4 %.0
     d["roofline"]["frac"], d["roofline"]["alu"]["frac"], d.get("e2e", {}).get("value", float("nan")),
     d.get("c1_train", {}).get("ms_per_step", float("nan")), d.get("c3_bootstrap", {}).get("ms", float("nan")),
     d.get("c4_train", {}).get("ms_per_step", float("nan")),
-    d.get("c5_train", {}).get("ms_per_step", float("nan")), d["clocks"]))
+    d.get("c5_train", {}).get("ms_per_step", float("nan")), d.get("clocks")))
 for k in ("c4_train", "c5_train"):
     if k in d:
         print(k, {kk: (round(v, 6) if isinstance(v, float) else v) for kk, v in d[k].items()

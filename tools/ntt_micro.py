@@ -21,12 +21,13 @@ def chain_for(logn, nprimes, bits=40):
     return ch
 
 res = {}
+BITS = int(os.environ.get("NTT_BITS", "40"))  # 60: the integer (Shoup) path
 for logn, rows, limbs in [(16, 3072, 24), (12, 2304, 9)]:
   try:
-      ch = chain_for(logn, limbs)
+      ch = chain_for(logn, limbs, BITS)
       n = 1 << logn
 
-      x = torch.randint(0, 2**39, (rows, n), dtype=torch.int64, device="cuda").view(U64)
+      x = torch.randint(0, 2**(BITS - 1), (rows, n), dtype=torch.int64, device="cuda").view(U64)
       ref = x.clone()
       for _ in range(3):
           ch.ntt_fwd(x, limbs); ch.ntt_inv(x, limbs)
@@ -43,4 +44,4 @@ for logn, rows, limbs in [(16, 3072, 24), (12, 2304, 9)]:
       res[f"N=2^{logn} rows={rows}"] = {"fwd_ms": f, "inv_ms": i, "fwd_GBps": gb / (f / 1e3), "inv_GBps": gb / (i / 1e3)}
   except Exception as exc:
     res[f"N=2^{logn}"] = {"error": repr(exc)[:80]}
-print(json.dumps({"lib": os.environ.get("CKB_LIB", "default"), **res}))
+print(json.dumps({"lib": os.environ.get("CKB_LIB", "default"), "bits": BITS, **res}))
