@@ -608,6 +608,10 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   return 0;
 }
 
+// Register rounds of the per-CTA-dispatch and integer kernels: radix-16 in
+// forward transforms (mixed launches then run their FP64 rows radix-16; the
+// integer rows are equal either way), radix-8 in inverse ones (integer
+// inverse rows 6% faster at radix-8) — A/B on tools/ntt_micro.py and bench.
 // Launches holding rows of both prime classes run as ONE launch of the
 // per-CTA-dispatch kernel (MODE 0: radix-8 for both paths): FP64-row CTAs and
 // integer-row CTAs then share the SMs, the FP64/L1-latency-bound and the
@@ -667,12 +671,12 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
       if (!any_f64 || (any_int && mixed_one_kernel()))
-        return launch_phase<FWD, 3, 0>(S, data, ph, nr, R, lm, st);
+        return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st);
       // second-pass column phase: column-mapped direct I/O (MODE 3)
       const bool cm = ph.rstride != 1 && !ph.first;
       int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st)
                  : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
-      if (!r && any_int) r = launch_phase<FWD, 3, 2>(S, data, ph, nr, R, lm, st);
+      if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st);
       return r;
     };
     if (FWD) {
