@@ -498,14 +498,22 @@ def main():
     # two streams (their kernels are bound by different resources and overlap)
     s_hm, s_hr = torch.cuda.Stream(), torch.cuda.Stream()
 
+    from paper_2506_19693_b200 import _native as nat_
+
     def keyswitch_pair():
         cur = torch.cuda.current_stream()
         s_hm.wait_stream(cur)
         s_hr.wait_stream(cur)
-        with torch.cuda.stream(s_hm):
-            be.batch_hmult(A, B, lvl)
-        with torch.cuda.stream(s_hr):
-            be.batch_hrot(A, steps_rot, lvl)
+        # two concurrent streams share the L2: each transform chunk gets half
+        # of the single-stream budget (ckb_set_ntt_chunk_bytes)
+        prev = nat_.LIB.ckb_set_ntt_chunk_bytes(48 << 20)
+        try:
+            with torch.cuda.stream(s_hm):
+                be.batch_hmult(A, B, lvl)
+            with torch.cuda.stream(s_hr):
+                be.batch_hrot(A, steps_rot, lvl)
+        finally:
+            nat_.LIB.ckb_set_ntt_chunk_bytes(prev)
         cur.wait_stream(s_hm)
         cur.wait_stream(s_hr)
 

@@ -76,6 +76,11 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
  * Replaces NttPlan.inverse (ckks/ntt.py:138-154) / RingElement.to_coeff (ring.py:117-123). */
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream);
+/* L2 budget of the two-phase transforms (N > 4096): rows are processed in
+ * chunks of this many bytes so the intermediate stays in L2 between the
+ * phases (default 96 MB, one stream).  Process-global; 0 only queries.
+ * Returns the previous value.  Give each of several concurrent streams a share. */
+uint64_t ckb_set_ntt_chunk_bytes(uint64_t bytes);
 /* Out-of-place forms: dst ([rows][N], contiguous) = NTT / iNTT of the rows of
  * src, row r = (item r / limbs, limb r % limbs) read at
  * src + item*src_item_stride + limb*N (0: limbs*N).  The transform's first pass

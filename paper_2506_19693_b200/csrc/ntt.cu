@@ -626,6 +626,13 @@ inline bool mixed_one_kernel() {
   return on;
 }
 
+// Rows of a two-phase transform are processed in chunks whose intermediate
+// stays in L2 between the phases.  96 MB measured best for one stream
+// (config-4 step -2%, config-2 sequential NTT -7% against 48 MB); callers
+// running transforms on several streams at once give each a share
+// (ckb_set_ntt_chunk_bytes; bench.py's concurrent HMult/HRot pair uses 48 MB).
+static size_t g_ntt_chunk_bytes = (size_t)96 << 20;
+
 template <bool FWD>
 int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
             void* stream, const uint64_t* src = nullptr, size_t src_istride = 0) {
@@ -663,7 +670,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items, FWD ? 0 : 1,
               FWD ? nullptr : src, src_istride};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
-  const int chunk = std::max(1, (int)((48u << 20) / ((size_t)N * 8)));
+  const int chunk = std::max(1, (int)(g_ntt_chunk_bytes / ((size_t)N * 8)));
   for (int r0 = 0; r0 < rows; r0 += chunk) {
     const int nr = std::min(chunk, rows - r0);
     pa.row0 = r0;
@@ -757,6 +764,12 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream) {
   return ntt_run<false>(ring, data, rows, limbs, limb_prime, stream);
+}
+
+uint64_t ckb_set_ntt_chunk_bytes(uint64_t bytes) {
+  const uint64_t prev = g_ntt_chunk_bytes;
+  if (bytes) g_ntt_chunk_bytes = bytes;
+  return prev;
 }
 
 int ckb_ntt_forward_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,
