@@ -215,6 +215,17 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
                           int n_drop2, const uint64_t* tab1, const uint64_t* tab2,
                           const uint64_t* tabE, const uint64_t* tabH, void* stream);
+/* Steps 1b + 2 fused: forward-transform E ([polys][m2][N], coefficient domain,
+ * used as scratch) and apply the combine below as the transform's last phase
+ * stores, so the transformed E is never written back (same arguments as
+ * ckb_divround_ntt_combine_acc; limb_prime is the full basis, whose first m2
+ * entries are E's primes).  Replaces ckb_ntt_forward(E) + the combine. */
+int ckb_ntt_forward_combine(const ckb_ring* ring, uint64_t* out, uint64_t* E, const uint64_t* x,
+                            int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                            int addend_period, int addend_stride, int polys, int limbs,
+                            const int32_t* limb_prime, int n_drop1, int n_drop2,
+                            const uint64_t* tab1, const uint64_t* tab2, const uint64_t* post,
+                            int64_t post_poly_stride, void* stream);
 /* NTT-domain divide-and-round, step 2: out_j = (x_j * P1^-1 + add_j - E_j) * P2^-1 with x,
  * addend and E (after its forward NTT) in the NTT domain; addend addressing as ckb_divround. */
 int ckb_divround_ntt_combine(const ckb_ring* ring, uint64_t* out, const uint64_t* x,

@@ -56,6 +56,10 @@ def _load():
                              ctypes.c_int),
         "ckb_ntt_forward": ([R, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_ntt_inverse": ([R, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_ntt_forward_combine": ([R, c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     c_i32p, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp,
+                                     ctypes.c_int64, c_vp], ctypes.c_int),
         "ckb_set_ntt_chunk_bytes": ([ctypes.c_uint64], ctypes.c_uint64),
         "ckb_ntt_forward_from": ([R, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                   c_i32p, c_vp], ctypes.c_int),
@@ -120,7 +124,7 @@ def _load():
 
 LIB = _load()
 EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inverse",
-            "ckb_set_ntt_chunk_bytes", "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
+            "ckb_set_ntt_chunk_bytes", "ckb_ntt_forward_combine", "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
             "ckb_elementwise", "ckb_pt_mac", "ckb_scalar_mac", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
             "ckb_debug_hps_margin", "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",

@@ -55,6 +55,24 @@ struct NttPhase {
   size_t src_istride;   // from src + i*src_istride + l*N (NULL: in place)
 };
 
+// Optional epilogue of a forward transform's last phase: the ModDown /
+// rescale combine (ckb_divround_ntt_combine) applied to the transformed
+// correction polynomial E as it is stored, so E never goes back to HBM:
+//   out_j = ((x_j * P1^-1 + add_j - E_j) * P2^-1) + post_j   (mod q_j)
+// The transformed rows are E's: row = poly * m2 + j.
+struct CombineEp {
+  uint64_t* out;  // NULL: no epilogue
+  const uint64_t* x;
+  size_t xs;      // x poly stride (elements)
+  const uint64_t* add;
+  int add_polys, add_period, add_stride, m1;
+  const uint64_t* tab1;
+  const uint64_t* tab2;
+  int n1, n2;
+  const uint64_t* post;
+  size_t post_stride;
+};
+
 // Shared-memory slot of element r of group g: one pad word per 16 elements
 // keeps the register rounds (r = w + 16k, r = 16w + k, ...) conflict-free, and
 // the G/128 extra words of group stride spread the column phase's tile I/O
@@ -435,7 +453,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
 template <int S, bool FWD, int RBT, int MODE = 0>
 __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
                                   MODE == 1 || MODE == 3 ? (FWD ? 6 : 8) : (RBT == 3 ? 4 : 3))
-    k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm) {
+    k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm, CombineEp ep) {
   constexpr int G = 1 << S;
   constexpr int RB = S < RBT ? S : RBT;  // log2 elements per thread
   constexpr int E = 1 << RB;
@@ -566,6 +584,59 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   else
     __syncthreads();  // the tile store reads across groups
 
+  if (FWD && ep.out && ph.last) {  // fused combine (rows are contiguous here)
+    const int m2 = ph.limbs;
+    const int j = row % m2;
+    const size_t pidx = row / m2;
+    const int s1 = 2 * (ep.n1 + 1), s2 = 2 * (ep.n2 + 1);
+    uint64_t a1 = 0, a1s = 0, b2 = 0, b2s = 0;
+    if (ep.n1) {
+      a1 = __ldg(ep.tab1 + (size_t)j * s1 + 2 * ep.n1);
+      a1s = __ldg(ep.tab1 + (size_t)j * s1 + 2 * ep.n1 + 1);
+    }
+    if (ep.n2) {
+      b2 = __ldg(ep.tab2 + (size_t)j * s2 + 2 * ep.n2);
+      b2s = __ldg(ep.tab2 + (size_t)j * s2 + 2 * ep.n2 + 1);
+    }
+    const uint64_t* xr = ep.x + pidx * ep.xs + (size_t)j * N;
+    const uint64_t* ar = nullptr;
+    if (ep.add) {
+      const size_t phs = pidx % ep.add_period;
+      if ((int)phs < ep.add_polys)
+        ar = ep.add + ((pidx / ep.add_period) * ep.add_stride + phs) * ep.m1 * N + (size_t)j * N;
+    }
+    const uint64_t* pr = ep.post ? ep.post + pidx * ep.post_stride + (size_t)j * N : nullptr;
+    uint64_t* orow = ep.out + (size_t)row * N;
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      int g, r;
+      const size_t off = pair_of(i, g, r);
+      const uint64_t e0 = smem[sidx<S>(g, r)], e1 = smem[sidx<S>(g, r + 1)];
+      ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + off);
+      if (ep.n1) {
+        v.x = ckb::mul_shoup(v.x, a1, a1s, p);
+        v.y = ckb::mul_shoup(v.y, a1, a1s, p);
+      }
+      if (ar) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(ar + off);
+        v.x = ckb::add_mod(v.x, a.x, p);
+        v.y = ckb::add_mod(v.y, a.y, p);
+      }
+      v.x = ckb::sub_mod(v.x, e0, p);
+      v.y = ckb::sub_mod(v.y, e1, p);
+      if (ep.n2) {
+        v.x = ckb::mul_shoup(v.x, b2, b2s, p);
+        v.y = ckb::mul_shoup(v.y, b2, b2s, p);
+      }
+      if (pr) {
+        const ulonglong2 w2 = *reinterpret_cast<const ulonglong2*>(pr + off);
+        v.x = ckb::add_mod(v.x, w2.x, p);
+        v.y = ckb::add_mod(v.y, w2.y, p);
+      }
+      *reinterpret_cast<ulonglong2*>(orow + off) = v;
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < E / 2; ++i) {
     int g, r;
@@ -579,7 +650,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
 
 template <bool FWD, int RBT, int MODE = 0>
 int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const RingDev& R,
-                 const LimbMap& lm, cudaStream_t st) {
+                 const LimbMap& lm, cudaStream_t st, const CombineEp& ep = CombineEp{}) {
   const int G = 1 << S;
   const int RB = S < RBT ? S : RBT;
   const int threads = ph.C * G >> RB;
@@ -589,7 +660,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   if (threads > kNttThreads) return CKB_E_LOGN;
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
-    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, ph, R, lm); \
+    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, ph, R, lm, ep); \
     break;
   switch (S) {
     CKB_NTT_CASE(4)
@@ -635,7 +706,8 @@ static size_t g_ntt_chunk_bytes = (size_t)96 << 20;
 
 template <bool FWD>
 int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
-            void* stream, const uint64_t* src = nullptr, size_t src_istride = 0) {
+            void* stream, const uint64_t* src = nullptr, size_t src_istride = 0,
+            const CombineEp& ep = CombineEp{}) {
   LimbMap lm;
   if (!make_map(lm, limb_prime, limbs) || rows < 0) return CKB_E_LIMBS;
   if (rows == 0) return 0;
@@ -646,7 +718,7 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   const int N = 1 << logn;
   if (logn <= 12) {
     NttPhase ph{limbs, 1, 1, 0, 1, 1, 0, 1, 0, 0, 0, 1, src, src_istride};
-    int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st);
+    int rc = launch_phase<FWD, 4>(logn, data, ph, rows, R, lm, st, ep);
     return rc ? rc : finish();
   }
   const int s2 = logn / 2;        // low stages (contiguous rows, phase B)
@@ -678,12 +750,12 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
       if (!any_f64 || (any_int && mixed_one_kernel()))
-        return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st);
+        return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st, ep);
       // second-pass column phase: column-mapped direct I/O (MODE 3)
       const bool cm = ph.rstride != 1 && !ph.first;
-      int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st)
-                 : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st);
-      if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st);
+      int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st, ep)
+                 : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st, ep);
+      if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st, ep);
       return r;
     };
     if (FWD) {
@@ -770,6 +842,39 @@ uint64_t ckb_set_ntt_chunk_bytes(uint64_t bytes) {
   const uint64_t prev = g_ntt_chunk_bytes;
   if (bytes) g_ntt_chunk_bytes = bytes;
   return prev;
+}
+
+int ckb_ntt_forward_combine(const ckb_ring* ring, uint64_t* out, uint64_t* E, const uint64_t* x,
+                            int64_t x_poly_stride, const uint64_t* addend, int addend_polys,
+                            int addend_period, int addend_stride, int polys, int limbs,
+                            const int32_t* limb_prime, int n_drop1, int n_drop2,
+                            const uint64_t* tab1, const uint64_t* tab2, const uint64_t* post,
+                            int64_t post_poly_stride, void* stream) {
+  if (n_drop1 < 0 || n_drop2 < 0 || n_drop1 + n_drop2 >= limbs || polys < 0 || !E || !out || !x)
+    return CKB_E_ARG;
+  if ((n_drop1 && !tab1) || (n_drop2 && !tab2)) return CKB_E_ARG;
+  if (addend && (addend_period < 1 || addend_polys < 0 || addend_polys > addend_period ||
+                 addend_stride < addend_polys))
+    return CKB_E_ARG;
+  const int m2 = limbs - n_drop1 - n_drop2;
+  if (!polys) return 0;
+  CombineEp ep;
+  ep.out = out;
+  ep.x = x;
+  ep.xs = x_poly_stride > 0 ? (size_t)x_poly_stride : ((size_t)limbs << ring->log_n);
+  ep.add = addend;
+  ep.add_polys = addend ? addend_polys : 0;
+  ep.add_period = addend ? addend_period : 1;
+  ep.add_stride = addend ? addend_stride : 0;
+  ep.m1 = limbs - n_drop1;
+  ep.tab1 = tab1;
+  ep.tab2 = tab2;
+  ep.n1 = n_drop1;
+  ep.n2 = n_drop2;
+  ep.post = post;
+  ep.post_stride = post_poly_stride > 0 ? (size_t)post_poly_stride : ((size_t)m2 << ring->log_n);
+  // the transform's rows are E's: m2 limbs per poly, primes = the first m2 of the basis
+  return ntt_run<true>(ring, E, polys * m2, m2, limb_prime, stream, nullptr, 0, ep);
 }
 
 int ckb_ntt_forward_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* src,

@@ -202,6 +202,7 @@ class GpuChain:
 
     F64_PRIME_LIMIT = nat.F64_PRIME_LIMIT
     use_hps = True  # wide ModDown drops via the fast basis-conversion correction
+    fuse_combine = True  # ModDown combine as the E transform's epilogue
 
     def _f64_share(self, lmap, limbs: int):
         return lambda: sum(self.all_primes[lmap[i]] < self.F64_PRIME_LIMIT
@@ -500,22 +501,30 @@ class GpuChain:
                                           nat.ptr(t2) if t2 is not None else None, nat.ptr(tE),
                                           nat.ptr(tH) if tH is not None else None,
                                           nat.stream_handle()), "divround_ntt_corr"))
-        self.ntt_fwd(E, m2, self.cmap(tuple(basis[:m2])))
         out = out if out is not None else torch.empty(polys, m2, n, dtype=U64, device=self.device)
         n_add = 0 if addend is None else (polys // addend_period) * addend_polys * m2
-        nb = polys * m2 * (3 if post is None else 4) + n_add
         if post is not None and (post.dtype != U64 or not post.is_contiguous()
                                  or post.numel() != polys * m2 * n):
             raise ValueError("post must be contiguous uint64 [polys, m2, N]")
+        args = (nat.ptr(x), xs, nat.ptr(addend) if addend is not None else None,
+                addend_polys if addend is not None else 0, addend_period, addend_stride)
+        tabs = (nat.ptr(t1) if t1 is not None else None, nat.ptr(t2) if t2 is not None else None,
+                nat.ptr(post) if post is not None else None, 0, nat.stream_handle())
+        if self.fuse_combine:
+            # E's forward NTT with the combine as its last phase's store (E in,
+            # out written; the transformed E never goes back to HBM)
+            nb = polys * m2 * (3 if post is None else 4) + n_add  # E read + x, out
+            _run("ntt_combine", nb * n * W, self._ntt_launches(polys * m2), lambda: nat.check(
+                nat.LIB.ckb_ntt_forward_combine(self.ring_p, nat.ptr(out), nat.ptr(E), *args,
+                                                polys, limbs, self.cmap(basis), n1, n2, *tabs),
+                "ntt_forward_combine"), self._f64_share(self.cmap(tuple(basis[:m2])), m2))
+            return out
+        self.ntt_fwd(E, m2, self.cmap(tuple(basis[:m2])))
+        nb = polys * m2 * (3 if post is None else 4) + n_add
         _run("divround_combine", nb * n * W, 1, lambda: nat.check(
             nat.LIB.ckb_divround_ntt_combine_acc(
-                self.ring_p, nat.ptr(out), nat.ptr(x), xs,
-                nat.ptr(addend) if addend is not None else None,
-                addend_polys if addend is not None else 0, addend_period, addend_stride,
-                nat.ptr(E), polys, limbs, self.cmap(basis), n1, n2,
-                nat.ptr(t1) if t1 is not None else None, nat.ptr(t2) if t2 is not None else None,
-                nat.ptr(post) if post is not None else None, 0, nat.stream_handle()),
-            "divround_ntt_combine"))
+                self.ring_p, nat.ptr(out), *args, nat.ptr(E), polys, limbs, self.cmap(basis),
+                n1, n2, *tabs), "divround_ntt_combine"))
         return out
 
     def automorphism_ntt(self, x, galois: int, out=None, g_items=None, rows_per_item: int = 0):
