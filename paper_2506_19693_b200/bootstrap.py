@@ -20,6 +20,7 @@ and finally aligns to params.refresh_level.  Constants: bootstrap_consts.py.
 
 from __future__ import annotations
 
+import contextlib
 import math
 
 import numpy as np
@@ -52,6 +53,9 @@ class Bootstrapper:
         be = self.be = backend
         ch = be.chain
         self.K, self.r, self.degree, self.levels = K, r, degree, levels
+        # side streams for the giant rows of small batches (see _linear)
+        self.streams, self.stream_batch_max = 3, 4
+        self._side = [torch.cuda.Stream(be.device) for _ in range(self.streams)]
         n = be.n
         slots = n // 2
         self.slots = slots
@@ -177,8 +181,60 @@ class Bootstrapper:
         slot[0] = -1  # the unrotated input
         data = data.contiguous().view(-1, 2, m, be.n)
         bsz, k = data.shape[0], ch.k
-        acc = addend = None
-        for g, row in sorted(rows.items()):
+        # giant rows are independent up to the final sum: small batches spread
+        # them over side streams (CUDA-graph branches when captured) so the
+        # rows' kernels, each too small to fill the GPU, run side by side;
+        # every stream keeps its own partial sums, added on the caller's stream
+        ns = self.streams if bsz <= self.stream_batch_max else 0
+        main = torch.cuda.current_stream()
+        parts = []  # (acc, addend) per stream
+        for st in self._side[:ns]:
+            st.wait_stream(main)
+        for gi, (g, row) in enumerate(sorted(rows.items())):
+            if ns:
+                si = gi % ns
+                while len(parts) <= si:
+                    parts.append([None, None])
+                acc, addend = parts[si]
+                ctx = torch.cuda.stream(self._side[si])
+            else:
+                if not parts:
+                    parts.append([None, None])
+                acc, addend = parts[0]
+                ctx = contextlib.nullcontext()
+            with ctx:
+                acc, addend = self._giant_row(data, stack, slot, tag, g, row, lvl, pt_scale,
+                                              n1, s, m, k, bsz, acc, addend)
+            parts[si if ns else 0] = [acc, addend]
+        if ns:
+            for st in self._side[:ns]:
+                main.wait_stream(st)
+            for a, d in parts:
+                for t in (a, d):
+                    if t is not None:
+                        t.record_stream(main)
+        acc, addend = parts[0]
+        for a, d in parts[1:]:
+            if a is not None:
+                acc = a if acc is None else ch.add(acc, a, m + k, out=acc, lmap=ch.ext_map(m))
+            if d is not None:
+                addend = d if addend is None else ch.add(addend, d, m, out=addend)
+        e = len(ch.entry_primes[lvl])
+        if acc is None:
+            out = be._rescale_data(addend, lvl)
+        else:
+            tail = addend[:, :, m - e:m].reshape(2 * bsz, e, be.n)
+            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=addend, addend_polys=2,
+                                  addend_period=2, addend_stride=2, addend_tail=tail,
+                                  basis=ch.ext_basis(m))
+            out = out.view(bsz, 2, m - e, be.n)
+        return out.view(*x[0].shape[:-2], m - e, be.n), lvl - 1, sc * pt_scale / q
+
+    def _giant_row(self, data, stack, slot, tag, g, row, lvl, pt_scale, n1, s, m, k, bsz,
+                   acc, addend):
+        """One giant row of a BSGS transform added into (acc [Q u P], addend [Q])."""
+        be, ch = self.be, self.be.chain
+        if True:
             # one multiply-accumulate pass over the row's terms (ckb_pt_mac)
             key = (tag, g, lvl, pt_scale)
             hit = self._pt_cache.get(key)
@@ -195,7 +251,7 @@ class Bootstrapper:
                     ch.add(inner, part, m, out=inner)
             if not g:
                 addend = inner if addend is None else ch.add(addend, inner, m, out=addend)
-                continue
+                return acc, addend
             # giant step: the rotation's key switch is accumulated in the
             # extended basis Q u P (rotation commutes with the exact rescale),
             # its c0' joins the addend; one ModDown + rescale ends the level
@@ -209,16 +265,7 @@ class Bootstrapper:
             # and add the whole item (contiguous rows)
             r[:, 1].zero_()
             addend = r if addend is None else ch.add(addend, r, m, out=addend)
-        e = len(ch.entry_primes[lvl])
-        if acc is None:
-            out = be._rescale_data(addend, lvl)
-        else:
-            tail = addend[:, :, m - e:m].reshape(2 * bsz, e, be.n)
-            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=addend, addend_polys=2,
-                                  addend_period=2, addend_stride=2, addend_tail=tail,
-                                  basis=ch.ext_basis(m))
-            out = out.view(bsz, 2, m - e, be.n)
-        return out.view(*x[0].shape[:-2], m - e, be.n), lvl - 1, sc * pt_scale / q
+            return acc, addend
 
     # -- EvalMod ------------------------------------------------------------------
     def _chebyshev_basis(self, x):
