@@ -269,23 +269,35 @@ class Bootstrapper:
 
     # -- EvalMod ------------------------------------------------------------------
     def _chebyshev_basis(self, x):
+        """T_1..T_16, T_32, T_64 (T_2j = 2 T_j^2 - 1, T_2j+1 = 2 T_j T_j+1 - T_1),
+        computed depth by depth: the products of one depth are independent, so
+        for small batches they go to the side streams (as _linear's giant rows)."""
         T = {1: x}
 
-        def get(k):
-            if k in T:
-                return T[k]
+        def one(k):
             if k % 2 == 0:
-                h = get(k // 2)
-                T[k] = self._add_const(self._double(self._mul(h, h)), -1.0)
-            else:
-                a, b = get(k // 2), get(k // 2 + 1)
-                T[k] = self._add(self._double(self._mul(a, b)), get(1), sub=True)
-            return T[k]
+                h = T[k // 2]
+                return self._add_const(self._double(self._mul(h, h)), -1.0)
+            a, b = T[k // 2], T[k // 2 + 1]
+            return self._add(self._double(self._mul(a, b)), T[1], sub=True)
 
-        for k in range(2, 17):
-            get(k)
-        get(32)
-        get(64)
+        main = torch.cuda.current_stream()
+        par = x[0].shape[0] <= 2 * self.stream_batch_max
+        for grp in ([2], [3, 4], [5, 6, 7, 8], list(range(9, 17)), [32], [64]):
+            if not par or len(grp) == 1:
+                for k in grp:
+                    T[k] = one(k)
+                continue
+            side = self._side
+            for st in side:
+                st.wait_stream(main)
+            for i, k in enumerate(grp):
+                with torch.cuda.stream(side[i % len(side)]):
+                    T[k] = one(k)
+            for st in side:
+                main.wait_stream(st)
+            for k in grp:
+                T[k][0].record_stream(main)
         return T
 
     def _eval_cheb(self, c, T, level: int, scale: float):
