@@ -300,7 +300,7 @@ class Bootstrapper:
                 T[k][0].record_stream(main)
         return T
 
-    def _eval_cheb(self, c, T, level: int, scale: float):
+    def _eval_cheb(self, c, T, level: int, scale: float, par: bool = False):
         """sum_k c_k T_k as a ciphertext exactly at (level, scale): every term
         is steered onto the target by the scale of its coefficient plaintext
         (leaves) or of its quotient (giant-step products), so same-level
@@ -339,9 +339,26 @@ class Bootstrapper:
         for j in range(1, deg - n + 1):
             rem[n - j] -= c[n + j]
         tn = self._restrict(T[n], level + 1)
-        qv = self._eval_cheb(q, T, level + 1, scale * self._q(level + 1) / tn[2])
-        prod = self._mul(qv, tn)
-        return self._add(prod, self._eval_cheb(rem, T, level, scale))
+        qscale = scale * self._q(level + 1) / tn[2]
+        if not par:
+            qv = self._eval_cheb(q, T, level + 1, qscale)
+            prod = self._mul(qv, tn)
+            return self._add(prod, self._eval_cheb(rem, T, level, scale))
+        # par: the quotient and remainder subtrees are independent — one side
+        # stream each (small batches), joined for the giant-step product
+        main = torch.cuda.current_stream()
+        sq, sr = self._side[0], self._side[1]
+        sq.wait_stream(main)
+        sr.wait_stream(main)
+        with torch.cuda.stream(sq):
+            prod = self._mul(self._eval_cheb(q, T, level + 1, qscale), tn)
+        with torch.cuda.stream(sr):
+            rv = self._eval_cheb(rem, T, level, scale)
+        main.wait_stream(sq)
+        main.wait_stream(sr)
+        prod[0].record_stream(main)
+        rv[0].record_stream(main)
+        return self._add(prod, rv)
 
     def _cheb_level(self, T, deg: int) -> int:
         """Lowest-depth target level: leaves need T_1..T_15 one level above."""
@@ -351,7 +368,8 @@ class Bootstrapper:
 
     def _evalmod(self, x):
         T = self._chebyshev_basis(x)
-        y = self._eval_cheb(self.cheb, T, self._cheb_level(T, len(self.cheb) - 1), x[2])
+        y = self._eval_cheb(self.cheb, T, self._cheb_level(T, len(self.cheb) - 1), x[2],
+                            par=x[0].shape[0] <= 2 * self.stream_batch_max)
         for _ in range(self.r):
             y = self._add_const(self._double(self._mul(y, y)), -1.0)
         return y
