@@ -33,6 +33,7 @@ Extra keyword options (all default to the reference's behaviour):
 from __future__ import annotations
 
 import collections
+import contextlib
 import dataclasses
 import io
 import json
@@ -747,13 +748,14 @@ class B200CkksCore:
         return hit
 
     def hoisted_rotations(self, data: torch.Tensor, level: int, galois_list,
-                          stack: bool = False):
+                          stack: bool = False, streams=None):
         """Rotate ciphertexts ([..., 2, m, N], NTT domain) by several Galois
         elements sharing a single ModUp: the digits are lifted and transformed
         once and permuted per rotation in the NTT domain (an automorphism
         commutes with the basis extension up to multiples of Q_j, which the key
         switch absorbs as noise).  stack=True returns one tensor
-        [len(galois_list), ..., 2, m, N] instead of a list."""
+        [len(galois_list), ..., 2, m, N] instead of a list.  streams: side
+        streams the rotations are spread over (independent after the ModUp)."""
         ch = self.chain
         m = self._limbs(level)
         ext = m + ch.k
@@ -765,14 +767,21 @@ class B200CkksCore:
         ch.ntt_fwd(digits, ext, ch.ext_map(m))
         c0s = d[:, 0].contiguous()
         res = torch.empty(len(galois_list), b, 2, m, self.n, dtype=U64, device=self.device)
+        main = torch.cuda.current_stream()
+        for st in streams or ():
+            st.wait_stream(main)
         for i, g in enumerate(galois_list):
             key = self.rotation_key(g)
-            dg = ch.automorphism_ntt(digits, g)
-            acc = ch.ks_inner(dg, m, self.alpha, key=key.data)
-            c0 = ch.automorphism_ntt(c0s, g)
-            ch.divround_ntt(acc, 2 * b, ext, ch.k, 0, addend=c0, addend_polys=1,
-                            addend_period=2, addend_stride=1, basis=ch.ext_basis(m),
-                            out=res[i].view(2 * b, m, self.n))
+            ctx = torch.cuda.stream(streams[i % len(streams)]) if streams else _nullctx()
+            with ctx:
+                dg = ch.automorphism_ntt(digits, g)
+                acc = ch.ks_inner(dg, m, self.alpha, key=key.data)
+                c0 = ch.automorphism_ntt(c0s, g)
+                ch.divround_ntt(acc, 2 * b, ext, ch.k, 0, addend=c0, addend_polys=1,
+                                addend_period=2, addend_stride=1, basis=ch.ext_basis(m),
+                                out=res[i].view(2 * b, m, self.n))
+        for st in streams or ():
+            main.wait_stream(st)
         res = res.view(len(galois_list), *lead, 2, m, self.n)
         return res if stack else list(res.unbind(0))
 
@@ -865,6 +874,9 @@ class B200CkksCore:
     def planes_of(self, payload: GpuCiphertext) -> np.ndarray:
         """Coefficient-domain (2, limbs, N) planes of a payload (RBCT order)."""
         return self._to_coeff(payload.data).cpu().numpy()
+
+
+_nullctx = contextlib.nullcontext
 
 
 def _coeff_bound(vals: np.ndarray, scale: float, n: int) -> float:

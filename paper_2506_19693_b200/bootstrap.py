@@ -175,8 +175,10 @@ class Bootstrapper:
         q = self._q(lvl)
         pt_scale = q if out_scale is None else out_scale * q / sc
         babies = sorted({b for row in rows.values() for b in row if b})
+        small = data.reshape(-1, 2, m, be.n).shape[0] <= self.stream_batch_max
         stack = (be.hoisted_rotations(data, lvl, [self._galois(b * s) for b in babies],
-                                      stack=True) if babies else None)
+                                      stack=True, streams=self._side if small else None)
+                 if babies else None)
         slot = {b: i for i, b in enumerate(babies)}
         slot[0] = -1  # the unrotated input
         data = data.contiguous().view(-1, 2, m, be.n)
