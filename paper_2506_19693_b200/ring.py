@@ -195,9 +195,11 @@ class GpuChain:
 
     # -- kernels -------------------------------------------------------------------
     def _ntt_launches(self, rows: int) -> int:
+        """Kernel launches of one transform call: one per phase and L2 chunk
+        (a launch holding both prime classes is one per-CTA-dispatch kernel)."""
         if self.log_n <= 12:
             return 1
-        chunk = max(1, (48 << 20) // (self.n * W))
+        chunk = max(1, int(nat.LIB.ckb_set_ntt_chunk_bytes(0)) // (self.n * W))
         return 2 * (-(-rows // chunk))
 
     F64_PRIME_LIMIT = nat.F64_PRIME_LIMIT
