@@ -187,7 +187,7 @@ class B200CkksCore:
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
                  conjugation_key: bool = False, real_bootstrap: bool = False,
-                 sampler: str = None):
+                 sampler: str = None, low_special: int = None):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -256,6 +256,33 @@ class B200CkksCore:
             s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
             ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
             self.rotation_keys[g] = self._make_ksk(s_rot, rng)
+        # Level-aware special modulus: ciphertexts at or below the refresh level
+        # (whose digits are at most q0 + (alpha-1) user primes) key-switch with
+        # the first `low_special` special primes only — P' >= the widest such
+        # digit keeps the key-switch noise ~N*sigma, far below the 2^scale_bits
+        # scale — so the ModUp / inner product / ModDown of every training-step
+        # multiply and rotation carry fewer 60-bit limbs.  A second relin key and
+        # rotation keys for the user steps over Q u P'; bootstrapping (above the
+        # refresh level) keeps the full P.  Off by default (the parity tests pin
+        # the full-P semantics).
+        self.k_low = None
+        if low_special is not None and 0 < int(low_special) < ch.k:
+            self.k_low = int(low_special)
+            rl = params.refresh_level
+            widest = max(math.prod(ch.all_primes[lo:min(lo + self.alpha, ch.level_limbs[rl])])
+                         for lo in range(0, ch.level_limbs[rl], self.alpha))
+            if math.prod(ch.special_primes[: self.k_low]) <= widest:
+                raise self._errors.InvalidParameters(
+                    f"low_special={self.k_low} special primes do not cover a digit at the "
+                    f"refresh level ({widest.bit_length()} bits)")
+            self.relin_key_low = self._make_ksk(self._mul_all(self.sk.s_full, self.sk.s_full),
+                                                rng, k=self.k_low)
+            self.rotation_keys_low = {}
+            for step in sorted({k % slots for k in self.rotation_indices} - {0}):
+                g = self.galois_for_step[step]
+                s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
+                ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
+                self.rotation_keys_low[g] = self._make_ksk(s_rot, rng, k=self.k_low)
         self._bs_rng = np.random.default_rng(rng_seed + 0x5EED)
 
     # ------------------------------------------------------------------ keys
@@ -269,19 +296,23 @@ class B200CkksCore:
         ch = self.chain
         return ch.mul(a, b, len(ch.all_primes), lmap=ch.all_map())
 
-    def _make_ksk(self, source_ntt: torch.Tensor, rng) -> KeySwitchKey:
+    def _make_ksk(self, source_ntt: torch.Tensor, rng, k: int = None) -> KeySwitchKey:
         """keys.py:49-71 on the device; row j holds P * source on the limbs of
-        digit j (a single limb when alpha == 1, exactly the reference)."""
+        digit j (a single limb when alpha == 1, exactly the reference).  k: key
+        over Q and the first k special primes only (P = their product)."""
         ch = self.chain
-        full = ch.all_primes
+        k = ch.k if k is None else k
+        full = ch.all_primes[: ch.lq + k]
         kl = len(full)
-        amap = ch.all_map()
+        amap = ch.cmap(tuple(range(kl)))
+        special = math.prod(ch.special_primes[:k])
         rows = []
         digits = [(lo, min(lo + self.alpha, ch.lq)) for lo in range(0, ch.lq, self.alpha)]
         out = torch.empty(len(digits), 2, kl, self.n, dtype=U64, device=self.device)
         for j, (lo, hi) in enumerate(digits):
             if self.sampler == "philox":
-                seed = torch.tensor([_mix64(self.rng_seed, 0x4B45590000 + self._ksk_count, j)],
+                tag = 0x4B45590000 if k == ch.k else 0x4C4F570000  # low-P keys: own streams
+                seed = torch.tensor([_mix64(self.rng_seed, tag + self._ksk_count, j)],
                                     dtype=torch.int64, device=self.device).view(U64)
                 a_d, e_d = ch.sample(seed, kl, lmap=amap)
                 a_np = None
@@ -295,11 +326,11 @@ class B200CkksCore:
                 a = ch.upload_u64(a_np)
                 e = ch.from_i64(torch.from_numpy(e_np).to(self.device), kl, amap)[0]
             ch.ntt_fwd(e, kl, amap)
-            b = ch.mul(a, self.sk.s_full, kl, lmap=amap)
+            b = ch.mul(a, self.sk.s_full[:kl].contiguous(), kl, lmap=amap)
             ch.sub(e, b, kl, out=b, lmap=amap)  # b = -a*s + e
             idx = tuple(range(lo, hi))
             lmap = ch.custom_map(idx)
-            pv = ch.scalar_pairs(ch.special_product, idx)
+            pv = ch.scalar_pairs(special, idx)
             msg = ch.scalar_mul(source_ntt[lo:hi].contiguous(), pv, hi - lo, lmap=lmap)
             b[lo:hi] = ch.add(b[lo:hi].contiguous(), msg, hi - lo, lmap=lmap)
             out[j, 0] = b
@@ -321,15 +352,16 @@ class B200CkksCore:
     def _limbs(self, level: int) -> int:
         return self.chain.level_limbs[level]
 
-    def _bconv(self, m: int):
+    def _bconv(self, m: int, k: int = None):
         """ModUp tables for hybrid digits at a ciphertext with m limbs:
         [digit][i][ qhat_i^-1 mod q_i, shoup, ([qhat_i]_{p_e}, shoup) for e in ext ]."""
         if self.alpha == 1:
             return None
-        if m in self._bconv_cache:
-            return self._bconv_cache[m]
         ch = self.chain
-        ext = list(range(m)) + list(range(ch.lq, ch.lq + ch.k))
+        k = ch.k if k is None else k
+        if (m, k) in self._bconv_cache:
+            return self._bconv_cache[(m, k)]
+        ext = list(range(m)) + list(range(ch.lq, ch.lq + k))
         nd = -(-m // self.alpha)
         width = 2 + 2 * len(ext)
         tab = np.zeros((nd, self.alpha, width), dtype=np.uint64)
@@ -348,12 +380,12 @@ class B200CkksCore:
                     tab[j, i, 2 + 2 * e] = c
                     tab[j, i, 3 + 2 * e] = shoup(c, p)
         t = self.chain.publish(torch.from_numpy(tab.reshape(-1)).to(self.device))
-        self._bconv_cache[m] = t
+        self._bconv_cache[(m, k)] = t
         return t
 
     def _key_switch_acc(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
                         key: KeySwitchKey = None, key_ptrs=None, own: torch.Tensor = None,
-                        own_stride: int = 0) -> torch.Tensor:
+                        own_stride: int = 0, k: int = None) -> torch.Tensor:
         """keys.py:74-97: digits of d (coefficient domain, batch items of [m, N]
         at b*d_stride), lifted to Q_l u P, NTT, inner product with the key rows.
         ``own`` is the NTT form of d (items at b*own_stride): a digit's own
@@ -362,16 +394,22 @@ class B200CkksCore:
         (keys.py:98-99) is left to the caller so it can fuse adds/rescales."""
         ch = self.chain
         a = self.alpha
+        k = ch.k if k is None else k
         nd = -(-m // a)
         # own limbs read from the NTT-domain input (a short last digit included);
         # the digits' NTT limb map holds <= 128 rows
-        skip = own is not None and nd * (m + ch.k) - m <= 128
-        digits = ch.modup(d, m, a, self._bconv(m), batch=batch, in_batch_stride=d_stride,
-                          skip_own=skip)
-        basis = ch.digit_basis(m, a, skip)
+        skip = own is not None and nd * (m + k) - m <= 128
+        digits = ch.modup(d, m, a, self._bconv(m, k), batch=batch, in_batch_stride=d_stride,
+                          skip_own=skip, k=k)
+        basis = ch.digit_basis(m, a, skip, k)
         ch.ntt_fwd(digits, len(basis), ch.cmap(basis))
         return ch.ks_inner(digits, m, a, key=key.data if key is not None else None,
-                           key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride)
+                           key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride,
+                           k=k)
+
+    def _low(self, level: int) -> bool:
+        """Key-switch this level with the low special modulus (see __init__)."""
+        return self.k_low is not None and level <= self.params.refresh_level
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
         """backend.py:94-112: restrict to target+1 limbs, multiply by the integer
@@ -539,12 +577,15 @@ class B200CkksCore:
         e = len(ch.entry_primes[level])
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
         d2 = ch.ntt_from(d[:, 2], bsz, m, 3 * m * self.n, inverse=True)
-        acc = self._key_switch_acc(d2, m, batch=bsz, key=self.relin_key, own=d[:, 2],
-                                   own_stride=3 * m * self.n)
+        low = self._low(level)
+        k = self.k_low if low else ch.k
+        acc = self._key_switch_acc(d2, m, batch=bsz,
+                                   key=self.relin_key_low if low else self.relin_key,
+                                   own=d[:, 2], own_stride=3 * m * self.n, k=k)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
-        out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, e, addend=d, addend_polys=2,
+        out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=d, addend_polys=2,
                               addend_period=2, addend_stride=3, addend_tail=tail,
-                              basis=ch.ext_basis(m))
+                              basis=ch.ext_basis(m, k))
         return out.view(bsz, 2, m - e, self.n)
 
     def _payload_rotate(self, a, k: int):
@@ -570,13 +611,16 @@ class B200CkksCore:
         bsz = a.shape[0]
         r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
         c1 = ch.ntt_from(r[:, 1], bsz, m, 2 * m * self.n, inverse=True)
+        k = ch.k
+        if key_ptrs is None and self._low(level) and galois in self.rotation_keys_low:
+            k, key = self.k_low, self.rotation_keys_low[galois]
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
-                                   own_stride=2 * m * self.n)
+                                   own_stride=2 * m * self.n, k=k)
         post = None
         if accumulate:
             post = a if a.is_contiguous() else a.contiguous()
-        out = ch.divround_ntt(acc, 2 * bsz, m + ch.k, ch.k, 0, addend=r, addend_polys=1,
-                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m),
+        out = ch.divround_ntt(acc, 2 * bsz, m + k, k, 0, addend=r, addend_polys=1,
+                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m, k),
                               post=post)
         return out.view(bsz, 2, m, self.n)
 

@@ -115,9 +115,11 @@ class GpuChain:
         """The first m ciphertext limbs."""
         return tuple(range(m))
 
-    def ext_basis(self, m: int) -> tuple:
-        """Ciphertext limbs [0, m) followed by the special primes (keys.py:81)."""
-        return tuple(range(m)) + tuple(range(self.lq, self.lq + self.k))
+    def ext_basis(self, m: int, k: int = None) -> tuple:
+        """Ciphertext limbs [0, m) followed by the (first k) special primes
+        (keys.py:81)."""
+        k = self.k if k is None else k
+        return tuple(range(m)) + tuple(range(self.lq, self.lq + k))
 
     def all_basis(self) -> tuple:
         return tuple(range(len(self.all_primes)))
@@ -132,8 +134,8 @@ class GpuChain:
     def q_map(self, m: int):
         return self.cmap(self.q_basis(m))
 
-    def ext_map(self, m: int):
-        return self.cmap(self.ext_basis(m))
+    def ext_map(self, m: int, k: int = None):
+        return self.cmap(self.ext_basis(m, k))
 
     def all_map(self):
         return self.cmap(self.all_basis())
@@ -327,27 +329,28 @@ class GpuChain:
         return out
 
     def modup(self, d, m: int, alpha: int, bconv, batch: int = None, in_batch_stride: int = 0,
-              skip_own: bool = False, out=None):
+              skip_own: bool = False, out=None, k: int = None):
         """d: batch items of [m][N] (item b at d + b*in_batch_stride elements).
         Returns digits [batch, rows, N]: nd * ext rows, or with skip_own the
         compact layout without each digit's own limbs (len(digit_basis(...)) rows;
         a short last digit keeps ext - width rows)."""
         if batch is None:
             batch = d.numel() // (m * self.n)
-        ext = m + self.k
-        rows = len(self.digit_basis(m, alpha, True)) if skip_own else -(-m // alpha) * ext
+        k = self.k if k is None else k
+        ext = m + k
+        rows = len(self.digit_basis(m, alpha, True, k)) if skip_own else -(-m // alpha) * ext
         out = out if out is not None else torch.empty(batch, rows, self.n, dtype=U64,
                                                       device=self.device)
         _run("modup", (batch * m + batch * rows) * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_modup(self.ring_p, nat.ptr(out), nat.ptr(d), in_batch_stride, batch,
-                              m, self.q_map(m), ext, self.ext_map(m), alpha,
+                              m, self.q_map(m), ext, self.ext_map(m, k), alpha,
                               nat.ptr(bconv) if bconv is not None else None, int(skip_own),
                               nat.stream_handle()), "modup"))
         return out
 
-    def digit_basis(self, m: int, alpha: int, skip_own: bool) -> tuple:
+    def digit_basis(self, m: int, alpha: int, skip_own: bool, k: int = None) -> tuple:
         """Per-row prime indices of a digits tensor [nd][rows] (for its NTT)."""
-        ext = self.ext_basis(m)
+        ext = self.ext_basis(m, k)
         if not skip_own:
             return ext
         nd = -(-m // alpha)
@@ -359,24 +362,25 @@ class GpuChain:
 
     def ks_inner(self, digits, m: int, alpha: int = 1, key: torch.Tensor = None,
                  key_ptrs: torch.Tensor = None, own: torch.Tensor = None, own_bstride: int = 0,
-                 out=None):
+                 out=None, k: int = None):
         """digits: ckb_modup's output ([batch, rows, N]; skip_own layout when own
         is given)."""
         batch = digits.shape[0]
         nd = -(-m // alpha)
-        ext = m + self.k
+        k = self.k if k is None else k
+        ext = m + k
         out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
                                                       device=self.device)
-        key_limbs = len(self.all_primes)
+        key_limbs = self.lq + k  # keys over Q u (first k special primes)
         n_keys = batch if key_ptrs is not None else 1
         nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext  # own rows counted as read
         _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
             nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
-                                 self.ext_map(m), alpha, m,
+                                 self.ext_map(m, k), alpha, m,
                                  nat.ptr(own) if own is not None else None, own_bstride,
                                  nat.ptr(key) if key is not None else None,
                                  nat.ptr(key_ptrs) if key_ptrs is not None else None,
-                                 key_limbs, self.ext_map(m), nat.stream_handle()), "ks_inner"))
+                                 key_limbs, self.ext_map(m, k), nat.stream_handle()), "ks_inner"))
         return out
 
     def divround(self, x, polys: int, limbs: int, n1: int, n2: int = 0, addend=None,

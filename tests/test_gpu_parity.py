@@ -454,6 +454,41 @@ def test_moddown_fast_conversion_paths_agree():
         assert np.array_equal(x, y) and np.array_equal(x, z)
 
 
+def test_low_special_modulus_keyswitch():
+    """Level-aware special modulus (low_special): at or below the refresh level
+    multiplies and rotations key-switch over Q u P' (first k' special primes)
+    and decrypt like the full-P key switch; above it the full P is used, and
+    a P' narrower than a digit is rejected."""
+    n, L, bd = 1 << 10, 6, 2
+    chain = (60,) + (45,) * (L - bd) + (60,) * bd + (360,)
+    params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=45, level=L,
+                          bootstrap_depth=bd)
+    opts = dict(backend="ckks", rng_seed=3, prime_layout="bootstrap", dnum=3, secret_hw=64)
+    full = he_api.keygen(params, {1}, **opts)
+    low = he_api.keygen(params, {1}, low_special=4, **opts)
+    assert low.backend.k_low == 4 and full.backend.k_low is None
+    rl = params.refresh_level
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-1, 1, n // 2)
+    w = rng.uniform(-1, 1, n // 2)
+    for cust in (full, low):
+        be = cust.backend
+        a = cust.encrypt(he_api.make_plain(v, n // 2, 45.0))
+        b = cust.encrypt(he_api.make_plain(w, n // 2, 45.0))
+        ev = cust.evaluator
+        # bring both to the refresh level, then multiply and rotate there
+        while a.level_remaining > rl:
+            a = ev.mul(a, cust.encrypt(he_api.make_plain(np.ones(n // 2), n // 2, 45.0)))
+            b = ev.mul(b, cust.encrypt(he_api.make_plain(np.ones(n // 2), n // 2, 45.0)))
+        assert be._low(a.level_remaining) == (cust is low)
+        prod = cust.decrypt(ev.mul(a, b)).values
+        rot = cust.decrypt(ev.rotate(a, 1)).values
+        assert np.max(np.abs(prod - v * w)) < 1e-6
+        assert np.max(np.abs(rot - np.roll(v, -1))) < 1e-6
+    with pytest.raises(Exception):
+        he_api.keygen(params, {1}, low_special=1, **opts)
+
+
 # ---------------------------------------------------------------------------
 # Decryption tolerances (tests/test_ckks_backend.py of the reference)
 # ---------------------------------------------------------------------------

@@ -9,6 +9,11 @@ from paper_2506_19693_b200.executor import WaveExecutor
 from paper_2506_19693_b200.scheme import SchemeParams
 
 
+# training steps below the refresh level key-switch over Q u P' with P' the
+# first 7 special primes (7 x 60 bits, above the widest digit there; see
+# backend.B200CkksCore low_special); bootstrapping keeps the full P
+LOW_SPECIAL = 7
+
 def run(reps=2, verbose=True, graph=True, special=660):
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c4_trace.npz")
     z = np.load(path); prog = Program.load(path)
@@ -17,7 +22,8 @@ def run(reps=2, verbose=True, graph=True, special=660):
                           scale_bits=45, level=L, bootstrap_depth=bd)
     t0 = time.perf_counter()
     cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=4,
-                         prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True)
+                         prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True,
+                         low_special=LOW_SPECIAL)
     torch.cuda.synchronize(); keygen_s = time.perf_counter() - t0
     env = prog.run(cust, 0, prog.n_setup)
     ex = WaveExecutor(prog, cust)
