@@ -187,7 +187,7 @@ class B200CkksCore:
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
                  conjugation_key: bool = False, real_bootstrap: bool = False,
-                 sampler: str = None, low_special: int = None):
+                 sampler: str = None, low_special=None):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -256,33 +256,46 @@ class B200CkksCore:
             s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
             ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
             self.rotation_keys[g] = self._make_ksk(s_rot, rng)
-        # Level-aware special modulus: ciphertexts at or below the refresh level
-        # (whose digits are at most q0 + (alpha-1) user primes) key-switch with
-        # the first `low_special` special primes only — P' >= the widest such
-        # digit keeps the key-switch noise ~N*sigma, far below the 2^scale_bits
-        # scale — so the ModUp / inner product / ModDown of every training-step
-        # multiply and rotation carry fewer 60-bit limbs.  A second relin key and
-        # rotation keys for the user steps over Q u P'; bootstrapping (above the
-        # refresh level) keeps the full P.  Off by default (the parity tests pin
-        # the full-P semantics).
+        # Level-aware special modulus: a ciphertext at level l key-switches over
+        # Q u P' with P' the first k(l) special primes, P' above the widest
+        # digit at l (the key-switch noise then stays ~N*sigma, far below the
+        # scale), so the ModUp / inner product / ModDown of the training steps'
+        # multiplies and rotations carry fewer 60-bit limbs.  low_special: an
+        # int k' (levels <= refresh level) or tiers [(max_level, k), ...]; own
+        # relin and rotation keys (user steps) per k.  Bootstrapping always
+        # uses the full P (its precision budget assumes 2^120 of headroom).
+        # Off by default (the parity tests pin the full-P semantics).
         self.k_low = None
-        if low_special is not None and 0 < int(low_special) < ch.k:
-            self.k_low = int(low_special)
-            rl = params.refresh_level
-            widest = max(math.prod(ch.all_primes[lo:min(lo + self.alpha, ch.level_limbs[rl])])
-                         for lo in range(0, ch.level_limbs[rl], self.alpha))
-            if math.prod(ch.special_primes[: self.k_low]) <= widest:
-                raise self._errors.InvalidParameters(
-                    f"low_special={self.k_low} special primes do not cover a digit at the "
-                    f"refresh level ({widest.bit_length()} bits)")
-            self.relin_key_low = self._make_ksk(self._mul_all(self.sk.s_full, self.sk.s_full),
-                                                rng, k=self.k_low)
-            self.rotation_keys_low = {}
-            for step in sorted({k % slots for k in self.rotation_indices} - {0}):
-                g = self.galois_for_step[step]
-                s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
-                ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
-                self.rotation_keys_low[g] = self._make_ksk(s_rot, rng, k=self.k_low)
+        self._ks_tiers = []
+        self._force_full_p = False
+        self.relin_keys_k: dict = {}
+        self.rotation_keys_k: dict = {}
+        if low_special is not None:
+            tiers = ([(params.refresh_level, int(low_special))] if isinstance(low_special, int)
+                     else sorted((int(l), int(k)) for l, k in low_special))
+            for max_level, kk in tiers:
+                if not 0 < kk < ch.k:
+                    continue
+                m = ch.level_limbs[min(max_level, params.level)]
+                widest = max(math.prod(ch.all_primes[lo:min(lo + self.alpha, m)])
+                             for lo in range(0, m, self.alpha))
+                if math.prod(ch.special_primes[:kk]) <= widest:
+                    raise self._errors.InvalidParameters(
+                        f"low_special: {kk} special primes do not cover a digit at level "
+                        f"{max_level} ({widest.bit_length()} bits)")
+                self._ks_tiers.append((max_level, kk))
+                if kk in self.relin_keys_k:
+                    continue
+                self.relin_keys_k[kk] = self._make_ksk(
+                    self._mul_all(self.sk.s_full, self.sk.s_full), rng, k=kk)
+                rk = self.rotation_keys_k[kk] = {}
+                for step in sorted({k % slots for k in self.rotation_indices} - {0}):
+                    g = self.galois_for_step[step]
+                    s_rot = ch.automorphism(s_coeff, g, len(ch.all_primes), lmap=ch.all_map())
+                    ch.ntt_fwd(s_rot, len(ch.all_primes), ch.all_map())
+                    rk[g] = self._make_ksk(s_rot, rng, k=kk)
+            if self._ks_tiers:
+                self.k_low = self._ks_tiers[0][1]
         self._bs_rng = np.random.default_rng(rng_seed + 0x5EED)
 
     # ------------------------------------------------------------------ keys
@@ -407,9 +420,16 @@ class B200CkksCore:
                            key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride,
                            k=k)
 
+    def _ks_k(self, level: int) -> int:
+        """Special primes a key switch at this level uses (see __init__)."""
+        if not self._force_full_p:
+            for max_level, kk in self._ks_tiers:
+                if level <= max_level:
+                    return kk
+        return self.chain.k
+
     def _low(self, level: int) -> bool:
-        """Key-switch this level with the low special modulus (see __init__)."""
-        return self.k_low is not None and level <= self.params.refresh_level
+        return self._ks_k(level) != self.chain.k
 
     def _adjust_to_level(self, ct: GpuCiphertext, target: int) -> GpuCiphertext:
         """backend.py:94-112: restrict to target+1 limbs, multiply by the integer
@@ -577,10 +597,9 @@ class B200CkksCore:
         e = len(ch.entry_primes[level])
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
         d2 = ch.ntt_from(d[:, 2], bsz, m, 3 * m * self.n, inverse=True)
-        low = self._low(level)
-        k = self.k_low if low else ch.k
+        k = self._ks_k(level)
         acc = self._key_switch_acc(d2, m, batch=bsz,
-                                   key=self.relin_key_low if low else self.relin_key,
+                                   key=self.relin_keys_k[k] if k != ch.k else self.relin_key,
                                    own=d[:, 2], own_stride=3 * m * self.n, k=k)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
         out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=d, addend_polys=2,
@@ -612,8 +631,9 @@ class B200CkksCore:
         r = ch.automorphism_ntt(a, galois, g_items=g_items, rows_per_item=2 * m)
         c1 = ch.ntt_from(r[:, 1], bsz, m, 2 * m * self.n, inverse=True)
         k = ch.k
-        if key_ptrs is None and self._low(level) and galois in self.rotation_keys_low:
-            k, key = self.k_low, self.rotation_keys_low[galois]
+        kk = self._ks_k(level)
+        if key_ptrs is None and kk != ch.k and galois in self.rotation_keys_k[kk]:
+            k, key = kk, self.rotation_keys_k[kk][galois]
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
                                    own_stride=2 * m * self.n, k=k)
         post = None
@@ -836,7 +856,15 @@ class B200CkksCore:
         return self.bootstrap_ct(GpuCiphertext(data, level)).data
 
     def bootstrap_ct(self, ct: GpuCiphertext) -> GpuCiphertext:
-        """Homomorphic bootstrapping of a payload (any level) to refresh_level."""
+        """Homomorphic bootstrapping of a payload (any level) to refresh_level
+        (always over the full special modulus)."""
+        prev, self._force_full_p = self._force_full_p, True
+        try:
+            return self._bootstrap_ct(ct)
+        finally:
+            self._force_full_p = prev
+
+    def _bootstrap_ct(self, ct: GpuCiphertext) -> GpuCiphertext:
         if self._bootstrapper is None:
             from .bootstrap import Bootstrapper
 

@@ -9,10 +9,11 @@ from paper_2506_19693_b200.executor import WaveExecutor
 from paper_2506_19693_b200.scheme import SchemeParams
 
 
-# training steps below the refresh level key-switch over Q u P' with P' the
-# first 7 special primes (7 x 60 bits, above the widest digit there; see
-# backend.B200CkksCore low_special); bootstrapping keeps the full P
-LOW_SPECIAL = 7
+# training-step key switches over Q u P' with P' the first special primes above
+# the widest digit of the level (backend.B200CkksCore low_special): levels <= 8 (digits <= 375 bits) over 7 x 60-bit special primes, levels 9..24
+# (digits <= 480 bits) over 9;
+# bootstrapping keeps the full P
+LOW_SPECIAL = [(8, 7), (24, 9)]
 
 def run(reps=2, verbose=True, graph=True, special=660):
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c4_trace.npz")

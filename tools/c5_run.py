@@ -11,10 +11,11 @@ from paper_2506_19693_b200.executor import WaveExecutor
 from paper_2506_19693_b200.scheme import SchemeParams
 
 
-# training steps below the refresh level key-switch over Q u P' with P' the
-# first 9 special primes (9 x 60 bits, above the widest digit there; see
-# backend.B200CkksCore low_special); bootstrapping keeps the full P
-LOW_SPECIAL = 9
+# training-step key switches over Q u P' with P' the first special primes above
+# the widest digit of the level (backend.B200CkksCore low_special): levels <= 16 (digits <= 510 bits) over 9 x 60-bit special primes, levels
+# 17..32 (digits <= 660 bits) over 12;
+# bootstrapping keeps the full P
+LOW_SPECIAL = [(16, 9), (32, 12)]
 
 def run(reps=1, max_group=64, verbose=True, special=780, graph=True):
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
