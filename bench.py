@@ -14,8 +14,11 @@ metric  = BASELINE's "encrypted train ms/step; bootstrap ms; keyswitch GB/s vs
           per batch) / their device time, in GB/s.
 Extra keys: per-stage times, NTT GB/s, the roofline of the dominant kernel,
 the config-1 encrypted training step (ms/step, replayed reference
-train_iteration; decrypted weights vs the reference), e2e through host
-buffers, the CPU oracle baseline, clocks.
+train_iteration; decrypted weights vs the reference), config-3 bootstrapping
+(ms, one CUDA graph), configs 4 / 5 (ms/step as the mean over their 8 / 5
+steps: the recorded first step and the recorded steady-state second step,
+decrypted weights vs the exact model), e2e through host buffers, the CPU
+oracle baseline, clocks.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
