@@ -832,7 +832,7 @@ __device__ __noinline__ uint64_t exact_rho(const uint64_t* __restrict__ src, siz
   return top > 0 ? fl : fl + 1;
 }
 
-template <int D1, int D2>
+template <int D1, int D2, int V>
 __global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
     int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
@@ -868,30 +868,42 @@ __global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
     dinv[u] = 1.0 / (double)p;
   }
   __syncthreads();
-  const size_t total = (size_t)polys * N;
+  const size_t per = N / V;
+  const size_t total = (size_t)polys * per;
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = t & (N - 1);
-    const size_t pidx = t >> log_n;
+    const size_t n = (t % per) * V;
+    const size_t pidx = t / per;
     const uint64_t* src = T + pidx * trows * N + n;
-    uint64_t y[D1];
-    double f = 0.0;
+    uint64_t y[D1][V];
+    double f[V];
+#pragma unroll
+    for (int c = 0; c < V; ++c) f[c] = 0.0;
 #pragma unroll
     for (int u = 0; u < D1; ++u) {
       if (u < n1) {
-        y[u] = ckb::mul_shoup(src[(size_t)(limbs - 1 - u - m2) * N], dsm[3 * u], dsm[3 * u + 1],
-                              dsm[3 * u + 2]);
-        f = fma((double)y[u], dinv[u], f);
+        uint64_t x[V];
+        ld_v<V>(x, src + (size_t)(limbs - 1 - u - m2) * N);
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          y[u][c] = ckb::mul_shoup(x[c], dsm[3 * u], dsm[3 * u + 1], dsm[3 * u + 2]);
+          f[c] = fma((double)y[u][c], dinv[u], f[c]);
+        }
       } else {
-        y[u] = 0;
+#pragma unroll
+        for (int c = 0; c < V; ++c) y[u][c] = 0;
       }
     }
-    const double rho_d = rint(f);
-    const uint64_t rho = fabs(f - rho_d) < margin  // 0.5 - 2^-30 (ckb_debug_hps_margin)
-                             ? (uint64_t)rho_d
-                             : exact_rho(src, N, limbs, m2, n1, f, tab1, R, lm);
-    int64_t r2[D2 > 0 ? D2 : 1];
+    uint64_t rho[V];
+#pragma unroll
+    for (int c = 0; c < V; ++c) {
+      const double rho_d = rint(f[c]);
+      rho[c] = fabs(f[c] - rho_d) < margin  // 0.5 - 2^-30 (ckb_debug_hps_margin)
+                   ? (uint64_t)rho_d
+                   : exact_rho(src + c, N, limbs, m2, n1, f[c], tab1, R, lm);
+    }
+    int64_t r2[D2 > 0 ? D2 : 1][V];
 #pragma unroll
     for (int d = 0; d < D2; ++d) {
       if (d < n2) {
@@ -899,21 +911,27 @@ __global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
         const uint64_t* mm = R.mods + (size_t)lm.p[li] * kModStride;
         const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
         const uint64_t* Ta = tab1 + (size_t)li * s1;
-        // (x - c1) P1^-1 = x P1^-1 - E1 at this limb
-        uint64_t v = ckb::mul_shoup(src[(size_t)(li - m2) * N], __ldg(Ta + 2 * n1),
-                                    __ldg(Ta + 2 * n1 + 1), m.p);
         const uint64_t* H = tabH + (size_t)li * n1;
-        uint64_t h = 0, l = (m.p << (__clzll((long long)m.p) - 4)) - rho;  // + multiple of p
-#pragma unroll
-        for (int u = 0; u < D1; ++u)
-          if (u < n1) ckb::mac128(h, l, y[u], __ldg(H + u));
-        v = ckb::sub_mod(v, ckb::reduce128_any(h, l, __ldg(mm + 8), __ldg(mm + 9), m), m.p);
-        if (has_add) v = ckb::add_mod(v, src[(size_t)(n1 + n2 + li - m2) * N], m.p);
         const uint64_t* Tb = tab2 + (size_t)li * s2;
+        uint64_t xv[V], av[V];
+        ld_v<V>(xv, src + (size_t)(li - m2) * N);
+        if (has_add) ld_v<V>(av, src + (size_t)(n1 + n2 + li - m2) * N);
 #pragma unroll
-        for (int u = 0; u < D2; ++u)
-          if (u < d) v = sub_rm(v, r2[u], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), m.p);
-        r2[d] = centered(ckb::mul_shoup(v, __ldg(Tb + 2 * n2), __ldg(Tb + 2 * n2 + 1), m.p), m.p);
+        for (int c = 0; c < V; ++c) {
+          // (x - c1) P1^-1 = x P1^-1 - E1 at this limb
+          uint64_t v = ckb::mul_shoup(xv[c], __ldg(Ta + 2 * n1), __ldg(Ta + 2 * n1 + 1), m.p);
+          uint64_t h = 0, l = (m.p << (__clzll((long long)m.p) - 4)) - rho[c];  // + k p
+#pragma unroll
+          for (int u = 0; u < D1; ++u)
+            if (u < n1) ckb::mac128(h, l, y[u][c], __ldg(H + u));
+          v = ckb::sub_mod(v, ckb::reduce128_any(h, l, __ldg(mm + 8), __ldg(mm + 9), m), m.p);
+          if (has_add) v = ckb::add_mod(v, av[c], m.p);
+#pragma unroll
+          for (int u = 0; u < D2; ++u)
+            if (u < d) v = sub_rm(v, r2[u][c], __ldg(Tb + 2 * u), __ldg(Tb + 2 * u + 1), m.p);
+          r2[d][c] =
+              centered(ckb::mul_shoup(v, __ldg(Tb + 2 * n2), __ldg(Tb + 2 * n2 + 1), m.p), m.p);
+        }
       }
     }
     uint64_t* dst = E + pidx * m2 * N + n;
@@ -922,16 +940,36 @@ __global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
       const uint64_t* Te = S + 6;
       const uint64_t* H = Te + sE;
       const int64_t off = (int64_t)Te[2 * (n1 + n2)];  // C_j: multiple of q_j in [2^59, 2^61)
-      uint64_t h = 0, l = (uint64_t)off - rho;
+      uint64_t h[V], l[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        h[c] = 0;
+        l[c] = (uint64_t)off - rho[c];
+      }
 #pragma unroll
       for (int u = 0; u < D1; ++u)
-        if (u < n1) ckb::mac128(h, l, y[u], H[u]);
+        if (u < n1) {
+          const uint64_t hu = H[u];
+#pragma unroll
+          for (int c = 0; c < V; ++c) ckb::mac128(h[c], l[c], y[u][c], hu);
+        }
 #pragma unroll
       for (int u = 0; u < D2; ++u)
-        if (u < n2) ckb::mac128(h, l, (uint64_t)(r2[u] + off), Te[2 * (n1 + u)]);
+        if (u < n2) {
+          const uint64_t tu = Te[2 * (n1 + u)];
+#pragma unroll
+          for (int c = 0; c < V; ++c) ckb::mac128(h[c], l[c], (uint64_t)(r2[u][c] + off), tu);
+        }
       const Mod m{S[0], S[1], S[2], S[3]};
-      dst[(size_t)j * N] = m.k >= 32 ? ckb::reduce128_big(h, l, S[4], S[5], m)
-                                     : ckb::reduce128_any(h, l, S[4], S[5], m);
+      uint64_t o[V];
+      if (m.k >= 32) {  // warp-uniform
+#pragma unroll
+        for (int c = 0; c < V; ++c) o[c] = ckb::reduce128_big(h[c], l[c], S[4], S[5], m);
+      } else {
+#pragma unroll
+        for (int c = 0; c < V; ++c) o[c] = ckb::reduce128_any(h[c], l[c], S[4], S[5], m);
+      }
+      st_v<V>(dst + (size_t)j * N, o);
     }
   }
 }
@@ -1660,10 +1698,11 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
     if (smh > 200 * 1024) return CKB_E_ARG;
 #define CKB_DH(A, B)                                                                        \
   if (d1 == A && d2 == B) {                                                                 \
+    constexpr int VV = A <= 8 ? 2 : 1; /* narrow drops: two coefficients per thread */      \
     if (smh > 48 * 1024)                                                                    \
-      cudaFuncSetAttribute(k_divround_corr_hps<A, B>,                                       \
+      cudaFuncSetAttribute(k_divround_corr_hps<A, B, VV>,                                   \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh);          \
-    k_divround_corr_hps<A, B><<<grid_for(total, 256), 256, smh, st0>>>(                     \
+    k_divround_corr_hps<A, B, VV><<<grid_for(total / VV, 256), 256, smh, st0>>>(            \
         E, T, has_addend, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
         tabE, tabH, g_hps_margin);                                                          \
     return finish();                                                                        \
