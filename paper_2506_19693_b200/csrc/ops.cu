@@ -1698,7 +1698,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
     if (smh > 200 * 1024) return CKB_E_ARG;
 #define CKB_DH(A, B)                                                                        \
   if (d1 == A && d2 == B) {                                                                 \
-    constexpr int VV = A <= 8 ? 2 : 1; /* narrow drops: two coefficients per thread */      \
+    constexpr int VV = A <= 11 ? 2 : 1; /* narrow drops: two coefficients per thread */     \
     if (smh > 48 * 1024)                                                                    \
       cudaFuncSetAttribute(k_divround_corr_hps<A, B, VV>,                                   \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh);          \
