@@ -508,15 +508,15 @@ def main():
         s_hm.wait_stream(cur)
         s_hr.wait_stream(cur)
         # two concurrent streams share the L2: each transform chunk gets half
-        # of the single-stream budget (ckb_set_ntt_chunk_bytes)
-        prev = nat_.LIB.ckb_set_ntt_chunk_bytes(48 << 20)
+        # of the single-stream budget (ckb_ring.ntt_chunk_bytes)
+        prev = be.chain.set_ntt_chunk_bytes(48 << 20)
         try:
             with torch.cuda.stream(s_hm):
                 be.batch_hmult(A, B, lvl)
             with torch.cuda.stream(s_hr):
                 be.batch_hrot(A, steps_rot, lvl)
         finally:
-            nat_.LIB.ckb_set_ntt_chunk_bytes(prev)
+            be.chain.set_ntt_chunk_bytes(prev)
         cur.wait_stream(s_hm)
         cur.wait_stream(s_hr)
 

@@ -56,7 +56,22 @@ typedef struct {
    * radix-16 kernel (host-side copy of the class the kernels derive from p;
    * all zero = one kernel choosing the path per row, same results). */
   uint64_t f64_mask[2];
+  /* L2 budget of the two-phase transforms (N > 4096): rows are processed in
+   * chunks of this many bytes so the intermediate stays in L2 between the
+   * phases.  0 = 96 MB (one stream); give each of several concurrent streams a
+   * share (the caller owns this struct; the library keeps no state). */
+  uint64_t ntt_chunk_bytes;
+  /* CKB_RING_* bits: configuration read at every call, never stored. */
+  uint32_t flags;
+  uint32_t reserved;
 } ckb_ring;
+
+/* ckb_ring.flags */
+#define CKB_RING_HPS_EXACT 1u /* test hook: settle every rho of the fast-conversion
+                                 ModDown correction via the exact mixed-radix path */
+#define CKB_RING_NTT_SPLIT 2u /* run FP64-class and integer-class NTT rows of one
+                                 call as two kernels instead of one per-CTA-dispatch
+                                 kernel (same integers; A/B measurements) */
 
 /* Library version (for load checks). */
 int ckb_version(void);
@@ -76,11 +91,6 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
  * Replaces NttPlan.inverse (ckks/ntt.py:138-154) / RingElement.to_coeff (ring.py:117-123). */
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream);
-/* L2 budget of the two-phase transforms (N > 4096): rows are processed in
- * chunks of this many bytes so the intermediate stays in L2 between the
- * phases (default 96 MB, one stream).  Process-global; 0 only queries.
- * Returns the previous value.  Give each of several concurrent streams a share. */
-uint64_t ckb_set_ntt_chunk_bytes(uint64_t bytes);
 /* Out-of-place forms: dst ([rows][N], contiguous) = NTT / iNTT of the rows of
  * src, row r = (item r / limbs, limb r % limbs) read at
  * src + item*src_item_stride + limb*N (0: limbs*N).  The transform's first pass
@@ -207,10 +217,8 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
  * basis conversion, c1 = sum_u y_u (P1/p_u) - rho P1 with rho = round(sum y_u/p_u)
  * in FP64; coefficients whose rounding is within 2^-30 of ambiguous take the
  * mixed-radix path, so E is bit-identical either way. */
-/* Test hook: the |frac(sum y_u/p_u) - 1/2| margin below which ckb_divround_ntt_corr
- * settles rho exactly (default 0.5 - 2^-30; 0 sends every coefficient through
- * the exact path).  Process-global; returns CKB_E_ARG outside [0, 0.5]. */
-int ckb_debug_hps_margin(double margin);
+/* (ckb_ring.flags & CKB_RING_HPS_EXACT sends every coefficient through the
+ * exact path; default margin |frac - 1/2| < 2^-30.) */
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
                           int n_drop2, const uint64_t* tab1, const uint64_t* tab2,

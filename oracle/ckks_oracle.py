@@ -323,6 +323,18 @@ def _P(p):
     return np.uint64(p) if p < (1 << 31) else p
 
 
+def _obj(plane) -> np.ndarray:
+    """A limb as an object array of exact Python ints (vectorised big-int math)."""
+    return np.array([int(v) for v in plane.tolist()], dtype=object)
+
+
+def _centered(plane, q: int) -> np.ndarray:
+    """Centred representative of residues mod q (keys.py:85-89, ring.py:171-175:
+    values above q // 2 map to v - q), as Python ints."""
+    d = _obj(plane)
+    return np.where(d > q // 2, d - q, d)
+
+
 def e_add(a: Elem, b: Elem) -> Elem:
     assert a.primes == b.primes and a.ntt == b.ntt
     return Elem(a.primes, [(x + y) % _P(p) for x, y, p in zip(a.planes, b.planes, a.primes)], a.ntt)
@@ -376,14 +388,13 @@ def divide_round_by_prime(a: Elem, drop: int) -> Elem:
     """ring.py:165-183: exact centered divide-and-round by one limb."""
     assert not a.ntt
     di = a.primes.index(drop)
-    digit = [int(v) for v in a.planes[di].tolist()]
-    digit = [v - drop if v > drop // 2 else v for v in digit]
+    digit = _centered(a.planes[di], drop)
     keep = [i for i in range(len(a.primes)) if i != di]
     primes = tuple(a.primes[i] for i in keep)
     out = []
     for i in keep:
         p = a.primes[i]
-        r = as_limb([v % p for v in digit], p)
+        r = as_limb(digit % p, p)
         inv = pow(drop, -1, p)
         out.append((a.planes[i] + (_P(p) - r)) % _P(p) * _P(inv) % _P(p))
     return Elem(primes, out, False)
@@ -545,18 +556,16 @@ def modup_digit(d: Elem, lo: int, hi: int, ext, centered: bool = True) -> Elem:
                y_i = [x_i * qhat_i^-1]_{q_i}, out_p = sum_i y_i * [qhat_i]_p
                (the digit's own limbs are copied).
     """
-    n = len(d.planes[0])
     if centered:
         assert hi - lo == 1
         q = d.primes[lo]
-        digit = [int(v) for v in d.planes[lo].tolist()]
-        digit = [v - q if v > q // 2 else v for v in digit]
+        digit = _centered(d.planes[lo], q)
         planes = []
         for p in ext:
             if p == q:
                 planes.append(d.planes[lo].copy())
             else:
-                planes.append(as_limb([v % p for v in digit], p))
+                planes.append(as_limb(digit % p, p))
         return Elem(tuple(ext), planes, False)
     qs = d.primes[lo:hi]
     Qj = math.prod(qs)
@@ -564,18 +573,14 @@ def modup_digit(d: Elem, lo: int, hi: int, ext, centered: bool = True) -> Elem:
     for i, q in enumerate(qs):
         qhat = Qj // q
         inv = pow(qhat % q, -1, q)
-        ys.append([int(v) * inv % q for v in d.planes[lo + i].tolist()])
+        ys.append(_obj(d.planes[lo + i]) * inv % q)
     planes = []
     for p in ext:
         if p in qs:
             planes.append(d.planes[d.primes.index(p)].copy())
             continue
-        consts = [(Qj // q) % p for q in qs]
-        acc = [0] * n
-        for y, c in zip(ys, consts):
-            for k in range(n):
-                acc[k] += y[k] * c
-        planes.append(as_limb([v % p for v in acc], p))
+        acc = sum(y * ((Qj // q) % p) for y, q in zip(ys, qs))
+        planes.append(as_limb(acc % p, p))
     return Elem(tuple(ext), planes, False)
 
 

@@ -24,7 +24,13 @@ c_vp = ctypes.c_void_p
 class CkbRing(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n_primes", ctypes.c_uint32),
                 ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp),
-                ("f64_mask", ctypes.c_uint64 * 2)]
+                ("f64_mask", ctypes.c_uint64 * 2), ("ntt_chunk_bytes", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+RING_HPS_EXACT = 1  # ckb_ring.flags (include/ckks_b200.h)
+RING_NTT_SPLIT = 2
+DEFAULT_NTT_CHUNK_BYTES = 96 << 20
 
 
 F64_PRIME_LIMIT = 1 << 46  # csrc/ntt.cu: primes below run the FP64 butterflies
@@ -60,7 +66,6 @@ def _load():
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      c_i32p, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp,
                                      ctypes.c_int64, c_vp], ctypes.c_int),
-        "ckb_set_ntt_chunk_bytes": ([ctypes.c_uint64], ctypes.c_uint64),
         "ckb_ntt_forward_from": ([R, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                   c_i32p, c_vp], ctypes.c_int),
         "ckb_ntt_inverse_from": ([R, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
@@ -89,7 +94,6 @@ def _load():
                               c_vp, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_from_i64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_to_f64": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
-        "ckb_debug_hps_margin": ([ctypes.c_double], ctypes.c_int),
         "ckb_divround_ntt_corr": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p,
                                    ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp],
                                   ctypes.c_int),
@@ -124,10 +128,10 @@ def _load():
 
 LIB = _load()
 EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inverse",
-            "ckb_set_ntt_chunk_bytes", "ckb_ntt_forward_combine", "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
+            "ckb_ntt_forward_combine", "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
             "ckb_elementwise", "ckb_pt_mac", "ckb_scalar_mac", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
-            "ckb_debug_hps_margin", "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
+            "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
             "ckb_automorphism_ntt",
             "ckb_reduce", "ckb_sample", "ckb_alu_probe",
             "ckb_alu_probe_f64")

@@ -28,6 +28,8 @@ Extra keyword options (all default to the reference's behaviour):
   secret_hw     None = dense ternary (ring.py:161-162); h = ternary with exactly
                 h non-zeros (BASELINE configs: 64 / 192)
   device        CUDA device (default: current)
+  encoder       "device" (cuFFT) | "numpy" (the reference's host FFT, bit-identical
+                encodings/decodings: mode-A whole-step parity tests only)
 """
 
 from __future__ import annotations
@@ -90,11 +92,19 @@ class GpuCiphertext:
 
 class DeviceEncoder:
     """Canonical embedding with the rotation-friendly 5^i slot order
-    (encoding.py:17-76), evaluated with cuFFT in float64 on the device."""
+    (encoding.py:17-76), evaluated with cuFFT in float64 on the device.
 
-    def __init__(self, n: int, device):
+    host=True (backend option encoder="numpy", for mode-A whole-step bit
+    identity only): the float64 FFTs run with numpy on the host exactly as
+    encoding.py:34-54 writes them, so encodings and decodings round like the
+    reference's (cuFFT and pocketfft differ in the last ulp, which moves a
+    rint by one in ~1 coefficient per encode).  The integer work around it
+    (residues, NTT, the CRT lift) stays on the device."""
+
+    def __init__(self, n: int, device, host: bool = False):
         self.n = n
         self.device = device
+        self.host = bool(host)
         slots = n // 2
         exps = np.empty(slots, dtype=np.int64)
         e = 1
@@ -106,11 +116,29 @@ class DeviceEncoder:
         self.bins = torch.from_numpy(self.bins_np).to(device)
         self.conj_bins = torch.from_numpy(self.conj_bins_np).to(device)
         twist = np.exp(1j * np.pi * np.arange(n) / n)
+        self.twist_np = twist
+        self.untwist_np = np.conj(twist)
         self.twist = torch.from_numpy(twist).to(device)
         self.untwist = torch.from_numpy(np.conj(twist)).to(device)
 
+    def _embed_host(self, rows: np.ndarray, scale: float) -> torch.Tensor:
+        """encoding.py:34-49 per row (numpy), -> rounded float64 on the device."""
+        out = np.empty((rows.shape[0], self.n))
+        for i, vals in enumerate(rows):
+            v = np.zeros(self.n // 2)
+            v[: vals.shape[0]] = vals
+            spectrum = np.zeros(self.n, dtype=np.complex128)
+            scaled = v * scale
+            spectrum[self.bins_np] = scaled
+            spectrum[self.conj_bins_np] = scaled
+            w = np.fft.fft(spectrum) / self.n
+            out[i] = np.rint(np.real(w * self.untwist_np))
+        return _h2d(out, self.device)
+
     def embed_device(self, values, scale: float) -> torch.Tensor:
         """Real slots -> int64 coefficients [N] on the device (encoding.py:34-49)."""
+        if self.host:
+            return self._embed_host(np.asarray(values, dtype=np.float64)[None], scale)[0]
         v = _h2d(np.asarray(values, dtype=np.float64), self.device)
         spec = torch.zeros(self.n, dtype=torch.complex128, device=self.device)
         scaled = torch.zeros(self.n // 2, dtype=torch.float64, device=self.device)
@@ -122,6 +150,8 @@ class DeviceEncoder:
 
     def embed_device_batch(self, values: np.ndarray, scale: float) -> torch.Tensor:
         """[B, <= N/2] real slot rows -> [B, N] coefficients (one batched FFT)."""
+        if self.host:
+            return self._embed_host(np.asarray(values, dtype=np.float64), scale)
         v = _h2d(np.asarray(values, dtype=np.float64), self.device)
         b = v.shape[0]
         spec = torch.zeros(b, self.n, dtype=torch.complex128, device=self.device)
@@ -150,6 +180,14 @@ class DeviceEncoder:
         return coeffs.to(torch.int64).cpu().numpy()
 
     def unembed_device(self, coeffs: torch.Tensor, scale: float) -> torch.Tensor:
+        if self.host:  # encoding.py:51-55 per row (numpy)
+            c = coeffs.cpu().numpy()
+            rows = c.reshape(-1, self.n)
+            out = np.empty((rows.shape[0], self.n // 2))
+            for i, r in enumerate(rows):
+                spectrum = np.fft.ifft(r.astype(np.float64) * self.twist_np) * self.n
+                out[i] = np.real(spectrum[self.bins_np]) / scale
+            return torch.from_numpy(out.reshape(*c.shape[:-1], self.n // 2))
         w = coeffs.to(torch.complex128) * self.twist
         spec = torch.fft.ifft(w) * self.n
         return torch.real(spec[..., self.bins]) / scale
@@ -187,7 +225,7 @@ class B200CkksCore:
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
                  conjugation_key: bool = False, real_bootstrap: bool = False,
-                 sampler: str = None, low_special=None):
+                 sampler: str = None, low_special=None, encoder: str = "device"):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -200,7 +238,9 @@ class B200CkksCore:
         self.ctx = self.chain
         ch = self.chain
         self.n = params.poly_degree
-        self.encoder = DeviceEncoder(self.n, self.device)
+        if encoder not in ("device", "numpy"):
+            raise self._errors.InvalidParameters(f"unknown encoder {encoder!r}")
+        self.encoder = DeviceEncoder(self.n, self.device, host=encoder == "numpy")
         self.rng_seed = rng_seed
         self.bootstrap_eps = bootstrap_eps
         # "numpy": the reference's default_rng streams (bit-exact keys/encryptions,

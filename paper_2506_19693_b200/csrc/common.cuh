@@ -32,6 +32,8 @@ struct RingDev {
   uint32_t log_n;
   uint32_t np;
   uint64_t f64_mask[2];  // host-side prime classes (ckb_ring.f64_mask)
+  uint64_t ntt_chunk_bytes;  // host-side (ckb_ring.ntt_chunk_bytes, 0 = default)
+  uint32_t flags;            // host-side (ckb_ring.flags)
 };
 
 __device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
@@ -59,6 +61,8 @@ inline RingDev make_ring(const ckb_ring* r) {
   d.np = r->n_primes;
   d.f64_mask[0] = r->f64_mask[0];
   d.f64_mask[1] = r->f64_mask[1];
+  d.ntt_chunk_bytes = r->ntt_chunk_bytes;
+  d.flags = r->flags;
   return d;
 }
 

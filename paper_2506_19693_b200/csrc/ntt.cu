@@ -688,21 +688,15 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
 // integer-row CTAs then share the SMs, the FP64/L1-latency-bound and the
 // multiplier-bound work overlapping (measured: c2 479 -> 485 GB/s, config-4
 // steady step forward NTT -5%, against the class-split MODE 1 + MODE 2 pair
-// whose FP64 kernel alone is faster).  CKB_NTT_MIXED=0 restores the split.
-inline bool mixed_one_kernel() {
-  static const bool on = [] {
-    const char* v = getenv("CKB_NTT_MIXED");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
+// whose FP64 kernel alone is faster).  ckb_ring.flags CKB_RING_NTT_SPLIT
+// restores the split.
 
 // Rows of a two-phase transform are processed in chunks whose intermediate
 // stays in L2 between the phases.  96 MB measured best for one stream
 // (config-4 step -2%, config-2 sequential NTT -7% against 48 MB); callers
 // running transforms on several streams at once give each a share
-// (ckb_set_ntt_chunk_bytes; bench.py's concurrent HMult/HRot pair uses 48 MB).
-static size_t g_ntt_chunk_bytes = (size_t)96 << 20;
+// (ckb_ring.ntt_chunk_bytes; bench.py's concurrent HMult/HRot pair uses 48 MB).
+constexpr size_t kDefaultNttChunkBytes = (size_t)96 << 20;
 
 template <bool FWD>
 int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int32_t* limb_prime,
@@ -742,14 +736,16 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   NttPhase pb{limbs, GA / CB, CB, GB, 1, N / GB, 1, FWD ? 1 : 0, 0, lg(CB), items, FWD ? 0 : 1,
               FWD ? nullptr : src, src_istride};
   // Chunk rows so one chunk's intermediate stays in the 126 MB L2 between phases.
-  const int chunk = std::max(1, (int)(g_ntt_chunk_bytes / ((size_t)N * 8)));
+  const size_t budget = R.ntt_chunk_bytes ? (size_t)R.ntt_chunk_bytes : kDefaultNttChunkBytes;
+  const int chunk = std::max(1, (int)(budget / ((size_t)N * 8)));
+  const bool mixed_one_kernel = !(R.flags & CKB_RING_NTT_SPLIT);
   for (int r0 = 0; r0 < rows; r0 += chunk) {
     const int nr = std::min(chunk, rows - r0);
     pa.row0 = r0;
     pb.row0 = r0;
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
-      if (!any_f64 || (any_int && mixed_one_kernel()))
+      if (!any_f64 || (any_int && mixed_one_kernel))
         return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st, ep);
       // second-pass column phase: column-mapped direct I/O (MODE 3)
       const bool cm = ph.rstride != 1 && !ph.first;
@@ -836,12 +832,6 @@ int ckb_ntt_forward(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
 int ckb_ntt_inverse(const ckb_ring* ring, uint64_t* data, int rows, int limbs,
                     const int32_t* limb_prime, void* stream) {
   return ntt_run<false>(ring, data, rows, limbs, limb_prime, stream);
-}
-
-uint64_t ckb_set_ntt_chunk_bytes(uint64_t bytes) {
-  const uint64_t prev = g_ntt_chunk_bytes;
-  if (bytes) g_ntt_chunk_bytes = bytes;
-  return prev;
 }
 
 int ckb_ntt_forward_combine(const ckb_ring* ring, uint64_t* out, uint64_t* E, const uint64_t* x,

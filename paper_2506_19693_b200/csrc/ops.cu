@@ -474,9 +474,9 @@ constexpr int kMaxDrop = 16;
 // first-drop width from which the correction takes the fast basis-conversion
 // form (k_divround_corr_hps) when the caller passes its table
 constexpr int kHpsMinDrop = 6;
-// |frac - 1/2| below which rho is settled by exact_rho (tests lower it to 0 to
-// run every coefficient through the exact path)
-static double g_hps_margin = 0.5 - 0x1p-30;
+// |frac - 1/2| below which rho is settled by exact_rho (ckb_ring.flags
+// CKB_RING_HPS_EXACT lowers it to 0: every coefficient takes the exact path)
+constexpr double kHpsMargin = 0.5 - 0x1p-30;
 
 // acc - r * M  (mod p) for a signed centered remainder r and a Shoup constant M.
 __device__ __forceinline__ uint64_t sub_rm(uint64_t acc, int64_t r, uint64_t M, uint64_t Ms,
@@ -828,6 +828,9 @@ __device__ __noinline__ uint64_t exact_rho(const uint64_t* __restrict__ src, siz
     r[d] = centered(ckb::mul_shoup(a, __ldg(Tb + 2 * n1), __ldg(Tb + 2 * n1 + 1), p), p);
     if (r[d] != 0) top = r[d];
   }
+  // c1 == 0 (every digit zero; reached only when the margin is forced to 0):
+  // S = rho * P1 exactly, so f is rho up to rounding
+  if (top == 0) return (uint64_t)rint(f);
   const uint64_t fl = (uint64_t)floor(f);
   return top > 0 ? fl : fl + 1;
 }
@@ -899,7 +902,7 @@ __global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
 #pragma unroll
     for (int c = 0; c < V; ++c) {
       const double rho_d = rint(f[c]);
-      rho[c] = fabs(f[c] - rho_d) < margin  // 0.5 - 2^-30 (ckb_debug_hps_margin)
+      rho[c] = fabs(f[c] - rho_d) < margin  // 0.5 - 2^-30 (0: CKB_RING_HPS_EXACT)
                    ? (uint64_t)rho_d
                    : exact_rho(src + c, N, limbs, m2, n1, f[c], tab1, R, lm);
     }
@@ -1665,11 +1668,6 @@ int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys,
   return finish();
 }
 
-int ckb_debug_hps_margin(double margin) {
-  if (!(margin >= 0.0 && margin <= 0.5)) return CKB_E_ARG;
-  g_hps_margin = margin;
-  return 0;
-}
 
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,
                           int polys, int limbs, const int32_t* limb_prime, int n_drop1,
@@ -1704,7 +1702,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh);          \
     k_divround_corr_hps<A, B, VV><<<grid_for(total / VV, 256), 256, smh, st0>>>(            \
         E, T, has_addend, polys, limbs, n_drop1, n_drop2, (int)R.log_n, R, lm, tab1, tab2,  \
-        tabE, tabH, g_hps_margin);                                                          \
+        tabE, tabH, (R.flags & CKB_RING_HPS_EXACT) ? 0.0 : kHpsMargin);                                                          \
     return finish();                                                                        \
   }
     CKB_DH(6, 0) CKB_DH(6, 1) CKB_DH(6, 2) CKB_DH(8, 0) CKB_DH(8, 1) CKB_DH(8, 2)

@@ -102,6 +102,20 @@ class GpuChain:
         self.ring_p = nat.ctypes.pointer(self.ring)
         self._maps: dict = {}
 
+    def set_ntt_chunk_bytes(self, nbytes: int) -> int:
+        """L2 budget of this chain's two-phase transforms (ckb_ring.ntt_chunk_bytes,
+        0 = the 96 MB default); returns the previous value.  The struct is ours:
+        the library reads it at every call and keeps no state."""
+        prev = int(self.ring.ntt_chunk_bytes)
+        self.ring.ntt_chunk_bytes = int(nbytes)
+        return prev
+
+    def set_ring_flag(self, flag: int, on: bool) -> bool:
+        """Set / clear a ckb_ring.flags bit (nat.RING_*); returns the previous state."""
+        prev = bool(self.ring.flags & flag)
+        self.ring.flags = (self.ring.flags | flag) if on else (self.ring.flags & ~flag)
+        return prev
+
     # -- bases ------------------------------------------------------------------
     # A basis is a tuple of indices into all_primes; the kernels receive it as
     # a ctypes int32 array (cached per tuple).
@@ -201,7 +215,8 @@ class GpuChain:
         (a launch holding both prime classes is one per-CTA-dispatch kernel)."""
         if self.log_n <= 12:
             return 1
-        chunk = max(1, int(nat.LIB.ckb_set_ntt_chunk_bytes(0)) // (self.n * W))
+        budget = self.ring.ntt_chunk_bytes or nat.DEFAULT_NTT_CHUNK_BYTES
+        chunk = max(1, int(budget) // (self.n * W))
         return 2 * (-(-rows // chunk))
 
     F64_PRIME_LIMIT = nat.F64_PRIME_LIMIT

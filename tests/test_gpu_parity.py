@@ -440,11 +440,10 @@ def test_moddown_fast_conversion_paths_agree():
 
     base = run()
     try:
-        assert nat.LIB.ckb_debug_hps_margin(0.0) == 0
+        be.chain.set_ring_flag(nat.RING_HPS_EXACT, True)
         forced = run()
-        assert nat.LIB.ckb_debug_hps_margin(0.6) != 0
     finally:
-        nat.LIB.ckb_debug_hps_margin(0.5 - 2.0**-30)
+        be.chain.set_ring_flag(nat.RING_HPS_EXACT, False)
     GC.use_hps = False
     try:
         chained = run()
