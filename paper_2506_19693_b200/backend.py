@@ -40,6 +40,7 @@ import dataclasses
 import io
 import json
 import math
+import numbers
 import struct
 
 import numpy as np
@@ -56,11 +57,14 @@ MAX_SAFE_COEFF = float(2**52)
 
 
 # While a CUDA graph is being captured (graphs.GraphedStep), the pinned
-# staging tensors of in-graph uploads are kept alive here for the graph's life.
+# staging tensors of in-graph uploads are kept alive here for the graph's life,
+# as (tag, pinned tensor) pairs: a replay reads whatever the pinned tensor then
+# holds, so GraphedStep rewrites the encryption-seed uploads ("seeds", serials)
+# before every replay (fresh randomness per replayed step).
 H2D_KEEPALIVE = None
 
 
-def _h2d(arr: np.ndarray, device) -> torch.Tensor:
+def _h2d(arr: np.ndarray, device, tag=None) -> torch.Tensor:
     """Host array -> device without a stream sync: staged through pinned memory
     (torch's caching host allocator) and copied asynchronously.  A plain copy
     from pageable memory would make the host wait for all queued GPU work."""
@@ -69,7 +73,7 @@ def _h2d(arr: np.ndarray, device) -> torch.Tensor:
         return t.to(device)
     pinned = t.pin_memory()
     if H2D_KEEPALIVE is not None:
-        H2D_KEEPALIVE.append(pinned)
+        H2D_KEEPALIVE.append((tag, pinned))
     return pinned.to(device, non_blocking=True)
 
 
@@ -311,11 +315,22 @@ class B200CkksCore:
         self.relin_keys_k: dict = {}
         self.rotation_keys_k: dict = {}
         if low_special is not None:
-            tiers = ([(params.refresh_level, int(low_special))] if isinstance(low_special, int)
-                     else sorted((int(l), int(k)) for l, k in low_special))
+            if isinstance(low_special, numbers.Integral):
+                tiers = [(params.refresh_level, int(low_special))]
+            else:
+                try:
+                    tiers = sorted((int(l), int(k)) for l, k in low_special)
+                except (TypeError, ValueError):
+                    raise self._errors.InvalidParameters(
+                        "low_special: an int or [(max_level, k), ...]") from None
             for max_level, kk in tiers:
                 if not 0 < kk < ch.k:
-                    continue
+                    raise self._errors.InvalidParameters(
+                        f"low_special: {kk} special primes for levels <= {max_level}; need "
+                        f"0 < k' < {ch.k}")
+                if not 0 <= max_level <= params.level:
+                    raise self._errors.InvalidParameters(
+                        f"low_special: tier level {max_level} outside 0..{params.level}")
                 m = ch.level_limbs[min(max_level, params.level)]
                 widest = max(math.prod(ch.all_primes[lo:min(lo + self.alpha, m)])
                              for lo in range(0, m, self.alpha))
@@ -701,8 +716,8 @@ class B200CkksCore:
         msgs = []
         if self.sampler == "philox":
             srs = [next(self._serials) if sr is None else sr for sr in serials]
-            seeds = _h2d(np.array([_mix64(self.rng_seed, 0x454E43, sr) for sr in srs],
-                                  dtype=np.int64), self.device).view(U64)
+            seeds = _h2d(self.encryption_seeds(srs), self.device,
+                         tag=("seeds", tuple(srs))).view(U64)
             a_d, e_d = ch.sample(seeds, m)
             msgs = [self._encode_rns(values, level) for values in values_list]
             out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)
@@ -722,6 +737,11 @@ class B200CkksCore:
         out[:, 1].copy_(torch.from_numpy(a_np))
         me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)  # [B, m, N]
         return self._finish_encrypt(out, me, msgs, m)
+
+    def encryption_seeds(self, serials) -> np.ndarray:
+        """Philox keys of the encryptions with these serials (one stream per
+        (rng_seed, serial), the device analogue of default_rng((seed, serial)))."""
+        return np.array([_mix64(self.rng_seed, 0x454E43, sr) for sr in serials], dtype=np.int64)
 
     def _finish_encrypt(self, out, me, msgs, m):
         """c1 = a (NTT domain), c0 = NTT(m + e) - a*s."""

@@ -161,7 +161,15 @@ class DataParallelExecutor(WaveExecutor):
                     if ha and hb:
                         todo.append(i)
                     elif ha or hb:
-                        env[ops[i][2]] = env[a if ha else b]
+                        # the join's partial sum on this rank is the one operand
+                        # present, at the join's level (add_ct adjusts operands of
+                        # different levels, backend.py:94-112): every rank's
+                        # partial then has the same limb count for the all-reduce
+                        src = env[a if ha else b]
+                        lvl = self.level_of[ops[i][2]]
+                        if src.level != lvl:
+                            src = GpuCiphertext(be._adjust_data(src.data, src.level, lvl), lvl)
+                        env[ops[i][2]] = src
             # all-reduces first, in a rank-independent order
             for i in sorted(todo):
                 for vid in plan.reduce_before.get(i, ()):

@@ -35,6 +35,9 @@ class WaveExecutor:
         self.cust = custodian
         self.be = custodian.backend
         self.max_group = max_group
+        # added to every serial the plan assigns: a replayed step (graphs.
+        # GraphedStep) draws fresh encryption randomness per replay
+        self.serial_offset = 0
         self._plan()
 
     # -- planning ------------------------------------------------------------
@@ -198,7 +201,7 @@ class WaveExecutor:
         # leave the backend's serial counter where sequential execution would
         import itertools
 
-        be._serials = itertools.count(self.serials_used)
+        be._serials = itertools.count(self.serials_used + self.serial_offset)
         return env
 
     def finish_deferred(self, env: dict) -> dict:
@@ -227,7 +230,7 @@ class WaveExecutor:
                                                            values[i].shape[0])
         rl = be.params.refresh_level
         data = be._encrypt_batch([values[i] for i in order], rl,
-                                 [self.serial_of[i] for i in order])
+                                 [self.serial_of[i] + self.serial_offset for i in order])
         for j, i in enumerate(order):
             env[ops[i][1]] = GpuCiphertext(data[j], rl)
             for ref in _inputs(ops[i]):
@@ -268,7 +271,7 @@ class WaveExecutor:
         if tag == "enc":
             top = be.params.level
             data = be._encrypt_batch([pvals(ops[i][2]) for i in idx], top,
-                                     [self.serial_of[i] for i in idx])
+                                     [self.serial_of[i] + self.serial_offset for i in idx])
             for j, i in enumerate(idx):
                 env[ops[i][1]] = GpuCiphertext(data[j], top)
             return
@@ -295,7 +298,7 @@ class WaveExecutor:
                                                      values.shape[0])
             rl = be.params.refresh_level
             env[ops[i][1]] = GpuCiphertext(
-                be._encrypt_batch([values], rl, [self.serial_of[i]])[0], rl)
+                be._encrypt_batch([values], rl, [self.serial_of[i] + self.serial_offset])[0], rl)
             return
         if tag == "rot":
             _, lvl, step, fused = key

@@ -488,6 +488,35 @@ def test_low_special_modulus_keyswitch():
         he_api.keygen(params, {1}, low_special=1, **opts)
 
 
+def test_low_special_two_tiers_pick_k_per_level():
+    """low_special as a tier list (what the config-4/5 runs use): each level
+    picks the k' of the first tier covering it (full P above the last tier),
+    results decrypt correctly at every level, numpy integers are accepted and
+    out-of-range tiers are rejected."""
+    n, L, bd = 1 << 10, 6, 2
+    chain = (60,) + (45,) * (L - bd) + (60,) * bd + (360,)
+    params = SchemeParams(poly_degree=n, modulus_chain=chain, scale_bits=45, level=L,
+                          bootstrap_depth=bd)
+    opts = dict(backend="ckks", rng_seed=3, prime_layout="bootstrap", dnum=3, secret_hw=64)
+    cust = he_api.keygen(params, {1}, low_special=[(np.int64(2), 3), (4, np.int32(4))], **opts)
+    be = cust.backend
+    assert [be._ks_k(lv) for lv in range(L + 1)] == [3, 3, 3, 4, 4, 6, 6]
+    rng = np.random.default_rng(1)
+    v = rng.uniform(-1, 1, n // 2)
+    a = cust.encrypt(he_api.make_plain(v, n // 2, 45.0))
+    ev = cust.evaluator
+    want = v.copy()
+    one = he_api.make_plain(np.ones(n // 2), n // 2, 45.0)
+    while a.level_remaining > 0:
+        r = ev.rotate(a, 1)
+        assert np.max(np.abs(cust.decrypt(r).values - np.roll(want, -1))) < 1e-6
+        a = ev.mul(a, cust.encrypt(one))
+        assert np.max(np.abs(cust.decrypt(a).values - want)) < 1e-6
+    for bad in ([(2, 6)], [(2, 0)], [(9, 3)], "x"):
+        with pytest.raises(he_errors.InvalidParameters):
+            he_api.keygen(params, {1}, low_special=bad, **opts)
+
+
 # ---------------------------------------------------------------------------
 # Decryption tolerances (tests/test_ckks_backend.py of the reference)
 # ---------------------------------------------------------------------------
@@ -628,22 +657,28 @@ def test_wave_executor_bit_identical_to_sequential(c1_program):
 def test_graphed_step_bit_identical_to_eager(c1_program):
     """graphs.GraphedStep: the config-1 step captured as one CUDA graph (the
     refreshes eager afterwards) reproduces the eager executor bit for bit, on
-    every replay."""
+    every replay, each replay with its own encryption serials."""
     from paper_2506_19693_b200.executor import WaveExecutor
     from paper_2506_19693_b200.graphs import GraphedStep
 
     prog, z = c1_program
     cust = _c1_custodian(z)
     env = prog.run(cust, 0, prog.n_setup)
+    from paper_2506_19693_b200.graphs import eager_equivalent
+
     ex = WaveExecutor(prog, cust)
-    want_env = ex.run(dict(env), only_after_setup=True)
-    want = [cust.backend.planes_of(want_env[o]) for o in prog.outputs]
     gs = GraphedStep(ex, env)
+    prev = None
     for _ in range(2):
         got_env = gs.step()
         got = [cust.backend.planes_of(got_env[o]) for o in prog.outputs]
+        want_env = eager_equivalent(gs)
+        want = [cust.backend.planes_of(want_env[o]) for o in prog.outputs]
         for a, b in zip(got, want):
             assert np.array_equal(a, b)
+        # every replay encrypts with fresh randomness (its own serials)
+        assert prev is None or not all(np.array_equal(a, b) for a, b in zip(got, prev))
+        prev = got
 
 
 # ---------------------------------------------------------------------------
