@@ -280,6 +280,46 @@ def run_c1_train(device_index):
             "reference_cpu_s_per_step_build_container": ref_s}
 
 
+def run_c1_dropin(cpu: bool = True) -> dict:
+    """Config 1 through the UNCHANGED reference layer code (tools/c1_dropin.py:
+    the reference package from baseline/_ref — keygen, build_model,
+    prepare_sample, nn.train_iteration — with plugin.install routing
+    backend="ckks" to the B200 backend at the BASELINE primes), and the
+    reference's own numpy CkksBackend timed on this host in the same run."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import c1_dropin as C
+
+    C.import_reference()
+    from paper_2506_19693_b200 import plugin
+
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "c1_modeA_weights.npy"))
+    cls, old = plugin.install(prime_layout="baseline", secret_hw=64)
+    try:
+        times = []
+        for rep in range(3):  # rep 0 warms tables / FFT plans
+            cust, model, shape, x, onehot = C.build()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            C.step(cust, model, shape, x, onehot)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        w = C.weights(model, cust)
+    finally:
+        plugin.uninstall(old)
+    out = {"ms_per_step": 1e3 * min(times[1:]), "first_step_ms": 1e3 * times[0],
+           "weights_max_abs_err_vs_reference_ckks": float(np.max(np.abs(w - gold))),
+           "path": "reference nn.train_iteration + prepare_sample (32 samples encrypted) through "
+                   "ciphermlp.api -> plugin-installed B200 CkksBackend, one HE call at a time",
+           "timing": "wall clock, device sync on both sides, best of 2 after a warm-up step"}
+    if cpu:
+        ref = C.time_reference_step((1, 2))
+        out["cpu_reference"] = ref
+        out["speedup_vs_cpu_reference"] = ref["ms_per_step_batch32"] / out["ms_per_step"]
+    return out
+
+
 def run_c1_dp(local: int, world: int) -> dict:
     """Config-1 step sharded by sample across `world` ranks (dp.py):
     each rank runs its share of the 32 per-sample pipelines, one exact residue
@@ -327,6 +367,15 @@ def run_c1_dp(local: int, world: int) -> dict:
             "allreduce_bytes_per_rank": ex.exchanged_bytes // len(range(4)),
             "weights_identical_across_ranks": bool(lo == hi),
             "timing": "CUDA events around the sharded step, max over ranks"}
+
+
+def security_note(be) -> str:
+    """HES gate of the chain actually built (params.py:70-77: 1,772 bits at N=2^16)."""
+    bits = sum(int(p).bit_length() for p in be.chain.all_primes)
+    bound = {2**12: 109, 2**13: 218, 2**14: 438, 2**15: 881, 2**16: 1772, 2**17: 3544}.get(
+        be.n, 0)
+    tag = "insecure-test" if bits > bound else "128-bit (HE standard)"
+    return f"{tag}: log2(QP) = {bits} bits vs the {bound}-bit bound at N={be.n}"
 
 
 def run_c3_bootstrap(special: int = 660):
@@ -378,6 +427,7 @@ def run_c3_bootstrap(special: int = 660):
             "graph_output_equal_eager": graph_equal, "first_call_ms": 1e3 * times[0],
             "max_abs_err": err, "precision_bits": -math.log2(err), "level_out": out.level,
             "keys": len(be.rotation_keys) + 1, "keygen_s": keygen_s,
+            "security": security_note(be),
             "params": "N=2^16, 2^15 slots, Q = 60 + 8x45 (user) + 16x60 (bootstrap) bits, "
                       "P = 11x60, dnum=3, HW 192, K=28, Chebyshev 119 + 2 double angles"}
 
@@ -421,6 +471,289 @@ def alu_probe_gbfly(p: int, reps: int = 3, f64: bool = False) -> float:
     return best
 
 
+def cpu_reference(L, args) -> dict:
+    """The reference algorithm (oracle port, its own prime layout) on this
+    host's cores: one HMult + one HRot of one ciphertext at N=2^16, L entries."""
+    from oracle import parallel_ref as PR
+
+    procs = args.ref_procs or PR.default_procs()
+    secs = _cpu_step(_cpu_case(L), procs)
+    _, k = c2_params(L)
+    hm1, hr1, _ = alg_bytes(L, k, 1, 1)
+    return {"value": (hm1 + hr1) / secs / 1e9, "unit": "GB/s", "cores": procs, "kind": "port",
+            "seconds": secs, "sample": _cpu_sample_text(L, procs)}
+
+
+def pair_alu_floor(be, L, k, bsz, peak_int, peak_f64):
+    """Arithmetic floor of one HMult batch + one HRot batch (the headline pair):
+    every modular multiply the algorithm needs — NTT butterflies (N/2 log N per
+    limb transform), ModUp terms (the digit's y_i and, per extended output, one
+    term per digit limb), inner-product MACs (2 per digit per ext limb), the
+    ModDown correction terms (y_u plus one per kept limb and dropped prime),
+    tensor products (4) and combine multiplies (2) — each charged to the FP64
+    (primes < 2^46) or integer (60-bit) pipe by its prime and timed at that
+    pipe's measured butterfly rate (ckb_alu_probe / ckb_alu_probe_f64; a
+    butterfly is one modular multiply plus an add and a subtract).  Memory
+    traffic is free in this model."""
+    n = 1 << N_LOG
+    bf = n // 2 * N_LOG  # butterflies per limb transform
+    alpha = -(-L // DNUM)
+    nd = -(-L // alpha)
+    m = L
+    m2 = m - 1
+    f = i = 0  # modular multiplies charged to the FP64 / integer pipe, per item
+    # HMult: tensor, iNTT(d2), ModUp, NTT(digits), inner product, ModDown + rescale
+    f += 4 * m * n + m * bf
+    for j in range(nd):
+        cnt = min(alpha, m - j * alpha)
+        f += cnt * n + (m - cnt) * (cnt * n + bf)
+        i += k * (cnt * n + bf)
+    f += 2 * nd * m * n
+    i += 2 * nd * k * n
+    i += 2 * (k + 1) * bf + 2 * (k + 1) * n       # iNTT of dropped limbs, their y_u
+    f += 2 * (m2 * (k + 1) * n + m2 * bf + 2 * m2 * n)
+    hm_f, hm_i = f, i
+    # HRot: automorphism (a permutation), iNTT(c1'), ModUp, NTT, MAC, ModDown
+    f = m * bf
+    i = 0
+    for j in range(nd):
+        cnt = min(alpha, m - j * alpha)
+        f += cnt * n + (m - cnt) * (cnt * n + bf)
+        i += k * (cnt * n + bf)
+    f += 2 * nd * m * n
+    i += 2 * nd * k * n
+    i += 2 * k * bf + 2 * k * n
+    f += 2 * (m * k * n + m * bf + 2 * m * n)
+    tot_f = bsz * (hm_f + f) / 1e9
+    tot_i = bsz * (hm_i + i) / 1e9
+    floor_s = tot_f / peak_f64 + tot_i / peak_int
+    return {"gmulmod_f64": tot_f, "gmulmod_int": tot_i, "floor_ms": 1e3 * floor_s,
+            "peak_int_gbfly": peak_int, "peak_f64_gbfly": peak_f64}
+
+
+def run_c2(L, bsz, args, rank, world, local, breakdown=False, keep=False) -> dict:
+    """One BASELINE config-2 point: keys, a 64-ciphertext batch, the HMult + HRot
+    pair on two streams timed with CUDA events (max over ranks), optionally the
+    sequential per-stage / per-kernel breakdown and the rooflines."""
+    import torch
+
+    from paper_2506_19693_b200 import dist as hdist
+    from paper_2506_19693_b200 import he_api, ring
+    from paper_2506_19693_b200.ring import KernelTimer
+
+    params, k = c2_params(L)
+    rng = np.random.default_rng(1234 + rank)
+    steps_rot = [int(s) for s in rng.integers(1, 1 << 15, bsz)]
+    t0 = time.perf_counter()
+    cust = he_api.keygen(params, set(steps_rot), backend="ckks", rng_seed=99 + rank,
+                         prime_layout="baseline", dnum=DNUM, secret_hw=192)
+    be = cust.backend
+    torch.cuda.synchronize()
+    keygen_s = time.perf_counter() - t0
+    lvl = params.level
+    m = be.chain.level_limbs[lvl]
+    n = 1 << N_LOG
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + rank)
+
+    def rand_batch():
+        t = torch.empty(bsz, 2, m, n, dtype=torch.int64, device="cuda")
+        for i, p in enumerate(be.chain.limbs_at(lvl)):
+            t[:, :, i].random_(0, p, generator=gen)
+        return t.view(torch.uint64)
+
+    A, B = rand_batch(), rand_batch()
+    X = torch.empty_like(A)
+    slots = params.slot_count
+    n_keys = len({s % slots for s in steps_rot})  # distinct Galois keys of the HRot batch
+    hm_b, hr_b, ntt_b = alg_bytes(L, k, bsz, n_keys)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    s_hm, s_hr = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def keyswitch_pair():
+        # the HMult and HRot batches are independent: two streams (their
+        # kernels are bound by different resources and overlap); each stream's
+        # transforms get half the single-stream L2 budget (ckb_ring)
+        cur = torch.cuda.current_stream()
+        s_hm.wait_stream(cur)
+        s_hr.wait_stream(cur)
+        prev = be.chain.set_ntt_chunk_bytes(48 << 20)
+        try:
+            with torch.cuda.stream(s_hm):
+                be.batch_hmult(A, B, lvl)
+            with torch.cuda.stream(s_hr):
+                be.batch_hrot(A, steps_rot, lvl)
+        finally:
+            be.chain.set_ntt_chunk_bytes(prev)
+        cur.wait_stream(s_hm)
+        cur.wait_stream(s_hr)
+
+    for _ in range(args.warmup):
+        X.copy_(A)
+        be.batch_ntt(X, lvl)
+        be.batch_ntt(X, lvl, inverse=True)
+        keyswitch_pair()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    pairs = []
+    start, end = ev(), ev()
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        e1, e2 = ev(), ev()
+        X.copy_(A)
+        be.batch_ntt(X, lvl)
+        be.batch_ntt(X, lvl, inverse=True)
+        e1.record()
+        keyswitch_pair()
+        e2.record()
+        pairs.append((e1, e2))
+    end.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms_step = hdist.max_over_ranks(start.elapsed_time(end)) / args.steps
+    ks_ms = hdist.max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in pairs])))
+    value = world * (hm_b + hr_b) / (ks_ms / 1e3) / 1e9  # weak scaling: every rank its batch
+    out = {"value": value, "ms_per_step": ms_step, "keyswitch_pair_ms": ks_ms, "L": L, "k": k,
+           "alpha": be.alpha, "batch": bsz, "distinct_rotation_keys": n_keys,
+           "alg_bytes": {"hmult": hm_b, "hrot": hr_b, "ntt_intt": ntt_b},
+           "keygen_s": keygen_s,
+           "timing": "value: HMult and HRot batches on two streams, CUDA events around the "
+                     "pair, mean over steps, max over ranks" +
+                     ("; stages_ms / kernels / roofline: a second pass of the same steps "
+                      "issued sequentially with events around every kernel" if breakdown else "")}
+    if clk:
+        out["clocks"] = clk
+    if breakdown:
+        timer = KernelTimer()
+        ring.TIMER = timer
+        stage = {"ntt": [], "hmult": [], "hrot": []}
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+            e0.record()
+            X.copy_(A)
+            be.batch_ntt(X, lvl)
+            be.batch_ntt(X, lvl, inverse=True)
+            e1.record()
+            be.batch_hmult(A, B, lvl)
+            e2.record()
+            be.batch_hrot(A, steps_rot, lvl)
+            e3.record()
+            stage["ntt"].append((e0, e1))
+            stage["hmult"].append((e1, e2))
+            stage["hrot"].append((e2, e3))
+        torch.cuda.synchronize()
+        ring.TIMER = None
+        st_ms = {kk: float(np.mean([a.elapsed_time(b) for a, b in v])) for kk, v in stage.items()}
+        ksum = timer.summary()
+        launches = sum(d["launches"] for d in ksum.values())
+        dom_name = max(ksum, key=lambda nm: ksum[nm]["ms"])
+        dom = ksum[dom_name]
+        peak, peak_kind = load_peaks()
+        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        out["stages_ms"] = st_ms
+        out["hmult_GBps"] = hm_b / (st_ms["hmult"] / 1e3) / 1e9
+        out["hrot_GBps"] = hr_b / (st_ms["hrot"] / 1e3) / 1e9
+        out["ntt_GBps"] = ntt_b / (st_ms["ntt"] / 1e3) / 1e9
+        out["hmult_us_per_ct"] = 1e3 * st_ms["hmult"] / bsz
+        out["hrot_us_per_ct"] = 1e3 * st_ms["hrot"] / bsz
+        out["kernels"] = {nm: {"ms_per_step": d["ms"] / args.steps,
+                               "launches_per_step": d["launches"] / args.steps,
+                               "GBps_alg": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                               "share": d["ms"] / sum(x["ms"] for x in ksum.values())}
+                          for nm, d in ksum.items()}
+        out["gpu_launches"] = launches
+        out["roofline"] = {"bound": "hbm", "kernel": dom_name, "achieved": achieved,
+                           "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                           "frac": achieved / peak,
+                           "traffic": (TRAFFIC.get(dom_name) or {}).get("dram_bytes_per_launch"),
+                           "traffic_detail": TRAFFIC.get(dom_name)}
+        p_int = int(be.chain.special_primes[0])  # a 60-bit special prime
+        p_f64 = int(be.chain.limbs_at(lvl)[-1])  # a 40-bit Q prime
+        peak_int = alu_probe_gbfly(p_int)
+        peak_f64 = alu_probe_gbfly(p_f64, f64=True)
+        if dom_name in ("ntt", "intt", "ntt_combine"):
+            # the NTT's binding roofline is the arithmetic pipes, not HBM: rows
+            # with primes < 2^46 run the FP64 butterfly, the others the integer
+            # one, each against its own register-resident probe
+            bf = dom["bytes"] * N_LOG / 32 / 1e9          # G butterflies (bytes = 16 N per limb)
+            bf_f64 = dom["f64_bytes"] * N_LOG / 32 / 1e9
+            floor_s = (bf - bf_f64) / peak_int + bf_f64 / peak_f64
+            got_s = dom["ms"] / 1e3
+            out["roofline"]["alu"] = {
+                "unit": "Gbutterfly/s", "achieved": bf / got_s, "peak": bf / floor_s,
+                "frac": floor_s / got_s, "f64_share": bf_f64 / bf, "peak_int": peak_int,
+                "peak_f64": peak_f64,
+                "peak_source": "ckb_alu_probe / ckb_alu_probe_f64 (register-resident "
+                               "butterflies, the NTT's own integer and FP64 arithmetic), "
+                               "weighted by this kernel's row mix"}
+        fl = pair_alu_floor(be, L, k, bsz, peak_int, peak_f64)
+        seq_ms = st_ms["hmult"] + st_ms["hrot"]
+        out["pair_roofline"] = {
+            "alu_floor_ms": fl["floor_ms"], "hbm_floor_ms": 1e3 * (hm_b + hr_b) / peak / 1e9,
+            "pair_ms": ks_ms, "sequential_ms": seq_ms, "alu_frac": fl["floor_ms"] / ks_ms,
+            "hbm_frac": (hm_b + hr_b) / (ks_ms / 1e3) / 1e9 / peak, **fl,
+            "model": pair_alu_floor.__doc__.split("\n\n")[0].replace("\n", " ")}
+    if keep:
+        out["_live"] = (be, A, B, steps_rot, lvl, hm_b, hr_b)
+    else:
+        del A, B, X, cust, be
+    return out
+
+
+def e2e_he_api(be, A, B, steps_rot, lvl, hm_b, hr_b, world, reps=2) -> dict:
+    """The c2 pair through the public HE API one ciphertext at a time, host
+    bytes in and out: RBCT blobs (ckks/backend.py:210-247) -> deserialize_cipher
+    (H2D + NTT) -> Evaluator.mul / Evaluator.rotate (the reference's
+    api.py:270-294 calls, level/depth bookkeeping included) -> serialize_cipher
+    (iNTT + D2H) for all 64 pairs; wall clock with a device sync at both ends."""
+    import torch
+
+    from paper_2506_19693_b200 import he_api
+    from paper_2506_19693_b200.backend import GpuCiphertext
+
+    cust = he_api.KeyCustodian(be, be.rotation_indices)
+    evl = cust.evaluator
+    bsz = A.shape[0]
+
+    def wrap(d):
+        return be._wrap(GpuCiphertext(d, lvl), lvl, 0)
+
+    blobs_a = [be.serialize_cipher(wrap(A[i])) for i in range(bsz)]
+    blobs_b = [be.serialize_cipher(wrap(B[i])) for i in range(bsz)]
+    slots = be.params.slot_count
+
+    def step():
+        out = []
+        for i in range(bsz):
+            ca, cb = be.deserialize_cipher(blobs_a[i]), be.deserialize_cipher(blobs_b[i])
+            out.append(be.serialize_cipher(evl.mul(ca, cb)))
+            out.append(be.serialize_cipher(evl.rotate(ca, steps_rot[i] % slots)))
+        return out
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        res = step()
+    torch.cuda.synchronize()
+    ms = 1e3 * (time.perf_counter() - t0) / reps
+    h2d = sum(len(b) for b in blobs_a) + sum(len(b) for b in blobs_b)
+    d2h = sum(len(b) for b in res)
+    return {"value": world * (hm_b + hr_b) / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "per-ciphertext HE API: RBCT bytes -> deserialize_cipher -> Evaluator.mul / "
+                    "Evaluator.rotate -> serialize_cipher, 64 pairs, wall clock"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -435,6 +768,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -461,185 +795,28 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    L, bsz = args.limbs, args.batch
-    params, k = c2_params(L)
-    rng = np.random.default_rng(1234 + rank)
-    steps_rot = [int(s) for s in rng.integers(1, 1 << 15, bsz)]
-    t0 = time.perf_counter()
-    cust = he_api.keygen(params, set(steps_rot), backend="ckks", rng_seed=99 + rank,
-                         prime_layout="baseline", dnum=DNUM, secret_hw=192)
-    be = cust.backend
-    torch.cuda.synchronize()
-    keygen_s = time.perf_counter() - t0
-    lvl = params.level
-    m = be.chain.level_limbs[lvl]
-    n = 1 << N_LOG
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(7 + rank)
-
-    def rand_batch():
-        t = torch.empty(bsz, 2, m, n, dtype=torch.int64, device="cuda")
-        for i, p in enumerate(be.chain.limbs_at(lvl)):
-            t[:, :, i].random_(0, p, generator=gen)
-        return t.view(torch.uint64)
-
-    A, B = rand_batch(), rand_batch()
-    X = torch.empty_like(A)
-
-    def step():
-        X.copy_(A)
-        be.batch_ntt(X, lvl)
-        be.batch_ntt(X, lvl, inverse=True)
-        out_m = be.batch_hmult(A, B, lvl)
-        out_r = be.batch_hrot(A, steps_rot, lvl)
-        return out_m, out_r
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     from paper_2506_19693_b200 import dist as hdist
 
-    # headline pass: the HMult and HRot batches are independent, so they run on
-    # two streams (their kernels are bound by different resources and overlap)
-    s_hm, s_hr = torch.cuda.Stream(), torch.cuda.Stream()
-
-    from paper_2506_19693_b200 import _native as nat_
-
-    def keyswitch_pair():
-        cur = torch.cuda.current_stream()
-        s_hm.wait_stream(cur)
-        s_hr.wait_stream(cur)
-        # two concurrent streams share the L2: each transform chunk gets half
-        # of the single-stream budget (ckb_ring.ntt_chunk_bytes)
-        prev = be.chain.set_ntt_chunk_bytes(48 << 20)
-        try:
-            with torch.cuda.stream(s_hm):
-                be.batch_hmult(A, B, lvl)
-            with torch.cuda.stream(s_hr):
-                be.batch_hrot(A, steps_rot, lvl)
-        finally:
-            be.chain.set_ntt_chunk_bytes(prev)
-        cur.wait_stream(s_hm)
-        cur.wait_stream(s_hr)
-
-    for _ in range(2):
-        keyswitch_pair()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    pairs = []
-    start, end = ev(), ev()
-    torch.cuda.synchronize()
-    start.record()
-    for _ in range(args.steps):
-        e1, e2 = ev(), ev()
-        X.copy_(A)
-        be.batch_ntt(X, lvl)
-        be.batch_ntt(X, lvl, inverse=True)
-        e1.record()
-        keyswitch_pair()
-        e2.record()
-        pairs.append((e1, e2))
-    end.record()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    ms_step = hdist.max_over_ranks(start.elapsed_time(end)) / args.steps
-    ks_ms = hdist.max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in pairs])))
-    hm_b, hr_b, ntt_b = alg_bytes(L, k, bsz, bsz)
-    value = world * (hm_b + hr_b) / (ks_ms / 1e3) / 1e9  # weak scaling: every rank its batch
-
-    # breakdown pass: the same steps issued sequentially with CUDA events around
-    # every kernel wrapper (per-stage and per-kernel times, the roofline)
-    timer = KernelTimer()
-    ring.TIMER = timer
-    stage = {"ntt": [], "hmult": [], "hrot": []}
-    torch.cuda.synchronize()
-    for _ in range(args.steps):
-        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
-        e0.record()
-        X.copy_(A)
-        be.batch_ntt(X, lvl)
-        be.batch_ntt(X, lvl, inverse=True)
-        e1.record()
-        be.batch_hmult(A, B, lvl)
-        e2.record()
-        be.batch_hrot(A, steps_rot, lvl)
-        e3.record()
-        stage["ntt"].append((e0, e1))
-        stage["hmult"].append((e1, e2))
-        stage["hrot"].append((e2, e3))
-    torch.cuda.synchronize()
-    ring.TIMER = None
-    st_ms = {kk: float(np.mean([a.elapsed_time(b) for a, b in v])) for kk, v in stage.items()}
-    ksum = timer.summary()
-    launches = sum(d["launches"] for d in ksum.values())
-    dom_name = max(ksum, key=lambda nm: ksum[nm]["ms"])
-    dom = ksum[dom_name]
-    peak, peak_kind = load_peaks()
-    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
-    kernels = {nm: {"ms_per_step": d["ms"] / args.steps, "launches_per_step": d["launches"] /
-                    args.steps, "GBps_alg": d["bytes"] / (d["ms"] / 1e3) / 1e9,
-                    "share": d["ms"] / sum(x["ms"] for x in ksum.values())}
-               for nm, d in ksum.items()}
-
+    L, bsz = args.limbs, args.batch
+    head = run_c2(L, bsz, args, rank, world, local, breakdown=True, keep=True)
+    be, A, B, steps_rot, lvl, hm_b, hr_b = head.pop("_live")
     line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
         "config": {"workload": f"c2 primitive sweep: N=2^16, L={L} x 40-bit, dnum={DNUM}, "
-                               f"k={k} x 60-bit special, batch {bsz} ct: NTT+iNTT, HMult, "
-                               f"HRot ({bsz} distinct keys)",
+                               f"k={head['k']} x 60-bit special, batch {bsz} ct: NTT+iNTT, "
+                               f"HMult, HRot ({head['distinct_rotation_keys']} distinct keys)",
                    "batch_per_gpu": bsz, "l2": "inputs 1.5 GiB per operand > 126 MB L2 (no flush)",
                    "parallelism": f"replicas x{world} (independent ciphertext batches)"},
-        "keyswitch_pair_ms": ks_ms,
-        "timing": "value: HMult and HRot batches on two streams, CUDA events around the pair, "
-                  "mean over steps, max over ranks; stages_ms / kernels / roofline: a second "
-                  "pass of the same steps issued sequentially with events around every kernel",
-        "stages_ms": st_ms,
-        "hmult_GBps": hm_b / (st_ms["hmult"] / 1e3) / 1e9,
-        "hrot_GBps": hr_b / (st_ms["hrot"] / 1e3) / 1e9,
-        "ntt_GBps": ntt_b / (st_ms["ntt"] / 1e3) / 1e9,
-        "hmult_us_per_ct": 1e3 * st_ms["hmult"] / bsz,
-        "hrot_us_per_ct": 1e3 * st_ms["hrot"] / bsz,
-        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": (TRAFFIC.get(dom_name) or {}).get("dram_bytes_per_launch"),
-                     "traffic_detail": TRAFFIC.get(dom_name)},
-        "kernels": kernels,
-        "gpu_launches": launches,
-        "keygen_s": keygen_s,
     }
-    if clk:
-        line["clocks"] = clk
-    if dom_name in ("ntt", "intt"):
-        # the NTT's binding roofline is the arithmetic pipes, not HBM: rows with
-        # primes < 2^46 run the FP64 butterfly, the others the integer one, each
-        # against its own register-resident probe; the mixed ceiling is the
-        # time the probes would need for this kernel's butterflies
-        p_int = int(be.chain.limbs_at(lvl)[0])  # the 60-bit base prime
-        p_f64 = int(be.chain.limbs_at(lvl)[-1])  # a 40-bit rescale prime
-        peak_int = alu_probe_gbfly(p_int)
-        peak_f64 = alu_probe_gbfly(p_f64, f64=True)
-        bf = dom["bytes"] * N_LOG / 32 / 1e9          # G butterflies (bytes = 16 N per limb)
-        bf_f64 = dom["f64_bytes"] * N_LOG / 32 / 1e9
-        floor_s = (bf - bf_f64) / peak_int + bf_f64 / peak_f64
-        got_s = dom["ms"] / 1e3
-        line["roofline"]["alu"] = {"unit": "Gbutterfly/s", "achieved": bf / got_s,
-                                   "peak": bf / floor_s, "frac": floor_s / got_s,
-                                   "f64_share": bf_f64 / bf, "peak_int": peak_int,
-                                   "peak_f64": peak_f64,
-                                   "peak_source": "ckb_alu_probe / ckb_alu_probe_f64 "
-                                                  "(register-resident butterflies, the "
-                                                  "NTT's own integer and FP64 arithmetic), "
-                                                  "weighted by this kernel's row mix"}
-
+    line.update({kk: v for kk, v in head.items() if kk not in ("value", "ms_per_step")})
+    m = be.chain.level_limbs[lvl]
+    n = 1 << N_LOG
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    if not args.no_e2e:
+        line["e2e_he_api"] = e2e_he_api(be, A, B, steps_rot, lvl, hm_b, hr_b, world)
     if not args.no_e2e:
         # e2e: host (pinned) inputs -> device -> HMult + HRot -> host, per step
         hA = A.cpu().pin_memory()
@@ -676,7 +853,7 @@ def main():
                        "h2d_bytes_per_step": hA.numel() * 8 + hB.numel() * 8,
                        "d2h_bytes_per_step": hOm.numel() * 8 + hOr.numel() * 8}
         del hA, hB, hOm, hOr, dA, dB
-    del A, B, X
+    del A, B
     torch.cuda.empty_cache()
 
     if rank == 0 and world == 1 and not args.no_c1:
@@ -684,6 +861,10 @@ def main():
             line["c1_train"] = run_c1_train(local)
         except Exception as exc:  # report, never hide
             line["c1_train"] = {"error": repr(exc)}
+        try:
+            line["c1_train_dropin"] = run_c1_dropin(cpu=not args.no_cpu)
+        except Exception as exc:  # report, never hide
+            line["c1_train_dropin"] = {"error": repr(exc)}
     if world > 1 and not args.no_c1:
         try:
             res = run_c1_dp(local, world)
@@ -715,15 +896,25 @@ def main():
         except Exception as exc:
             line["c5_train"] = {"error": repr(exc)}
         torch.cuda.empty_cache()
+    if not args.no_sweep:
+        # BASELINE config 2's other limb counts, each a full c2 step of its own
+        # (keys, batch, two-stream pair timing) with the CPU reference at that L
+        sweep = {}
+        for Ls in (4, 12):
+            if Ls == L:
+                continue
+            try:
+                r = run_c2(Ls, bsz, args, rank, world, local, breakdown=False)
+                if rank == 0 and world == 1 and not args.no_cpu:
+                    r["cpu_reference"] = cpu_reference(Ls, args)
+                    r["speedup_vs_cpu_reference"] = r["value"] / r["cpu_reference"]["value"]
+                sweep[f"L{Ls}"] = r
+            except Exception as exc:  # report, never hide
+                sweep[f"L{Ls}"] = {"error": repr(exc)}
+            torch.cuda.empty_cache()
+        line["c2_sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu:
-        from oracle import parallel_ref as PR
-
-        procs = args.ref_procs or PR.default_procs()
-        secs = _cpu_step(_cpu_case(L), procs)
-        hm1, hr1, _ = alg_bytes(L, k, 1, 1)
-        line["cpu_baseline"] = {"value": (hm1 + hr1) / secs / 1e9, "unit": "GB/s", "cores": procs,
-                                "kind": "port", "seconds": secs,
-                                "sample": _cpu_sample_text(L, procs)}
+        line["cpu_baseline"] = cpu_reference(L, args)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
