@@ -1,0 +1,76 @@
+"""Per-kernel CUDA-event times of one config-2 HMult batch + HRot batch (N=2^16,
+L=24, dnum=3, k=6, 64 ct, sequential issue; ring.KernelTimer around every
+wrapper) for A/B of builds: CKB_LIB=<variant .so> python tools/ks_micro.py [L] [B]"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2506_19693_b200 import he_api, ring  # noqa: E402
+
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+bsz = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+params, k = bench.c2_params(L)
+rng = np.random.default_rng(1234)
+steps = [int(s) for s in rng.integers(1, 1 << 15, bsz)]
+cust = he_api.keygen(params, set(steps), backend="ckks", rng_seed=99, prime_layout="baseline",
+                     dnum=bench.DNUM, secret_hw=192)
+be = cust.backend
+lvl = params.level
+m = be.chain.level_limbs[lvl]
+n = 1 << bench.N_LOG
+g = torch.Generator(device="cuda")
+g.manual_seed(7)
+
+
+def rb():
+    t = torch.empty(bsz, 2, m, n, dtype=torch.int64, device="cuda")
+    for i, p in enumerate(be.chain.limbs_at(lvl)):
+        t[:, :, i].random_(0, p, generator=g)
+    return t.view(torch.uint64)
+
+
+A, B = rb(), rb()
+for _ in range(2):
+    be.batch_hmult(A, B, lvl)
+    be.batch_hrot(A, steps, lvl)
+torch.cuda.synchronize()
+reps = 5
+res = {}
+for name, fn in (("hmult", lambda: be.batch_hmult(A, B, lvl)),
+                 ("hrot", lambda: be.batch_hrot(A, steps, lvl))):
+    t = ring.KernelTimer()
+    ring.TIMER = t
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    ring.TIMER = None
+    res[name] = {"total": round(e0.elapsed_time(e1) / reps, 3),
+                 **{kk: round(v["ms"] / reps, 3) for kk, v in t.summary().items()}}
+# the pair on two streams, untimed per kernel
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    prev = be.chain.set_ntt_chunk_bytes(48 << 20)
+    with torch.cuda.stream(s1):
+        be.batch_hmult(A, B, lvl)
+    with torch.cuda.stream(s2):
+        be.batch_hrot(A, steps, lvl)
+    be.chain.set_ntt_chunk_bytes(prev)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+e1.record()
+torch.cuda.synchronize()
+res["pair_ms"] = round(e0.elapsed_time(e1) / reps, 3)
+print(os.environ.get("CKB_LIB", "default").split("/")[-2], json.dumps(res))
