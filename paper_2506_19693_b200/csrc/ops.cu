@@ -360,6 +360,164 @@ __global__ void __launch_bounds__(256) k_modup_mixed(
   }
 }
 
+// ModUp v2 (alpha > 1): the digit's outputs are split once per CTA into an
+// FP64 list (output prime < 2^46 and every digit prime < 2^46: y_i exact in a
+// double, sum_i mulmod_f64 on the FP64 pipe) and an integer list (Acc4
+// carry-free sums + one reduction on the integer pipes), so the per-output loops
+// carry no class branches, and each thread converts TWO coefficients (16-byte
+// loads and stores; the constants loaded from shared memory serve both).
+// y_i is kept in doubles: the exact value when the digit is FP64-class, else
+// the bit pattern of the u64 (the integer loop reads it back either way).
+// Smem: [nf][AMAX] double2 {c, c/p} | [nf] double2 {p, 1/p} | [ni][AMAX] pack30(c)
+//       | [ni] ModSm | [nf + ni] int row index | [AMAX] {qinv, shoup, q}.
+#ifndef CKB_MODUP_MINB
+#define CKB_MODUP_MINB 2
+#endif
+template <int AMAX>
+__global__ void __launch_bounds__(256, CKB_MODUP_MINB) k_modup_v2(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_bstride, int batch,
+    int limbs, int ext, int alpha, int out_rows, int item_rows, int skip_own, int log_n,
+    RingDev R, LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv) {
+  extern __shared__ __align__(16) uint64_t sm[];
+  __shared__ int s_nf, s_ni, s_fin;
+  const size_t N = (size_t)1 << log_n;
+  const int j = blockIdx.y;
+  const int first = j * alpha;
+  const int cnt = min(alpha, limbs - first);
+  const size_t stride_i = 2 + 2 * (size_t)ext;
+  const uint64_t* tab = bconv + (size_t)j * alpha * stride_i;
+  double2* fc = reinterpret_cast<double2*>(sm);
+  double2* fpp = fc + (size_t)ext * AMAX;
+  uint64_t* ic = reinterpret_cast<uint64_t*>(fpp + ext);
+  ModSm* ims = reinterpret_cast<ModSm*>(ic + (size_t)ext * AMAX);
+  int* rowi = reinterpret_cast<int*>(ims + ext);       // [ext]: f rows then i rows
+  uint64_t* qc = reinterpret_cast<uint64_t*>(rowi + 2 * ext + 2);
+  if (threadIdx.x == 0) {
+    int fin = 1;
+    for (int i = 0; i < cnt; ++i)
+      fin &= (__ldg(R.mods + (size_t)lm.p[first + i] * kModStride) >> 46) == 0;
+    int nf = 0, ni = 0;
+    for (int e = 0; e < ext; ++e) {
+      if (e >= first && e < first + cnt) continue;
+      const bool f = fin && (__ldg(R.mods + (size_t)em.p[e] * kModStride) >> 46) == 0;
+      const int row = digit_row(e, first, cnt, skip_own);
+      if (f) rowi[nf++] = (e << 16) | row;
+      else rowi[ext + ni++] = (e << 16) | row;
+    }
+    s_nf = nf;
+    s_ni = ni;
+    s_fin = fin;
+  }
+  __syncthreads();
+  const int nf = s_nf, ni = s_ni;
+  const bool fin = s_fin;
+  for (int q = threadIdx.x; q < nf * AMAX; q += blockDim.x) {
+    const int a = q / AMAX, i = q % AMAX;
+    const int e = rowi[a] >> 16;
+    const double pe = (double)__ldg(R.mods + (size_t)em.p[e] * kModStride);
+    const double c = i < cnt ? (double)__ldg(tab + (size_t)i * stride_i + 2 + 2 * e) : 0.0;
+    fc[q] = make_double2(c, c / pe);
+  }
+  for (int a = threadIdx.x; a < nf; a += blockDim.x) {
+    const double pe = (double)__ldg(R.mods + (size_t)em.p[rowi[a] >> 16] * kModStride);
+    fpp[a] = make_double2(pe, 1.0 / pe);
+  }
+  for (int q = threadIdx.x; q < ni * AMAX; q += blockDim.x) {
+    const int b = q / AMAX, i = q % AMAX;
+    const int e = rowi[ext + b] >> 16;
+    ic[q] = i < cnt ? ckb::pack30(__ldg(tab + (size_t)i * stride_i + 2 + 2 * e)) : 0;
+  }
+  for (int b = threadIdx.x; b < ni; b += blockDim.x) {
+    const uint64_t* mm = R.mods + (size_t)em.p[rowi[ext + b] >> 16] * kModStride;
+    ims[b] = ModSm{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3), __ldg(mm + 8),
+                   __ldg(mm + 9)};
+  }
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    qc[3 * i] = __ldg(tab + (size_t)i * stride_i);
+    qc[3 * i + 1] = __ldg(tab + (size_t)i * stride_i + 1);
+    qc[3 * i + 2] = __ldg(R.mods + (size_t)lm.p[first + i] * kModStride);
+  }
+  __syncthreads();
+  const size_t half = N >> 1;
+  const size_t total = (size_t)batch * half;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = (t & (half - 1)) * 2;
+    const size_t bi = t / half;
+    const uint64_t* src = in + bi * in_bstride + n;
+    uint64_t* dst = out + (bi * (size_t)item_rows + (size_t)j * out_rows) * N + n;
+    double y0[AMAX], y1[AMAX];
+#pragma unroll
+    for (int i = 0; i < AMAX; ++i) {
+      if (i < cnt) {
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(src + (size_t)(first + i) * N));
+        const uint64_t w = qc[3 * i], ws = qc[3 * i + 1], q = qc[3 * i + 2];
+        const uint64_t a = ckb::mul_shoup(x.x, w, ws, q), b = ckb::mul_shoup(x.y, w, ws, q);
+        y0[i] = fin ? ckb_f64::u64_to_f64(a) : __longlong_as_double((long long)a);
+        y1[i] = fin ? ckb_f64::u64_to_f64(b) : __longlong_as_double((long long)b);
+        if (!skip_own)
+          *reinterpret_cast<ulonglong2*>(dst + (size_t)(first + i) * N) = x;
+      } else {
+        y0[i] = y1[i] = 0.0;  // short last digit: zero terms (0.0 has bit pattern 0)
+      }
+    }
+    for (int a = 0; a < nf; ++a) {  // FP64 pipe
+      const double2 pp = fpp[a];
+      const double2* cr = fc + (size_t)a * AMAX;
+      double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+#pragma unroll
+      for (int i = 0; i < AMAX; i += 2) {
+        const double2 c = cr[i];
+        s00 += ckb_f64::mulmod_f64(y0[i], c.x, c.y, pp.x);
+        s10 += ckb_f64::mulmod_f64(y1[i], c.x, c.y, pp.x);
+        if (i + 1 < AMAX) {
+          const double2 d = cr[i + 1];
+          s01 += ckb_f64::mulmod_f64(y0[i + 1], d.x, d.y, pp.x);
+          s11 += ckb_f64::mulmod_f64(y1[i + 1], d.x, d.y, pp.x);
+        }
+      }
+      ulonglong2 o;
+      o.x = ckb_f64::f64_to_u64(ckb_f64::canon_f64(s00 + s01, pp.x, pp.y));
+      o.y = ckb_f64::f64_to_u64(ckb_f64::canon_f64(s10 + s11, pp.x, pp.y));
+      *reinterpret_cast<ulonglong2*>(dst + (size_t)(rowi[a] & 0xFFFF) * N) = o;
+    }
+    for (int b = 0; b < ni; ++b) {  // integer pipes
+      const uint64_t* cr = ic + (size_t)b * AMAX;
+      uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll
+      for (int i0 = 0; i0 < AMAX; i0 += 8) {  // <= 8 terms per 64-bit partial
+        ckb::Acc4 a0, a1;
+#pragma unroll
+        for (int i = i0; i < (i0 + 8 < AMAX ? i0 + 8 : AMAX); ++i) {
+          const ckb::Split30 c = ckb::unpack30(cr[i]);
+          const uint64_t u0 = fin ? ckb_f64::f64_to_u64(y0[i]) : (uint64_t)__double_as_longlong(y0[i]);
+          const uint64_t u1 = fin ? ckb_f64::f64_to_u64(y1[i]) : (uint64_t)__double_as_longlong(y1[i]);
+          a0.mac(ckb::split30(u0), c);
+          a1.mac(ckb::split30(u1), c);
+        }
+        a0.fold_into(h0, l0);
+        a1.fold_into(h1, l1);
+      }
+      const ModSm ms = ims[b];
+      const Mod m{ms.p, ms.mu, ms.k, ms.two_p};
+      ulonglong2 o;
+      if (ms.k >= 32) {  // CTA-uniform
+        o.x = ckb::reduce128_big(h0, l0, ms.r64, ms.r64s, m);
+        o.y = ckb::reduce128_big(h1, l1, ms.r64, ms.r64s, m);
+      } else {
+        o.x = ckb::reduce128_any(h0, l0, ms.r64, ms.r64s, m);
+        o.y = ckb::reduce128_any(h1, l1, ms.r64, ms.r64s, m);
+      }
+      *reinterpret_cast<ulonglong2*>(dst + (size_t)(rowi[ext + b] & 0xFFFF) * N) = o;
+    }
+  }
+}
+
+inline size_t modup_v2_smem(int ext, int amax) {
+  return (size_t)ext * amax * 16 + (size_t)ext * 16 + (size_t)ext * amax * 8 +
+         (size_t)ext * sizeof(ModSm) + (2 * (size_t)ext + 2) * 4 + 3 * (size_t)amax * 8 + 16;
+}
+
 // acc[b][c][e] = sum_j digit_j[e] * key_b[j][c][key_limb(e)] with 128-bit lazy
 // accumulation and one reduction per output.  With own != NULL the digits'
 // own limbs come from `own` (the NTT-domain input the digits were cut from);
@@ -1494,6 +1652,26 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
     digit_f64 = ok;
   }
   for (int e = 0; e < ext_limbs; ++e) out_f64 |= is_f64(em.p[e]);
+#ifndef CKB_MODUP_V1
+  if (alpha > 1) {  // per-class output lists, two coefficients per thread
+    using KernV = decltype(&k_modup_v2<2>);
+    static const KernV vk[17] = {nullptr, nullptr, k_modup_v2<2>, k_modup_v2<3>, k_modup_v2<4>,
+                                 k_modup_v2<5>, k_modup_v2<6>, k_modup_v2<7>, k_modup_v2<8>,
+                                 k_modup_v2<9>, k_modup_v2<10>, k_modup_v2<11>, k_modup_v2<12>,
+                                 k_modup_v2<13>, k_modup_v2<14>, k_modup_v2<15>, k_modup_v2<16>};
+    const size_t vsmem = modup_v2_smem(ext_limbs, alpha);
+    if (vsmem > 200 * 1024) return CKB_E_ARG;
+    if (vsmem > 48 * 1024)
+      cudaFuncSetAttribute(vk[alpha], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem);
+    const size_t work = (size_t)batch << (R.log_n - 1);
+    dim3 vgrid((unsigned)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096 / nd + 1)),
+               (unsigned)nd);
+    vk[alpha]<<<vgrid, 256, vsmem, (cudaStream_t)stream>>>(
+        out, in, bstride, batch, limbs, ext_limbs, alpha, out_rows, item_rows, skip_own,
+        (int)R.log_n, R, lm, em, bconv);
+    return finish();
+  }
+#endif
   if (alpha > 1 && alpha <= 16 && digit_f64 && out_f64) {
     using KernM = decltype(&k_modup_mixed<2, false>);
 #define CKB_MM(C)                                                                            \

@@ -73,4 +73,4 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 res["pair_ms"] = round(e0.elapsed_time(e1) / reps, 3)
-print(os.environ.get("CKB_LIB", "default").split("/")[-2], json.dumps(res))
+print((os.environ.get("CKB_LIB") or "x/default/x").split("/")[-2], json.dumps(res))
