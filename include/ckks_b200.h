@@ -103,6 +103,21 @@ int ckb_ntt_inverse_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* sr
                          int64_t src_item_stride, int rows, int limbs, const int32_t* limb_prime,
                          void* stream);
 
+/* Key switching, steps 3-4 fused for N > 4096 (keys.py:88-97): the digits
+ * written by ckb_modup with skip_own ([batch][item_rows][N], coefficient
+ * domain; used as scratch) are forward-transformed — the column phase per
+ * L2-resident chunk of items, then ONE kernel per chunk that finishes each
+ * (item, extended limb, row tile) for every digit and accumulates the products
+ * with the key rows — so acc ([batch][2][ext][N], NTT domain) is written
+ * directly: replaces ckb_ntt_forward(digits) + ckb_ks_inner.  digit_prime: the
+ * prime index of each digits row of one item (item_rows entries, the compact
+ * skip_own order); the other arguments as ckb_ks_inner. */
+int ckb_ks_ntt_mac(const ckb_ring* ring, uint64_t* acc, uint64_t* digits, int batch, int limbs,
+                   int alpha, int ext_limbs, const int32_t* ext_prime, const int32_t* digit_prime,
+                   const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                   const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                   void* stream);
+
 /* Limb-wise arithmetic over rows*N residues.  Replace RingElement.add/sub/neg/
  * mul (ring.py:80-131).  op: 0 add, 1 sub, 2 mul (Hadamard), 3 neg (b unused),
  * 4 mul_add: out = a*b + c.  If 0 < b_rows < rows, b (and c) hold b_rows rows

@@ -470,6 +470,10 @@ class B200CkksCore:
         digits = ch.modup(d, m, a, self._bconv(m, k), batch=batch, in_batch_stride=d_stride,
                           skip_own=skip, k=k)
         basis = ch.digit_basis(m, a, skip, k)
+        if skip and ch.fuse_ks_mac and ch.log_n in (16, 17):
+            # the digits' row-phase transform fused with the inner product
+            return ch.ks_ntt_mac(digits, m, a, key=key.data if key is not None else None,
+                                 key_ptrs=key_ptrs, own=own, own_bstride=own_stride, k=k)
         ch.ntt_fwd(digits, len(basis), ch.cmap(basis))
         return ch.ks_inner(digits, m, a, key=key.data if key is not None else None,
                            key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride,

@@ -766,6 +766,164 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
   return finish();
 }
 
+// ---------------------------------------------------------------------------
+// Key switching: the digits' forward NTT row phase fused with the key inner
+// product (keys.py:91-97).  ModUp's digits, after the column phase, are
+// finished row tile by row tile; one CTA owns (item, extended limb e, tile)
+// and, for every digit j, transforms digit j's row of limb e (or, for the limb
+// the digit owns, reads the NTT-domain input it was cut from), multiplies it
+// by key_j's (b, a) rows and accumulates — so the transformed digits never go
+// to HBM and the separate inner-product pass (k_ks_inner) disappears.
+// Accumulators live in shared memory (each thread owns its pairs: no barrier
+// between digits beyond the tile's own); FP64-class rows accumulate exact
+// mulmod_f64 terms (|acc| <= 1.5 p nd), integer rows Barrett products.
+// ---------------------------------------------------------------------------
+struct KsMac {
+  uint64_t* acc;                 // [batch][2][ext][N]
+  const uint64_t* dig;           // [batch][item_rows][N] after the column phase
+  const uint64_t* own;           // NTT-domain input limbs, item stride own_bs
+  size_t own_bs;
+  const uint64_t* key;           // one key, or
+  const uint64_t* const* key_ptrs;  // one key per item
+  int key_limbs, nd, ext, out_rows, item_rows, alpha, m, item0, tiles;
+};
+
+template <int S, int RBT>
+__global__ void __launch_bounds__(128, 4)
+    k_ntt_rows_mac(KsMac km, RingDev R, LimbMap em, LimbMap kmap) {
+  constexpr int G = 1 << S;
+  constexpr int RB = S < RBT ? S : RBT;
+  constexpr int E = 1 << RB;
+  constexpr int C = kTwoPhaseTile / G;  // rows (groups) per tile
+  constexpr int T = C * G / E;          // threads
+  static_assert((G / E) <= 32, "row groups must be warp-local");
+  extern __shared__ uint64_t smem[];
+  double2* accb = reinterpret_cast<double2*>(smem + C * (G + G / 16 + G / 128));
+  double2* acca = accb + (E / 2) * T;
+  const int N = 1 << R.log_n;
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x % km.tiles;
+  const int e = (blockIdx.x / km.tiles) % km.ext;
+  const int item = km.item0 + blockIdx.x / (km.tiles * km.ext);
+  const int pi = em.p[e];
+  const uint64_t* mm = R.mods + (size_t)pi * kModStride;
+  const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
+  const bool f64 = (p >> 46) == 0;  // CTA-uniform
+  const Mod mod{p, __ldg(mm + 1), __ldg(mm + 2), two_p};
+  const double pd = (double)p, pinv = 1.0 / pd;
+  const int g0 = tile * C;
+  const int gq = tid / (G / E), w = tid % (G / E);
+  const int tbase = N / G + g0 + gq;  // row phase: M0 = N/G, gt = 1
+  const uint64_t* K = km.key_ptrs ? km.key_ptrs[item] : km.key;
+  const size_t krow = 2 * (size_t)km.key_limbs * N;
+  const uint64_t* kb0 = K + (size_t)kmap.p[e] * N;
+  const int owner = e < km.m ? e / km.alpha : -1;
+  auto pair_off = [&](int i, int& g, int& r) -> size_t {  // warp-local pairs of my row
+    g = tid / (G / E);
+    r = 2 * (tid % (G / E) + (G / E) * i);
+    return (size_t)(g0 + g) * G + r;
+  };
+  for (int j = 0; j < km.nd; ++j) {
+    const bool is_own = j == owner;
+    if (!is_own) {
+      const int cj = min(km.alpha, km.m - j * km.alpha);
+      const int drow = j * km.out_rows + (e >= j * km.alpha + cj ? e - cj : e);
+      const uint64_t* base = km.dig + ((size_t)item * km.item_rows + drow) * N;
+      if (f64) {
+        const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
+        fwd_rounds_f64<S, RB, S, false>(smem, dtab, pd, pinv, gq, tbase, w, 1,
+                                        base + (size_t)(g0 + gq) * G, nullptr, 1, false);
+      } else {
+        ulonglong2 v[E / 2];
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) {
+          int g, r;
+          v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(base + pair_off(i, g, r)));
+        }
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) {
+          int g, r;
+          pair_off(i, g, r);
+          smem[sidx<S>(g, r)] = v[i].x;
+          smem[sidx<S>(g, r + 1)] = v[i].y;
+        }
+        __syncwarp();
+        const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
+        fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, 1);
+      }
+      __syncwarp();
+    }
+    const uint64_t* kb = kb0 + j * krow;
+    const uint64_t* ka = kb + (size_t)km.key_limbs * N;
+    const uint64_t* orow = is_own ? km.own + (size_t)item * km.own_bs + (size_t)e * N : nullptr;
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      int g, r;
+      const size_t off = pair_off(i, g, r);
+      ulonglong2 x;
+      if (is_own) {
+        x = *reinterpret_cast<const ulonglong2*>(orow + off);
+      } else {
+        x.x = smem[sidx<S>(g, r)];
+        x.y = smem[sidx<S>(g, r + 1)];
+      }
+      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(kb + off));
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(ka + off));
+      const int slot = i * T + tid;
+      if (f64) {
+        const double x0 = u64_to_f64(x.x), x1 = u64_to_f64(x.y);
+        const double b0 = u64_to_f64(b.x), b1 = u64_to_f64(b.y);
+        const double a0 = u64_to_f64(a.x), a1 = u64_to_f64(a.y);
+        double2 tb = make_double2(mulmod_f64(x0, b0, b0 * pinv, pd), mulmod_f64(x1, b1, b1 * pinv, pd));
+        double2 ta = make_double2(mulmod_f64(x0, a0, a0 * pinv, pd), mulmod_f64(x1, a1, a1 * pinv, pd));
+        if (j) {
+          const double2 pb = accb[slot], pa = acca[slot];
+          tb.x += pb.x;
+          tb.y += pb.y;
+          ta.x += pa.x;
+          ta.y += pa.y;
+        }
+        accb[slot] = tb;
+        acca[slot] = ta;
+      } else {
+        uint64_t tb0 = ckb::mul_mod(x.x, b.x, mod), tb1 = ckb::mul_mod(x.y, b.y, mod);
+        uint64_t ta0 = ckb::mul_mod(x.x, a.x, mod), ta1 = ckb::mul_mod(x.y, a.y, mod);
+        if (j) {
+          const double2 pb = accb[slot], pa = acca[slot];
+          tb0 = ckb::add_mod(tb0, (uint64_t)__double_as_longlong(pb.x), p);
+          tb1 = ckb::add_mod(tb1, (uint64_t)__double_as_longlong(pb.y), p);
+          ta0 = ckb::add_mod(ta0, (uint64_t)__double_as_longlong(pa.x), p);
+          ta1 = ckb::add_mod(ta1, (uint64_t)__double_as_longlong(pa.y), p);
+        }
+        accb[slot] = make_double2(__longlong_as_double((long long)tb0),
+                                  __longlong_as_double((long long)tb1));
+        acca[slot] = make_double2(__longlong_as_double((long long)ta0),
+                                  __longlong_as_double((long long)ta1));
+      }
+    }
+    __syncwarp();  // the next digit's rounds reuse the tile
+  }
+  uint64_t* ob = km.acc + ((size_t)item * 2 * km.ext + e) * N;
+  uint64_t* oa = ob + (size_t)km.ext * N;
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) {
+    int g, r;
+    const size_t off = pair_off(i, g, r);
+    const int slot = i * T + tid;
+    const double2 vb = accb[slot], va = acca[slot];
+    ulonglong2 b, a;
+    if (f64) {
+      b = make_ulonglong2(f64_to_u64(canon_f64(vb.x, pd, pinv)), f64_to_u64(canon_f64(vb.y, pd, pinv)));
+      a = make_ulonglong2(f64_to_u64(canon_f64(va.x, pd, pinv)), f64_to_u64(canon_f64(va.y, pd, pinv)));
+    } else {
+      b = make_ulonglong2((uint64_t)__double_as_longlong(vb.x), (uint64_t)__double_as_longlong(vb.y));
+      a = make_ulonglong2((uint64_t)__double_as_longlong(va.x), (uint64_t)__double_as_longlong(va.y));
+    }
+    *reinterpret_cast<ulonglong2*>(ob + off) = b;
+    *reinterpret_cast<ulonglong2*>(oa + off) = a;
+  }
+}
+
 // ALU ceiling probe (the IMAD pipe is the NTT's binding
 // roofline, so its peak is measured, not assumed).  Each thread keeps 8
 // residues in registers and runs radix-8 rounds of the same lazy CT butterfly
@@ -883,6 +1041,74 @@ int ckb_ntt_inverse_from(const ckb_ring* ring, uint64_t* dst, const uint64_t* sr
                         src_item_stride ? (size_t)src_item_stride : ((size_t)limbs << ring->log_n));
 }
 
+
+int ckb_ks_ntt_mac(const ckb_ring* ring, uint64_t* acc, uint64_t* digits, int batch, int limbs,
+                   int alpha, int ext_limbs, const int32_t* ext_prime, const int32_t* digit_prime,
+                   const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                   const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                   void* stream) {
+  LimbMap em, kmap;
+  if (!make_map(em, ext_prime, ext_limbs) || !make_map(kmap, key_limb, ext_limbs))
+    return CKB_E_LIMBS;
+  if (batch < 0 || alpha < 1 || limbs < 1 || ext_limbs <= limbs || !own || !digits || !acc ||
+      (!key && !key_ptrs))
+    return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const int logn = (int)R.log_n;
+  if (logn <= 12 || logn > 20) return CKB_E_LOGN;  // two-phase transforms only
+  const int nd = (limbs + alpha - 1) / alpha;
+  const int out_rows = ext_limbs - alpha;
+  const int item_rows = (nd - 1) * out_rows + ext_limbs - (limbs - (nd - 1) * alpha);
+  if (item_rows > kMaxLimbs) return CKB_E_LIMBS;
+  LimbMap dm;
+  if (!make_map(dm, digit_prime, item_rows)) return CKB_E_LIMBS;
+  if (!batch) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = 1 << logn;
+  const int s2 = logn / 2, s1 = logn - s2;
+  if (s1 > 12 || s2 != 8) return CKB_E_LOGN;  // the fused row kernel is built for 256-row groups
+  const int GA = 1 << s1, GB = 1 << s2;
+  const int CA = std::max(1, kTwoPhaseTile / GA), CB = std::max(1, kTwoPhaseTile / GB);
+  auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
+  bool any_f64 = false, any_int = false;
+  for (int i = 0; i < item_rows; ++i) {
+    const int pi = dm.p[i];
+    ((R.f64_mask[pi >> 6] >> (pi & 63)) & 1 ? any_f64 : any_int) = true;
+  }
+  const size_t budget = R.ntt_chunk_bytes ? (size_t)R.ntt_chunk_bytes : kDefaultNttChunkBytes;
+  const int chunk = std::max(1, (int)(budget / ((size_t)item_rows * N * 8)));
+  const bool mixed_one_kernel = !(R.flags & CKB_RING_NTT_SPLIT);
+  KsMac km{acc, digits, own, own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << logn),
+           key, key_ptrs, key_limbs, nd, ext_limbs, out_rows, item_rows, alpha, limbs, 0, GA / CB};
+  constexpr int S = 8, RBT = 4;
+  constexpr int G = 1 << S, E = 1 << RBT, C = kTwoPhaseTile / G, T = C * G / E;
+  const size_t smem = (size_t)C * (G + G / 16 + G / 128) * 8 + 2 * (size_t)(E / 2) * T * 16;
+  static bool attr = false;  // idempotent, set before the first launch of this process
+  if (!attr) {
+    cudaFuncSetAttribute(k_ntt_rows_mac<S, RBT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  for (int i0 = 0; i0 < batch; i0 += chunk) {
+    const int ni = std::min(chunk, batch - i0);
+    uint64_t* data = digits + (size_t)i0 * item_rows * N;
+    // column phase of the chunk's digit rows (limb-major within the chunk)
+    NttPhase pa{item_rows, GB / CA, CA, 1, GB, 1, 0, 0, 0, lg(CA), ni > 1 ? ni : 0, 1, nullptr, 0};
+    int rc;
+    const int rows = ni * item_rows;
+    if (!any_f64 || (any_int && mixed_one_kernel)) {
+      rc = launch_phase<true, 4, 0>(s1, data, pa, rows, R, dm, st);
+    } else {
+      rc = launch_phase<true, 4, 1>(s1, data, pa, rows, R, dm, st);
+      if (!rc && any_int) rc = launch_phase<true, 4, 2>(s1, data, pa, rows, R, dm, st);
+    }
+    if (rc) return rc;
+    km.item0 = i0;
+    const int blocks = ni * ext_limbs * km.tiles;
+    k_ntt_rows_mac<S, RBT><<<blocks, T, smem, st>>>(km, R, em, kmap);
+  }
+  return finish();
+}
 
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream) {
   if (p < 3 || (p >> 62) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;

@@ -398,6 +398,38 @@ class GpuChain:
                                  key_limbs, self.ext_map(m, k), nat.stream_handle()), "ks_inner"))
         return out
 
+    # digits' row-phase NTT fused with the key inner product (ckb_ks_ntt_mac,
+    # N = 2^16 / 2^17).  Bit-identical to the unfused path (tests) but slower
+    # on the config-2 batch (6.0 ms vs 4.7 ms for NTT + ks_inner per 64-ct
+    # HMult: three serial row passes per CTA at 16 warps/SM), so off by default.
+    fuse_ks_mac = False
+
+    def ks_ntt_mac(self, digits, m: int, alpha: int, key: torch.Tensor = None,
+                   key_ptrs: torch.Tensor = None, own: torch.Tensor = None, own_bstride: int = 0,
+                   out=None, k: int = None):
+        """Forward NTT of ckb_modup's skip_own digits fused with the inner
+        product (ckb_ks_ntt_mac): acc [batch, 2, m + k, N], NTT domain; the
+        digits tensor is scratch afterwards."""
+        batch = digits.shape[0]
+        nd = -(-m // alpha)
+        k = self.k if k is None else k
+        ext = m + k
+        out = out if out is not None else torch.empty(batch, 2, ext, self.n, dtype=U64,
+                                                      device=self.device)
+        basis = self.digit_basis(m, alpha, True, k)
+        rows = batch * len(basis)
+        n_keys = batch if key_ptrs is not None else 1
+        nb = 2 * rows + n_keys * nd * 2 * ext + batch * (m + 2 * ext)  # NTT r/w, keys, own, acc
+        _run("ks_ntt_mac", nb * self.n * W, self._ntt_launches(rows), lambda: nat.check(
+            nat.LIB.ckb_ks_ntt_mac(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, m, alpha,
+                                   ext, self.ext_map(m, k), self.cmap(basis), nat.ptr(own),
+                                   own_bstride,
+                                   nat.ptr(key) if key is not None else None,
+                                   nat.ptr(key_ptrs) if key_ptrs is not None else None,
+                                   self.lq + k, self.ext_map(m, k), nat.stream_handle()),
+            "ks_ntt_mac"), self._f64_share(self.cmap(basis), len(basis)))
+        return out
+
     def divround(self, x, polys: int, limbs: int, n1: int, n2: int = 0, addend=None,
                  addend_polys: int = 0, addend_period: int = 1, addend_stride: int = None,
                  prescale=None, in_poly_stride: int = 0, basis: tuple = None, out=None):

@@ -202,3 +202,46 @@ def test_c2_full_size_digest(c2_digests, L):
     ca, cb = be._wrap(_wrap_payload(a, lvl), lvl, 0), be._wrap(_wrap_payload(b, lvl), lvl, 0)
     assert _sha(be.planes_of(ev.mul(ca, cb).payload)) == g["hmult_sha256"]
     assert _sha(be.planes_of(ev.rotate(ca, g["rot_step"]).payload)) == g["hrot_sha256"]
+
+
+@pytest.mark.parametrize("case", ["c2_L24", "c2_L23_short_digit", "bootstrap_layout_low_p"])
+def test_fused_ntt_mac_equals_unfused(case):
+    """ckb_ks_ntt_mac (the digits' row-phase NTT fused with the key inner
+    product, N=2^16) gives the same ciphertexts as the unfused transform +
+    ckb_ks_inner, for batched HMult and per-item-key HRot: the config-2 chain,
+    a short last digit (L=23, digits 8/8/7) and the bootstrap layout (60-bit Q
+    primes: integer-class rows in the fused kernel) with a level-aware special
+    modulus (keys over Q u P', k' < k)."""
+    n = 1 << 16
+    if case.startswith("c2"):
+        L = 24 if case == "c2_L24" else 23
+        params, _, _ = _c2_params(L, n)
+        opts = dict(prime_layout="baseline", dnum=DNUM, secret_hw=192)
+    else:
+        from paper_2506_19693_b200.scheme import SchemeParams
+
+        params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 4 + (60,) * 2 + (360,),
+                              scale_bits=45, level=6, bootstrap_depth=2)
+        opts = dict(prime_layout="bootstrap", dnum=3, secret_hw=64, low_special=[(4, 4)])
+    rng = np.random.default_rng(3)
+    steps = [int(s) for s in rng.choice(np.arange(1, n // 2), size=3, replace=False)]
+    cust = he_api.keygen(params, set(steps), backend="ckks", rng_seed=5, **opts)
+    be = cust.backend
+    ch = be.chain
+    for lvl in sorted({params.level, 3}):
+        m = ch.level_limbs[lvl]
+        x = torch.stack([be.payload_from_planes(_planes(ch.limbs_at(lvl), n, rng), lvl).data
+                         for _ in range(3)])
+        y = torch.stack([be.payload_from_planes(_planes(ch.limbs_at(lvl), n, rng), lvl).data
+                         for _ in range(3)])
+        outs = []
+        for fused in (True, False):
+            type(ch).fuse_ks_mac = fused
+            try:
+                outs.append((be.batch_hmult(x, y, lvl).clone(), be.batch_hrot(x, steps, lvl).clone(),
+                             be._hrot(x, lvl, galois=be.galois_for_step[steps[0]],
+                                      key=be.rotation_key(be.galois_for_step[steps[0]])).clone()))
+            finally:
+                type(ch).fuse_ks_mac = False
+        for a, b in zip(*outs):
+            assert torch.equal(a.view(torch.int64), b.view(torch.int64)), (case, lvl, m)

@@ -12,6 +12,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2506_19693_b200 import he_api, ring  # noqa: E402
 
+if os.environ.get("CKB_FUSE_KS"):  # A/B: 1 = fused digits NTT + inner product
+    ring.GpuChain.fuse_ks_mac = os.environ["CKB_FUSE_KS"] == "1"
+
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 bsz = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 params, k = bench.c2_params(L)
@@ -73,4 +76,7 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 res["pair_ms"] = round(e0.elapsed_time(e1) / reps, 3)
-print((os.environ.get("CKB_LIB") or "x/default/x").split("/")[-2], json.dumps(res))
+tag = (os.environ.get("CKB_LIB") or "x/default/x").split("/")[-2]
+if os.environ.get("CKB_FUSE_KS") == "1":
+    tag += "+fused"
+print(tag, json.dumps(res))
