@@ -30,6 +30,8 @@ Extra keyword options (all default to the reference's behaviour):
   device        CUDA device (default: current)
   encoder       "device" (cuFFT) | "numpy" (the reference's host FFT, bit-identical
                 encodings/decodings: mode-A whole-step parity tests only)
+  deferred      record HE calls and run them batched (executor.WaveExecutor) when a
+                result is decrypted / serialized / flushed (deferred.py)
 """
 
 from __future__ import annotations
@@ -229,7 +231,8 @@ class B200CkksCore:
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
                  secret_hw=None, device=None, encode_cache: int = 512,
                  conjugation_key: bool = False, real_bootstrap: bool = False,
-                 sampler: str = None, low_special=None, encoder: str = "device"):
+                 sampler: str = None, low_special=None, encoder: str = "device",
+                 deferred: bool = False, deferred_max_group: int = None):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -352,6 +355,18 @@ class B200CkksCore:
             if self._ks_tiers:
                 self.k_low = self._ks_tiers[0][1]
         self._bs_rng = np.random.default_rng(rng_seed + 0x5EED)
+        # deferred=True: HE calls are recorded and run batched on the first
+        # decrypt / serialize / flush (deferred.py)
+        self._rec = None
+        if deferred:
+            from .deferred import Recorder
+
+            self._rec = Recorder(self, max_group=deferred_max_group)
+
+    def flush(self) -> None:
+        """Run every deferred HE call recorded so far (no-op when eager)."""
+        if self._rec is not None:
+            self._rec.flush()
 
     # ------------------------------------------------------------------ keys
     def _to_ntt_all(self, coeffs: np.ndarray) -> torch.Tensor:
@@ -578,6 +593,16 @@ class B200CkksCore:
             self._enc_cache.popitem(last=False)
         return res
 
+    def _check_encodable(self, values, level: int) -> None:
+        """Deferred mode: raise EncodingOverflow at call time, as the eager
+        encode would (encoding.py:46-48, 60-64).  The host-side bound clears
+        almost every vector; the others are encoded exactly now."""
+        vals = np.asarray(values, dtype=np.float64)
+        hb = _coeff_bound(vals, self._scale(level), self.n)
+        if hb < self._encode_limit and 4 * int(hb) < self.chain.modulus_at(level):
+            return
+        self._encode_rns(vals, level)
+
     def encode_many(self, items) -> None:
         """Batched _encode_rns for [(values, level, ntt)]: one FFT, one residue
         conversion and one NTT launch per (level, ntt) group, results stored in
@@ -618,6 +643,15 @@ class B200CkksCore:
 
     # ------------------------------------------------------------------ hooks
     def _payload_elementwise(self, kind: str, a, b, out_level: int):
+        if self._rec is not None:
+            r = self._rec
+            if kind.endswith("_ct"):
+                ib = r.operand(b.payload)
+            else:
+                self._check_encodable(b.values if kind[:3] != "sub" else -b.values,
+                                      a.level_remaining)
+                ib = r.plaintext(b.values)
+            return r.record(("ew", kind, None, r.operand(a.payload), ib), out_level)
         ch = self.chain
         ct_a: GpuCiphertext = a.payload
         op = kind[:3]
@@ -667,6 +701,9 @@ class B200CkksCore:
         return out.view(bsz, 2, m - e, self.n)
 
     def _payload_rotate(self, a, k: int):
+        if self._rec is not None:
+            r = self._rec
+            return r.record(("rot", None, r.operand(a.payload), int(k)), a.level_remaining)
         ct: GpuCiphertext = a.payload
         if k == 0:
             return GpuCiphertext(ct.data.clone(), ct.level)
@@ -757,6 +794,11 @@ class B200CkksCore:
         return out
 
     def _payload_encrypt(self, pv, level: int, serial: int):
+        if self._rec is not None:  # the RNG serial the eager call would draw
+            self._check_encodable(pv.values, level)
+            r = self._rec
+            return r.record(("enc", None, r.plaintext(pv.values)), level,
+                            serial=next(self._serials))
         return self._encrypt_values(pv.values, level)
 
     def _phase(self, ct: GpuCiphertext) -> torch.Tensor:
@@ -796,6 +838,8 @@ class B200CkksCore:
         return (spec[self.encoder.bins] / sc).cpu().numpy()
 
     def _payload_decrypt(self, cv):
+        if self._rec is not None:
+            return self._decrypt_values(self._rec.resolve(cv.payload))
         return self._decrypt_values(cv.payload)
 
     def _payload_bootstrap(self, cv, serial: int):
@@ -803,6 +847,10 @@ class B200CkksCore:
         re-encrypt at refresh_level.  With real_bootstrap=True the ciphertext is
         instead dropped to level 0 and bootstrapped homomorphically
         (bootstrap.py); the serial is still consumed as the refresh would."""
+        if self._rec is not None:  # one serial, as either eager form draws
+            r = self._rec
+            return r.record(("bs", None, r.operand(cv.payload)), self.params.refresh_level,
+                            serial=next(self._serials))
         if self.real_bootstrap:
             next(self._serials)
             return self.bootstrap_ct(cv.payload)
@@ -816,6 +864,8 @@ class B200CkksCore:
     def serialize_cipher(self, cv) -> bytes:
         """RBCT (backend.py:210-222): header then c0, c1 coefficient planes, LE u64."""
         ct: GpuCiphertext = cv.payload
+        if self._rec is not None:
+            ct = self._rec.resolve(ct)
         head = struct.pack("<4sIQId", CT_MAGIC, SERIAL_VERSION, self.n, ct.level, cv.scale_bits)
         body = self._to_coeff(ct.data).cpu().numpy().astype("<u8").tobytes()
         return head + body
@@ -1009,6 +1059,8 @@ class B200CkksCore:
 
     def planes_of(self, payload: GpuCiphertext) -> np.ndarray:
         """Coefficient-domain (2, limbs, N) planes of a payload (RBCT order)."""
+        if self._rec is not None:
+            payload = self._rec.resolve(payload)
         return self._to_coeff(payload.data).cpu().numpy()
 
 

@@ -27,7 +27,7 @@ from .backend import GpuCiphertext
 
 
 class WaveExecutor:
-    def __init__(self, program, custodian, max_group: int = None):
+    def __init__(self, program, custodian, max_group: int = None, inputs: dict = None):
         """max_group: split a wave's same-signature group into sub-batches of at
         most this many ops (bounds the temporaries of very wide steps; results
         are unchanged — every op is computed independently)."""
@@ -35,6 +35,9 @@ class WaveExecutor:
         self.cust = custodian
         self.be = custodian.backend
         self.max_group = max_group
+        # values the program reads but no op produces (deferred.Recorder: the
+        # already-materialized operands), id -> level
+        self.inputs = dict(inputs or {})
         # added to every serial the plan assigns: a replayed step (graphs.
         # GraphedStep) draws fresh encryption randomness per replay
         self.serial_offset = 0
@@ -49,7 +52,7 @@ class WaveExecutor:
         counter = 0
         depth = {}
         waves = collections.defaultdict(list)
-        level = {}
+        level = dict(self.inputs)
         self._last_bs_depth = 0
         top = be.params.level
         rl = be.params.refresh_level
@@ -78,7 +81,7 @@ class WaveExecutor:
                 lvl = rl
             else:
                 raise ValueError(tag)
-            d = 1 + max((depth[x] for x in ins), default=0)
+            d = 1 + max((depth.get(x, 0) for x in ins), default=0)
             if tag == "bs" and not be.real_bootstrap:
                 # debug refreshes keep program order (their bs_rng draws); real
                 # bootstraps are deterministic and batch freely

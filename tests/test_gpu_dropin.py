@@ -89,3 +89,53 @@ def test_c1_step_baseline_primes_within_1e3_of_reference(installed, golden_dir):
     C.step(cust, model, shape, x, onehot)
     w = C.weights(model, cust)
     assert float(np.max(np.abs(w - gold_w))) <= 1e-3
+
+
+@needs[0]
+@needs[1]
+def test_c1_step_mode_a_deferred_byte_identical(installed, golden_dir):
+    """deferred=True (deferred.py): the unchanged train_iteration's HE calls are
+    recorded and run batched by the wave executor on the first decrypt /
+    serialize — with the same bytes as the reference (and as eager)."""
+    import c1_dropin as C
+
+    gold, gold_w = _gold(golden_dir)
+    installed(prime_layout="reference", sampler="numpy", encoder="numpy", deferred=True)
+    cust, model, shape, x, onehot = C.build()
+    seen = C.capture_refresh_inputs(cust)  # serializing the refresh inputs forces a flush
+    C.step(cust, model, shape, x, onehot)
+    outs = [C.sha(cust.backend.serialize_cipher(pm.payload)) for pm in C.outputs(model)]
+    assert seen == gold["refresh_inputs_sha256"]
+    assert outs == gold["outputs_sha256"]
+    assert np.array_equal(C.weights(model, cust), gold_w)
+
+
+@needs[0]
+@needs[1]
+def test_deferred_errors_surface_at_call_time(installed):
+    """Deferred mode keeps the HE API's error timing: level exhaustion and
+    missing keys from the base class, EncodingOverflow from the encode check."""
+    import c1_dropin as C
+
+    C.import_reference()
+    from ciphermlp.api import keygen, make_plain
+    from ciphermlp.errors import EncodingOverflow, LevelExhausted, MissingRotationKey
+    from ciphermlp.params import make_params
+
+    installed(deferred=True)
+    params = make_params(level=2, scale_bits=40, poly_degree=2**10)
+    cust = keygen(params, {1}, backend="ckks", rng_seed=1)
+    slots = params.slot_count
+    with pytest.raises(EncodingOverflow):
+        cust.encrypt(make_plain(np.full(slots, 2.0**25), slots, 40.0))
+    v = np.random.default_rng(0).uniform(-1, 1, slots)
+    ct = cust.encrypt(make_plain(v, slots, 40.0))
+    with pytest.raises(MissingRotationKey):
+        cust.evaluator.rotate(ct, 2)
+    x = ct
+    for _ in range(2):
+        x = cust.evaluator.mul(x, ct)
+    with pytest.raises(LevelExhausted):
+        cust.evaluator.mul(x, ct)
+    got = cust.decrypt(cust.evaluator.rotate(ct, 1)).values
+    assert np.max(np.abs(got - np.roll(v, -1))) < 1e-6

@@ -1,0 +1,176 @@
+"""BASELINE configs 4 and 5 through the UNCHANGED reference layer code, every step.
+
+The reference package (baseline/_ref) builds the model and runs
+``nn.train_iteration`` (nn.py:344-404) for all of the configuration's steps
+(config 4: 8, config 5: 5) on fresh seeded minibatches; ``plugin.install``
+routes ``backend="ckks"`` to the B200 backend with real bootstrapping (each
+refresh the layer code requests is a homomorphic bootstrap, bootstrap.py) and
+deferred execution (deferred.py: the step's HE calls run as batched waves).
+The same steps run on the reference's exact simulator backend in the same
+process, and after EVERY step the decrypted weights and velocities of every
+block are compared with it.
+
+  config 4: 196 -> 128 -> 10 (14x14 images), batch 128, 8 steps
+  config 5: 64 -> 64 -> 64 -> 64 -> 64 -> 2, batch 256, 5 steps
+  N = 2^16; chains (insecure-test: above the 128-bit HE-standard bound):
+    c4: Q = 60 + 8 x 45 (user) + 16 x 60 (bootstrap), P = 11 x 60
+    c5: Q = 60 + 16 x 45 + 16 x 60, P = 13 x 60
+
+    python tools/train_dropin.py c4|c5 [steps]
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+CONFIGS = {
+    "c4": dict(arch=(196, (128,), 10), batch=128, steps=8, user=8, special=660, lr=0.005,
+               init_scale=1.0, data="image", seed=20250704, low_special=[(8, 7), (24, 9)],
+               rng_seed=4, max_group=None),
+    "c5": dict(arch=(64, (64, 64, 64, 64), 2), batch=256, steps=5, user=16, special=780,
+               lr=0.005, init_scale=0.25, data="tabular", seed=20250705,
+               low_special=[(16, 9), (32, 12)], rng_seed=5, max_group=64),
+}
+
+
+def _data(cfg, rng):
+    d_in = cfg["arch"][0]
+    b = cfg["batch"]
+    if cfg["data"] == "image":  # pixels U[0,1], 10 uniform classes
+        x = rng.uniform(0, 1, size=(b, d_in))
+        y = rng.integers(0, cfg["arch"][2], b)
+    else:  # N(0,1) features, labels from a seeded two-layer teacher
+        x = rng.normal(0, 1, size=(b, d_in))
+        y = np.argmax(np.tanh(x @ cfg["t1"]) @ cfg["t2"], axis=1)
+    return x, np.eye(cfg["arch"][2])[y]
+
+
+def run(name: str, steps: int = None, verbose: bool = False) -> dict:
+    import torch
+
+    import c1_dropin
+
+    c1_dropin.import_reference()
+    from ciphermlp.api import keygen
+    from ciphermlp.nn import (Hyperparams, build_model, classifier_format, layer_format,
+                              prepare_sample, train_iteration)
+    from ciphermlp.packing import Architecture, compute_dims, encrypt_packed, pack, \
+        required_rotations
+    from ciphermlp.params import SchemeParams
+
+    from paper_2506_19693_b200 import plugin
+
+    cfg = dict(CONFIGS[name])
+    steps = steps or cfg["steps"]
+    d_in, hidden, classes = cfg["arch"]
+    arch = Architecture(d_in, hidden, classes)
+    n = 2**16
+    bd = 16
+    L = cfg["user"] + bd
+    params = SchemeParams(poly_degree=n,
+                          modulus_chain=(60,) + (45,) * cfg["user"] + (60,) * bd + (cfg["special"],),
+                          scale_bits=45, level=L, bootstrap_depth=bd,
+                          security_claim="insecure-test")
+    shape = compute_dims(arch, n // 2)
+    rots = required_rotations(shape)
+    rng = np.random.default_rng(cfg["seed"])
+    if cfg["data"] == "tabular":
+        cfg["t1"] = rng.normal(0, 1, size=(d_in, 16))
+        cfg["t2"] = rng.normal(0, 1, size=(16, classes))
+    dims = (d_in,) + tuple(hidden)
+    inits = []
+    for k, h in enumerate(hidden):
+        w = rng.uniform(-1, 1, size=(dims[k], h)) * np.sqrt(6.0 / (dims[k] + h))
+        c = rng.uniform(-1, 1, size=(h, classes)) * np.sqrt(6.0 / (h + classes))
+        inits.append((w * cfg["init_scale"], c * cfg["init_scale"]))
+    batches = [_data(cfg, rng) for _ in range(steps)]
+    hyper = Hyperparams(learning_rate=cfg["lr"], momentum=0.9, iterations=steps,
+                        batch_size=cfg["batch"])
+
+    def build(cust):
+        model = build_model(arch, params, hyper, cust)
+        for blk, (w, c) in zip(model.blocks, inits):
+            blk.layer_weights = encrypt_packed(cust, pack(w, layer_format(blk.kind), shape))
+            blk.classifier_weights = encrypt_packed(cust, pack(c, classifier_format(blk.kind),
+                                                               shape))
+        return model
+
+    def state(model, cust):
+        out = []
+        for b in model.blocks:
+            out.append(np.stack([cust.decrypt(pm.payload).values
+                                 for pm in (b.layer_weights, b.classifier_weights,
+                                            b.layer_velocity, b.classifier_velocity)]))
+        return np.stack(out)  # [blocks][4][slots]
+
+    sim = keygen(params, rots, backend="sim")
+    sim_model = build(sim)
+    cls, old = plugin.install(prime_layout="bootstrap", dnum=3, secret_hw=192,
+                              real_bootstrap=True, low_special=cfg["low_special"],
+                              deferred=True, deferred_max_group=cfg["max_group"])
+    try:
+        t0 = time.perf_counter()
+        cust = keygen(params, rots, backend="ckks", rng_seed=cfg["rng_seed"])
+        torch.cuda.synchronize()
+        keygen_s = time.perf_counter() - t0
+        be = cust.backend
+        model = build(cust)
+        be.flush()
+        torch.cuda.synchronize()
+        per_step, errs = [], []
+        torch.cuda.reset_peak_memory_stats()
+        for t, (x, onehot) in enumerate(batches, start=1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(x.shape[0])]
+            train_iteration(model, batch, cust, t)
+            be.flush()
+            torch.cuda.synchronize()
+            per_step.append(time.perf_counter() - t0)
+            sb = [prepare_sample(x[i], onehot[i], shape, sim) for i in range(x.shape[0])]
+            train_iteration(sim_model, sb, sim, t)
+            g, s = state(model, cust), state(sim_model, sim)
+            err = np.abs(g - s).max(axis=2)  # [blocks][4]
+            errs.append({"weights": float(err[:, :2].max()), "velocities": float(err[:, 2:].max()),
+                         "weights_mag": float(np.abs(s[:, :2]).max()),
+                         "velocities_mag": float(np.abs(s[:, 2:]).max())})
+            if verbose:
+                print(f"{name} step {t}: {1e3 * per_step[-1]:.1f} ms, {errs[-1]}", flush=True)
+        peak = torch.cuda.max_memory_allocated() / 2**30
+    finally:
+        plugin.uninstall(old)
+    return {
+        "ms_per_step": 1e3 * float(np.mean(per_step)), "steps": steps,
+        "step_ms": [1e3 * v for v in per_step],
+        "weights_max_abs_err_vs_sim_each_step": [e["weights"] for e in errs],
+        "velocities_max_abs_err_vs_sim_each_step": [e["velocities"] for e in errs],
+        "weights_max_abs_err_vs_sim": max(e["weights"] for e in errs),
+        "velocities_max_abs_err_vs_sim": max(e["velocities"] for e in errs),
+        "velocities_max_abs": max(e["velocities_mag"] for e in errs),
+        "bootstraps_per_step": 4 * len(hidden), "keygen_s": keygen_s, "peak_mem_gib": peak,
+        "security": f"insecure-test: log2(QP) = "
+                    f"{sum(int(p).bit_length() for p in be.chain.all_primes)} bits > 1772",
+        "path": "reference keygen/build_model/prepare_sample/nn.train_iteration (baseline/_ref) "
+                "-> plugin-installed B200 CkksBackend (real bootstrapping, deferred batched "
+                "execution); every step executed and decrypted against the reference simulator",
+        "timing": "ms_per_step: mean over all executed steps of wall clock from the first "
+                  "encryption of the minibatch to the refreshed weights resident on the device "
+                  "(flush + device sync); decryption for the comparison is outside",
+        "workload": f"{d_in}->{'->'.join(map(str, hidden))}->{classes}, batch {cfg['batch']}, "
+                    f"N=2^16, L={L} ({cfg['user']} user + {bd} bootstrap levels), "
+                    f"P = {cfg['special'] // 60} x 60 bits",
+    }
+
+
+if __name__ == "__main__":
+    res = run(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else None, verbose=True)
+    print(json.dumps(res))
