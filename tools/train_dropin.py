@@ -33,7 +33,10 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 CONFIGS = {
-    "c4": dict(arch=(196, (128,), 10), batch=128, steps=8, user=8, special=660, lr=0.005,
+    # lr 0.0005 with plain Xavier init: the exact model stays bounded over all 8
+    # steps (lr 0.005 diverges at step 4 even without encryption: weights 2e2,
+    # velocities 3e6 — a property of the z^2+z network, not of CKKS)
+    "c4": dict(arch=(196, (128,), 10), batch=128, steps=8, user=8, special=660, lr=0.0005,
                init_scale=1.0, data="image", seed=20250704, low_special=[(8, 7), (24, 9)],
                rng_seed=4, max_group=None),
     "c5": dict(arch=(64, (64, 64, 64, 64), 2), batch=256, steps=5, user=16, special=780,
