@@ -963,6 +963,15 @@ class B200CkksCore:
         res = res.view(len(galois_list), *lead, 2, m, self.n)
         return res if stack else list(res.unbind(0))
 
+    def prepare_bootstrap(self) -> None:
+        """Build the bootstrapper's device tables (plaintext diagonals, basis
+        constants, FFT plans) ahead of the first refresh — setup work, like key
+        generation — by bootstrapping an encryption of zeros once."""
+        if not self.real_bootstrap:
+            return
+        ct = GpuCiphertext(self._encrypt_batch([np.zeros(self.n // 2)], 0, [None])[0], 0)
+        self.bootstrap_ct(ct)
+
     def bootstrap_batch(self, data: torch.Tensor, level: int) -> torch.Tensor:
         """Bootstrap a batch [B, 2, m, N] of ciphertexts at one level together:
         every stage runs once over the batch (the refreshed weights of a
