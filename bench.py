@@ -332,6 +332,64 @@ def run_c1_dropin(cpu: bool = True) -> dict:
     return out
 
 
+def run_c4_dp(local: int, world: int, reps: int = 3) -> dict:
+    """Config 4's recorded step (tests/golden/c4_trace.npz: 128 samples, real
+    bootstrapping) sharded by sample across `world` ranks (dp.py): per-sample
+    pipelines on their owner, one exact residue all-reduce of the delta-W folds
+    (NCCL), the update and the 4 bootstraps replicated.  Strong scaling (the
+    batch of 128 is fixed); CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_19693_b200 import dist as hdist
+    from paper_2506_19693_b200 import he_api
+    from paper_2506_19693_b200.dp import DataParallelExecutor
+    from paper_2506_19693_b200.replay import Program
+    from paper_2506_19693_b200.scheme import SchemeParams
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import c4_run
+
+    path = os.path.join(ROOT, "tests", "golden", "c4_trace.npz")
+    z = np.load(path)
+    prog = Program.load(path)
+    n, L, sb, bd = (int(v) for v in z["params"])
+    params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                          scale_bits=45, level=L, bootstrap_depth=bd)
+    cust = he_api.keygen(params, [int(r) for r in z["rotations"]], backend="ckks", rng_seed=4,
+                         prime_layout="bootstrap", dnum=3, secret_hw=192, real_bootstrap=True,
+                         low_special=c4_run.LOW_SPECIAL)
+    cust.backend.prepare_bootstrap()
+    env = prog.run(cust, 0, prog.n_setup)
+    ex = DataParallelExecutor(prog, cust, encs_per_sample=3)
+    times = []
+    out = None
+    for rep in range(reps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cust.backend._enc_cache.clear()
+        a.record()
+        out = ex.run(dict(env), only_after_setup=True)
+        b.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rep:
+            times.append(hdist.max_over_ranks(a.elapsed_time(b)))
+    w = np.stack([cust.backend._decrypt_values(out[o]) for o in prog.outputs])
+    planes = np.concatenate([cust.backend.planes_of(out[o]).ravel() for o in prog.outputs])
+    digest = int(np.bitwise_xor.reduce(planes.view(np.int64)))
+    lo = hdist.reduce_scalar(digest, dist.ReduceOp.MIN, torch.int64)
+    hi = hdist.reduce_scalar(digest, dist.ReduceOp.MAX, torch.int64)
+    return {"ms_per_step": min(times), "ranks": world, "scaling": "strong",
+            "samples": ex.plan.n_samples,
+            "samples_per_rank": len(hdist.shard(ex.plan.n_samples, dist.get_rank(), world)),
+            "weights_identical_across_ranks": bool(lo == hi),
+            "weights_max_abs_err_vs_sim": float(np.max(np.abs(w[:2] - z["sim_weights"][:2]))),
+            "timing": "the recorded config-4 first step (4 real bootstraps), CUDA events around "
+                      "the sharded step, max over ranks, best of 3 after a warm-up"}
+
+
 def run_c1_dp(local: int, world: int) -> dict:
     """Config-1 step sharded by sample across `world` ranks (dp.py):
     each rank runs its share of the 32 per-sample pipelines, one exact residue
@@ -802,6 +860,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         backend = os.environ.get("CKB_DIST_BACKEND", "nccl")
+        # NCCL's own log (stderr) records the communicator's rank count and
+        # transport (NVLink / NVLS) for the driver's checks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -884,6 +945,14 @@ def main():
             res = {"error": repr(exc)}
         if rank == 0:
             line["c1_train_dp"] = res
+    if world > 1 and not args.no_c4:
+        try:
+            torch.cuda.empty_cache()
+            res = run_c4_dp(local, world)
+        except Exception as exc:
+            res = {"error": repr(exc)}
+        if rank == 0:
+            line["c4_train_dp"] = res
     if rank == 0 and world == 1 and not args.no_c3:
         try:
             line["c3_bootstrap"] = run_c3_bootstrap()

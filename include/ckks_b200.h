@@ -299,6 +299,20 @@ int ckb_sample(const ckb_ring* ring, uint64_t* a, int64_t* e, const uint64_t* se
 int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int polys, int limbs,
                  const int32_t* limb_prime, void* stream);
 
+/* Encoder (encoding.py:34-49 + make_element, ring.py:139-145), around the
+ * caller's forward FFT (cuFFT).  Step 1: spec ([batch][N] complex128,
+ * interleaved) gets values[b][i] * scale (0 for i >= width) at bins[i] and at
+ * bins[N/2 + i] (the conjugate bins); every entry is written.  Step 2: after
+ * spec = FFT(spec), coefficient j = rint(Re(spec[j] / N * conj(twist_j))) with
+ * twist ([N] complex128) = exp(i pi j / N), written as residues of every limb
+ * to out ([batch][limbs][N]); if maxabs (one device u64) is non-NULL it is
+ * raised to the bit pattern of max |coefficient| (the EncodingOverflow check). */
+int ckb_embed_scatter(double* spec, const double* values, int batch, int width,
+                      int64_t values_stride, double scale, const int32_t* bins, int log_n,
+                      void* stream);
+int ckb_embed_finish(const ckb_ring* ring, uint64_t* out, const double* spec, int batch,
+                     int limbs, const int32_t* limb_prime, const double* twist, uint64_t* maxabs,
+                     void* stream);
 /* Centered CRT lift to float64 (ring.py:192-208 + encoding.py:67-69 astype):
  * in: [polys][limbs][N] coefficient domain; out: [polys][N] double. */
 int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys, int limbs,

@@ -126,6 +126,35 @@ class DeviceEncoder:
         self.untwist_np = np.conj(twist)
         self.twist = torch.from_numpy(twist).to(device)
         self.untwist = torch.from_numpy(np.conj(twist)).to(device)
+        self.bins32 = torch.from_numpy(
+            np.concatenate([self.bins_np, self.conj_bins_np]).astype(np.int32)).to(device)
+
+    def embed_residues(self, values: np.ndarray, scale: float, chain, limbs: int,
+                       need_max: bool = False):
+        """[B, <= N/2] real slot rows -> residues [B, limbs, N] of their encodings
+        (encoding.py:34-49 + ring.py:139-145): ckb_embed_scatter, cuFFT,
+        ckb_embed_finish (twist, rint and every limb's residue in one pass).
+        need_max: also the exact max |coefficient| (a device scalar) for the
+        overflow checks the host-side bound could not clear."""
+        from . import _native as nat
+
+        vals = np.ascontiguousarray(np.atleast_2d(np.asarray(values, dtype=np.float64)))
+        b, w = vals.shape
+        n = self.n
+        v = _h2d(vals, self.device) if w else torch.zeros(b, 1, dtype=torch.float64,
+                                                          device=self.device)
+        spec = torch.empty(b, n, dtype=torch.complex128, device=self.device)
+        nat.check(nat.LIB.ckb_embed_scatter(nat.ptr(spec), nat.ptr(v), b, w, w, float(scale),
+                                            nat.ptr(self.bins32), n.bit_length() - 1,
+                                            nat.stream_handle()), "embed_scatter")
+        spec = torch.fft.fft(spec, dim=1)
+        res = torch.empty(b, limbs, n, dtype=torch.uint64, device=self.device)
+        mx = torch.zeros(1, dtype=torch.int64, device=self.device) if need_max else None
+        nat.check(nat.LIB.ckb_embed_finish(chain.ring_p, nat.ptr(res), nat.ptr(spec), b, limbs,
+                                           chain.q_map(limbs), nat.ptr(self.twist),
+                                           nat.ptr(mx) if mx is not None else None,
+                                           nat.stream_handle()), "embed_finish")
+        return res, mx
 
     def _embed_host(self, rows: np.ndarray, scale: float) -> torch.Tensor:
         """encoding.py:34-49 per row (numpy), -> rounded float64 on the device."""
@@ -561,8 +590,28 @@ class B200CkksCore:
         ch = self.chain
         m = self._limbs(level)
         sc = self._scale(level) if scale is None else scale
-        coeffs = self.encoder.embed_device(vals, sc)
         lim = self._encode_limit if limit is None else limit
+        if not self.encoder.host:  # one scatter + cuFFT + one finish kernel
+            hb = _coeff_bound(vals, sc, self.n)
+            fast = hb < lim and 4 * int(hb) < ch.modulus_at(level)
+            res, mx = self.encoder.embed_residues(vals, sc, ch, m, need_max=not fast)
+            res = res[0]
+            if not fast:
+                bound = float(mx.view(torch.float64).item())
+                if bound >= lim:
+                    raise self._errors.EncodingOverflow(
+                        "scaled values exceed the exactly-representable coefficient range")
+                if 4 * int(bound) >= ch.modulus_at(level):
+                    raise self._errors.EncodingOverflow(
+                        f"encoded coefficients (~2^{np.log2(bound + 1):.1f}) do not fit the "
+                        f"current modulus with headroom")
+            if ntt:
+                ch.ntt_fwd(res, m)
+            self._enc_cache[key] = res
+            if len(self._enc_cache) > self._enc_cache_cap:
+                self._enc_cache.popitem(last=False)
+            return res
+        coeffs = self.encoder.embed_device(vals, sc)
         # Every coefficient is (1/N) x a sum over the N spectrum entries (each
         # slot twice), so |c_j| <= scale * 2 sum|v| / N <= scale * max|v| (+ 1/2
         # from rounding): when that host-side bound already clears both checks,
@@ -632,8 +681,10 @@ class B200CkksCore:
             mat = np.zeros((len(rows), width))
             for i, r in enumerate(rows):
                 mat[i, : r.shape[0]] = r
-            coeffs = self.encoder.embed_device_batch(mat, sc)
-            res = ch.from_i64(coeffs.to(torch.int64), m)  # [B, m, N]
+            if self.encoder.host:
+                res = ch.from_i64(self.encoder.embed_device_batch(mat, sc).to(torch.int64), m)
+            else:
+                res, _ = self.encoder.embed_residues(mat, sc, ch, m)  # [B, m, N]
             if ntt:
                 ch.ntt_fwd(res, m)
             for i, key in enumerate(keys):

@@ -1336,6 +1336,59 @@ __global__ void k_from_i64(uint64_t* __restrict__ out, const int64_t* __restrict
   }
 }
 
+// Encoder (encoding.py:34-49): slot scatter into the conjugate-symmetric
+// spectrum, then — after the forward FFT (cuFFT) — the twist, rounding and the
+// residues of every limb in one pass.  bins / conj_bins cover all N indices
+// exactly once (the odd residues mod 2N are +-5^i), so the scatter writes every
+// spectrum entry: no zero fill.
+__global__ void k_embed_scatter(double2* __restrict__ spec, const double* __restrict__ values,
+                                int batch, int width, size_t vstride, double scale,
+                                const int32_t* __restrict__ bins, int log_n) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t half = N >> 1;
+  const size_t total = (size_t)batch * half;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = t / half, i = t % half;
+    const double v = (int)i < width ? values[b * vstride + i] * scale : 0.0;
+    double2* row = spec + b * N;
+    row[__ldg(bins + i)] = make_double2(v, 0.0);
+    row[__ldg(bins + half + i)] = make_double2(v, 0.0);
+  }
+}
+
+__device__ __forceinline__ uint64_t i64_residue(int64_t v, const Mod& m) {
+  if (v >= 0) return ckb::reduce64((uint64_t)v, m);
+  const uint64_t mag = ckb::reduce64((uint64_t)(-(v + 1)) + 1, m);
+  return mag == 0 ? 0 : m.p - mag;
+}
+
+__global__ void k_embed_finish(uint64_t* __restrict__ out, const double2* __restrict__ spec,
+                               int batch, int limbs, int log_n, const double2* __restrict__ twist,
+                               unsigned long long* __restrict__ maxabs, RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  const double inv_n = 1.0 / (double)N;
+  const size_t total = (size_t)batch * N;
+  double local = 0.0;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = t >> log_n, j = t & (N - 1);
+    const double2 w = spec[t];
+    const double2 tw = __ldg(twist + j);  // {cos(pi j / N), sin(pi j / N)}
+    // Re((w / N) * conj(psi^j))
+    const double c = rint(w.x * inv_n * tw.x + w.y * inv_n * tw.y);
+    local = fmax(local, fabs(c));
+    const int64_t v = (int64_t)c;  // |c| < 2^62 whenever the caller's bound check passes
+    uint64_t* o = out + (b * limbs) * N + j;
+    for (int l = 0; l < limbs; ++l) o[(size_t)l * N] = i64_residue(v, load_mod(R, lm.p[l]));
+  }
+  if (maxabs) {  // non-negative doubles order like their bit patterns
+    for (int off = 16; off; off >>= 1) local = fmax(local, __shfl_xor_sync(0xffffffffu, local, off));
+    if ((threadIdx.x & 31) == 0)
+      atomicMax(maxabs, (unsigned long long)__double_as_longlong(local));
+  }
+}
+
 // Garner mixed-radix digits, centered by comparing x/Q with 1/2, then the
 // value is rebuilt exactly modulo 2^64 when it fits in 63 bits (the case for
 // every decryptable phase) and approximately otherwise.
@@ -1831,6 +1884,35 @@ int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int pol
   if (!total) return 0;
   k_from_i64<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, in, total, (int)R.log_n,
                                                                       limbs, R, lm);
+  return finish();
+}
+
+int ckb_embed_scatter(double* spec, const double* values, int batch, int width,
+                      int64_t values_stride, double scale, const int32_t* bins, int log_n,
+                      void* stream) {
+  if (batch < 0 || width < 0 || width > (1 << (log_n - 1)) || log_n < 1 || log_n > 20 ||
+      !spec || !bins || (width && !values))
+    return CKB_E_ARG;
+  const size_t total = (size_t)batch << (log_n - 1);
+  if (!total) return 0;
+  k_embed_scatter<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<double2*>(spec), values, batch, width,
+      values_stride > 0 ? (size_t)values_stride : (size_t)width, scale, bins, log_n);
+  return finish();
+}
+
+int ckb_embed_finish(const ckb_ring* ring, uint64_t* out, const double* spec, int batch,
+                     int limbs, const int32_t* limb_prime, const double* twist, uint64_t* maxabs,
+                     void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || batch < 0 || !out || !spec || !twist) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  const size_t total = (size_t)batch << R.log_n;
+  if (!total) return 0;
+  k_embed_finish<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, reinterpret_cast<const double2*>(spec), batch, limbs, (int)R.log_n,
+      reinterpret_cast<const double2*>(twist), reinterpret_cast<unsigned long long*>(maxabs), R,
+      lm);
   return finish();
 }
 
