@@ -509,6 +509,41 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   // tools/ab_ntt.sh): forward -3%; a first phase streaming from DRAM is 9%
   // faster with the 16-byte tile loads, so it keeps them.
   const bool direct = f64 && warp_local && !ph.first;
+#ifndef CKB_NO_COMBINE_PREFETCH
+  // Fused ModDown combine: the x and addend tiles this thread combines in the
+  // epilogue are copied into shared memory asynchronously (cp.async, no
+  // registers held) while the rounds run, so the epilogue reads them without
+  // exposing DRAM latency.  Each thread fetches exactly its own pairs: a
+  // cp.async.wait_all before the epilogue is the only synchronisation.
+  uint64_t* pf = smem + (size_t)C * (G + G / 16 + G / 128);
+  const bool prefetch = FWD && ep.out && ph.last && rows_contig;
+  const uint64_t* pf_add = nullptr;
+  if (prefetch) {
+    const int m2 = ph.limbs;
+    const int j = row % m2;
+    const size_t pidx = row / m2;
+    const uint64_t* xr = ep.x + pidx * ep.xs + (size_t)j * N;
+    if (ep.add) {
+      const size_t phs = pidx % ep.add_period;
+      if ((int)phs < ep.add_polys)
+        pf_add = ep.add + ((pidx / ep.add_period) * ep.add_stride + phs) * ep.m1 * N +
+                 (size_t)j * N;
+    }
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      int g, r;
+      const size_t off = pair_of(i, g, r);
+      const unsigned sx = (unsigned)__cvta_generic_to_shared(pf + 2 * ((size_t)i * T + tid));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sx), "l"(xr + off));
+      if (pf_add) {
+        const unsigned sa =
+            (unsigned)__cvta_generic_to_shared(pf + 2 * ((size_t)(E / 2 + i) * T + tid));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(pf_add + off));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+#endif
   // FP64-only kernel, column phase: lanes span the tile's C columns
   // (gq = tid % C, w = tid / C) so both the first round's loads and the last
   // round's stores go straight to global memory (each warp instruction
@@ -607,18 +642,32 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
     }
     const uint64_t* pr = ep.post ? ep.post + pidx * ep.post_stride + (size_t)j * N : nullptr;
     uint64_t* orow = ep.out + (size_t)row * N;
+#ifndef CKB_NO_COMBINE_PREFETCH
+    if (prefetch) asm volatile("cp.async.wait_all;\n" ::: "memory");
+#endif
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       int g, r;
       const size_t off = pair_of(i, g, r);
       const uint64_t e0 = smem[sidx<S>(g, r)], e1 = smem[sidx<S>(g, r + 1)];
+#ifndef CKB_NO_COMBINE_PREFETCH
+      ulonglong2 v = prefetch ? *reinterpret_cast<const ulonglong2*>(pf + 2 * ((size_t)i * T + tid))
+                              : *reinterpret_cast<const ulonglong2*>(xr + off);
+#else
       ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + off);
+#endif
       if (ep.n1) {
         v.x = ckb::mul_shoup(v.x, a1, a1s, p);
         v.y = ckb::mul_shoup(v.y, a1, a1s, p);
       }
       if (ar) {
+#ifndef CKB_NO_COMBINE_PREFETCH
+        const ulonglong2 a =
+            prefetch ? *reinterpret_cast<const ulonglong2*>(pf + 2 * ((size_t)(E / 2 + i) * T + tid))
+                     : *reinterpret_cast<const ulonglong2*>(ar + off);
+#else
         const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(ar + off);
+#endif
         v.x = ckb::add_mod(v.x, a.x, p);
         v.y = ckb::add_mod(v.y, a.y, p);
       }
@@ -654,12 +703,19 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   const int G = 1 << S;
   const int RB = S < RBT ? S : RBT;
   const int threads = ph.C * G >> RB;
-  const size_t smem = (size_t)ph.C * (G + G / 16 + G / 128) * sizeof(uint64_t);
+  size_t smem = (size_t)ph.C * (G + G / 16 + G / 128) * sizeof(uint64_t);
+#ifndef CKB_NO_COMBINE_PREFETCH
+  if (FWD && ep.out && ph.last && ph.rstride == 1)  // prefetched x and addend tiles
+    smem += 2 * (size_t)ph.C * G * sizeof(uint64_t);
+#endif
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
   if (threads > kNttThreads) return CKB_E_LOGN;
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
+    if (smem > 48 * 1024)                                                          \
+      cudaFuncSetAttribute(k_ntt_phase<SS, FWD, RBT, MODE>,                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, ph, R, lm, ep); \
     break;
   switch (S) {
