@@ -38,14 +38,23 @@ def rb():
 
 
 A, B = rb(), rb()
+if os.environ.get("CKB_CHUNK_MB"):  # L2 budget of the sequential transforms
+    be.chain.set_ntt_chunk_bytes(int(os.environ["CKB_CHUNK_MB"]) << 20)
+X = torch.empty_like(A)
 for _ in range(2):
     be.batch_hmult(A, B, lvl)
     be.batch_hrot(A, steps, lvl)
 torch.cuda.synchronize()
 reps = 5
 res = {}
+def ntt_stage():
+    X.copy_(A)
+    be.batch_ntt(X, lvl)
+    be.batch_ntt(X, lvl, inverse=True)
+
+
 for name, fn in (("hmult", lambda: be.batch_hmult(A, B, lvl)),
-                 ("hrot", lambda: be.batch_hrot(A, steps, lvl))):
+                 ("hrot", lambda: be.batch_hrot(A, steps, lvl)), ("ntt_stage", ntt_stage)):
     t = ring.KernelTimer()
     ring.TIMER = t
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -77,6 +86,8 @@ e1.record()
 torch.cuda.synchronize()
 res["pair_ms"] = round(e0.elapsed_time(e1) / reps, 3)
 tag = (os.environ.get("CKB_LIB") or "x/default/x").split("/")[-2]
+if os.environ.get("CKB_CHUNK_MB"):
+    tag += f"+chunk{os.environ['CKB_CHUNK_MB']}"
 if os.environ.get("CKB_FUSE_KS") == "1":
     tag += "+fused"
 print(tag, json.dumps(res))
