@@ -57,7 +57,7 @@ def _data(cfg, rng):
     return x, np.eye(cfg["arch"][2])[y]
 
 
-def run(name: str, steps: int = None, verbose: bool = False) -> dict:
+def run(name: str, steps: int = None, verbose: bool = False, profile_step: int = 0) -> dict:
     import torch
 
     import c1_dropin
@@ -130,30 +130,57 @@ def run(name: str, steps: int = None, verbose: bool = False) -> dict:
         model = build(cust)
         be.flush()
         torch.cuda.synchronize()
-        per_step, errs = [], []
+        per_step, errs, snaps = [], [], []
         torch.cuda.reset_peak_memory_stats()
+        # The steps run back to back, as a training loop does: each step's
+        # flush only issues its batched waves, so the layer code records step
+        # t+1 while the GPU still executes step t.  Device sync at both ends of
+        # the whole run; CUDA events at the step boundaries give per-step times.
+        marks = [torch.cuda.Event(enable_timing=True)]
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        marks[0].record()
         for t, (x, onehot) in enumerate(batches, start=1):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
+            prof = None
+            if t == profile_step:  # host-side cProfile of one step (tools/c4_hostprof.py)
+                import cProfile
+
+                prof = cProfile.Profile()
+                prof.enable()
             batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(x.shape[0])]
             train_iteration(model, batch, cust, t)
             be.flush()
-            torch.cuda.synchronize()
-            per_step.append(time.perf_counter() - t0)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
+            if prof is not None:
+                import pstats
+
+                prof.disable()
+                pstats.Stats(prof).sort_stats("tottime").print_stats(30)
+                pstats.Stats(prof).sort_stats("cumulative").print_stats(40)
+            snaps.append([(b.layer_weights, b.classifier_weights, b.layer_velocity,
+                           b.classifier_velocity) for b in model.blocks])
+        torch.cuda.synchronize()
+        total_s = time.perf_counter() - t_start
+        per_step = [marks[k].elapsed_time(marks[k + 1]) / 1e3 for k in range(steps)]
+        for t, (x, onehot) in enumerate(batches, start=1):  # the exact model, then compare
             sb = [prepare_sample(x[i], onehot[i], shape, sim) for i in range(x.shape[0])]
             train_iteration(sim_model, sb, sim, t)
-            g, s = state(model, cust), state(sim_model, sim)
+            g = np.stack([np.stack([cust.decrypt(pm.payload).values for pm in blk])
+                          for blk in snaps[t - 1]])
+            s = state(sim_model, sim)
             err = np.abs(g - s).max(axis=2)  # [blocks][4]
             errs.append({"weights": float(err[:, :2].max()), "velocities": float(err[:, 2:].max()),
                          "weights_mag": float(np.abs(s[:, :2]).max()),
                          "velocities_mag": float(np.abs(s[:, 2:]).max())})
             if verbose:
-                print(f"{name} step {t}: {1e3 * per_step[-1]:.1f} ms, {errs[-1]}", flush=True)
+                print(f"{name} step {t}: {1e3 * per_step[t - 1]:.1f} ms, {errs[-1]}", flush=True)
         peak = torch.cuda.max_memory_allocated() / 2**30
     finally:
         plugin.uninstall(old)
     return {
-        "ms_per_step": 1e3 * float(np.mean(per_step)), "steps": steps,
+        "ms_per_step": 1e3 * total_s / steps, "steps": steps,
         "step_ms": [1e3 * v for v in per_step],
         "weights_max_abs_err_vs_sim_each_step": [e["weights"] for e in errs],
         "velocities_max_abs_err_vs_sim_each_step": [e["velocities"] for e in errs],
@@ -167,9 +194,11 @@ def run(name: str, steps: int = None, verbose: bool = False) -> dict:
         "path": "reference keygen/build_model/prepare_sample/nn.train_iteration (baseline/_ref) "
                 "-> plugin-installed B200 CkksBackend (real bootstrapping, deferred batched "
                 "execution); every step executed and decrypted against the reference simulator",
-        "timing": "ms_per_step: mean over all executed steps of wall clock from the first "
-                  "encryption of the minibatch to the refreshed weights resident on the device "
-                  "(flush + device sync); decryption for the comparison is outside",
+        "timing": "ms_per_step: wall clock of all steps run back to back (the first "
+                  "minibatch encryption to the last refreshed weights on the device, device "
+                  "sync at both ends) / steps; step_ms: CUDA events at the step boundaries; "
+                  "every step's weights are kept and decrypted against the simulator after "
+                  "the timed run",
         "workload": f"{d_in}->{'->'.join(map(str, hidden))}->{classes}, batch {cfg['batch']}, "
                     f"N=2^16, L={L} ({cfg['user']} user + {bd} bootstrap levels), "
                     f"P = {cfg['special'] // 60} x 60 bits",
