@@ -586,6 +586,80 @@ __global__ void __launch_bounds__(256) k_ks_inner(
 }
 
 // Runtime digit count (alpha = 1 chains with many digits).
+// One key for the whole batch (relinearisation, a single rotation step): each
+// thread owns one (ext limb, coefficient pair), loads that pair of every key
+// row ONCE into registers and walks the batch, so the key is read from memory
+// once per batch instead of once per item (the per-item form re-read the
+// 90 MB relinearisation key from L2 for each of the 64 items of config 2).
+template <int ND>
+__global__ void __launch_bounds__(256) k_ks_inner_shared(
+    uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int ext,
+    int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
+    size_t own_bstride, int log_n, const uint64_t* __restrict__ key, int key_limbs, RingDev R,
+    LimbMap em, LimbMap km, LimbMap od) {
+  const size_t N = (size_t)1 << log_n;
+  const int lh = log_n - 1;
+  const size_t total = (size_t)ext << lh;
+  const size_t krow = 2 * (size_t)key_limbs * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t n = (t & ((N >> 1) - 1)) * 2;
+    const int e = (int)(t >> lh);
+    const uint64_t* kb = key + (size_t)km.p[e] * N + n;
+    const uint64_t* ka = kb + (size_t)key_limbs * N;
+    ulonglong2 b[ND], a[ND];
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      b[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + j * krow));
+      a[j] = __ldg(reinterpret_cast<const ulonglong2*>(ka + j * krow));
+    }
+    const int owner = own ? od.p[e] : -1;
+    size_t rowoff[ND];
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const int cj = min(alpha, limbs - j * alpha);
+      const int row = own ? e - (e >= j * alpha + cj ? cj : 0) : e;
+      rowoff[j] = ((size_t)j * out_rows + row) * N + n;
+    }
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    for (int bi = 0; bi < batch; ++bi) {
+      const uint64_t* dbase = dig + (size_t)bi * item_rows * N;
+      ulonglong2 x[ND];
+#pragma unroll
+      for (int j = 0; j < ND; ++j) {
+        const uint64_t* xp = (j == owner) ? own + bi * own_bstride + (size_t)e * N + n
+                                          : dbase + rowoff[j];
+        x[j] = __ldcs(reinterpret_cast<const ulonglong2*>(xp));
+      }
+      uint64_t hb0 = 0, lb0 = 0, ha0 = 0, la0 = 0, hb1 = 0, lb1 = 0, ha1 = 0, la1 = 0;
+#pragma unroll
+      for (int j = 0; j < ND; ++j) {
+        ckb::mac128(hb0, lb0, x[j].x, b[j].x);
+        ckb::mac128(ha0, la0, x[j].x, a[j].x);
+        ckb::mac128(hb1, lb1, x[j].y, b[j].y);
+        ckb::mac128(ha1, la1, x[j].y, a[j].y);
+      }
+      ulonglong2 ob, oa;
+      if (m.k >= 32) {
+        ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
+                             ckb::reduce128_big(hb1, lb1, r64, r64s, m));
+        oa = make_ulonglong2(ckb::reduce128_big(ha0, la0, r64, r64s, m),
+                             ckb::reduce128_big(ha1, la1, r64, r64s, m));
+      } else {
+        ob = make_ulonglong2(ckb::reduce128_any(hb0, lb0, r64, r64s, m),
+                             ckb::reduce128_any(hb1, lb1, r64, r64s, m));
+        oa = make_ulonglong2(ckb::reduce128_any(ha0, la0, r64, r64s, m),
+                             ckb::reduce128_any(ha1, la1, r64, r64s, m));
+      }
+      uint64_t* o = acc + ((size_t)bi * 2 * ext + e) * N + n;
+      __stcs(reinterpret_cast<ulonglong2*>(o), ob);
+      __stcs(reinterpret_cast<ulonglong2*>(o + (size_t)ext * N), oa);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_ks_inner_any(
     uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int nd, int ext,
     int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
@@ -1781,6 +1855,24 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
   const size_t ob = own_batch_stride > 0 ? (size_t)own_batch_stride : ((size_t)limbs << R.log_n);
   const int grid = grid_for(total / 2, 256);
   cudaStream_t st = (cudaStream_t)stream;
+#ifndef CKB_KS_PER_ITEM
+  if (key && !key_ptrs && batch > 1 && n_digits <= 4) {  // one key: read it once per batch
+    const size_t pairs = (size_t)ext_limbs << (R.log_n - 1);
+    const int g = (int)std::min<size_t>((pairs + 255) / 256, 148 * 8);
+#define CKB_KSS(ND)                                                                         \
+  k_ks_inner_shared<ND><<<g, 256, 0, st>>>(acc, digits, batch, ext_limbs, out_rows,         \
+                                           item_rows, alpha, limbs, own, ob, (int)R.log_n,  \
+                                           key, key_limbs, R, em, km, od)
+    switch (n_digits) {
+      case 1: CKB_KSS(1); break;
+      case 2: CKB_KSS(2); break;
+      case 3: CKB_KSS(3); break;
+      default: CKB_KSS(4); break;
+    }
+#undef CKB_KSS
+    return finish();
+  }
+#endif
 #define CKB_KS(ND)                                                                           \
   k_ks_inner<ND><<<grid, 256, 0, st>>>(acc, digits, batch, n_digits, ext_limbs, out_rows,   \
                                        item_rows, alpha, limbs, own, ob, (int)R.log_n, key, \
