@@ -102,6 +102,8 @@ class DataParallelExecutor(WaveExecutor):
     """WaveExecutor over this rank's share of the program.  `allreduce(x, limbs)`
     defaults to dist.allreduce_residues on the current process group."""
 
+    rewrite_sums = False  # the fold's add_ct joins are the sharding's exchange points
+
     def __init__(self, program, custodian, encs_per_sample: int, rank: int = None,
                  world: int = None, allreduce=None):
         super().__init__(program, custodian)

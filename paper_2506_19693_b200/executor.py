@@ -57,15 +57,22 @@ class WaveExecutor:
         top = be.params.level
         rl = be.params.refresh_level
         self.n_setup = self.prog.n_setup
+        self._plan_fusion()
+        self._plan_sums()
+
         for i, op in enumerate(ops):
             tag = op[0]
+            if i in self.absorbed:  # inner add of a summation tree (_plan_sums)
+                counter += 1
+                level[op[2]] = min(level[op[3]], level[op[4]])  # bookkeeping only
+                continue
             if tag == "enc":
                 ser[i] = counter + 1          # api.py:225 then backend.py:174
                 counter += 2
                 out, ins, lvl = op[1], [], top
             elif tag == "ew":
                 kind, out, a, b = op[1], op[2], op[3], op[4]
-                ins = [a] + ([b] if kind.endswith("_ct") else [])
+                ins = self.sums.get(i) or ([a] + ([b] if kind.endswith("_ct") else []))
                 lvl = min(level[x] for x in ins)
                 if kind.startswith("mul"):
                     lvl -= 1
@@ -107,7 +114,75 @@ class WaveExecutor:
         self.level_of = level
         self.waves = [waves[d] for d in sorted(waves)]
         self.serials_used = counter
-        self._plan_fusion()
+        last = {}
+        for i, op in enumerate(ops):
+            if i in self.absorbed:
+                continue
+            for ref in self.sums.get(i) or _inputs(op):
+                last[ref] = i
+        self.last_use = last
+
+    rewrite_sums = True  # the data-parallel executor keeps the fold's joins
+
+    def _plan_sums(self):
+        """Summation trees: a chain of add_ct ops whose intermediate sums have
+        exactly one reader (the delta-W fold over the B samples, nn.py:373-381:
+        acc = acc + dW_s) becomes ONE n-ary sum at its last add, executed as a
+        log-depth tree of batched adds (modular addition is exact and
+        associative, so the value is unchanged) instead of B - 1 dependent
+        single-ciphertext waves.  Leaves must share one level (no adjusts)."""
+        ops = self.prog.ops
+        self.sums, self.absorbed = {}, set()
+        if not self.rewrite_sums:
+            return
+        keep = self.prog.keep
+        readers = collections.defaultdict(list)
+        producer = {}
+        for j, op in enumerate(ops):
+            for x in _inputs(op):
+                readers[x].append(j)
+            producer[_output(op)] = j
+
+        def is_add(j):
+            op = ops[j]
+            return (op[0] == "ew" and op[1] == "add_ct" and j >= self.n_setup
+                    and j not in self.fused_adds)
+
+        def internal(x, j):
+            i = producer.get(x)
+            return (i is not None and is_add(i) and x not in keep and readers.get(x) == [j])
+
+        # levels of every value (no rewrite) to check the leaves
+        level = dict(self.inputs)
+        top, rl = self.be.params.level, self.be.params.refresh_level
+        for op in ops:
+            tag = op[0]
+            if tag == "enc":
+                level[op[1]] = top
+            elif tag == "ew":
+                ins = [op[3]] + ([op[4]] if op[1].endswith("_ct") else [])
+                lv = min(level[x] for x in ins)
+                level[op[2]] = lv - 1 if op[1].startswith("mul") else lv
+            elif tag == "rot":
+                level[op[1]] = level[op[2]]
+            else:
+                level[op[1]] = rl
+        for j in range(len(ops)):
+            if not is_add(j) or any(internal(_output(ops[j]), r)
+                                    for r in readers.get(_output(ops[j]), [])):
+                continue  # not a root (its sum feeds the next add of a chain)
+            leaves, inner, stack = [], [], [j]
+            while stack:
+                k = stack.pop()
+                for x in (ops[k][3], ops[k][4]):
+                    if internal(x, k):
+                        inner.append(producer[x])
+                        stack.append(producer[x])
+                    else:
+                        leaves.append(x)
+            if len(leaves) >= 3 and len({level[x] for x in leaves}) == 1:
+                self.sums[j] = leaves
+                self.absorbed.update(inner)
 
     def _plan_fusion(self):
         """Rotate-and-accumulate pairs: rot i (o = rotate(s, k)) whose result's
@@ -147,7 +222,7 @@ class WaveExecutor:
         ops = self.prog.ops
         env = {} if env is None else {k: getattr(v, "payload", v) for k, v in env.items()}
         keep = self.prog.keep
-        last = self.prog._last_use
+        last = self.last_use
         slots = be.params.slot_count
         pts = self.prog.plaintexts
 
@@ -178,6 +253,10 @@ class WaveExecutor:
                 tag = op[0]
                 if i in self.fused_adds:
                     continue  # produced by its rotation (_plan_fusion)
+                if i in self.sums:  # n-ary summation tree (_plan_sums)
+                    leaves = self.sums[i]
+                    groups[("sum", env[leaves[0]].level, len(leaves))].append(i)
+                    continue
                 if tag == "enc":
                     groups[("enc",)].append(i)
                 elif tag == "ew":
@@ -198,7 +277,7 @@ class WaveExecutor:
                 for lo in range(0, len(idx), step):
                     self._run_group(key, idx[lo:lo + step], env, pvals)
             for i in wave:
-                for ref in _inputs(ops[i]):
+                for ref in self.sums.get(i) or _inputs(ops[i]):
                     if last.get(ref) == i and ref not in keep:
                         env.pop(ref, None)
         # leave the backend's serial counter where sequential execution would
@@ -215,7 +294,7 @@ class WaveExecutor:
         be = self.be
         ops = self.prog.ops
         keep = self.prog.keep
-        last = self.prog._last_use
+        last = self.last_use
         order = sorted(self.deferred)
         if not order:
             return env
@@ -303,6 +382,18 @@ class WaveExecutor:
             env[ops[i][1]] = GpuCiphertext(
                 be._encrypt_batch([values], rl, [self.serial_of[i] + self.serial_offset])[0], rl)
             return
+        if tag == "sum":  # log-depth tree of batched adds over every root's leaves
+            _, lvl, _k = key
+            m = be._limbs(lvl)
+            x = torch.stack([torch.stack([env[v].data for v in self.sums[i]]) for i in idx])
+            while x.shape[1] > 1:
+                k = x.shape[1]
+                h = k // 2
+                y = ch.add(x[:, :h].contiguous(), x[:, h:2 * h].contiguous(), m)
+                x = torch.cat([y, x[:, 2 * h:]], dim=1) if k % 2 else y
+            for j, i in enumerate(idx):
+                env[ops[i][2]] = GpuCiphertext(x[j, 0], lvl)
+            return
         if tag == "rot":
             _, lvl, step, fused = key
             x = self._stack([env[ops[i][2]].data for i in idx])
@@ -351,6 +442,10 @@ class WaveExecutor:
                 out_level = la
         for j, i in enumerate(idx):
             env[ops[i][2]] = GpuCiphertext(out[j], out_level)
+
+
+def _output(op):
+    return op[2] if op[0] == "ew" else op[1]
 
 
 def _inputs(op):
