@@ -346,6 +346,10 @@ class B200CkksCore:
         self._force_full_p = False
         self.relin_keys_k: dict = {}
         self.rotation_keys_k: dict = {}
+        if isinstance(low_special, str):
+            if low_special != "auto":
+                raise self._errors.InvalidParameters(f"unknown low_special {low_special!r}")
+            low_special = self._auto_tiers() or None
         if low_special is not None:
             if isinstance(low_special, numbers.Integral):
                 tiers = [(params.refresh_level, int(low_special))]
@@ -398,6 +402,35 @@ class B200CkksCore:
             self._rec.flush()
 
     # ------------------------------------------------------------------ keys
+    AUTO_TIER_MARGIN_BITS = 0  # the same rule __init__ checks explicit tiers with
+
+    def _auto_tiers(self) -> list:
+        """low_special="auto": per level the fewest special primes whose product
+        exceeds the widest digit at that level (times 2^AUTO_TIER_MARGIN_BITS;
+        the key-switch error is then ~ sigma * sqrt(N) * digits, far below the
+        ~2^45 scale), merged into tiers of consecutive levels; levels that need
+        the whole P keep it.  Every tier costs its own relinearisation and
+        rotation keys."""
+        ch = self.chain
+        need = []
+        for lv in range(self.params.level + 1):
+            m = ch.level_limbs[lv]
+            widest = max(math.prod(ch.all_primes[lo:min(lo + self.alpha, m)])
+                         for lo in range(0, m, self.alpha))
+            target = widest << self.AUTO_TIER_MARGIN_BITS
+            kk = next((k for k in range(1, ch.k + 1)
+                       if math.prod(ch.special_primes[:k]) > target), ch.k)
+            need.append(kk)
+        tiers = []
+        for lv, kk in enumerate(need):
+            if kk >= ch.k:
+                break  # levels above keep the full P
+            if tiers and tiers[-1][1] == kk:
+                tiers[-1] = (lv, kk)
+            else:
+                tiers.append((lv, kk))
+        return tiers
+
     def _to_ntt_all(self, coeffs: np.ndarray) -> torch.Tensor:
         ch = self.chain
         t = torch.as_tensor(np.asarray(coeffs, dtype=np.int64), device=self.device)

@@ -37,11 +37,18 @@ CONFIGS = {
     # steps (lr 0.005 diverges at step 4 even without encryption: weights 2e2,
     # velocities 3e6 — a property of the z^2+z network, not of CKKS)
     "c4": dict(arch=(196, (128,), 10), batch=128, steps=8, user=8, special=660, lr=0.0005,
-               init_scale=1.0, data="image", seed=20250704, low_special=[(8, 7), (24, 9)],
+               init_scale=1.0, data="image", seed=20250704,
+               # fewest special primes above the widest digit per level range
+               # (backend._auto_tiers' rule); the low user levels of the steady
+               # steps key-switch over 2..6 instead of 7 60-bit primes
+               low_special=[(1, 2), (2, 3), (4, 4), (5, 5), (6, 6), (8, 7), (24, 9)],
                rng_seed=4, max_group=None),
     "c5": dict(arch=(64, (64, 64, 64, 64), 2), batch=256, steps=5, user=16, special=780,
                lr=0.005, init_scale=0.25, data="tabular", seed=20250705,
-               low_special=[(16, 9), (32, 12)], rng_seed=5, max_group=64),
+               # coarser low tiers than config 4: each tier's keys cost ~3 GB
+               # next to the step's ~150 GB peak
+               low_special=[(2, 3), (5, 5), (8, 7), (16, 9), (32, 12)], rng_seed=5,
+               max_group=64),
 }
 
 
