@@ -64,7 +64,8 @@ def _data(cfg, rng):
     return x, np.eye(cfg["arch"][2])[y]
 
 
-def run(name: str, steps: int = None, verbose: bool = False, profile_step: int = 0) -> dict:
+def run(name: str, steps: int = None, verbose: bool = False, profile_step: int = 0,
+        kernels_step: int = 0) -> dict:
     import torch
 
     import c1_dropin
@@ -154,9 +155,20 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
 
                 prof = cProfile.Profile()
                 prof.enable()
+            if t == kernels_step:  # per-kernel CUDA-event breakdown of one step
+                from paper_2506_19693_b200 import ring as _ring
+
+                _ring.TIMER = _ring.KernelTimer()
             batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(x.shape[0])]
             train_iteration(model, batch, cust, t)
             be.flush()
+            if t == kernels_step:
+                summ = _ring.TIMER.summary()
+                _ring.TIMER = None
+                tot = sum(v["ms"] for v in summ.values())
+                for k_, v in sorted(summ.items(), key=lambda kv: -kv[1]["ms"]):
+                    print(f"  {k_:16s} {v['ms']:9.1f} ms {100 * v['ms'] / tot:5.1f}% "
+                          f"{v['calls']:6d} calls", flush=True)
             ev = torch.cuda.Event(enable_timing=True)
             ev.record()
             marks.append(ev)
