@@ -450,9 +450,13 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
   }
 }
 
+#ifndef CKB_NTT_MODE0_MINB
+#define CKB_NTT_MODE0_MINB 3
+#endif
 template <int S, bool FWD, int RBT, int MODE = 0>
 __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
-                                  MODE == 1 || MODE == 3 ? (FWD ? 6 : 8) : (RBT == 3 ? 4 : 3))
+                                  MODE == 1 || MODE == 3 ? (FWD ? 6 : 8)
+                                                         : (RBT == 3 ? 4 : CKB_NTT_MODE0_MINB))
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm, CombineEp ep) {
   constexpr int G = 1 << S;
   constexpr int RB = S < RBT ? S : RBT;  // log2 elements per thread
@@ -804,7 +808,10 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
       if (!any_f64 || (any_int && mixed_one_kernel))
         return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st, ep);
       // second-pass column phase: column-mapped direct I/O (MODE 3)
-      const bool cm = ph.rstride != 1 && !ph.first;
+      // column phases (first or second) of pure-FP64 launches: column-mapped
+      // direct global I/O (MODE 3) — first passes too since round 2
+      // (ModDown combine -4%, batch NTT -1%, tools/ks_micro.py A/B)
+      const bool cm = ph.rstride != 1;
       int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st, ep)
                  : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st, ep);
       if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st, ep);

@@ -1067,8 +1067,11 @@ __device__ __noinline__ uint64_t exact_rho(const uint64_t* __restrict__ src, siz
   return top > 0 ? fl : fl + 1;
 }
 
+#ifndef CKB_CORR_MINB
+#define CKB_CORR_MINB 3
+#endif
 template <int D1, int D2, int V>
-__global__ void __launch_bounds__(256, 3) k_divround_corr_hps(
+__global__ void __launch_bounds__(256, CKB_CORR_MINB) k_divround_corr_hps(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
     int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
     const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE,

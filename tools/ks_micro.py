@@ -38,6 +38,10 @@ def rb():
 
 
 A, B = rb(), rb()
+if os.environ.get("CKB_NTT_SPLIT") == "1":  # class-split NTT launches (ckb_ring flag)
+    from paper_2506_19693_b200 import _native as _nat
+
+    be.chain.set_ring_flag(_nat.RING_NTT_SPLIT, True)
 if os.environ.get("CKB_CHUNK_MB"):  # L2 budget of the sequential transforms
     be.chain.set_ntt_chunk_bytes(int(os.environ["CKB_CHUNK_MB"]) << 20)
 X = torch.empty_like(A)
@@ -88,6 +92,8 @@ res["pair_ms"] = round(e0.elapsed_time(e1) / reps, 3)
 tag = (os.environ.get("CKB_LIB") or "x/default/x").split("/")[-2]
 if os.environ.get("CKB_CHUNK_MB"):
     tag += f"+chunk{os.environ['CKB_CHUNK_MB']}"
+if os.environ.get("CKB_NTT_SPLIT") == "1":
+    tag += "+split"
 if os.environ.get("CKB_FUSE_KS") == "1":
     tag += "+fused"
 print(tag, json.dumps(res))
