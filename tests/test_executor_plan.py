@@ -72,3 +72,35 @@ def test_steady_step_program(golden_dir, name, n_bs):
     # or below it (the step consumes user levels only)
     assert max(ex.level_of[op[2] if op[0] == "ew" else op[1]]
                for op in p2.ops[p2.n_setup:] if op[0] != "enc") <= 8
+
+
+@pytest.mark.parametrize("name,n_sums,leaves,waves_max", [
+    ("c1_trace.npz", 2, 32, 70), ("c4_trace.npz", 2, 128, 80), ("c5_trace.npz", 8, 256, 160)])
+def test_fold_chains_become_summation_trees(golden_dir, name, n_sums, leaves, waves_max):
+    """executor._plan_sums: the delta-W fold (nn.py:373-381, acc = acc + dW_s
+    over the batch) becomes one n-ary sum per block and weight kind; the inner
+    adds leave the wave plan, every leaf is read by the sum, the values a sum
+    replaces have no other reader, and the step's waves shrink accordingly."""
+    prog = Program.load(os.path.join(golden_dir, name))
+    ex = WaveExecutor(prog, _stub_custodian(prog, real_bootstrap=name != "c1_trace.npz"))
+    assert len(ex.sums) == n_sums
+    assert all(len(v) == leaves for v in ex.sums.values())
+    assert len(ex.absorbed) == n_sums * (leaves - 2)
+    planned = {i for wave in ex.waves for i in wave}
+    assert not (planned & ex.absorbed) and set(ex.sums) <= planned
+    readers = {}
+    for k, op in enumerate(prog.ops):
+        for x in _inputs(op):
+            readers.setdefault(x, []).append(k)
+    for j in ex.absorbed:  # an absorbed add's result feeds exactly one add of its tree
+        out = prog.ops[j][2]
+        assert len(readers[out]) == 1 and out not in prog.keep
+    for root, lv in ex.sums.items():  # each leaf's last use is its sum
+        assert all(ex.last_use[x] >= root for x in lv)
+    assert len(ex.waves) <= waves_max
+
+
+def test_data_parallel_executor_keeps_the_fold_joins():
+    from paper_2506_19693_b200.dp import DataParallelExecutor
+
+    assert DataParallelExecutor.rewrite_sums is False
