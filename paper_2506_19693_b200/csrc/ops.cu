@@ -106,6 +106,37 @@ __global__ void k_scalar_mul(uint64_t* __restrict__ out, const uint64_t* __restr
   }
 }
 
+// Two coefficients per thread with 16-byte loads and stores (N >= 2).
+__global__ void k_tensor2(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                          const uint64_t* __restrict__ b, size_t total, int log_n, int limbs,
+                          RingDev R, LimbMap lm) {
+  const size_t N = (size_t)1 << log_n;
+  const size_t poly = (size_t)limbs * N;
+  for (size_t i = 2 * (blockIdx.x * (size_t)blockDim.x + threadIdx.x); i < total;
+       i += 2 * (size_t)gridDim.x * blockDim.x) {
+    const size_t bi = i / poly, off = i - bi * poly;
+    const int l = (int)(off >> log_n);
+    const Mod m = load_mod(R, lm.p[l]);
+    const uint64_t* pa = a + bi * 2 * poly + off;
+    const uint64_t* pb = b + bi * 2 * poly + off;
+    const ulonglong2 a0 = __ldcs(reinterpret_cast<const ulonglong2*>(pa));
+    const ulonglong2 a1 = __ldcs(reinterpret_cast<const ulonglong2*>(pa + poly));
+    const ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2*>(pb));
+    const ulonglong2 b1 = __ldcs(reinterpret_cast<const ulonglong2*>(pb + poly));
+    uint64_t* po = out + bi * 3 * poly + off;
+    ulonglong2 d0, d1, d2;
+    d0.x = ckb::mul_mod(a0.x, b0.x, m);
+    d0.y = ckb::mul_mod(a0.y, b0.y, m);
+    d1.x = ckb::add_mod(ckb::mul_mod(a0.x, b1.x, m), ckb::mul_mod(a1.x, b0.x, m), m.p);
+    d1.y = ckb::add_mod(ckb::mul_mod(a0.y, b1.y, m), ckb::mul_mod(a1.y, b0.y, m), m.p);
+    d2.x = ckb::mul_mod(a1.x, b1.x, m);
+    d2.y = ckb::mul_mod(a1.y, b1.y, m);
+    *reinterpret_cast<ulonglong2*>(po) = d0;
+    *reinterpret_cast<ulonglong2*>(po + poly) = d1;
+    *reinterpret_cast<ulonglong2*>(po + 2 * poly) = d2;
+  }
+}
+
 __global__ void k_tensor(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                          const uint64_t* __restrict__ b, size_t total, int log_n, int limbs,
                          RingDev R, LimbMap lm) {
@@ -1301,6 +1332,49 @@ __global__ void k_automorphism_ntt(uint64_t* __restrict__ out, const uint64_t* _
   }
 }
 
+// Blocked form.  In the bit-reversed evaluation order the automorphism maps
+// the slots of an output block (fixed top bits of the index) onto ONE input
+// block: bits 1..t of e*g mod 2N depend only on bits 1..t of e, and those are
+// the top t index bits after the bit reversal.  So a CTA loads its source block
+// contiguously (16-byte vectors), permutes inside shared memory and writes its
+// output block contiguously: both global streams are coalesced, where the
+// gather form read 8 bytes per 32-byte sector.
+constexpr int kAutLogBlock = 11;  // 2048 slots = 16 KiB per CTA
+__global__ void __launch_bounds__(256) k_automorphism_ntt_blk(
+    uint64_t* __restrict__ out, const uint64_t* __restrict__ in, int log_n, uint64_t g0,
+    const uint64_t* __restrict__ g_items, int rows_per_item) {
+  __shared__ __align__(16) uint64_t tile[1 << kAutLogBlock];
+  const int lb = min(kAutLogBlock, log_n);
+  const uint32_t B = 1u << lb;
+  const int nblk = 1 << (log_n - lb);
+  const size_t row = blockIdx.x / nblk;
+  const uint32_t b = blockIdx.x % nblk;
+  const uint64_t N = 1ull << log_n;
+  const uint64_t mask2 = 2 * N - 1;
+  const uint64_t g = g_items ? __ldg(g_items + row / rows_per_item) : g0;
+  auto src_of = [&](uint32_t t) -> uint32_t {
+    const uint32_t bt = __brev(t) >> (32 - log_n);
+    const uint64_t e = ((2ull * bt + 1) * g) & mask2;
+    return __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
+  };
+  const uint32_t t0 = b << lb;
+  const uint32_t sb = src_of(t0) >> lb;
+  const uint64_t* ib = in + row * N + (size_t)sb * B;
+  for (uint32_t k = 2 * threadIdx.x; k < B; k += 2 * blockDim.x) {
+    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(ib + k));
+    tile[k] = v.x;
+    tile[k + 1] = v.y;
+  }
+  __syncthreads();
+  uint64_t* ob = out + row * N + (size_t)t0;
+  for (uint32_t k = 2 * threadIdx.x; k < B; k += 2 * blockDim.x) {
+    ulonglong2 v;
+    v.x = tile[src_of(t0 + k) & (B - 1)];
+    v.y = tile[src_of(t0 + k + 1) & (B - 1)];
+    __stcs(reinterpret_cast<ulonglong2*>(ob + k), v);
+  }
+}
+
 // x mod p for arbitrary 64-bit words (after an integer all-reduce of residues).
 __global__ void k_reduce(uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t total,
                          int log_n, int limbs, RingDev R, LimbMap lm) {
@@ -1741,6 +1815,12 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
   const RingDev R = make_ring(ring);
   const size_t total = ((size_t)batch * limbs) << R.log_n;
   if (!total) return 0;
+  if (R.log_n >= 1) {  // pairs never straddle a limb
+    k_tensor2<<<grid_for(total / 2, 256), 256, 0, (cudaStream_t)stream>>>(out, a, b, total,
+                                                                          (int)R.log_n, limbs, R,
+                                                                          lm);
+    return finish();
+  }
   k_tensor<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(out, a, b, total,
                                                                     (int)R.log_n, limbs, R, lm);
   return finish();
@@ -2151,6 +2231,15 @@ int ckb_automorphism_ntt(const ckb_ring* ring, uint64_t* out, const uint64_t* in
   const RingDev R = make_ring(ring);
   const size_t total = (size_t)rows << R.log_n;
   if (!total) return 0;
+#ifndef CKB_AUT_GATHER
+  if (R.log_n >= 1) {
+    const int lb = std::min(kAutLogBlock, (int)R.log_n);
+    const size_t blocks = (size_t)rows << (R.log_n - lb);
+    k_automorphism_ntt_blk<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        out, in, (int)R.log_n, galois, galois_items, rows_per_item);
+    return finish();
+  }
+#endif
   k_automorphism_ntt<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       out, in, total, (int)R.log_n, galois, galois_items, rows_per_item);
   return finish();
