@@ -655,15 +655,24 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
     const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
     const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
     const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
-    for (int bi = 0; bi < batch; ++bi) {
+    auto load_item = [&](int bi, ulonglong2* x) {
       const uint64_t* dbase = dig + (size_t)bi * item_rows * N;
-      ulonglong2 x[ND];
 #pragma unroll
       for (int j = 0; j < ND; ++j) {
         const uint64_t* xp = (j == owner) ? own + bi * own_bstride + (size_t)e * N + n
                                           : dbase + rowoff[j];
         x[j] = __ldcs(reinterpret_cast<const ulonglong2*>(xp));
       }
+    };
+    ulonglong2 xn[ND];
+    load_item(0, xn);
+    for (int bi = 0; bi < batch; ++bi) {
+      ulonglong2 x[ND];
+#pragma unroll
+      for (int j = 0; j < ND; ++j) x[j] = xn[j];
+#ifndef CKB_KSS_NO_PREFETCH
+      if (bi + 1 < batch) load_item(bi + 1, xn);  // next item's loads in flight during this MAC
+#endif
       uint64_t hb0 = 0, lb0 = 0, ha0 = 0, la0 = 0, hb1 = 0, lb1 = 0, ha1 = 0, la1 = 0;
 #pragma unroll
       for (int j = 0; j < ND; ++j) {
@@ -687,6 +696,9 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
       uint64_t* o = acc + ((size_t)bi * 2 * ext + e) * N + n;
       __stcs(reinterpret_cast<ulonglong2*>(o), ob);
       __stcs(reinterpret_cast<ulonglong2*>(o + (size_t)ext * N), oa);
+#ifdef CKB_KSS_NO_PREFETCH
+      if (bi + 1 < batch) load_item(bi + 1, xn);
+#endif
     }
   }
 }
