@@ -1113,6 +1113,12 @@ __device__ __noinline__ uint64_t exact_rho(const uint64_t* __restrict__ src, siz
 #ifndef CKB_CORR_MINB
 #define CKB_CORR_MINB 3
 #endif
+// widest first drop handled two coefficients per thread (A/B: round 1 measured
+// config 5's steady step 5.89 -> 5.77 s with 11, despite the spills of the
+// <11, *, 2> instantiations under the 80-register bound)
+#ifndef CKB_CORR_VV2_MAX
+#define CKB_CORR_VV2_MAX 11
+#endif
 template <int D1, int D2, int V>
 __global__ void __launch_bounds__(256, CKB_CORR_MINB) k_divround_corr_hps(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
@@ -2143,7 +2149,7 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
     if (smh > 200 * 1024) return CKB_E_ARG;
 #define CKB_DH(A, B)                                                                        \
   if (d1 == A && d2 == B) {                                                                 \
-    constexpr int VV = A <= 11 ? 2 : 1; /* narrow drops: two coefficients per thread */     \
+    constexpr int VV = A <= CKB_CORR_VV2_MAX ? 2 : 1; /* two coefficients per thread */    \
     if (smh > 48 * 1024)                                                                    \
       cudaFuncSetAttribute(k_divround_corr_hps<A, B, VV>,                                   \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh);          \
