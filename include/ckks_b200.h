@@ -64,14 +64,27 @@ typedef struct {
   /* CKB_RING_* bits: configuration read at every call, never stored. */
   uint32_t flags;
   uint32_t reserved;
+  /* bit i set: prime i is >= 2^40 (8 byte columns in the tensor-core basis
+   * conversions instead of 5); read only under CKB_RING_TC. */
+  uint64_t wide_mask[2];
 } ckb_ring;
 
 /* ckb_ring.flags */
 #define CKB_RING_HPS_EXACT 1u /* test hook: settle every rho of the fast-conversion
                                  ModDown correction via the exact mixed-radix path */
+#define CKB_RING_TC 4u        /* run ModUp and the fast-conversion ModDown
+                                 correction on the tensor cores (tcgen05.mma
+                                 kind::i8, byte-sliced; bit-identical results).
+                                 Requires wide_mask. */
 #define CKB_RING_NTT_SPLIT 2u /* run FP64-class and integer-class NTT rows of one
                                  call as two kernels instead of one per-CTA-dispatch
                                  kernel (same integers; A/B measurements) */
+
+/* Test hook: D[128][n] = A[128][k] . B[n][k]^T over u8 with s32 results on
+ * the tensor cores (one tcgen05.mma kind::i8 tile; the operand layout of the
+ * basis conversions).  k: multiple of 32 in [32, 256]; n: multiple of 16 in
+ * [16, 256].  Device pointers. */
+int ckb_tc_selftest(const uint8_t* A, const uint8_t* B, int32_t* D, int k, int n, void* stream);
 
 /* Library version (for load checks). */
 int ckb_version(void);

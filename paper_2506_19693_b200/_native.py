@@ -25,11 +25,13 @@ class CkbRing(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n_primes", ctypes.c_uint32),
                 ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp),
                 ("f64_mask", ctypes.c_uint64 * 2), ("ntt_chunk_bytes", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("wide_mask", ctypes.c_uint64 * 2)]
 
 
 RING_HPS_EXACT = 1  # ckb_ring.flags (include/ckks_b200.h)
 RING_NTT_SPLIT = 2
+RING_TC = 4  # tensor-core ModUp / ModDown correction (needs wide_mask)
 DEFAULT_NTT_CHUNK_BYTES = 96 << 20
 
 
@@ -40,6 +42,17 @@ def f64_mask(primes) -> tuple:
     m = 0
     for i, p in enumerate(primes):
         if int(p) < F64_PRIME_LIMIT and i < 128:
+            m |= 1 << i
+    return (m & (2**64 - 1), m >> 64)
+
+
+TC_WIDE_LIMIT = 1 << 40  # csrc/tc.cu: primes at or above take 8 byte columns
+
+
+def wide_mask(primes) -> tuple:
+    m = 0
+    for i, p in enumerate(primes):
+        if int(p) >= TC_WIDE_LIMIT and i < 128:
             m |= 1 << i
     return (m & (2**64 - 1), m >> 64)
 
@@ -117,6 +130,7 @@ def _load():
         "ckb_reduce": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_sample": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_double,
                         c_vp], ctypes.c_int),
+        "ckb_tc_selftest": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_alu_probe": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c_vp,
                            c_vp], ctypes.c_int),
         "ckb_alu_probe_f64": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
@@ -141,7 +155,7 @@ EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inver
             "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
             "ckb_automorphism_ntt",
             "ckb_reduce", "ckb_sample", "ckb_alu_probe",
-            "ckb_alu_probe_f64")
+            "ckb_alu_probe_f64", "ckb_tc_selftest")
 
 
 def check(rc: int, what: str) -> None:

@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libckks_b200.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
-SOURCES = ["ntt.cu", "ops.cu"]
+SOURCES = ["ntt.cu", "ops.cu", "tc.cu"]
 HEADERS = ["common.cuh", "modarith.cuh", "fp64.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -34,6 +34,7 @@ struct RingDev {
   uint64_t f64_mask[2];  // host-side prime classes (ckb_ring.f64_mask)
   uint64_t ntt_chunk_bytes;  // host-side (ckb_ring.ntt_chunk_bytes, 0 = default)
   uint32_t flags;            // host-side (ckb_ring.flags)
+  uint64_t wide_mask[2];     // host-side (ckb_ring.wide_mask)
 };
 
 __device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
@@ -63,8 +64,19 @@ inline RingDev make_ring(const ckb_ring* r) {
   d.f64_mask[1] = r->f64_mask[1];
   d.ntt_chunk_bytes = r->ntt_chunk_bytes;
   d.flags = r->flags;
+  d.wide_mask[0] = r->wide_mask[0];
+  d.wide_mask[1] = r->wide_mask[1];
   return d;
 }
+
+// Tensor-core basis conversions (tc.cu).  Return 1 when not applicable (the
+// caller runs its CUDA-core kernel), else the launch status.
+int tc_modup(const RingDev& R, uint64_t* out, const uint64_t* in, size_t bstride, int batch,
+             int limbs, const LimbMap& lm, int ext, const LimbMap& em, int alpha,
+             const uint64_t* bconv, int skip_own, int out_rows, int item_rows, cudaStream_t st);
+int tc_corr(const RingDev& R, uint64_t* E, const uint64_t* T, int has_add, int polys, int limbs,
+            const LimbMap& lm, int n1, int n2, const uint64_t* tab1, const uint64_t* tab2,
+            const uint64_t* tabE, const uint64_t* tabH, double margin, cudaStream_t st);
 
 inline int finish() { return (int)cudaGetLastError(); }
 

@@ -1880,6 +1880,11 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
     digit_f64 = ok;
   }
   for (int e = 0; e < ext_limbs; ++e) out_f64 |= is_f64(em.p[e]);
+  {
+    const int rc = tc_modup(R, out, in, bstride, batch, limbs, lm, ext_limbs, em, alpha, bconv,
+                            skip_own, out_rows, item_rows, (cudaStream_t)stream);
+    if (rc != 1) return rc;
+  }
 #ifndef CKB_MODUP_V1
   if (alpha > 1) {  // per-class output lists, two coefficients per thread
     using KernV = decltype(&k_modup_v2<2>);
@@ -2143,6 +2148,9 @@ int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, 
   const int d2 = n_drop2 == 0 ? 0 : n_drop2 <= 1 ? 1 : n_drop2 <= 2 ? 2 : 8;
   cudaStream_t st0 = (cudaStream_t)stream;
   if (tabH && n_drop1 >= kHpsMinDrop && n_drop2 <= 2) {  // fast basis-conversion form
+    const int rc = tc_corr(R, E, T, has_addend, polys, limbs, lm, n_drop1, n_drop2, tab1, tab2,
+                           tabE, tabH, (R.flags & CKB_RING_HPS_EXACT) ? 0.0 : kHpsMargin, st0);
+    if (rc != 1) return rc;
     const int m2h = limbs - n_drop1 - n_drop2;
     const size_t smh = (size_t)m2h * (6 + 2 * (n_drop1 + n_drop2 + 1) + n_drop1) * 8 +
                        4 * kMaxDrop * 8;

@@ -15,6 +15,7 @@ Every wrapper launches on the caller's current CUDA stream.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -72,6 +73,11 @@ def _run(name, nbytes, launches, fn, f64_share=None):
 
 
 class GpuChain:
+    # ModUp and the fast-conversion ModDown correction on the tensor cores
+    # (csrc/tc.cu, CKB_RING_TC; bit-identical to the CUDA-core kernels, which
+    # CKB_NO_TC=1 selects for A/B runs).  Per chain: set_ring_flag(RING_TC, ...).
+    use_tc = os.environ.get("CKB_NO_TC") != "1"
+
     def __init__(self, params, layout: str = "reference", device=None):
         self.params = params
         self.layout = layout
@@ -99,6 +105,9 @@ class GpuChain:
         self.ring = nat.CkbRing(self.log_n, len(self.all_primes), self._mods.data_ptr(),
                                 self._ntt.data_ptr(), self._pair.data_ptr(),
                                 (nat.ctypes.c_uint64 * 2)(*nat.f64_mask(self.all_primes)))
+        self.ring.wide_mask = (nat.ctypes.c_uint64 * 2)(*nat.wide_mask(self.all_primes))
+        if self.use_tc:
+            self.ring.flags |= nat.RING_TC
         self.ring_p = nat.ctypes.pointer(self.ring)
         self._maps: dict = {}
 
