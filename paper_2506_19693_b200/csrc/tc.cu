@@ -243,44 +243,66 @@ __device__ __forceinline__ uint64_t tc_reduce_narrow(uint64_t v, const TcSlot& S
   return r >= S.p ? r - S.p : r;
 }
 
+// One group of 8 narrow outputs (40 accumulator columns from 5g).  GUARD:
+// the tail group (outputs past n_narrow are skipped); full groups run
+// branch-free so the compiler interleaves the 8 independent reductions.
+template <bool FAST, bool GUARD>
+__device__ __forceinline__ void tc_group8(uint32_t tl, int g, int n_narrow, const TcSlot* slots,
+                                          uint64_t* __restrict__ out) {
+  uint32_t v[40];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) tmem_ld8(tl + (uint32_t)(5 * g + 8 * q), v + 8 * q);
+  tmem_wait<40>(v);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    if (!GUARD || g + o < n_narrow) {
+      const TcSlot& S = slots[g + o];
+      uint64_t x = (uint64_t)v[5 * o + 1] * 256u + v[5 * o];
+      x += (uint64_t)v[5 * o + 2] * 65536u;
+      x += (uint64_t)v[5 * o + 3] * 16777216u;
+      x += (uint64_t)v[5 * o + 4] << 32;
+      out[S.roff] = tc_reduce_narrow<FAST>(x, S);
+    }
+  }
+}
+
+__device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const TcSlot& S,
+                                         uint64_t* __restrict__ out) {
+  uint64_t lo = (uint64_t)v[1] * 256u + v[0];
+  lo += (uint64_t)v[2] * 65536u;
+  lo += (uint64_t)v[3] * 16777216u;
+  lo += S.addc;
+  uint64_t hi = (uint64_t)v[5] * 256u + v[4];
+  hi += (uint64_t)v[6] * 65536u;
+  hi += (uint64_t)v[7] * 16777216u;
+  const uint64_t l = lo + (hi << 32);
+  const uint64_t h = (hi >> 32) + (l < lo ? 1 : 0);
+  const Mod m{S.p, S.mu, S.k, S.two_p};
+  out[S.roff] = ckb::barrett_reduce128(h, l, m);
+}
+
 // Read this thread's TMEM lane and store every output: out[slot.roff].
 // FAST: every narrow output prime has >= 26 bits (the 32-bit quotient path).
 template <bool FAST>
 __device__ __forceinline__ void tc_epilogue_t(uint32_t tl, TcCols cols, const TcSlot* slots,
                                               uint64_t* __restrict__ out) {
-  for (int g = 0; g < cols.n_narrow; g += 8) {
-    uint32_t v[40];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) tmem_ld8(tl + (uint32_t)(5 * g + 8 * q), v + 8 * q);
-    tmem_wait<40>(v);
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      if (g + o < cols.n_narrow) {
-        const TcSlot& S = slots[g + o];
-        uint64_t x = (uint64_t)v[5 * o + 1] * 256u + v[5 * o];
-        x += (uint64_t)v[5 * o + 2] * 65536u;
-        x += (uint64_t)v[5 * o + 3] * 16777216u;
-        x += (uint64_t)v[5 * o + 4] << 32;
-        out[S.roff] = tc_reduce_narrow<FAST>(x, S);
-      }
-    }
+  int g = 0;
+  for (; g + 8 <= cols.n_narrow; g += 8) tc_group8<FAST, false>(tl, g, cols.n_narrow, slots, out);
+  if (g < cols.n_narrow) tc_group8<FAST, true>(tl, g, cols.n_narrow, slots, out);
+  int s = 0;
+  for (; s + 2 <= cols.n_wide; s += 2) {  // two wide outputs per round
+    uint32_t v[16];
+    tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
+    tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s + 8), v + 8);
+    tmem_wait<16>(v);
+    tc_wide1(tl, v, slots[cols.n_narrow + s], out);
+    tc_wide1(tl, v + 8, slots[cols.n_narrow + s + 1], out);
   }
-  for (int s = 0; s < cols.n_wide; ++s) {
+  if (s < cols.n_wide) {
     uint32_t v[8];
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
     tmem_wait<8>(v);
-    const TcSlot& S = slots[cols.n_narrow + s];
-    uint64_t lo = (uint64_t)v[1] * 256u + v[0];
-    lo += (uint64_t)v[2] * 65536u;
-    lo += (uint64_t)v[3] * 16777216u;
-    lo += S.addc;
-    uint64_t hi = (uint64_t)v[5] * 256u + v[4];
-    hi += (uint64_t)v[6] * 65536u;
-    hi += (uint64_t)v[7] * 16777216u;
-    const uint64_t l = lo + (hi << 32);
-    const uint64_t h = (hi >> 32) + (l < lo ? 1 : 0);
-    const Mod m{S.p, S.mu, S.k, S.two_p};
-    out[S.roff] = ckb::barrett_reduce128(h, l, m);
+    tc_wide1(tl, v, slots[cols.n_narrow + s], out);
   }
 }
 
