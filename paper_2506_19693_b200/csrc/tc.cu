@@ -266,6 +266,11 @@ __device__ __forceinline__ void tc_group8(uint32_t tl, int g, int n_narrow, cons
   }
 }
 
+// A wide output's 8 columns: v = lo + hi 2^32 < 2^80.  FAST (prime of 49..62
+// bits): top = v >> (k-1) < 2^32 and q = hi32(top * mu32) is within 2 of
+// floor(v / p) (v / 2^(k+31) < 0.82, 2^(k-1) / p <= 1); the remainder fits 64
+// bits, so it is computed mod 2^64 from the low word.  Else 128-bit Barrett.
+template <bool FAST>
 __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const TcSlot& S,
                                          uint64_t* __restrict__ out) {
   uint64_t lo = (uint64_t)v[1] * 256u + v[0];
@@ -277,6 +282,14 @@ __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const T
   hi += (uint64_t)v[7] * 16777216u;
   const uint64_t l = lo + (hi << 32);
   const uint64_t h = (hi >> 32) + (l < lo ? 1 : 0);
+  if (FAST || S.mu32 != 0) {
+    const uint32_t top = (uint32_t)__funnelshift_r((uint32_t)(l >> 32), (uint32_t)h, S.sh - 32);
+    const uint32_t q = __umulhi(top, S.mu32);
+    uint64_t r = l - (uint64_t)q * S.p;
+    r = r >= S.p ? r - S.p : r;
+    out[S.roff] = r >= S.p ? r - S.p : r;
+    return;
+  }
   const Mod m{S.p, S.mu, S.k, S.two_p};
   out[S.roff] = ckb::barrett_reduce128(h, l, m);
 }
@@ -295,14 +308,14 @@ __device__ __forceinline__ void tc_epilogue_t(uint32_t tl, TcCols cols, const Tc
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s + 8), v + 8);
     tmem_wait<16>(v);
-    tc_wide1(tl, v, slots[cols.n_narrow + s], out);
-    tc_wide1(tl, v + 8, slots[cols.n_narrow + s + 1], out);
+    tc_wide1<FAST>(tl, v, slots[cols.n_narrow + s], out);
+    tc_wide1<FAST>(tl, v + 8, slots[cols.n_narrow + s + 1], out);
   }
   if (s < cols.n_wide) {
     uint32_t v[8];
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
     tmem_wait<8>(v);
-    tc_wide1(tl, v, slots[cols.n_narrow + s], out);
+    tc_wide1<FAST>(tl, v, slots[cols.n_narrow + s], out);
   }
 }
 
@@ -313,6 +326,20 @@ __device__ __forceinline__ void tc_epilogue(uint32_t tl, TcCols cols, const TcSl
   } else {
     tc_epilogue_t<false>(tl, cols, slots, out);
   }
+}
+
+// floor(2^e / p) for 63 <= e <= 95 and p >= 2^(e-63) (setup only: bitwise long division)
+__device__ inline uint64_t div_pow2(int e, uint64_t p) {
+  uint64_t q = (1ull << 63) / p, r = (1ull << 63) - q * p;
+  for (int i = 63; i < e; ++i) {
+    q <<= 1;
+    r <<= 1;  // r < p < 2^63
+    if (r >= p) {
+      r -= p;
+      q |= 1;
+    }
+  }
+  return q;
 }
 
 __device__ inline void load_slot(TcSlot& s, const RingDev& R, int pi, int row, size_t N) {
@@ -329,15 +356,11 @@ __device__ inline void load_slot(TcSlot& s, const RingDev& R, int pi, int row, s
   s.key = row;
   s.pad = 0;
   s.sh = (uint32_t)s.k - 1;
-  s.mu32 = 0;
-  if (s.k >= 26 && s.k <= kNarrowBits) {  // floor(2^(31+k) / p) in [2^31, 2^32)
-    if (s.k < 33) {
-      s.mu32 = (uint32_t)((1ull << (31 + s.k)) / s.p);
-    } else {  // 2^63 / p, then e = k - 32 more bits of long division
-      const uint64_t q1 = (1ull << 63) / s.p, r1 = (1ull << 63) - q1 * s.p;
-      const int e = (int)s.k - 32;
-      s.mu32 = (uint32_t)((q1 << e) + ((r1 << e) / s.p));
-    }
+  s.mu32 = 0;  // floor(2^(31+k) / p) in [2^31, 2^32) where the quotient path applies
+  if (s.k >= 26 && s.k <= kNarrowBits) {
+    s.mu32 = (uint32_t)(s.k < 33 ? (1ull << (31 + s.k)) / s.p : div_pow2(31 + (int)s.k, s.p));
+  } else if (s.k >= 49 && s.k <= 62) {
+    s.mu32 = (uint32_t)div_pow2(31 + (int)s.k, s.p);
   }
 }
 
@@ -353,7 +376,10 @@ __device__ inline void order_slots(TcSlot* slots, const TcSlot* tmp, int n, int*
     }
   *n_narrow = a;
   for (int s = 0; s < n; ++s)
-    if (tmp[s].k > kNarrowBits) slots[a++] = tmp[s];
+    if (tmp[s].k > kNarrowBits) {
+      *fast &= tmp[s].mu32 != 0;
+      slots[a++] = tmp[s];
+    }
 }
 
 struct TcShared {
