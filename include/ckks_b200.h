@@ -64,9 +64,12 @@ typedef struct {
   /* CKB_RING_* bits: configuration read at every call, never stored. */
   uint32_t flags;
   uint32_t reserved;
-  /* bit i set: prime i is >= 2^40 (8 byte columns in the tensor-core basis
-   * conversions instead of 5); read only under CKB_RING_TC. */
+  /* Prime size classes of the tensor-core basis conversions (byte columns
+   * per output): bit i of wide_mask: prime i >= 2^48 (8 columns); of
+   * mid_mask: 2^40 <= prime i < 2^48 (6 columns); neither: < 2^40 (5).
+   * Read only under CKB_RING_TC; a mismatch with the primes traps. */
   uint64_t wide_mask[2];
+  uint64_t mid_mask[2];
 } ckb_ring;
 
 /* ckb_ring.flags */

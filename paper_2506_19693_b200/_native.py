@@ -26,7 +26,7 @@ class CkbRing(ctypes.Structure):
                 ("mods", c_vp), ("ntt", c_vp), ("pair", c_vp),
                 ("f64_mask", ctypes.c_uint64 * 2), ("ntt_chunk_bytes", ctypes.c_uint64),
                 ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
-                ("wide_mask", ctypes.c_uint64 * 2)]
+                ("wide_mask", ctypes.c_uint64 * 2), ("mid_mask", ctypes.c_uint64 * 2)]
 
 
 RING_HPS_EXACT = 1  # ckb_ring.flags (include/ckks_b200.h)
@@ -46,15 +46,24 @@ def f64_mask(primes) -> tuple:
     return (m & (2**64 - 1), m >> 64)
 
 
-TC_WIDE_LIMIT = 1 << 40  # csrc/tc.cu: primes at or above take 8 byte columns
+TC_MID_LIMIT = 1 << 40   # csrc/tc.cu column classes: < 2^40: 5 byte columns,
+TC_WIDE_LIMIT = 1 << 48  # [2^40, 2^48): 6, >= 2^48: 8
+
+
+def _mask(primes, lo, hi) -> tuple:
+    m = 0
+    for i, p in enumerate(primes):
+        if lo <= int(p) < hi and i < 128:
+            m |= 1 << i
+    return (m & (2**64 - 1), m >> 64)
 
 
 def wide_mask(primes) -> tuple:
-    m = 0
-    for i, p in enumerate(primes):
-        if int(p) >= TC_WIDE_LIMIT and i < 128:
-            m |= 1 << i
-    return (m & (2**64 - 1), m >> 64)
+    return _mask(primes, TC_WIDE_LIMIT, 1 << 64)
+
+
+def mid_mask(primes) -> tuple:
+    return _mask(primes, TC_MID_LIMIT, TC_WIDE_LIMIT)
 
 
 class NativeError(RuntimeError):

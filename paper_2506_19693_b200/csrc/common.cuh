@@ -35,6 +35,7 @@ struct RingDev {
   uint64_t ntt_chunk_bytes;  // host-side (ckb_ring.ntt_chunk_bytes, 0 = default)
   uint32_t flags;            // host-side (ckb_ring.flags)
   uint64_t wide_mask[2];     // host-side (ckb_ring.wide_mask)
+  uint64_t mid_mask[2];      // host-side (ckb_ring.mid_mask)
 };
 
 __device__ __forceinline__ Mod load_mod(const RingDev& R, int pi) {
@@ -66,6 +67,8 @@ inline RingDev make_ring(const ckb_ring* r) {
   d.flags = r->flags;
   d.wide_mask[0] = r->wide_mask[0];
   d.wide_mask[1] = r->wide_mask[1];
+  d.mid_mask[0] = r->mid_mask[0];
+  d.mid_mask[1] = r->mid_mask[1];
   return d;
 }
 

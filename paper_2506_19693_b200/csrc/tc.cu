@@ -38,7 +38,8 @@ using namespace ckb_internal;
 namespace {
 
 constexpr int kTcRows = 128;      // GEMM M (one TMEM lane per coefficient)
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 128;   // per TMEM lane set; CTAs run 128 * h threads (h = 1, 2, 4)
+constexpr int kTcMaxThreads = 512;
 constexpr int kNarrowBits = 40;   // primes < 2^40: 5 byte columns, else 8
 
 // ---------------------------------------------------------------------------
@@ -153,29 +154,62 @@ struct __align__(16) TcSlot {
   uint32_t roff;   // row * N (elements from the tile's output base)
   int key;         // constant lookup index (ext limb / kept limb)
   uint64_t mu, k, two_p, r64, r64s;  // Barrett (wide outputs) and the generic reduction
+  uint64_t w256s;                    // floor(256 * 2^64 / p): B-matrix byte shifts
   int row, pad;
 };
 
-// Column layout of the accumulator: narrow outputs (p < 2^40) first, 5
-// columns each, read in groups of 8 outputs (40 columns); wide outputs after,
-// 8 columns each from an 8-aligned start.
+// Column layout of the accumulator, by output prime size: narrow (<= 40
+// bits, 5 byte columns, read in groups of 8 outputs = 40 columns), mid (41..48
+// bits, 6 columns, groups of 4 = 24 columns), wide (>= 49 bits, 8 columns,
+// pairs).  Each class starts 8-aligned.  Work units (one group or pair each)
+// are spread over the warps that share a TMEM lane quarter.
 struct TcCols {
-  int n_narrow, n_wide, col_wide, n_mma, n_alloc;
+  int n_narrow, n_mid, n_wide, col_mid, col_wide, n_mma, n_alloc;
+  int u_narrow, u_mid, u_wide;  // work units per class
 };
 
-__host__ __device__ inline TcCols tc_cols(int n_narrow, int n_wide) {
+__host__ __device__ inline int tc_class_of_bits(int k) { return k <= 40 ? 0 : k <= 48 ? 1 : 2; }
+
+__host__ __device__ inline TcCols tc_cols(int n_narrow, int n_mid, int n_wide) {
   TcCols c;
   c.n_narrow = n_narrow;
+  c.n_mid = n_mid;
   c.n_wide = n_wide;
-  c.col_wide = (5 * n_narrow + 7) & ~7;
+  c.col_mid = (5 * n_narrow + 7) & ~7;
+  c.col_wide = (c.col_mid + 6 * n_mid + 7) & ~7;
   const int used = c.col_wide + 8 * n_wide;
   c.n_mma = (used + 15) & ~15;
-  const int r40 = 40 * ((n_narrow + 7) / 8);
-  const int read = c.n_mma > r40 ? c.n_mma : r40;
+  c.u_narrow = (n_narrow + 7) / 8;
+  c.u_mid = (n_mid + 3) / 4;
+  c.u_wide = (n_wide + 1) / 2;
+  int read = c.n_mma;
+  read = read > 40 * c.u_narrow ? read : 40 * c.u_narrow;
+  read = read > c.col_mid + 24 * c.u_mid ? read : c.col_mid + 24 * c.u_mid;
+  read = read > c.col_wide + 16 * c.u_wide ? read : c.col_wide + 16 * c.u_wide;
   int a = 32;
   while (a < read) a <<= 1;
   c.n_alloc = a;
   return c;
+}
+
+__host__ __device__ inline int tc_col0(const TcCols& c, int s) {
+  if (s < c.n_narrow) return 5 * s;
+  if (s < c.n_narrow + c.n_mid) return c.col_mid + 6 * (s - c.n_narrow);
+  return c.col_wide + 8 * (s - c.n_narrow - c.n_mid);
+}
+
+// floor(2^e / p) for 63 <= e <= 95 and p >= 2^(e-63) (setup only: bitwise long division)
+__device__ inline uint64_t div_pow2(int e, uint64_t p) {
+  uint64_t q = (1ull << 63) / p, r = (1ull << 63) - q * p;
+  for (int i = 63; i < e; ++i) {
+    q <<= 1;
+    r <<= 1;  // r < p < 2^63
+    if (r >= p) {
+      r -= p;
+      q |= 1;
+    }
+  }
+  return q;
 }
 
 // B[col][8u + a] = byte b of 2^(8a) C_uj mod p_j for the column (j, b).
@@ -187,23 +221,22 @@ __device__ void tc_build_b(uint8_t* B, int kp, int n_rows, const TcSlot* slots, 
   for (int i = threadIdx.x; i < n_rows * kp / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(B)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  const int nslots = cols.n_narrow + cols.n_wide;
-  for (int q = threadIdx.x; q < nslots * nvals * 8; q += blockDim.x) {
-    const int s = q / (nvals * 8);
-    const int u = (q / 8) % nvals;
-    const int a = q % 8;
+  const int nslots = cols.n_narrow + cols.n_mid + cols.n_wide;
+  // one (slot, value) per thread: d_0 = C, d_{a+1} = 256 d_a mod p (Shoup)
+  for (int q = threadIdx.x; q < nslots * nvals; q += blockDim.x) {
+    const int s = q / nvals;
+    const int u = q % nvals;
     const TcSlot& S = slots[s];
-    const Mod m{S.p, S.mu, S.k, S.two_p};
-    const uint64_t c = cfun(u, s);
-    const uint64_t sh = ckb::reduce128_any(0, 1ull << (8 * a), S.r64, S.r64s, m);
-    const uint64_t d = ckb::reduce128_any(ckb::mulhi(c, sh), c * sh, S.r64, S.r64s, m);
-    const bool wide = s >= cols.n_narrow;
-    const int col0 = wide ? cols.col_wide + 8 * (s - cols.n_narrow) : 5 * s;
-    const int nb = wide ? 8 : 5;
-    const int kk = 8 * u + a;
-    for (int b = 0; b < nb; ++b) {
-      const int n = col0 + b;
-      B[kmaj_off(n, kk >> 4, kp) + (kk & 15)] = (uint8_t)(d >> (8 * b));
+    const uint64_t w = 256;  // NTT primes exceed 2^9
+    const uint64_t w256s = S.w256s;
+    uint64_t d = cfun(u, s);
+    const int col0 = tc_col0(cols, s);
+    const int nb = s < cols.n_narrow ? 5 : s < cols.n_narrow + cols.n_mid ? 6 : 8;
+    for (int a = 0; a < 8; ++a) {
+      const int kk = 8 * u + a;
+      for (int b = 0; b < nb; ++b)
+        B[kmaj_off(col0 + b, kk >> 4, kp) + (kk & 15)] = (uint8_t)(d >> (8 * b));
+      d = ckb::mul_shoup(d, w, w256s, S.p);
     }
   }
   fence_async_smem();
@@ -294,53 +327,72 @@ __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const T
   out[S.roff] = ckb::barrett_reduce128(h, l, m);
 }
 
-// Read this thread's TMEM lane and store every output: out[slot.roff].
-// FAST: every narrow output prime has >= 26 bits (the 32-bit quotient path).
+// One group of 4 mid outputs (24 columns): v = sum_b<6 2^(8b) P_b < 2^64.
 template <bool FAST>
+__device__ __forceinline__ void tc_group4_mid(uint32_t tl, int col, int g, int n_mid,
+                                              const TcSlot* slots, uint64_t* __restrict__ out) {
+  uint32_t v[24];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) tmem_ld8(tl + (uint32_t)(col + 8 * q), v + 8 * q);
+  tmem_wait<24>(v);
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    if (g + o < n_mid) {
+      const TcSlot& S = slots[g + o];
+      uint64_t x = (uint64_t)v[6 * o + 1] * 256u + v[6 * o];
+      x += (uint64_t)v[6 * o + 2] * 65536u;
+      x += (uint64_t)v[6 * o + 3] * 16777216u;
+      x += ((uint64_t)v[6 * o + 5] * 256u + v[6 * o + 4]) << 32;
+      out[S.roff] = tc_reduce_narrow<FAST>(x, S);
+    }
+  }
+}
+
+// Read this thread's TMEM lane and store its share of the outputs: the work
+// units (narrow groups, mid groups, wide pairs, numbered in that order) with
+// index = sub (mod H); out[slot.roff].  FAST: every output takes the 32-bit
+// quotient path.
+template <bool FAST, int H>
 __device__ __forceinline__ void tc_epilogue_t(uint32_t tl, TcCols cols, const TcSlot* slots,
-                                              uint64_t* __restrict__ out) {
-  int g = 0;
-  for (; g + 8 <= cols.n_narrow; g += 8) tc_group8<FAST, false>(tl, g, cols.n_narrow, slots, out);
-  if (g < cols.n_narrow) tc_group8<FAST, true>(tl, g, cols.n_narrow, slots, out);
-  int s = 0;
-  for (; s + 2 <= cols.n_wide; s += 2) {  // two wide outputs per round
+                                              uint64_t* __restrict__ out, int sub) {
+  const int un = cols.u_narrow, um = cols.u_mid, uw = cols.u_wide;
+  for (int u = sub; u < un; u += H) {
+    const int g = 8 * u;
+    if (g + 8 <= cols.n_narrow)
+      tc_group8<FAST, false>(tl, g, cols.n_narrow, slots, out);
+    else
+      tc_group8<FAST, true>(tl, g, cols.n_narrow, slots, out);
+  }
+  for (int u = un + ((sub - un) % H + H) % H; u < un + um; u += H) {
+    const int g = 4 * (u - un);
+    tc_group4_mid<FAST>(tl, cols.col_mid + 6 * g, g, cols.n_mid, slots + cols.n_narrow, out);
+  }
+  const TcSlot* ws = slots + cols.n_narrow + cols.n_mid;
+  for (int u = un + um + ((sub - un - um) % H + H) % H; u < un + um + uw; u += H) {
+    const int s = 2 * (u - un - um);
     uint32_t v[16];
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
     tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s + 8), v + 8);
     tmem_wait<16>(v);
-    tc_wide1<FAST>(tl, v, slots[cols.n_narrow + s], out);
-    tc_wide1<FAST>(tl, v + 8, slots[cols.n_narrow + s + 1], out);
-  }
-  if (s < cols.n_wide) {
-    uint32_t v[8];
-    tmem_ld8(tl + (uint32_t)(cols.col_wide + 8 * s), v);
-    tmem_wait<8>(v);
-    tc_wide1<FAST>(tl, v, slots[cols.n_narrow + s], out);
+    tc_wide1<FAST>(tl, v, ws[s], out);
+    if (s + 1 < cols.n_wide) tc_wide1<FAST>(tl, v + 8, ws[s + 1], out);
   }
 }
 
 __device__ __forceinline__ void tc_epilogue(uint32_t tl, TcCols cols, const TcSlot* slots,
-                                            uint64_t* __restrict__ out, bool fast) {
+                                            uint64_t* __restrict__ out, bool fast, int sub,
+                                            int h) {
   if (fast) {
-    tc_epilogue_t<true>(tl, cols, slots, out);
+    if (h == 1) tc_epilogue_t<true, 1>(tl, cols, slots, out, sub);
+    else if (h == 2) tc_epilogue_t<true, 2>(tl, cols, slots, out, sub);
+    else tc_epilogue_t<true, 4>(tl, cols, slots, out, sub);
   } else {
-    tc_epilogue_t<false>(tl, cols, slots, out);
+    if (h == 1) tc_epilogue_t<false, 1>(tl, cols, slots, out, sub);
+    else if (h == 2) tc_epilogue_t<false, 2>(tl, cols, slots, out, sub);
+    else tc_epilogue_t<false, 4>(tl, cols, slots, out, sub);
   }
 }
 
-// floor(2^e / p) for 63 <= e <= 95 and p >= 2^(e-63) (setup only: bitwise long division)
-__device__ inline uint64_t div_pow2(int e, uint64_t p) {
-  uint64_t q = (1ull << 63) / p, r = (1ull << 63) - q * p;
-  for (int i = 63; i < e; ++i) {
-    q <<= 1;
-    r <<= 1;  // r < p < 2^63
-    if (r >= p) {
-      r -= p;
-      q |= 1;
-    }
-  }
-  return q;
-}
 
 __device__ inline void load_slot(TcSlot& s, const RingDev& R, int pi, int row, size_t N) {
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
@@ -356,8 +408,9 @@ __device__ inline void load_slot(TcSlot& s, const RingDev& R, int pi, int row, s
   s.key = row;
   s.pad = 0;
   s.sh = (uint32_t)s.k - 1;
+  s.w256s = div_pow2(72, s.p);
   s.mu32 = 0;  // floor(2^(31+k) / p) in [2^31, 2^32) where the quotient path applies
-  if (s.k >= 26 && s.k <= kNarrowBits) {
+  if (s.k >= 26 && s.k <= 48) {
     s.mu32 = (uint32_t)(s.k < 33 ? (1ull << (31 + s.k)) / s.p : div_pow2(31 + (int)s.k, s.p));
   } else if (s.k >= 49 && s.k <= 62) {
     s.mu32 = (uint32_t)div_pow2(31 + (int)s.k, s.p);
@@ -365,29 +418,35 @@ __device__ inline void load_slot(TcSlot& s, const RingDev& R, int pi, int row, s
 }
 
 // Split the output primes into the narrow / wide lists (thread 0).
-__device__ inline void order_slots(TcSlot* slots, const TcSlot* tmp, int n, int* n_narrow,
-                                   int* fast) {
-  int a = 0;
-  *fast = 1;
-  for (int s = 0; s < n; ++s)
-    if (tmp[s].k <= kNarrowBits) {
-      *fast &= tmp[s].mu32 != 0;
-      slots[a++] = tmp[s];
-    }
-  *n_narrow = a;
-  for (int s = 0; s < n; ++s)
-    if (tmp[s].k > kNarrowBits) {
-      *fast &= tmp[s].mu32 != 0;
-      slots[a++] = tmp[s];
-    }
-}
-
 struct TcShared {
   uint64_t bar;
   uint32_t tmem;
-  int n_narrow;
-  int fast;  // every narrow output takes the 32-bit quotient path
+  int counts[3];  // outputs per class (narrow, mid, wide)
+  int fast;       // every output takes the 32-bit quotient path
 };
+
+// Sort the n output slots (tmp, built in parallel) by class (narrow, mid,
+// wide) into slots, stable; counts and the FAST flag into sh.  All threads.
+__device__ inline void order_slots(TcSlot* slots, const TcSlot* tmp, int n, TcShared& sh) {
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const int c = tc_class_of_bits((int)tmp[t].k);
+    int pos = 0;
+    for (int i = 0; i < n; ++i) {
+      const int ci = tc_class_of_bits((int)tmp[i].k);
+      pos += ci < c || (ci == c && i < t);
+    }
+    slots[pos] = tmp[t];
+  }
+  if (threadIdx.x == 0) {
+    sh.counts[0] = sh.counts[1] = sh.counts[2] = 0;
+    sh.fast = 1;
+    for (int i = 0; i < n; ++i) {
+      sh.counts[tc_class_of_bits((int)tmp[i].k)]++;
+      sh.fast &= tmp[i].mu32 != 0;
+    }
+  }
+  __syncthreads();
+}
 
 // ---------------------------------------------------------------------------
 // ModUp.  grid.y = digit j; persistent over (item, 128-coefficient tile).
@@ -396,7 +455,7 @@ struct TcShared {
 // Smem: A [128][kp] | B [n_alloc][kp] | slots [ext] | tmp slots [ext].
 // ---------------------------------------------------------------------------
 template <int AMAX>
-__global__ void __launch_bounds__(kTcThreads) k_modup_tc(
+__global__ void __launch_bounds__(kTcMaxThreads) k_modup_tc(
     uint64_t* __restrict__ out, const uint64_t* __restrict__ in, size_t in_bstride, int batch,
     int limbs, int ext, int alpha, int out_rows, int item_rows, int skip_own, int log_n,
     RingDev R, LimbMap lm, LimbMap em, const uint64_t* __restrict__ bconv, int kp_max,
@@ -406,6 +465,7 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
   __shared__ uint64_t s_w[AMAX][3];
   const size_t N = (size_t)1 << log_n;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int row = tid & (kTcRows - 1), sub = tid >> 7, h = blockDim.x >> 7;
   const int j = blockIdx.y;
   const int first = j * alpha;
   const int cnt = min(alpha, limbs - first);
@@ -417,15 +477,15 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
   TcSlot* slots = reinterpret_cast<TcSlot*>(B + (size_t)nrows_max * kp_max);
   TcSlot* tmp = slots + ext;
   // output list (every ext limb outside the digit) and the digit constants
+  // output list (every ext limb outside the digit, one per thread) and the
+  // digit constants
+  for (int e = tid; e < ext; e += blockDim.x) {
+    if (e >= first && e < first + cnt) continue;
+    const int idx = e < first ? e : e - cnt;
+    load_slot(tmp[idx], R, em.p[e], skip_own ? idx : e, N);
+    tmp[idx].key = e;  // ext index (constant lookup)
+  }
   if (tid == 0) {
-    int n = 0;
-    for (int e = 0; e < ext; ++e) {
-      if (e >= first && e < first + cnt) continue;
-      load_slot(tmp[n], R, em.p[e], skip_own ? (e < first ? e : e - cnt) : e, N);
-      tmp[n].key = e;  // ext index (constant lookup)
-      ++n;
-    }
-    order_slots(slots, tmp, n, &sh.n_narrow, &sh.fast);
     mbar_init(&sh.bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -435,8 +495,9 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
     s_w[tid][2] = __ldg(R.mods + (size_t)lm.p[first + tid] * kModStride);
   }
   __syncthreads();
-  const int nout = ext - cnt;
-  const TcCols cols = tc_cols(sh.n_narrow, nout - sh.n_narrow);
+  order_slots(slots, tmp, ext - cnt, sh);
+  const TcCols cols = tc_cols(sh.counts[0], sh.counts[1], sh.counts[2]);
+  if (cols.n_alloc > nrows_max) __trap();  // host masks disagree with the primes
   if (warp == 0) tmem_alloc(&sh.tmem, (uint32_t)cols.n_alloc);
   tc_build_b(B, kp, cols.n_alloc, slots, cols, cnt, [&](int u, int s) -> uint64_t {
     const TcSlot& S = slots[s];
@@ -445,7 +506,7 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
   });
   tc_after();
   const uint32_t tmem = sh.tmem;
-  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const bool fast = sh.fast;
 
   const int tpr = (int)(N / kTcRows);
@@ -453,21 +514,22 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
   uint64_t x[AMAX];
   auto load = [&](int tile) {
     const int bi = tile / tpr;
-    const size_t coef = (size_t)(tile % tpr) * kTcRows + tid;
+    const size_t coef = (size_t)(tile % tpr) * kTcRows + row;
     const uint64_t* src = in + (size_t)bi * in_bstride + (size_t)first * N + coef;
 #pragma unroll
-    for (int i = 0; i < AMAX; ++i) x[i] = i < cnt ? __ldcs(src + (size_t)i * N) : 0;
+    for (int i = 0; i < AMAX; ++i)  // this thread's 16-byte chunks: i/2 = sub (mod h)
+      x[i] = i < cnt && ((i >> 1) & (h - 1)) == sub ? __ldcs(src + (size_t)i * N) : 0;
   };
   if ((int)blockIdx.x < ntiles) load(blockIdx.x);
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int bi = tile / tpr;
-    const size_t coef = (size_t)(tile % tpr) * kTcRows + tid;
+    const size_t coef = (size_t)(tile % tpr) * kTcRows + row;
     uint64_t* obase = out + ((size_t)bi * item_rows + (size_t)j * out_rows) * N + coef;
     // A row: y_i as raw little-endian bytes, two values per 16-byte chunk
 #pragma unroll
     for (int c = 0; c < (8 * AMAX + 31) / 32 * 2; ++c) {
-      if (c < kp / 16) {
+      if (c < kp / 16 && (c & (h - 1)) == sub) {
         uint64_t y[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -478,7 +540,7 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
             if (!skip_own) obase[(size_t)(first + i) * N] = x[i];
           }
         }
-        *reinterpret_cast<ulonglong2*>(A + kmaj_off(tid, c, kp)) = make_ulonglong2(y[0], y[1]);
+        *reinterpret_cast<ulonglong2*>(A + kmaj_off(row, c, kp)) = make_ulonglong2(y[0], y[1]);
       }
     }
     fence_async_smem();
@@ -493,7 +555,7 @@ __global__ void __launch_bounds__(kTcThreads) k_modup_tc(
     mbar_wait(&sh.bar, phase);
     phase ^= 1;
     tc_after();
-    tc_epilogue(tl, cols, slots, obase, fast);
+    tc_epilogue(tl, cols, slots, obase, fast, sub, h);
     tc_before();
   }
   __syncthreads();
@@ -548,7 +610,7 @@ __device__ __noinline__ uint64_t exact_rho_tc(const uint64_t* __restrict__ src, 
 }
 
 template <int D1, int D2>
-__global__ void __launch_bounds__(kTcThreads) k_corr_tc(
+__global__ void __launch_bounds__(kTcMaxThreads) k_corr_tc(
     uint64_t* __restrict__ E, const uint64_t* __restrict__ T, int has_add, int polys, int limbs,
     int n1, int n2, int log_n, RingDev R, LimbMap lm, const uint64_t* __restrict__ tab1,
     const uint64_t* __restrict__ tab2, const uint64_t* __restrict__ tabE,
@@ -558,6 +620,7 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
   __shared__ uint64_t s_d[kTcMaxDrop][4];  // (P1/p_u)^-1, shoup, p_u, 1/p_u (bits)
   const size_t N = (size_t)1 << log_n;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int row = tid & (kTcRows - 1), sub = tid >> 7, h = blockDim.x >> 7;
   const int m1 = limbs - n1;
   const int m2 = m1 - n2;
   const int s1 = 2 * (n1 + 1), s2 = 2 * (n2 + 1), sE = 2 * (n1 + n2 + 1);
@@ -566,20 +629,19 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
   uint8_t* B = smem + kTcRows * kp;
   TcSlot* slots = reinterpret_cast<TcSlot*>(B + (size_t)nrows * kp);
   TcSlot* tmp = slots + m2;
-  if (tid == 0) {
-    for (int jj = 0; jj < m2; ++jj) {
-      load_slot(tmp[jj], R, lm.p[jj], jj, N);
-      // addc_j = -sum_d q_{li_d} Te_jd  (the shift making r2_d + q_{li_d} >= 0)
-      const Mod m{tmp[jj].p, tmp[jj].mu, tmp[jj].k, tmp[jj].two_p};
-      uint64_t a = 0;
-      for (int d = 0; d < n2; ++d) {
-        const uint64_t ql = __ldg(R.mods + (size_t)lm.p[m1 - 1 - d] * kModStride) % m.p;
-        const uint64_t te = __ldg(tabE + (size_t)jj * sE + 2 * (n1 + d)) % m.p;
-        a = ckb::add_mod(a, ckb::mul_mod(ql, te, m), m.p);
-      }
-      tmp[jj].addc = ckb::neg_mod(a, m.p);
+  for (int jj = tid; jj < m2; jj += blockDim.x) {  // one output slot per thread
+    load_slot(tmp[jj], R, lm.p[jj], jj, N);
+    // addc_j = -sum_d q_{li_d} Te_jd  (the shift making r2_d + q_{li_d} >= 0)
+    const Mod m{tmp[jj].p, tmp[jj].mu, tmp[jj].k, tmp[jj].two_p};
+    uint64_t a = 0;
+    for (int d = 0; d < n2; ++d) {
+      const uint64_t ql = __ldg(R.mods + (size_t)lm.p[m1 - 1 - d] * kModStride) % m.p;
+      const uint64_t te = __ldg(tabE + (size_t)jj * sE + 2 * (n1 + d)) % m.p;
+      a = ckb::add_mod(a, ckb::mul_mod(ql, te, m), m.p);
     }
-    order_slots(slots, tmp, m2, &sh.n_narrow, &sh.fast);
+    tmp[jj].addc = ckb::neg_mod(a, m.p);
+  }
+  if (tid == 0) {
     mbar_init(&sh.bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -591,7 +653,9 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
     s_d[tid][3] = (uint64_t)__double_as_longlong(1.0 / (double)p);
   }
   __syncthreads();
-  const TcCols cols = tc_cols(sh.n_narrow, m2 - sh.n_narrow);
+  order_slots(slots, tmp, m2, sh);
+  const TcCols cols = tc_cols(sh.counts[0], sh.counts[1], sh.counts[2]);
+  if (cols.n_alloc > nrows) __trap();  // host masks disagree with the primes
   if (warp == 0) tmem_alloc(&sh.tmem, (uint32_t)cols.n_alloc);
   tc_build_b(B, kp, cols.n_alloc, slots, cols, NVC, [&](int u, int s) -> uint64_t {
     const TcSlot& S = slots[s];
@@ -604,7 +668,7 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
   });
   tc_after();
   const uint32_t tmem = sh.tmem;
-  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const bool fast = sh.fast;
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   const int tpr = (int)(N / kTcRows);
@@ -612,18 +676,19 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
   uint64_t x[D1];
   auto load = [&](int tile) {
     const size_t pidx = tile / tpr;
-    const size_t n = (size_t)(tile % tpr) * kTcRows + tid;
+    const size_t n = (size_t)(tile % tpr) * kTcRows + row;
     const uint64_t* src = T + pidx * trows * N + n;
 #pragma unroll
     for (int u = 0; u < D1; ++u)
-      x[u] = u < n1 ? __ldcs(src + (size_t)(limbs - 1 - u - m2) * N) : 0;
+      x[u] = u < n1 && sub == 0 ? __ldcs(src + (size_t)(limbs - 1 - u - m2) * N) : 0;
   };
   if ((int)blockIdx.x < ntiles) load(blockIdx.x);
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t pidx = tile / tpr;
-    const size_t n = (size_t)(tile % tpr) * kTcRows + tid;
+    const size_t n = (size_t)(tile % tpr) * kTcRows + row;
     const uint64_t* src = T + pidx * trows * N + n;
+    if (sub == 0) {  // the row's values: one thread per row (rho and r2 need them all)
     uint64_t v[D1];
     double f = 0.0;
 #pragma unroll
@@ -681,7 +746,8 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
     for (int c = 0; c < (8 * NV + 31) / 32 * 2; ++c) {
       const uint64_t a0 = 2 * c < NV ? vals[2 * c < NV ? 2 * c : 0] : 0;
       const uint64_t a1 = 2 * c + 1 < NV ? vals[2 * c + 1 < NV ? 2 * c + 1 : 0] : 0;
-      *reinterpret_cast<ulonglong2*>(A + kmaj_off(tid, c, kp)) = make_ulonglong2(a0, a1);
+      *reinterpret_cast<ulonglong2*>(A + kmaj_off(row, c, kp)) = make_ulonglong2(a0, a1);
+    }
     }
     fence_async_smem();
     tc_before();
@@ -695,7 +761,7 @@ __global__ void __launch_bounds__(kTcThreads) k_corr_tc(
     mbar_wait(&sh.bar, phase);
     phase ^= 1;
     tc_after();
-    tc_epilogue(tl, cols, slots, E + pidx * m2 * N + n, fast);
+    tc_epilogue(tl, cols, slots, E + pidx * m2 * N + n, fast, sub, h);
     tc_before();
   }
   __syncthreads();
@@ -760,7 +826,7 @@ inline int tc_alloc_cols(int n) {
 // smem request that leaves room for exactly `ctas` resident CTAs per SM (so
 // every resident CTA's TMEM allocation fits the 512 columns)
 inline size_t tc_smem_request(size_t need, int n_alloc) {
-  const int ctas = std::max(1, std::min(4, 512 / n_alloc));
+  const int ctas = std::max(1, std::min(4, 512 / n_alloc));  // = tc_ctas
   return std::max(need, (size_t)(228 * 1024) / (ctas + 1));
 }
 
@@ -768,7 +834,16 @@ inline size_t tc_smem_request(size_t need, int n_alloc) {
 
 namespace ckb_internal {
 
-bool tc_wide(const RingDev& R, int pi) { return (R.wide_mask[pi >> 6] >> (pi & 63)) & 1; }
+// column class of prime index pi from the host-side masks (0 narrow, 1 mid, 2 wide)
+int tc_class(const RingDev& R, int pi) {
+  if ((R.wide_mask[pi >> 6] >> (pi & 63)) & 1) return 2;
+  if ((R.mid_mask[pi >> 6] >> (pi & 63)) & 1) return 1;
+  return 0;
+}
+
+// CTA shape: as many CTAs per SM as the 512 TMEM columns allow (<= 4), and
+// 16 warps per SM in every case (h warps share each TMEM lane quarter).
+inline int tc_ctas(int n_alloc) { return std::max(1, std::min(4, 512 / n_alloc)); }
 
 // returns 1 when not applicable (caller falls back), else the launch status
 int tc_modup(const RingDev& R, uint64_t* out, const uint64_t* in, size_t bstride, int batch,
@@ -779,12 +854,12 @@ int tc_modup(const RingDev& R, uint64_t* out, const uint64_t* in, size_t bstride
   int worst_rows = 0;
   for (int d = 0; d < nd; ++d) {
     const int first = d * alpha, cnt = std::min(alpha, limbs - first);
-    int nn = 0, nw = 0;
+    int n3[3] = {0, 0, 0};
     for (int e = 0; e < ext; ++e) {
       if (e >= first && e < first + cnt) continue;
-      (tc_wide(R, em.p[e]) ? nw : nn)++;
+      n3[tc_class(R, em.p[e])]++;
     }
-    const TcCols c = tc_cols(nn, nw);
+    const TcCols c = tc_cols(n3[0], n3[1], n3[2]);
     worst_rows = std::max(worst_rows, c.n_alloc);
   }
   if (worst_rows > 512) return 1;
@@ -792,14 +867,14 @@ int tc_modup(const RingDev& R, uint64_t* out, const uint64_t* in, size_t bstride
   const size_t need = (size_t)kTcRows * kp_max + (size_t)worst_rows * kp_max +
                       2 * (size_t)ext * sizeof(TcSlot);
   const size_t smem = tc_smem_request(need, worst_rows);
-  const int ctas = std::max(1, std::min(4, 512 / worst_rows));
+  const int ctas = tc_ctas(worst_rows);
   using K = decltype(&k_modup_tc<2>);
   K k = alpha <= 2 ? k_modup_tc<2> : alpha <= 4 ? k_modup_tc<4> : alpha <= 8 ? k_modup_tc<8>
       : alpha <= 12 ? k_modup_tc<12> : k_modup_tc<16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int ntiles = batch * (int)((1u << R.log_n) / kTcRows);
   const int gx = std::max(1, std::min(ntiles, (148 * ctas + nd - 1) / nd));
-  k<<<dim3((unsigned)gx, (unsigned)nd), kTcThreads, smem, st>>>(
+  k<<<dim3((unsigned)gx, (unsigned)nd), kTcThreads * (4 / ctas), smem, st>>>(
       out, in, bstride, batch, limbs, ext, alpha, out_rows, item_rows, skip_own, (int)R.log_n, R,
       lm, em, bconv, kp_max, worst_rows);
   return finish();
@@ -811,9 +886,9 @@ int tc_corr(const RingDev& R, uint64_t* E, const uint64_t* T, int has_add, int p
   if (!(R.flags & CKB_RING_TC) || R.log_n < 7 || !tabH || n1 < 1 || n1 > kTcMaxDrop || n2 > 2)
     return 1;
   const int m2 = limbs - n1 - n2;
-  int nn = 0, nw = 0;
-  for (int jj = 0; jj < m2; ++jj) (tc_wide(R, lm.p[jj]) ? nw : nn)++;
-  const TcCols c = tc_cols(nn, nw);
+  int n3[3] = {0, 0, 0};
+  for (int jj = 0; jj < m2; ++jj) n3[tc_class(R, lm.p[jj])]++;
+  const TcCols c = tc_cols(n3[0], n3[1], n3[2]);
   if (c.n_alloc > 512) return 1;
   const int d1 = n1 <= 6 ? 6 : n1 <= 8 ? 8 : n1 <= 11 ? 11 : n1 <= 13 ? 13 : 16;
   const int d2 = n2 == 0 ? 0 : n2 == 1 ? 1 : 2;
@@ -833,7 +908,7 @@ int tc_corr(const RingDev& R, uint64_t* E, const uint64_t* T, int has_add, int p
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int ntiles = polys * (int)((1u << R.log_n) / kTcRows);
   const int gx = std::max(1, std::min(ntiles, 148 * ctas));
-  k<<<gx, kTcThreads, smem, st>>>(E, T, has_add, polys, limbs, n1, n2, (int)R.log_n, R, lm, tab1,
+  k<<<gx, kTcThreads * (4 / ctas), smem, st>>>(E, T, has_add, polys, limbs, n1, n2, (int)R.log_n, R, lm, tab1,
                                   tab2, tabE, tabH, margin, kp, c.n_alloc);
   return finish();
 }

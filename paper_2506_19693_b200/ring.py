@@ -106,6 +106,7 @@ class GpuChain:
                                 self._ntt.data_ptr(), self._pair.data_ptr(),
                                 (nat.ctypes.c_uint64 * 2)(*nat.f64_mask(self.all_primes)))
         self.ring.wide_mask = (nat.ctypes.c_uint64 * 2)(*nat.wide_mask(self.all_primes))
+        self.ring.mid_mask = (nat.ctypes.c_uint64 * 2)(*nat.mid_mask(self.all_primes))
         if self.use_tc:
             self.ring.flags |= nat.RING_TC
         self.ring_p = nat.ctypes.pointer(self.ring)

@@ -59,6 +59,11 @@ def _case(case, n):
                               scale_bits=45, level=6, bootstrap_depth=2)
         return params, dict(prime_layout="bootstrap", dnum=3, secret_hw=64,
                             low_special=[(4, 4)])
+    if case == "c3_layout":  # config-3 chain: 45-bit (6 columns) and 60-bit (8) outputs,
+        # 256- and 512-column accumulators (2 and 1 CTAs per SM, 8 / 16 warps each)
+        params = SchemeParams(poly_degree=n, modulus_chain=(60,) + (45,) * 8 + (60,) * 16 + (660,),
+                              scale_bits=45, level=24, bootstrap_depth=16)
+        return params, dict(prime_layout="bootstrap", dnum=3, secret_hw=64)
     if case == "reference_layout":  # config-1 style chain: sub-2^31 primes, per-limb digits
         params = make_params(level=3, scale_bits=26, poly_degree=n, first_bits=40,
                              special_bits=200)
@@ -77,7 +82,7 @@ def _outputs(be, x, y, steps, lvl):
 
 
 @pytest.mark.parametrize("case", ["c2_L24", "c2_L12", "c2_L4", "c2_L23_short", "boot_low_p",
-                                  "reference_layout", "c2_L24_hps_exact"])
+                                  "c3_layout", "reference_layout", "c2_L24_hps_exact"])
 def test_tc_bit_identical_to_cuda_cores(case):
     n = 4096
     exact = case.endswith("_hps_exact")
@@ -115,3 +120,4 @@ def test_tc_default_on():
     ch = cust.backend.chain
     assert bool(ch.ring.flags & nat.RING_TC) == (os.environ.get("CKB_NO_TC") != "1")
     assert (ch.ring.wide_mask[0], ch.ring.wide_mask[1]) == nat.wide_mask(ch.all_primes)
+    assert (ch.ring.mid_mask[0], ch.ring.mid_mask[1]) == nat.mid_mask(ch.all_primes)
