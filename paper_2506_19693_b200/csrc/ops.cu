@@ -106,7 +106,16 @@ __global__ void k_scalar_mul(uint64_t* __restrict__ out, const uint64_t* __restr
   }
 }
 
-// Two coefficients per thread with 16-byte loads and stores (N >= 2).
+// a * b mod p on the FP64 pipe for p < 2^46 (canonical a, b): q = rint(a (b/p))
+// is within 1 of a b / p (relative error < 2^-51), so t = (a b - q p) is
+// formed exactly from h = fl(a b), l = a b - h and lies in (-1.5p, 1.5p).
+__device__ __forceinline__ double mulmod2_f64(double a, double b, double p, double pinv) {
+  return ckb_f64::mulmod_f64(a, b, b * pinv, p);
+}
+
+// Two coefficients per thread with 16-byte loads and stores (N >= 2).  Rows
+// whose prime is < 2^46 (warp-uniform: a warp covers 64 coefficients of one
+// row) multiply on the FP64 pipe, the others with Barrett products.
 __global__ void k_tensor2(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                           const uint64_t* __restrict__ b, size_t total, int log_n, int limbs,
                           RingDev R, LimbMap lm) {
@@ -114,23 +123,48 @@ __global__ void k_tensor2(uint64_t* __restrict__ out, const uint64_t* __restrict
   const size_t poly = (size_t)limbs * N;
   for (size_t i = 2 * (blockIdx.x * (size_t)blockDim.x + threadIdx.x); i < total;
        i += 2 * (size_t)gridDim.x * blockDim.x) {
-    const size_t bi = i / poly, off = i - bi * poly;
-    const int l = (int)(off >> log_n);
+    const unsigned row = (unsigned)(i >> log_n);
+    const unsigned bi = row / (unsigned)limbs;
+    const int l = (int)(row - bi * (unsigned)limbs);
+    const size_t off = i - (size_t)bi * poly;
     const Mod m = load_mod(R, lm.p[l]);
-    const uint64_t* pa = a + bi * 2 * poly + off;
-    const uint64_t* pb = b + bi * 2 * poly + off;
+    const uint64_t* pa = a + (size_t)bi * 2 * poly + off;
+    const uint64_t* pb = b + (size_t)bi * 2 * poly + off;
     const ulonglong2 a0 = __ldcs(reinterpret_cast<const ulonglong2*>(pa));
     const ulonglong2 a1 = __ldcs(reinterpret_cast<const ulonglong2*>(pa + poly));
     const ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2*>(pb));
     const ulonglong2 b1 = __ldcs(reinterpret_cast<const ulonglong2*>(pb + poly));
-    uint64_t* po = out + bi * 3 * poly + off;
+    uint64_t* po = out + (size_t)bi * 3 * poly + off;
     ulonglong2 d0, d1, d2;
-    d0.x = ckb::mul_mod(a0.x, b0.x, m);
-    d0.y = ckb::mul_mod(a0.y, b0.y, m);
-    d1.x = ckb::add_mod(ckb::mul_mod(a0.x, b1.x, m), ckb::mul_mod(a1.x, b0.x, m), m.p);
-    d1.y = ckb::add_mod(ckb::mul_mod(a0.y, b1.y, m), ckb::mul_mod(a1.y, b0.y, m), m.p);
-    d2.x = ckb::mul_mod(a1.x, b1.x, m);
-    d2.y = ckb::mul_mod(a1.y, b1.y, m);
+#ifndef CKB_TENSOR_NO_F64
+    if ((m.p >> 46) == 0) {
+      using namespace ckb_f64;
+      const double p = (double)m.p, pinv = 1.0 / p;
+      const double x0[2] = {u64_to_f64(a0.x), u64_to_f64(a0.y)};
+      const double x1[2] = {u64_to_f64(a1.x), u64_to_f64(a1.y)};
+      const double y0[2] = {u64_to_f64(b0.x), u64_to_f64(b0.y)};
+      const double y1[2] = {u64_to_f64(b1.x), u64_to_f64(b1.y)};
+      uint64_t r0[2], r1[2], r2[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        r0[c] = f64_to_u64(canon_f64(mulmod2_f64(x0[c], y0[c], p, pinv), p, pinv));
+        r1[c] = f64_to_u64(canon_f64(mulmod2_f64(x0[c], y1[c], p, pinv) +
+                                         mulmod2_f64(x1[c], y0[c], p, pinv), p, pinv));
+        r2[c] = f64_to_u64(canon_f64(mulmod2_f64(x1[c], y1[c], p, pinv), p, pinv));
+      }
+      d0 = make_ulonglong2(r0[0], r0[1]);
+      d1 = make_ulonglong2(r1[0], r1[1]);
+      d2 = make_ulonglong2(r2[0], r2[1]);
+    } else
+#endif
+    {
+      d0.x = ckb::mul_mod(a0.x, b0.x, m);
+      d0.y = ckb::mul_mod(a0.y, b0.y, m);
+      d1.x = ckb::add_mod(ckb::mul_mod(a0.x, b1.x, m), ckb::mul_mod(a1.x, b0.x, m), m.p);
+      d1.y = ckb::add_mod(ckb::mul_mod(a0.y, b1.y, m), ckb::mul_mod(a1.y, b0.y, m), m.p);
+      d2.x = ckb::mul_mod(a1.x, b1.x, m);
+      d2.y = ckb::mul_mod(a1.y, b1.y, m);
+    }
     *reinterpret_cast<ulonglong2*>(po) = d0;
     *reinterpret_cast<ulonglong2*>(po + poly) = d1;
     *reinterpret_cast<ulonglong2*>(po + 2 * poly) = d2;
