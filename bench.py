@@ -541,6 +541,30 @@ def alu_probe_gbfly(p: int, reps: int = 3, f64: bool = False) -> float:
     return best
 
 
+def tc_probe_gmacs(reps: int = 3) -> float:
+    """Measured u8 MAC rate (G MAC/s) of the tensor pipes: every SM issuing
+    back-to-back tcgen05.mma kind::i8 M=128 N=256 K=32 (ckb_tc_probe): the
+    roofline of the basis-conversion GEMMs (csrc/tc.cu)."""
+    import torch
+
+    from paper_2506_19693_b200 import _native as nat
+
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ctas, iters = sms * 2, 4000
+    nat.check(nat.LIB.ckb_tc_probe(ctas, 10, nat.ptr(sink), nat.stream_handle()), "tc_probe")
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        nat.check(nat.LIB.ckb_tc_probe(ctas, iters, nat.ptr(sink), nat.stream_handle()),
+                  "tc_probe")
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, ctas * iters * (1 << 20) / (a.elapsed_time(b) / 1e3) / 1e9)
+    return best
+
+
 def cpu_reference(L, args) -> dict:
     """The reference algorithm (oracle port, its own prime layout) on this
     host's cores: one HMult + one HRot of one ciphertext at N=2^16, L entries."""
@@ -554,51 +578,70 @@ def cpu_reference(L, args) -> dict:
             "seconds": secs, "sample": _cpu_sample_text(L, procs)}
 
 
-def pair_alu_floor(be, L, k, bsz, peak_int, peak_f64):
+def pair_alu_floor(be, L, k, bsz, peak_int, peak_f64, peak_tc=None):
     """Arithmetic floor of one HMult batch + one HRot batch (the headline pair):
     every modular multiply the algorithm needs — NTT butterflies (N/2 log N per
-    limb transform), ModUp terms (the digit's y_i and, per extended output, one
-    term per digit limb), inner-product MACs (2 per digit per ext limb), the
-    ModDown correction terms (y_u plus one per kept limb and dropped prime),
-    tensor products (4) and combine multiplies (2) — each charged to the FP64
-    (primes < 2^46) or integer (60-bit) pipe by its prime and timed at that
-    pipe's measured butterfly rate (ckb_alu_probe / ckb_alu_probe_f64; a
-    butterfly is one modular multiply plus an add and a subtract).  Memory
-    traffic is free in this model."""
+    limb transform), the ModUp premultiplies y_i, inner-product MACs (2 per
+    digit per ext limb), the ModDown y_u, tensor products (4) and combine
+    multiplies (2) — each charged to the FP64 (primes < 2^46) or integer
+    (60-bit) pipe by its prime and timed at that pipe's measured butterfly rate
+    (ckb_alu_probe / ckb_alu_probe_f64; a butterfly is one modular multiply
+    plus an add and a subtract).  The basis conversions (ModUp's per-output
+    sums over the digit, the ModDown correction's sums over the dropped primes)
+    run on the tensor cores when the chain sets CKB_RING_TC: their u8 MACs
+    (8 value bytes x 5 or 8 constant bytes per term) are timed at the measured
+    tensor-pipe rate (ckb_tc_probe) and their per-output reductions at the
+    integer rate; without the tensor cores every term is a CUDA-core modular
+    multiply.  Pipes are summed (no overlap credited); memory traffic is free."""
     n = 1 << N_LOG
     bf = n // 2 * N_LOG  # butterflies per limb transform
     alpha = -(-L // DNUM)
     nd = -(-L // alpha)
     m = L
     m2 = m - 1
-    f = i = 0  # modular multiplies charged to the FP64 / integer pipe, per item
+    tc = peak_tc is not None
+    nb = lambda wide: 8 if wide else 5  # noqa: E731  (config 2: 40-bit Q, 60-bit P)
+    acc = {"f": 0, "i": 0, "t": 0}
+
+    def modup():
+        for j in range(nd):
+            cnt = min(alpha, m - j * alpha)
+            acc["f"] += cnt * n + (m - cnt) * bf
+            acc["i"] += k * bf
+            if tc:
+                acc["t"] += n * cnt * 8 * ((m - cnt) * nb(False) + k * nb(True))
+                acc["i"] += (m - cnt + k) * n
+            else:
+                acc["f"] += (m - cnt) * cnt * n
+                acc["i"] += k * cnt * n
+        acc["f"] += 2 * nd * m * n          # inner product, Q limbs
+        acc["i"] += 2 * nd * k * n          # inner product, P limbs
+
+    def moddown(kept, n2):
+        acc["i"] += 2 * (k + n2) * bf + 2 * (k + n2) * n  # iNTT of dropped limbs, their y_u
+        if tc:
+            nvals = k + 1 + n2
+            acc["t"] += 2 * n * kept * nvals * 8 * nb(False)
+            acc["i"] += 2 * kept * n
+        else:
+            acc["f"] += 2 * kept * (k + n2) * n
+        acc["f"] += 2 * (kept * bf + 2 * kept * n)      # NTT of E, combine
+
     # HMult: tensor, iNTT(d2), ModUp, NTT(digits), inner product, ModDown + rescale
-    f += 4 * m * n + m * bf
-    for j in range(nd):
-        cnt = min(alpha, m - j * alpha)
-        f += cnt * n + (m - cnt) * (cnt * n + bf)
-        i += k * (cnt * n + bf)
-    f += 2 * nd * m * n
-    i += 2 * nd * k * n
-    i += 2 * (k + 1) * bf + 2 * (k + 1) * n       # iNTT of dropped limbs, their y_u
-    f += 2 * (m2 * (k + 1) * n + m2 * bf + 2 * m2 * n)
-    hm_f, hm_i = f, i
+    acc["f"] += 4 * m * n + m * bf
+    modup()
+    moddown(m2, 1)
     # HRot: automorphism (a permutation), iNTT(c1'), ModUp, NTT, MAC, ModDown
-    f = m * bf
-    i = 0
-    for j in range(nd):
-        cnt = min(alpha, m - j * alpha)
-        f += cnt * n + (m - cnt) * (cnt * n + bf)
-        i += k * (cnt * n + bf)
-    f += 2 * nd * m * n
-    i += 2 * nd * k * n
-    i += 2 * k * bf + 2 * k * n
-    f += 2 * (m * k * n + m * bf + 2 * m * n)
-    tot_f = bsz * (hm_f + f) / 1e9
-    tot_i = bsz * (hm_i + i) / 1e9
-    floor_s = tot_f / peak_f64 + tot_i / peak_int
-    return {"gmulmod_f64": tot_f, "gmulmod_int": tot_i, "floor_ms": 1e3 * floor_s,
-            "peak_int_gbfly": peak_int, "peak_f64_gbfly": peak_f64}
+    acc["f"] += m * bf
+    modup()
+    moddown(m, 0)
+    tot_f = bsz * acc["f"] / 1e9
+    tot_i = bsz * acc["i"] / 1e9
+    tot_t = bsz * acc["t"] / 1e9
+    floor_s = tot_f / peak_f64 + tot_i / peak_int + (tot_t / peak_tc if tc else 0.0)
+    return {"gmulmod_f64": tot_f, "gmulmod_int": tot_i, "gmac_u8_tensor": tot_t,
+            "floor_ms": 1e3 * floor_s, "peak_int_gbfly": peak_int, "peak_f64_gbfly": peak_f64,
+            "peak_tc_gmacs": peak_tc, "tensor_cores": tc}
 
 
 def run_c2(L, bsz, args, rank, world, local, breakdown=False, keep=False) -> dict:
@@ -765,7 +808,11 @@ def run_c2(L, bsz, args, rank, world, local, breakdown=False, keep=False) -> dic
                 "peak_source": "ckb_alu_probe / ckb_alu_probe_f64 (register-resident "
                                "butterflies, the NTT's own integer and FP64 arithmetic), "
                                "weighted by this kernel's row mix"}
-        fl = pair_alu_floor(be, L, k, bsz, peak_int, peak_f64)
+        from paper_2506_19693_b200 import _native as nat_
+
+        use_tc = bool(be.chain.ring.flags & nat_.RING_TC)
+        fl = pair_alu_floor(be, L, k, bsz, peak_int, peak_f64,
+                            tc_probe_gmacs() if use_tc else None)
         seq_ms = st_ms["hmult"] + st_ms["hrot"]
         out["pair_roofline"] = {
             "alu_floor_ms": fl["floor_ms"], "hbm_floor_ms": 1e3 * (hm_b + hr_b) / peak / 1e9,

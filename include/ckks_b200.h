@@ -89,6 +89,12 @@ typedef struct {
  * [16, 256].  Device pointers. */
 int ckb_tc_selftest(const uint8_t* A, const uint8_t* B, int32_t* D, int k, int n, void* stream);
 
+/* Tensor-pipe ceiling probe (measurement): `ctas` CTAs each issue `iters`
+ * back-to-back tcgen05.mma kind::i8 M=128 N=256 K=32 (2^20 u8 MACs each);
+ * time it on `stream` for the int8 MAC/s roofline of the basis conversions.
+ * sink: one device int32 (kept live, normally untouched). */
+int ckb_tc_probe(int ctas, int iters, int32_t* sink, void* stream);
+
 /* Library version (for load checks). */
 int ckb_version(void);
 

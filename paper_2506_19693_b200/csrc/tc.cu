@@ -817,6 +817,42 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_selftest(const uint8_t* __res
   if (warp == 0) tmem_free(tmem, (uint32_t)n_alloc);
 }
 
+// Tensor-pipe ceiling probe: each CTA issues `iters` back-to-back
+// M=128 x N=256 x K=32 u8 MMAs (1 Mi MACs each) into one TMEM accumulator.
+__global__ void __launch_bounds__(128) k_tc_probe(int iters, int32_t* __restrict__ sink) {
+  __shared__ __align__(1024) uint8_t A[128 * 32];
+  __shared__ __align__(1024) uint8_t B[256 * 32];
+  __shared__ TcShared sh;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int q = tid; q < 128 * 32; q += blockDim.x) A[q] = (uint8_t)(q * 7 + blockIdx.x);
+  for (int q = tid; q < 256 * 32; q += blockDim.x) B[q] = (uint8_t)(q * 13);
+  if (tid == 0) {
+    mbar_init(&sh.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (warp == 0) tmem_alloc(&sh.tmem, 256);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sh.tmem;
+  if (tid == 0) {
+    const uint64_t ad = sdesc(su32(A), 128, 32 * 8), bd = sdesc(su32(B), 128, 32 * 8);
+    for (int it = 0; it < iters; ++it) mma_u8(tmem, ad, bd, idesc_u8(128, 256), it > 0);
+    mma_commit(&sh.bar);
+  }
+  mbar_wait(&sh.bar, 0);
+  tc_after();
+  uint32_t v[8];
+  tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16), v);
+  tmem_wait<8>(v);
+  if (v[0] == 0x7fffffffu) sink[0] = (int32_t)v[1];  // keep the result live
+  tc_before();
+  __syncthreads();
+  if (warp == 0) tmem_free(tmem, 256);
+}
+
 inline int tc_alloc_cols(int n) {
   int a = 32;
   while (a < n) a <<= 1;
@@ -914,6 +950,12 @@ int tc_corr(const RingDev& R, uint64_t* E, const uint64_t* T, int has_add, int p
 }
 
 }  // namespace ckb_internal
+
+extern "C" int ckb_tc_probe(int ctas, int iters, int32_t* sink, void* stream) {
+  if (ctas < 1 || iters < 1 || !sink) return CKB_E_ARG;
+  k_tc_probe<<<ctas, 128, 0, (cudaStream_t)stream>>>(iters, sink);
+  return finish();
+}
 
 extern "C" int ckb_tc_selftest(const uint8_t* A, const uint8_t* B, int32_t* D, int k, int n,
                                void* stream) {
