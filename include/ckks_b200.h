@@ -195,7 +195,9 @@ int ckb_tensor(const ckb_ring* ring, uint64_t* out, const uint64_t* a, const uin
  * its item; a short last digit (limbs % alpha != 0) therefore has more rows and
  * an item holds (digits-1)*(ext_limbs-alpha) + ext_limbs - width_last rows.  The
  * skipped limbs' NTT is the NTT-domain input itself, which ckb_ks_inner reads
- * directly. */
+ * directly.  With CKB_RING_TC (alpha > 1, N >= 128) the per-output sums run on
+ * the tensor cores (tcgen05.mma kind::i8, byte-sliced; csrc/tc.cu), same
+ * integers. */
 int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_batch_stride,
               int batch, int limbs, const int32_t* limb_prime, int ext_limbs,
               const int32_t* ext_prime, int alpha, const uint64_t* bconv, int skip_own,
@@ -253,7 +255,9 @@ int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_
  * last limb).  The first chain's centred residue then comes from one fast
  * basis conversion, c1 = sum_u y_u (P1/p_u) - rho P1 with rho = round(sum y_u/p_u)
  * in FP64; coefficients whose rounding is within 2^-30 of ambiguous take the
- * mixed-radix path, so E is bit-identical either way. */
+ * mixed-radix path, so E is bit-identical either way.  With CKB_RING_TC the
+ * fast-conversion form's sums over the dropped primes (and rho, r2) run as
+ * one u8 GEMM on the tensor cores (csrc/tc.cu), same integers. */
 /* (ckb_ring.flags & CKB_RING_HPS_EXACT sends every coefficient through the
  * exact path; default margin |frac - 1/2| < 2^-30.) */
 int ckb_divround_ntt_corr(const ckb_ring* ring, uint64_t* E, const uint64_t* T, int has_addend,

@@ -3,8 +3,9 @@
 //
 // Every kernel replaces one numpy routine of the reference CKKS backend
 // (/root/reference/pkg/src/ciphermlp/ckks/*.py); see the header for the map.
-// The work is 64-bit modular integer arithmetic: HBM- or IMAD-bound, never a
-// GEMM, so there are no tensor-core paths here.
+// The work is 64-bit modular integer arithmetic (IMAD / FP64 pipes); the one
+// GEMM-shaped contraction, the basis conversion of ModUp and of the ModDown
+// correction, runs on the tensor cores as a byte-sliced u8 GEMM (tc.cu).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
