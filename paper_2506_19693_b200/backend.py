@@ -524,7 +524,7 @@ class B200CkksCore:
                     c = qhat % p
                     tab[j, i, 2 + 2 * e] = c
                     tab[j, i, 3 + 2 * e] = shoup(c, p)
-        t = self.chain.publish(torch.from_numpy(tab.reshape(-1)).to(self.device))
+        t = self.chain.upload_table(tab.reshape(-1))
         self._bconv_cache[(m, k)] = t
         return t
 
@@ -860,7 +860,7 @@ class B200CkksCore:
             e_np[i] = np.rint(rng.normal(0.0, ERROR_SIGMA, self.n)).astype(np.int64)
         out = torch.empty(bsz, 2, m, self.n, dtype=U64, device=self.device)
         out[:, 1].copy_(torch.from_numpy(a_np))
-        me = ch.from_i64(torch.from_numpy(e_np).to(self.device), m)  # [B, m, N]
+        me = ch.from_i64(_h2d(e_np, self.device), m)  # [B, m, N]
         return self._finish_encrypt(out, me, msgs, m)
 
     def encryption_seeds(self, serials) -> np.ndarray:
@@ -1127,10 +1127,9 @@ class B200CkksCore:
             two_n = 2 * self.n
             gal = [self.galois_for_step.get(s % slots, pow(5, s % slots, two_n)) for s in key]
             keys = [self.rotation_key(g) for g in gal]
-            g_items = torch.tensor(gal, dtype=torch.int64, device=self.device).view(U64)
-            ptrs = torch.tensor([k.data.data_ptr() for k in keys], dtype=torch.int64,
-                                device=self.device)
-            self.chain.publish(ptrs)
+            g_items = self.chain.upload_table(np.array(gal, dtype=np.int64)).view(U64)
+            ptrs = self.chain.upload_table(np.array([k.data.data_ptr() for k in keys],
+                                                    dtype=np.int64))
             cache[key] = (g_items, ptrs, keys)
         return cache[key]
 

@@ -660,6 +660,37 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
 #else
       ulonglong2 v = *reinterpret_cast<const ulonglong2*>(xr + off);
 #endif
+#ifndef CKB_COMBINE_INT
+      if (f64) {  // the combine on the FP64 pipe (exact; same integers)
+        const double pd = (double)p, pinv = 1.0 / pd;
+        double c[2] = {u64_to_f64(v.x), u64_to_f64(v.y)};
+        const double ev[2] = {u64_to_f64(e0), u64_to_f64(e1)};
+        const double a1d = u64_to_f64(a1), b2d = u64_to_f64(b2);
+        ulonglong2 a = make_ulonglong2(0, 0), w2 = make_ulonglong2(0, 0);
+        if (ar) {
+#ifndef CKB_NO_COMBINE_PREFETCH
+          a = prefetch ? *reinterpret_cast<const ulonglong2*>(pf + 2 * ((size_t)(E / 2 + i) * T + tid))
+                       : *reinterpret_cast<const ulonglong2*>(ar + off);
+#else
+          a = *reinterpret_cast<const ulonglong2*>(ar + off);
+#endif
+        }
+        if (pr) w2 = *reinterpret_cast<const ulonglong2*>(pr + off);
+        const double av[2] = {u64_to_f64(a.x), u64_to_f64(a.y)};
+        const double wv[2] = {u64_to_f64(w2.x), u64_to_f64(w2.y)};
+        uint64_t o[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double t = ep.n1 ? mulmod_f64(c[h], a1d, a1d * pinv, pd) : c[h];  // |t| < 1.5p
+          t = t + av[h] - ev[h];                                            // |t| < 3.5p
+          if (ep.n2) t = mulmod_f64(t, b2d, b2d * pinv, pd);                // |t| < 1.5p
+          t += wv[h];
+          o[h] = f64_to_u64(canon_f64(t, pd, pinv));
+        }
+        *reinterpret_cast<ulonglong2*>(orow + off) = make_ulonglong2(o[0], o[1]);
+        continue;
+      }
+#endif
       if (ep.n1) {
         v.x = ckb::mul_shoup(v.x, a1, a1s, p);
         v.y = ckb::mul_shoup(v.y, a1, a1s, p);

@@ -177,11 +177,34 @@ class GpuChain:
         return nat.u64_array(vals)
 
     def publish(self, t: torch.Tensor) -> torch.Tensor:
-        """A lazily built, cached device table: wait once for it to be complete
-        so groups issued on other streams (executor fork/join) can read it."""
+        """A lazily built, cached device table computed ON THE DEVICE: wait once
+        for it to be complete so groups issued on other streams (executor
+        fork/join, bootstrap side streams) can read it.  Host-built tables go
+        through upload_table instead, which does not drain the queue."""
         if t is not None and t.is_cuda:
             torch.cuda.current_stream(t.device).synchronize()
         return t
+
+    _upload_stream = None
+
+    def upload_table(self, arr: np.ndarray) -> torch.Tensor:
+        """Host-built constant table -> device, complete on return, WITHOUT
+        waiting for the compute work queued on the current stream: staged in
+        pinned memory and copied on a private side stream, whose copy alone the
+        host waits for (a pageable .to(device) or a current-stream sync would
+        drain the GPU's queue at every first use of a table: ~1.4 s of idle GPU
+        in a config-5 step).  Complete before any later launch on any stream."""
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if self.device.type != "cuda":
+            return t.to(self.device)
+        if GpuChain._upload_stream is None:
+            GpuChain._upload_stream = torch.cuda.Stream(device=self.device)
+        st = GpuChain._upload_stream
+        pinned = t.pin_memory()
+        with torch.cuda.stream(st):
+            out = pinned.to(self.device, non_blocking=True)
+        st.synchronize()
+        return out
 
     def _drop_chain_table(self, basis: tuple, n_drop: int) -> torch.Tensor:
         """Mixed-radix constants for dropping the last n_drop limbs of basis
@@ -203,15 +226,14 @@ class GpuChain:
             mt = math.prod(drops[:t]) % p
             inv = pow(mt, -1, p)
             tab[j, n_drop] = (inv, shoup(inv, p))
-        return torch.from_numpy(tab.reshape(-1)).to(self.device)
+        return self.upload_table(tab.reshape(-1))
 
     def drop_tables(self, basis: tuple, n1: int, n2: int):
         key = ("drop", basis, n1, n2)
         hit = self._maps.get(key)
         if hit is None:
-            t1 = self.publish(self._drop_chain_table(basis, n1) if n1 else None)
-            t2 = self.publish(self._drop_chain_table(basis[: len(basis) - n1], n2)
-                              if n2 else None)
+            t1 = self._drop_chain_table(basis, n1) if n1 else None
+            t2 = self._drop_chain_table(basis[: len(basis) - n1], n2) if n2 else None
             hit = self._maps[key] = (t1, t2)
         return hit
 
@@ -302,7 +324,7 @@ class GpuChain:
         scalar_mac; build once and reuse (no upload inside graph captures)."""
         tab = np.array([[int(a) % self.all_primes[j] for j in range(limbs)] for a in scalars],
                        dtype=np.uint64)
-        return self.publish(torch.from_numpy(tab.reshape(-1)).to(self.device))
+        return self.upload_table(tab.reshape(-1))
 
     def scalar_mac(self, terms, sc: torch.Tensor, limbs: int, out=None):
         """sum_k a_k * terms[k] (ckb_scalar_mac): terms are ciphertext tensors
@@ -484,7 +506,7 @@ class GpuChain:
             for u in range(n2):
                 c = math.prod(d2[:u]) % p
                 tab[j, n1 + u] = (c, shoup(c, p))
-        return torch.from_numpy(tab.reshape(-1)).to(self.device)
+        return self.upload_table(tab.reshape(-1))
 
     HPS_MIN_DROP = 6  # csrc/ops.cu kHpsMinDrop
 
@@ -506,7 +528,7 @@ class GpuChain:
             w = pow((P1 // p) % p, -1, p)
             tab[m1 * n1 + 2 * u] = w
             tab[m1 * n1 + 2 * u + 1] = shoup(w, p)
-        return torch.from_numpy(tab).to(self.device)
+        return self.upload_table(tab)
 
     def hps_table(self, basis: tuple, n1: int, n2: int):
         if n1 < self.HPS_MIN_DROP or n2 > 2:
@@ -514,14 +536,14 @@ class GpuChain:
         key = ("hps", basis, n1)
         hit = self._maps.get(key)
         if hit is None:
-            hit = self._maps[key] = self.publish(self._hps_table(basis, n1))
+            hit = self._maps[key] = self._hps_table(basis, n1)
         return hit
 
     def corr_table(self, basis: tuple, n1: int, n2: int) -> torch.Tensor:
         key = ("corr", basis, n1, n2)
         hit = self._maps.get(key)
         if hit is None:
-            hit = self._maps[key] = self.publish(self._corr_table(basis, n1, n2))
+            hit = self._maps[key] = self._corr_table(basis, n1, n2)
         return hit
 
     def divround_ntt(self, x, polys: int, limbs: int, n1: int, n2: int = 0, *,
@@ -654,4 +676,4 @@ class GpuChain:
 
     # -- host <-> device helpers -------------------------------------------------------
     def upload_u64(self, arr: np.ndarray) -> torch.Tensor:
-        return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint64)).to(self.device)
+        return self.upload_table(np.ascontiguousarray(arr, dtype=np.uint64))

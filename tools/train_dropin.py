@@ -178,6 +178,7 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
                 prof.disable()
                 pstats.Stats(prof).sort_stats("tottime").print_stats(30)
                 pstats.Stats(prof).sort_stats("cumulative").print_stats(40)
+                pstats.Stats(prof).sort_stats("tottime").print_callers(8)
             snaps.append([(b.layer_weights, b.classifier_weights, b.layer_velocity,
                            b.classifier_velocity) for b in model.blocks])
         torch.cuda.synchronize()
