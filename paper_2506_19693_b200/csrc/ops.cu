@@ -602,9 +602,9 @@ __global__ void __launch_bounds__(256) k_ks_inner(
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t n = (t & ((N >> 1) - 1)) * 2;
-    const size_t be = t >> lh;
-    const int e = (int)(be % ext);
-    const size_t bi = be / ext;
+    const unsigned be = (unsigned)(t >> lh);
+    const int e = (int)(be % (unsigned)ext);
+    const size_t bi = be / (unsigned)ext;
     const uint64_t* K = key_ptrs ? key_ptrs[bi] : key;
     const uint64_t* kb = K + (size_t)km.p[e] * N + n;
     const uint64_t* ka = kb + (size_t)key_limbs * N;
@@ -621,6 +621,30 @@ __global__ void __launch_bounds__(256) k_ks_inner(
       b[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + j * krow));
       a[j] = __ldg(reinterpret_cast<const ulonglong2*>(ka + j * krow));
     }
+    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
+    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
+    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    ulonglong2 ob, oa;
+#ifndef CKB_KSS_INT
+    if ((m.p >> 46) == 0) {  // warp-uniform: the FP64 pipe, exact products
+      using namespace ckb_f64;
+      const double pd = (double)m.p, pinv = 1.0 / pd;
+      double sb0 = 0, sb1 = 0, sa0 = 0, sa1 = 0;
+#pragma unroll
+      for (int j = 0; j < ND; ++j) {
+        const double x0 = u64_to_f64(x[j].x), x1 = u64_to_f64(x[j].y);
+        const double b0 = u64_to_f64(b[j].x), b1 = u64_to_f64(b[j].y);
+        const double a0 = u64_to_f64(a[j].x), a1 = u64_to_f64(a[j].y);
+        sb0 += mulmod_f64(x0, b0, b0 * pinv, pd);
+        sb1 += mulmod_f64(x1, b1, b1 * pinv, pd);
+        sa0 += mulmod_f64(x0, a0, a0 * pinv, pd);
+        sa1 += mulmod_f64(x1, a1, a1 * pinv, pd);
+      }
+      ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
+      oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
+    } else
+#endif
+    {
     uint64_t hb0 = 0, lb0 = 0, ha0 = 0, la0 = 0, hb1 = 0, lb1 = 0, ha1 = 0, la1 = 0;
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
@@ -629,10 +653,6 @@ __global__ void __launch_bounds__(256) k_ks_inner(
       ckb::mac128(hb1, lb1, x[j].y, b[j].y);
       ckb::mac128(ha1, la1, x[j].y, a[j].y);
     }
-    const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
-    const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
-    const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
-    ulonglong2 ob, oa;
     if (m.k >= 32) {
       ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
                            ckb::reduce128_big(hb1, lb1, r64, r64s, m));
@@ -643,6 +663,7 @@ __global__ void __launch_bounds__(256) k_ks_inner(
                            ckb::reduce128_any(hb1, lb1, r64, r64s, m));
       oa = make_ulonglong2(ckb::reduce128_any(ha0, la0, r64, r64s, m),
                            ckb::reduce128_any(ha1, la1, r64, r64s, m));
+    }
     }
     uint64_t* o = acc + (bi * 2 * ext + e) * N + n;
     *reinterpret_cast<ulonglong2*>(o) = ob;
@@ -707,6 +728,27 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
 #ifndef CKB_KSS_NO_PREFETCH
       if (bi + 1 < batch) load_item(bi + 1, xn);  // next item's loads in flight during this MAC
 #endif
+      ulonglong2 ob, oa;
+#ifndef CKB_KSS_INT
+      if ((m.p >> 46) == 0) {  // warp-uniform: the FP64 pipe, exact products
+        using namespace ckb_f64;
+        const double pd = (double)m.p, pinv = 1.0 / pd;
+        double sb0 = 0, sb1 = 0, sa0 = 0, sa1 = 0;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+          const double x0 = u64_to_f64(x[j].x), x1 = u64_to_f64(x[j].y);
+          const double b0 = u64_to_f64(b[j].x), b1 = u64_to_f64(b[j].y);
+          const double a0 = u64_to_f64(a[j].x), a1 = u64_to_f64(a[j].y);
+          sb0 += mulmod_f64(x0, b0, b0 * pinv, pd);
+          sb1 += mulmod_f64(x1, b1, b1 * pinv, pd);
+          sa0 += mulmod_f64(x0, a0, a0 * pinv, pd);
+          sa1 += mulmod_f64(x1, a1, a1 * pinv, pd);
+        }
+        ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
+        oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
+      } else
+#endif
+      {
       uint64_t hb0 = 0, lb0 = 0, ha0 = 0, la0 = 0, hb1 = 0, lb1 = 0, ha1 = 0, la1 = 0;
 #pragma unroll
       for (int j = 0; j < ND; ++j) {
@@ -715,7 +757,6 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
         ckb::mac128(hb1, lb1, x[j].y, b[j].y);
         ckb::mac128(ha1, la1, x[j].y, a[j].y);
       }
-      ulonglong2 ob, oa;
       if (m.k >= 32) {
         ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
                              ckb::reduce128_big(hb1, lb1, r64, r64s, m));
@@ -726,6 +767,7 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
                              ckb::reduce128_any(hb1, lb1, r64, r64s, m));
         oa = make_ulonglong2(ckb::reduce128_any(ha0, la0, r64, r64s, m),
                              ckb::reduce128_any(ha1, la1, r64, r64s, m));
+      }
       }
       uint64_t* o = acc + ((size_t)bi * 2 * ext + e) * N + n;
       __stcs(reinterpret_cast<ulonglong2*>(o), ob);
