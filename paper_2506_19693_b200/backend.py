@@ -261,7 +261,8 @@ class B200CkksCore:
                  secret_hw=None, device=None, encode_cache: int = 512,
                  conjugation_key: bool = False, real_bootstrap: bool = False,
                  sampler: str = None, low_special=None, encoder: str = "device",
-                 deferred: bool = False, deferred_max_group: int = None):
+                 deferred: bool = False, deferred_max_group: int = None,
+                 deferred_async: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 CKKS backend needs a CUDA device; there is no CPU path")
         if keyset_id is None:
@@ -394,12 +395,21 @@ class B200CkksCore:
         if deferred:
             from .deferred import Recorder
 
-            self._rec = Recorder(self, max_group=deferred_max_group)
+            self._rec = Recorder(self, max_group=deferred_max_group, pipelined=deferred_async)
 
-    def flush(self) -> None:
-        """Run every deferred HE call recorded so far (no-op when eager)."""
+    def flush(self, on_issued=None) -> None:
+        """Run every deferred HE call recorded so far (no-op when eager).  With
+        deferred_async the program is handed to the issuing thread and this
+        returns at once; on_issued() runs right after its last launch."""
         if self._rec is not None:
-            self._rec.flush()
+            self._rec.flush(on_issued=on_issued)
+        elif on_issued is not None:
+            on_issued()
+
+    def wait(self) -> None:
+        """Join pipelined deferred programs (no-op otherwise)."""
+        if self._rec is not None:
+            self._rec.wait()
 
     # ------------------------------------------------------------------ keys
     AUTO_TIER_MARGIN_BITS = 0  # the same rule __init__ checks explicit tiers with

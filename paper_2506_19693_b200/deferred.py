@@ -18,10 +18,21 @@ refreshes keep program order (their eps draws), and integer ops are exact, so
 the batched results equal sequential ones (tests/test_gpu_dropin.py).  The
 level / depth / keyset checks of the HE API still run at call time in the
 base class; only the arithmetic is deferred.
+
+Pipelined flushes (``deferred_async=True``): ``flush()`` hands the recorded
+program to one worker thread that plans it and issues its launches, and
+returns at once, so the layer code records step t+1 while step t's kernels
+are still being issued and run (the launch queue holds well under one step of
+a bootstrapped training configuration, so a synchronous flush leaves the GPU
+idle for the whole recording of the next step).  Programs run in flush order;
+a value from a pending program is an *input* of the next one, read when that
+program starts.  ``resolve`` (decrypt / serialize) and ``wait()`` join the
+worker.  The live RNG serial counter belongs to the recording thread only.
 """
 
 from __future__ import annotations
 
+import concurrent.futures
 import itertools
 import types
 import weakref
@@ -75,10 +86,14 @@ def _inputs(op):
 class Recorder:
     """Per-backend recording state."""
 
-    def __init__(self, backend, max_ops: int = 250_000, max_group: int = None):
+    def __init__(self, backend, max_ops: int = 250_000, max_group: int = None,
+                 pipelined: bool = False):
         self.be = backend
         self.max_ops = max_ops
         self.max_group = max_group  # WaveExecutor sub-batch bound (peak memory)
+        self.pipelined = pipelined
+        self._worker = None
+        self._pending = []
         self._ids = itertools.count()
         self._reset()
 
@@ -96,7 +111,10 @@ class Recorder:
         if isinstance(payload, LazyPayload):
             if payload.value is not None:  # ran in an earlier flush
                 payload = payload.value
-            else:
+            elif payload.vid in self.lazy:  # recorded in this program
+                return payload.vid
+            else:  # produced by a pending (pipelined) program: an input, read at run time
+                self.inputs[payload.vid] = payload
                 return payload.vid
         key = id(payload)
         vid = self.input_of.get(key)
@@ -132,26 +150,81 @@ class Recorder:
         return out
 
     # -- execution --------------------------------------------------------------
-    def flush(self) -> None:
+    def flush(self, on_issued=None) -> None:
+        """Run (pipelined: submit) everything recorded so far.  on_issued(): called
+        on the issuing thread right after the program's last launch (e.g. to
+        record a CUDA event at a training-step boundary)."""
         if not self.ops:
+            if on_issued is not None:
+                if self.pipelined and self._pending:
+                    self._submit(on_issued)
+                else:
+                    on_issued()
             return
+        snap = (self.ops, self.serials, self.inputs, dict(self.lazy),
+                np.stack(self.pt_rows) if self.pt_rows else np.zeros((0, 1)))
+        self._reset()
+        if not self.pipelined:
+            self._run(snap, restore_serials=True)
+            if on_issued is not None:
+                on_issued()
+            return
+
+        def job():
+            self._run(snap, restore_serials=False)
+            if on_issued is not None:
+                on_issued()
+
+        self._submit(job)
+
+    def _submit(self, fn) -> None:
+        if self._worker is None:
+            self._worker = concurrent.futures.ThreadPoolExecutor(
+                max_workers=1, thread_name_prefix="ckb-flush")
+        dev = getattr(self.be, "device", None)
+
+        def job():
+            import torch
+
+            if dev is not None and torch.device(dev).type == "cuda":
+                torch.cuda.set_device(dev)  # the recording thread's device (one per rank)
+            fn()
+
+        self._pending.append(self._worker.submit(job))
+
+    def wait(self) -> None:
+        """Join every pending pipelined program (re-raises its error)."""
+        pending, self._pending = self._pending, []
+        for f in pending:
+            f.result()
+
+    def _run(self, snap, restore_serials: bool) -> None:
         from .executor import WaveExecutor
 
         be = self.be
-        ops, serials, inputs = self.ops, self.serials, self.inputs
-        live = dict(self.lazy)  # vid -> LazyPayload still referenced by the caller
-        pts = np.stack(self.pt_rows) if self.pt_rows else np.zeros((0, 1))
-        self._reset()
+        ops, serials, inputs, live, pts = snap
+        # values of earlier (pipelined) programs have been produced by now:
+        # programs run in flush order on one thread
+        vals = {}
+        for k, v in inputs.items():
+            if isinstance(v, LazyPayload):
+                if v.value is None:
+                    raise RuntimeError("deferred input was not produced by an earlier program")
+                v = v.value
+            vals[k] = v
         prog = _Program(ops, pts, [v for v in live if v not in inputs])
         view = types.SimpleNamespace(backend=be)
         ex = WaveExecutor(prog, view, max_group=self.max_group,
-                          inputs={k: v.level for k, v in inputs.items()})
+                          inputs={k: v.level for k, v in vals.items()})
         ex.serial_of = dict(serials)
-        saved = be._serials
-        try:
-            env = ex.run(dict(inputs))
-        finally:
-            be._serials = saved  # the live counter already advanced at record time
+        if restore_serials:
+            saved = be._serials
+            try:
+                env = ex.run(dict(vals))
+            finally:
+                be._serials = saved  # the live counter already advanced at record time
+        else:  # the recording thread owns the live counter: leave it alone
+            env = ex.run(dict(vals), update_serials=False)
         for vid, lp in live.items():
             val = env.get(vid)
             if val is not None:
@@ -161,6 +234,7 @@ class Recorder:
         if isinstance(payload, LazyPayload):
             if payload.value is None:
                 self.flush()
+                self.wait()
             if payload.value is None:
                 raise RuntimeError("deferred value was not produced by its program")
             return payload.value

@@ -212,7 +212,8 @@ class WaveExecutor:
         self.fused_adds = set(self.fuse.values())
 
     # -- execution -----------------------------------------------------------
-    def run(self, env=None, only_after_setup: bool = False, defer_refresh: bool = False) -> dict:
+    def run(self, env=None, only_after_setup: bool = False, defer_refresh: bool = False,
+            update_serials: bool = True) -> dict:
         """Execute the program; returns id -> GpuCiphertext for live values.
         With only_after_setup, ops before program.n_setup must already be in env.
         defer_refresh: debug refreshes (a host round trip each) are not run but
@@ -281,9 +282,11 @@ class WaveExecutor:
                     if last.get(ref) == i and ref not in keep:
                         env.pop(ref, None)
         # leave the backend's serial counter where sequential execution would
-        import itertools
+        # (not for a pipelined deferred program: the recording thread owns it)
+        if update_serials:
+            import itertools
 
-        be._serials = itertools.count(self.serials_used + self.serial_offset)
+            be._serials = itertools.count(self.serials_used + self.serial_offset)
         return env
 
     def finish_deferred(self, env: dict) -> dict:

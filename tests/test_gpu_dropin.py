@@ -139,3 +139,36 @@ def test_deferred_errors_surface_at_call_time(installed):
         cust.evaluator.mul(x, ct)
     got = cust.decrypt(cust.evaluator.rotate(ct, 1)).values
     assert np.max(np.abs(got - np.roll(v, -1))) < 1e-6
+
+
+@needs[0]
+@needs[1]
+def test_c1_step_mode_a_pipelined_flush_byte_identical(installed, golden_dir):
+    """deferred_async=True (pipelined flushes, deferred.py): the program is
+    planned and issued on the worker thread while the caller goes on; the
+    step's bytes equal the reference's, and two steps recorded back to back
+    (step 2 reading step 1's pending outputs) equal a synchronous deferred run."""
+    import c1_dropin as C
+
+    gold, gold_w = _gold(golden_dir)
+    installed(prime_layout="reference", sampler="numpy", encoder="numpy", deferred=True,
+              deferred_async=True)
+    cust, model, shape, x, onehot = C.build()
+    seen = C.capture_refresh_inputs(cust)
+    C.step(cust, model, shape, x, onehot)
+    cust.backend.flush()  # returns at once
+    outs = [C.sha(cust.backend.serialize_cipher(pm.payload)) for pm in C.outputs(model)]
+    assert seen == gold["refresh_inputs_sha256"]
+    assert outs == gold["outputs_sha256"]
+    assert np.array_equal(C.weights(model, cust), gold_w)
+
+    def two_steps(**opts):
+        installed(prime_layout="reference", sampler="numpy", encoder="numpy", deferred=True,
+                  **opts)
+        cust, model, shape, x, onehot = C.build()
+        for t in (1, 2):
+            C.step(cust, model, shape, x, onehot, t=t)
+            cust.backend.flush()
+        return [C.sha(cust.backend.serialize_cipher(pm.payload)) for pm in C.outputs(model)]
+
+    assert two_steps(deferred_async=True) == two_steps(deferred_async=False)

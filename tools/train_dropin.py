@@ -125,9 +125,14 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
 
     sim = keygen(params, rots, backend="sim")
     sim_model = build(sim)
+    # pipelined flushes (deferred.py): the layer code records step t+1 while
+    # step t is issued and run; off for the instrumented (profile) runs
+    pipelined = (not profile_step and not kernels_step
+                 and os.environ.get("CKB_PIPELINED", "1") == "1")
     cls, old = plugin.install(prime_layout="bootstrap", dnum=3, secret_hw=192,
                               real_bootstrap=True, low_special=cfg["low_special"],
-                              deferred=True, deferred_max_group=cfg["max_group"])
+                              deferred=True, deferred_max_group=cfg["max_group"],
+                              deferred_async=pipelined)
     try:
         t0 = time.perf_counter()
         cust = keygen(params, rots, backend="ckks", rng_seed=cfg["rng_seed"])
@@ -137,6 +142,7 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
         keygen_s = time.perf_counter() - t0
         model = build(cust)
         be.flush()
+        be.wait()
         torch.cuda.synchronize()
         per_step, errs, snaps = [], [], []
         torch.cuda.reset_peak_memory_stats()
@@ -161,7 +167,13 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
                 _ring.TIMER = _ring.KernelTimer()
             batch = [prepare_sample(x[i], onehot[i], shape, cust) for i in range(x.shape[0])]
             train_iteration(model, batch, cust, t)
-            be.flush()
+
+            def mark():  # the step boundary, after the step's last launch
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                marks.append(ev)
+
+            be.flush(on_issued=mark)
             if t == kernels_step:
                 summ = _ring.TIMER.summary()
                 _ring.TIMER = None
@@ -169,9 +181,6 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
                 for k_, v in sorted(summ.items(), key=lambda kv: -kv[1]["ms"]):
                     print(f"  {k_:16s} {v['ms']:9.1f} ms {100 * v['ms'] / tot:5.1f}% "
                           f"{v['calls']:6d} calls", flush=True)
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record()
-            marks.append(ev)
             if prof is not None:
                 import pstats
 
@@ -181,6 +190,7 @@ def run(name: str, steps: int = None, verbose: bool = False, profile_step: int =
                 pstats.Stats(prof).sort_stats("tottime").print_callers(8)
             snaps.append([(b.layer_weights, b.classifier_weights, b.layer_velocity,
                            b.classifier_velocity) for b in model.blocks])
+        be.wait()
         torch.cuda.synchronize()
         total_s = time.perf_counter() - t_start
         per_step = [marks[k].elapsed_time(marks[k + 1]) / 1e3 for k in range(steps)]
