@@ -322,6 +322,20 @@ int ckb_sample(const ckb_ring* ring, uint64_t* a, int64_t* e, const uint64_t* se
 
 /* Signed int64 coefficients -> residues (ring.py:139-145):
  * in: [polys][N] int64; out: [polys][limbs][N]. */
+/* Packed residue transfer format for host <-> device copies of ciphertext
+ * batches (no reference counterpart: the reference never leaves host memory;
+ * RBCT, ckks/backend.py:210-247, stays the serialisation format).  Limb l of
+ * each of `items` items ([items][limbs][N] uint64, canonical) is stored with
+ * w_l bytes per residue — 5 for primes < 2^40, 6 below 2^48, else 8 (the
+ * ckb_ring size masks) — little-endian, an item's limbs back to back.
+ * ckb_packed_bytes: the packed size; ckb_pack / ckb_unpack: device buffers,
+ * 8-byte aligned; unpack(pack(x)) == x for canonical x. */
+int64_t ckb_packed_bytes(const ckb_ring* ring, int items, int limbs, const int32_t* limb_prime);
+int ckb_pack(const ckb_ring* ring, uint8_t* out, const uint64_t* in, int items, int limbs,
+             const int32_t* limb_prime, void* stream);
+int ckb_unpack(const ckb_ring* ring, uint64_t* out, const uint8_t* in, int items, int limbs,
+               const int32_t* limb_prime, void* stream);
+
 int ckb_from_i64(const ckb_ring* ring, uint64_t* out, const int64_t* in, int polys, int limbs,
                  const int32_t* limb_prime, void* stream);
 

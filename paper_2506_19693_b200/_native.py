@@ -139,6 +139,9 @@ def _load():
         "ckb_reduce": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_sample": ([R, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_double,
                         c_vp], ctypes.c_int),
+        "ckb_packed_bytes": ([R, ctypes.c_int, ctypes.c_int, c_i32p], ctypes.c_int64),
+        "ckb_pack": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_unpack": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
         "ckb_tc_probe": ([ctypes.c_int, ctypes.c_int, c_vp, c_vp], ctypes.c_int),
         "ckb_tc_selftest": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_alu_probe": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c_vp,
@@ -165,7 +168,8 @@ EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inver
             "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
             "ckb_automorphism_ntt",
             "ckb_reduce", "ckb_sample", "ckb_alu_probe",
-            "ckb_alu_probe_f64", "ckb_tc_selftest", "ckb_tc_probe")
+            "ckb_alu_probe_f64", "ckb_tc_selftest", "ckb_tc_probe", "ckb_packed_bytes", "ckb_pack",
+            "ckb_unpack")
 
 
 def check(rc: int, what: str) -> None:

@@ -1148,6 +1148,20 @@ class B200CkksCore:
         g_items, ptrs, _ = self._rotation_tables(steps)
         return self._hrot(a, level, g_items=g_items, key_ptrs=ptrs)
 
+    def pack_batch(self, data: torch.Tensor, level: int) -> torch.Tensor:
+        """[B, 2, limbs(level), N] payload batch -> [B, bytes] uint8 in the packed
+        transfer format (ckb_pack: 5 bytes per residue of a prime < 2^40), for
+        host <-> device copies of ciphertext batches (streaming.Pipeline)."""
+        m = self._limbs(level)
+        b = data.shape[0]
+        return self.chain.pack(data.contiguous(), 2 * b, m).view(b, -1)
+
+    def unpack_batch(self, packed: torch.Tensor, level: int) -> torch.Tensor:
+        """Inverse of pack_batch: [B, bytes] uint8 -> [B, 2, limbs(level), N]."""
+        m = self._limbs(level)
+        b = packed.shape[0]
+        return self.chain.unpack(packed.contiguous(), 2 * b, m).view(b, 2, m, self.n)
+
     def batch_ntt(self, a: torch.Tensor, level: int, inverse: bool = False) -> torch.Tensor:
         """In-place NTT / iNTT of every limb of a [..., limbs(level), N] batch."""
         m = self._limbs(level)

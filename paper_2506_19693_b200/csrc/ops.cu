@@ -1700,6 +1700,110 @@ static uint64_t f64_bits(double d) {
   return u;
 }
 
+
+// ---------------------------------------------------------------------------
+// Packed residue transfer format (host <-> device copies): limb l of an item
+// stores each residue in w_l bytes (5 below 2^40, 6 below 2^48, else 8: the
+// ckb_ring size classes), little-endian, the item's limbs back to back:
+// item i, limb l at byte i*item_bytes + off_l*N.  A thread moves 8 residues
+// (64 B unpacked, 8*w_l B = w_l words packed; all offsets 8-byte aligned).
+// ---------------------------------------------------------------------------
+struct PackMap {
+  int16_t w[kMaxLimbs];    // bytes per residue
+  int32_t off[kMaxLimbs];  // prefix sum of w (bytes per coefficient before limb l)
+};
+
+__global__ void k_pack(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                       size_t groups, int log_n, int limbs, int item_w, PackMap pm) {
+  const size_t N = (size_t)1 << log_n;
+  const int gpr = (int)(N >> 3);  // 8-residue groups per row
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < groups;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = g / gpr;
+    const int c = (int)(g - row * gpr);
+    const size_t item = row / limbs;
+    const int l = (int)(row - item * limbs);
+    const int w = pm.w[l];
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(in + row * N + 8 * (size_t)c);
+    uint64_t v[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const ulonglong2 t = __ldcs(src + k);
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+    uint64_t* dst = out + (item * (size_t)item_w * N + (size_t)pm.off[l] * N) / 8 + (size_t)c * w;
+    if (w == 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dst[k] = v[k];
+      continue;
+    }
+    // concatenate 8 values of 8w bits into w words
+    unsigned __int128 acc = 0;
+    int bits = 0, o = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc |= (unsigned __int128)v[k] << bits;
+      bits += 8 * w;
+      if (bits >= 64) {
+        dst[o++] = (uint64_t)acc;
+        acc >>= 64;
+        bits -= 64;
+      }
+    }
+  }
+}
+
+__global__ void k_unpack(uint64_t* __restrict__ out, const uint64_t* __restrict__ in,
+                         size_t groups, int log_n, int limbs, int item_w, PackMap pm) {
+  const size_t N = (size_t)1 << log_n;
+  const int gpr = (int)(N >> 3);
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < groups;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = g / gpr;
+    const int c = (int)(g - row * gpr);
+    const size_t item = row / limbs;
+    const int l = (int)(row - item * limbs);
+    const int w = pm.w[l];
+    const uint64_t* src = in + (item * (size_t)item_w * N + (size_t)pm.off[l] * N) / 8 + (size_t)c * w;
+    uint64_t v[8];
+    if (w == 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(src + k);
+    } else {
+      const uint64_t mask = (1ull << (8 * w)) - 1;
+      unsigned __int128 acc = 0;
+      int bits = 0, i = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (bits < 8 * w) {
+          acc |= (unsigned __int128)__ldcs(src + i++) << bits;
+          bits += 64;
+        }
+        v[k] = (uint64_t)acc & mask;
+        acc >>= 8 * w;
+        bits -= 8 * w;
+      }
+    }
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(out + row * N + 8 * (size_t)c);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k] = make_ulonglong2(v[2 * k], v[2 * k + 1]);
+  }
+}
+
+static int make_packmap(PackMap& pm, const RingDev& R, const LimbMap& lm, int limbs) {
+  int off = 0;
+  for (int l = 0; l < limbs; ++l) {
+    const int pi = lm.p[l];
+    const bool wide = (R.wide_mask[pi >> 6] >> (pi & 63)) & 1;
+    const bool mid = (R.mid_mask[pi >> 6] >> (pi & 63)) & 1;
+    pm.w[l] = (int16_t)(wide ? 8 : mid ? 6 : 5);
+    pm.off[l] = off;
+    off += pm.w[l];
+  }
+  return off;
+}
+
 extern "C" {
 
 int ckb_version(void) { return 1; }
@@ -2146,6 +2250,44 @@ int ckb_automorphism(const ckb_ring* ring, uint64_t* out, const uint64_t* in, in
   if (!total) return 0;
   k_automorphism<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       out, in, total, (int)R.log_n, limbs, inv, galois_inv_items, rows_per_item, R, lm);
+  return finish();
+}
+
+int64_t ckb_packed_bytes(const ckb_ring* ring, int items, int limbs, const int32_t* limb_prime) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || items < 0) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  PackMap pm;
+  return (int64_t)items * make_packmap(pm, R, lm, limbs) * ((int64_t)1 << R.log_n);
+}
+
+int ckb_pack(const ckb_ring* ring, uint8_t* out, const uint64_t* in, int items, int limbs,
+             const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || items < 0 || !out || !in) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  if (R.log_n < 3) return CKB_E_LOGN;
+  PackMap pm;
+  const int item_w = make_packmap(pm, R, lm, limbs);
+  const size_t groups = ((size_t)items * limbs) << (R.log_n - 3);
+  if (!groups) return 0;
+  k_pack<<<grid_for(groups, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<uint64_t*>(out), in, groups, (int)R.log_n, limbs, item_w, pm);
+  return finish();
+}
+
+int ckb_unpack(const ckb_ring* ring, uint64_t* out, const uint8_t* in, int items, int limbs,
+               const int32_t* limb_prime, void* stream) {
+  LimbMap lm;
+  if (!make_map(lm, limb_prime, limbs) || items < 0 || !out || !in) return CKB_E_ARG;
+  const RingDev R = make_ring(ring);
+  if (R.log_n < 3) return CKB_E_LOGN;
+  PackMap pm;
+  const int item_w = make_packmap(pm, R, lm, limbs);
+  const size_t groups = ((size_t)items * limbs) << (R.log_n - 3);
+  if (!groups) return 0;
+  k_unpack<<<grid_for(groups, 256), 256, 0, (cudaStream_t)stream>>>(
+      out, reinterpret_cast<const uint64_t*>(in), groups, (int)R.log_n, limbs, item_w, pm);
   return finish();
 }
 

@@ -675,5 +675,31 @@ class GpuChain:
         return out
 
     # -- host <-> device helpers -------------------------------------------------------
+    def packed_bytes(self, items: int, limbs: int, lmap=None) -> int:
+        """Size of the packed transfer format (ckb_pack) of [items][limbs][N]."""
+        return int(nat.LIB.ckb_packed_bytes(self.ring_p, items, limbs, lmap or self.q_map(limbs)))
+
+    def pack(self, x: torch.Tensor, items: int, limbs: int, lmap=None, out=None) -> torch.Tensor:
+        """[items][limbs][N] residues -> uint8 packed transfer format (5 bytes per
+        residue below 2^40, 6 below 2^48, else 8): fewer PCIe bytes per copy."""
+        lm = lmap or self.q_map(limbs)
+        nb = self.packed_bytes(items, limbs, lm)
+        out = out if out is not None else torch.empty(nb, dtype=torch.uint8, device=self.device)
+        _run("pack", items * limbs * self.n * W + nb, 1, lambda: nat.check(
+            nat.LIB.ckb_pack(self.ring_p, nat.ptr(out), nat.ptr(x), items, limbs, lm,
+                             nat.stream_handle()), "pack"))
+        return out
+
+    def unpack(self, packed: torch.Tensor, items: int, limbs: int, lmap=None,
+               out=None) -> torch.Tensor:
+        """Inverse of pack: -> [items, limbs, N] uint64."""
+        lm = lmap or self.q_map(limbs)
+        out = out if out is not None else torch.empty(items, limbs, self.n, dtype=U64,
+                                                      device=self.device)
+        _run("unpack", items * limbs * self.n * W + packed.numel(), 1, lambda: nat.check(
+            nat.LIB.ckb_unpack(self.ring_p, nat.ptr(out), nat.ptr(packed), items, limbs, lm,
+                               nat.stream_handle()), "unpack"))
+        return out
+
     def upload_u64(self, arr: np.ndarray) -> torch.Tensor:
         return self.upload_table(np.ascontiguousarray(arr, dtype=np.uint64))

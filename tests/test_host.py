@@ -21,7 +21,7 @@ def test_library_exports_every_header_symbol():
     from paper_2506_19693_b200 import _native
 
     header = open(os.path.join(ROOT, "include", "ckks_b200.h")).read()
-    declared = set(re.findall(r"\b(?:int|uint64_t)\s+(ckb_\w+)\s*\(", header))
+    declared = set(re.findall(r"\b(?:int|int64_t|uint64_t)\s+(ckb_\w+)\s*\(", header))
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(_native.LIB, name)
