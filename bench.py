@@ -765,7 +765,11 @@ def run_c2(L, bsz, args, rank, world, local, breakdown=False, keep=False) -> dic
             stage["hrot"].append((e2, e3))
         torch.cuda.synchronize()
         ring.TIMER = None
-        st_ms = {kk: float(np.mean([a.elapsed_time(b) for a, b in v])) for kk, v in stage.items()}
+        # median over the steps (a rare stall of one step would skew a mean);
+        # the spread is reported beside it
+        st_all = {kk: [a.elapsed_time(b) for a, b in v] for kk, v in stage.items()}
+        st_ms = {kk: float(np.median(v)) for kk, v in st_all.items()}
+        out["stages_ms_minmax"] = {kk: [float(min(v)), float(max(v))] for kk, v in st_all.items()}
         ksum = timer.summary()
         launches = sum(d["launches"] for d in ksum.values())
         dom_name = max(ksum, key=lambda nm: ksum[nm]["ms"])
