@@ -36,7 +36,9 @@ def rb():
 
 
 A, B = rb(), rb()
-s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+prio = os.environ.get("PAIR_PRIO", "")  # "hm" / "hr": that stream at high priority
+s1 = torch.cuda.Stream(priority=-1 if prio == "hm" else 0)
+s2 = torch.cuda.Stream(priority=-1 if prio == "hr" else 0)
 
 
 def pair():
