@@ -1029,6 +1029,9 @@ def main():
     for cname, skip in (("c4", args.no_c4), ("c5", args.no_c5)):
         if rank == 0 and world == 1 and not skip:
             try:
+                import gc as _gc
+
+                _gc.collect()  # earlier legs' backends (reference cycles) and graph pools
                 torch.cuda.empty_cache()
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
                 import train_dropin
