@@ -45,3 +45,45 @@ def test_resolved_payloads_become_inputs_of_the_next_program():
     lp.value = done  # as after a flush
     vid = rec.operand(lp)
     assert rec.inputs[vid] is done and rec.operand(done) == vid
+
+
+def test_pipelined_flushes_run_in_order_and_chain_pending_values():
+    """deferred_async (pipelined): flush() returns at once; programs run in flush
+    order on one worker; a value of a still-pending program enters the next
+    program as an input and is read when that program runs; resolve() joins."""
+    import threading
+    import time
+
+    class _Be:
+        device = "cpu"
+
+    rec = Recorder(backend=_Be(), pipelined=True)
+    gate = threading.Event()
+    ran = []
+
+    def fake_run(snap, restore_serials):
+        ops, serials, inputs, live, pts = snap
+        assert restore_serials is False  # the recording thread owns the live counter
+        gate.wait(5)
+        for k, v in inputs.items():  # earlier programs have produced their values
+            if isinstance(v, LazyPayload):
+                assert v.value is not None
+        ran.append([op[0] for op in ops])
+        for vid, lp in live.items():
+            lp.value = _Payload(lp.level)
+
+    rec._run = fake_run
+    issued = []
+    a = rec.record(("enc", None, rec.plaintext(np.ones(4))), 5, serial=1)
+    rec.flush(on_issued=lambda: issued.append(1))
+    assert a.value is None and rec._pending  # returned before the program ran
+    vid = rec.operand(a)  # pending value of program 1 -> input of program 2
+    assert rec.inputs[vid] is a
+    b = rec.record(("rot", None, vid, 1), 5)
+    rec.flush(on_issued=lambda: issued.append(2))
+    time.sleep(0.05)
+    assert ran == []  # still gated
+    gate.set()
+    assert rec.resolve(b) is b.value  # joins every pending program
+    assert ran == [["enc"], ["rot"]] and issued == [1, 2]
+    assert a.value is not None and not rec._pending
