@@ -79,6 +79,12 @@ typedef struct {
                                  correction on the tensor cores (tcgen05.mma
                                  kind::i8, byte-sliced; bit-identical results).
                                  Requires wide_mask. */
+#define CKB_RING_LAZY_BCONV 8u /* with CKB_RING_TC: the tensor-core basis
+                                 conversions (ckb_modup digits, the correction
+                                 E of ckb_divround_ntt_corr) may leave outputs
+                                 in [0, 3p) instead of [0, p) — valid inputs of
+                                 ckb_ntt_forward*, their only consumer in a key
+                                 switch; saves the final reductions */
 #define CKB_RING_NTT_SPLIT 2u /* run FP64-class and integer-class NTT rows of one
                                  call as two kernels instead of one per-CTA-dispatch
                                  kernel (same integers; A/B measurements) */

@@ -32,6 +32,7 @@ class CkbRing(ctypes.Structure):
 RING_HPS_EXACT = 1  # ckb_ring.flags (include/ckks_b200.h)
 RING_NTT_SPLIT = 2
 RING_TC = 4  # tensor-core ModUp / ModDown correction (needs wide_mask)
+RING_LAZY_BCONV = 8  # their outputs in [0, 3p): forward-NTT inputs only
 DEFAULT_NTT_CHUNK_BYTES = 96 << 20
 
 

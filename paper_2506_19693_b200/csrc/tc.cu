@@ -262,7 +262,7 @@ __device__ __forceinline__ void tc_issue(uint32_t tmem, const uint8_t* A, const 
 // s = k - 1 and mu32 = floor(2^(32+s) / p): top = v >> s < 2^32 and
 // q = hi32(top * mu32) underestimates floor(v / p) by at most 2
 // (v / 2^(s+32) < 1/2 and 2^s / p <= 1), so v - q p lies in [0, 3p).
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ uint64_t tc_reduce_narrow(uint64_t v, const TcSlot& S) {
   v += S.addc;
   if (!FAST && S.mu32 == 0) {  // primes below 2^26 (test chains): generic 128-bit reduction
@@ -272,6 +272,7 @@ __device__ __forceinline__ uint64_t tc_reduce_narrow(uint64_t v, const TcSlot& S
   const uint32_t top = (uint32_t)(v >> S.sh);
   const uint32_t q = __umulhi(top, S.mu32);
   uint64_t r = v - (uint64_t)q * S.p;
+  if (FAST == 2) return r;  // lazy: [0, 3p), a forward-NTT input (CKB_RING_LAZY_BCONV)
   r = r >= S.p ? r - S.p : r;
   return r >= S.p ? r - S.p : r;
 }
@@ -279,7 +280,7 @@ __device__ __forceinline__ uint64_t tc_reduce_narrow(uint64_t v, const TcSlot& S
 // One group of 8 narrow outputs (40 accumulator columns from 5g).  GUARD:
 // the tail group (outputs past n_narrow are skipped); full groups run
 // branch-free so the compiler interleaves the 8 independent reductions.
-template <bool FAST, bool GUARD>
+template <int FAST, bool GUARD>
 __device__ __forceinline__ void tc_group8(uint32_t tl, int g, int n_narrow, const TcSlot* slots,
                                           uint64_t* __restrict__ out) {
   uint32_t v[40];
@@ -303,7 +304,7 @@ __device__ __forceinline__ void tc_group8(uint32_t tl, int g, int n_narrow, cons
 // bits): top = v >> (k-1) < 2^32 and q = hi32(top * mu32) is within 2 of
 // floor(v / p) (v / 2^(k+31) < 0.82, 2^(k-1) / p <= 1); the remainder fits 64
 // bits, so it is computed mod 2^64 from the low word.  Else 128-bit Barrett.
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const TcSlot& S,
                                          uint64_t* __restrict__ out) {
   uint64_t lo = (uint64_t)v[1] * 256u + v[0];
@@ -319,8 +320,11 @@ __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const T
     const uint32_t top = (uint32_t)__funnelshift_r((uint32_t)(l >> 32), (uint32_t)h, S.sh - 32);
     const uint32_t q = __umulhi(top, S.mu32);
     uint64_t r = l - (uint64_t)q * S.p;
-    r = r >= S.p ? r - S.p : r;
-    out[S.roff] = r >= S.p ? r - S.p : r;
+    if (FAST != 2) {
+      r = r >= S.p ? r - S.p : r;
+      r = r >= S.p ? r - S.p : r;
+    }
+    out[S.roff] = r;
     return;
   }
   const Mod m{S.p, S.mu, S.k, S.two_p};
@@ -328,7 +332,7 @@ __device__ __forceinline__ void tc_wide1(uint32_t tl, const uint32_t* v, const T
 }
 
 // One group of 4 mid outputs (24 columns): v = sum_b<6 2^(8b) P_b < 2^64.
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ void tc_group4_mid(uint32_t tl, int col, int g, int n_mid,
                                               const TcSlot* slots, uint64_t* __restrict__ out) {
   uint32_t v[24];
@@ -352,7 +356,7 @@ __device__ __forceinline__ void tc_group4_mid(uint32_t tl, int col, int g, int n
 // units (narrow groups, mid groups, wide pairs, numbered in that order) with
 // index = sub (mod H); out[slot.roff].  FAST: every output takes the 32-bit
 // quotient path.
-template <bool FAST, int H>
+template <int FAST, int H>
 __device__ __forceinline__ void tc_epilogue_t(uint32_t tl, TcCols cols, const TcSlot* slots,
                                               uint64_t* __restrict__ out, int sub) {
   const int un = cols.u_narrow, um = cols.u_mid, uw = cols.u_wide;
@@ -381,15 +385,19 @@ __device__ __forceinline__ void tc_epilogue_t(uint32_t tl, TcCols cols, const Tc
 
 __device__ __forceinline__ void tc_epilogue(uint32_t tl, TcCols cols, const TcSlot* slots,
                                             uint64_t* __restrict__ out, bool fast, int sub,
-                                            int h) {
-  if (fast) {
-    if (h == 1) tc_epilogue_t<true, 1>(tl, cols, slots, out, sub);
-    else if (h == 2) tc_epilogue_t<true, 2>(tl, cols, slots, out, sub);
-    else tc_epilogue_t<true, 4>(tl, cols, slots, out, sub);
+                                            int h, bool lazy) {
+  if (fast && lazy) {
+    if (h == 1) tc_epilogue_t<2, 1>(tl, cols, slots, out, sub);
+    else if (h == 2) tc_epilogue_t<2, 2>(tl, cols, slots, out, sub);
+    else tc_epilogue_t<2, 4>(tl, cols, slots, out, sub);
+  } else if (fast) {
+    if (h == 1) tc_epilogue_t<1, 1>(tl, cols, slots, out, sub);
+    else if (h == 2) tc_epilogue_t<1, 2>(tl, cols, slots, out, sub);
+    else tc_epilogue_t<1, 4>(tl, cols, slots, out, sub);
   } else {
-    if (h == 1) tc_epilogue_t<false, 1>(tl, cols, slots, out, sub);
-    else if (h == 2) tc_epilogue_t<false, 2>(tl, cols, slots, out, sub);
-    else tc_epilogue_t<false, 4>(tl, cols, slots, out, sub);
+    if (h == 1) tc_epilogue_t<0, 1>(tl, cols, slots, out, sub);
+    else if (h == 2) tc_epilogue_t<0, 2>(tl, cols, slots, out, sub);
+    else tc_epilogue_t<0, 4>(tl, cols, slots, out, sub);
   }
 }
 
@@ -508,6 +516,7 @@ __global__ void __launch_bounds__(kTcMaxThreads) k_modup_tc(
   const uint32_t tmem = sh.tmem;
   const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const bool fast = sh.fast;
+  const bool lazy = (R.flags & CKB_RING_LAZY_BCONV) != 0;
 
   const int tpr = (int)(N / kTcRows);
   const int ntiles = batch * tpr;
@@ -555,7 +564,7 @@ __global__ void __launch_bounds__(kTcMaxThreads) k_modup_tc(
     mbar_wait(&sh.bar, phase);
     phase ^= 1;
     tc_after();
-    tc_epilogue(tl, cols, slots, obase, fast, sub, h);
+    tc_epilogue(tl, cols, slots, obase, fast, sub, h, lazy);
     tc_before();
   }
   __syncthreads();
@@ -670,6 +679,7 @@ __global__ void __launch_bounds__(kTcMaxThreads) k_corr_tc(
   const uint32_t tmem = sh.tmem;
   const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const bool fast = sh.fast;
+  const bool lazy = (R.flags & CKB_RING_LAZY_BCONV) != 0;
   const int trows = n1 + n2 + (has_add ? n2 : 0);
   const int tpr = (int)(N / kTcRows);
   const int ntiles = polys * tpr;
@@ -761,7 +771,7 @@ __global__ void __launch_bounds__(kTcMaxThreads) k_corr_tc(
     mbar_wait(&sh.bar, phase);
     phase ^= 1;
     tc_after();
-    tc_epilogue(tl, cols, slots, E + pidx * m2 * N + n, fast, sub, h);
+    tc_epilogue(tl, cols, slots, E + pidx * m2 * N + n, fast, sub, h, lazy);
     tc_before();
   }
   __syncthreads();

@@ -107,8 +107,8 @@ class GpuChain:
                                 (nat.ctypes.c_uint64 * 2)(*nat.f64_mask(self.all_primes)))
         self.ring.wide_mask = (nat.ctypes.c_uint64 * 2)(*nat.wide_mask(self.all_primes))
         self.ring.mid_mask = (nat.ctypes.c_uint64 * 2)(*nat.mid_mask(self.all_primes))
-        if self.use_tc:
-            self.ring.flags |= nat.RING_TC
+        if self.use_tc:  # outputs of the basis conversions only feed forward NTTs
+            self.ring.flags |= nat.RING_TC | nat.RING_LAZY_BCONV
         self.ring_p = nat.ctypes.pointer(self.ring)
         self._maps: dict = {}
 

@@ -75,10 +75,15 @@ def _outputs(be, x, y, steps, lvl):
     ch = be.chain
     m = ch.level_limbs[lvl]
     coeff = x[:, 0].contiguous()  # any canonical residues will do for ModUp
+    # ModUp's own outputs canonical (the lazy [0, 3p) form only feeds NTTs)
+    lazy = ch.set_ring_flag(nat.RING_LAZY_BCONV, False)
+    try:
+        mu = ch.modup(coeff, m, be.alpha, be._bconv(m, ch.k), skip_own=False).clone()
+    finally:
+        ch.set_ring_flag(nat.RING_LAZY_BCONV, lazy)
     return (be.batch_hmult(x, y, lvl).clone(), be.batch_hrot(x, steps, lvl).clone(),
             be._hrot(x, lvl, galois=be.galois_for_step[steps[0]],
-                     key=be.rotation_key(be.galois_for_step[steps[0]])).clone(),
-            ch.modup(coeff, m, be.alpha, be._bconv(m, ch.k), skip_own=False).clone())
+                     key=be.rotation_key(be.galois_for_step[steps[0]])).clone(), mu)
 
 
 @pytest.mark.parametrize("case", ["c2_L24", "c2_L12", "c2_L4", "c2_L23_short", "boot_low_p",
@@ -111,6 +116,32 @@ def test_tc_bit_identical_to_cuda_cores(case):
                 assert torch.equal(a.view(torch.int64), b.view(torch.int64)), (case, lvl, i)
     finally:
         ch.set_ring_flag(nat.RING_HPS_EXACT, False)
+
+
+def test_tc_lazy_outputs_reduce_to_the_canonical_ones():
+    """CKB_RING_LAZY_BCONV: ModUp outputs in [0, 3p), congruent to the canonical ones."""
+    params, opts = _case("c2_L24", 4096)
+    cust = he_api.keygen(params, set(), backend="ckks", rng_seed=2, **opts)
+    be = cust.backend
+    ch = be.chain
+    lvl = params.level
+    m = ch.level_limbs[lvl]
+    rng = np.random.default_rng(4)
+    x = torch.stack([be.payload_from_planes(_planes(ch.limbs_at(lvl), 4096, rng), lvl).data
+                     for _ in range(2)])[:, 0].contiguous()
+    outs = {}
+    for lazy in (True, False):
+        prev = ch.set_ring_flag(nat.RING_LAZY_BCONV, lazy)
+        outs[lazy] = ch.modup(x, m, be.alpha, be._bconv(m, ch.k), skip_own=False).cpu().numpy()
+        ch.set_ring_flag(nat.RING_LAZY_BCONV, prev)
+    ext = list(range(m)) + list(range(ch.lq, ch.lq + ch.k))
+    nd = -(-m // be.alpha)
+    primes = np.array([ch.all_primes[i] for i in ext], dtype=np.uint64)
+    lz = outs[True].reshape(2, nd, len(ext), -1)
+    cn = outs[False].reshape(2, nd, len(ext), -1)
+    p = primes[None, None, :, None]
+    assert np.all(lz < 3 * p) and np.array_equal(lz % p, cn) and np.all(cn < p)
+    assert not np.array_equal(lz, cn)  # the lazy form is in use
 
 
 def test_tc_default_on():

@@ -42,6 +42,10 @@ if os.environ.get("CKB_NTT_SPLIT") == "1":  # class-split NTT launches (ckb_ring
     from paper_2506_19693_b200 import _native as _nat
 
     be.chain.set_ring_flag(_nat.RING_NTT_SPLIT, True)
+if os.environ.get("CKB_LAZY") == "0":  # canonical basis-conversion outputs (A/B)
+    from paper_2506_19693_b200 import _native as _nat0
+
+    be.chain.set_ring_flag(_nat0.RING_LAZY_BCONV, False)
 if os.environ.get("CKB_CHUNK_MB"):  # L2 budget of the sequential transforms
     be.chain.set_ntt_chunk_bytes(int(os.environ["CKB_CHUNK_MB"]) << 20)
 X = torch.empty_like(A)
@@ -96,4 +100,6 @@ if os.environ.get("CKB_NTT_SPLIT") == "1":
     tag += "+split"
 if os.environ.get("CKB_FUSE_KS") == "1":
     tag += "+fused"
+if os.environ.get("CKB_LAZY") == "0":
+    tag += "+eager_bconv"
 print(tag, json.dumps(res))
