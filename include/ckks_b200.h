@@ -221,6 +221,20 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
                  const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
                  const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
                  void* stream);
+/* The same with an addend folded in for ext limbs e < fold_limbs (the Q limbs):
+ *   acc[b][0][e] += fold_b[b][e] * P_e,  acc[b][1][e] += fold_a[b][e] * P_e  (mod q_e)
+ * fold_b / fold_a: DEVICE [limbs][N] per item at b*stride (NTT domain; fold_a may
+ * be NULL), fold_mul: DEVICE [fold_limbs][2] {P mod q_e, shoup(.)} with P the
+ * special modulus the following ModDown divides by.  That ModDown then yields
+ * x P^-1 + addend directly (backend.py:136-143's d0/d1, :155-171's c0'), so it
+ * reads no addend (and needs no addend rows for a fused rescale).  n_digits <= 8. */
+int ckb_ks_inner_fold(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
+                      int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
+                      const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                      const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                      const uint64_t* fold_b, int64_t fold_b_stride, const uint64_t* fold_a,
+                      int64_t fold_a_stride, const uint64_t* fold_mul, int fold_limbs,
+                      void* stream);
 
 /* Exact divide-and-round chain (ring.py:165-189, keys.py:98-99, backend.py:86-112):
  *   x <- x * prescale[limb]              (optional; level adjust, backend.py:108-111)

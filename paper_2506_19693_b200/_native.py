@@ -116,6 +116,10 @@ def _load():
         "ckb_ks_inner": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p,
                           ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int64, c_vp, c_vp,
                           ctypes.c_int, c_i32p, c_vp], ctypes.c_int),
+        "ckb_ks_inner_fold": ([R, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p,
+                               ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int64, c_vp, c_vp,
+                               ctypes.c_int, c_i32p, c_vp, ctypes.c_int64, c_vp, ctypes.c_int64,
+                               c_vp, ctypes.c_int, c_vp], ctypes.c_int),
         "ckb_divround": ([R, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, ctypes.c_int,
                           ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i32p, ctypes.c_int,
                           ctypes.c_int, c_u64p, c_vp, c_vp, c_vp],
@@ -164,7 +168,7 @@ def _load():
 LIB = _load()
 EXPORTED = ("ckb_version", "ckb_build_tables", "ckb_ntt_forward", "ckb_ntt_inverse",
             "ckb_ntt_forward_combine", "ckb_ntt_forward_from", "ckb_ntt_inverse_from",
-            "ckb_elementwise", "ckb_pt_mac", "ckb_scalar_mac", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner", "ckb_ks_ntt_mac", "ckb_embed_scatter", "ckb_embed_finish",
+            "ckb_elementwise", "ckb_pt_mac", "ckb_scalar_mac", "ckb_scalar_mul", "ckb_tensor", "ckb_modup", "ckb_ks_inner", "ckb_ks_inner_fold", "ckb_ks_ntt_mac", "ckb_embed_scatter", "ckb_embed_finish",
             "ckb_divround", "ckb_automorphism", "ckb_from_i64", "ckb_to_f64",
             "ckb_divround_ntt_corr", "ckb_divround_ntt_combine", "ckb_divround_ntt_combine_acc",
             "ckb_automorphism_ntt",

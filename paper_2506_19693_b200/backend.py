@@ -255,6 +255,10 @@ class B200CkksCore:
     _errors = he_errors
     _api = he_api
     _instances = 0
+    # ModDown addends (HMult's d0/d1, HRot's c0') folded into the key inner
+    # product as addend * P (ckb_ks_inner_fold) instead of read by the ModDown
+    # correction and combine; same integers.  CKB_NO_FOLD=1 for A/B runs.
+    fold_addends = __import__("os").environ.get("CKB_NO_FOLD") != "1"
 
     def __init__(self, params, rotation_indices=(), rng_seed: int = 0, bootstrap_eps: float = 0.0,
                  keyset_id=None, _secret=None, *, prime_layout: str = "reference", dnum=None,
@@ -540,7 +544,7 @@ class B200CkksCore:
 
     def _key_switch_acc(self, d: torch.Tensor, m: int, batch: int = 1, d_stride: int = 0,
                         key: KeySwitchKey = None, key_ptrs=None, own: torch.Tensor = None,
-                        own_stride: int = 0, k: int = None) -> torch.Tensor:
+                        own_stride: int = 0, k: int = None, fold=None) -> torch.Tensor:
         """keys.py:74-97: digits of d (coefficient domain, batch items of [m, N]
         at b*d_stride), lifted to Q_l u P, NTT, inner product with the key rows.
         ``own`` is the NTT form of d (items at b*own_stride): a digit's own
@@ -557,14 +561,20 @@ class B200CkksCore:
         digits = ch.modup(d, m, a, self._bconv(m, k), batch=batch, in_batch_stride=d_stride,
                           skip_own=skip, k=k)
         basis = ch.digit_basis(m, a, skip, k)
-        if skip and ch.fuse_ks_mac and ch.log_n in (16, 17):
+        if skip and ch.fuse_ks_mac and ch.log_n in (16, 17) and fold is None:
             # the digits' row-phase transform fused with the inner product
             return ch.ks_ntt_mac(digits, m, a, key=key.data if key is not None else None,
                                  key_ptrs=key_ptrs, own=own, own_bstride=own_stride, k=k)
         ch.ntt_fwd(digits, len(basis), ch.cmap(basis))
         return ch.ks_inner(digits, m, a, key=key.data if key is not None else None,
                            key_ptrs=key_ptrs, own=own if skip else None, own_bstride=own_stride,
-                           k=k)
+                           k=k, fold=fold)
+
+    def _can_fold(self, m: int) -> bool:
+        """The ModDown addend can ride in the inner product (ckb_ks_inner_fold:
+        hybrid digits, at most 8 of them; not the fused ks_ntt_mac path)."""
+        return (self.fold_addends and self.alpha > 1 and -(-m // self.alpha) <= 8
+                and not (self.chain.fuse_ks_mac and self.chain.log_n in (16, 17)))
 
     def _ks_k(self, level: int) -> int:
         """Special primes a key switch at this level uses (see __init__)."""
@@ -785,9 +795,15 @@ class B200CkksCore:
         d = ch.tensor(a, b, m)  # [B, 3, m, N]
         d2 = ch.ntt_from(d[:, 2], bsz, m, 3 * m * self.n, inverse=True)
         k = self._ks_k(level)
-        acc = self._key_switch_acc(d2, m, batch=bsz,
-                                   key=self.relin_keys_k[k] if k != ch.k else self.relin_key,
-                                   own=d[:, 2], own_stride=3 * m * self.n, k=k)
+        key = self.relin_keys_k[k] if k != ch.k else self.relin_key
+        if self._can_fold(m):  # d0 / d1 ride in the inner product as d*P
+            acc = self._key_switch_acc(d2, m, batch=bsz, key=key, own=d[:, 2],
+                                       own_stride=3 * m * self.n, k=k,
+                                       fold=(d[:, 0], 3 * m * self.n, d[:, 1], 3 * m * self.n))
+            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, basis=ch.ext_basis(m, k))
+            return out.view(bsz, 2, m - e, self.n)
+        acc = self._key_switch_acc(d2, m, batch=bsz, key=key, own=d[:, 2],
+                                   own_stride=3 * m * self.n, k=k)
         tail = d[:, 0:2, m - e:m].reshape(2 * bsz, e, self.n)
         out = ch.divround_ntt(acc, 2 * bsz, m + k, k, e, addend=d, addend_polys=2,
                               addend_period=2, addend_stride=3, addend_tail=tail,
@@ -824,14 +840,18 @@ class B200CkksCore:
         kk = self._ks_k(level)
         if key_ptrs is None and kk != ch.k and galois in self.rotation_keys_k[kk]:
             k, key = kk, self.rotation_keys_k[kk][galois]
+        fold = (r[:, 0], 2 * m * self.n, None, 0) if self._can_fold(m) else None
         acc = self._key_switch_acc(c1, m, batch=bsz, key=key, key_ptrs=key_ptrs, own=r[:, 1],
-                                   own_stride=2 * m * self.n, k=k)
+                                   own_stride=2 * m * self.n, k=k, fold=fold)
         post = None
         if accumulate:
             post = a if a.is_contiguous() else a.contiguous()
-        out = ch.divround_ntt(acc, 2 * bsz, m + k, k, 0, addend=r, addend_polys=1,
-                              addend_period=2, addend_stride=2, basis=ch.ext_basis(m, k),
-                              post=post)
+        if fold is not None:  # c0' rode in the inner product as c0' * P
+            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, 0, basis=ch.ext_basis(m, k), post=post)
+        else:
+            out = ch.divround_ntt(acc, 2 * bsz, m + k, k, 0, addend=r, addend_polys=1,
+                                  addend_period=2, addend_stride=2, basis=ch.ext_basis(m, k),
+                                  post=post)
         return out.view(bsz, 2, m, self.n)
 
     def _encrypt_values(self, values, level: int, serial: int = None) -> GpuCiphertext:

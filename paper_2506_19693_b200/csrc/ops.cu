@@ -583,6 +583,18 @@ inline size_t modup_v2_smem(int ext, int amax) {
          (size_t)ext * sizeof(ModSm) + (2 * (size_t)ext + 2) * 4 + 3 * (size_t)amax * 8 + 16;
 }
 
+// Optional addend folded into the inner product for the first `limbs` ext
+// limbs (the Q limbs): acc_b[e] += b[e] * P_e and acc_a[e] += a[e] * P_e
+// (P_e = the special modulus mod q_e, with its Shoup word), so the ModDown
+// that follows yields x P^-1 + addend without reading the addend again.
+struct KsFold {
+  const uint64_t* b;  // item i, limb e at b + i*bs + e*N (NULL: no fold)
+  const uint64_t* a;  // likewise for the a output (NULL: none)
+  size_t bs, as;
+  const uint64_t* mul;  // [limbs][2] {P mod q_e, shoup}
+  int limbs;
+};
+
 // acc[b][c][e] = sum_j digit_j[e] * key_b[j][c][key_limb(e)] with 128-bit lazy
 // accumulation and one reduction per output.  With own != NULL the digits'
 // own limbs come from `own` (the NTT-domain input the digits were cut from);
@@ -594,7 +606,7 @@ __global__ void __launch_bounds__(256) k_ks_inner(
     int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
     size_t own_bstride, int log_n,
     const uint64_t* __restrict__ key, const uint64_t* const* __restrict__ key_ptrs, int key_limbs,
-    RingDev R, LimbMap em, LimbMap km, LimbMap od) {
+    RingDev R, LimbMap em, LimbMap km, LimbMap od, KsFold fold) {
   const size_t N = (size_t)1 << log_n;
   const int lh = log_n - 1;
   const size_t total = (size_t)batch * ext << lh;
@@ -624,6 +636,14 @@ __global__ void __launch_bounds__(256) k_ks_inner(
     const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
     const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
     const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    const bool fold_e = fold.b != nullptr && e < fold.limbs;
+    ulonglong2 fb = make_ulonglong2(0, 0), fa = make_ulonglong2(0, 0);
+    uint64_t fP = 0;
+    if (fold_e) {
+      fP = __ldg(fold.mul + 2 * e);
+      fb = *reinterpret_cast<const ulonglong2*>(fold.b + bi * fold.bs + (size_t)e * N + n);
+      if (fold.a) fa = *reinterpret_cast<const ulonglong2*>(fold.a + bi * fold.as + (size_t)e * N + n);
+    }
     ulonglong2 ob, oa;
 #ifndef CKB_KSS_INT
     if ((m.p >> 46) == 0) {  // warp-uniform: the FP64 pipe, exact products
@@ -640,6 +660,13 @@ __global__ void __launch_bounds__(256) k_ks_inner(
         sa0 += mulmod_f64(x0, a0, a0 * pinv, pd);
         sa1 += mulmod_f64(x1, a1, a1 * pinv, pd);
       }
+      if (fold_e) {
+        const double P = u64_to_f64(fP), Pp = P * pinv;
+        sb0 += mulmod_f64(u64_to_f64(fb.x), P, Pp, pd);
+        sb1 += mulmod_f64(u64_to_f64(fb.y), P, Pp, pd);
+        sa0 += mulmod_f64(u64_to_f64(fa.x), P, Pp, pd);
+        sa1 += mulmod_f64(u64_to_f64(fa.y), P, Pp, pd);
+      }
       ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
       oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
     } else
@@ -652,6 +679,12 @@ __global__ void __launch_bounds__(256) k_ks_inner(
       ckb::mac128(ha0, la0, x[j].x, a[j].x);
       ckb::mac128(hb1, lb1, x[j].y, b[j].y);
       ckb::mac128(ha1, la1, x[j].y, a[j].y);
+    }
+    if (fold_e) {
+      ckb::mac128(hb0, lb0, fb.x, fP);
+      ckb::mac128(hb1, lb1, fb.y, fP);
+      ckb::mac128(ha0, la0, fa.x, fP);
+      ckb::mac128(ha1, la1, fa.y, fP);
     }
     if (m.k >= 32) {
       ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
@@ -678,11 +711,11 @@ __global__ void __launch_bounds__(256) k_ks_inner(
 // once per batch instead of once per item (the per-item form re-read the
 // 90 MB relinearisation key from L2 for each of the 64 items of config 2).
 template <int ND>
-__global__ void __launch_bounds__(256) k_ks_inner_shared(
+__global__ void __launch_bounds__(256, 2) k_ks_inner_shared(
     uint64_t* __restrict__ acc, const uint64_t* __restrict__ dig, int batch, int ext,
     int out_rows, int item_rows, int alpha, int limbs, const uint64_t* __restrict__ own,
     size_t own_bstride, int log_n, const uint64_t* __restrict__ key, int key_limbs, RingDev R,
-    LimbMap em, LimbMap km, LimbMap od) {
+    LimbMap em, LimbMap km, LimbMap od, KsFold fold) {
   const size_t N = (size_t)1 << log_n;
   const int lh = log_n - 1;
   const size_t total = (size_t)ext << lh;
@@ -710,6 +743,9 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
     const uint64_t* mm = R.mods + (size_t)em.p[e] * kModStride;
     const Mod m{__ldg(mm), __ldg(mm + 1), __ldg(mm + 2), __ldg(mm + 3)};
     const uint64_t r64 = __ldg(mm + 8), r64s = __ldg(mm + 9);
+    const bool fold_e = fold.b != nullptr && e < fold.limbs;
+    const uint64_t fP = fold_e ? __ldg(fold.mul + 2 * e) : 0;
+    // x[0..ND) the digits; with a fold, x[ND] / x[ND+1] the b / a addends
     auto load_item = [&](int bi, ulonglong2* x) {
       const uint64_t* dbase = dig + (size_t)bi * item_rows * N;
 #pragma unroll
@@ -718,13 +754,19 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
                                           : dbase + rowoff[j];
         x[j] = __ldcs(reinterpret_cast<const ulonglong2*>(xp));
       }
+      if (fold_e) {
+        x[ND] = *reinterpret_cast<const ulonglong2*>(fold.b + bi * fold.bs + (size_t)e * N + n);
+        x[ND + 1] = fold.a ? *reinterpret_cast<const ulonglong2*>(fold.a + bi * fold.as +
+                                                                  (size_t)e * N + n)
+                           : make_ulonglong2(0, 0);
+      }
     };
-    ulonglong2 xn[ND];
+    ulonglong2 xn[ND + 2];
     load_item(0, xn);
     for (int bi = 0; bi < batch; ++bi) {
-      ulonglong2 x[ND];
+      ulonglong2 x[ND + 2];
 #pragma unroll
-      for (int j = 0; j < ND; ++j) x[j] = xn[j];
+      for (int j = 0; j < ND + 2; ++j) x[j] = xn[j];
 #ifndef CKB_KSS_NO_PREFETCH
       if (bi + 1 < batch) load_item(bi + 1, xn);  // next item's loads in flight during this MAC
 #endif
@@ -744,6 +786,13 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
           sa0 += mulmod_f64(x0, a0, a0 * pinv, pd);
           sa1 += mulmod_f64(x1, a1, a1 * pinv, pd);
         }
+        if (fold_e) {
+          const double P = u64_to_f64(fP), Pp = P * pinv;
+          sb0 += mulmod_f64(u64_to_f64(x[ND].x), P, Pp, pd);
+          sb1 += mulmod_f64(u64_to_f64(x[ND].y), P, Pp, pd);
+          sa0 += mulmod_f64(u64_to_f64(x[ND + 1].x), P, Pp, pd);
+          sa1 += mulmod_f64(u64_to_f64(x[ND + 1].y), P, Pp, pd);
+        }
         ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
         oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
       } else
@@ -756,6 +805,12 @@ __global__ void __launch_bounds__(256) k_ks_inner_shared(
         ckb::mac128(ha0, la0, x[j].x, a[j].x);
         ckb::mac128(hb1, lb1, x[j].y, b[j].y);
         ckb::mac128(ha1, la1, x[j].y, a[j].y);
+      }
+      if (fold_e) {
+        ckb::mac128(hb0, lb0, x[ND].x, fP);
+        ckb::mac128(hb1, lb1, x[ND].y, fP);
+        ckb::mac128(ha0, la0, x[ND + 1].x, fP);
+        ckb::mac128(ha1, la1, x[ND + 1].y, fP);
       }
       if (m.k >= 32) {
         ob = make_ulonglong2(ckb::reduce128_big(hb0, lb0, r64, r64s, m),
@@ -2121,11 +2176,19 @@ int ckb_modup(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t i
   return finish();
 }
 
-int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
-                 int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
-                 const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
-                 const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
-                 void* stream) {
+int ckb_ks_inner_fold(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
+                      int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
+                      const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                      const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                      const uint64_t* fold_b, int64_t fold_b_stride, const uint64_t* fold_a,
+                      int64_t fold_a_stride, const uint64_t* fold_mul, int fold_limbs,
+                      void* stream) {
+  KsFold fold{fold_b, fold_a, (size_t)fold_b_stride, (size_t)fold_a_stride, fold_mul,
+              fold_limbs};
+  if (fold_b && (!fold_mul || fold_limbs < 1 || fold_limbs > ext_limbs || fold_b_stride < 0 ||
+                 fold_a_stride < 0))
+    return CKB_E_ARG;
+  if (fold_b && n_digits > 8) return CKB_E_ARG;  // the generic kernel has no fold
   LimbMap em, km, od;
   if (!make_map(em, ext_prime, ext_limbs) || !make_map(km, key_limb, ext_limbs))
     return CKB_E_LIMBS;
@@ -2148,7 +2211,7 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
 #define CKB_KSS(ND)                                                                         \
   k_ks_inner_shared<ND><<<g, 256, 0, st>>>(acc, digits, batch, ext_limbs, out_rows,         \
                                            item_rows, alpha, limbs, own, ob, (int)R.log_n,  \
-                                           key, key_limbs, R, em, km, od)
+                                           key, key_limbs, R, em, km, od, fold)
     switch (n_digits) {
       case 1: CKB_KSS(1); break;
       case 2: CKB_KSS(2); break;
@@ -2163,7 +2226,7 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
   k_ks_inner<ND><<<grid, 256, 0, st>>>(acc, digits, batch, n_digits, ext_limbs, out_rows,   \
                                        item_rows, alpha, limbs, own, ob, (int)R.log_n, key, \
                                        key_ptrs,                                            \
-                                       key_limbs, R, em, km, od)
+                                       key_limbs, R, em, km, od, fold)
   switch (n_digits) {
     case 1: CKB_KS(1); break;
     case 2: CKB_KS(2); break;
@@ -2181,6 +2244,16 @@ int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, in
   }
 #undef CKB_KS
   return finish();
+}
+
+int ckb_ks_inner(const ckb_ring* ring, uint64_t* acc, const uint64_t* digits, int batch,
+                 int n_digits, int ext_limbs, const int32_t* ext_prime, int alpha, int limbs,
+                 const uint64_t* own, int64_t own_batch_stride, const uint64_t* key,
+                 const uint64_t* const* key_ptrs, int key_limbs, const int32_t* key_limb,
+                 void* stream) {
+  return ckb_ks_inner_fold(ring, acc, digits, batch, n_digits, ext_limbs, ext_prime, alpha,
+                           limbs, own, own_batch_stride, key, key_ptrs, key_limbs, key_limb,
+                           nullptr, 0, nullptr, 0, nullptr, 0, stream);
 }
 
 int ckb_divround(const ckb_ring* ring, uint64_t* out, const uint64_t* in, int64_t in_poly_stride,

@@ -407,11 +407,27 @@ class GpuChain:
             out += tuple(pi for e, pi in enumerate(ext) if e not in own)
         return out
 
+    def fold_table(self, m: int, k: int) -> torch.Tensor:
+        """[m][2] {P_k mod q_e, shoup}: the special modulus of a k-prime key switch
+        on the first m Q limbs (ckb_ks_inner_fold)."""
+        key = ("fold", m, k)
+        hit = self._maps.get(key)
+        if hit is None:
+            pk = math.prod(self.special_primes[:k])
+            vals = []
+            for q in self.primes[:m]:
+                v = pk % q
+                vals += [v, shoup(v, q)]
+            hit = self._maps[key] = self.upload_table(np.array(vals, dtype=np.uint64))
+        return hit
+
     def ks_inner(self, digits, m: int, alpha: int = 1, key: torch.Tensor = None,
                  key_ptrs: torch.Tensor = None, own: torch.Tensor = None, own_bstride: int = 0,
-                 out=None, k: int = None):
+                 out=None, k: int = None, fold=None):
         """digits: ckb_modup's output ([batch, rows, N]; skip_own layout when own
-        is given)."""
+        is given).  fold = (b, b_stride, a, a_stride): addends (tensors or views
+        with item stride *_stride elements; a may be None) folded into the Q limbs
+        as addend * P, so the ModDown that follows yields x P^-1 + addend."""
         batch = digits.shape[0]
         nd = -(-m // alpha)
         k = self.k if k is None else k
@@ -421,13 +437,28 @@ class GpuChain:
         key_limbs = self.lq + k  # keys over Q u (first k special primes)
         n_keys = batch if key_ptrs is not None else 1
         nb = batch * nd * ext + n_keys * nd * 2 * ext + batch * 2 * ext  # own rows counted as read
+        if fold is None:
+            _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
+                nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
+                                     self.ext_map(m, k), alpha, m,
+                                     nat.ptr(own) if own is not None else None, own_bstride,
+                                     nat.ptr(key) if key is not None else None,
+                                     nat.ptr(key_ptrs) if key_ptrs is not None else None,
+                                     key_limbs, self.ext_map(m, k), nat.stream_handle()),
+                "ks_inner"))
+            return out
+        fb, fbs, fa, fas = fold
+        nb += batch * m * (1 if fa is None else 2)
+        ftab = self.fold_table(m, k)
         _run("ks_inner", nb * self.n * W, 1, lambda: nat.check(
-            nat.LIB.ckb_ks_inner(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
-                                 self.ext_map(m, k), alpha, m,
-                                 nat.ptr(own) if own is not None else None, own_bstride,
-                                 nat.ptr(key) if key is not None else None,
-                                 nat.ptr(key_ptrs) if key_ptrs is not None else None,
-                                 key_limbs, self.ext_map(m, k), nat.stream_handle()), "ks_inner"))
+            nat.LIB.ckb_ks_inner_fold(self.ring_p, nat.ptr(out), nat.ptr(digits), batch, nd, ext,
+                                      self.ext_map(m, k), alpha, m,
+                                      nat.ptr(own) if own is not None else None, own_bstride,
+                                      nat.ptr(key) if key is not None else None,
+                                      nat.ptr(key_ptrs) if key_ptrs is not None else None,
+                                      key_limbs, self.ext_map(m, k), nat.ptr(fb), fbs,
+                                      nat.ptr(fa) if fa is not None else None, fas,
+                                      nat.ptr(ftab), m, nat.stream_handle()), "ks_inner_fold"))
         return out
 
     # digits' row-phase NTT fused with the key inner product (ckb_ks_ntt_mac,
