@@ -740,8 +740,8 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   const int threads = ph.C * G >> RB;
   size_t smem = (size_t)ph.C * (G + G / 16 + G / 128) * sizeof(uint64_t);
 #ifndef CKB_NO_COMBINE_PREFETCH
-  if (FWD && ep.out && ph.last && ph.rstride == 1)  // prefetched x and addend tiles
-    smem += 2 * (size_t)ph.C * G * sizeof(uint64_t);
+  if (FWD && ep.out && ph.last && ph.rstride == 1)  // prefetched x (and addend) tiles
+    smem += (ep.add ? 2 : 1) * (size_t)ph.C * G * sizeof(uint64_t);
 #endif
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
