@@ -40,10 +40,13 @@ extern "C" {
 
 /* Device-resident tables for one ring degree and one prime chain.
  *   mods : [n_primes][16] {p, barrett_mu, bitlen, 2p, N^-1, shoup(N^-1),
- *                          psi_inv_brv[1]*N^-1, shoup(.), 2^64 mod p, shoup(.), 0...}
+ *                          psi_inv_brv[1]*N^-1, shoup(.), 2^64 mod p, shoup(.),
+ *                          IEEE-754 bits of 1.0/p, 0...}
  *   ntt  : [n_primes][2][N][2] {psi_brv[j], shoup(.)} pairs, then {inv_psi_brv[j], shoup(.)};
  *          for primes < 2^46 (the FP64 butterfly path) each direction's 2N words
- *          are instead [N] doubles w then [N] doubles w / p (IEEE-754 bits)
+ *          are instead [N] doubles w (IEEE-754 bits) then the same [N] doubles with
+ *          the entries of the two bottom stages interleaved inside each warp's
+ *          block (contiguous vector loads in the row phase, csrc/ntt.cu)
  *   pair : [n_primes][n_primes][4] {p_i^-1 mod p_j, shoup(.), p_i mod p_j, 0}
  * Built on the host by ckb_build_tables, uploaded by the caller. */
 typedef struct {

@@ -53,7 +53,22 @@ struct NttPhase {
                 // (the FP64 path keeps doubles between the two phases)
   const uint64_t* src;  // out-of-place first phase: row (item i, limb l) is read
   size_t src_istride;   // from src + i*src_istride + l*N (NULL: in place)
+  // block decode without integer divisions (set by prep_phase): tiles_per_row
+  // is a power of two, rows split into (item, limb) by a multiply-high
+  int log_tpr;
+  uint32_t items_magic, limbs_magic;  // 0: divide
 };
+
+// floor(x / d) for 0 <= x <= max_x as __umulhi(x, magic): magic = floor(2^32/d)+1
+// is exact while x * d < 2^32; 0 when that cannot be guaranteed.
+inline uint32_t div_magic(int d, long long max_x) {
+  if (d <= 1 || max_x * (long long)d >= (1ll << 32)) return 0;
+  return (uint32_t)((1ull << 32) / (uint32_t)d) + 1;
+}
+
+__device__ __forceinline__ int fast_div(int x, int d, uint32_t magic) {
+  return magic ? (int)__umulhi((uint32_t)x, magic) : x / d;
+}
 
 // Optional epilogue of a forward transform's last phase: the ModDown /
 // rescale combine (ckb_divround_ntt_combine) applied to the transformed
@@ -279,6 +294,39 @@ __device__ __forceinline__ void load_tw_f64(const double* __restrict__ tw, int t
   for (int i = 0; i < NT; ++i) Wpv[i] = Wv[i] * pinv;
 }
 
+// Bottom round of a row phase (register bits = the low bits of r): thread T of
+// the launch needs NT consecutive twiddles starting at NT*T, so a warp's vector
+// load strides 8*NT bytes between lanes and touches 4x (NT = 8) / 2x (NT = 4)
+// the cache lines it uses.  The table's second half (ckb_build_tables) holds
+// the same entries with each warp's block of 32*NT interleaved by 16-byte
+// chunk: chunk c of lane l at block + 64 c + 2 l, so every load is one
+// contiguous 512 bytes per warp.
+template <int NT>
+__device__ __forceinline__ void load_tw_f64_perm(const double* __restrict__ ptab, int t0, double* Wv,
+                                                 double* Wpv, double pinv) {
+  static_assert(NT >= 2, "");
+  const int lane = threadIdx.x & 31;
+  const double* b = ptab + t0 - (NT - 2) * lane;
+#pragma unroll
+  for (int c = 0; c < NT / 2; ++c) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(b + 64 * c));
+    Wv[2 * c] = v.x;
+    Wv[2 * c + 1] = v.y;
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) Wpv[i] = Wv[i] * pinv;
+}
+
+__device__ __forceinline__ void load_tw_f64_pn(int nt, const double* __restrict__ ptab, int t0,
+                                               double* Wv, double* Wpv, double pinv) {
+  switch (nt) {  // constant after unrolling
+    case 8: load_tw_f64_perm<8>(ptab, t0, Wv, Wpv, pinv); break;
+    case 4: load_tw_f64_perm<4>(ptab, t0, Wv, Wpv, pinv); break;
+    case 2: load_tw_f64_perm<2>(ptab, t0, Wv, Wpv, pinv); break;
+    default: load_tw_f64<1>(ptab, t0, Wv, Wpv, pinv); break;
+  }
+}
+
 __device__ __forceinline__ void load_tw_f64_n(int nt, const double* __restrict__ tw, int t0,
                                               double* Wv, double* Wpv, double pinv) {
   switch (nt) {  // constant after unrolling
@@ -332,7 +380,9 @@ __device__ __forceinline__ void rsync() {
   }
 }
 
-template <int S, int RB, int HI, bool CM>
+// PT: the bottom round (WLO == 0) reads the interleaved copy of the table
+// (tw + N), see load_tw_f64_perm.
+template <int S, int RB, int HI, bool CM, bool PT = false>
 __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, int gq, int tbase, int w,
                                                int last, const uint64_t* gsrc, uint64_t* gdst,
@@ -351,7 +401,10 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
       const int bb = b - WLO;
       const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
       double Wv[E / 2], Wpv[E / 2];
-      load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
+      if constexpr (PT && WLO == 0)
+        load_tw_f64_pn((E / 2) >> bb, tw + ((size_t)1 << (2 * S)), t0, Wv, Wpv, pinv);
+      else
+        load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if (k & (1 << bb)) continue;
@@ -380,11 +433,11 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
       for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(x[k]);
     }
     rsync<S, RB, CM>();
-    fwd_rounds_f64<S, RB, LO, CM>(s, tw, p, pinv, gq, tbase, w, last, gsrc, gdst, gs, u64in);
+    fwd_rounds_f64<S, RB, LO, CM, PT>(s, tw, p, pinv, gq, tbase, w, last, gsrc, gdst, gs, u64in);
   }
 }
 
-template <int S, int RB, int LO, bool CM>
+template <int S, int RB, int LO, bool CM, bool PT = false>
 __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __restrict__ tw,
                                                double p, double pinv, double ninv, double ninvp,
                                                double fw, double fwp, int gq, int tbase, int w,
@@ -413,7 +466,10 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
       } else {
         const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
         double Wv[E / 2], Wpv[E / 2];
-        load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
+        if constexpr (PT && WLO == 0)
+          load_tw_f64_pn((E / 2) >> bb, tw + ((size_t)1 << (2 * S)), t0, Wv, Wpv, pinv);
+        else
+          load_tw_f64_n((E / 2) >> bb, tw, t0, Wv, Wpv, pinv);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
@@ -445,43 +501,67 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
         sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv));
     }
     rsync<S, RB, CM>();
-    inv_rounds_f64<S, RB, HI, CM>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last, gsrc,
-                                  gdst, gs, u64in);
+    inv_rounds_f64<S, RB, HI, CM, PT>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last,
+                                      gsrc, gdst, gs, u64in);
   }
 }
 
 #ifndef CKB_NTT_MODE0_MINB
 #define CKB_NTT_MODE0_MINB 3
 #endif
+// MODE 0: per-CTA dispatch on the row's prime class; 1: FP64 rows only; 2:
+// integer rows only; 3: FP64 rows, column-mapped direct global I/O; 4 / 5:
+// MODE 3 / MODE 1 for the column / row phase of a two-phase transform with
+// log2 N = 2S, whose geometry is then a compile-time fact (strides 1 and G,
+// 2048/G groups per CTA, which phase is first and last, the twiddle base):
+// global addresses become immediate offsets of one base pointer (a runtime
+// stride costs six integer instructions per load and store), the first/last
+// variants of the I/O disappear, and the row phase's bottom round reads the
+// interleaved twiddle copy (load_tw_f64_perm).
 template <int S, bool FWD, int RBT, int MODE = 0>
-__global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
-                                  MODE == 1 || MODE == 3 ? (FWD ? 6 : 8)
+__global__ void __launch_bounds__(MODE == 1 || MODE >= 3 ? 128 : kNttThreads,
+                                  MODE == 1 || MODE >= 3 ? (FWD ? 6 : 8)
                                                          : (RBT == 3 ? 4 : CKB_NTT_MODE0_MINB))
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm, CombineEp ep) {
   constexpr int G = 1 << S;
+  constexpr bool kStCol = MODE == 4, kStRow = MODE == 5, kSt = kStCol || kStRow;
+  constexpr bool kF64Only = MODE == 1 || MODE >= 3;
+  // forward: columns then rows; inverse: rows then columns
+  const int p_first = kSt ? (FWD == kStCol ? 1 : 0) : ph.first;
+  const int p_last = kSt ? (FWD == kStCol ? 0 : 1) : ph.last;
+  const int p_rstride = kStCol ? G : kStRow ? 1 : ph.rstride;
+  const int p_gstride = kStCol ? 1 : kStRow ? G : ph.gstride;
+  const int p_logC = kSt ? (S < 11 ? 11 - S : 0) : ph.logC;
   constexpr int RB = S < RBT ? S : RBT;  // log2 elements per thread
   constexpr int E = 1 << RB;
   extern __shared__ uint64_t smem[];
   const int N = 1 << R.log_n;
-  const int rl = ph.row0 + blockIdx.x / ph.tiles_per_row;
+  const int rl = ph.row0 + (int)(blockIdx.x >> ph.log_tpr);
   // limb-major enumeration keeps one prime's twiddle table hot in L2 per chunk
-  const int row = ph.items ? (rl % ph.items) * ph.limbs + rl / ph.items : rl;
-  const int tile = blockIdx.x % ph.tiles_per_row;
-  const int pi = lm.p[row % ph.limbs];
+  int limb, item;  // row = item * limbs + limb
+  if (ph.items) {
+    limb = fast_div(rl, ph.items, ph.items_magic);
+    item = rl - limb * ph.items;
+  } else {
+    item = fast_div(rl, ph.limbs, ph.limbs_magic);
+    limb = rl - item * ph.limbs;
+  }
+  const int row = item * ph.limbs + limb;
+  const int tile = blockIdx.x & (ph.tiles_per_row - 1);
+  const int pi = lm.p[limb];
   const uint64_t* mm = R.mods + (size_t)pi * kModStride;
   const uint64_t p = __ldg(mm), two_p = __ldg(mm + 3);
-  const bool f64 = MODE == 1 || MODE == 3 || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
-  if (((MODE == 1 || MODE == 3) && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
+  const bool f64 = kF64Only || (MODE == 0 && (p >> 46) == 0);  // CTA-uniform
+  if ((kF64Only && (p >> 46) != 0) || (MODE == 2 && (p >> 46) == 0)) return;
   uint64_t* base = data + (size_t)row * N;
   // tile loads of an out-of-place first phase come from the source row
-  const uint64_t* ibase = ph.src ? ph.src + (size_t)(row / ph.limbs) * ph.src_istride +
-                                       (size_t)(row % ph.limbs) * N
+  const uint64_t* ibase = ph.src ? ph.src + (size_t)item * ph.src_istride + (size_t)limb * N
                                  : base;
-  const int C = ph.C;
+  const int C = kSt ? (1 << (S < 11 ? 11 - S : 0)) : ph.C;
   const int T = blockDim.x;
   const int tid = threadIdx.x;
   const int g0 = tile * C;
-  const bool rows_contig = ph.rstride == 1;
+  const bool rows_contig = p_rstride == 1;
 
   // tile -> smem, 16-byte vectors (pairs adjacent in global memory).  Every
   // thread moves exactly E/2 pairs (C*G/2 pairs over C*G/E threads); all
@@ -501,18 +581,18 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
         g = e >> S;
         r = e & (G - 1);
       }
-      return (size_t)(g0 + g) * ph.gstride + r;
+      return (size_t)(g0 + g) * p_gstride + r;
     }
-    r = e >> ph.logC;
+    r = e >> p_logC;
     g = e & (C - 1);
-    return (size_t)r * ph.rstride + g0 + g;
+    return (size_t)r * p_rstride + g0 + g;
   };
   // FP64 path on contiguous rows of a second phase (input = the first phase's
   // L2-resident doubles): the first register round reads global memory
   // directly, no tile staging through shared memory.  Measured (A/B,
   // tools/ab_ntt.sh): forward -3%; a first phase streaming from DRAM is 9%
   // faster with the 16-byte tile loads, so it keeps them.
-  const bool direct = f64 && warp_local && !ph.first;
+  const bool direct = f64 && warp_local && !p_first;
 #ifndef CKB_NO_COMBINE_PREFETCH
   // Fused ModDown combine: the x and addend tiles this thread combines in the
   // epilogue are copied into shared memory asynchronously (cp.async, no
@@ -520,17 +600,17 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   // exposing DRAM latency.  Each thread fetches exactly its own pairs: a
   // cp.async.wait_all before the epilogue is the only synchronisation.
   uint64_t* pf = smem + (size_t)C * (G + G / 16 + G / 128);
-  const bool prefetch = FWD && ep.out && ph.last && rows_contig;
+  const bool prefetch = FWD && ep.out && p_last && rows_contig;
   const uint64_t* pf_add = nullptr;
   if (prefetch) {
-    const int m2 = ph.limbs;
-    const int j = row % m2;
-    const size_t pidx = row / m2;
-    const uint64_t* xr = ep.x + pidx * ep.xs + (size_t)j * N;
+    const int j = limb;
+    const unsigned pidx = (unsigned)item;
+    const uint64_t* xr = ep.x + (size_t)pidx * ep.xs + (size_t)j * N;
     if (ep.add) {
-      const size_t phs = pidx % ep.add_period;
+      const unsigned phs = pidx % (unsigned)ep.add_period;
       if ((int)phs < ep.add_polys)
-        pf_add = ep.add + ((pidx / ep.add_period) * ep.add_stride + phs) * ep.m1 * N +
+        pf_add = ep.add +
+                 ((size_t)(pidx / (unsigned)ep.add_period) * ep.add_stride + phs) * ep.m1 * N +
                  (size_t)j * N;
     }
 #pragma unroll
@@ -556,7 +636,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   // (second phases only, chosen by the host: a first phase streaming from
   // DRAM keeps the 16-byte tile loads — A/B: forward column phase +5% with
   // the column mapping, inverse column phase -4%)
-  constexpr bool colmap = MODE == 3;
+  constexpr bool colmap = MODE == 3 || MODE == 4;
   if (!direct && !colmap) {
     ulonglong2 v[E / 2];
 #pragma unroll
@@ -564,7 +644,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
       int g, r;
       v[i] = __ldcs(reinterpret_cast<const ulonglong2*>(ibase + pair_of(i, g, r)));
     }
-    if (f64 && ph.first) {  // canonical residues -> exact doubles
+    if (f64 && p_first) {  // canonical residues -> exact doubles
 #pragma unroll
       for (int i = 0; i < E / 2; ++i) {
         v[i].x = (uint64_t)__double_as_longlong(u64_to_f64(v[i].x));
@@ -588,34 +668,35 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
     __syncthreads();
 
   const int gq = colmap ? (tid & (C - 1)) : tid / (G / E);
-  const int w = colmap ? (tid >> ph.logC) : tid % (G / E);
-  const int tbase = ph.M0 + ph.gt * (g0 + gq);
+  const int w = colmap ? (tid >> p_logC) : tid % (G / E);
+  const int tbase = kStCol ? 1 : kStRow ? G + g0 + gq : ph.M0 + ph.gt * (g0 + gq);
   // per prime: N forward then N inverse {w, shoup(w)} pairs
   const ulonglong2* tables = reinterpret_cast<const ulonglong2*>(R.ntt + (size_t)pi * 4 * N);
   if (MODE != 2 && f64) {
-    const double pd = (double)p, pinv = 1.0 / pd;
+    const double pd = (double)p, pinv = __longlong_as_double((long long)__ldg(mm + 10));  // 1/p
     // FP64-path table: [N] double(w) forward, [N] w/p, then the inverse pair
     const double* dtab = reinterpret_cast<const double*>(R.ntt + (size_t)pi * 4 * N);
-    const uint64_t* gsrc = colmap ? base + g0 + gq
-                                  : (direct ? base + (size_t)(g0 + gq) * ph.gstride : nullptr);
+    // (a column-mapped first phase reads the out-of-place source directly)
+    const uint64_t* gsrc = colmap ? ibase + g0 + gq
+                                  : (direct ? base + (size_t)(g0 + gq) * p_gstride : nullptr);
     uint64_t* gdst = colmap ? base + g0 + gq : nullptr;
-    const int gs = colmap ? ph.rstride : 1;
+    const int gs = colmap ? p_rstride : 1;
     if constexpr (FWD) {
-      fwd_rounds_f64<S, RB, S, colmap>(smem, dtab, pd, pinv, gq, tbase, w, ph.last, gsrc, gdst,
-                                       gs, gsrc != nullptr && ph.first);
+      fwd_rounds_f64<S, RB, S, colmap, kStRow>(smem, dtab, pd, pinv, gq, tbase, w, p_last, gsrc,
+                                               gdst, gs, gsrc != nullptr && p_first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
-      inv_rounds_f64<S, RB, 0, colmap>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw,
-                                       fw * pinv, gq, tbase, w, ph.last, gsrc, gdst, gs,
-                                       gsrc != nullptr && ph.first);
+      inv_rounds_f64<S, RB, 0, colmap, kStRow>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv,
+                                               fw, fw * pinv, gq, tbase, w, p_last, gsrc, gdst,
+                                               gs, gsrc != nullptr && p_first);
     }
     if constexpr (colmap) return;  // stored straight to global memory
-  } else if constexpr (MODE != 1) {
+  } else if constexpr (!kF64Only) {
     if constexpr (FWD) {
-      fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, ph.last);
+      fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, p_last);
     } else {
       inv_rounds<S, RB, 0>(smem, tables + N, p, two_p, __ldg(mm + 4), __ldg(mm + 5),
-                           __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, ph.last);
+                           __ldg(mm + 6), __ldg(mm + 7), gq, tbase, w, p_last);
     }
   }
   if (warp_local)
@@ -623,10 +704,9 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   else
     __syncthreads();  // the tile store reads across groups
 
-  if (FWD && ep.out && ph.last) {  // fused combine (rows are contiguous here)
-    const int m2 = ph.limbs;
-    const int j = row % m2;
-    const size_t pidx = row / m2;
+  if (FWD && ep.out && p_last) {  // fused combine (rows are contiguous here)
+    const int j = limb;
+    const unsigned pidx = (unsigned)item;
     const int s1 = 2 * (ep.n1 + 1), s2 = 2 * (ep.n2 + 1);
     uint64_t a1 = 0, a1s = 0, b2 = 0, b2s = 0;
     if (ep.n1) {
@@ -637,14 +717,17 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
       b2 = __ldg(ep.tab2 + (size_t)j * s2 + 2 * ep.n2);
       b2s = __ldg(ep.tab2 + (size_t)j * s2 + 2 * ep.n2 + 1);
     }
-    const uint64_t* xr = ep.x + pidx * ep.xs + (size_t)j * N;
+    const uint64_t* xr = ep.x + (size_t)pidx * ep.xs + (size_t)j * N;
     const uint64_t* ar = nullptr;
     if (ep.add) {
-      const size_t phs = pidx % ep.add_period;
+      const unsigned phs = pidx % (unsigned)ep.add_period;
       if ((int)phs < ep.add_polys)
-        ar = ep.add + ((pidx / ep.add_period) * ep.add_stride + phs) * ep.m1 * N + (size_t)j * N;
+        ar = ep.add +
+             ((size_t)(pidx / (unsigned)ep.add_period) * ep.add_stride + phs) * ep.m1 * N +
+             (size_t)j * N;
     }
-    const uint64_t* pr = ep.post ? ep.post + pidx * ep.post_stride + (size_t)j * N : nullptr;
+    const uint64_t* pr =
+        ep.post ? ep.post + (size_t)pidx * ep.post_stride + (size_t)j * N : nullptr;
     uint64_t* orow = ep.out + (size_t)row * N;
 #ifndef CKB_NO_COMBINE_PREFETCH
     if (prefetch) asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -662,7 +745,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
 #endif
 #ifndef CKB_COMBINE_INT
       if (f64) {  // the combine on the FP64 pipe (exact; same integers)
-        const double pd = (double)p, pinv = 1.0 / pd;
+        const double pd = (double)p, pinv = __longlong_as_double((long long)__ldg(mm + 10));
         double c[2] = {u64_to_f64(v.x), u64_to_f64(v.y)};
         const double ev[2] = {u64_to_f64(e0), u64_to_f64(e1)};
         const double a1d = u64_to_f64(a1), b2d = u64_to_f64(b2);
@@ -746,25 +829,47 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   const int blocks = nrows * ph.tiles_per_row;
   if (blocks <= 0) return 0;
   if (threads > kNttThreads) return CKB_E_LOGN;
+  NttPhase q = ph;  // block decode constants
+  q.log_tpr = 0;
+  while ((1 << q.log_tpr) < ph.tiles_per_row) ++q.log_tpr;
+  if ((1 << q.log_tpr) != ph.tiles_per_row) return CKB_E_LOGN;
+  q.items_magic = ph.items ? div_magic(ph.items, (long long)ph.row0 + nrows) : 0;
+  q.limbs_magic = div_magic(ph.limbs, (long long)ph.row0 + nrows);
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
     if (smem > 48 * 1024)                                                          \
       cudaFuncSetAttribute(k_ntt_phase<SS, FWD, RBT, MODE>,                        \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, ph, R, lm, ep); \
+    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, q, R, lm, ep); \
     break;
-  switch (S) {
-    CKB_NTT_CASE(4)
-    CKB_NTT_CASE(5)
-    CKB_NTT_CASE(6)
-    CKB_NTT_CASE(7)
-    CKB_NTT_CASE(8)
-    CKB_NTT_CASE(9)
-    CKB_NTT_CASE(10)
-    CKB_NTT_CASE(11)
-    CKB_NTT_CASE(12)
-    default:
-      return CKB_E_LOGN;
+  if constexpr (MODE == 4 || MODE == 5) {  // log2 N = 2S in 14..20
+    constexpr bool col = MODE == 4;
+    if (S < 7 || S > 10 || ph.C != (1 << (11 - S)) || ph.rstride != (col ? G : 1) ||
+        ph.gstride != (col ? 1 : G) || ph.M0 != (col ? 1 : G) || ph.gt != (col ? 0 : 1) ||
+        ph.first != (FWD == col ? 1 : 0) || ph.last != (FWD == col ? 0 : 1))
+      return CKB_E_ARG;
+    switch (S) {
+      CKB_NTT_CASE(7)
+      CKB_NTT_CASE(8)
+      CKB_NTT_CASE(9)
+      CKB_NTT_CASE(10)
+      default:
+        return CKB_E_LOGN;
+    }
+  } else {
+    switch (S) {
+      CKB_NTT_CASE(4)
+      CKB_NTT_CASE(5)
+      CKB_NTT_CASE(6)
+      CKB_NTT_CASE(7)
+      CKB_NTT_CASE(8)
+      CKB_NTT_CASE(9)
+      CKB_NTT_CASE(10)
+      CKB_NTT_CASE(11)
+      CKB_NTT_CASE(12)
+      default:
+        return CKB_E_LOGN;
+    }
   }
 #undef CKB_NTT_CASE
   return 0;
@@ -843,8 +948,15 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
       // direct global I/O (MODE 3) — first passes too since round 2
       // (ModDown combine -4%, batch NTT -1%, tools/ks_micro.py A/B)
       const bool cm = ph.rstride != 1;
-      int r = cm ? launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st, ep)
-                 : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st, ep);
+#ifndef CKB_NTT_NO_STATIC_COL
+      const bool st2 = logn == 2 * S && S >= 7 && S <= 10;  // MODE 4 / 5
+#else
+      const bool st2 = false;
+#endif
+      int r = cm ? (st2 ? launch_phase<FWD, 4, 4>(S, data, ph, nr, R, lm, st, ep)
+                        : launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st, ep))
+                 : (st2 ? launch_phase<FWD, 4, 5>(S, data, ph, nr, R, lm, st, ep)
+                        : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st, ep));
       if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st, ep);
       return r;
     };

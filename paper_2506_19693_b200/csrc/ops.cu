@@ -1889,12 +1889,9 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
       // bit-reverse j over log_n bits
       uint64_t r = 0;
       for (uint32_t b = 0; b < log_n; ++b) r |= ((j >> b) & 1ull) << (log_n - 1 - b);
-      if ((p >> 46) == 0) {  // FP64 NTT path (csrc/ntt.cu): [N] double(w), then [N] w/p
-        const double pd = (double)p;
+      if ((p >> 46) == 0) {  // FP64 NTT path (csrc/ntt.cu): [N] double(w) per direction
         t[r] = f64_bits((double)acc);
-        t[N + r] = f64_bits((double)acc / pd);
         t[2 * N + r] = f64_bits((double)acc_inv);
-        t[3 * N + r] = f64_bits((double)acc_inv / pd);
       } else {
         t[2 * r] = acc;
         t[2 * r + 1] = ckb::shoup_of(acc, p);
@@ -1903,6 +1900,25 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
       }
       acc = ckb::mul_mod_host(acc, psi, p);
       acc_inv = ckb::mul_mod_host(acc_inv, psi_inv, p);
+    }
+    if ((p >> 46) == 0) {
+      // second half of each direction: the same twiddles, with the entries of
+      // the two bottom stages ([N/2, N): 8 per thread, [N/4, N/2): 4 per
+      // thread) interleaved by 16-byte chunk inside every warp's block of
+      // 256 / 128 so the row phase's vector loads are contiguous per warp
+      // (ntt.cu load_tw_f64_perm): chunk c of lane l at block + 64 c + 2 l.
+      for (int dir = 0; dir < 2; ++dir) {
+        const uint64_t* w = t + (size_t)dir * 2 * N;
+        uint64_t* q = t + (size_t)dir * 2 * N + N;
+        for (uint64_t j = 0; j < N; ++j) q[j] = w[j];
+        for (int nt = 8; nt >= 4 && N >= 512; nt >>= 1) {
+          const uint64_t lo = nt == 8 ? N / 2 : N / 4, blk = 32 * (uint64_t)nt;
+          for (uint64_t b0 = lo; b0 < 2 * lo; b0 += blk)
+            for (uint64_t l = 0; l < 32; ++l)
+              for (uint64_t e = 0; e < (uint64_t)nt; ++e)
+                q[b0 + (e / 2) * 64 + 2 * l + (e & 1)] = w[b0 + nt * l + e];
+        }
+      }
     }
     const ckb::Mod m = ckb::make_mod(p);
     const uint64_t ninv = ckb::inv_mod_host(N % p, p);
@@ -1920,7 +1936,9 @@ int ckb_build_tables(uint32_t log_n, const uint64_t* primes, uint32_t np, uint64
     const uint64_t r64 = (uint64_t)(((unsigned __int128)1 << 64) % p);
     mo[8] = r64;
     mo[9] = ckb::shoup_of(r64, p);
-    for (int z = 10; z < kModStride; ++z) mo[z] = 0;
+    const double pinv = 1.0 / (double)p;  // the FP64 kernels' 1/p (IEEE division, as on the device)
+    memcpy(&mo[10], &pinv, sizeof(double));
+    for (int z = 11; z < kModStride; ++z) mo[z] = 0;
   }
   for (uint32_t i = 0; i < np; ++i) {
     for (uint32_t j = 0; j < np; ++j) {

@@ -103,13 +103,15 @@ def test_ntt_big_primes_vs_oracle_and_roundtrip(logn, bits):
     assert int(_u64(f).max()) < p
 
 
-@pytest.mark.parametrize("logn", [12, 16])
-def test_ntt_out_of_place_matches_in_place(logn):
+@pytest.mark.parametrize("bits0", [60, 40])
+@pytest.mark.parametrize("logn", [12, 14, 16])
+def test_ntt_out_of_place_matches_in_place(logn, bits0):
     """ckb_ntt_{forward,inverse}_from on a strided component view (items of
-    [3][m][N], FP64-path and integer-path primes mixed) equals the in-place
-    transform of a contiguous copy, and leaves the source untouched."""
+    [3][m][N]; FP64-path and integer-path primes mixed, or FP64-path primes
+    only: the column-mapped first phase reads the source directly) equals the
+    in-place transform of a contiguous copy, and leaves the source untouched."""
     n = 1 << logn
-    params = SchemeParams(poly_degree=n, modulus_chain=(60, 40, 40, 60), scale_bits=40, level=2)
+    params = SchemeParams(poly_degree=n, modulus_chain=(bits0, 40, 40, 60), scale_bits=40, level=2)
     ch = GpuChain(params, layout="baseline")
     m, b = 3, 5
     rng = np.random.default_rng(logn)
