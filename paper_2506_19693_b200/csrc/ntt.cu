@@ -510,22 +510,40 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
 #define CKB_NTT_MODE0_MINB 3
 #endif
 // MODE 0: per-CTA dispatch on the row's prime class; 1: FP64 rows only; 2:
-// integer rows only; 3: FP64 rows, column-mapped direct global I/O; 4 / 5:
-// MODE 3 / MODE 1 for the column / row phase of a two-phase transform with
+// integer rows only; 3: FP64 rows, column-mapped direct global I/O.
+// ST = 1 / 2: the column / row phase of a two-phase transform with
 // log2 N = 2S, whose geometry is then a compile-time fact (strides 1 and G,
 // 2048/G groups per CTA, which phase is first and last, the twiddle base):
 // global addresses become immediate offsets of one base pointer (a runtime
 // stride costs six integer instructions per load and store), the first/last
-// variants of the I/O disappear, and the row phase's bottom round reads the
-// interleaved twiddle copy (load_tw_f64_perm).
-template <int S, bool FWD, int RBT, int MODE = 0>
-__global__ void __launch_bounds__(MODE == 1 || MODE >= 3 ? 128 : kNttThreads,
-                                  MODE == 1 || MODE >= 3 ? (FWD ? 6 : 8)
+// variants of the I/O disappear, and the radix-16 row phase's bottom round
+// reads the interleaved twiddle copy (load_tw_f64_perm).  In a MODE 0 launch
+// with ST the FP64 rows' CTAs also take the column-mapped / direct I/O paths
+// of MODE 3 / MODE 1 (the choice is CTA-uniform).
+// resident CTAs per SM (register caps) of the compile-time-geometry kernels,
+// A/B on tools/ntt_micro.py: inverse row phase 8 / 7 / 6 CTAs: 1.491 / 1.442 /
+// 1.397 ms per 3072-row inverse transform
+#ifndef CKB_NTT_M5_INV_MINB
+#define CKB_NTT_M5_INV_MINB 6
+#endif
+#ifndef CKB_NTT_M4_INV_MINB
+#define CKB_NTT_M4_INV_MINB 8
+#endif
+#ifndef CKB_NTT_ST_FWD_MINB
+#define CKB_NTT_ST_FWD_MINB 6
+#endif
+template <int S, bool FWD, int RBT, int MODE = 0, int ST = 0>
+__global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
+                                  MODE == 1 || MODE == 3
+                                      ? (FWD ? (ST ? CKB_NTT_ST_FWD_MINB : 6)
+                                             : (ST == 2   ? CKB_NTT_M5_INV_MINB
+                                                : ST == 1 ? CKB_NTT_M4_INV_MINB
+                                                          : 8))
                                                          : (RBT == 3 ? 4 : CKB_NTT_MODE0_MINB))
     k_ntt_phase(uint64_t* __restrict__ data, NttPhase ph, RingDev R, LimbMap lm, CombineEp ep) {
   constexpr int G = 1 << S;
-  constexpr bool kStCol = MODE == 4, kStRow = MODE == 5, kSt = kStCol || kStRow;
-  constexpr bool kF64Only = MODE == 1 || MODE >= 3;
+  constexpr bool kStCol = ST == 1, kStRow = ST == 2, kSt = ST != 0;
+  constexpr bool kF64Only = MODE == 1 || MODE == 3;
   // forward: columns then rows; inverse: rows then columns
   const int p_first = kSt ? (FWD == kStCol ? 1 : 0) : ph.first;
   const int p_last = kSt ? (FWD == kStCol ? 0 : 1) : ph.last;
@@ -636,7 +654,9 @@ __global__ void __launch_bounds__(MODE == 1 || MODE >= 3 ? 128 : kNttThreads,
   // (second phases only, chosen by the host: a first phase streaming from
   // DRAM keeps the 16-byte tile loads — A/B: forward column phase +5% with
   // the column mapping, inverse column phase -4%)
-  constexpr bool colmap = MODE == 3 || MODE == 4;
+  // (MODE 0 + ST: the FP64 rows of a mixed column phase take it too)
+  constexpr bool kColF64 = MODE == 3 || (MODE == 0 && kStCol);  // FP64 rows column-mapped
+  const bool colmap = MODE == 3 || (kColF64 && f64);
   if (!direct && !colmap) {
     ulonglong2 v[E / 2];
 #pragma unroll
@@ -682,15 +702,16 @@ __global__ void __launch_bounds__(MODE == 1 || MODE >= 3 ? 128 : kNttThreads,
     uint64_t* gdst = colmap ? base + g0 + gq : nullptr;
     const int gs = colmap ? p_rstride : 1;
     if constexpr (FWD) {
-      fwd_rounds_f64<S, RB, S, colmap, kStRow>(smem, dtab, pd, pinv, gq, tbase, w, p_last, gsrc,
-                                               gdst, gs, gsrc != nullptr && p_first);
+      fwd_rounds_f64<S, RB, S, kColF64, kStRow && RB == 4>(smem, dtab, pd, pinv, gq, tbase, w,
+                                                           p_last, gsrc, gdst, gs,
+                                                           gsrc != nullptr && p_first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
-      inv_rounds_f64<S, RB, 0, colmap, kStRow>(smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv,
-                                               fw, fw * pinv, gq, tbase, w, p_last, gsrc, gdst,
-                                               gs, gsrc != nullptr && p_first);
+      inv_rounds_f64<S, RB, 0, kColF64, kStRow && RB == 4>(
+          smem, dtab + 2 * N, pd, pinv, ninv, ninv * pinv, fw, fw * pinv, gq, tbase, w, p_last,
+          gsrc, gdst, gs, gsrc != nullptr && p_first);
     }
-    if constexpr (colmap) return;  // stored straight to global memory
+    if constexpr (kColF64) return;  // stored straight to global memory
   } else if constexpr (!kF64Only) {
     if constexpr (FWD) {
       fwd_rounds<S, RB, S>(smem, tables, p, two_p, gq, tbase, w, p_last);
@@ -815,7 +836,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE >= 3 ? 128 : kNttThreads,
   }
 }
 
-template <bool FWD, int RBT, int MODE = 0>
+template <bool FWD, int RBT, int MODE = 0, int ST = 0>
 int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const RingDev& R,
                  const LimbMap& lm, cudaStream_t st, const CombineEp& ep = CombineEp{}) {
   const int G = 1 << S;
@@ -838,12 +859,12 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
     if (smem > 48 * 1024)                                                          \
-      cudaFuncSetAttribute(k_ntt_phase<SS, FWD, RBT, MODE>,                        \
+      cudaFuncSetAttribute(k_ntt_phase<SS, FWD, RBT, MODE, ST>,                    \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_ntt_phase<SS, FWD, RBT, MODE><<<blocks, threads, smem, st>>>(data, q, R, lm, ep); \
+    k_ntt_phase<SS, FWD, RBT, MODE, ST><<<blocks, threads, smem, st>>>(data, q, R, lm, ep); \
     break;
-  if constexpr (MODE == 4 || MODE == 5) {  // log2 N = 2S in 14..20
-    constexpr bool col = MODE == 4;
+  if constexpr (ST != 0) {  // log2 N = 2S in 14..20
+    constexpr bool col = ST == 1;
     if (S < 7 || S > 10 || ph.C != (1 << (11 - S)) || ph.rstride != (col ? G : 1) ||
         ph.gstride != (col ? 1 : G) || ph.M0 != (col ? 1 : G) || ph.gt != (col ? 0 : 1) ||
         ph.first != (FWD == col ? 1 : 0) || ph.last != (FWD == col ? 0 : 1))
@@ -941,21 +962,26 @@ int ntt_run(const ckb_ring* ring, uint64_t* data, int rows, int limbs, const int
     pb.row0 = r0;
     int rc = 0;
     auto run = [&](int S, const NttPhase& ph) {
-      if (!any_f64 || (any_int && mixed_one_kernel))
-        return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st, ep);
-      // second-pass column phase: column-mapped direct I/O (MODE 3)
-      // column phases (first or second) of pure-FP64 launches: column-mapped
-      // direct global I/O (MODE 3) — first passes too since round 2
-      // (ModDown combine -4%, batch NTT -1%, tools/ks_micro.py A/B)
-      const bool cm = ph.rstride != 1;
-#ifndef CKB_NTT_NO_STATIC_COL
-      const bool st2 = logn == 2 * S && S >= 7 && S <= 10;  // MODE 4 / 5
+      const bool cm = ph.rstride != 1;  // column phase
+#ifndef CKB_NTT_NO_STATIC
+      const bool st2 = logn == 2 * S && S >= 7 && S <= 10;  // compile-time geometry (ST)
 #else
       const bool st2 = false;
 #endif
-      int r = cm ? (st2 ? launch_phase<FWD, 4, 4>(S, data, ph, nr, R, lm, st, ep)
+      if (!any_f64 || (any_int && mixed_one_kernel)) {
+#ifndef CKB_NTT_NO_STATIC_MIXED
+        if (st2)
+          return cm ? launch_phase<FWD, FWD ? 4 : 3, 0, 1>(S, data, ph, nr, R, lm, st, ep)
+                    : launch_phase<FWD, FWD ? 4 : 3, 0, 2>(S, data, ph, nr, R, lm, st, ep);
+#endif
+        return launch_phase<FWD, FWD ? 4 : 3, 0>(S, data, ph, nr, R, lm, st, ep);
+      }
+      // column phases (first or second) of pure-FP64 launches: column-mapped
+      // direct global I/O (MODE 3) — first passes too since round 2
+      // (ModDown combine -4%, batch NTT -1%, tools/ks_micro.py A/B)
+      int r = cm ? (st2 ? launch_phase<FWD, 4, 3, 1>(S, data, ph, nr, R, lm, st, ep)
                         : launch_phase<FWD, 4, 3>(S, data, ph, nr, R, lm, st, ep))
-                 : (st2 ? launch_phase<FWD, 4, 5>(S, data, ph, nr, R, lm, st, ep)
+                 : (st2 ? launch_phase<FWD, 4, 1, 2>(S, data, ph, nr, R, lm, st, ep)
                         : launch_phase<FWD, 4, 1>(S, data, ph, nr, R, lm, st, ep));
       if (!r && any_int) r = launch_phase<FWD, FWD ? 4 : 3, 2>(S, data, ph, nr, R, lm, st, ep);
       return r;
