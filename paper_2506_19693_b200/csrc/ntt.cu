@@ -257,9 +257,11 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
 //   t = fma(-q, p, h) + l  (exact integer, |t| <= 1.5p).
 // Bounds (p < 2^46): forward values grow by <= 1.5p per stage (|v| < 27p over
 // 17 stages, < 2^51, so Y*(W/p) stays below the 2^51 rint range); inverse
-// sums double per stage and are reduced to [-p/2, p/2] after every register
-// round (<= 3 stages: |v| <= 12p).  All arithmetic is exact integer
-// arithmetic, so results equal the integer path's bit for bit.
+// sums double per stage: after every register round (<= 4 stages) the sum-side
+// outputs are reduced to [-p/2, p/2] and the product-side outputs (<= 1.5p)
+// are kept, so a round's inputs are <= 1.5p and its differences <= 24p.
+// All arithmetic is exact integer arithmetic, so results equal the integer
+// path's bit for bit.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void ct_bfly_f64(double& X, double& Y, double W, double Wp, double p) {
   const double t = mulmod_f64(Y, W, Wp, p);
@@ -478,6 +480,14 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
         }
       }
     }
+    // Re-centring between rounds: an element whose last stage of this round
+    // made it the product side of its butterfly (bit HI-1-WLO of k set) is a
+    // mulmod_f64 output, |v| <= 1.5p, and goes on as it is; the sum sides (up
+    // to 16x the round's input bound) are reduced to [-p/2, p/2].  A round's
+    // inputs are then <= 1.5p, its differences <= 24p < 2^51 / 2^46 p.
+    auto recentre = [&](int k) {
+      return ((k >> (HI - 1 - WLO)) & 1) ? x[k] : center_f64(x[k], p, pinv);
+    };
     if constexpr (CM && HI == S) {
       const size_t step = (size_t)gs << WLO;
       uint64_t* g = gdst + (size_t)rbase * gs;
@@ -487,7 +497,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
       } else {
 #pragma unroll
         for (int k = 0; k < E; ++k)
-          __stcs(g + k * step, (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv)));
+          __stcs(g + k * step, (uint64_t)__double_as_longlong(recentre(k)));
       }
       return;
     }
@@ -497,8 +507,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
         sb[koff<WLO>(k)] = f64_to_u64(canon_f64(x[k], p, pinv));
     } else {
 #pragma unroll
-      for (int k = 0; k < E; ++k)
-        sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(center_f64(x[k], p, pinv));
+      for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(recentre(k));
     }
     rsync<S, RB, CM>();
     inv_rounds_f64<S, RB, HI, CM, PT>(s, tw, p, pinv, ninv, ninvp, fw, fwp, gq, tbase, w, last,
