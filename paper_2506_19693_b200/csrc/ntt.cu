@@ -419,7 +419,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
       uint64_t* g = gdst + (size_t)rbase * gs;
       if (last) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) __stcs(g + k * step, f64_to_u64(canon_f64(x[k], p, pinv)));
+        for (int k = 0; k < E; ++k) __stcs(g + k * step, canon_u64(x[k], p, pinv));
       } else {
 #pragma unroll
         for (int k = 0; k < E; ++k) __stcs(g + k * step, (uint64_t)__double_as_longlong(x[k]));
@@ -429,7 +429,7 @@ __device__ __forceinline__ void fwd_rounds_f64(uint64_t* s, const double* __rest
     if (LO == 0 && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k)
-        sb[koff<WLO>(k)] = f64_to_u64(canon_f64(x[k], p, pinv));
+        sb[koff<WLO>(k)] = canon_u64(x[k], p, pinv);
     } else {
 #pragma unroll
       for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(x[k]);
@@ -493,7 +493,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
       uint64_t* g = gdst + (size_t)rbase * gs;
       if (last) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) __stcs(g + k * step, f64_to_u64(canon_f64(x[k], p, pinv)));
+        for (int k = 0; k < E; ++k) __stcs(g + k * step, canon_u64(x[k], p, pinv));
       } else {
 #pragma unroll
         for (int k = 0; k < E; ++k)
@@ -504,7 +504,7 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
     if (HI == S && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k)
-        sb[koff<WLO>(k)] = f64_to_u64(canon_f64(x[k], p, pinv));
+        sb[koff<WLO>(k)] = canon_u64(x[k], p, pinv);
     } else {
 #pragma unroll
       for (int k = 0; k < E; ++k) sb[koff<WLO>(k)] = (uint64_t)__double_as_longlong(recentre(k));
@@ -696,6 +696,8 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   else if (!colmap)
     __syncthreads();
 
+  // (log2 N <= 16 keeps |x P^-1 + add - E| below 2^51 for the epilogue's products)
+  const bool raw_e = FWD && p_last && f64 && R.log_n <= 16;
   const int gq = colmap ? (tid & (C - 1)) : tid / (G / E);
   const int w = colmap ? (tid >> p_logC) : tid % (G / E);
   const int tbase = kStCol ? 1 : kStRow ? G + g0 + gq : ph.M0 + ph.gt * (g0 + gq);
@@ -711,8 +713,10 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
     uint64_t* gdst = colmap ? base + g0 + gq : nullptr;
     const int gs = colmap ? p_rstride : 1;
     if constexpr (FWD) {
+      // fused combine: E stays a (non-canonical, |E| < 27p) double for the epilogue
+      const int f_last = (ep.out && raw_e) ? 0 : p_last;
       fwd_rounds_f64<S, RB, S, kColF64, kStRow && RB == 4>(smem, dtab, pd, pinv, gq, tbase, w,
-                                                           p_last, gsrc, gdst, gs,
+                                                           f_last, gsrc, gdst, gs,
                                                            gsrc != nullptr && p_first);
     } else {
       const double ninv = u64_to_f64(__ldg(mm + 4)), fw = u64_to_f64(__ldg(mm + 6));
@@ -777,7 +781,8 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
       if (f64) {  // the combine on the FP64 pipe (exact; same integers)
         const double pd = (double)p, pinv = __longlong_as_double((long long)__ldg(mm + 10));
         double c[2] = {u64_to_f64(v.x), u64_to_f64(v.y)};
-        const double ev[2] = {u64_to_f64(e0), u64_to_f64(e1)};
+        const double ev[2] = {raw_e ? __longlong_as_double((long long)e0) : u64_to_f64(e0),
+                              raw_e ? __longlong_as_double((long long)e1) : u64_to_f64(e1)};
         const double a1d = u64_to_f64(a1), b2d = u64_to_f64(b2);
         ulonglong2 a = make_ulonglong2(0, 0), w2 = make_ulonglong2(0, 0);
         if (ar) {
@@ -798,7 +803,7 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
           t = t + av[h] - ev[h];                                            // |t| < 3.5p
           if (ep.n2) t = mulmod_f64(t, b2d, b2d * pinv, pd);                // |t| < 1.5p
           t += wv[h];
-          o[h] = f64_to_u64(canon_f64(t, pd, pinv));
+          o[h] = canon_u64(t, pd, pinv);
         }
         *reinterpret_cast<ulonglong2*>(orow + off) = make_ulonglong2(o[0], o[1]);
         continue;
@@ -1154,8 +1159,8 @@ __global__ void __launch_bounds__(128, 4)
     const double2 vb = accb[slot], va = acca[slot];
     ulonglong2 b, a;
     if (f64) {
-      b = make_ulonglong2(f64_to_u64(canon_f64(vb.x, pd, pinv)), f64_to_u64(canon_f64(vb.y, pd, pinv)));
-      a = make_ulonglong2(f64_to_u64(canon_f64(va.x, pd, pinv)), f64_to_u64(canon_f64(va.y, pd, pinv)));
+      b = make_ulonglong2(canon_u64(vb.x, pd, pinv), canon_u64(vb.y, pd, pinv));
+      a = make_ulonglong2(canon_u64(va.x, pd, pinv), canon_u64(va.y, pd, pinv));
     } else {
       b = make_ulonglong2((uint64_t)__double_as_longlong(vb.x), (uint64_t)__double_as_longlong(vb.y));
       a = make_ulonglong2((uint64_t)__double_as_longlong(va.x), (uint64_t)__double_as_longlong(va.y));

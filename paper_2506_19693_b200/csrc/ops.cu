@@ -147,10 +147,10 @@ __global__ void k_tensor2(uint64_t* __restrict__ out, const uint64_t* __restrict
       uint64_t r0[2], r1[2], r2[2];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        r0[c] = f64_to_u64(canon_f64(mulmod2_f64(x0[c], y0[c], p, pinv), p, pinv));
-        r1[c] = f64_to_u64(canon_f64(mulmod2_f64(x0[c], y1[c], p, pinv) +
-                                         mulmod2_f64(x1[c], y0[c], p, pinv), p, pinv));
-        r2[c] = f64_to_u64(canon_f64(mulmod2_f64(x1[c], y1[c], p, pinv), p, pinv));
+        r0[c] = canon_u64(mulmod2_f64(x0[c], y0[c], p, pinv), p, pinv);
+        r1[c] = canon_u64(mulmod2_f64(x0[c], y1[c], p, pinv) +
+                                         mulmod2_f64(x1[c], y0[c], p, pinv), p, pinv);
+        r2[c] = canon_u64(mulmod2_f64(x1[c], y1[c], p, pinv), p, pinv);
       }
       d0 = make_ulonglong2(r0[0], r0[1]);
       d1 = make_ulonglong2(r1[0], r1[1]);
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256) k_modup_mixed(
             const double2 c = cd[i * ext + e];
             acc[i & 1] += ckb_f64::mulmod_f64(yd[i], c.x, c.y, pd);
           }
-        o = ckb_f64::f64_to_u64(ckb_f64::canon_f64(acc[0] + acc[1], pd, pinv[e]));
+        o = ckb_f64::canon_u64(acc[0] + acc[1], pd, pinv[e]);
       } else {  // integer pipe (Acc4 carry-free sums, one reduction)
         uint64_t h = 0, l = 0;
 #pragma unroll
@@ -542,8 +542,8 @@ __global__ void __launch_bounds__(256, CKB_MODUP_MINB) k_modup_v2(
         }
       }
       ulonglong2 o;
-      o.x = ckb_f64::f64_to_u64(ckb_f64::canon_f64(s00 + s01, pp.x, pp.y));
-      o.y = ckb_f64::f64_to_u64(ckb_f64::canon_f64(s10 + s11, pp.x, pp.y));
+      o.x = ckb_f64::canon_u64(s00 + s01, pp.x, pp.y);
+      o.y = ckb_f64::canon_u64(s10 + s11, pp.x, pp.y);
       *reinterpret_cast<ulonglong2*>(dst + (size_t)(rowi[a] & 0xFFFF) * N) = o;
     }
     for (int b = 0; b < ni; ++b) {  // integer pipes
@@ -667,8 +667,8 @@ __global__ void __launch_bounds__(256) k_ks_inner(
         sa0 += mulmod_f64(u64_to_f64(fa.x), P, Pp, pd);
         sa1 += mulmod_f64(u64_to_f64(fa.y), P, Pp, pd);
       }
-      ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
-      oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
+      ob = make_ulonglong2(canon_u64(sb0, pd, pinv), canon_u64(sb1, pd, pinv));
+      oa = make_ulonglong2(canon_u64(sa0, pd, pinv), canon_u64(sa1, pd, pinv));
     } else
 #endif
     {
@@ -793,8 +793,8 @@ __global__ void __launch_bounds__(256, 2) k_ks_inner_shared(
           sa0 += mulmod_f64(u64_to_f64(x[ND + 1].x), P, Pp, pd);
           sa1 += mulmod_f64(u64_to_f64(x[ND + 1].y), P, Pp, pd);
         }
-        ob = make_ulonglong2(f64_to_u64(canon_f64(sb0, pd, pinv)), f64_to_u64(canon_f64(sb1, pd, pinv)));
-        oa = make_ulonglong2(f64_to_u64(canon_f64(sa0, pd, pinv)), f64_to_u64(canon_f64(sa1, pd, pinv)));
+        ob = make_ulonglong2(canon_u64(sb0, pd, pinv), canon_u64(sb1, pd, pinv));
+        oa = make_ulonglong2(canon_u64(sa0, pd, pinv), canon_u64(sa1, pd, pinv));
       } else
 #endif
       {
