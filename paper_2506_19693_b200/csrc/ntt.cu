@@ -57,6 +57,7 @@ struct NttPhase {
   // is a power of two, rows split into (item, limb) by a multiply-high
   int log_tpr;
   uint32_t items_magic, limbs_magic;  // 0: divide
+  int pf_dist;  // first phases: L2-prefetch the tile of block + pf_dist (0: off)
 };
 
 // floor(x / d) for 0 <= x <= max_x as __umulhi(x, magic): magic = floor(2^32/d)+1
@@ -538,6 +539,9 @@ __device__ __forceinline__ void inv_rounds_f64(uint64_t* s, const double* __rest
 #ifndef CKB_NTT_M4_INV_MINB
 #define CKB_NTT_M4_INV_MINB 8
 #endif
+#ifndef CKB_NTT_PF_DIST
+#define CKB_NTT_PF_DIST 296  // 2 CTAs per SM ahead (A/B 148..888: 1.376 / 1.370 / 1.370 / 1.374 / 1.375 / 1.379 ms)
+#endif
 #ifndef CKB_NTT_ST_FWD_MINB
 #define CKB_NTT_ST_FWD_MINB 6
 #endif
@@ -588,6 +592,31 @@ __global__ void __launch_bounds__(MODE == 1 || MODE == 3 ? 128 : kNttThreads,
   const int T = blockDim.x;
   const int tid = threadIdx.x;
   const int g0 = tile * C;
+#ifndef CKB_NTT_NO_L2_PREFETCH
+  // The forward transform's first (column) phase streams its tiles from DRAM
+  // at ~33% occupancy: each CTA asks L2 for the tile of a CTA that will start
+  // soon (block index + pf_dist), so that CTA's strided loads are L2 hits.
+  // (A/B: the inverse's first, row phase and the forward's second phase are slower with it)
+  if (kStCol && FWD && ph.pf_dist) {
+    const unsigned b2 = blockIdx.x + (unsigned)ph.pf_dist;
+    if (b2 < gridDim.x) {
+      const int rl2 = ph.row0 + (int)(b2 >> ph.log_tpr);
+      int limb2, item2;
+      if (ph.items) {
+        limb2 = fast_div(rl2, ph.items, ph.items_magic);
+        item2 = rl2 - limb2 * ph.items;
+      } else {
+        item2 = fast_div(rl2, ph.limbs, ph.limbs_magic);
+        limb2 = rl2 - item2 * ph.limbs;
+      }
+      const uint64_t* b2p = ph.src ? ph.src + (size_t)item2 * ph.src_istride + (size_t)limb2 * N
+                                   : data + (size_t)(item2 * ph.limbs + limb2) * N;
+      const int t2 = (int)(b2 & (unsigned)(ph.tiles_per_row - 1));
+      for (int r = tid; r < G; r += T)  // G rows of C words: one line per row
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b2p + (size_t)r * G + (size_t)t2 * C));
+    }
+  }
+#endif
   const bool rows_contig = p_rstride == 1;
 
   // tile -> smem, 16-byte vectors (pairs adjacent in global memory).  Every
@@ -870,6 +899,7 @@ int launch_phase(int S, uint64_t* data, const NttPhase& ph, int nrows, const Rin
   if ((1 << q.log_tpr) != ph.tiles_per_row) return CKB_E_LOGN;
   q.items_magic = ph.items ? div_magic(ph.items, (long long)ph.row0 + nrows) : 0;
   q.limbs_magic = div_magic(ph.limbs, (long long)ph.row0 + nrows);
+  q.pf_dist = CKB_NTT_PF_DIST;
 #define CKB_NTT_CASE(SS)                                                           \
   case SS:                                                                         \
     if (smem > 48 * 1024)                                                          \
