@@ -121,6 +121,55 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def pcie_probe(device_index: int, mb: int = 256, reps: int = 3) -> dict:
+    """Raw pinned-memory copy rates of this box (H2D alone, D2H alone, both at once on two
+    streams) and the GPU's PCIe link, so the end-to-end number can be read against the
+    transfer floor of the box it ran on (boxes of this pool differ by up to 3x)."""
+    import torch
+
+    n = mb << 20
+    h_in = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(up, dn):
+        best = None
+        for _ in range(reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s_up.wait_event(e0)
+            s_dn.wait_event(e0)
+            if up:
+                with torch.cuda.stream(s_up):
+                    d_in.copy_(h_in, non_blocking=True)
+            if dn:
+                with torch.cuda.stream(s_dn):
+                    h_out.copy_(d_out, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s_up)
+            torch.cuda.current_stream().wait_stream(s_dn)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return n * (int(up) + int(dn)) / (best / 1e3) / 1e9
+
+    out = {"h2d_GBps": timed(True, False), "d2h_GBps": timed(False, True),
+           "bidir_GBps": timed(True, True), "buffer_MB": mb}
+    try:
+        q = subprocess.run(
+            ["nvidia-smi", "-i", str(device_index),
+             "--query-gpu=pcie.link.gen.current,pcie.link.width.current,pcie.link.gen.max",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+        g, w, gm = [int(x) for x in q.stdout.strip().split(",")]
+        out["link"] = {"gen": g, "width": w, "gen_max": gm}
+    except Exception:
+        out["link"] = None
+    return out
+
+
 # ---------------------------------------------------------------------------
 # CPU baselines (oracle port of the reference algorithm, reference prime layout)
 # ---------------------------------------------------------------------------
@@ -991,6 +1040,14 @@ def main():
                                           "timed region",
                        "output_equal_batch_call": bool(ok)}
         del hA, hB, hOm, hOr
+        try:  # the box's own PCIe floor for these bytes, beside the number it bounds
+            pc = pcie_probe(local)
+            moved = line["e2e"]["h2d_bytes_per_step"] + line["e2e"]["d2h_bytes_per_step"]
+            pc["floor_ms"] = moved / (pc["bidir_GBps"] * 1e9) * 1e3
+            pc["frac"] = pc["floor_ms"] / e2e_ms
+            line["e2e"]["pcie"] = pc
+        except Exception as exc:  # report, never hide
+            line["e2e"]["pcie"] = {"error": repr(exc)}
 
     del A, B
     torch.cuda.empty_cache()
