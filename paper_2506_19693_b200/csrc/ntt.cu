@@ -120,23 +120,48 @@ __device__ __forceinline__ void round_sync() {
   }
 }
 
-// Harvey forward (CT) butterfly, values in [0, 4p).
+// Integer butterflies.  The Shoup quotient q = hi64(x * ws) costs four 32-bit
+// multiplies; the butterfly is bound by the multiplier pipe (ten per product),
+// so the NTT estimates it with three, dropping the low x low partial product
+// and the carries of the two cross products' low halves:
+//   q' = xh wsh + hi32(xh wsl) + hi32(xl wsh)  in [q - 2, q],
+// so x w - q' p lies in [0, 4p) instead of [0, 2p) (any x < 2^64).  The lazy
+// ranges widen by one bit to absorb it at no extra instruction: forward values
+// live in [0, 8p), inverse values in [0, 4p) (p < 2^60, ckb_build_tables).
+// kLz = 2: the bound of a reduced value is 4p (CKB_NTT_SHOUP4: the exact
+// quotient and the [0, 4p) / [0, 2p) ranges, kLz = 1).
+#ifdef CKB_NTT_SHOUP4
+constexpr int kLz = 1;
+__device__ __forceinline__ uint64_t ntt_mul_lazy(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
+  return ckb::mul_shoup_lazy(x, w, ws, p);
+}
+#else
+constexpr int kLz = 2;
+__device__ __forceinline__ uint64_t ntt_mul_lazy(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  const uint32_t sl = (uint32_t)ws, sh = (uint32_t)(ws >> 32);
+  const uint64_t q = (uint64_t)xh * sh + __umulhi(xh, sl) + __umulhi(xl, sh);
+  return x * w - q * p;
+}
+#endif
+
+// Harvey forward (CT) butterfly, values in [0, 2 lz): lz = kLz * 2p.
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
-                                        uint64_t p, uint64_t two_p) {
-  uint64_t a = X >= two_p ? X - two_p : X;
-  const uint64_t t = ckb::mul_shoup_lazy(Y, W, Ws, p);
+                                        uint64_t p, uint64_t lz) {
+  uint64_t a = X >= lz ? X - lz : X;
+  const uint64_t t = ntt_mul_lazy(Y, W, Ws, p);
   X = a + t;
-  Y = a - t + two_p;
+  Y = a - t + lz;
 }
 
-// Harvey inverse (GS) butterfly, values in [0, 2p).
+// Harvey inverse (GS) butterfly, values in [0, lz).
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
-                                        uint64_t p, uint64_t two_p) {
+                                        uint64_t p, uint64_t lz) {
   uint64_t sum = X + Y;
-  sum = sum >= two_p ? sum - two_p : sum;
-  const uint64_t d = X - Y + two_p;
+  sum = sum >= lz ? sum - lz : sum;
+  const uint64_t d = X - Y + lz;
   X = sum;
-  Y = ckb::mul_shoup_lazy(d, W, Ws, p);
+  Y = ntt_mul_lazy(d, W, Ws, p);
 }
 
 // One radix-16 round: the thread's 16 elements differ in bits [WLO, WLO+4) of
@@ -174,13 +199,14 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __rest
       for (int k = 0; k < E; ++k) {
         if (k & (1 << bb)) continue;
         const int i = k >> (bb + 1);
-        ct_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
+        ct_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, kLz * two_p);
       }
     }
     if (LO == 0 && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         uint64_t X = x[k];
+        if (kLz == 2) X = X >= 2 * two_p ? X - 2 * two_p : X;
         X = X >= two_p ? X - two_p : X;
         x[k] = X >= p ? X - p : X;
       }
@@ -218,9 +244,9 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
           if (k & (1 << bb)) continue;
           const uint64_t X = x[k], Y = x[k | (1 << bb)];
           uint64_t sum = X + Y;
-          sum = sum >= two_p ? sum - two_p : sum;
+          sum = sum >= kLz * two_p ? sum - kLz * two_p : sum;
           x[k] = ckb::mul_shoup(sum, ninv, ninvs, p);
-          x[k | (1 << bb)] = ckb::mul_shoup(X - Y + two_p, fw, fws, p);
+          x[k | (1 << bb)] = ckb::mul_shoup(X - Y + kLz * two_p, fw, fws, p);
         }
       } else {
         const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
@@ -237,7 +263,7 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
         for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
           const int i = k >> (bb + 1);
-          gs_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, two_p);
+          gs_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, kLz * two_p);
         }
       }
     }
@@ -1265,7 +1291,7 @@ __global__ void __launch_bounds__(256) k_alu_probe(uint64_t p, uint64_t w0, int 
     for (int b = 2; b >= 0; --b) {
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (!(k & (1 << b))) ct_bfly(x[k], x[k | (1 << b)], W[b], Ws[b], p, two_p);
+        if (!(k & (1 << b))) ct_bfly(x[k], x[k | (1 << b)], W[b], Ws[b], p, kLz * two_p);
     }
   }
   uint64_t acc = 0;
@@ -1432,7 +1458,7 @@ int ckb_ks_ntt_mac(const ckb_ring* ring, uint64_t* acc, uint64_t* digits, int ba
 }
 
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream) {
-  if (p < 3 || (p >> 62) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
+  if (p < 3 || (p >> 60) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
   k_alu_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w, iters, sink);
   return finish();
 }

@@ -1,0 +1,10 @@
+#!/bin/bash
+# A/B of the integer NTT butterfly's quotient (3-multiply estimate vs exact Shoup, -DCKB_NTT_SHOUP4)
+V=paper_2506_19693_b200/_lib/variants/shoup4/libckks_b200.so
+for rep in 1 2; do for lib in "" $V; do
+  CKB_LIB=$lib python -c "
+import bench, os
+print(os.environ.get('CKB_LIB') or 'default', 'int probe Gbfly/s', bench.alu_probe_gbfly((1<<60) - (1<<18)*33 + 1))"
+  CKB_LIB=$lib NTT_BITS=60 python tools/ntt_micro.py
+done; done
+for lib in "" $V; do echo "LIB=$lib"; CKB_LIB=$lib python tools/ks_micro.py; done

@@ -57,6 +57,10 @@ plans = {
     "pair_2streams_48MB": ([[("m", 0, 64)], [("r", 0, 64)]], 48 << 20),
     "pair_2streams_96MB": ([[("m", 0, 64)], [("r", 0, 64)]], 96 << 20),
     "pair_2streams_32MB": ([[("m", 0, 64)], [("r", 0, 64)]], 32 << 20),
+    "pair_2streams_40MB": ([[("m", 0, 64)], [("r", 0, 64)]], 40 << 20),
+    "pair_2streams_56MB": ([[("m", 0, 64)], [("r", 0, 64)]], 56 << 20),
+    "pair_2streams_64MB": ([[("m", 0, 64)], [("r", 0, 64)]], 64 << 20),
+    "pair_2streams_80MB": ([[("m", 0, 64)], [("r", 0, 64)]], 80 << 20),
     "halves_4streams_24MB": ([[("m", 0, 32)], [("m", 32, 64)], [("r", 0, 32)], [("r", 32, 64)]],
                              24 << 20),
     "offset_2streams_48MB": ([[("m", 0, 32), ("r", 0, 32)], [("r", 32, 64), ("m", 32, 64)]],
