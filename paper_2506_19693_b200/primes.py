@@ -33,7 +33,7 @@ import numpy as np
 from .he_errors import InvalidParameters
 
 REF_MAX_LIMB_BITS = 30
-MAX_PRIME_BITS = 60  # every prime < 2^60: lazy [0, 4p) butterflies need p < 2^62, and the
+MAX_PRIME_BITS = 60  # every prime < 2^60: lazy [0, 8p) butterflies need p < 2^61, and the
                      # carry-free split dot products (modarith.cuh Acc4) need one operand < 2^60
 _WITNESSES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
 

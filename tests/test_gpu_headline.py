@@ -124,16 +124,25 @@ def test_batch_hrot_per_item_keys_bit_exact(L, batch):
                for i in range(batch))
 
 
+@pytest.mark.parametrize("inputs", ["random", "extreme"])
 @pytest.mark.parametrize("bits", [40, 60])
-def test_ntt_n65536_single_limb_bit_exact(bits):
+def test_ntt_n65536_single_limb_bit_exact(bits, inputs):
     """The N=2^16 two-phase transform (forward and inverse) bit-exact against
     the oracle's NttPlan (ntt.py:121-154) on three limbs: 40-bit primes run
-    the FP64 butterfly, 60-bit primes the integer one."""
+    the FP64 butterfly, 60-bit primes the integer one.  "extreme": rows that
+    drive the lazy ranges of the butterflies to their bounds (every residue
+    p - 1; p - 1 and 0 alternating; p - 1 in the upper half only)."""
     n = 1 << 16
     p = O.largest_ntt_prime_below(bits, 2 * n, set())
     ch = _single_prime_chain(n, p)
     rng = np.random.default_rng(bits)
-    a_np = rng.integers(0, p, (3, n), dtype=np.uint64)
+    if inputs == "random":
+        a_np = rng.integers(0, p, (3, n), dtype=np.uint64)
+    else:
+        a_np = np.zeros((3, n), dtype=np.uint64)
+        a_np[0, :] = p - 1
+        a_np[1, ::2] = p - 1
+        a_np[2, n // 2:] = p - 1
     plan = O.NttPlan(p, n)
     f = ch.ntt_fwd(torch.from_numpy(a_np).cuda(), 1).cpu().numpy()
     inv = ch.ntt_inv(torch.from_numpy(a_np).cuda(), 1).cpu().numpy()

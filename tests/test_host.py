@@ -37,11 +37,22 @@ def test_build_tables_match_oracle_plan(logn, bits):
     mods, ntt, pair = _native.build_tables(logn, [p])
     plan = O.NttPlan(p, n)
     t = ntt.reshape(1, 2, n, 2)
-    if p < 2**46:  # FP64 NTT path: [N] double(w), [N] w/p per direction
+    if p < 2**46:  # FP64 NTT path, per direction: [N] double(w), then the same entries
+        # with the two bottom stages' blocks interleaved by 16-byte chunk per warp
+        # (ops.cu ckb_build_tables / ntt.cu load_tw_f64_perm)
         d = ntt.view(np.float64).reshape(1, 2, 2, n)
         assert [int(v) for v in d[0, 0, 0]] == [int(v) for v in plan.psi_brv]
         assert [int(v) for v in d[0, 1, 0]] == [int(v) for v in plan.inv_psi_brv]
-        assert list(d[0, 0, 1, :8]) == [float(w) / p for w in plan.psi_brv[:8]]
+        for dr, w in ((0, plan.psi_brv), (1, plan.inv_psi_brv)):
+            want = [int(v) for v in w]
+            if n >= 512:
+                for nt, lo in ((8, n // 2), (4, n // 4)):
+                    for b0 in range(lo, 2 * lo, 32 * nt):
+                        for lane in range(32):
+                            for e in range(nt):
+                                want[b0 + (e // 2) * 64 + 2 * lane + (e & 1)] = int(
+                                    w[b0 + nt * lane + e])
+            assert [int(v) for v in d[0, dr, 1]] == want
     else:
         assert [int(v) for v in t[0, 0, :, 0]] == [int(v) for v in plan.psi_brv]
         assert [int(v) for v in t[0, 1, :, 0]] == [int(v) for v in plan.inv_psi_brv]
