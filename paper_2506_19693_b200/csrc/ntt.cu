@@ -31,8 +31,9 @@ namespace {
 // Inside a CTA the tile (C groups x G) is staged in shared memory; each thread
 // keeps 16 elements in registers and applies up to 4 stages per round
 // (radix-16), with one smem exchange between rounds.  Butterflies are the
-// Harvey lazy forms with Shoup twiddles: forward values live in [0, 4p),
-// inverse values in [0, 2p), and the last phase canonicalises.
+// Harvey lazy forms with Shoup twiddles and a 3-multiply quotient estimate:
+// forward values live in [0, 8p), inverse values in [0, 4p) (see
+// ntt_mul_lazy), and the last phase canonicalises.
 // Twiddle of stage bit b for element r in group gidx (derivation in DESIGN.md):
 //   idx = ((M0 + gt*gidx) << (S-1-b)) + (r >> (b+1))
 // ===========================================================================
