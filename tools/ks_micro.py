@@ -9,6 +9,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import _l2persist  # noqa: E402  (tools/ on sys.path when run as a script)
+_l2persist.apply()
 import bench  # noqa: E402
 from paper_2506_19693_b200 import he_api, ring  # noqa: E402
 

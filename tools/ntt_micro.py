@@ -2,6 +2,8 @@
 import os, sys, json
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import _l2persist  # noqa: E402  (tools/ on sys.path when run as a script)
+_l2persist.apply()
 from oracle import ckks_oracle as O
 from paper_2506_19693_b200 import _native as nat
 from paper_2506_19693_b200.ring import GpuChain, U64
