@@ -142,7 +142,19 @@ __device__ __forceinline__ uint64_t ntt_mul_lazy(uint64_t x, uint64_t w, uint64_
   const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
   const uint32_t sl = (uint32_t)ws, sh = (uint32_t)(ws >> 32);
   const uint64_t q = (uint64_t)xh * sh + __umulhi(xh, sl) + __umulhi(xl, sh);
+#ifdef CKB_NTT_MUL_PLAIN
   return x * w - q * p;
+#else
+  // x w + q (-p) mod 2^64 as two wide multiply-adds for the low words and four
+  // 32-bit multiply-adds into the high word (no negation, no 64-bit add chain)
+  const uint64_t np = 0 - p;  // loop-invariant
+  const uint32_t wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
+  const uint32_t ql = (uint32_t)q, qh = (uint32_t)(q >> 32);
+  const uint32_t nl = (uint32_t)np, nh = (uint32_t)(np >> 32);
+  const uint64_t t = (uint64_t)xl * wl + (uint64_t)ql * nl;
+  const uint32_t hi = (uint32_t)(t >> 32) + xh * wl + xl * wh + qh * nl + ql * nh;
+  return ((uint64_t)hi << 32) | (uint32_t)t;
+#endif
 }
 #endif
 
