@@ -384,7 +384,9 @@ int ckb_to_f64(const ckb_ring* ring, double* out, const uint64_t* in, int polys,
 /* ALU roofline probe (no reference counterpart; SURVEY §8(d) "measure the IMAD
  * pipe's peak with a microbenchmark"): blocks x 256 threads each run `iters`
  * radix-8 rounds (12 lazy CT butterflies, the NTT's own) on register-resident
- * residues mod p.  Butterflies launched = blocks * 256 * 12 * iters. */
+ * residues mod p < 2^60, with the NTT's stage schedule (reducing and skipping
+ * stages alternate, so `iters` must be even: CKB_E_ARG otherwise).
+ * Butterflies launched = blocks * 256 * 12 * iters. */
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream);
 
 /* The same probe with the butterfly computed on the FP64 pipe (residues as exact

@@ -159,9 +159,16 @@ __device__ __forceinline__ uint64_t ntt_mul_lazy(uint64_t x, uint64_t w, uint64_
 #endif
 
 // Harvey forward (CT) butterfly, values in [0, 2 lz): lz = kLz * 2p.
+// RED = false (kLz == 2 only): the conditional subtraction of X is skipped.
+// Both outputs carry X's bound plus lz (the product side absorbs any Y), and
+// p < 2^60 leaves room for 16p: alternating stages reduce X from [0, 16p) to
+// [0, 8p) (outputs < 12p) and skip the reduction (inputs < 12p, outputs
+// < 16p), which halves the compare/select work of the forward transform.
+template <bool RED = true>
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
                                         uint64_t p, uint64_t lz) {
-  uint64_t a = X >= lz ? X - lz : X;
+  uint64_t a = X;
+  if constexpr (RED) a = X >= lz ? X - lz : X;
   const uint64_t t = ntt_mul_lazy(Y, W, Ws, p);
   X = a + t;
   Y = a - t + lz;
@@ -212,13 +219,26 @@ __device__ __forceinline__ void fwd_rounds(uint64_t* s, const ulonglong2* __rest
       for (int k = 0; k < E; ++k) {
         if (k & (1 << bb)) continue;
         const int i = k >> (bb + 1);
+#if defined(CKB_NTT_SHOUP4) || defined(CKB_NTT_CT_REDUCE_ALL)
         ct_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, kLz * two_p);
+#else
+        // stage i = S-1-b of the phase: even stages reduce X by 8p (inputs
+        // < 16p: a phase may end on a skipping stage), odd stages skip
+        if (((S - 1 - b) & 1) == 0) {
+          uint64_t& X = x[k];
+          X = X >= 4 * two_p ? X - 4 * two_p : X;
+        }
+        ct_bfly<false>(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, 2 * two_p);
+#endif
       }
     }
     if (LO == 0 && last) {
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         uint64_t X = x[k];
+#if !defined(CKB_NTT_SHOUP4) && !defined(CKB_NTT_CT_REDUCE_ALL)
+        X = X >= 4 * two_p ? X - 4 * two_p : X;
+#endif
         if (kLz == 2) X = X >= 2 * two_p ? X - 2 * two_p : X;
         X = X >= two_p ? X - two_p : X;
         x[k] = X >= p ? X - p : X;
@@ -1299,6 +1319,7 @@ __global__ void __launch_bounds__(256) k_alu_probe(uint64_t p, uint64_t w0, int 
   W[2] = (w0 * 7 + blockIdx.x) % p;
 #pragma unroll
   for (int i = 0; i < 3; ++i) Ws[i] = (uint64_t)(((unsigned __int128)W[i] << 64) / p);
+#if defined(CKB_NTT_SHOUP4) || defined(CKB_NTT_CT_REDUCE_ALL)
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int b = 2; b >= 0; --b) {
@@ -1307,6 +1328,21 @@ __global__ void __launch_bounds__(256) k_alu_probe(uint64_t p, uint64_t w0, int 
         if (!(k & (1 << b))) ct_bfly(x[k], x[k | (1 << b)], W[b], Ws[b], p, kLz * two_p);
     }
   }
+#else
+  // the NTT's stage schedule: reducing and skipping stages alternate (fwd_rounds)
+  for (int it = 0; it < iters; it += 2) {
+#pragma unroll
+    for (int st = 0; st < 6; ++st) {
+      const int b = 2 - st % 3;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k & (1 << b)) continue;
+        if ((st & 1) == 0) x[k] = x[k] >= 4 * two_p ? x[k] - 4 * two_p : x[k];
+        ct_bfly<false>(x[k], x[k | (1 << b)], W[b], Ws[b], p, 2 * two_p);
+      }
+    }
+  }
+#endif
   uint64_t acc = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc ^= x[k];
@@ -1471,7 +1507,8 @@ int ckb_ks_ntt_mac(const ckb_ring* ring, uint64_t* acc, uint64_t* digits, int ba
 }
 
 int ckb_alu_probe(uint64_t p, uint64_t w, int iters, int blocks, uint64_t* sink, void* stream) {
-  if (p < 3 || (p >> 60) != 0 || w >= p || iters < 1 || blocks < 1 || !sink) return CKB_E_ARG;
+  if (p < 3 || (p >> 60) != 0 || w >= p || iters < 1 || (iters & 1) || blocks < 1 || !sink)
+    return CKB_E_ARG;
   k_alu_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w, iters, sink);
   return finish();
 }
