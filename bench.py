@@ -1006,7 +1006,9 @@ def main():
         from paper_2506_19693_b200.streaming import Pipeline
 
         pipe = Pipeline()
-        chunk = int(os.environ.get("CKB_E2E_CHUNK", "0")) or max(1, bsz // 16)
+        # 8 chunks: on this pool's faster hosts 16 chunks are 2-4% quicker, but their ~4,400
+        # kernel launches per step make the step host-enqueue-bound (2x slower) on the slower ones
+        chunk = int(os.environ.get("CKB_E2E_CHUNK", "0")) or max(1, bsz // 8)
 
         def e2e_chunk(dev, lo, hi):
             a = be.unpack_batch(dev[0], lvl)
