@@ -184,6 +184,22 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t W, ui
   Y = ntt_mul_lazy(d, W, Ws, p);
 }
 
+// The same butterfly with bound tracking (kLz == 2; b = 4p is the bound of a
+// product).  Values live in [0, 2b); FRESH: both inputs are products of the
+// previous stage (< b), so the sum (< 2b) needs no reduction and the difference
+// is offset by b instead of 2b.  Inside a register round the inputs of a
+// butterfly share their history, so FRESH is a compile-time property of the
+// element index: 3/8 of the butterflies skip the compare/select.
+template <bool FRESH>
+__device__ __forceinline__ void gs_bfly_t(uint64_t& X, uint64_t& Y, uint64_t W, uint64_t Ws,
+                                          uint64_t p, uint64_t b) {
+  uint64_t sum = X + Y;
+  if constexpr (!FRESH) sum = sum >= 2 * b ? sum - 2 * b : sum;
+  const uint64_t d = X - Y + (FRESH ? b : 2 * b);
+  X = sum;
+  Y = ntt_mul_lazy(d, W, Ws, p);
+}
+
 // One radix-16 round: the thread's 16 elements differ in bits [WLO, WLO+4) of
 // r; stages b in (HI-1 .. LO) for the forward, (LO .. HI-1) for the inverse.
 // The twiddle of the butterfly at k is tw[t0(b) + (k >> (bb+1))]: only
@@ -276,10 +292,16 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
         for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
           const uint64_t X = x[k], Y = x[k | (1 << bb)];
+#if defined(CKB_NTT_SHOUP4) || defined(CKB_NTT_GS_REDUCE_ALL)
           uint64_t sum = X + Y;
           sum = sum >= kLz * two_p ? sum - kLz * two_p : sum;
           x[k] = ckb::mul_shoup(sum, ninv, ninvs, p);
           x[k | (1 << bb)] = ckb::mul_shoup(X - Y + kLz * two_p, fw, fws, p);
+#else
+          // inputs < 8p: the exact Shoup products take any 64-bit operand
+          x[k] = ckb::mul_shoup(X + Y, ninv, ninvs, p);
+          x[k | (1 << bb)] = ckb::mul_shoup(X - Y + 4 * two_p, fw, fws, p);
+#endif
         }
       } else {
         const int t0 = (tbase << (S - 1 - b)) + (rbase >> (b + 1));
@@ -296,7 +318,16 @@ __device__ __forceinline__ void inv_rounds(uint64_t* s, const ulonglong2* __rest
         for (int k = 0; k < E; ++k) {
           if (k & (1 << bb)) continue;
           const int i = k >> (bb + 1);
+#if defined(CKB_NTT_SHOUP4) || defined(CKB_NTT_GS_REDUCE_ALL)
           gs_bfly(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, kLz * two_p);
+#else
+          // fresh: not the round's first stage, and the element was on the
+          // product side of the previous stage (bit bb-1 of k)
+          if (b > LO && ((k >> (bb > 0 ? bb - 1 : 0)) & 1))
+            gs_bfly_t<true>(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, 2 * two_p);
+          else
+            gs_bfly_t<false>(x[k], x[k | (1 << bb)], Wv[i], Wsv[i], p, 2 * two_p);
+#endif
         }
       }
     }

@@ -1,6 +1,6 @@
 #!/bin/bash
-# A/B of the integer NTT butterfly's quotient (default vs a variant build (here: -DCKB_NTT_CT_REDUCE_ALL))
-V=paper_2506_19693_b200/_lib/variants/redall/libckks_b200.so
+# A/B of the integer NTT butterfly's quotient (default vs a variant build (here: -DCKB_NTT_GS_REDUCE_ALL))
+V=paper_2506_19693_b200/_lib/variants/gsall/libckks_b200.so
 for rep in 1 2; do for lib in "" $V; do
   CKB_LIB=$lib python -c "
 import bench, os
