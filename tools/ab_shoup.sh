@@ -1,6 +1,7 @@
 #!/bin/bash
-# A/B of the integer NTT butterfly's quotient (default vs a variant build (here: -DCKB_NTT_GS_REDUCE_ALL))
-V=paper_2506_19693_b200/_lib/variants/gsall/libckks_b200.so
+# A/B of the integer NTT butterfly: the default library against a variant build (tools/ab_build.py NAME -DFLAG;
+# flags used in round 2: CKB_NTT_SHOUP4, CKB_NTT_MUL_PLAIN, CKB_NTT_CT_REDUCE_ALL, CKB_NTT_GS_REDUCE_ALL): tools/ab_shoup.sh NAME
+V=paper_2506_19693_b200/_lib/variants/${1:-gsall}/libckks_b200.so
 for rep in 1 2; do for lib in "" $V; do
   CKB_LIB=$lib python -c "
 import bench, os
