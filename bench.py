@@ -1006,9 +1006,10 @@ def main():
         from paper_2506_19693_b200.streaming import Pipeline
 
         pipe = Pipeline()
-        # 8 chunks: on this pool's faster hosts 16 chunks are 2-4% quicker, but their ~4,400
-        # kernel launches per step make the step host-enqueue-bound (2x slower) on the slower ones
-        chunk = int(os.environ.get("CKB_E2E_CHUNK", "0")) or max(1, bsz // 8)
+        # 16 chunks when each chunk replays as a CUDA graph (below); eager calls use 8: 16 chunks
+        # are ~4,400 kernel launches per step and host-enqueue-bound on this pool's slower hosts
+        use_graphs = os.environ.get("CKB_E2E_GRAPHS", "1") != "0"
+        chunk = int(os.environ.get("CKB_E2E_CHUNK", "0")) or max(1, bsz // (16 if use_graphs else 8))
 
         def e2e_chunk(dev, lo, hi):
             a = be.unpack_batch(dev[0], lvl)
@@ -1016,8 +1017,34 @@ def main():
             return [be.pack_batch(be.batch_hmult(a, b, lvl), lvl_out),
                     be.pack_batch(be.batch_hrot(a, steps_rot[lo:hi], lvl), lvl)]
 
+        # One CUDA graph per chunk (its rotation steps and key pointers are fixed): the
+        # chunk's ~280 kernel launches replay as one, so the step is no longer bound by the
+        # host's enqueue rate (eager: 2,200 launches per step in 8 chunks, 64 ms on this pool's
+        # slower hosts against a 40 ms PCIe floor).  CKB_E2E_GRAPHS=0 keeps the eager calls.
+        graphs, graph_err = None, None
+        if use_graphs:
+            try:
+                from paper_2506_19693_b200.graphs import GraphedCall
+
+                graphs = []
+                for lo in range(0, bsz, chunk):
+                    hi = min(bsz, lo + chunk)
+                    graphs.append(GraphedCall(
+                        lambda a, b, lo=lo, hi=hi: e2e_chunk([a, b], lo, hi),
+                        hA[lo:hi].to("cuda"), hB[lo:hi].to("cuda"), warmup=1))
+            except Exception as exc:  # report, never hide; the eager path still runs
+                graphs, graph_err = None, repr(exc)
+                torch.cuda.synchronize()
+                chunk = int(os.environ.get("CKB_E2E_CHUNK", "0")) or max(1, bsz // 8)
+
+        def e2e_chunk_graph(dev, lo, hi):
+            g = graphs[lo // chunk]
+            g.load(*dev)  # device-to-device into the graph's static inputs
+            return g()    # (its static outputs are read by this step's D2H copy, which the
+                          #  step's final join orders before the next step's replay)
+
         def e2e_step():  # H2D / unpack, HMult+HRot, pack / D2H overlapped across chunks
-            pipe.run(e2e_chunk, [hA, hB], [hOm, hOr], chunk)
+            pipe.run(e2e_chunk_graph if graphs else e2e_chunk, [hA, hB], [hOm, hOr], chunk)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -1025,6 +1052,10 @@ def main():
         chk = be.unpack_batch(hOm[:chunk].to("cuda"), lvl_out)
         ok = torch.equal(chk.view(torch.int64),
                          be.batch_hmult(A[:chunk], B[:chunk], lvl).view(torch.int64))
+        lo_l = ((bsz - 1) // chunk) * chunk  # ... and the last chunk's rotations
+        chk = be.unpack_batch(hOr[lo_l:].to("cuda"), lvl)
+        ok = ok and torch.equal(chk.view(torch.int64),
+                                be.batch_hrot(A[lo_l:], steps_rot[lo_l:], lvl).view(torch.int64))
         s0, s1 = ev(), ev()
         s0.record()
         e2e_reps = max(4, args.steps)
@@ -1040,7 +1071,10 @@ def main():
                        "transfer_format": "packed residues (ckb_pack: 5 bytes per 40-bit "
                                           "residue), unpacked/packed on the device in the "
                                           "timed region",
-                       "output_equal_batch_call": bool(ok)}
+                       "cuda_graphs": bool(graphs), "output_equal_batch_call": bool(ok)}
+        if graph_err:
+            line["e2e"]["cuda_graphs_error"] = graph_err
+        graphs = None
         del hA, hB, hOm, hOr
         try:  # the box's own PCIe floor for these bytes, beside the number it bounds
             pc = pcie_probe(local)
